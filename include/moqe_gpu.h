@@ -1,0 +1,153 @@
+/* moqe_gpu.h — C-ABI of the B200-native MoQE expert-FFN path.
+ *
+ * Drop-in boundary for the reference C++ API of the "quantize experts ->
+ * moe_ffn_forward (gate -> permute -> expert FFN -> combine)" path. Every
+ * entry point names the reference interface it replaces (paths relative to
+ * /root/reference/proj). Plain pointers and sizes only; no torch types.
+ *
+ * Conventions
+ *  - Pointers marked (device) are CUDA device pointers owned by the caller;
+ *    (host) pointers are host memory. `stream` is a cudaStream_t (NULL = legacy
+ *    default stream). Work is stream-ordered unless stated "blocking".
+ *  - Matrices are row-major. For a weight W [K x N] the channel is the column
+ *    (output feature), as in the reference (include/moqe/tensor.hpp:10-13).
+ *  - Codes are signed b-bit integers stored one per int8 (CodeArray,
+ *    include/moqe/bitpack.hpp:9-14); packed bytes use the reference layout
+ *    (offset binary, LSB-first, 3-bit in 24-bit groups; bitpack.hpp:22-28).
+ *  - Scales are f32 values holding binary16-representable numbers, one per
+ *    column (per-channel) or one per matrix (per-tensor), exactly like
+ *    QuantizedTensor::scales (include/moqe/quant.hpp:33).
+ *  - Errors are returned as moqe_status; the reference throws the matching
+ *    exception (std::invalid_argument / std::out_of_range / std::range_error).
+ *    moqe_gpu_last_error() gives a thread-local message.
+ */
+#ifndef MOQE_GPU_H
+#define MOQE_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MOQE_GPU_ABI_VERSION 1
+
+typedef enum moqe_status {
+    MOQE_OK = 0,
+    MOQE_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+    MOQE_OUT_OF_RANGE = 2,     /* std::out_of_range (bitpack.cpp:27-29) */
+    MOQE_RANGE_ERROR = 3,      /* std::range_error (tensor.cpp:101-104) */
+    MOQE_CUDA_ERROR = 4,
+    MOQE_NCCL_ERROR = 5,
+    MOQE_NOT_SUPPORTED = 6
+} moqe_status;
+
+typedef enum moqe_granularity { MOQE_PER_CHANNEL = 0, MOQE_PER_TENSOR = 1 } moqe_granularity;
+typedef enum moqe_dtype { MOQE_F32 = 0, MOQE_F16 = 1 } moqe_dtype;
+
+typedef struct moqe_bank* moqe_bank_t;
+
+int moqe_gpu_abi_version(void);
+const char* moqe_gpu_last_error(void);
+const char* moqe_gpu_status_string(moqe_status st);
+
+/* ---- bit-packing --------------------------------------------------------
+ * packed_size:  moqe::packed_size   include/moqe/bitpack.hpp:25 (bitpack.cpp:12-16)
+ *               returns (size_t)-1 for an unsupported width.
+ * pack:         moqe::pack          include/moqe/bitpack.hpp:28 (bitpack.cpp:18-39)
+ *               codes (device) -> out (device, packed_size bytes). Blocking:
+ *               an out-of-range code returns MOQE_OUT_OF_RANGE.
+ * unpack:       moqe::unpack        include/moqe/bitpack.hpp:30-31 (bitpack.cpp:41-68)
+ *               len must equal packed_size(bits, count) else MOQE_INVALID_ARGUMENT.
+ */
+size_t moqe_gpu_packed_size(int bits, size_t count);
+moqe_status moqe_gpu_pack(const int8_t* codes, int64_t count, int bits, uint8_t* out,
+                          void* stream);
+moqe_status moqe_gpu_unpack(const uint8_t* data, int64_t len, int bits, int64_t count,
+                            int8_t* codes, void* stream);
+
+/* ---- linear quantizer (batched over `batch` matrices of [rows x cols]) ----
+ * linear_scales:   moqe::linear_scales   include/moqe/quant.hpp:48 (quant.cpp:59-69)
+ * quantize_linear: moqe::quantize_linear include/moqe/quant.hpp:50 (quant.cpp:71-95)
+ * quantize_pack:   quantize_linear + pack fused ("quantize experts" as
+ *                  write_checkpoint stores it, checkpoint.cpp:255-261). packed
+ *                  holds batch * packed_size(bits, rows*cols) bytes.
+ * All blocking (errors detected on the device are reported like the
+ * reference throws): non-finite input -> MOQE_INVALID_ARGUMENT,
+ * scale overflowing binary16 -> MOQE_RANGE_ERROR. Pointers are device.
+ * codes/packed may be NULL to skip that output.
+ */
+moqe_status moqe_gpu_linear_scales(const float* a, int64_t batch, int64_t rows, int64_t cols,
+                                   int bits, moqe_granularity g, float* scales, void* stream);
+moqe_status moqe_gpu_quantize_linear(const float* a, int64_t batch, int64_t rows, int64_t cols,
+                                     int bits, moqe_granularity g, int8_t* codes,
+                                     float* scales, void* stream);
+moqe_status moqe_gpu_quantize_pack(const float* a, int64_t batch, int64_t rows, int64_t cols,
+                                   int bits, moqe_granularity g, uint8_t* packed,
+                                   float* scales, int8_t* codes, void* stream);
+
+/* ---- routing ------------------------------------------------------------------
+ * moqe::top1_route include/moqe/model.hpp:65 (model.cpp:328-346), plus top-2
+ * with renormalised gates (BASELINE config 4). h [t x d] (device, f32 or f16),
+ * wg [d x n_experts] f32 (device). Logits are fp32 in the reference's
+ * summation order (bit-identical), argmax ties -> lowest index, top-1 gate =
+ * softmax probability of the winner (double). expert/gate: [t x top_k] (device).
+ */
+moqe_status moqe_gpu_route(const void* h, moqe_dtype h_dtype, int64_t t, int64_t d,
+                           const float* wg, int n_experts, int top_k, int32_t* expert,
+                           float* gate, void* stream);
+
+/* ---- device-resident expert bank ------------------------------------------
+ * ExpertBank (include/moqe/model.hpp:74-82) of quantized experts
+ * W1 [d_model x d_ffn], W2 [d_ffn x d_model] (+ optional biases), uploaded
+ * once. packed_w1: n_experts * packed_size(bits, d*f) bytes, reference layout
+ * (what MQE1 stores, checkpoint.cpp:255-261); scales1: n_experts * d_ffn f32;
+ * packed_w2 / scales2 likewise with d_model scales; b1: n_experts*d_ffn or
+ * NULL; b2: n_experts*d_model or NULL (model.cpp:382,385 skip null biases).
+ * inputs_on_device: 1 if all input pointers are device pointers, 0 for host.
+ * The bank re-tiles the packed bytes on the device (same bits, no requantize).
+ * Blocking. */
+moqe_status moqe_gpu_bank_create(int n_experts, int64_t d_model, int64_t d_ffn, int bits,
+                                 const uint8_t* packed_w1, const float* scales1,
+                                 const uint8_t* packed_w2, const float* scales2,
+                                 const float* b1, const float* b2, int inputs_on_device,
+                                 moqe_bank_t* out);
+moqe_status moqe_gpu_bank_destroy(moqe_bank_t bank);
+/* Router weights Wg [d_model x n_experts] f32 kept with the bank
+ * (RouterState, include/moqe/model.hpp:56-58). Blocking. */
+moqe_status moqe_gpu_bank_set_router(moqe_bank_t bank, const float* wg, int on_device);
+/* Bytes of device weight storage (packed codes, excluding scales/biases). */
+int64_t moqe_gpu_bank_weight_bytes(moqe_bank_t bank);
+
+/* Execution-path selection for moe_forward:
+ *   MOQE_PATH_AUTO  — weight-streaming GEMV for experts with <= 32 routed rows,
+ *                     tcgen05 grouped GEMM for the rest (decided on device).
+ *   MOQE_PATH_GEMV  — force the GEMV path (requires t*top_k <= 32*n_experts? no:
+ *                     experts with more rows are processed in 32-row passes).
+ *   MOQE_PATH_GEMM  — force the tcgen05 grouped GEMM for all experts. */
+typedef enum moqe_path { MOQE_PATH_AUTO = 0, MOQE_PATH_GEMV = 1, MOQE_PATH_GEMM = 2 } moqe_path;
+
+/* ---- forward ----------------------------------------------------------------------
+ * moqe::moe_ffn_forward include/moqe/model.hpp:87 (model.cpp:348-393):
+ * out[tok] = sum_k gate_k * (relu(h W1_e + b1) W2_e + b2), e = expert_k(tok).
+ * h [t x d] (device, f32 or f16), wg (device) or NULL to use the bank's router,
+ * out [t x d] (device, f32 or f16). expert_out/gate_out [t x top_k] (device)
+ * optional. Stream-ordered, no host synchronisation; the bank's workspace
+ * makes concurrent forwards on one bank unsafe (one stream per bank).
+ * t == 0 is valid (no work). */
+moqe_status moqe_gpu_moe_forward(moqe_bank_t bank, const void* h, moqe_dtype h_dtype, int64_t t,
+                                 const float* wg, int top_k, void* out, moqe_dtype out_dtype,
+                                 int32_t* expert_out, float* gate_out, moqe_path path,
+                                 void* stream);
+
+/* Host-buffer convenience (the reference's by-value API): copies h (host,
+ * pinned or pageable) in, runs moe_forward, copies out (host) back. Blocking. */
+moqe_status moqe_gpu_moe_forward_host(moqe_bank_t bank, const void* h_host, moqe_dtype h_dtype,
+                                      int64_t t, int top_k, void* out_host,
+                                      moqe_dtype out_dtype, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOQE_GPU_H */

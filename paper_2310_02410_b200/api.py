@@ -1,0 +1,323 @@
+"""Python mirror of the reference's public API for the MoQE expert-FFN path.
+
+Same names, argument meaning and error behaviour as the reference C++ API
+(/root/reference/proj/include/moqe/*.hpp), on CUDA tensors. Every call goes
+through the C-ABI (include/moqe_gpu.h) into hand-written sm_100a kernels; torch
+only provides device memory and the current stream.
+
+  reference (moqe::)                          here
+  -----------------------------------------   ---------------------------------
+  packed_size   bitpack.hpp:25                packed_size
+  pack / unpack bitpack.hpp:28-31             pack / unpack
+  linear_scales quant.hpp:48                  linear_scales
+  quantize_linear quant.hpp:50                quantize_linear (-> QuantizedTensor)
+  dequantize    quant.hpp:64                  (not on the path: experts are never
+                                               materialised)
+  top1_route    model.hpp:65                  top1_route / route (top-1, top-2)
+  ExpertBank    model.hpp:80-82               ExpertBank (device resident)
+  moe_ffn_forward model.hpp:87                moe_ffn_forward
+  quantize_model  model.hpp:109-113           quantize_model (expert recipe)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import sys
+from dataclasses import dataclass, field
+from typing import Dict, Iterable, Optional, Tuple
+
+import torch
+
+from . import _lib
+from ._lib import check
+
+PER_CHANNEL = "channel"
+PER_TENSOR = "tensor"
+_GRAN = {PER_CHANNEL: _lib.PER_CHANNEL, PER_TENSOR: _lib.PER_TENSOR}
+_PATH = {"auto": _lib.PATH_AUTO, "gemv": _lib.PATH_GEMV, "gemm": _lib.PATH_GEMM}
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _dev(t: torch.Tensor, dtype: torch.dtype, what: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise _lib.InvalidArgument(f"{what}: expected a CUDA tensor")
+    return t.to(dtype).contiguous()
+
+
+def valid_bits(bits: int) -> bool:
+    return bits in (2, 3, 4, 8)
+
+
+def packed_size(bits: int, count: int) -> int:
+    """moqe::packed_size (bitpack.cpp:12-16)."""
+    lib = _lib.load()
+    n = lib.moqe_gpu_packed_size(bits, count)
+    if n == C.c_size_t(-1).value:
+        raise _lib.InvalidArgument(f"bitpack: unsupported width {bits}")
+    return int(n)
+
+
+def pack(codes: torch.Tensor, bits: int) -> torch.Tensor:
+    """moqe::pack (bitpack.cpp:18-39): offset binary, LSB-first, 3-bit groups."""
+    c = _dev(codes, torch.int8, "pack").reshape(-1)
+    n = packed_size(bits, c.numel())
+    out = torch.empty(max(n, 1), dtype=torch.uint8, device=c.device)
+    check(_lib.load().moqe_gpu_pack(_ptr(c), c.numel(), bits, _ptr(out), _stream()))
+    return out[:n]
+
+
+def unpack(data: torch.Tensor, bits: int, count: int) -> torch.Tensor:
+    """moqe::unpack (bitpack.cpp:41-68)."""
+    d = _dev(data, torch.uint8, "unpack").reshape(-1)
+    out = torch.empty(max(count, 1), dtype=torch.int8, device=d.device)
+    check(_lib.load().moqe_gpu_unpack(_ptr(d), d.numel(), bits, count, _ptr(out), _stream()))
+    return out[:count]
+
+
+def _as_batch(a: torch.Tensor, what: str) -> Tuple[torch.Tensor, int, int, int]:
+    a = _dev(a, torch.float32, what)
+    if a.dim() == 2:
+        return a, 1, a.shape[0], a.shape[1]
+    if a.dim() == 3:
+        return a, a.shape[0], a.shape[1], a.shape[2]
+    raise _lib.InvalidArgument("quant: tensor must be 2D")
+
+
+def linear_scales(a: torch.Tensor, bits: int, granularity: str = PER_CHANNEL) -> torch.Tensor:
+    """moqe::linear_scales (quant.cpp:59-69); a is [K,N] or a batch [B,K,N]."""
+    a, B, K, N = _as_batch(a, "linear_scales")
+    g = _GRAN[granularity]
+    ns = 1 if g == _lib.PER_TENSOR else N
+    s = torch.empty((B, ns), dtype=torch.float32, device=a.device)
+    check(_lib.load().moqe_gpu_linear_scales(_ptr(a), B, K, N, bits, g, _ptr(s), _stream()))
+    return s[0] if a.dim() == 2 else s
+
+
+@dataclass
+class QuantizedTensor:
+    """moqe::QuantizedTensor (quant.hpp:22-35), linear scheme, on the device."""
+    bits: int
+    granularity: str
+    shape: Tuple[int, int]
+    codes: torch.Tensor          # int8, one per code (CodeArray)
+    scales: torch.Tensor         # f32 binary16 values, [N] or [1]
+    packed: Optional[torch.Tensor] = None  # reference byte layout
+
+    scheme: str = field(default="linear")
+
+
+def quantize_linear(a: torch.Tensor, bits: int, granularity: str = PER_CHANNEL):
+    """moqe::quantize_linear (quant.cpp:71-95). Batched input returns a list."""
+    a3, B, K, N = _as_batch(a, "quantize_linear")
+    g = _GRAN[granularity]
+    ns = 1 if g == _lib.PER_TENSOR else N
+    codes = torch.empty((B, K, N), dtype=torch.int8, device=a3.device)
+    scales = torch.empty((B, ns), dtype=torch.float32, device=a3.device)
+    psz = packed_size(bits, K * N) if valid_bits(bits) else 0
+    packed = torch.empty((B, max(psz, 1)), dtype=torch.uint8, device=a3.device)
+    check(_lib.load().moqe_gpu_quantize_pack(_ptr(a3), B, K, N, bits, g, _ptr(packed), _ptr(scales),
+                                             _ptr(codes), _stream()))
+    qts = [QuantizedTensor(bits, granularity, (K, N), codes[i], scales[i], packed[i, :psz])
+           for i in range(B)]
+    return qts[0] if a3.dim() == 2 else qts
+
+
+def quantize_pack(a: torch.Tensor, bits: int, granularity: str = PER_CHANNEL):
+    """Fused quantize + pack over a batch [B,K,N] -> (packed [B, psz] u8, scales [B, N] f32)."""
+    a3, B, K, N = _as_batch(a, "quantize_pack")
+    g = _GRAN[granularity]
+    ns = 1 if g == _lib.PER_TENSOR else N
+    psz = packed_size(bits, K * N)
+    packed = torch.empty((B, max(psz, 1)), dtype=torch.uint8, device=a3.device)
+    scales = torch.empty((B, ns), dtype=torch.float32, device=a3.device)
+    check(_lib.load().moqe_gpu_quantize_pack(_ptr(a3), B, K, N, bits, g, _ptr(packed), _ptr(scales),
+                                             None, _stream()))
+    return packed[:, :psz], scales
+
+
+def route(h: torch.Tensor, gate_weights: torch.Tensor, top_k: int = 1):
+    """top1_route (model.cpp:328-346) generalised to top-2 with renormalised gates.
+
+    Returns (expert int32 [T] or [T,2], gate f32 [T] or [T,2])."""
+    if gate_weights is None:
+        raise _lib.InvalidArgument("top1_route: no gate weights")
+    hd = h.dtype if h.dtype in (torch.float16, torch.float32) else torch.float32
+    h = _dev(h, hd, "top1_route")
+    wg = _dev(gate_weights, torch.float32, "top1_route")
+    if h.dim() != 2 or wg.dim() != 2 or wg.shape[0] != h.shape[1]:
+        raise _lib.InvalidArgument("matmul: shape mismatch")
+    T, E = h.shape[0], wg.shape[1]
+    ex = torch.empty((max(T, 1) * top_k,), dtype=torch.int32, device=h.device)
+    gt = torch.empty((max(T, 1) * top_k,), dtype=torch.float32, device=h.device)
+    check(_lib.load().moqe_gpu_route(_ptr(h), _lib.F16 if hd == torch.float16 else _lib.F32, T,
+                                     h.shape[1], _ptr(wg), E, top_k, _ptr(ex), _ptr(gt), _stream()))
+    shape = (T,) if top_k == 1 else (T, top_k)
+    return ex[: T * top_k].reshape(shape), gt[: T * top_k].reshape(shape)
+
+
+def top1_route(h: torch.Tensor, gate_weights: torch.Tensor):
+    """moqe::top1_route (model.hpp:65)."""
+    return route(h, gate_weights, 1)
+
+
+class ExpertBank:
+    """Device-resident moqe::ExpertBank of linear-quantized experts (model.hpp:74-82).
+
+    W1_e [d_model x d_ffn], W2_e [d_ffn x d_model], per-output-channel scales,
+    optional biases. Weights are uploaded once (reference packed bytes) and
+    re-tiled on the device; forwards never re-quantize or materialise them."""
+
+    def __init__(self, n_experts: int, d_model: int, d_ffn: int, bits: int,
+                 packed_w1: torch.Tensor, scales1: torch.Tensor, packed_w2: torch.Tensor,
+                 scales2: torch.Tensor, b1: Optional[torch.Tensor] = None,
+                 b2: Optional[torch.Tensor] = None, router: Optional[torch.Tensor] = None):
+        self.E, self.d, self.f, self.bits = n_experts, d_model, d_ffn, bits
+        lib = _lib.load()
+        dev = packed_w1.is_cuda
+        conv = (lambda t, dt: t.to(dt).contiguous()) if dev else (lambda t, dt: t.to(dt).contiguous().cpu())
+        keep = [conv(packed_w1, torch.uint8), conv(scales1, torch.float32),
+                conv(packed_w2, torch.uint8), conv(scales2, torch.float32),
+                None if b1 is None else conv(b1, torch.float32),
+                None if b2 is None else conv(b2, torch.float32)]
+        h = C.c_void_p()
+        check(lib.moqe_gpu_bank_create(n_experts, d_model, d_ffn, bits, *[_ptr(t) for t in keep],
+                                       1 if dev else 0, C.byref(h)))
+        self._h = h
+        torch.cuda.synchronize()
+        if router is not None:
+            self.set_router(router)
+
+    @classmethod
+    def from_float(cls, w1: torch.Tensor, w2: torch.Tensor, bits: int,
+                   b1: Optional[torch.Tensor] = None, b2: Optional[torch.Tensor] = None,
+                   router: Optional[torch.Tensor] = None) -> "ExpertBank":
+        """Quantize-experts on the GPU (per-channel linear) then build the bank."""
+        E, d, f = w1.shape
+        p1, s1 = quantize_pack(w1, bits)
+        p2, s2 = quantize_pack(w2, bits)
+        return cls(E, d, f, bits, p1, s1, p2, s2, b1, b2, router)
+
+    def set_router(self, wg: torch.Tensor) -> None:
+        wg = wg.to(torch.float32).contiguous()
+        check(_lib.load().moqe_gpu_bank_set_router(self._h, _ptr(wg), 1 if wg.is_cuda else 0))
+
+    @property
+    def handle(self) -> int:
+        return self._h.value
+
+    def weight_bytes(self) -> int:
+        return int(_lib.load().moqe_gpu_bank_weight_bytes(self._h))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) and self._h.value:
+            _lib.load().moqe_gpu_bank_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            if sys.is_finalizing():
+                return
+            self.close()
+        except Exception:
+            pass
+
+
+def moe_ffn_forward(h: torch.Tensor, bank: ExpertBank, gate_weights: Optional[torch.Tensor] = None,
+                    top_k: int = 1, out_dtype: torch.dtype = torch.float32, path: str = "auto",
+                    return_routing: bool = False, out: Optional[torch.Tensor] = None):
+    """moqe::moe_ffn_forward (model.cpp:348-393) on the GPU.
+
+    h [T, d_model] f32/f16 CUDA tensor; gate_weights [d_model, E] (None: the
+    bank's router). Returns out [T, d_model] (out_dtype), plus (expert, gate)
+    when return_routing."""
+    if bank is None:
+        raise _lib.InvalidArgument("moe_ffn_forward: empty expert bank")
+    hd = h.dtype if h.dtype in (torch.float16, torch.float32) else torch.float32
+    h = _dev(h, hd, "moe_ffn_forward")
+    if h.dim() != 2 or h.shape[1] != bank.d:
+        raise _lib.InvalidArgument("matmul: shape mismatch")
+    T = h.shape[0]
+    wg = None if gate_weights is None else _dev(gate_weights, torch.float32, "moe_ffn_forward")
+    if wg is not None and tuple(wg.shape) != (bank.d, bank.E):
+        raise _lib.InvalidArgument("matmul: shape mismatch")
+    if out is None:
+        out = torch.empty((T, bank.d), dtype=out_dtype, device=h.device)
+    ex = gt = None
+    if return_routing:
+        ex = torch.empty((max(T, 1) * top_k,), dtype=torch.int32, device=h.device)
+        gt = torch.empty((max(T, 1) * top_k,), dtype=torch.float32, device=h.device)
+    check(_lib.load().moqe_gpu_moe_forward(
+        bank._h, _ptr(h), _lib.F16 if hd == torch.float16 else _lib.F32, T, _ptr(wg), top_k,
+        _ptr(out), _lib.F16 if out.dtype == torch.float16 else _lib.F32, _ptr(ex), _ptr(gt),
+        _PATH[path], _stream()))
+    if return_routing:
+        shape = (T,) if top_k == 1 else (T, top_k)
+        return out, ex[: T * top_k].reshape(shape), gt[: T * top_k].reshape(shape)
+    return out
+
+
+def moe_ffn_forward_host(h_host: torch.Tensor, bank: ExpertBank, top_k: int = 1,
+                         out: Optional[torch.Tensor] = None, out_dtype=torch.float32) -> torch.Tensor:
+    """By-value (host buffer) call, like the reference API: copies in, forward, copies out."""
+    hd = h_host.dtype
+    if out is None:
+        out = torch.empty((h_host.shape[0], bank.d), dtype=out_dtype, pin_memory=True)
+    check(_lib.load().moqe_gpu_moe_forward_host(
+        bank._h, _ptr(h_host), _lib.F16 if hd == torch.float16 else _lib.F32, h_host.shape[0],
+        top_k, _ptr(out), _lib.F16 if out.dtype == torch.float16 else _lib.F32, _stream()))
+    return out
+
+
+# ---- quantize_model (model.cpp:577-636), "quantize experts" recipe ---------------
+
+EXPERT_FFN = "expert_ffn"
+
+
+def quantize_model(ckpt: Dict[str, Tuple[torch.Tensor, str]], groups: Iterable[str], bits: int,
+                   granularity: str = PER_CHANNEL, subset: str = "all") -> Dict[str, object]:
+    """Replace every 2-D tensor whose group is in `groups` by its QuantizedTensor.
+
+    ckpt maps name -> (tensor, group). Mirrors moqe::quantize_model: empty group
+    list and bad widths are rejected; 1-D tensors are skipped with a warning;
+    optional layer parity filter ("even"/"odd", layer index from the canonical
+    name). Same-shape matrices are quantized in one batched launch."""
+    groups = set(groups)
+    if not groups:
+        raise _lib.InvalidArgument("quantize_model: empty group list")
+    if not valid_bits(bits):
+        raise _lib.InvalidArgument("quantize_model: unsupported bit width")
+
+    def layer_of(name: str):
+        for part in name.split("."):
+            if part.isdigit():
+                return int(part)
+        return None
+
+    out: Dict[str, object] = dict(ckpt)
+    todo: Dict[Tuple[int, int], list] = {}
+    for name, (t, grp) in ckpt.items():
+        if grp not in groups:
+            continue
+        if subset != "all":
+            li = layer_of(name)
+            if li is None or (subset == "even" and li % 2) or (subset == "odd" and li % 2 == 0):
+                continue
+        if isinstance(t, QuantizedTensor):
+            print(f"warning: {name} already quantized, skipping", file=sys.stderr)
+            continue
+        if t.dim() != 2:
+            print(f"warning: skipping non-2D tensor {name}", file=sys.stderr)
+            continue
+        todo.setdefault(tuple(t.shape), []).append(name)
+    for shape, names in todo.items():
+        batch = torch.stack([ckpt[n][0].to(torch.float32) for n in names]).cuda()
+        qts = quantize_linear(batch, bits, granularity)
+        for n, q in zip(names, qts):
+            out[n] = q
+    return out

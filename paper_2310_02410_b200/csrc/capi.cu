@@ -1,0 +1,398 @@
+// capi.cu — C-ABI entry points: device-resident expert bank, workspace and
+// the moe_forward orchestration (route -> permute -> GEMV / tcgen05 GEMM ->
+// combine), all stream-ordered with no host synchronisation on the hot path.
+//
+// Reference interface replaced: moqe::moe_ffn_forward
+// (include/moqe/model.hpp:87, proj/src/model.cpp:348-393) and the ExpertBank /
+// RouterState types (model.hpp:56-82).
+#include <cuda_fp16.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "kernels.cuh"
+
+namespace moqe_gpu {
+
+// ---- errors --------------------------------------------------------------------
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+moqe_status fail(moqe_status st, const std::string& msg) {
+    set_error(msg);
+    return st;
+}
+moqe_status cuda_fail(cudaError_t err, const char* what) {
+    set_error(std::string(what) + ": " + cudaGetErrorString(err));
+    return MOQE_CUDA_ERROR;
+}
+
+__global__ void k_f32_to_f16(const float* __restrict__ a, __half* __restrict__ b, int64_t n) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) b[i] = __float2half_rn(a[i]);
+}
+
+}  // namespace moqe_gpu
+
+using namespace moqe_gpu;
+
+struct Workspace {
+    int64_t cap_rows = 0, cap_tokens = 0;
+    void* block = nullptr;
+    Plan P{};
+    __half* mid = nullptr;
+    __half* x_perm = nullptr;
+    float* partial = nullptr;
+    int64_t part_rows = 0;
+    float* out_acc = nullptr;
+    unsigned* split_cnt = nullptr;
+};
+
+struct moqe_bank {
+    int E = 0, bits = 0;
+    int64_t d = 0, f = 0;
+    int Kp1 = 0, Np1 = 0, Kp2 = 0, Np2 = 0;
+    uint8_t* w1 = nullptr;
+    uint8_t* w2 = nullptr;
+    int64_t w1_stride = 0, w2_stride = 0;
+    float* s1 = nullptr;
+    float* s2 = nullptr;
+    float* b1 = nullptr;
+    float* b2 = nullptr;
+    float* wg = nullptr;
+    int num_sms = 148;
+    int device = 0;
+    cudaStream_t host_stream = nullptr;
+    void* h_dev = nullptr;   // host-API staging
+    void* o_dev = nullptr;
+    int64_t host_cap = 0;
+    Workspace ws;
+};
+
+namespace {
+
+template <class T>
+T* carve(char*& p, int64_t n) {
+    T* r = reinterpret_cast<T*>(p);
+    p += round_up(int64_t(sizeof(T)) * std::max<int64_t>(n, 1), 256);
+    return r;
+}
+
+moqe_status ensure_workspace(moqe_bank* b, int64_t T, int topk) {
+    Workspace& w = b->ws;
+    const int64_t R = T * topk;
+    if (T <= w.cap_tokens && R <= w.cap_rows) return MOQE_OK;
+    const int64_t capT = std::max(T, w.cap_tokens);
+    const int64_t capR = std::max<int64_t>(std::max(R, w.cap_rows), capT * 2);  // room for top-2
+    if (w.block) {
+        MOQE_CUDA(cudaDeviceSynchronize());
+        cudaFree(w.block);
+        w.block = nullptr;
+    }
+    const int E = b->E;
+    const int64_t nctas = (capT + route_tokens_per_cta(capT) - 1) / route_tokens_per_cta(capT) +
+                          (capT + kRouteWarps - 1) / kRouteWarps;  // either tile size
+    const int maxmt = std::max(b->Np1, b->Np2) / TILE_N;
+    const int64_t part_rows = capR;
+    const int64_t part = gemv_partial_floats(part_rows, b->Kp1, b->Np1, b->Kp2, b->Np2);
+    // sizing pass
+    int64_t bytes = 0;
+    auto add = [&](int64_t sz, int64_t n) { bytes += round_up(sz * std::max<int64_t>(n, 1), 256); };
+    add(4, capR); add(4, capR); add(4, capR); add(4, nctas * E); add(4, E); add(4, E + 1);
+    add(4, capR); add(4, capR); add(4, capR); add(4, E); add(4, E); add(4, E + 1); add(4, 8);
+    add(4, 8); add(4, E); add(4, 2 * E * maxmt);
+    add(2, capR * b->Np1); add(2, capR * b->Kp1); add(4, part); add(4, capT * b->d);
+    MOQE_CUDA(cudaMalloc(&w.block, bytes));
+    MOQE_CUDA(cudaMemset(w.block, 0, bytes));
+    char* p = static_cast<char*>(w.block);
+    Plan& P = w.P;
+    P.expert = carve<int32_t>(p, capR);
+    P.gate = carve<float>(p, capR);
+    P.lrank = carve<int32_t>(p, capR);
+    P.cta_counts = carve<int32_t>(p, nctas * E);
+    P.counts = carve<int32_t>(p, E);
+    P.offsets = carve<int32_t>(p, E + 1);
+    P.perm_token = carve<int32_t>(p, capR);
+    P.perm_gate = carve<float>(p, capR);
+    P.inv_pos = carve<int32_t>(p, capR);
+    P.gemv_list = carve<int32_t>(p, E);
+    P.gemm_list = carve<int32_t>(p, E);
+    P.gemm_tile_start = carve<int32_t>(p, E + 1);
+    P.meta = carve<int32_t>(p, 8);
+    P.tickets = carve<unsigned>(p, 8);
+    P.done = carve<unsigned>(p, E);
+    w.split_cnt = carve<unsigned>(p, 2 * E * maxmt);
+    P.split_done = w.split_cnt;
+    w.mid = carve<__half>(p, capR * b->Np1);
+    w.x_perm = carve<__half>(p, capR * b->Kp1);
+    w.partial = carve<float>(p, part);
+    P.partial = w.partial;
+    w.out_acc = carve<float>(p, capT * b->d);
+    w.part_rows = part_rows;
+    w.cap_rows = capR;
+    w.cap_tokens = capT;
+    return MOQE_OK;
+}
+
+void free_bank(moqe_bank* b) {
+    if (!b) return;
+    cudaFree(b->w1);
+    cudaFree(b->w2);
+    cudaFree(b->s1);
+    cudaFree(b->s2);
+    cudaFree(b->b1);
+    cudaFree(b->b2);
+    cudaFree(b->wg);
+    cudaFree(b->ws.block);
+    cudaFree(b->h_dev);
+    cudaFree(b->o_dev);
+    if (b->host_stream) cudaStreamDestroy(b->host_stream);
+    delete b;
+}
+
+// copy [E][n] (host or device) into a zero-padded device [E][np] array
+moqe_status upload_padded(float** dst, const float* src, int E, int64_t n, int64_t np, bool on_dev) {
+    MOQE_CUDA(cudaMalloc(dst, sizeof(float) * E * np));
+    MOQE_CUDA(cudaMemset(*dst, 0, sizeof(float) * E * np));
+    MOQE_CUDA(cudaMemcpy2D(*dst, np * sizeof(float), src, n * sizeof(float), n * sizeof(float), E,
+                           on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+    return MOQE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int moqe_gpu_abi_version(void) { return MOQE_GPU_ABI_VERSION; }
+const char* moqe_gpu_last_error(void) { return g_last_error.c_str(); }
+const char* moqe_gpu_status_string(moqe_status st) {
+    switch (st) {
+        case MOQE_OK: return "ok";
+        case MOQE_INVALID_ARGUMENT: return "invalid_argument";
+        case MOQE_OUT_OF_RANGE: return "out_of_range";
+        case MOQE_RANGE_ERROR: return "range_error";
+        case MOQE_CUDA_ERROR: return "cuda_error";
+        case MOQE_NCCL_ERROR: return "nccl_error";
+        case MOQE_NOT_SUPPORTED: return "not_supported";
+    }
+    return "unknown";
+}
+
+moqe_status moqe_gpu_bank_create(int n_experts, int64_t d_model, int64_t d_ffn, int bits,
+                                 const uint8_t* packed_w1, const float* scales1,
+                                 const uint8_t* packed_w2, const float* scales2, const float* b1,
+                                 const float* b2, int inputs_on_device, moqe_bank_t* out) {
+    if (!out) return fail(MOQE_INVALID_ARGUMENT, "bank_create: null output handle");
+    *out = nullptr;
+    if (n_experts <= 0) return fail(MOQE_INVALID_ARGUMENT, "moe_ffn_forward: empty expert bank");
+    if (n_experts > 256) return fail(MOQE_NOT_SUPPORTED, "bank_create: at most 256 experts");
+    if (!valid_bits(bits)) return fail(MOQE_INVALID_ARGUMENT, "quant: unsupported bit width");
+    if (d_model <= 0 || d_ffn <= 0) return fail(MOQE_INVALID_ARGUMENT, "bank_create: bad dimensions");
+    if (!packed_w1 || !packed_w2 || !scales1 || !scales2)
+        return fail(MOQE_INVALID_ARGUMENT, "bank_create: null weights");
+    auto* b = new moqe_bank;
+    b->E = n_experts;
+    b->d = d_model;
+    b->f = d_ffn;
+    b->bits = bits;
+    b->Kp1 = int(round_up(d_model, TILE_K));
+    b->Np1 = int(round_up(d_ffn, TILE_N));
+    b->Kp2 = b->Np1;  // fc2 consumes the full (zero-padded) fc1 output width
+    b->Np2 = int(round_up(d_model, TILE_N));
+    cudaError_t ce = cudaGetDevice(&b->device);
+    if (ce == cudaSuccess) ce = cudaDeviceGetAttribute(&b->num_sms, cudaDevAttrMultiProcessorCount, b->device);
+    if (ce != cudaSuccess) {
+        free_bank(b);
+        return cuda_fail(ce, "cudaGetDevice");
+    }
+    const bool dev = inputs_on_device != 0;
+    b->w1_stride = int64_t(b->Np1 / TILE_N) * (b->Kp1 / TILE_K) * tile_bytes(bits);
+    b->w2_stride = int64_t(b->Np2 / TILE_N) * (b->Kp2 / TILE_K) * tile_bytes(bits);
+    const int64_t src1 = packed_size(bits, d_model * d_ffn), src2 = src1;
+    uint8_t* stage = nullptr;
+    moqe_status st = MOQE_OK;
+    do {
+        if ((ce = cudaMalloc(&b->w1, b->w1_stride * n_experts)) != cudaSuccess) break;
+        if ((ce = cudaMalloc(&b->w2, b->w2_stride * n_experts)) != cudaSuccess) break;
+        const uint8_t* s1p = packed_w1;
+        const uint8_t* s2p = packed_w2;
+        if (!dev) {
+            if ((ce = cudaMalloc(&stage, std::max(src1, src2) * n_experts)) != cudaSuccess) break;
+            if ((ce = cudaMemcpy(stage, packed_w1, src1 * n_experts, cudaMemcpyHostToDevice)) != cudaSuccess) break;
+            s1p = stage;
+        }
+        if ((st = retile(s1p, d_model, d_ffn, bits, n_experts, b->w1, b->Kp1, b->Np1, nullptr)) != MOQE_OK) break;
+        if (!dev) {
+            if ((ce = cudaDeviceSynchronize()) != cudaSuccess) break;
+            if ((ce = cudaMemcpy(stage, packed_w2, src2 * n_experts, cudaMemcpyHostToDevice)) != cudaSuccess) break;
+            s2p = stage;
+        }
+        if ((st = retile(s2p, d_ffn, d_model, bits, n_experts, b->w2, b->Kp2, b->Np2, nullptr)) != MOQE_OK) break;
+        if ((st = upload_padded(&b->s1, scales1, n_experts, d_ffn, b->Np1, dev)) != MOQE_OK) break;
+        if ((st = upload_padded(&b->s2, scales2, n_experts, d_model, b->Np2, dev)) != MOQE_OK) break;
+        if (b1 && (st = upload_padded(&b->b1, b1, n_experts, d_ffn, b->Np1, dev)) != MOQE_OK) break;
+        if (b2 && (st = upload_padded(&b->b2, b2, n_experts, d_model, b->Np2, dev)) != MOQE_OK) break;
+        if ((ce = cudaDeviceSynchronize()) != cudaSuccess) break;
+    } while (false);
+    if (stage) cudaFree(stage);
+    if (ce != cudaSuccess) st = cuda_fail(ce, "bank_create");
+    if (st != MOQE_OK) {
+        free_bank(b);
+        return st;
+    }
+    *out = b;
+    return MOQE_OK;
+}
+
+moqe_status moqe_gpu_bank_destroy(moqe_bank_t bank) {
+    if (bank) cudaDeviceSynchronize();
+    free_bank(bank);
+    return MOQE_OK;
+}
+
+moqe_status moqe_gpu_bank_set_router(moqe_bank_t b, const float* wg, int on_device) {
+    if (!b || !wg) return fail(MOQE_INVALID_ARGUMENT, "top1_route: no gate weights");
+    if (!b->wg) MOQE_CUDA(cudaMalloc(&b->wg, sizeof(float) * b->d * b->E));
+    MOQE_CUDA(cudaMemcpy(b->wg, wg, sizeof(float) * b->d * b->E,
+                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+    return MOQE_OK;
+}
+
+int64_t moqe_gpu_bank_weight_bytes(moqe_bank_t b) {
+    if (!b) return -1;
+    return (b->w1_stride + b->w2_stride) * b->E;
+}
+
+moqe_status moqe_gpu_moe_forward(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64_t t,
+                                 const float* wg, int top_k, void* out, moqe_dtype out_dtype,
+                                 int32_t* expert_out, float* gate_out, moqe_path path, void* stream) {
+    if (!b) return fail(MOQE_INVALID_ARGUMENT, "moe_ffn_forward: empty expert bank");
+    if (t < 0) return fail(MOQE_INVALID_ARGUMENT, "moe_ffn_forward: negative token count");
+    if (top_k != 1 && top_k != 2) return fail(MOQE_INVALID_ARGUMENT, "moe_forward: top_k must be 1 or 2");
+    if (top_k == 2 && b->E < 2) return fail(MOQE_INVALID_ARGUMENT, "moe_forward: top-2 needs >= 2 experts");
+    if (h_dtype != MOQE_F32 && h_dtype != MOQE_F16) return fail(MOQE_INVALID_ARGUMENT, "moe_forward: bad h dtype");
+    if (out_dtype != MOQE_F32 && out_dtype != MOQE_F16) return fail(MOQE_INVALID_ARGUMENT, "moe_forward: bad out dtype");
+    if (!wg) wg = b->wg;
+    if (!wg) return fail(MOQE_INVALID_ARGUMENT, "top1_route: no gate weights");
+    if (t == 0) return MOQE_OK;
+    if (!h || !out) return fail(MOQE_INVALID_ARGUMENT, "moe_forward: null buffer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    moqe_status s = ensure_workspace(b, t, top_k);
+    if (s != MOQE_OK) return s;
+    Workspace& w = b->ws;
+    Plan P = w.P;
+    if (expert_out) P.expert = expert_out;
+    if (gate_out) P.gate = gate_out;
+    const int64_t R = t * top_k;
+    int eff_path = int(path);
+    if (eff_path == MOQE_PATH_GEMM && !gemm_available())
+        return fail(MOQE_NOT_SUPPORTED, "moe_forward: tcgen05 GEMM path not built");
+    if (eff_path == MOQE_PATH_AUTO && !gemm_available()) eff_path = MOQE_PATH_GEMV;
+    // tcgen05 GEMM path handles experts with > kGemvMaxRows rows; tiny batches never need it.
+    const bool need_gemm = eff_path == MOQE_PATH_GEMM || (eff_path == MOQE_PATH_AUTO && R > kGemvMaxRows);
+    const bool need_gemv = eff_path != MOQE_PATH_GEMM;
+    const bool inline_scatter = !need_gemm && R <= 256;
+    float* acc = nullptr;
+    if (top_k == 2) acc = out_dtype == MOQE_F32 ? static_cast<float*>(out) : w.out_acc;
+
+    RouteArgs ra{h, h_dtype == MOQE_F16, t, int(b->d), wg, b->E, top_k, eff_path, inline_scatter ? 1 : 0,
+                 gemm_block_n(), inline_scatter ? acc : nullptr};
+    cudaError_t ce = launch_route(ra, P, st);
+    if (ce != cudaSuccess) return cuda_fail(ce, "k_route");
+    if (!inline_scatter) {
+        ce = launch_scatter(h, h_dtype == MOQE_F16, t, int(b->d), top_k, b->E, eff_path, P,
+                            need_gemm ? w.x_perm : nullptr, b->Kp1, acc, st);
+        if (ce != cudaSuccess) return cuda_fail(ce, "k_scatter");
+    }
+    if (need_gemv) {
+        GemvArgs g{h, h_dtype == MOQE_F16, t, int(b->d), int(b->f), top_k, b->E, b->w1, b->w2,
+                   b->w1_stride, b->w2_stride, b->s1, b->s2, b->b1, b->b2, b->Kp1, b->Np1, b->Kp2, b->Np2,
+                   w.mid, out, out_dtype == MOQE_F16, acc, w.partial, w.part_rows, w.split_cnt};
+        ce = launch_gemv(b->bits, R > 16, g, P, st, b->num_sms);
+        if (ce != cudaSuccess) return cuda_fail(ce, "k_ffn_gemv");
+    }
+    if (need_gemm) {
+        GemmArgs g{w.x_perm, w.mid, b->w1, b->w2, b->w1_stride, b->w2_stride, b->s1, b->s2, b->b1, b->b2,
+                   b->Kp1, b->Np1, b->Kp2, b->Np2, w.cap_rows, int(b->d), out, out_dtype == MOQE_F16, acc};
+        ce = launch_gemm(b->bits, g, P, st, b->num_sms);
+        if (ce != cudaSuccess) return cuda_fail(ce, "k_ffn_gemm");
+    }
+    if (top_k == 2 && out_dtype == MOQE_F16) {
+        const int64_t n = t * b->d;
+        k_f32_to_f16<<<unsigned((n + 255) / 256), 256, 0, st>>>(acc, static_cast<__half*>(out), n);
+        MOQE_CHECK_LAUNCH("k_f32_to_f16");
+    }
+    return MOQE_OK;
+}
+
+moqe_status moqe_gpu_moe_forward_host(moqe_bank_t b, const void* h_host, moqe_dtype h_dtype, int64_t t,
+                                      int top_k, void* out_host, moqe_dtype out_dtype, void* stream) {
+    if (!b) return fail(MOQE_INVALID_ARGUMENT, "moe_ffn_forward: empty expert bank");
+    if (t < 0) return fail(MOQE_INVALID_ARGUMENT, "moe_ffn_forward: negative token count");
+    if (t == 0) return MOQE_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t hb = t * b->d * (h_dtype == MOQE_F16 ? 2 : 4);
+    const int64_t ob = t * b->d * (out_dtype == MOQE_F16 ? 2 : 4);
+    const int64_t need = std::max(hb, ob);
+    if (need > b->host_cap) {
+        MOQE_CUDA(cudaDeviceSynchronize());
+        cudaFree(b->h_dev);
+        cudaFree(b->o_dev);
+        b->h_dev = b->o_dev = nullptr;
+        MOQE_CUDA(cudaMalloc(&b->h_dev, need));
+        MOQE_CUDA(cudaMalloc(&b->o_dev, need));
+        b->host_cap = need;
+    }
+    MOQE_CUDA(cudaMemcpyAsync(b->h_dev, h_host, hb, cudaMemcpyHostToDevice, st));
+    moqe_status s = moqe_gpu_moe_forward(b, b->h_dev, h_dtype, t, nullptr, top_k, b->o_dev, out_dtype,
+                                         nullptr, nullptr, MOQE_PATH_AUTO, st);
+    if (s != MOQE_OK) return s;
+    MOQE_CUDA(cudaMemcpyAsync(out_host, b->o_dev, ob, cudaMemcpyDeviceToHost, st));
+    MOQE_CUDA(cudaStreamSynchronize(st));
+    return MOQE_OK;
+}
+
+moqe_status moqe_gpu_route(const void* h, moqe_dtype h_dtype, int64_t t, int64_t d, const float* wg,
+                           int n_experts, int top_k, int32_t* expert, float* gate, void* stream) {
+    if (!wg) return fail(MOQE_INVALID_ARGUMENT, "top1_route: no gate weights");
+    if (n_experts <= 0 || n_experts > 256) return fail(MOQE_INVALID_ARGUMENT, "route: bad expert count");
+    if (top_k != 1 && top_k != 2) return fail(MOQE_INVALID_ARGUMENT, "route: top_k must be 1 or 2");
+    if (top_k == 2 && n_experts < 2) return fail(MOQE_INVALID_ARGUMENT, "route: top-2 needs >= 2 experts");
+    if (t < 0 || d <= 0) return fail(MOQE_INVALID_ARGUMENT, "matmul: shape mismatch");
+    if (t == 0) return MOQE_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int E = n_experts;
+    const int64_t R = t * top_k;
+    const int64_t nctas = (t + route_tokens_per_cta(t) - 1) / route_tokens_per_cta(t);
+    int64_t bytes = 0;
+    auto sz = [&](int64_t n) { int64_t r = bytes; bytes += round_up(4 * std::max<int64_t>(n, 1), 256); return r; };
+    const int64_t o_lrank = sz(R), o_cta = sz(nctas * E), o_counts = sz(E), o_off = sz(E + 1),
+                  o_pt = sz(R), o_pg = sz(R), o_inv = sz(R), o_gl = sz(E), o_ml = sz(E), o_ts = sz(E + 1),
+                  o_meta = sz(8), o_tk = sz(8), o_done = sz(E);
+    char* blk = nullptr;
+    MOQE_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&blk), bytes, st));
+    MOQE_CUDA(cudaMemsetAsync(blk, 0, bytes, st));
+    Plan P{};
+    P.expert = expert;
+    P.gate = gate;
+    P.lrank = reinterpret_cast<int32_t*>(blk + o_lrank);
+    P.cta_counts = reinterpret_cast<int32_t*>(blk + o_cta);
+    P.counts = reinterpret_cast<int32_t*>(blk + o_counts);
+    P.offsets = reinterpret_cast<int32_t*>(blk + o_off);
+    P.perm_token = reinterpret_cast<int32_t*>(blk + o_pt);
+    P.perm_gate = reinterpret_cast<float*>(blk + o_pg);
+    P.inv_pos = reinterpret_cast<int32_t*>(blk + o_inv);
+    P.gemv_list = reinterpret_cast<int32_t*>(blk + o_gl);
+    P.gemm_list = reinterpret_cast<int32_t*>(blk + o_ml);
+    P.gemm_tile_start = reinterpret_cast<int32_t*>(blk + o_ts);
+    P.meta = reinterpret_cast<int32_t*>(blk + o_meta);
+    P.tickets = reinterpret_cast<unsigned*>(blk + o_tk);
+    P.done = reinterpret_cast<unsigned*>(blk + o_done);
+    RouteArgs ra{h, h_dtype == MOQE_F16, t, int(d), wg, E, top_k, 0, 0, 128, nullptr};
+    cudaError_t ce = launch_route(ra, P, st);
+    cudaFreeAsync(blk, st);
+    if (ce != cudaSuccess) return cuda_fail(ce, "k_route");
+    return MOQE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,31 @@
+// plan.cuh — device workspace shared by route -> permute -> expert FFN kernels.
+#pragma once
+#include <stdint.h>
+
+namespace moqe_gpu {
+
+constexpr int kGemvMaxRows = 32;   // experts with <= this many routed rows take the GEMV path
+constexpr int kRouteWarps = 8;     // warps per routing CTA
+
+// All pointers are device memory owned by the bank's workspace.
+struct Plan {
+    int32_t* expert;      // [T*k]  routed expert per (token, slot)
+    float* gate;          // [T*k]  gate per (token, slot)
+    int32_t* lrank;       // [T*k]  stable rank among same-expert rows inside its route CTA
+    int32_t* cta_counts;  // [n_route_ctas * E] per-CTA histogram -> per-CTA base after plan
+    int32_t* counts;      // [E]
+    int32_t* offsets;     // [E+1] exclusive scan of counts
+    int32_t* perm_token;  // [T*k]  token of permuted row pos (rows grouped by expert, ascending token)
+    float* perm_gate;     // [T*k]
+    int32_t* inv_pos;     // [T*k]  permuted row of (token, slot)
+    int32_t* gemv_list;   // [E]    experts for the GEMV path (expert order)
+    int32_t* gemm_list;   // [E]    experts for the tcgen05 path
+    int32_t* gemm_tile_start;  // [E+1] prefix of GEMM tiles per listed expert (per m-tile row)
+    int32_t* meta;        // [8]    0: n_gemv, 1: n_gemm, 2: gemm n-tiles total, 3: max n_e
+    unsigned* tickets;    // [8]    0: route last-CTA, 1: gemv items, 2: gemm fc1, 3: gemm fc2
+    unsigned* done;       // [E]    GEMV fc1 m-tiles finished per expert
+    unsigned* split_done; // [E * max_mt] GEMV fc2 split-K arrivals
+    float* partial;       // GEMV fc2 split-K partials
+};
+
+}  // namespace moqe_gpu

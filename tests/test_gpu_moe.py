@@ -1,0 +1,141 @@
+"""GPU moe_forward parity against the oracle / reference goldens.
+
+Tolerance (BASELINE.json north_star): |gpu - ref| <= 2e-3 + 1e-2*|ref|
+elementwise; routing ids bit-exact (logits are bit-identical by construction,
+so no near-tie exemption is needed)."""
+import numpy as np
+import pytest
+
+from helpers import allclose_report, fp16_valued, make_layer
+
+pytestmark = pytest.mark.gpu
+ATOL, RTOL = 2e-3, 1e-2
+
+
+def _t(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _bank(gpu, L):
+    return gpu.ExpertBank(L["E"], L["d"], L["f"], L["bits"], _t(L["p1"]), _t(L["s1"]), _t(L["p2"]),
+                          _t(L["s2"]), None if L["b1"] is None else _t(L["b1"]),
+                          None if L["b2"] is None else _t(L["b2"]))
+
+
+@pytest.mark.parametrize("bits", [2, 3, 4, 8])
+def test_golden_moe(gpu, golden, bits):
+    G = golden["moe"]
+    E, d, f = G[f"q1_{bits}"].shape
+    b1 = _t(G[f"b1_{bits}"]) if f"b1_{bits}" in G else None
+    b2 = _t(G[f"b2_{bits}"]) if f"b2_{bits}" in G else None
+    bank = gpu.ExpertBank(E, d, f, bits, _t(G[f"p1_{bits}"]), _t(G[f"s1_{bits}"]), _t(G[f"p2_{bits}"]),
+                          _t(G[f"s2_{bits}"]), b1, b2)
+    for path in ("auto", "gemv"):
+        out, ex, g = gpu.moe_ffn_forward(_t(G[f"h_{bits}"]), bank, _t(G[f"wg_{bits}"]), path=path,
+                                         return_routing=True)
+        assert np.array_equal(ex.cpu().numpy(), G[f"expert_{bits}"])
+        nbad, mx = allclose_report(out.cpu().numpy(), G[f"out_{bits}"], ATOL, RTOL)
+        assert nbad == 0, (path, mx)
+
+
+CASES = [
+    # (E, d, f, bits, T, topk, bias)
+    (32, 1024, 4096, 3, 24, 1, False),   # north-star decode shape
+    (32, 1024, 4096, 2, 24, 1, False),
+    (32, 1024, 4096, 4, 24, 1, False),
+    (32, 1024, 4096, 8, 24, 1, False),
+    (8, 256, 512, 4, 16, 1, True),
+    (8, 256, 512, 3, 7, 2, False),
+    (5, 72, 200, 2, 13, 1, True),        # ragged dims (padding paths)
+    (4, 64, 128, 8, 1, 1, False),
+    (16, 128, 256, 4, 200, 1, False),    # > 32 rows per expert: GEMV passes / GEMM
+    (16, 128, 256, 3, 300, 2, True),
+]
+
+
+@pytest.mark.parametrize("E,d,f,bits,T,topk,bias", CASES)
+def test_moe_vs_oracle(gpu, orc, E, d, f, bits, T, topk, bias):
+    import torch
+    L = make_layer(orc, E * 31 + T + bits, E, d, f, bits, T, with_bias=bias)
+    want, ex_o, g_o = orc.moe_forward(L["h"], L["wg"], L["q1"], L["s1"], L["q2"], L["s2"], top_k=topk,
+                                      b1=L["b1"], b2=L["b2"])
+    bank = _bank(gpu, L)
+    paths = ["auto", "gemv"] + (["gemm"] if gpu.api._lib.load() and _gemm_ok(gpu) else [])
+    for path in paths:
+        for hdt in (torch.float32, torch.float16):
+            out, ex, g = gpu.moe_ffn_forward(_t(L["h"]).to(hdt), bank, _t(L["wg"]), top_k=topk, path=path,
+                                             return_routing=True)
+            assert np.array_equal(ex.cpu().numpy(), ex_o), path
+            assert np.allclose(g.cpu().numpy(), g_o, rtol=1e-6, atol=0)
+            nbad, mx = allclose_report(out.cpu().numpy(), want, ATOL, RTOL)
+            assert nbad == 0, (path, hdt, mx)
+
+
+def _gemm_ok(gpu):
+    try:
+        import torch
+        L = {"E": 2, "d": 64, "f": 128, "bits": 4}
+        rng = np.random.default_rng(0)
+        p = np.zeros((2, gpu.packed_size(4, 64 * 128)), np.uint8)
+        bank = gpu.ExpertBank(2, 64, 128, 4, _t(p), _t(np.ones((2, 128), np.float32)), _t(p),
+                              _t(np.ones((2, 64), np.float32)))
+        gpu.moe_ffn_forward(_t(np.ones((40, 64), np.float32)), bank, _t(np.zeros((64, 2), np.float32)), path="gemm")
+        return True
+    except gpu.NotSupported:
+        return False
+
+
+def test_moe_f16_output_and_determinism(gpu, orc):
+    import torch
+    L = make_layer(orc, 5, 32, 1024, 4096, 3, 24)
+    bank = _bank(gpu, L)
+    h, wg = _t(L["h"]).half(), _t(L["wg"])
+    a = gpu.moe_ffn_forward(h, bank, wg)
+    b = gpu.moe_ffn_forward(h, bank, wg)
+    assert torch.equal(a, b)  # bit-identical across runs (test_model.cpp:170-181)
+    o16 = gpu.moe_ffn_forward(h, bank, wg, out_dtype=torch.float16)
+    assert o16.dtype == torch.float16
+    want = orc.moe_forward(L["h"], L["wg"], L["q1"], L["s1"], L["q2"], L["s2"])[0]
+    nbad, mx = allclose_report(o16.float().cpu().numpy(), want, ATOL, RTOL)
+    assert nbad == 0, mx
+
+
+def test_moe_empty_and_errors(gpu, orc):
+    import torch
+    L = make_layer(orc, 6, 4, 64, 128, 4, 3)
+    bank = _bank(gpu, L)
+    out = gpu.moe_ffn_forward(torch.zeros((0, 64), device="cuda"), bank, _t(L["wg"]))
+    assert out.shape == (0, 64)
+    with pytest.raises(gpu.InvalidArgument):
+        gpu.moe_ffn_forward(_t(L["h"]), bank, None)  # no router (top1_route: no gate weights)
+    with pytest.raises(gpu.InvalidArgument):
+        gpu.moe_ffn_forward(_t(L["h"][:, :32]), bank, _t(L["wg"]))
+    with pytest.raises(gpu.InvalidArgument):
+        gpu.ExpertBank(0, 64, 128, 4, _t(L["p1"]), _t(L["s1"]), _t(L["p2"]), _t(L["s2"]))
+
+
+def test_bank_from_float_and_host_api(gpu, orc):
+    import torch
+    L = make_layer(orc, 7, 8, 128, 256, 4, 20)
+    bank = gpu.ExpertBank.from_float(_t(L["w1"]), _t(L["w2"]), 4, router=_t(L["wg"]))
+    want = orc.moe_forward(L["h"], L["wg"], L["q1"], L["s1"], L["q2"], L["s2"])[0]
+    out = gpu.moe_ffn_forward(_t(L["h"]), bank)  # bank's router
+    assert allclose_report(out.cpu().numpy(), want, ATOL, RTOL)[0] == 0
+    h_host = torch.from_numpy(L["h"]).pin_memory()
+    out_h = gpu.moe_ffn_forward_host(h_host, bank)
+    assert torch.equal(out_h, out.cpu())
+
+
+def test_zero_input_gives_gated_bias(gpu):
+    # proj/tests/test_model.cpp:118-134 (zero weights quantize to zero codes/scales)
+    import torch
+    E, d, f = 3, 4, 8
+    p = np.zeros((E, gpu.packed_size(4, d * f)), np.uint8) + 0x88  # code 0 everywhere
+    bank = gpu.ExpertBank(E, d, f, 4, _t(p), _t(np.zeros((E, f), np.float32)), _t(p),
+                          _t(np.zeros((E, d), np.float32)), _t(np.zeros((E, f), np.float32)),
+                          _t(np.tile((np.arange(d) - 1.5).astype(np.float32), (E, 1))))
+    out, ex, g = gpu.moe_ffn_forward(torch.zeros((2, d), device="cuda"), bank,
+                                     torch.zeros((d, E), device="cuda"), return_routing=True)
+    assert (ex.cpu().numpy() == 0).all()
+    assert np.allclose(out.cpu().numpy(), (np.arange(d) - 1.5) / 3.0, rtol=1e-6)

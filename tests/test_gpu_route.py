@@ -1,0 +1,52 @@
+"""GPU gating parity: expert ids bit-exact with the reference (logits are
+computed in the reference's exact fp32 order), gates within float rounding."""
+import math
+
+import numpy as np
+import pytest
+
+from helpers import fp16_valued
+
+pytestmark = pytest.mark.gpu
+
+
+def _t(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def test_route_known_answers(gpu):
+    # proj/tests/test_model.cpp:35-61
+    ex, g = gpu.top1_route(_t(np.array([[1, 2], [-1, 0], [4, 4]], np.float32)),
+                           _t(np.array([[0.5], [-0.25]], np.float32)))
+    assert (ex.cpu().numpy() == 0).all() and (g.cpu().numpy() == 1.0).all()
+    ex, g = gpu.top1_route(_t(np.array([[1, 2, 3], [-1, -2, -3]], np.float32)), _t(np.zeros((3, 4), np.float32)))
+    assert (ex.cpu().numpy() == 0).all() and np.allclose(g.cpu().numpy(), 0.25, rtol=1e-6)
+    ex, g = gpu.top1_route(_t(np.array([[1.0]], np.float32)), _t(np.array([[2.0, 0.0]], np.float32)))
+    assert ex.item() == 0 and math.isclose(g.item(), math.exp(2) / (math.exp(2) + 1), rel_tol=1e-6)
+    with pytest.raises(gpu.InvalidArgument):
+        gpu.top1_route(_t(np.ones((2, 2), np.float32)), None)
+
+
+def test_route_golden(gpu, golden):
+    G = golden["route"]
+    for i in range(3):
+        ex, g = gpu.top1_route(_t(G[f"h_{i}"]), _t(G[f"wg_{i}"]))
+        assert np.array_equal(ex.cpu().numpy(), G[f"expert_{i}"])
+        assert np.allclose(g.cpu().numpy(), G[f"gate_{i}"], rtol=2e-7, atol=0)
+
+
+@pytest.mark.parametrize("T,d,E,topk", [(24, 1024, 32, 1), (4096, 1024, 32, 1), (3000, 1024, 64, 1),
+                                        (257, 2048, 128, 2), (5000, 256, 128, 2), (1, 8, 3, 2),
+                                        (70, 33, 200, 1)])
+def test_route_vs_oracle(gpu, orc, T, d, E, topk):
+    rng = np.random.default_rng(T * 7 + E)
+    h = fp16_valued(rng.standard_normal((T, d)))
+    wg = (rng.standard_normal((d, E)) * 0.02).astype(np.float32)
+    ex_o, g_o = orc.route(h, wg, topk)
+    for dt in ("f32", "f16"):
+        import torch
+        hh = _t(h) if dt == "f32" else _t(h).half()
+        ex, g = gpu.route(hh, _t(wg), topk)
+        assert np.array_equal(ex.cpu().numpy(), ex_o), dt
+        assert np.allclose(g.cpu().numpy(), g_o, rtol=1e-6, atol=0), dt
