@@ -1,0 +1,458 @@
+#!/usr/bin/env python
+"""bench.py — MoQE expert-FFN layer throughput on B200.
+
+Headline workload (BASELINE.json configs[1], north-star decode point): one
+MoE FFN layer, d_model=1024, d_ffn=4096, 32 experts, top-1, int3
+per-channel experts, T=24 tokens (one decode step, batch 24), fp16
+activations ~N(0,1), weights ~N(0,0.02), gate ~N(0,0.02). One step = one
+moe_forward (route -> permute -> expert FFN -> combine) of one layer.
+L2 hygiene: 8 independent layer replicas (different weights, routers and
+inputs) rotate, so each step's weights were last touched 7 steps earlier
+(total working set > 126 MB L2).
+
+Prints ONE JSON line (rank 0). `--impl reference` times the reference's own
+CPU moe_ffn_forward (oracle/_ref, built from /root/reference) on the host
+cores on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MoE FFN tokens/s & packed-weight HBM GB/s (vs 8TB/s), int4/3/2, 1-8 B200"
+SEED = 20231004
+N_LAYERS = 8
+
+
+def packed_bytes(bits: int, n: int) -> int:
+    return 3 * ((n + 7) // 8) if bits == 3 else (n * bits + 7) // 8
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.15)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        sm = []
+        mx = None
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, r[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------
+# workload
+
+def layer0_numpy(E, d, f):
+    """Layer 0 weights/inputs, generated identically for both arms (seeded numpy)."""
+    rng = np.random.default_rng(SEED)
+    w1 = (rng.standard_normal((E, d, f), dtype=np.float32) * np.float32(0.02))
+    w2 = (rng.standard_normal((E, f, d), dtype=np.float32) * np.float32(0.02))
+    wg = (rng.standard_normal((d, E), dtype=np.float32) * np.float32(0.02))
+    return w1, w2, wg, rng
+
+
+def tokens_numpy(rng, T, d):
+    return rng.standard_normal((T, d), dtype=np.float32).astype(np.float16)
+
+
+class GpuLayer:
+    def __init__(self, m, bank, wg, h, touched, counts):
+        self.m, self.bank, self.wg, self.h = m, bank, wg, h
+        self.touched, self.counts = touched, counts
+
+
+def build_gpu_layers(m, torch, E, d, f, bits, T, top_k, n_layers, dev):
+    layers = []
+    w1n, w2n, wgn, rng = layer0_numpy(E, d, f)
+    for li in range(n_layers):
+        if li == 0:
+            w1 = torch.from_numpy(w1n).to(dev)
+            w2 = torch.from_numpy(w2n).to(dev)
+            wg = torch.from_numpy(wgn).to(dev)
+            h = torch.from_numpy(tokens_numpy(rng, T, d)).to(dev)
+        else:
+            g = torch.Generator(device=dev).manual_seed(SEED + li)
+            w1 = torch.randn((E, d, f), generator=g, device=dev) * 0.02
+            w2 = torch.randn((E, f, d), generator=g, device=dev) * 0.02
+            wg = torch.randn((d, E), generator=g, device=dev) * 0.02
+            h = torch.randn((T, d), generator=g, device=dev).half()
+        bank = m.ExpertBank.from_float(w1, w2, bits, router=wg)
+        del w1, w2
+        _, ex, _ = m.moe_ffn_forward(h, bank, wg, top_k=top_k, return_routing=True)
+        counts = torch.bincount(ex.reshape(-1).long(), minlength=E).cpu().numpy()
+        layers.append(GpuLayer(m, bank, wg, h, int((counts > 0).sum()), counts))
+    torch.cuda.synchronize()
+    return layers
+
+
+def kernel_bytes(L, d, f, bits, T, top_k, out_bytes=4):
+    """Algorithmic bytes of the fused expert-FFN kernel (minus router):
+    packed W1+W2 + fp16-equivalent scales of every touched expert + fp16 input
+    rows + output rows."""
+    per_expert = packed_bytes(bits, d * f) * 2 + 2 * (f + d)
+    return L.touched * per_expert + T * top_k * d * 2 + T * d * out_bytes
+
+
+def step_flops(d, f, E, T, top_k):
+    return 2 * T * d * E + 4 * d * f * T * top_k
+
+
+def capture(torch, fn, layers, idxs):
+    """Capture one forward per listed layer into a CUDA graph (the forward is
+    stream-ordered with no host sync, so the whole route -> FFN chain replays
+    without host launch overhead)."""
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in idxs:
+            fn(layers[i])
+    return g
+
+
+def time_steps(torch, fn, layers, steps, warmup, dist=None, graphs=True):
+    """Device time of EXACTLY `steps` steps (layer i % L at step i), CUDA events
+    on the replay stream, barrier + synchronize on both sides, max over ranks."""
+    L = len(layers)
+    if graphs:
+        full = capture(torch, fn, layers, list(range(L)))
+        rem = steps % L
+        grem = capture(torch, fn, layers, list(range(rem))) if rem else None
+        run = lambda: ([full.replay() for _ in range(steps // L)], grem.replay() if grem else None)
+        for _ in range(max(1, -(-warmup // L))):
+            full.replay()
+    else:
+        run = lambda: [fn(layers[i % L]) for i in range(steps)]
+        for i in range(warmup):
+            fn(layers[i % L])
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    st = torch.cuda.current_stream()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    run()
+    b.record(st)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
+
+
+def profile_kernels(m, torch, layers, steps, fwd):
+    """Per-kernel CUDA-event durations on the launching stream: a graph of one
+    forward per layer with event nodes around every kernel, replayed until
+    >= `steps` steps have been measured."""
+    import ctypes as C
+    lib = m.load_library()
+    for L in layers:
+        lib.moqe_gpu_bank_profile(L.bank._h, 1)
+    g = capture(torch, fwd, layers, list(range(len(layers))))
+    for L in layers:
+        lib.moqe_gpu_bank_profile(L.bank._h, 0)
+    g.replay()
+    ms = (C.c_double * 6)()
+    n = (C.c_int64 * 6)()
+    for L in layers:
+        lib.moqe_gpu_bank_profile_read(L.bank._h, ms, n, 1)  # discard the warm replay
+    tot_ms = np.zeros(6)
+    tot_n = np.zeros(6, np.int64)
+    per_layer = [(np.zeros(6), np.zeros(6, np.int64)) for _ in layers]
+    reps = max(1, -(-steps // len(layers)))
+    for _ in range(reps):
+        g.replay()
+        for j, L in enumerate(layers):
+            lib.moqe_gpu_bank_profile_read(L.bank._h, ms, n, 1)
+            tot_ms += np.array(ms[:])
+            tot_n += np.array(n[:])
+            per_layer[j][0][:] += np.array(ms[:])
+            per_layer[j][1][:] += np.array(n[:])
+    for L in layers:
+        lib.moqe_gpu_bank_profile_read(L.bank._h, ms, n, 0)
+    del g
+    return tot_ms, tot_n, per_layer
+
+
+KINDS = ["route", "scatter", "gemv", "gemm_fc1", "gemm_fc2", "convert"]
+
+
+def run_point(m, torch, E, d, f, bits, T, top_k, steps, warmup, dev, hbm_peak, tc_peak, dist=None,
+              n_layers=N_LAYERS, detail=False):
+    layers = build_gpu_layers(m, torch, E, d, f, bits, T, top_k, n_layers, dev)
+    outs = [torch.empty((T, d), dtype=torch.float32, device=dev) for _ in layers]
+
+    # reuse preallocated outputs to keep allocator traffic out of the loop
+    def fwd_out(L, _o={id(L): o for L, o in zip(layers, outs)}):
+        m.moe_ffn_forward(L.h, L.bank, L.wg, top_k=top_k, out=_o[id(L)])
+
+    ms = time_steps(torch, fwd_out, layers, steps, warmup, dist)
+    prof_ms, prof_n, per_layer = profile_kernels(m, torch, layers, steps, fwd_out)
+    # dominant kernel = largest share of the step
+    dom = int(np.argmax(prof_ms))
+    avg_launch_ms = prof_ms[dom] / max(prof_n[dom], 1)
+    if KINDS[dom] == "gemv":
+        # bytes per launch averaged over the rotating layers (launch counts per layer)
+        tot_b = sum(kernel_bytes(L, d, f, bits, T, top_k) * n[2] for L, (_, n) in zip(layers, per_layer))
+        per_launch = tot_b / max(prof_n[2], 1)
+        achieved = per_launch / (avg_launch_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                "kernel": "k_ffn_gemv", "bytes_per_launch": int(per_launch),
+                "avg_launch_us": round(avg_launch_ms * 1e3, 3)}
+    else:
+        fl = step_flops(d, f, E, T, top_k) - 2 * T * d * E
+        share = 0.5 if KINDS[dom] in ("gemm_fc1", "gemm_fc2") else 1.0
+        achieved = fl * share / (avg_launch_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": tc_peak, "unit": "TFLOP/s",
+                "frac": round(achieved / tc_peak, 4), "traffic": None, "kernel": KINDS[dom],
+                "flops_per_launch": int(fl * share), "avg_launch_us": round(avg_launch_ms * 1e3, 3)}
+    touched = float(np.mean([L.touched for L in layers]))
+    step_b = np.mean([kernel_bytes(L, d, f, bits, T, top_k) for L in layers]) + d * E * 4
+    res = {
+        "bits": bits, "tokens": T, "top_k": top_k, "ms_per_step": ms,
+        "tokens_per_s": T / (ms * 1e-3),
+        "step_GBps": step_b / (ms * 1e-3) / 1e9,
+        "step_TFLOPs": step_flops(d, f, E, T, top_k) / (ms * 1e-3) / 1e12,
+        "touched_experts": touched, "roofline": roof,
+        "kernel_share": {KINDS[k]: round(float(prof_ms[k] / max(prof_ms.sum(), 1e-12)), 4)
+                         for k in range(6) if prof_n[k]},
+        "launches_per_step": int(round(prof_n.sum() / max(1, -(-steps // len(layers)) * len(layers)))),
+    }
+    return res, layers
+
+
+def e2e_point(m, torch, layers, steps, warmup, top_k, d):
+    """Through the by-value C-ABI call with pinned HOST buffers (H2D + D2H inside)."""
+    hs = [L.h.cpu().pin_memory() for L in layers]
+    T = hs[0].shape[0]
+    outs = [torch.empty((T, d), dtype=torch.float32).pin_memory() for _ in layers]
+    idx = {id(L): i for i, L in enumerate(layers)}
+
+    def fn(L):
+        i = idx[id(L)]
+        m.moe_ffn_forward_host(hs[i], L.bank, top_k=top_k, out=outs[i])
+
+    ms = time_steps(torch, fn, layers, steps, warmup, graphs=False)
+    return {"value": round(T / (ms * 1e-3), 1), "unit": "tokens/s",
+            "h2d_bytes_per_step": int(T * d * 2), "d2h_bytes_per_step": int(T * d * 4),
+            "ms_per_step": round(ms, 5)}
+
+
+# ---------------------------------------------------------------------------------------
+# reference CPU arm
+
+def reference_baseline(E, d, f, bits, T, reps=3, threads=None):
+    """Time the reference moqe::moe_ffn_forward (oracle/_ref) on the host cores,
+    token-sharded over all threads (bit-identical to 1 thread)."""
+    import oracle
+    orc = oracle.orc()
+    kind = "reference" if oracle.ref_available() else "port"
+    w1, w2, wg, rng = layer0_numpy(E, d, f)
+    h = tokens_numpy(rng, T, d).astype(np.float32)
+    q1 = np.empty((E, d, f), np.int8)
+    q2 = np.empty((E, f, d), np.int8)
+    s1 = np.empty((E, f), np.float32)
+    s2 = np.empty((E, d), np.float32)
+    for e in range(E):
+        q1[e], s1[e] = orc.quantize_linear(w1[e], bits)
+        q2[e], s2[e] = orc.quantize_linear(w2[e], bits)
+    del w1, w2
+    threads = threads or os.cpu_count() or 1
+    if kind == "reference":
+        bank = oracle.ref().bank(q1, s1, q2, s2, bits)
+        run = lambda: bank.forward(h, wg, threads)
+    else:
+        run = lambda: orc.moe_forward(h, wg, q1, s1, q2, s2, n_threads=threads)
+    run()  # discarded warm-up (bench.cpp:96-105 convention)
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        run()
+        ts.append(time.perf_counter() - t0)
+    med = statistics.median(ts)
+    return {"value": round(T / med, 3), "unit": "tokens/s", "cores": threads, "kind": kind,
+            "sample": f"T={T} int{bits} E={E} d={d} f={f} top-1 layer; 1 warm-up + median of {reps} "
+                      f"timed moe_ffn_forward calls, token-sharded over {threads} threads",
+            "seconds_per_step": round(med, 4)}
+
+
+# ---------------------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--bits", type=int, default=3)
+    ap.add_argument("--tokens", type=int, default=24)
+    ap.add_argument("--experts", type=int, default=32)
+    ap.add_argument("--d-model", type=int, default=1024)
+    ap.add_argument("--d-ffn", type=int, default=4096)
+    ap.add_argument("--top-k", type=int, default=1)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    E, d, f, bits, T, k = args.experts, args.d_model, args.d_ffn, args.bits, args.tokens, args.top_k
+    config = {"workload": f"config2 decode: MoE FFN layer d_model={d} d_ffn={f} {E} experts top-{k} "
+                          f"int{bits} per-channel, T={T} tokens",
+              "d_model": d, "d_ffn": f, "experts": E, "top_k": k, "weight_bits": bits, "tokens": T,
+              "activations": "fp16 ~N(0,1)", "weights": "~N(0,0.02) quantized per output channel",
+              "l2": f"{N_LAYERS} rotating layer replicas (working set > 126 MB L2)", "seed": SEED,
+              "launch": f"CUDA graph replay, one graph = {N_LAYERS} layer forwards"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        base = reference_baseline(E, d, f, bits, T)
+        line = {"metric": METRIC, "value": base["value"], "unit": "tokens/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": base["seconds_per_step"] * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic", "config": config, "impl": "reference",
+                "cpu_baseline": {k2: base[k2] for k2 in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": base["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import paper_2310_02410_b200 as m
+
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        dist = tdist
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    m.load_library()
+    hbm_peak, tc_peak, peak_kind = load_peaks()
+
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    head, layers = run_point(m, torch, E, d, f, bits, T, k, args.steps, args.warmup, dev, hbm_peak,
+                             tc_peak, dist)
+    clocks = sampler.stop() if sampler else None
+    e2e = e2e_point(m, torch, layers, max(args.steps // 4, 20), args.warmup, k, d) if rank == 0 else None
+    del layers
+    torch.cuda.empty_cache()
+
+    sweep = []
+    if rank == 0 and world == 1 and not args.no_sweep:
+        pts = [(b, t) for b in (8, 4, 3, 2) for t in (24, 4096)] + [(3, 16384), (2, 16384)]
+        for b, t in pts:
+            if (b, t) == (bits, T):
+                continue
+            try:
+                r, lay = run_point(m, torch, E, d, f, b, t, 1, max(min(args.steps, 60), 10), 5, dev,
+                                   hbm_peak, tc_peak, n_layers=4 if t >= 4096 else N_LAYERS)
+                del lay
+                torch.cuda.empty_cache()
+                sweep.append({kk: (round(v, 5) if isinstance(v, float) else v) for kk, v in r.items()})
+            except Exception as ex:  # report, never hide
+                sweep.append({"bits": b, "tokens": t, "error": str(ex)[:200]})
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = reference_baseline(E, d, f, bits, T)
+        cpu.pop("seconds_per_step", None)
+
+    if rank == 0:
+        value = head["tokens_per_s"] * world
+        roof = dict(head["roofline"])
+        roof["peak_kind"] = peak_kind
+        line = {"metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(head["ms_per_step"], 5),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+                "data": "synthetic", "config": config, "roofline": roof, "cpu_baseline": cpu,
+                "e2e": e2e, "gpu_launches": head["launches_per_step"] * args.steps,
+                "clocks": clocks,
+                "detail": {"step_GBps": round(head["step_GBps"], 1),
+                           "step_TFLOPs": round(head["step_TFLOPs"], 3),
+                           "touched_experts": head["touched_experts"],
+                           "kernel_share": head["kernel_share"],
+                           "accumulate": "f32", "weights": f"int{bits} codes -> f16 in registers/smem"},
+                "sweep": sweep}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

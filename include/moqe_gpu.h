@@ -123,8 +123,8 @@ int64_t moqe_gpu_bank_weight_bytes(moqe_bank_t bank);
 /* Execution-path selection for moe_forward:
  *   MOQE_PATH_AUTO  — weight-streaming GEMV for experts with <= 32 routed rows,
  *                     tcgen05 grouped GEMM for the rest (decided on device).
- *   MOQE_PATH_GEMV  — force the GEMV path (requires t*top_k <= 32*n_experts? no:
- *                     experts with more rows are processed in 32-row passes).
+ *   MOQE_PATH_GEMV  — force the GEMV path for every expert (experts with more
+ *                     than 32 rows are processed in 32-row passes).
  *   MOQE_PATH_GEMM  — force the tcgen05 grouped GEMM for all experts. */
 typedef enum moqe_path { MOQE_PATH_AUTO = 0, MOQE_PATH_GEMV = 1, MOQE_PATH_GEMM = 2 } moqe_path;
 
@@ -140,6 +140,18 @@ moqe_status moqe_gpu_moe_forward(moqe_bank_t bank, const void* h, moqe_dtype h_d
                                  const float* wg, int top_k, void* out, moqe_dtype out_dtype,
                                  int32_t* expert_out, float* gate_out, moqe_path path,
                                  void* stream);
+
+/* Per-kernel device timing (measurement support for bench.py): when enabled,
+ * every kernel moe_forward launches on `stream` is bracketed by CUDA events.
+ * Works under CUDA-graph capture (the events become graph nodes).
+ * profile_read synchronises and returns milliseconds and launch counts per
+ * kernel kind for the events recorded since the last clearing read; with
+ * keep != 0 the recorded events are kept (read again after the next graph
+ * replay). Kinds: 0 route(+plan), 1 scatter, 2 gemv (fused fc1+fc2),
+ * 3 gemm fc1, 4 gemm fc2, 5 convert. */
+#define MOQE_PROFILE_KINDS 6
+moqe_status moqe_gpu_bank_profile(moqe_bank_t bank, int enable);
+moqe_status moqe_gpu_bank_profile_read(moqe_bank_t bank, double* ms, int64_t* launches, int keep);
 
 /* Host-buffer convenience (the reference's by-value API): copies h (host,
  * pinned or pageable) in, runs moe_forward, copies out (host) back. Blocking. */

@@ -10,6 +10,8 @@
 #include <algorithm>
 #include <cstring>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "kernels.cuh"
 
@@ -67,7 +69,37 @@ struct moqe_bank {
     void* o_dev = nullptr;
     int64_t host_cap = 0;
     Workspace ws;
+    // per-kernel event timing (bench support)
+    bool prof = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
+    std::vector<std::pair<int, int>> ev_used;  // (kind, pool index)
+    double prof_ms[MOQE_PROFILE_KINDS] = {0};
+    int64_t prof_n[MOQE_PROFILE_KINDS] = {0};
 };
+
+namespace {
+struct KernelTimer {
+    moqe_bank* b;
+    int kind;
+    int idx = -1;
+    cudaStream_t st;
+    KernelTimer(moqe_bank* bank, int k, cudaStream_t s) : b(bank), kind(k), st(s) {
+        if (!b->prof) return;
+        idx = int(b->ev_used.size());
+        if (idx >= int(b->ev_pool.size())) {
+            cudaEvent_t a, z;
+            cudaEventCreate(&a);
+            cudaEventCreate(&z);
+            b->ev_pool.emplace_back(a, z);
+        }
+        b->ev_used.emplace_back(kind, idx);
+        cudaEventRecord(b->ev_pool[idx].first, st);
+    }
+    ~KernelTimer() {
+        if (idx >= 0) cudaEventRecord(b->ev_pool[idx].second, st);
+    }
+};
+}  // namespace
 
 namespace {
 
@@ -90,8 +122,7 @@ moqe_status ensure_workspace(moqe_bank* b, int64_t T, int topk) {
         w.block = nullptr;
     }
     const int E = b->E;
-    const int64_t nctas = (capT + route_tokens_per_cta(capT) - 1) / route_tokens_per_cta(capT) +
-                          (capT + kRouteWarps - 1) / kRouteWarps;  // either tile size
+    const int64_t nctas = (capT + 3) / 4;  // routing CTAs cover >= 4 tokens each
     const int maxmt = std::max(b->Np1, b->Np2) / TILE_N;
     const int64_t part_rows = capR;
     const int64_t part = gemv_partial_floats(part_rows, b->Kp1, b->Np1, b->Kp2, b->Np2);
@@ -297,9 +328,14 @@ moqe_status moqe_gpu_moe_forward(moqe_bank_t b, const void* h, moqe_dtype h_dtyp
 
     RouteArgs ra{h, h_dtype == MOQE_F16, t, int(b->d), wg, b->E, top_k, eff_path, inline_scatter ? 1 : 0,
                  gemm_block_n(), inline_scatter ? acc : nullptr};
-    cudaError_t ce = launch_route(ra, P, st);
+    cudaError_t ce;
+    {
+        KernelTimer kt(b, 0, st);
+        ce = launch_route(ra, P, st);
+    }
     if (ce != cudaSuccess) return cuda_fail(ce, "k_route");
     if (!inline_scatter) {
+        KernelTimer kt(b, 1, st);
         ce = launch_scatter(h, h_dtype == MOQE_F16, t, int(b->d), top_k, b->E, eff_path, P,
                             need_gemm ? w.x_perm : nullptr, b->Kp1, acc, st);
         if (ce != cudaSuccess) return cuda_fail(ce, "k_scatter");
@@ -308,19 +344,54 @@ moqe_status moqe_gpu_moe_forward(moqe_bank_t b, const void* h, moqe_dtype h_dtyp
         GemvArgs g{h, h_dtype == MOQE_F16, t, int(b->d), int(b->f), top_k, b->E, b->w1, b->w2,
                    b->w1_stride, b->w2_stride, b->s1, b->s2, b->b1, b->b2, b->Kp1, b->Np1, b->Kp2, b->Np2,
                    w.mid, out, out_dtype == MOQE_F16, acc, w.partial, w.part_rows, w.split_cnt};
+        KernelTimer kt(b, 2, st);
         ce = launch_gemv(b->bits, R > 16, g, P, st, b->num_sms);
         if (ce != cudaSuccess) return cuda_fail(ce, "k_ffn_gemv");
     }
     if (need_gemm) {
         GemmArgs g{w.x_perm, w.mid, b->w1, b->w2, b->w1_stride, b->w2_stride, b->s1, b->s2, b->b1, b->b2,
                    b->Kp1, b->Np1, b->Kp2, b->Np2, w.cap_rows, int(b->d), out, out_dtype == MOQE_F16, acc};
-        ce = launch_gemm(b->bits, g, P, st, b->num_sms);
-        if (ce != cudaSuccess) return cuda_fail(ce, "k_ffn_gemm");
+        {
+            KernelTimer kt(b, 3, st);
+            ce = launch_gemm(b->bits, 1, g, P, st, b->num_sms);
+        }
+        if (ce != cudaSuccess) return cuda_fail(ce, "k_ffn_gemm fc1");
+        {
+            KernelTimer kt(b, 4, st);
+            ce = launch_gemm(b->bits, 2, g, P, st, b->num_sms);
+        }
+        if (ce != cudaSuccess) return cuda_fail(ce, "k_ffn_gemm fc2");
     }
     if (top_k == 2 && out_dtype == MOQE_F16) {
         const int64_t n = t * b->d;
+        KernelTimer kt(b, 5, st);
         k_f32_to_f16<<<unsigned((n + 255) / 256), 256, 0, st>>>(acc, static_cast<__half*>(out), n);
         MOQE_CHECK_LAUNCH("k_f32_to_f16");
+    }
+    return MOQE_OK;
+}
+
+moqe_status moqe_gpu_bank_profile(moqe_bank_t b, int enable) {
+    if (!b) return fail(MOQE_INVALID_ARGUMENT, "profile: null bank");
+    b->prof = enable != 0;
+    return MOQE_OK;
+}
+
+moqe_status moqe_gpu_bank_profile_read(moqe_bank_t b, double* ms, int64_t* launches, int keep) {
+    if (!b) return fail(MOQE_INVALID_ARGUMENT, "profile: null bank");
+    MOQE_CUDA(cudaDeviceSynchronize());
+    for (auto& ku : b->ev_used) {
+        float t = 0.f;
+        MOQE_CUDA(cudaEventElapsedTime(&t, b->ev_pool[ku.second].first, b->ev_pool[ku.second].second));
+        b->prof_ms[ku.first] += t;
+        b->prof_n[ku.first] += 1;
+    }
+    if (!keep) b->ev_used.clear();
+    for (int k = 0; k < MOQE_PROFILE_KINDS; ++k) {
+        if (ms) ms[k] = b->prof_ms[k];
+        if (launches) launches[k] = b->prof_n[k];
+        b->prof_ms[k] = 0;
+        b->prof_n[k] = 0;
     }
     return MOQE_OK;
 }

@@ -5,5 +5,5 @@
 namespace moqe_gpu {
 bool gemm_available() { return false; }
 int gemm_block_n() { return 128; }
-cudaError_t launch_gemm(int, const GemmArgs&, const Plan&, cudaStream_t, int) { return cudaErrorNotSupported; }
+cudaError_t launch_gemm(int, int, const GemmArgs&, const Plan&, cudaStream_t, int) { return cudaErrorNotSupported; }
 }  // namespace moqe_gpu

@@ -74,6 +74,6 @@ struct GemmArgs {
 };
 bool gemm_available();
 int gemm_block_n();
-cudaError_t launch_gemm(int bits, const GemmArgs& g, const Plan& P, cudaStream_t st, int num_sms);
+cudaError_t launch_gemm(int bits, int phase, const GemmArgs& g, const Plan& P, cudaStream_t st, int num_sms);
 
 }  // namespace moqe_gpu

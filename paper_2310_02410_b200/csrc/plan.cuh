@@ -4,8 +4,7 @@
 
 namespace moqe_gpu {
 
-constexpr int kGemvMaxRows = 32;   // experts with <= this many routed rows take the GEMV path
-constexpr int kRouteWarps = 8;     // warps per routing CTA
+constexpr int kGemvMaxRows = 16;   // experts with <= this many routed rows take the GEMV path
 
 // All pointers are device memory owned by the bank's workspace.
 struct Plan {

@@ -2,6 +2,8 @@
 #pragma once
 #include <stdint.h>
 
+#include "common.cuh"
+
 namespace moqe_gpu {
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {

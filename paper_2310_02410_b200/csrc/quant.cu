@@ -15,6 +15,7 @@
 #include <cuda_fp16.h>
 
 #include "common.cuh"
+#include "codec.cuh"
 
 namespace moqe_gpu {
 
@@ -217,12 +218,14 @@ __global__ void k_retile(const uint8_t* __restrict__ src, int64_t K, int64_t N, 
         const int64_t k = kb * TILE_K + kk;
         q[kk] = (k < K && n < N) ? extract_code(s, k * N + n, bits) : 0;
     }
-    // row (n, kb) lives in tile (n/128, kb) at row n%128
+    // row (n, kb) lives in tile (n/128, kb) at row n%128, re-encoded (codec.cuh)
     const int64_t tile = (n / TILE_N) * kbs + kb;
     uint8_t* row = dst + m * dst_stride + tile * tile_bytes(bits) + (n % TILE_N) * row_bytes(bits);
-    for (int g = 0; g < TILE_K / 8; ++g) {
-        const uint64_t w = pack_group(q + g * 8, bits);
-        for (int i = 0; i < bits; ++i) row[g * bits + i] = uint8_t(w >> (8 * i));
+    switch (bits) {
+        case 2: encode_row<2>(q, row); break;
+        case 3: encode_row<3>(q, row); break;
+        case 4: encode_row<4>(q, row); break;
+        default: encode_row<8>(q, row); break;
     }
 }
 

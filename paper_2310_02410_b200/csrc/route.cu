@@ -152,107 +152,59 @@ __device__ void plan_tail(const RouteArgs& a, Plan P, int n_ctas, int tt) {
     }
 }
 
-// One warp computes TPW tokens x E experts (lane j handles experts j, j+32, ...).
-template <int EPL, int TPW>
-__global__ void __launch_bounds__(kRouteWarps * 32) k_route(RouteArgs a, Plan P) {
-    constexpr int TT = kRouteWarps * TPW;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int E = a.E, d = a.d, k = a.topk;
-    const int64_t tok0 = int64_t(blockIdx.x) * TT + warp * TPW;
-
-    float acc[TPW][EPL];
+// Shared tail of both routing kernels: per-token argmax / gate from logits
+// held by the warp (lane j <-> experts j, j+32, ...), stable local ranks, CTA
+// histogram, last-CTA planning.
+template <int EPL>
+__device__ __forceinline__ void finish_token(const RouteArgs& a, Plan& P, const float (&acc)[EPL], int64_t t,
+                                             int lt, int* s_exp) {
+    const int lane = threadIdx.x & 31, E = a.E, k = a.topk;
+    float b1v, b2v = 0.f;
+    int b1i, b2i = 0;
+    warp_argmax<EPL>(acc, E, -1, b1v, b1i);
+    float g1, g2 = 0.f;
+    if (k == 1) {
+        // softmax in double (model.cpp:214-227); gate = prob[best] (:343)
+        const double mx = double(b1v);
+        double s = 0.0;
 #pragma unroll
-    for (int i = 0; i < TPW; ++i)
+        for (int e = 0; e < EPL; ++e)
+            if (lane + 32 * e < E) s += exp(double(acc[e]) - mx);
 #pragma unroll
-        for (int e = 0; e < EPL; ++e) acc[i][e] = 0.0f;
-
-    for (int p0 = 0; p0 < d; p0 += 32) {
-        float hv[TPW];
-#pragma unroll
-        for (int i = 0; i < TPW; ++i) {
-            const int64_t t = tok0 + i;
-            hv[i] = (t < a.T && p0 + lane < d) ? load_act(a.h, a.h_f16, t * d + p0 + lane) : 0.0f;
-        }
-        const int qn = min(32, d - p0);
-#pragma unroll 4
-        for (int q = 0; q < qn; ++q) {
-            float w[EPL];
-#pragma unroll
-            for (int e = 0; e < EPL; ++e) {
-                const int j = lane + 32 * e;
-                w[e] = j < E ? __ldg(a.wg + int64_t(p0 + q) * E + j) : 0.0f;
-            }
-#pragma unroll
-            for (int i = 0; i < TPW; ++i) {
-                const float av = __shfl_sync(0xffffffffu, hv[i], q);
-#pragma unroll
-                for (int e = 0; e < EPL; ++e) {
-                    // reference: `if (av == 0.0f) continue; orow[j] += av * brow[j];`
-                    const float pr = __fmul_rn(av, w[e]);
-                    acc[i][e] = av != 0.0f ? __fadd_rn(acc[i][e], pr) : acc[i][e];
-                }
-            }
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        const float eb = float(exp(double(b1v) - mx));
+        g1 = float(double(eb) / s);
+    } else {
+        warp_argmax<EPL>(acc, E, b1i, b2v, b2i);
+        const double z = exp(double(b2v) - double(b1v));
+        g1 = float(1.0 / (1.0 + z));
+        g2 = float(z / (1.0 + z));
+    }
+    if (lane == 0) {
+        P.expert[t * k] = b1i;
+        P.gate[t * k] = g1;
+        s_exp[lt * k] = b1i;
+        if (k == 2) {
+            P.expert[t * k + 1] = b2i;
+            P.gate[t * k + 1] = g2;
+            s_exp[lt * k + 1] = b2i;
         }
     }
+}
 
-    __shared__ int s_exp[TT * 2];
-    __shared__ int s_hist[256];
-    for (int e = threadIdx.x; e < E; e += blockDim.x) s_hist[e] = 0;
-
-#pragma unroll
-    for (int i = 0; i < TPW; ++i) {
-        const int64_t t = tok0 + i;
-        const int lt = warp * TPW + i;
-        if (t >= a.T) {  // warp-uniform
-            if (lane == 0) { s_exp[lt * k] = -1; if (k == 2) s_exp[lt * k + 1] = -1; }
-            continue;
-        }
-        float b1v, b2v = 0.f;
-        int b1i, b2i = 0;
-        warp_argmax<EPL>(acc[i], E, -1, b1v, b1i);
-        float g1, g2 = 0.f;
-        if (k == 1) {
-            // softmax in double (model.cpp:214-227); gate = prob[best] (:343)
-            const double mx = double(b1v);
-            double s = 0.0;
-#pragma unroll
-            for (int e = 0; e < EPL; ++e)
-                if (lane + 32 * e < E) s += exp(double(acc[i][e]) - mx);
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-            const float eb = float(exp(double(b1v) - mx));
-            g1 = float(double(eb) / s);
-        } else {
-            warp_argmax<EPL>(acc[i], E, b1i, b2v, b2i);
-            const double z = exp(double(b2v) - double(b1v));
-            g1 = float(1.0 / (1.0 + z));
-            g2 = float(z / (1.0 + z));
-        }
-        if (lane == 0) {
-            P.expert[t * k] = b1i;
-            P.gate[t * k] = g1;
-            s_exp[lt * k] = b1i;
-            if (k == 2) {
-                P.expert[t * k + 1] = b2i;
-                P.gate[t * k + 1] = g2;
-                s_exp[lt * k + 1] = b2i;
-            }
-        }
-    }
+__device__ __forceinline__ void ranks_hist_plan(const RouteArgs& a, Plan& P, int* s_exp, int* s_hist, int tt) {
+    const int E = a.E, k = a.topk;
     __syncthreads();
-    // stable local ranks + CTA histogram
-    for (int i = threadIdx.x; i < TT * k; i += blockDim.x) {
+    for (int i = threadIdx.x; i < tt * k; i += blockDim.x) {
         const int e = s_exp[i];
         if (e < 0) continue;
         int r = 0;
         for (int j = 0; j < i; ++j) r += s_exp[j] == e;
-        P.lrank[int64_t(blockIdx.x) * TT * k + i] = r;
+        P.lrank[int64_t(blockIdx.x) * tt * k + i] = r;
         atomicAdd(&s_hist[e], 1);
     }
     __syncthreads();
     for (int e = threadIdx.x; e < E; e += blockDim.x) P.cta_counts[int64_t(blockIdx.x) * E + e] = s_hist[e];
-
-    // last CTA plans
     __threadfence();
     __syncthreads();
     __shared__ bool s_last;
@@ -260,7 +212,161 @@ __global__ void __launch_bounds__(kRouteWarps * 32) k_route(RouteArgs a, Plan P)
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    plan_tail(a, P, gridDim.x, TT);
+    plan_tail(a, P, gridDim.x, tt);
+}
+
+constexpr int kRouteSmallWarps = 4;   // one token per warp; a warp per SM sub-partition
+
+// Wg rows staged per chunk for a given expert count.
+__host__ __device__ constexpr int route_chunk_rows(int E) { return E <= 128 ? 4096 / (E < 32 ? 32 : E) : 32; }
+
+// Small T (decode): one warp per token, lane j <-> experts j, j+32, ...
+// Wg streams through a double-buffered smem chunk (register prefetch of the
+// next chunk overlaps the current chunk's sequential fp32 chain). EFIX > 0
+// compiles the expert count in (E == EFIX), so the 32-row inner loop unrolls
+// to immediate shuffles and smem offsets; EFIX == 0 is the generic path.
+template <int EPL, int EFIX>
+__global__ void __launch_bounds__(kRouteSmallWarps * 32) k_route_small(RouteArgs a, Plan P) {
+    constexpr int TT = kRouteSmallWarps;
+    extern __shared__ __align__(16) float s_w[];  // [2][rows * E]
+    __shared__ int s_exp[TT * 2];
+    __shared__ int s_hist[256];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int E = EFIX ? EFIX : a.E, d = a.d;
+    const int rows = EFIX ? route_chunk_rows(EFIX) : route_chunk_rows(a.E);
+    const int chunk = rows * E;
+    const int per_t = (chunk + blockDim.x - 1) / blockDim.x;  // <= 64
+    const int nchunks = (d + rows - 1) / rows;
+    const int64_t t = int64_t(blockIdx.x) * TT + warp;
+    const bool live = t < a.T;
+    for (int e = threadIdx.x; e < E; e += blockDim.x) s_hist[e] = 0;
+
+    float acc[EPL];
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) acc[e] = 0.0f;
+    float pre[64];
+    auto load_chunk = [&](int c) {
+        const int64_t base = int64_t(c) * chunk, lim = min(int64_t(d) * E, base + chunk);
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+            if (i < per_t) {
+                const int64_t idx = base + i * blockDim.x + threadIdx.x;
+                pre[i] = idx < lim ? __ldg(a.wg + idx) : 0.0f;
+            }
+        }
+    };
+    auto h_at = [&](int p) { return (live && p < d) ? load_act(a.h, a.h_f16, t * d + p) : 0.0f; };
+    load_chunk(0);
+    float hnext = h_at(lane);
+    for (int c = 0; c < nchunks; ++c) {
+        float* buf = s_w + (c & 1) * chunk;
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+            if (i < per_t && i * int(blockDim.x) + int(threadIdx.x) < chunk) buf[i * blockDim.x + threadIdx.x] = pre[i];
+        __syncthreads();
+        if (c + 1 < nchunks) load_chunk(c + 1);
+        const int p0 = c * rows;
+        for (int q0 = 0; q0 < rows; q0 += 32) {
+            const float hv = hnext;
+            hnext = h_at(p0 + q0 + 32 + lane);  // prefetch the next 32 activations
+            if (!live) continue;
+            const float* wb = buf + q0 * E + lane;
+#pragma unroll
+            for (int q = 0; q < 32; ++q) {
+                const float av = __shfl_sync(0xffffffffu, hv, q);  // 0 beyond d
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) {
+                    const float w = (EFIX || lane + 32 * e < E) ? wb[q * E + 32 * e] : 0.0f;
+                    // reference: `if (av == 0.0f) continue; orow[j] += av * brow[j];`
+                    const float pr = __fmul_rn(av, w);
+                    if (av != 0.0f) acc[e] = __fadd_rn(acc[e], pr);
+                }
+            }
+        }
+        // buffer (c&1) is rewritten at c+2, after the next iteration's barrier
+    }
+    if (live) finish_token<EPL>(a, P, acc, t, warp, s_exp);
+    else if (lane == 0) { s_exp[warp * a.topk] = -1; if (a.topk == 2) s_exp[warp * a.topk + 1] = -1; }
+    ranks_hist_plan(a, P, s_exp, s_hist, TT);
+}
+
+constexpr int kRouteBigWarps = 4;     // 128 tokens per CTA, one token per thread
+constexpr int kRouteBigGroup = 32;    // experts accumulated per pass
+constexpr int kRouteBigRows = 32;     // Wg / h rows staged per chunk
+
+// Large T (prefill): one token per thread; each Wg row is broadcast from smem
+// to the warp (LDS.128 = 4 experts), so a MAC costs one FMUL + one FADD.
+// Experts are processed in groups of 32 (logits kept in smem) so registers
+// stay bounded for any E <= 256; argmax/softmax then run per token.
+__global__ void __launch_bounds__(kRouteBigWarps * 32) k_route_big(RouteArgs a, Plan P) {
+    constexpr int TT = kRouteBigWarps * 32;
+    extern __shared__ __align__(16) float sm[];
+    float* s_h = sm;                                     // [kRouteBigRows][TT] transposed token rows
+    float* s_w = s_h + kRouteBigRows * (TT + 1);         // [kRouteBigRows][kRouteBigGroup]
+    float* s_log = s_w + kRouteBigRows * kRouteBigGroup; // [TT][E+1] logits
+    int* s_exp = reinterpret_cast<int*>(s_log + TT * (a.E + 1));  // [TT*2]
+    int* s_hist = s_exp + TT * 2;                        // [E]
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int E = a.E, d = a.d, LS = a.E + 1;
+    const int64_t t0 = int64_t(blockIdx.x) * TT;
+    for (int e = tid; e < E; e += blockDim.x) s_hist[e] = 0;
+
+    for (int g0 = 0; g0 < E; g0 += kRouteBigGroup) {
+        const int gn = min(kRouteBigGroup, E - g0);
+        float acc[kRouteBigGroup];
+#pragma unroll
+        for (int e = 0; e < kRouteBigGroup; ++e) acc[e] = 0.0f;
+        for (int p0 = 0; p0 < d; p0 += kRouteBigRows) {
+            const int pn = min(kRouteBigRows, d - p0);
+            __syncthreads();
+            // stage h[t0..t0+TT][p0..p0+pn] transposed (warp reads 32 p of one token row)
+            for (int r = warp; r < TT; r += kRouteBigWarps) {
+                const int64_t t = t0 + r;
+                s_h[lane * (TT + 1) + r] = (t < a.T && lane < pn) ? load_act(a.h, a.h_f16, t * d + p0 + lane) : 0.0f;
+            }
+            for (int i = tid; i < kRouteBigRows * kRouteBigGroup; i += blockDim.x) {
+                const int q = i / kRouteBigGroup, e = i % kRouteBigGroup;
+                s_w[i] = (q < pn && e < gn) ? __ldg(a.wg + int64_t(p0 + q) * E + g0 + e) : 0.0f;
+            }
+            __syncthreads();
+            for (int q = 0; q < pn; ++q) {
+                const float av = s_h[q * (TT + 1) + tid];
+                const float4* wr = reinterpret_cast<const float4*>(s_w + q * kRouteBigGroup);
+#pragma unroll
+                for (int e4 = 0; e4 < kRouteBigGroup / 4; ++e4) {
+                    const float4 w = wr[e4];
+                    const float p0f = __fmul_rn(av, w.x), p1f = __fmul_rn(av, w.y);
+                    const float p2f = __fmul_rn(av, w.z), p3f = __fmul_rn(av, w.w);
+                    if (av != 0.0f) {
+                        acc[4 * e4 + 0] = __fadd_rn(acc[4 * e4 + 0], p0f);
+                        acc[4 * e4 + 1] = __fadd_rn(acc[4 * e4 + 1], p1f);
+                        acc[4 * e4 + 2] = __fadd_rn(acc[4 * e4 + 2], p2f);
+                        acc[4 * e4 + 3] = __fadd_rn(acc[4 * e4 + 3], p3f);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < kRouteBigGroup; ++e)
+            if (e < gn) s_log[tid * LS + g0 + e] = acc[e];
+    }
+    __syncthreads();
+    // per-token argmax + gate (one warp per token, reusing the warp helpers)
+    for (int r = warp; r < TT; r += kRouteBigWarps) {
+        const int64_t t = t0 + r;
+        if (t >= a.T) {
+            if (lane == 0) { s_exp[r * a.topk] = -1; if (a.topk == 2) s_exp[r * a.topk + 1] = -1; }
+            continue;
+        }
+        float l[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int j = lane + 32 * e;
+            l[e] = j < E ? s_log[r * LS + j] : 0.0f;
+        }
+        finish_token<8>(a, P, l, t, r, s_exp);
+    }
+    ranks_hist_plan(a, P, s_exp, s_hist, TT);
 }
 
 // Scatter routing metadata and gather token rows into the expert-grouped
@@ -296,29 +402,53 @@ __global__ void __launch_bounds__(256) k_scatter(const void* h, int h_f16, int64
     for (int j = d + lane; j < ldx; j += 32) dst[j] = __float2half_rn(0.f);
 }
 
+// Route tile: tokens per routing CTA for a given T (must match scatter's tt).
+constexpr int64_t kRouteBigThreshold = 512;
+int route_tokens_per_cta(int64_t T) {
+    return T <= kRouteBigThreshold ? kRouteSmallWarps : kRouteBigWarps * 32;
+}
+
 namespace {
-template <int EPL, int TPW>
-cudaError_t launch_route_t(const RouteArgs& a, const Plan& P, cudaStream_t st) {
-    constexpr int TT = kRouteWarps * TPW;
-    const unsigned grid = unsigned((a.T + TT - 1) / TT);
-    k_route<EPL, TPW><<<grid, kRouteWarps * 32, 0, st>>>(a, P);
-    return cudaGetLastError();
+size_t route_big_smem(int E) {
+    return sizeof(float) * (kRouteBigRows * (kRouteBigWarps * 32 + 1) + kRouteBigRows * kRouteBigGroup +
+                            kRouteBigWarps * 32 * (E + 1)) +
+           sizeof(int) * (kRouteBigWarps * 32 * 2 + E);
 }
 }  // namespace
 
-// Route tile: tokens per routing CTA for a given T (must match scatter's tt).
-int route_tokens_per_cta(int64_t T) { return T <= 2048 ? kRouteWarps : kRouteWarps * 8; }
-
 cudaError_t launch_route(const RouteArgs& a, const Plan& P, cudaStream_t st) {
-    const bool big = a.T > 2048;
-    const int epl = (a.E + 31) / 32;
-#define MOQE_ROUTE_CASE(EPLV)                                                              \
-    if (epl <= EPLV) return big ? launch_route_t<EPLV, 8>(a, P, st) : launch_route_t<EPLV, 1>(a, P, st);
-    MOQE_ROUTE_CASE(1)
-    MOQE_ROUTE_CASE(2)
-    MOQE_ROUTE_CASE(4)
-    MOQE_ROUTE_CASE(8)
-#undef MOQE_ROUTE_CASE
+    const int tt = route_tokens_per_cta(a.T);
+    const unsigned grid = unsigned((a.T + tt - 1) / tt);
+    if (a.T > kRouteBigThreshold) {
+        const size_t smem = route_big_smem(a.E);
+        static int configured = 0;
+        if (!configured) {
+            cudaError_t e = cudaFuncSetAttribute(k_route_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 int(route_big_smem(256)));
+            if (e != cudaSuccess) return e;
+            configured = 1;
+        }
+        k_route_big<<<grid, kRouteBigWarps * 32, smem, st>>>(a, P);
+        return cudaGetLastError();
+    }
+    const size_t smem = size_t(2) * route_chunk_rows(a.E) * a.E * sizeof(float);
+    static bool configured = false;
+    if (!configured) {
+        const int mx = int(2 * 32 * 256 * sizeof(float));
+        cudaFuncSetAttribute(k_route_small<1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_route_small<2, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_route_small<4, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_route_small<8, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_route_small<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        configured = true;
+    }
+    switch (a.E) {
+        case 32: k_route_small<1, 32><<<grid, kRouteSmallWarps * 32, smem, st>>>(a, P); return cudaGetLastError();
+        case 64: k_route_small<2, 64><<<grid, kRouteSmallWarps * 32, smem, st>>>(a, P); return cudaGetLastError();
+        case 128: k_route_small<4, 128><<<grid, kRouteSmallWarps * 32, smem, st>>>(a, P); return cudaGetLastError();
+        case 256: k_route_small<8, 256><<<grid, kRouteSmallWarps * 32, smem, st>>>(a, P); return cudaGetLastError();
+        default: k_route_small<8, 0><<<grid, kRouteSmallWarps * 32, smem, st>>>(a, P); return cudaGetLastError();
+    }
     return cudaErrorInvalidValue;
 }
 
