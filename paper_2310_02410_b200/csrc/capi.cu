@@ -93,10 +93,10 @@ struct KernelTimer {
             b->ev_pool.emplace_back(a, z);
         }
         b->ev_used.emplace_back(kind, idx);
-        cudaEventRecord(b->ev_pool[idx].first, st);
+        cudaEventRecordWithFlags(b->ev_pool[idx].first, st, cudaEventRecordExternal);
     }
     ~KernelTimer() {
-        if (idx >= 0) cudaEventRecord(b->ev_pool[idx].second, st);
+        if (idx >= 0) cudaEventRecordWithFlags(b->ev_pool[idx].second, st, cudaEventRecordExternal);
     }
 };
 }  // namespace
@@ -226,7 +226,7 @@ moqe_status moqe_gpu_bank_create(int n_experts, int64_t d_model, int64_t d_ffn, 
     b->d = d_model;
     b->f = d_ffn;
     b->bits = bits;
-    b->Kp1 = int(round_up(d_model, TILE_K));
+    b->Kp1 = int(round_up(d_model, 2 * TILE_K));  // even number of k-blocks (GEMV stages hold 2)
     b->Np1 = int(round_up(d_ffn, TILE_N));
     b->Kp2 = b->Np1;  // fc2 consumes the full (zero-padded) fc1 output width
     b->Np2 = int(round_up(d_model, TILE_N));
@@ -308,6 +308,7 @@ moqe_status moqe_gpu_moe_forward(moqe_bank_t b, const void* h, moqe_dtype h_dtyp
     if (t == 0) return MOQE_OK;
     if (!h || !out) return fail(MOQE_INVALID_ARGUMENT, "moe_forward: null buffer");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    (void)cudaGetLastError();  // launch checks below must not see a stale error from unrelated calls
     moqe_status s = ensure_workspace(b, t, top_k);
     if (s != MOQE_OK) return s;
     Workspace& w = b->ws;

@@ -44,7 +44,9 @@ struct GemvItem {
 template <int BITS>
 struct GemvCfg {
     static constexpr int TB = tile_bytes(BITS);
-    static constexpr int NST = BITS == 2 ? 16 : BITS == 3 ? 12 : BITS == 4 ? 8 : 5;
+    static constexpr int KPS = 2;  // k-blocks (tiles) per ring stage
+    static constexpr int SB = KPS * TB;
+    static constexpr int NST = BITS == 2 ? 8 : BITS == 3 ? 6 : BITS == 4 ? 4 : 3;
 };
 
 struct GemvTables {
@@ -105,11 +107,13 @@ template <int BITS, int NT>
 __device__ __forceinline__ void gemv_mainloop(const uint8_t* ring, const uint8_t* act, uint64_t* full,
                                               uint64_t* empty, int& stage, int& sphase, int nblk, int warp,
                                               int lane, float (&acc)[2][4]) {
-    constexpr int TB = GemvCfg<BITS>::TB, NST = GemvCfg<BITS>::NST;
+    constexpr int TB = GemvCfg<BITS>::TB, SB = GemvCfg<BITS>::SB, NST = GemvCfg<BITS>::NST;
     const int gq = lane >> 2, tq = lane & 3;
-    for (int kb = 0; kb < nblk; ++kb) {
+    for (int kb = 0; kb < nblk; kb += 2) {  // nblk is even (k-chunks are multiples of 128)
         mbar_wait(&full[stage], sphase);
-        gemv_kblock<BITS, NT>(ring + stage * TB, act, kb, warp, gq, tq, acc);
+        const uint8_t* st = ring + stage * SB;
+        gemv_kblock<BITS, NT>(st, act, kb, warp, gq, tq, acc);
+        gemv_kblock<BITS, NT>(st + TB, act, kb + 1, warp, gq, tq, acc);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
         if (++stage == NST) { stage = 0; sphase ^= 1; }
@@ -119,10 +123,10 @@ __device__ __forceinline__ void gemv_mainloop(const uint8_t* ring, const uint8_t
 template <int BITS>
 __global__ void __launch_bounds__(kGemvThreads, 2) k_ffn_gemv(GemvArgs g, Plan P) {
     using Cfg = GemvCfg<BITS>;
-    constexpr int TB = Cfg::TB, NST = Cfg::NST;
+    constexpr int TB = Cfg::TB, SB = Cfg::SB, NST = Cfg::NST;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* ring = smem;
-    uint8_t* actbuf = smem + NST * TB;  // [2][kGemvRows][kActStride]
+    uint8_t* actbuf = smem + NST * SB;  // [2][kGemvRows][kActStride]
     uint64_t* full = reinterpret_cast<uint64_t*>(actbuf + 2 * kGemvRows * kActStride);
     uint64_t* empty = full + NST;
     uint64_t* ifull = empty + NST;
@@ -237,10 +241,10 @@ __global__ void __launch_bounds__(kGemvThreads, 2) k_ffn_gemv(GemvArgs g, Plan P
                 const int kb0 = k0 / TILE_K, kb1 = kb0 + klen / TILE_K;
                 const uint8_t* base = (p1 ? g.w1 + int64_t(it.e) * g.w1_stride : g.w2 + int64_t(it.e) * g.w2_stride) +
                                       (int64_t(it.mt) * kbs) * TB;
-                for (int kb = kb0; kb < kb1; ++kb) {
+                for (int kb = kb0; kb < kb1; kb += Cfg::KPS) {  // KPS consecutive tiles are contiguous
                     mbar_wait(&empty[stage], sphase ^ 1);
-                    mbar_arrive_expect_tx(&full[stage], TB);
-                    bulk_g2s_hint(ring + stage * TB, base + int64_t(kb) * TB, TB, &full[stage], pol);
+                    mbar_arrive_expect_tx(&full[stage], SB);
+                    bulk_g2s_hint(ring + stage * SB, base + int64_t(kb) * TB, SB, &full[stage], pol);
                     if (++stage == NST) { stage = 0; sphase ^= 1; }
                 }
             }
@@ -299,17 +303,20 @@ __global__ void __launch_bounds__(kGemvThreads, 2) k_ffn_gemv(GemvArgs g, Plan P
                     if (n < ntl && r < it.nrows)
                         __stcg(part + (int64_t(it.ks) * g.part_rows + it.row0 + r) * Np + chb + 8 * (i >> 1), acc[n][i]);
                 }
-            __threadfence();
             named_bar_sync(1, NCT);
             const int maxmt = max(nmt1, nmt2);
             unsigned* cnt = g.split_cnt + (p1 ? 0 : g.E * maxmt) + it.e * maxmt + it.mt;
-            if (ctid == 0) s_flag = atomicAdd(cnt, 1u) == unsigned(S * it.npass - 1);
+            if (ctid == 0) {
+                __threadfence();  // release the CTA's partials (ordered by the barrier above)
+                const bool last = atomicAdd(cnt, 1u) == unsigned(S * it.npass - 1);
+                if (last) {
+                    __threadfence();  // acquire the other CTAs' partials
+                    *cnt = 0;         // self-reset for the next forward
+                }
+                s_flag = last;
+            }
             named_bar_sync(1, NCT);
             do_epi = s_flag;
-            if (do_epi) {
-                __threadfence();
-                if (ctid == 0) *cnt = 0;  // self-reset for the next forward
-            }
         }
         if (do_epi) {
             const int npass_here = S > 1 ? it.npass : 1;
@@ -344,9 +351,11 @@ __global__ void __launch_bounds__(kGemvThreads, 2) k_ffn_gemv(GemvArgs g, Plan P
                     }
             }
             if (p1) {
-                __threadfence();
                 named_bar_sync(1, NCT);
-                if (ctid == 0) atomicAdd(&P.done[it.e], unsigned(S > 1 ? it.npass : 1));
+                if (ctid == 0) {
+                    __threadfence();  // publish mid rows before counting the m-tile done
+                    atomicAdd(&P.done[it.e], unsigned(S > 1 ? it.npass : 1));
+                }
             }
         }
         named_bar_sync(1, NCT);
@@ -358,7 +367,7 @@ __global__ void __launch_bounds__(kGemvThreads, 2) k_ffn_gemv(GemvArgs g, Plan P
 namespace {
 template <int BITS>
 size_t gemv_smem() {
-    return size_t(GemvCfg<BITS>::NST) * GemvCfg<BITS>::TB + size_t(2 * kGemvRows) * kActStride +
+    return size_t(GemvCfg<BITS>::NST) * GemvCfg<BITS>::SB + size_t(2 * kGemvRows) * kActStride +
            (2 * GemvCfg<BITS>::NST + 2 * kItemQ + 4) * 8 + kItemQ * sizeof(GemvItem) + sizeof(GemvTables) + 64;
 }
 

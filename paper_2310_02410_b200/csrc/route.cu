@@ -221,65 +221,78 @@ constexpr int kRouteSmallWarps = 4;   // one token per warp; a warp per SM sub-p
 __host__ __device__ constexpr int route_chunk_rows(int E) { return E <= 128 ? 4096 / (E < 32 ? 32 : E) : 32; }
 
 // Small T (decode): one warp per token, lane j <-> experts j, j+32, ...
-// Wg streams through a double-buffered smem chunk (register prefetch of the
-// next chunk overlaps the current chunk's sequential fp32 chain). EFIX > 0
-// compiles the expert count in (E == EFIX), so the 32-row inner loop unrolls
-// to immediate shuffles and smem offsets; EFIX == 0 is the generic path.
+// The token rows sit in smem (loaded once); Wg streams through a
+// double-buffered smem chunk (register prefetch of the next chunk overlaps the
+// current chunk's sequential fp32 chain). EFIX > 0 compiles the expert count
+// in (E == EFIX): the chunk copy is unpredicated float4 and the 32-row inner
+// loop unrolls to immediate smem offsets; EFIX == 0 is the generic path.
 template <int EPL, int EFIX>
 __global__ void __launch_bounds__(kRouteSmallWarps * 32) k_route_small(RouteArgs a, Plan P) {
     constexpr int TT = kRouteSmallWarps;
-    extern __shared__ __align__(16) float s_w[];  // [2][rows * E]
+    constexpr int NT = kRouteSmallWarps * 32;
+    extern __shared__ __align__(16) float s_dyn[];
     __shared__ int s_exp[TT * 2];
     __shared__ int s_hist[256];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int E = EFIX ? EFIX : a.E, d = a.d;
     const int rows = EFIX ? route_chunk_rows(EFIX) : route_chunk_rows(a.E);
     const int chunk = rows * E;
-    const int per_t = (chunk + blockDim.x - 1) / blockDim.x;  // <= 64
     const int nchunks = (d + rows - 1) / rows;
+    const int dpad = nchunks * rows;
+    float* s_w = s_dyn;                     // [2][chunk]
+    float* s_hrow = s_dyn + 2 * chunk;      // [TT][dpad] token rows, zero padded
     const int64_t t = int64_t(blockIdx.x) * TT + warp;
     const bool live = t < a.T;
     for (int e = threadIdx.x; e < E; e += blockDim.x) s_hist[e] = 0;
+    for (int p = lane; p < dpad; p += 32)
+        s_hrow[warp * dpad + p] = (live && p < d) ? load_act(a.h, a.h_f16, t * d + p) : 0.0f;
 
     float acc[EPL];
 #pragma unroll
     for (int e = 0; e < EPL; ++e) acc[e] = 0.0f;
-    float pre[64];
+    // EFIX: chunk == 4096 floats (E <= 128) or 32*E; each thread moves chunk/NT floats as float4
+    constexpr int V4 = EFIX ? (route_chunk_rows(EFIX) * EFIX) / (4 * NT) : 1;
+    float4 pre[V4];
+    const int64_t lim = int64_t(d) * E;
     auto load_chunk = [&](int c) {
-        const int64_t base = int64_t(c) * chunk, lim = min(int64_t(d) * E, base + chunk);
+        const int64_t base = int64_t(c) * chunk;
+        if constexpr (EFIX != 0) {
 #pragma unroll
-        for (int i = 0; i < 64; ++i) {
-            if (i < per_t) {
-                const int64_t idx = base + i * blockDim.x + threadIdx.x;
-                pre[i] = idx < lim ? __ldg(a.wg + idx) : 0.0f;
+            for (int i = 0; i < V4; ++i) {
+                const int64_t idx = base + 4 * (int64_t(i) * NT + threadIdx.x);
+                pre[i] = idx + 3 < lim ? __ldg(reinterpret_cast<const float4*>(a.wg + idx)) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
         }
     };
-    auto h_at = [&](int p) { return (live && p < d) ? load_act(a.h, a.h_f16, t * d + p) : 0.0f; };
+    auto store_chunk = [&](int c, float* buf) {
+        if constexpr (EFIX != 0) {
+#pragma unroll
+            for (int i = 0; i < V4; ++i) reinterpret_cast<float4*>(buf)[i * NT + threadIdx.x] = pre[i];
+        } else {
+            const int64_t base = int64_t(c) * chunk;
+            for (int i = threadIdx.x; i < chunk; i += NT) buf[i] = base + i < lim ? __ldg(a.wg + base + i) : 0.0f;
+        }
+    };
     load_chunk(0);
-    float hnext = h_at(lane);
     for (int c = 0; c < nchunks; ++c) {
         float* buf = s_w + (c & 1) * chunk;
-#pragma unroll
-        for (int i = 0; i < 64; ++i)
-            if (i < per_t && i * int(blockDim.x) + int(threadIdx.x) < chunk) buf[i * blockDim.x + threadIdx.x] = pre[i];
+        store_chunk(c, buf);
         __syncthreads();
         if (c + 1 < nchunks) load_chunk(c + 1);
-        const int p0 = c * rows;
-        for (int q0 = 0; q0 < rows; q0 += 32) {
-            const float hv = hnext;
-            hnext = h_at(p0 + q0 + 32 + lane);  // prefetch the next 32 activations
-            if (!live) continue;
-            const float* wb = buf + q0 * E + lane;
+        if (live) {
+            const float* hr = s_hrow + warp * dpad + c * rows;
+            for (int q0 = 0; q0 < rows; q0 += 32) {
+                const float* wb = buf + q0 * E + lane;
 #pragma unroll
-            for (int q = 0; q < 32; ++q) {
-                const float av = __shfl_sync(0xffffffffu, hv, q);  // 0 beyond d
+                for (int q = 0; q < 32; ++q) {
+                    const float av = hr[q0 + q];  // smem broadcast; 0 beyond d
 #pragma unroll
-                for (int e = 0; e < EPL; ++e) {
-                    const float w = (EFIX || lane + 32 * e < E) ? wb[q * E + 32 * e] : 0.0f;
-                    // reference: `if (av == 0.0f) continue; orow[j] += av * brow[j];`
-                    const float pr = __fmul_rn(av, w);
-                    if (av != 0.0f) acc[e] = __fadd_rn(acc[e], pr);
+                    for (int e = 0; e < EPL; ++e) {
+                        const float w = (EFIX || lane + 32 * e < E) ? wb[q * E + 32 * e] : 0.0f;
+                        // reference: `if (av == 0.0f) continue; orow[j] += av * brow[j];`
+                        const float pr = __fmul_rn(av, w);
+                        if (av != 0.0f) acc[e] = __fadd_rn(acc[e], pr);
+                    }
                 }
             }
         }
@@ -290,48 +303,68 @@ __global__ void __launch_bounds__(kRouteSmallWarps * 32) k_route_small(RouteArgs
     ranks_hist_plan(a, P, s_exp, s_hist, TT);
 }
 
-constexpr int kRouteBigWarps = 4;     // 128 tokens per CTA, one token per thread
+constexpr int kRouteBigWarps = 2;     // 64 tokens per CTA, one token per thread
 constexpr int kRouteBigGroup = 32;    // experts accumulated per pass
 constexpr int kRouteBigRows = 32;     // Wg / h rows staged per chunk
 
 // Large T (prefill): one token per thread; each Wg row is broadcast from smem
 // to the warp (LDS.128 = 4 experts), so a MAC costs one FMUL + one FADD.
-// Experts are processed in groups of 32 (logits kept in smem) so registers
-// stay bounded for any E <= 256; argmax/softmax then run per token.
+// Staging is double-buffered through registers (all loads of chunk c+1 are in
+// flight while chunk c is consumed). Experts are processed in groups of 32
+// (logits kept in smem) so registers stay bounded for any E <= 256;
+// argmax/softmax then run one warp per token.
 __global__ void __launch_bounds__(kRouteBigWarps * 32) k_route_big(RouteArgs a, Plan P) {
     constexpr int TT = kRouteBigWarps * 32;
+    constexpr int NT = TT;
+    constexpr int HS = TT + 1;  // transposed h stride (conflict-free)
     extern __shared__ __align__(16) float sm[];
-    float* s_h = sm;                                     // [kRouteBigRows][TT] transposed token rows
-    float* s_w = s_h + kRouteBigRows * (TT + 1);         // [kRouteBigRows][kRouteBigGroup]
-    float* s_log = s_w + kRouteBigRows * kRouteBigGroup; // [TT][E+1] logits
-    int* s_exp = reinterpret_cast<int*>(s_log + TT * (a.E + 1));  // [TT*2]
-    int* s_hist = s_exp + TT * 2;                        // [E]
+    float* s_h = sm;                                     // [2][kRouteBigRows][HS]
+    float* s_w = s_h + 2 * kRouteBigRows * HS;           // [2][kRouteBigRows][kRouteBigGroup] (16B aligned: 2*32*65 floats)
+    float* s_log = s_w + 2 * kRouteBigRows * kRouteBigGroup;  // [TT][E+1]
+    int* s_exp = reinterpret_cast<int*>(s_log + TT * (a.E + 1));
+    int* s_hist = s_exp + TT * 2;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int E = a.E, d = a.d, LS = a.E + 1;
     const int64_t t0 = int64_t(blockIdx.x) * TT;
     for (int e = tid; e < E; e += blockDim.x) s_hist[e] = 0;
-
+    const int nchunks = (d + kRouteBigRows - 1) / kRouteBigRows;
+    // per thread per chunk: h = TT*32 values -> 32 per thread (token row segments);
+    // Wg = 32 rows x 32 experts -> 16 per thread
+    constexpr int HV = kRouteBigRows * TT / NT, WV = kRouteBigRows * kRouteBigGroup / NT;
+    float ph[HV], pw[WV];
     for (int g0 = 0; g0 < E; g0 += kRouteBigGroup) {
         const int gn = min(kRouteBigGroup, E - g0);
+        auto load = [&](int c) {
+            const int p0 = c * kRouteBigRows;
+#pragma unroll
+            for (int i = 0; i < HV; ++i) {  // element (r = token, q = p offset), q fastest per warp
+                const int r = i * (NT / 32) + warp, q = lane;
+                const int64_t tt = t0 + r;
+                ph[i] = (tt < a.T && p0 + q < d) ? load_act(a.h, a.h_f16, tt * d + p0 + q) : 0.0f;
+            }
+#pragma unroll
+            for (int i = 0; i < WV; ++i) {
+                const int idx = i * NT + tid, q = idx / kRouteBigGroup, e = idx % kRouteBigGroup;
+                pw[i] = (p0 + q < d && e < gn) ? __ldg(a.wg + int64_t(p0 + q) * E + g0 + e) : 0.0f;
+            }
+        };
         float acc[kRouteBigGroup];
 #pragma unroll
         for (int e = 0; e < kRouteBigGroup; ++e) acc[e] = 0.0f;
-        for (int p0 = 0; p0 < d; p0 += kRouteBigRows) {
-            const int pn = min(kRouteBigRows, d - p0);
+        load(0);
+        for (int c = 0; c < nchunks; ++c) {
+            float* bh = s_h + (c & 1) * kRouteBigRows * HS;
+            float* bw = s_w + (c & 1) * kRouteBigRows * kRouteBigGroup;
+#pragma unroll
+            for (int i = 0; i < HV; ++i) bh[lane * HS + i * (NT / 32) + warp] = ph[i];
+#pragma unroll
+            for (int i = 0; i < WV; ++i) bw[i * NT + tid] = pw[i];
             __syncthreads();
-            // stage h[t0..t0+TT][p0..p0+pn] transposed (warp reads 32 p of one token row)
-            for (int r = warp; r < TT; r += kRouteBigWarps) {
-                const int64_t t = t0 + r;
-                s_h[lane * (TT + 1) + r] = (t < a.T && lane < pn) ? load_act(a.h, a.h_f16, t * d + p0 + lane) : 0.0f;
-            }
-            for (int i = tid; i < kRouteBigRows * kRouteBigGroup; i += blockDim.x) {
-                const int q = i / kRouteBigGroup, e = i % kRouteBigGroup;
-                s_w[i] = (q < pn && e < gn) ? __ldg(a.wg + int64_t(p0 + q) * E + g0 + e) : 0.0f;
-            }
-            __syncthreads();
+            if (c + 1 < nchunks) load(c + 1);
+            const int pn = min(kRouteBigRows, d - c * kRouteBigRows);
             for (int q = 0; q < pn; ++q) {
-                const float av = s_h[q * (TT + 1) + tid];
-                const float4* wr = reinterpret_cast<const float4*>(s_w + q * kRouteBigGroup);
+                const float av = bh[q * HS + tid];
+                const float4* wr = reinterpret_cast<const float4*>(bw + q * kRouteBigGroup);
 #pragma unroll
                 for (int e4 = 0; e4 < kRouteBigGroup / 4; ++e4) {
                     const float4 w = wr[e4];
@@ -349,8 +382,8 @@ __global__ void __launch_bounds__(kRouteBigWarps * 32) k_route_big(RouteArgs a, 
 #pragma unroll
         for (int e = 0; e < kRouteBigGroup; ++e)
             if (e < gn) s_log[tid * LS + g0 + e] = acc[e];
+        __syncthreads();
     }
-    __syncthreads();
     // per-token argmax + gate (one warp per token, reusing the warp helpers)
     for (int r = warp; r < TT; r += kRouteBigWarps) {
         const int64_t t = t0 + r;
@@ -410,7 +443,7 @@ int route_tokens_per_cta(int64_t T) {
 
 namespace {
 size_t route_big_smem(int E) {
-    return sizeof(float) * (kRouteBigRows * (kRouteBigWarps * 32 + 1) + kRouteBigRows * kRouteBigGroup +
+    return sizeof(float) * (2 * kRouteBigRows * (kRouteBigWarps * 32 + 1) + 2 * kRouteBigRows * kRouteBigGroup +
                             kRouteBigWarps * 32 * (E + 1)) +
            sizeof(int) * (kRouteBigWarps * 32 * 2 + E);
 }
@@ -431,10 +464,13 @@ cudaError_t launch_route(const RouteArgs& a, const Plan& P, cudaStream_t st) {
         k_route_big<<<grid, kRouteBigWarps * 32, smem, st>>>(a, P);
         return cudaGetLastError();
     }
-    const size_t smem = size_t(2) * route_chunk_rows(a.E) * a.E * sizeof(float);
+    const int rows = route_chunk_rows(a.E);
+    const int dpad = (a.d + rows - 1) / rows * rows;
+    const size_t smem = (size_t(2) * rows * a.E + size_t(kRouteSmallWarps) * dpad) * sizeof(float);
+    if (smem > 200 * 1024) return cudaErrorInvalidValue;
     static bool configured = false;
     if (!configured) {
-        const int mx = int(2 * 32 * 256 * sizeof(float));
+        const int mx = 200 * 1024;
         cudaFuncSetAttribute(k_route_small<1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(k_route_small<2, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(k_route_small<4, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
