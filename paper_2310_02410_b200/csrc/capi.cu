@@ -132,7 +132,7 @@ moqe_status ensure_workspace(moqe_bank* b, int64_t T, int topk) {
     add(4, capR); add(4, capR); add(4, capR); add(4, nctas * E); add(4, E); add(4, E + 1);
     add(4, capR); add(4, capR); add(4, capR); add(4, E); add(4, E); add(4, E + 1); add(4, 8);
     add(4, 8); add(4, E); add(4, 2 * E * maxmt);
-    add(2, capR * b->Np1); add(2, capR * b->Kp1); add(4, part); add(4, capT * b->d);
+    add(2, capR * b->Np1); add(2, capR * b->Kp1); add(4, part); add(4, capT * b->d); add(4, capT * E);
     MOQE_CUDA(cudaMalloc(&w.block, bytes));
     MOQE_CUDA(cudaMemset(w.block, 0, bytes));
     char* p = static_cast<char*>(w.block);
@@ -159,6 +159,7 @@ moqe_status ensure_workspace(moqe_bank* b, int64_t T, int topk) {
     w.partial = carve<float>(p, part);
     P.partial = w.partial;
     w.out_acc = carve<float>(p, capT * b->d);
+    P.logits = carve<float>(p, capT * E);
     w.part_rows = part_rows;
     w.cap_rows = capR;
     w.cap_tokens = capT;
@@ -320,6 +321,9 @@ moqe_status moqe_gpu_moe_forward(moqe_bank_t b, const void* h, moqe_dtype h_dtyp
     if (eff_path == MOQE_PATH_GEMM && !gemm_available())
         return fail(MOQE_NOT_SUPPORTED, "moe_forward: tcgen05 GEMM path not built");
     if (eff_path == MOQE_PATH_AUTO && !gemm_available()) eff_path = MOQE_PATH_GEMV;
+    // Small batches: no expert can exceed a few GEMV passes, so skip the (empty)
+    // scatter + tcgen05 launches entirely; the GEMV takes every expert.
+    if (eff_path == MOQE_PATH_AUTO && t * top_k <= 4 * kGemvMaxRows) eff_path = MOQE_PATH_GEMV;
     // tcgen05 GEMM path handles experts with > kGemvMaxRows rows; tiny batches never need it.
     const bool need_gemm = eff_path == MOQE_PATH_GEMM || (eff_path == MOQE_PATH_AUTO && R > kGemvMaxRows);
     const bool need_gemv = eff_path != MOQE_PATH_GEMM;
@@ -440,7 +444,7 @@ moqe_status moqe_gpu_route(const void* h, moqe_dtype h_dtype, int64_t t, int64_t
     auto sz = [&](int64_t n) { int64_t r = bytes; bytes += round_up(4 * std::max<int64_t>(n, 1), 256); return r; };
     const int64_t o_lrank = sz(R), o_cta = sz(nctas * E), o_counts = sz(E), o_off = sz(E + 1),
                   o_pt = sz(R), o_pg = sz(R), o_inv = sz(R), o_gl = sz(E), o_ml = sz(E), o_ts = sz(E + 1),
-                  o_meta = sz(8), o_tk = sz(8), o_done = sz(E);
+                  o_meta = sz(8), o_tk = sz(8), o_done = sz(E), o_log = sz(t * E);
     char* blk = nullptr;
     MOQE_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&blk), bytes, st));
     MOQE_CUDA(cudaMemsetAsync(blk, 0, bytes, st));
@@ -460,6 +464,7 @@ moqe_status moqe_gpu_route(const void* h, moqe_dtype h_dtype, int64_t t, int64_t
     P.meta = reinterpret_cast<int32_t*>(blk + o_meta);
     P.tickets = reinterpret_cast<unsigned*>(blk + o_tk);
     P.done = reinterpret_cast<unsigned*>(blk + o_done);
+    P.logits = reinterpret_cast<float*>(blk + o_log);
     RouteArgs ra{h, h_dtype == MOQE_F16, t, int(d), wg, E, top_k, 0, 0, 128, nullptr};
     cudaError_t ce = launch_route(ra, P, st);
     cudaFreeAsync(blk, st);

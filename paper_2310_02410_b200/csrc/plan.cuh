@@ -25,6 +25,7 @@ struct Plan {
     unsigned* done;       // [E]    GEMV fc1 m-tiles finished per expert
     unsigned* split_done; // [E * max_mt] GEMV fc2 split-K arrivals
     float* partial;       // GEMV fc2 split-K partials
+    float* logits;        // [T][E] router logits (large-T path)
 };
 
 }  // namespace moqe_gpu

@@ -205,13 +205,15 @@ __device__ __forceinline__ void ranks_hist_plan(const RouteArgs& a, Plan& P, int
     }
     __syncthreads();
     for (int e = threadIdx.x; e < E; e += blockDim.x) P.cta_counts[int64_t(blockIdx.x) * E + e] = s_hist[e];
-    __threadfence();
     __syncthreads();
     __shared__ bool s_last;
-    if (threadIdx.x == 0) s_last = atomicAdd(&P.tickets[0], 1u) == gridDim.x - 1;
+    if (threadIdx.x == 0) {
+        __threadfence();  // release this CTA's routing results (ordered by the barrier)
+        s_last = atomicAdd(&P.tickets[0], 1u) == gridDim.x - 1;
+        if (s_last) __threadfence();  // acquire everyone else's
+    }
     __syncthreads();
     if (!s_last) return;
-    __threadfence();
     plan_tail(a, P, gridDim.x, tt);
 }
 
@@ -303,103 +305,136 @@ __global__ void __launch_bounds__(kRouteSmallWarps * 32) k_route_small(RouteArgs
     ranks_hist_plan(a, P, s_exp, s_hist, TT);
 }
 
-constexpr int kRouteBigWarps = 2;     // 64 tokens per CTA, one token per thread
-constexpr int kRouteBigGroup = 32;    // experts accumulated per pass
-constexpr int kRouteBigRows = 32;     // Wg / h rows staged per chunk
-
-// Large T (prefill): one token per thread; each Wg row is broadcast from smem
-// to the warp (LDS.128 = 4 experts), so a MAC costs one FMUL + one FADD.
-// Staging is double-buffered through registers (all loads of chunk c+1 are in
-// flight while chunk c is consumed). Experts are processed in groups of 32
-// (logits kept in smem) so registers stay bounded for any E <= 256;
-// argmax/softmax then run one warp per token.
-__global__ void __launch_bounds__(kRouteBigWarps * 32) k_route_big(RouteArgs a, Plan P) {
-    constexpr int TT = kRouteBigWarps * 32;
-    constexpr int NT = TT;
-    constexpr int HS = TT + 1;  // transposed h stride (conflict-free)
-    extern __shared__ __align__(16) float sm[];
-    float* s_h = sm;                                     // [2][kRouteBigRows][HS]
-    float* s_w = s_h + 2 * kRouteBigRows * HS;           // [2][kRouteBigRows][kRouteBigGroup] (16B aligned: 2*32*65 floats)
-    float* s_log = s_w + 2 * kRouteBigRows * kRouteBigGroup;  // [TT][E+1]
-    int* s_exp = reinterpret_cast<int*>(s_log + TT * (a.E + 1));
-    int* s_hist = s_exp + TT * 2;
+// ---- large T (prefill) ----------------------------------------------------------------
+// k_route_logits: one warp = 32 tokens (lane = token) x 8 experts; a CTA = 4
+// warps = 32 tokens x 32 experts, grid (T/32, E/32). Each Wg row is a smem
+// broadcast (2 x LDS.128 per warp per k), so a MAC costs one FMUL + one FADD
+// in the reference's exact order. Staging is double-buffered in registers.
+constexpr int kRLTok = 32, kRLExp = 32, kRLRows = 32;
+// VEC: fp16 activations with d % 8 == 0 and E % 32 == 0 -> one 16-byte h load
+// and two float4 Wg loads per thread per 32-row chunk; otherwise scalar.
+template <bool VEC>
+__global__ void __launch_bounds__(128) k_route_logits(RouteArgs a, float* __restrict__ logits) {
+    __shared__ __align__(16) float s_h[2][kRLRows][kRLTok + 1];
+    __shared__ __align__(16) float s_w[2][kRLRows][kRLExp];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int E = a.E, d = a.d, LS = a.E + 1;
-    const int64_t t0 = int64_t(blockIdx.x) * TT;
-    for (int e = tid; e < E; e += blockDim.x) s_hist[e] = 0;
-    const int nchunks = (d + kRouteBigRows - 1) / kRouteBigRows;
-    // per thread per chunk: h = TT*32 values -> 32 per thread (token row segments);
-    // Wg = 32 rows x 32 experts -> 16 per thread
-    constexpr int HV = kRouteBigRows * TT / NT, WV = kRouteBigRows * kRouteBigGroup / NT;
-    float ph[HV], pw[WV];
-    for (int g0 = 0; g0 < E; g0 += kRouteBigGroup) {
-        const int gn = min(kRouteBigGroup, E - g0);
-        auto load = [&](int c) {
-            const int p0 = c * kRouteBigRows;
+    const int E = a.E, d = a.d;
+    const int64_t t0 = int64_t(blockIdx.x) * kRLTok;
+    const int e0 = blockIdx.y * kRLExp;
+    const int nchunks = (d + kRLRows - 1) / kRLRows;
+    float ph[8], pw[8];
+    auto load = [&](int c) {
+        const int p0 = c * kRLRows;
+        if constexpr (VEC) {
+            const int r = tid >> 2, c8 = tid & 3;  // token row, 8-wide p segment
+            const int64_t t = t0 + r;
+            uint4 hv = make_uint4(0, 0, 0, 0);
+            if (t < a.T && p0 + 8 * c8 < d)
+                hv = __ldg(reinterpret_cast<const uint4*>(static_cast<const __half*>(a.h) + t * d + p0 + 8 * c8));
+            const __half2* h2 = reinterpret_cast<const __half2*>(&hv);
 #pragma unroll
-            for (int i = 0; i < HV; ++i) {  // element (r = token, q = p offset), q fastest per warp
-                const int r = i * (NT / 32) + warp, q = lane;
-                const int64_t tt = t0 + r;
-                ph[i] = (tt < a.T && p0 + q < d) ? load_act(a.h, a.h_f16, tt * d + p0 + q) : 0.0f;
+            for (int i = 0; i < 4; ++i) {
+                const float2 f = __half22float2(h2[i]);
+                ph[2 * i] = f.x;
+                ph[2 * i + 1] = f.y;
             }
 #pragma unroll
-            for (int i = 0; i < WV; ++i) {
-                const int idx = i * NT + tid, q = idx / kRouteBigGroup, e = idx % kRouteBigGroup;
-                pw[i] = (p0 + q < d && e < gn) ? __ldg(a.wg + int64_t(p0 + q) * E + g0 + e) : 0.0f;
+            for (int i = 0; i < 2; ++i) {
+                const int idx = i * 128 + tid, q = idx >> 3, c4 = idx & 7;
+                float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (p0 + q < d) w = __ldg(reinterpret_cast<const float4*>(a.wg + int64_t(p0 + q) * E + e0 + 4 * c4));
+                pw[4 * i] = w.x; pw[4 * i + 1] = w.y; pw[4 * i + 2] = w.z; pw[4 * i + 3] = w.w;
             }
-        };
-        float acc[kRouteBigGroup];
+        } else {
 #pragma unroll
-        for (int e = 0; e < kRouteBigGroup; ++e) acc[e] = 0.0f;
-        load(0);
-        for (int c = 0; c < nchunks; ++c) {
-            float* bh = s_h + (c & 1) * kRouteBigRows * HS;
-            float* bw = s_w + (c & 1) * kRouteBigRows * kRouteBigGroup;
-#pragma unroll
-            for (int i = 0; i < HV; ++i) bh[lane * HS + i * (NT / 32) + warp] = ph[i];
-#pragma unroll
-            for (int i = 0; i < WV; ++i) bw[i * NT + tid] = pw[i];
-            __syncthreads();
-            if (c + 1 < nchunks) load(c + 1);
-            const int pn = min(kRouteBigRows, d - c * kRouteBigRows);
-            for (int q = 0; q < pn; ++q) {
-                const float av = bh[q * HS + tid];
-                const float4* wr = reinterpret_cast<const float4*>(bw + q * kRouteBigGroup);
-#pragma unroll
-                for (int e4 = 0; e4 < kRouteBigGroup / 4; ++e4) {
-                    const float4 w = wr[e4];
-                    const float p0f = __fmul_rn(av, w.x), p1f = __fmul_rn(av, w.y);
-                    const float p2f = __fmul_rn(av, w.z), p3f = __fmul_rn(av, w.w);
-                    if (av != 0.0f) {
-                        acc[4 * e4 + 0] = __fadd_rn(acc[4 * e4 + 0], p0f);
-                        acc[4 * e4 + 1] = __fadd_rn(acc[4 * e4 + 1], p1f);
-                        acc[4 * e4 + 2] = __fadd_rn(acc[4 * e4 + 2], p2f);
-                        acc[4 * e4 + 3] = __fadd_rn(acc[4 * e4 + 3], p3f);
-                    }
-                }
+            for (int i = 0; i < 8; ++i) {
+                const int r = i * 4 + warp;
+                const int64_t t = t0 + r;
+                ph[i] = (t < a.T && p0 + lane < d) ? load_act(a.h, a.h_f16, t * d + p0 + lane) : 0.0f;
+                const int q = i * 4 + warp;
+                pw[i] = (p0 + q < d && e0 + lane < E) ? __ldg(a.wg + int64_t(p0 + q) * E + e0 + lane) : 0.0f;
             }
         }
+    };
+    auto store = [&](int b) {
+        if constexpr (VEC) {
+            const int r = tid >> 2, c8 = tid & 3;
 #pragma unroll
-        for (int e = 0; e < kRouteBigGroup; ++e)
-            if (e < gn) s_log[tid * LS + g0 + e] = acc[e];
+            for (int i = 0; i < 8; ++i) s_h[b][8 * c8 + i][r] = ph[i];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int idx = i * 128 + tid, q = idx >> 3, c4 = idx & 7;
+                *reinterpret_cast<float4*>(&s_w[b][q][4 * c4]) = make_float4(pw[4 * i], pw[4 * i + 1], pw[4 * i + 2], pw[4 * i + 3]);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                s_h[b][lane][i * 4 + warp] = ph[i];
+                s_w[b][i * 4 + warp][lane] = pw[i];
+            }
+        }
+    };
+    float acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
+    load(0);
+    for (int c = 0; c < nchunks; ++c) {
+        const int b = c & 1;
+        store(b);
         __syncthreads();
-    }
-    // per-token argmax + gate (one warp per token, reusing the warp helpers)
-    for (int r = warp; r < TT; r += kRouteBigWarps) {
-        const int64_t t = t0 + r;
-        if (t >= a.T) {
-            if (lane == 0) { s_exp[r * a.topk] = -1; if (a.topk == 2) s_exp[r * a.topk + 1] = -1; }
-            continue;
+        if (c + 1 < nchunks) load(c + 1);
+        const int pn = min(kRLRows, d - c * kRLRows);
+#pragma unroll 8
+        for (int q = 0; q < kRLRows; ++q) {
+            if (q >= pn) break;
+            const float av = s_h[b][q][lane];
+            const float4 w0 = *reinterpret_cast<const float4*>(&s_w[b][q][8 * warp]);
+            const float4 w1 = *reinterpret_cast<const float4*>(&s_w[b][q][8 * warp + 4]);
+            const float w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+            float pr[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) pr[e] = __fmul_rn(av, w[e]);
+            // reference: `if (av == 0.0f) continue; orow[j] += av * brow[j];`
+            if (av != 0.0f) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc[e] = __fadd_rn(acc[e], pr[e]);
+            }
         }
+    }
+    const int64_t t = t0 + lane;
+    if (t < a.T) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int j = e0 + 8 * warp + e;
+            if (j < E) logits[t * E + j] = acc[e];
+        }
+    }
+}
+
+constexpr int kRouteSelWarps = 32;  // tokens per selection CTA
+// k_route_select: one warp per token reads its E logits, applies the
+// reference argmax / softmax gate (or top-2), then stable ranks, CTA
+// histogram and the last-CTA plan as in the small-T kernel.
+__global__ void __launch_bounds__(kRouteSelWarps * 32) k_route_select(RouteArgs a, Plan P) {
+    __shared__ int s_exp[kRouteSelWarps * 2];
+    __shared__ int s_hist[256];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int E = a.E;
+    for (int e = threadIdx.x; e < E; e += blockDim.x) s_hist[e] = 0;
+    const int64_t t = int64_t(blockIdx.x) * kRouteSelWarps + warp;
+    if (t < a.T) {
         float l[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
             const int j = lane + 32 * e;
-            l[e] = j < E ? s_log[r * LS + j] : 0.0f;
+            l[e] = j < E ? __ldcg(P.logits + t * E + j) : 0.0f;
         }
-        finish_token<8>(a, P, l, t, r, s_exp);
+        finish_token<8>(a, P, l, t, warp, s_exp);
+    } else if (lane == 0) {
+        s_exp[warp * a.topk] = -1;
+        if (a.topk == 2) s_exp[warp * a.topk + 1] = -1;
     }
-    ranks_hist_plan(a, P, s_exp, s_hist, TT);
+    ranks_hist_plan(a, P, s_exp, s_hist, kRouteSelWarps);
 }
 
 // Scatter routing metadata and gather token rows into the expert-grouped
@@ -437,31 +472,18 @@ __global__ void __launch_bounds__(256) k_scatter(const void* h, int h_f16, int64
 
 // Route tile: tokens per routing CTA for a given T (must match scatter's tt).
 constexpr int64_t kRouteBigThreshold = 512;
-int route_tokens_per_cta(int64_t T) {
-    return T <= kRouteBigThreshold ? kRouteSmallWarps : kRouteBigWarps * 32;
-}
-
-namespace {
-size_t route_big_smem(int E) {
-    return sizeof(float) * (2 * kRouteBigRows * (kRouteBigWarps * 32 + 1) + 2 * kRouteBigRows * kRouteBigGroup +
-                            kRouteBigWarps * 32 * (E + 1)) +
-           sizeof(int) * (kRouteBigWarps * 32 * 2 + E);
-}
-}  // namespace
+int route_tokens_per_cta(int64_t T) { return T <= kRouteBigThreshold ? kRouteSmallWarps : kRouteSelWarps; }
 
 cudaError_t launch_route(const RouteArgs& a, const Plan& P, cudaStream_t st) {
     const int tt = route_tokens_per_cta(a.T);
     const unsigned grid = unsigned((a.T + tt - 1) / tt);
     if (a.T > kRouteBigThreshold) {
-        const size_t smem = route_big_smem(a.E);
-        static int configured = 0;
-        if (!configured) {
-            cudaError_t e = cudaFuncSetAttribute(k_route_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 int(route_big_smem(256)));
-            if (e != cudaSuccess) return e;
-            configured = 1;
-        }
-        k_route_big<<<grid, kRouteBigWarps * 32, smem, st>>>(a, P);
+        if (P.logits == nullptr) return cudaErrorInvalidValue;
+        dim3 lg(unsigned((a.T + kRLTok - 1) / kRLTok), unsigned((a.E + kRLExp - 1) / kRLExp));
+        const bool vec = a.h_f16 && (a.d % 8) == 0 && (a.E % 32) == 0 && (reinterpret_cast<uintptr_t>(a.h) & 15) == 0;
+        if (vec) k_route_logits<true><<<lg, 128, 0, st>>>(a, P.logits);
+        else k_route_logits<false><<<lg, 128, 0, st>>>(a, P.logits);
+        k_route_select<<<grid, kRouteSelWarps * 32, 0, st>>>(a, P);
         return cudaGetLastError();
     }
     const int rows = route_chunk_rows(a.E);
