@@ -310,6 +310,33 @@ def e2e_point(m, torch, layers, steps, warmup, top_k, d):
 
 
 # ---------------------------------------------------------------------------------------
+# expert parallelism (N > 1): experts sharded E/G, T tokens per rank (weak scaling)
+
+def run_point_ep(m, torch, dist, E, d, f, bits, T, top_k, steps, warmup, dev, rank, world, n_layers=N_LAYERS):
+    from paper_2310_02410_b200.ep import ExpertParallelMoE, shard_range
+    lo, hi = shard_range(E, world, rank)
+    layers = []
+    for li in range(n_layers):
+        w1 = torch.empty((hi - lo, d, f), device=dev)
+        w2 = torch.empty((hi - lo, f, d), device=dev)
+        for e in range(lo, hi):  # expert e's weights are the same whichever rank owns it
+            g = torch.Generator(device=dev).manual_seed(SEED + 1000 * li + e)
+            w1[e - lo] = torch.randn((d, f), generator=g, device=dev) * 0.02
+            w2[e - lo] = torch.randn((f, d), generator=g, device=dev) * 0.02
+        gr = torch.Generator(device=dev).manual_seed(SEED + 1000 * li + 999)
+        wg = torch.randn((d, E), generator=gr, device=dev) * 0.02
+        gh = torch.Generator(device=dev).manual_seed(SEED + 7919 * (li + 1) + rank)
+        h = torch.randn((T, d), generator=gh, device=dev).half()
+        bank = m.ExpertBank.from_float(w1, w2, bits)
+        del w1, w2
+        layers.append((ExpertParallelMoE(bank, wg, E, top_k=top_k), h))
+    torch.cuda.synchronize()
+    fwd = lambda L: L[0].forward(L[1])
+    ms = time_steps(torch, fwd, layers, steps, warmup, dist, graphs=False)
+    return {"ms_per_step": ms, "tokens_per_s_per_rank": T / (ms * 1e-3), "experts_per_rank": hi - lo}
+
+
+# ---------------------------------------------------------------------------------------
 # reference CPU arm
 
 def reference_baseline(E, d, f, bits, T, reps=3, threads=None):
@@ -363,6 +390,7 @@ def main():
     ap.add_argument("--top-k", type=int, default=1)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ep", action="store_true", help="expert-parallel path even at one rank")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -404,6 +432,34 @@ def main():
     torch.cuda.set_device(dev)
     m.load_library()
     hbm_peak, tc_peak, peak_kind = load_peaks()
+
+    if world > 1 or args.ep:
+        if dist is None:
+            import torch.distributed as tdist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29517")
+            tdist.init_process_group("nccl", world_size=1, rank=0, device_id=dev)
+            dist = tdist
+        sampler = ClockSampler(local) if rank == 0 else None
+        if sampler:
+            sampler.start()
+        ep = run_point_ep(m, torch, dist, E, d, f, bits, T, k, args.steps, args.warmup, dev, rank, world)
+        clocks = sampler.stop() if sampler else None
+        if rank == 0:
+            config["workload"] = (f"expert-parallel MoE FFN layer d_model={d} d_ffn={f} {E} experts "
+                                  f"({ep['experts_per_rank']}/rank) top-{k} int{bits}, T={T} tokens per rank")
+            config["parallelism"] = f"ep{world}"
+            line = {"metric": METRIC, "value": round(ep["tokens_per_s_per_rank"] * world, 1), "unit": "tokens/s",
+                    "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                    "ms_per_step": round(ep["ms_per_step"], 5), "higher_is_better": True, "scaling": "weak",
+                    "vs_baseline": None, "dtype": "f16", "data": "synthetic", "config": config,
+                    "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": None, "clocks": clocks,
+                    "detail": {"note": "eager EP steps (NCCL all_to_all dispatch/return, host-known split sizes); "
+                                       "max over ranks"}}
+            print(json.dumps(line), flush=True)
+        dist.barrier()
+        dist.destroy_process_group()
+        return
 
     sampler = ClockSampler(local) if rank == 0 else None
     if sampler:

@@ -141,6 +141,15 @@ moqe_status moqe_gpu_moe_forward(moqe_bank_t bank, const void* h, moqe_dtype h_d
                                  int32_t* expert_out, float* gate_out, moqe_path path,
                                  void* stream);
 
+/* Expert FFN on rows that are already routed (expert-parallel owner side):
+ * out[r] = gate[r] * (relu(x[r] W1_e + b1) W2_e + b2), e = expert[r] (bank-local
+ * expert index). x [rows x d] (device, f32/f16), expert int32 [rows], gate f32
+ * [rows], out [rows x d]. Same kernels as moe_forward minus the router; rows are
+ * grouped per expert in ascending row order (model.cpp:360-364). */
+moqe_status moqe_gpu_expert_ffn(moqe_bank_t bank, const void* x, moqe_dtype x_dtype, int64_t rows,
+                                const int32_t* expert, const float* gate, void* out, moqe_dtype out_dtype,
+                                moqe_path path, void* stream);
+
 /* Per-kernel device timing (measurement support for bench.py): when enabled,
  * every kernel moe_forward launches on `stream` is bracketed by CUDA events.
  * Works under CUDA-graph capture (the events become graph nodes).

@@ -181,6 +181,19 @@ class Oracle(_Lib):
         shp = (t,) if top_k == 1 else (t, top_k)
         return out[:t], ex[: t * top_k].reshape(shp), g[: t * top_k].reshape(shp)
 
+    def expert_ffn(self, x, q1, s1, q2, s2, b1=None, b2=None):
+        """relu(x W1' + b1) W2' + b2 for rows x [m x d] (model.cpp:381-385)."""
+        x = np.ascontiguousarray(x, np.float32)
+        m, d = x.shape
+        f = q1.shape[1]
+        y = np.zeros((max(m, 1), d), np.float32)
+        arr = lambda a, t: None if a is None else np.ascontiguousarray(a, t)
+        self.lib.orc_expert_ffn(_p(x, C.c_float), m, d, f, _p(arr(q1, np.int8), C.c_int8),
+                                _p(arr(s1, np.float32), C.c_float), _p(arr(q2, np.int8), C.c_int8),
+                                _p(arr(s2, np.float32), C.c_float), _p(arr(b1, np.float32), C.c_float),
+                                _p(arr(b2, np.float32), C.c_float), _p(y, C.c_float))
+        return y[:m]
+
     def layer_norm(self, x, gain, bias):
         x = np.ascontiguousarray(x, np.float32)
         out = np.zeros_like(x)

@@ -262,6 +262,30 @@ def moe_ffn_forward(h: torch.Tensor, bank: ExpertBank, gate_weights: Optional[to
     return out
 
 
+def expert_ffn(x: torch.Tensor, bank: ExpertBank, expert: torch.Tensor, gate: torch.Tensor,
+               out_dtype: torch.dtype = torch.float32, path: str = "auto",
+               out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Expert FFN on pre-routed rows (expert-parallel owner side):
+    out[r] = gate[r] * FFN_{expert[r]}(x[r]), expert ids local to `bank`."""
+    xd = x.dtype if x.dtype in (torch.float16, torch.float32) else torch.float32
+    x = _dev(x, xd, "expert_ffn")
+    if x.dim() != 2 or x.shape[1] != bank.d:
+        raise _lib.InvalidArgument("matmul: shape mismatch")
+    ex = _dev(expert, torch.int32, "expert_ffn").reshape(-1)
+    gt = _dev(gate, torch.float32, "expert_ffn").reshape(-1)
+    R = x.shape[0]
+    if ex.numel() != R or gt.numel() != R:
+        raise _lib.InvalidArgument("expert_ffn: one expert id and gate per row")
+    if R and (int(ex.min()) < 0 or int(ex.max()) >= bank.E):
+        raise _lib.InvalidArgument("expert_ffn: expert id out of range")
+    if out is None:
+        out = torch.empty((R, bank.d), dtype=out_dtype, device=x.device)
+    check(_lib.load().moqe_gpu_expert_ffn(
+        bank._h, _ptr(x), _lib.F16 if xd == torch.float16 else _lib.F32, R, _ptr(ex), _ptr(gt), _ptr(out),
+        _lib.F16 if out.dtype == torch.float16 else _lib.F32, _PATH[path], _stream()))
+    return out
+
+
 def moe_ffn_forward_host(h_host: torch.Tensor, bank: ExpertBank, top_k: int = 1,
                          out: Optional[torch.Tensor] = None, out_dtype=torch.float32) -> torch.Tensor:
     """By-value (host buffer) call, like the reference API: copies in, forward, copies out."""

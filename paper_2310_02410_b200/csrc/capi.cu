@@ -295,17 +295,24 @@ int64_t moqe_gpu_bank_weight_bytes(moqe_bank_t b) {
     return (b->w1_stride + b->w2_stride) * b->E;
 }
 
-moqe_status moqe_gpu_moe_forward(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64_t t,
-                                 const float* wg, int top_k, void* out, moqe_dtype out_dtype,
-                                 int32_t* expert_out, float* gate_out, moqe_path path, void* stream) {
+namespace {
+// Shared forward body. With pre_expert/pre_gate (expert-parallel owner side),
+// rows arrive already routed: the plan is built from the given ids (top-1 per
+// row) and the router is skipped.
+moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64_t t, const float* wg, int top_k,
+                         void* out, moqe_dtype out_dtype, int32_t* expert_out, float* gate_out, moqe_path path,
+                         void* stream, const int32_t* pre_expert, const float* pre_gate) {
     if (!b) return fail(MOQE_INVALID_ARGUMENT, "moe_ffn_forward: empty expert bank");
     if (t < 0) return fail(MOQE_INVALID_ARGUMENT, "moe_ffn_forward: negative token count");
     if (top_k != 1 && top_k != 2) return fail(MOQE_INVALID_ARGUMENT, "moe_forward: top_k must be 1 or 2");
     if (top_k == 2 && b->E < 2) return fail(MOQE_INVALID_ARGUMENT, "moe_forward: top-2 needs >= 2 experts");
     if (h_dtype != MOQE_F32 && h_dtype != MOQE_F16) return fail(MOQE_INVALID_ARGUMENT, "moe_forward: bad h dtype");
     if (out_dtype != MOQE_F32 && out_dtype != MOQE_F16) return fail(MOQE_INVALID_ARGUMENT, "moe_forward: bad out dtype");
-    if (!wg) wg = b->wg;
-    if (!wg) return fail(MOQE_INVALID_ARGUMENT, "top1_route: no gate weights");
+    const bool pre = pre_expert != nullptr;
+    if (!pre) {
+        if (!wg) wg = b->wg;
+        if (!wg) return fail(MOQE_INVALID_ARGUMENT, "top1_route: no gate weights");
+    }
     if (t == 0) return MOQE_OK;
     if (!h || !out) return fail(MOQE_INVALID_ARGUMENT, "moe_forward: null buffer");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -314,8 +321,13 @@ moqe_status moqe_gpu_moe_forward(moqe_bank_t b, const void* h, moqe_dtype h_dtyp
     if (s != MOQE_OK) return s;
     Workspace& w = b->ws;
     Plan P = w.P;
-    if (expert_out) P.expert = expert_out;
-    if (gate_out) P.gate = gate_out;
+    if (pre) {
+        P.expert = const_cast<int32_t*>(pre_expert);
+        P.gate = const_cast<float*>(pre_gate);
+    } else {
+        if (expert_out) P.expert = expert_out;
+        if (gate_out) P.gate = gate_out;
+    }
     const int64_t R = t * top_k;
     int eff_path = int(path);
     if (eff_path == MOQE_PATH_GEMM && !gemm_available())
@@ -323,8 +335,7 @@ moqe_status moqe_gpu_moe_forward(moqe_bank_t b, const void* h, moqe_dtype h_dtyp
     if (eff_path == MOQE_PATH_AUTO && !gemm_available()) eff_path = MOQE_PATH_GEMV;
     // Small batches: no expert can exceed a few GEMV passes, so skip the (empty)
     // scatter + tcgen05 launches entirely; the GEMV takes every expert.
-    if (eff_path == MOQE_PATH_AUTO && t * top_k <= 4 * kGemvMaxRows) eff_path = MOQE_PATH_GEMV;
-    // tcgen05 GEMM path handles experts with > kGemvMaxRows rows; tiny batches never need it.
+    if (eff_path == MOQE_PATH_AUTO && R <= 4 * kGemvMaxRows) eff_path = MOQE_PATH_GEMV;
     const bool need_gemm = eff_path == MOQE_PATH_GEMM || (eff_path == MOQE_PATH_AUTO && R > kGemvMaxRows);
     const bool need_gemv = eff_path != MOQE_PATH_GEMM;
     const bool inline_scatter = !need_gemm && R <= 256;
@@ -336,12 +347,13 @@ moqe_status moqe_gpu_moe_forward(moqe_bank_t b, const void* h, moqe_dtype h_dtyp
     cudaError_t ce;
     {
         KernelTimer kt(b, 0, st);
-        ce = launch_route(ra, P, st);
+        ce = pre ? launch_plan_from_ids(ra, P, st) : launch_route(ra, P, st);
     }
-    if (ce != cudaSuccess) return cuda_fail(ce, "k_route");
+    if (ce != cudaSuccess) return cuda_fail(ce, pre ? "k_plan_from_ids" : "k_route");
     if (!inline_scatter) {
         KernelTimer kt(b, 1, st);
-        ce = launch_scatter(h, h_dtype == MOQE_F16, t, int(b->d), top_k, b->E, eff_path, P,
+        const int tt = pre ? kPlanIdsTile : route_tokens_per_cta(t);
+        ce = launch_scatter(h, h_dtype == MOQE_F16, t, int(b->d), top_k, b->E, eff_path, tt, P,
                             need_gemm ? w.x_perm : nullptr, b->Kp1, acc, st);
         if (ce != cudaSuccess) return cuda_fail(ce, "k_scatter");
     }
@@ -374,6 +386,22 @@ moqe_status moqe_gpu_moe_forward(moqe_bank_t b, const void* h, moqe_dtype h_dtyp
         MOQE_CHECK_LAUNCH("k_f32_to_f16");
     }
     return MOQE_OK;
+}
+}  // namespace
+
+moqe_status moqe_gpu_moe_forward(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64_t t,
+                                 const float* wg, int top_k, void* out, moqe_dtype out_dtype,
+                                 int32_t* expert_out, float* gate_out, moqe_path path, void* stream) {
+    return forward_impl(b, h, h_dtype, t, wg, top_k, out, out_dtype, expert_out, gate_out, path, stream, nullptr,
+                        nullptr);
+}
+
+moqe_status moqe_gpu_expert_ffn(moqe_bank_t b, const void* x, moqe_dtype x_dtype, int64_t rows,
+                                const int32_t* expert, const float* gate, void* out, moqe_dtype out_dtype,
+                                moqe_path path, void* stream) {
+    if (!expert || !gate) return fail(MOQE_INVALID_ARGUMENT, "expert_ffn: null expert ids / gates");
+    return forward_impl(b, x, x_dtype, rows, nullptr, 1, out, out_dtype, nullptr, nullptr, path, stream, expert,
+                        gate);
 }
 
 moqe_status moqe_gpu_bank_profile(moqe_bank_t b, int enable) {

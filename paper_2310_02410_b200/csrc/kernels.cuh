@@ -24,7 +24,10 @@ struct RouteArgs {
 };
 cudaError_t launch_route(const RouteArgs& a, const Plan& P, cudaStream_t st);
 int route_tokens_per_cta(int64_t T);
-cudaError_t launch_scatter(const void* h, int h_f16, int64_t T, int d, int topk, int E, int path,
+// rows already routed: plan with kRouteSelWarps rows per CTA (scatter must use that tile)
+cudaError_t launch_plan_from_ids(const RouteArgs& a, const Plan& P, cudaStream_t st);
+constexpr int kPlanIdsTile = 32;
+cudaError_t launch_scatter(const void* h, int h_f16, int64_t T, int d, int topk, int E, int path, int tt,
                            const Plan& P, __half* x_perm, int ldx, float* zero_out, cudaStream_t st);
 
 moqe_status retile(const uint8_t* src, int64_t K, int64_t N, int bits, int n_mats, uint8_t* dst,

@@ -437,6 +437,30 @@ __global__ void __launch_bounds__(kRouteSelWarps * 32) k_route_select(RouteArgs 
     ranks_hist_plan(a, P, s_exp, s_hist, kRouteSelWarps);
 }
 
+// Pre-routed rows (expert-parallel owner side): expert ids / gates are inputs;
+// build stable ranks, per-CTA histograms and the plan exactly as routing does.
+__global__ void __launch_bounds__(kRouteSelWarps * 32) k_plan_from_ids(RouteArgs a, Plan P) {
+    __shared__ int s_exp[kRouteSelWarps * 2];
+    __shared__ int s_hist[256];
+    for (int e = threadIdx.x; e < a.E; e += blockDim.x) s_hist[e] = 0;
+    if (threadIdx.x < kRouteSelWarps) {
+        const int64_t t = int64_t(blockIdx.x) * kRouteSelWarps + threadIdx.x;
+        int e = -1;
+        if (t < a.T) {
+            e = P.expert[t];
+            if (e < 0 || e >= a.E) e = -1;  // validated on the host; never index out of range
+        }
+        s_exp[threadIdx.x] = e;
+    }
+    ranks_hist_plan(a, P, s_exp, s_hist, kRouteSelWarps);
+}
+
+cudaError_t launch_plan_from_ids(const RouteArgs& a, const Plan& P, cudaStream_t st) {
+    const unsigned grid = unsigned((a.T + kRouteSelWarps - 1) / kRouteSelWarps);
+    k_plan_from_ids<<<grid, kRouteSelWarps * 32, 0, st>>>(a, P);
+    return cudaGetLastError();
+}
+
 // Scatter routing metadata and gather token rows into the expert-grouped
 // fp16 activation matrix x_perm [T*k x ldx] (tcgen05 B operand; zero-padded
 // to ldx columns). One warp per (token, slot).
@@ -510,12 +534,11 @@ cudaError_t launch_route(const RouteArgs& a, const Plan& P, cudaStream_t st) {
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_scatter(const void* h, int h_f16, int64_t T, int d, int topk, int E, int path,
+cudaError_t launch_scatter(const void* h, int h_f16, int64_t T, int d, int topk, int E, int path, int tt,
                            const Plan& P, __half* x_perm, int ldx, float* zero_out, cudaStream_t st) {
     const int64_t n = T * topk;
     if (n == 0) return cudaSuccess;
-    k_scatter<<<unsigned((n + 7) / 8), 256, 0, st>>>(h, h_f16, T, d, topk, E, route_tokens_per_cta(T),
-                                                     path, P, x_perm, ldx, zero_out);
+    k_scatter<<<unsigned((n + 7) / 8), 256, 0, st>>>(h, h_f16, T, d, topk, E, tt, path, P, x_perm, ldx, zero_out);
     return cudaGetLastError();
 }
 

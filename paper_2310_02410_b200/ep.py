@@ -1,0 +1,115 @@
+"""Expert parallelism for the MoQE layer: experts sharded across ranks, token
+rows dispatched to the expert owners and returned with an all-to-all.
+
+The reference is single-process (SPEC.md:330 lists distributed expert
+parallelism as a non-goal); this is the B200 scale-out of the same layer math
+(BASELINE config 4: 128 experts, top-2, experts sharded 128/G over G GPUs).
+Rank g owns experts [g*E/G, (g+1)*E/G) and holds its own tokens; the router
+weights are replicated.
+
+One forward:
+  1. route local tokens (exact fp32 router kernel; global expert ids + gates)
+  2. group (token, slot) rows by owner rank, ascending token order (stable)
+  3. exchange per-rank counts, then all_to_all the fp16 rows, the owner-local
+     expert ids and the gates (NCCL over NVLink on GPU, gloo in the CPU tests)
+  4. owners run the expert FFN on the received rows (moqe_gpu_expert_ffn: the
+     same GEMV / tcgen05 kernels as moe_forward; out = gate * FFN(row))
+  5. all_to_all the gate-weighted rows back
+  6. combine: out[t] = sum over t's slots, added onto zero (two addends,
+     commutative -> deterministic).
+Outputs equal the single-GPU moe_forward of the whole layer up to the fp32
+combine order, which is identical for top-1/top-2.
+"""
+from __future__ import annotations
+
+from typing import Callable, Optional, Tuple
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(n_experts: int, world: int, rank: int) -> Tuple[int, int]:
+    if n_experts % world:
+        raise ValueError(f"{n_experts} experts do not shard evenly over {world} ranks")
+    per = n_experts // world
+    return rank * per, (rank + 1) * per
+
+
+def dispatch_plan(expert: torch.Tensor, n_experts: int, world: int):
+    """Flatten (token, slot) assignments and order them by owner rank
+    (stable: ascending token order inside each destination).
+
+    Returns (order, tok, dest_sorted, send_counts): `order` indexes the flat
+    assignment list, tok[i] is the source token of flat assignment i."""
+    T = expert.shape[0]
+    k = 1 if expert.dim() == 1 else expert.shape[1]
+    flat = expert.reshape(-1).long()
+    tok = torch.arange(T, device=expert.device).repeat_interleave(k)
+    per = n_experts // world
+    dest = flat // per
+    dest_sorted, order = torch.sort(dest, stable=True)
+    send_counts = torch.bincount(dest, minlength=world)
+    return order, tok, dest_sorted, send_counts
+
+
+class ExpertParallelMoE:
+    """A sharded MoE FFN layer: this rank's ExpertBank + replicated router.
+
+    `route_fn(h) -> (expert [T,k] int32 global ids, gate [T,k] f32)` and
+    `expert_fn(x, local_expert, gate) -> gate-weighted rows` default to the
+    GPU kernels; tests inject CPU stand-ins to check the exchange logic."""
+
+    def __init__(self, bank, router: torch.Tensor, n_experts: int, top_k: int = 2,
+                 group: Optional[dist.ProcessGroup] = None,
+                 route_fn: Optional[Callable] = None, expert_fn: Optional[Callable] = None,
+                 path: str = "auto"):
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.E = n_experts
+        self.lo, self.hi = shard_range(n_experts, self.world, self.rank)
+        self.top_k = top_k
+        self.bank = bank
+        self.router = router
+        self.path = path
+        if route_fn is None or expert_fn is None:
+            from . import api
+        self.route_fn = route_fn or (lambda h: api.route(h, self.router, self.top_k))
+        self.expert_fn = expert_fn or (lambda x, e, g: api.expert_ffn(x, self.bank, e, g, path=self.path))
+
+    def _a2a(self, out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits) -> None:
+        dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
+
+    def forward(self, h: torch.Tensor) -> torch.Tensor:
+        T, d = h.shape
+        ex, gate = self.route_fn(h)
+        ex = ex.reshape(T, -1)
+        gate = gate.reshape(T, -1)
+        order, tok, dest_sorted, send_counts = dispatch_plan(ex, self.E, self.world)
+        src_tok = tok[order]
+        send_rows = h.index_select(0, src_tok).contiguous()
+        send_exp = (ex.reshape(-1)[order] - dest_sorted * (self.E // self.world)).to(torch.int32).contiguous()
+        send_gate = gate.reshape(-1)[order].to(torch.float32).contiguous()
+
+        # 1) counts
+        recv_counts = torch.empty_like(send_counts)
+        self._a2a(recv_counts, send_counts, None, None)
+        s_split = send_counts.tolist()
+        r_split = recv_counts.tolist()
+        R = int(sum(r_split))
+        # 2) rows + metadata to the owners
+        recv_rows = torch.empty((R, d), dtype=h.dtype, device=h.device)
+        recv_exp = torch.empty((R,), dtype=torch.int32, device=h.device)
+        recv_gate = torch.empty((R,), dtype=torch.float32, device=h.device)
+        self._a2a(recv_rows, send_rows, r_split, s_split)
+        self._a2a(recv_exp, send_exp, r_split, s_split)
+        self._a2a(recv_gate, send_gate, r_split, s_split)
+        # 3) owner-side expert FFN (gate-weighted rows, fp32)
+        y = self.expert_fn(recv_rows, recv_exp, recv_gate).to(torch.float32).contiguous()
+        # 4) back to the sources, in the order they were sent
+        back = torch.empty((send_rows.shape[0], d), dtype=torch.float32, device=h.device)
+        self._a2a(back, y, s_split, r_split)
+        # 5) combine the top-k slots (<= 2 addends onto zero: order-independent)
+        out = torch.zeros((T, d), dtype=torch.float32, device=h.device)
+        out.index_add_(0, src_tok, back)
+        return out
