@@ -277,6 +277,12 @@ def run_point(m, torch, E, d, f, bits, T, top_k, steps, warmup, dev, hbm_peak, t
                 "frac": round(achieved / tc_peak, 4), "traffic": None, "kernel": "k_ffn_gemm " + KINDS[dom],
                 "flops_per_launch": int(fl), "avg_launch_us": round(avg_launch_ms * 1e3, 3),
                 "fc1_plus_fc2_TFLOPs": round(2 * fl / (both_ms * 1e-3) / 1e12, 1)}
+    try:  # ncu-measured DRAM bytes per launch of this kernel/config (profiles/round1/traffic.json)
+        with open(os.path.join(ROOT, "profiles", "round1", "traffic.json")) as fh:
+            tr = json.load(fh).get(f"{roof['kernel']}/int{bits}/T{T}")
+        roof["traffic"] = tr
+    except Exception:
+        pass
     touched = float(np.mean([L.touched for L in layers]))
     step_b = np.mean([kernel_bytes(L, d, f, bits, T, top_k) for L in layers]) + d * E * 4
     res = {
