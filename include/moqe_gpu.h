@@ -162,6 +162,16 @@ moqe_status moqe_gpu_expert_ffn(moqe_bank_t bank, const void* x, moqe_dtype x_dt
 moqe_status moqe_gpu_bank_profile(moqe_bank_t bank, int enable);
 moqe_status moqe_gpu_bank_profile_read(moqe_bank_t bank, double* ms, int64_t* launches, int keep);
 
+/* Device event trace of the decode GEMV (diagnostics; off by default).
+ * trace(bank, 1) allocates a [num_sms][512][2] u64 buffer of (globaltimer ns,
+ * event word) pairs, filled by later forwards (word: role<<60 | event<<56 |
+ * phase<<48 | expert<<32 | m-tile<<16 | k-split; roles 0 producer, 1 converter,
+ * 2 consumer, 3 kernel start). trace_read synchronises, copies up to `cap`
+ * words (out may be NULL to query the size), clears the buffer and returns the
+ * word count, or -1 when tracing is off. */
+moqe_status moqe_gpu_bank_trace(moqe_bank_t bank, int enable);
+int64_t moqe_gpu_bank_trace_read(moqe_bank_t bank, uint64_t* out, int64_t cap);
+
 /* Host-buffer convenience (the reference's by-value API): copies h (host,
  * pinned or pageable) in, runs moe_forward, copies out (host) back. Blocking. */
 moqe_status moqe_gpu_moe_forward_host(moqe_bank_t bank, const void* h_host, moqe_dtype h_dtype,

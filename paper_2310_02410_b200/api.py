@@ -214,6 +214,24 @@ class ExpertBank:
     def weight_bytes(self) -> int:
         return int(_lib.load().moqe_gpu_bank_weight_bytes(self._h))
 
+    def trace(self, enable: bool = True) -> None:
+        """Enable / disable the decode kernel's device event trace (diagnostics)."""
+        check(_lib.load().moqe_gpu_bank_trace(self._h, 1 if enable else 0))
+
+    def trace_read(self):
+        """Trace since the last read: (gemv [num_sms, 512, 2] of (time ns, event word),
+        router [64, 16] of per-CTA stamps: 0 start, 1 row loaded, 2..9 chunk c done,
+        10 chain done, 11 ticket, 12 plan done)."""
+        import numpy as np
+        lib = _lib.load()
+        n = int(lib.moqe_gpu_bank_trace_read(self._h, None, 0))
+        if n < 0:
+            raise _lib.InvalidArgument("trace: tracing is not enabled")
+        buf = np.zeros(n, np.uint64)
+        lib.moqe_gpu_bank_trace_read(self._h, buf.ctypes.data, n)
+        nr = 64 * 16
+        return buf[: n - nr].reshape(-1, 512, 2), buf[n - nr:].reshape(64, 16)
+
     def close(self) -> None:
         if getattr(self, "_h", None) and self._h.value:
             _lib.load().moqe_gpu_bank_destroy(self._h)

@@ -8,6 +8,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <utility>
@@ -48,6 +49,10 @@ struct Workspace {
     int64_t part_rows = 0;
     float* out_acc = nullptr;
     unsigned* split_cnt = nullptr;
+    uint8_t* xb = nullptr;         // GEMV activation digit fragments
+    unsigned* xb_flag = nullptr;
+    int64_t xb_slot_bytes = 0;
+    float* l1part = nullptr;
 };
 
 struct moqe_bank {
@@ -62,6 +67,8 @@ struct moqe_bank {
     float* b1 = nullptr;
     float* b2 = nullptr;
     float* wg = nullptr;
+    float* smax1 = nullptr;  // [E][fc2 k-chunks] fc2 fixed-point bound constants (decode GEMV)
+    float* bmax1 = nullptr;
     int num_sms = 148;
     int device = 0;
     cudaStream_t host_stream = nullptr;
@@ -74,10 +81,15 @@ struct moqe_bank {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
     std::vector<std::pair<int, int>> ev_used;  // (kind, pool index)
     double prof_ms[MOQE_PROFILE_KINDS] = {0};
+    unsigned long long* trace = nullptr;  // GEMV event trace (moqe_gpu_bank_trace)
     int64_t prof_n[MOQE_PROFILE_KINDS] = {0};
 };
 
 namespace {
+int gemv_dbg() {
+    static const int v = [] { const char* s = getenv("MOQE_GEMV_DBG"); return s ? atoi(s) : 0; }();
+    return v;
+}
 struct KernelTimer {
     moqe_bank* b;
     int kind;
@@ -133,6 +145,9 @@ moqe_status ensure_workspace(moqe_bank* b, int64_t T, int topk) {
     add(4, capR); add(4, capR); add(4, capR); add(4, E); add(4, E); add(4, E + 1); add(4, 8);
     add(4, 8); add(4, E); add(4, 2 * E * maxmt);
     add(2, capR * b->Np1); add(2, capR * b->Kp1); add(4, part); add(4, capT * b->d); add(4, capT * E);
+    const int64_t xb_slots = gemv_xb_passes(capR, E) * gemv_ksplit(b->Kp2);
+    const int64_t xb_bytes = gemv_xb_slot_bytes(b->bits);
+    add(xb_bytes, xb_slots); add(4, xb_slots * gemv_stages_per_chunk()); add(4, capR * gemv_ksplit(b->Kp1));
     MOQE_CUDA(cudaMalloc(&w.block, bytes));
     MOQE_CUDA(cudaMemset(w.block, 0, bytes));
     char* p = static_cast<char*>(w.block);
@@ -160,6 +175,10 @@ moqe_status ensure_workspace(moqe_bank* b, int64_t T, int topk) {
     P.partial = w.partial;
     w.out_acc = carve<float>(p, capT * b->d);
     P.logits = carve<float>(p, capT * E);
+    w.xb = carve<uint8_t>(p, xb_bytes * xb_slots);
+    w.xb_flag = carve<unsigned>(p, xb_slots * gemv_stages_per_chunk());
+    w.xb_slot_bytes = xb_bytes;
+    w.l1part = carve<float>(p, capR * gemv_ksplit(b->Kp1));
     w.part_rows = part_rows;
     w.cap_rows = capR;
     w.cap_tokens = capT;
@@ -175,9 +194,12 @@ void free_bank(moqe_bank* b) {
     cudaFree(b->b1);
     cudaFree(b->b2);
     cudaFree(b->wg);
+    cudaFree(b->smax1);
+    cudaFree(b->bmax1);
     cudaFree(b->ws.block);
     cudaFree(b->h_dev);
     cudaFree(b->o_dev);
+    cudaFree(b->trace);
     if (b->host_stream) cudaStreamDestroy(b->host_stream);
     delete b;
 }
@@ -264,6 +286,14 @@ moqe_status moqe_gpu_bank_create(int n_experts, int64_t d_model, int64_t d_ffn, 
         if ((st = upload_padded(&b->s2, scales2, n_experts, d_model, b->Np2, dev)) != MOQE_OK) break;
         if (b1 && (st = upload_padded(&b->b1, b1, n_experts, d_ffn, b->Np1, dev)) != MOQE_OK) break;
         if (b2 && (st = upload_padded(&b->b2, b2, n_experts, d_model, b->Np2, dev)) != MOQE_OK) break;
+        {
+            const int64_t nk = int64_t(n_experts) * gemv_ksplit(b->Kp2);
+            if ((ce = cudaMalloc(&b->smax1, sizeof(float) * nk)) != cudaSuccess) break;
+            if ((ce = cudaMalloc(&b->bmax1, sizeof(float) * nk)) != cudaSuccess) break;
+            if ((ce = launch_chunk_max(b->s1, b->b1, n_experts, b->Np1, b->Kp2, b->smax1, b->bmax1, nullptr)) !=
+                cudaSuccess)
+                break;
+        }
         if ((ce = cudaDeviceSynchronize()) != cudaSuccess) break;
     } while (false);
     if (stage) cudaFree(stage);
@@ -343,7 +373,8 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
     if (top_k == 2) acc = out_dtype == MOQE_F32 ? static_cast<float*>(out) : w.out_acc;
 
     RouteArgs ra{h, h_dtype == MOQE_F16, t, int(b->d), wg, b->E, top_k, eff_path, inline_scatter ? 1 : 0,
-                 gemm_block_n(), inline_scatter ? acc : nullptr};
+                 gemm_block_n(), inline_scatter ? acc : nullptr,
+                 b->trace ? b->trace + int64_t(b->num_sms) * kTraceCap * 2 : nullptr};
     cudaError_t ce;
     {
         KernelTimer kt(b, 0, st);
@@ -360,7 +391,8 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
     if (need_gemv) {
         GemvArgs g{h, h_dtype == MOQE_F16, t, int(b->d), int(b->f), top_k, b->E, b->w1, b->w2,
                    b->w1_stride, b->w2_stride, b->s1, b->s2, b->b1, b->b2, b->Kp1, b->Np1, b->Kp2, b->Np2,
-                   w.mid, out, out_dtype == MOQE_F16, acc, w.partial, w.part_rows, w.split_cnt};
+                   w.mid, out, out_dtype == MOQE_F16, acc, w.partial, w.part_rows, w.split_cnt,
+                   w.xb, w.xb_flag, w.xb_slot_bytes, b->smax1, b->bmax1, w.l1part, b->trace, gemv_dbg()};
         KernelTimer kt(b, 2, st);
         ce = launch_gemv(b->bits, R > 16, g, P, st, b->num_sms);
         if (ce != cudaSuccess) return cuda_fail(ce, "k_ffn_gemv");
@@ -402,6 +434,30 @@ moqe_status moqe_gpu_expert_ffn(moqe_bank_t b, const void* x, moqe_dtype x_dtype
     if (!expert || !gate) return fail(MOQE_INVALID_ARGUMENT, "expert_ffn: null expert ids / gates");
     return forward_impl(b, x, x_dtype, rows, nullptr, 1, out, out_dtype, nullptr, nullptr, path, stream, expert,
                         gate);
+}
+
+moqe_status moqe_gpu_bank_trace(moqe_bank_t b, int enable) {
+    if (!b) return fail(MOQE_INVALID_ARGUMENT, "trace: null bank");
+    MOQE_CUDA(cudaDeviceSynchronize());
+    cudaFree(b->trace);
+    b->trace = nullptr;
+    if (enable) {
+        const size_t bytes = (size_t(b->num_sms) * kTraceCap * 2 + kTraceRouteCtas * 16) * sizeof(unsigned long long);
+        MOQE_CUDA(cudaMalloc(&b->trace, bytes));
+        MOQE_CUDA(cudaMemset(b->trace, 0, bytes));
+    }
+    return MOQE_OK;
+}
+
+int64_t moqe_gpu_bank_trace_read(moqe_bank_t b, uint64_t* out, int64_t cap) {
+    if (!b || !b->trace) return -1;
+    const int64_t n = int64_t(b->num_sms) * kTraceCap * 2 + kTraceRouteCtas * 16;
+    if (out) {
+        if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+        if (cudaMemcpy(out, b->trace, sizeof(uint64_t) * std::min(n, cap), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+        cudaMemset(b->trace, 0, sizeof(uint64_t) * n);
+    }
+    return n;
 }
 
 moqe_status moqe_gpu_bank_profile(moqe_bank_t b, int enable) {

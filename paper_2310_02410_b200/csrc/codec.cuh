@@ -14,10 +14,12 @@
 //   8     64         bytes [16t, 16t+16): natural order (the reference packing)
 //   4     32         two u32 at 8t: per word, low half nibbles c0 c2 c4 c6,
 //                    high half c1 c3 c5 c7
-//   3     24         u32 A at 4t: low half c0 c2 c4 c6 c8 @3-bit slots, bit15 =
-//                    c14>>2; high half c1 c3 c5 c7 c9, bit31 = c15>>2.
-//                    u16 B at 16+2t: lo byte c10 | c12<<3 | (c14&3)<<6,
-//                    hi byte c11 | c13<<3 | (c15&3)<<6
+//   3     24         u32 A at 4t: byte0 = c0 | c2<<3 | (c8&3)<<6, byte1 = c4 | c6<<3
+//                    | (c10&3)<<6, byte2 = c1 | c3<<3 | (c9&3)<<6, byte3 = c5 | c7<<3 |
+//                    (c11&3)<<6; u16 B at 16+2t: lo byte c12 | c14<<3 | (c8>>2)<<6 |
+//                    (c10>>2)<<7, hi byte c13 | c15<<3 | (c9>>2)<<6 | (c11>>2)<<7
+//                    (every field byte-aligned at the same offset in each byte, so
+//                    one LOP3 yields four u8 codes for the decode IMMA path too)
 //   2     16         u32 at 4t: low half c0 c2 .. c14 @2-bit slots, high half
 //                    c1 c3 .. c15
 // (u = code + 2^(bits-1), offset binary like bitpack.cpp:18-39.)
@@ -49,12 +51,10 @@ __device__ __forceinline__ void encode_row(const int (&q)[64], uint8_t* row) {
             for (int p = 0; p < 8; ++p) W |= (u[2 * p] << (2 * p)) | (u[2 * p + 1] << (16 + 2 * p));
             for (int b = 0; b < 4; ++b) row[4 * t + b] = uint8_t(W >> (8 * b));
         } else {  // 3
-            uint32_t A = 0;
-            for (int p = 0; p < 5; ++p) A |= (u[2 * p] << (3 * p)) | (u[2 * p + 1] << (16 + 3 * p));
-            A |= ((u[14] >> 2) & 1u) << 15;
-            A |= ((u[15] >> 2) & 1u) << 31;
-            const uint32_t lo = u[10] | (u[12] << 3) | ((u[14] & 3u) << 6);
-            const uint32_t hi = u[11] | (u[13] << 3) | ((u[15] & 3u) << 6);
+            const uint32_t A = (u[0] | u[2] << 3 | (u[8] & 3u) << 6) | (u[4] | u[6] << 3 | (u[10] & 3u) << 6) << 8 |
+                               (u[1] | u[3] << 3 | (u[9] & 3u) << 6) << 16 | (u[5] | u[7] << 3 | (u[11] & 3u) << 6) << 24;
+            const uint32_t lo = u[12] | u[14] << 3 | (u[8] >> 2) << 6 | (u[10] >> 2) << 7;
+            const uint32_t hi = u[13] | u[15] << 3 | (u[9] >> 2) << 6 | (u[11] >> 2) << 7;
             for (int b = 0; b < 4; ++b) row[4 * t + b] = uint8_t(A >> (8 * b));
             row[16 + 2 * t] = uint8_t(lo);
             row[16 + 2 * t + 1] = uint8_t(hi);
@@ -110,17 +110,16 @@ __device__ __forceinline__ void unpack_chunk(const uint8_t* row, int t, uint32_t
     } else if constexpr (BITS == 3) {
         const uint32_t A = *reinterpret_cast<const uint32_t*>(row + 4 * t);
         const uint32_t B = *reinterpret_cast<const uint16_t*>(row + 16 + 2 * t);
-        const uint32_t A9 = A >> 9;
+        const uint32_t A8 = A >> 8;
+        const uint32_t Bx = prmt(B, 0u, 0x4140u);  // (B.lo, 0, B.hi, 0)
         o[0] = h2_fma(lop_magic<0x00070007u>(A, mg), 1.0f, -1028.0f);
         o[1] = h2_fma(lop_magic<0x00380038u>(A, mg), 1.0f / 8, -132.0f);
-        o[2] = h2_fma(lop_magic<0x01C001C0u>(A, mg), 1.0f / 64, -20.0f);
-        o[3] = h2_fma(lop_magic<0x00070007u>(A9, mg), 1.0f, -1028.0f);
-        o[4] = h2_fma(lop_magic<0x00380038u>(A9, mg), 1.0f / 8, -132.0f);
-        const uint32_t Bx = prmt(B, 0u, 0x4140u);
-        o[5] = h2_fma(lop_magic<0x00070007u>(Bx, mg), 1.0f, -1028.0f);
-        o[6] = h2_fma(lop_magic<0x00380038u>(Bx, mg), 1.0f / 8, -132.0f);
-        const uint32_t top = (Bx & 0x00C000C0u) | ((A >> 7) & 0x01000100u);
-        o[7] = h2_fma(top | mg, 1.0f / 64, -20.0f);
+        o[2] = h2_fma(lop_magic<0x00070007u>(A8, mg), 1.0f, -1028.0f);
+        o[3] = h2_fma(lop_magic<0x00380038u>(A8, mg), 1.0f / 8, -132.0f);
+        o[4] = h2_fma(lop_magic<0x00C000C0u>(A, mg) | ((Bx << 2) & 0x01000100u), 1.0f / 64, -20.0f);
+        o[5] = h2_fma(lop_magic<0x00C000C0u>(A8, mg) | ((Bx << 1) & 0x01000100u), 1.0f / 64, -20.0f);
+        o[6] = h2_fma(lop_magic<0x00070007u>(Bx, mg), 1.0f, -1028.0f);
+        o[7] = h2_fma(lop_magic<0x00380038u>(Bx, mg), 1.0f / 8, -132.0f);
     } else {  // 8
         const uint4 w = *reinterpret_cast<const uint4*>(row + 16 * t);
         const uint32_t ws[4] = {w.x, w.y, w.z, w.w};

@@ -4,10 +4,30 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "common.cuh"
 #include "plan.cuh"
 
 namespace moqe_gpu {
+
+// Launch with programmatic stream serialization: the grid may start while the
+// preceding kernel in the stream drains; the kernel calls pdl_wait() before it
+// reads that kernel's results.
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 struct RouteArgs {
     const void* h;
@@ -21,7 +41,9 @@ struct RouteArgs {
     int inline_scatter;  // plan CTA also scatters metadata (small T, GEMV only)
     int gemm_bn;         // GEMM n-tile rows, for tile counting
     float* zero_out;     // top-2 fp32 accumulation rows to zero (inline scatter), or null
+    unsigned long long* trace;  // router phase stamps [kTraceRouteCtas][16] or null (diagnostics)
 };
+constexpr int kTraceRouteCtas = 64;
 cudaError_t launch_route(const RouteArgs& a, const Plan& P, cudaStream_t st);
 int route_tokens_per_cta(int64_t T);
 // rows already routed: plan with kRouteSelWarps rows per CTA (scatter must use that tile)
@@ -53,10 +75,26 @@ struct GemvArgs {
     float* partial;                // split-K partials: phase1 [S1][R][Np1], phase2 [S2][R][Np2]
     int64_t part_rows;             // R capacity
     unsigned* split_cnt;           // [2][E][max(Nmt)]
+    uint8_t* xb;                   // fc2 activation digit fragments, one slot per (row pass, fc2 k-chunk)
+    unsigned* xb_flag;             // [slots][8 stages] forward epoch when the stage is written
+    int64_t xb_slot_bytes;
+    const float* smax1;            // [E][fc2 k-chunks] max fc1 scale over the chunk's channels
+    const float* bmax1;            // [E][fc2 k-chunks] max |fc1 bias| over the chunk's channels
+    float* l1part;                 // [rows][fc1 k-splits] |x|_1 per row and split (d > 1024 only)
+    unsigned long long* trace;     // [grid][kTraceCap][2] (time ns, event) or null
+    int dbg;                       // diagnostics only (env MOQE_GEMV_DBG): 1 skip epilogue, 2 skip B waits
 };
+constexpr int kTraceCap = 512;
 cudaError_t launch_gemv(int bits, bool two_m16, const GemvArgs& g, const Plan& P, cudaStream_t st,
                         int num_sms);
 int64_t gemv_partial_floats(int64_t rows, int Kp1, int Np1, int Kp2, int Np2);
+// fragment slots: bytes per slot and slot counts for `rows` GEMV rows over `E` experts
+int64_t gemv_xb_slot_bytes(int bits);
+int64_t gemv_xb_passes(int64_t rows, int E);
+int gemv_ksplit(int Kp);
+int gemv_stages_per_chunk();
+cudaError_t launch_chunk_max(const float* s1, const float* b1, int E, int Np1, int Kp2, float* smax, float* bmax,
+                             cudaStream_t st);
 
 struct GemmArgs {
     const __half* x_perm;  // [R][Kp1] expert-grouped activations

@@ -4,7 +4,7 @@
 
 namespace moqe_gpu {
 
-constexpr int kGemvMaxRows = 16;   // experts with <= this many routed rows take the GEMV path
+constexpr int kGemvMaxRows = 12;   // experts with <= this many routed rows take the GEMV path (2 passes)
 
 // All pointers are device memory owned by the bank's workspace.
 struct Plan {
@@ -20,7 +20,7 @@ struct Plan {
     int32_t* gemv_list;   // [E]    experts for the GEMV path (expert order)
     int32_t* gemm_list;   // [E]    experts for the tcgen05 path
     int32_t* gemm_tile_start;  // [E+1] prefix of GEMM tiles per listed expert (per m-tile row)
-    int32_t* meta;        // [8]    0: n_gemv, 1: n_gemm, 2: gemm n-tiles total, 3: max n_e
+    int32_t* meta;        // [8]    0: n_gemv, 1: n_gemm, 2: gemm n-tiles total, 3: max n_e, 5: forward epoch
     unsigned* tickets;    // [8]    0: route last-CTA, 1: gemv items, 2: gemm fc1, 3: gemm fc2
     unsigned* done;       // [E]    GEMV fc1 m-tiles finished per expert
     unsigned* split_done; // [E * max_mt] GEMV fc2 split-K arrivals

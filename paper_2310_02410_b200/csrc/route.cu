@@ -19,6 +19,7 @@
 #include <cuda_fp16.h>
 
 #include "kernels.cuh"
+#include "ptx.cuh"
 
 namespace moqe_gpu {
 
@@ -49,9 +50,27 @@ __device__ __forceinline__ void warp_argmax(const float (&l)[EPL], int E, int sk
 }
 
 // Last-CTA planning: per-CTA bases, counts, offsets, expert lists, resets.
-__device__ void plan_tail(const RouteArgs& a, Plan P, int n_ctas, int tt) {
+// `scr` (optional, >= n_ctas*E ints of smem) stages the per-CTA histograms so
+// the cross-CTA scan costs one L2 round trip instead of one per expert.
+__device__ void plan_tail(const RouteArgs& a, Plan P, int n_ctas, int tt, int* scr, int scr_ints) {
     const int E = a.E, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nw = blockDim.x >> 5;
+    const bool staged = scr != nullptr && int64_t(n_ctas) * E <= scr_ints;
+    if (staged) {
+        for (int i = threadIdx.x; i < n_ctas * E; i += blockDim.x) scr[i] = __ldcg(P.cta_counts + i);
+        __syncthreads();
+        for (int e = threadIdx.x; e < E; e += blockDim.x) {
+            int run = 0;
+            for (int c = 0; c < n_ctas; ++c) {
+                const int v = scr[c * E + e];
+                scr[c * E + e] = run;
+                run += v;
+            }
+            P.counts[e] = run;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < n_ctas * E; i += blockDim.x) P.cta_counts[i] = scr[i];
+    } else {
     // 1. exclusive scan of per-CTA counts over CTAs, per expert (warp per expert)
     for (int e = warp; e < E; e += nw) {
         int running = 0;
@@ -76,6 +95,7 @@ __device__ void plan_tail(const RouteArgs& a, Plan P, int n_ctas, int tt) {
             }
         }
         if (lane == 0) P.counts[e] = running;
+    }
     }
     __syncthreads();
     // 2. offsets + expert lists (warp 0, expert order)
@@ -124,6 +144,7 @@ __device__ void plan_tail(const RouteArgs& a, Plan P, int n_ctas, int tt) {
             P.meta[1] = ngemm;
             P.meta[2] = tiles;
             P.meta[3] = mx;
+            P.meta[5] += 1;  // forward epoch (GEMV fragment-ready flags compare against it)
             P.tickets[1] = 0;
             P.tickets[2] = 0;
             P.tickets[3] = 0;
@@ -138,7 +159,8 @@ __device__ void plan_tail(const RouteArgs& a, Plan P, int n_ctas, int tt) {
         for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
             const int64_t t = i / a.topk;
             const int e = __ldcg(P.expert + i);
-            const int pos = P.offsets[e] + P.cta_counts[(t / tt) * E + e] + __ldcg(P.lrank + i);
+            const int base = staged ? scr[(t / tt) * E + e] : P.cta_counts[(t / tt) * E + e];
+            const int pos = P.offsets[e] + base + __ldcg(P.lrank + i);
             P.perm_token[pos] = int32_t(t);
             P.perm_gate[pos] = __ldcg(P.gate + i);
             P.inv_pos[i] = pos;
@@ -192,7 +214,9 @@ __device__ __forceinline__ void finish_token(const RouteArgs& a, Plan& P, const 
     }
 }
 
-__device__ __forceinline__ void ranks_hist_plan(const RouteArgs& a, Plan& P, int* s_exp, int* s_hist, int tt) {
+__device__ __forceinline__ void ranks_hist_plan(const RouteArgs& a, Plan& P, int* s_exp, int* s_hist, int tt,
+                                                int* scr = nullptr, int scr_ints = 0,
+                                                unsigned long long* tr = nullptr) {
     const int E = a.E, k = a.topk;
     __syncthreads();
     for (int i = threadIdx.x; i < tt * k; i += blockDim.x) {
@@ -213,96 +237,176 @@ __device__ __forceinline__ void ranks_hist_plan(const RouteArgs& a, Plan& P, int
         if (s_last) __threadfence();  // acquire everyone else's
     }
     __syncthreads();
+    if (tr && threadIdx.x == 0) tr[11] = gtime_ns();
     if (!s_last) return;
-    plan_tail(a, P, gridDim.x, tt);
+    plan_tail(a, P, gridDim.x, tt, scr, scr_ints);
+    __syncthreads();
+    if (tr && threadIdx.x == 0) tr[12] = gtime_ns();
 }
 
-constexpr int kRouteSmallWarps = 4;   // one token per warp; a warp per SM sub-partition
+constexpr int kRouteSmallWarps = 4;   // token warps per CTA (one token each, one per SM sub-partition)
+constexpr int kRouteSlots = 8;        // Wg chunk ring (8 x 16 KB)
+constexpr int kRouteChunkFloats = 4096;
 
-// Wg rows staged per chunk for a given expert count.
-__host__ __device__ constexpr int route_chunk_rows(int E) { return E <= 128 ? 4096 / (E < 32 ? 32 : E) : 32; }
+// Wg rows per 16 KB chunk (a multiple of 4 so chunk byte offsets stay 16-byte aligned).
+__host__ __device__ constexpr int route_chunk_rows(int E) {
+    return E <= 1024 ? ((kRouteChunkFloats / E) & ~3) > 0 ? ((kRouteChunkFloats / E) & ~3) : 4 : 4;
+}
+__host__ __device__ inline int route_dpad(int d, int E) {
+    const int r = route_chunk_rows(E);
+    return (d + r - 1) / r * r;
+}
+size_t route_small_smem(int d, int E) {
+    return size_t(kRouteSlots) * route_chunk_rows(E) * E * sizeof(float) +
+           size_t(kRouteSmallWarps) * route_dpad(d, E) * sizeof(float) + 2 * kRouteSlots * sizeof(uint64_t);
+}
 
 // Small T (decode): one warp per token, lane j <-> experts j, j+32, ...
-// The token rows sit in smem (loaded once); Wg streams through a
-// double-buffered smem chunk (register prefetch of the next chunk overlaps the
-// current chunk's sequential fp32 chain). EFIX > 0 compiles the expert count
-// in (E == EFIX): the chunk copy is unpredicated float4 and the 32-row inner
-// loop unrolls to immediate smem offsets; EFIX == 0 is the generic path.
+// Warp 4 streams Wg through an 8-slot smem ring with TMA bulk copies
+// (mbarrier full/empty pairs, no CTA-wide barriers in the k loop); the token
+// warps hold their row in smem as fp32 and run the reference's exact
+// sequential fp32 chain (FMUL then FADD in ascending k, zero activations
+// skipped), reading 4 activations per LDS.128 broadcast and one Wg word per
+// k. EFIX > 0 compiles the expert count in (E == EFIX).
 template <int EPL, int EFIX>
-__global__ void __launch_bounds__(kRouteSmallWarps * 32) k_route_small(RouteArgs a, Plan P) {
+__global__ void __launch_bounds__((kRouteSmallWarps + 1) * 32, 1) k_route_small(RouteArgs a, Plan P) {
     constexpr int TT = kRouteSmallWarps;
-    constexpr int NT = kRouteSmallWarps * 32;
-    extern __shared__ __align__(16) float s_dyn[];
+    extern __shared__ __align__(128) float s_dyn[];
     __shared__ int s_exp[TT * 2];
     __shared__ int s_hist[256];
+    pdl_trigger();  // the expert-FFN grid may launch and run its prologue now
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned long long* tr = (a.trace && blockIdx.x < kTraceRouteCtas) ? a.trace + blockIdx.x * 16 : nullptr;
+    if (tr && threadIdx.x == 0) tr[0] = gtime_ns();
     const int E = EFIX ? EFIX : a.E, d = a.d;
-    const int rows = EFIX ? route_chunk_rows(EFIX) : route_chunk_rows(a.E);
+    const int rows = route_chunk_rows(E);
     const int chunk = rows * E;
-    const int nchunks = (d + rows - 1) / rows;
-    const int dpad = nchunks * rows;
-    float* s_w = s_dyn;                     // [2][chunk]
-    float* s_hrow = s_dyn + 2 * chunk;      // [TT][dpad] token rows, zero padded
-    const int64_t t = int64_t(blockIdx.x) * TT + warp;
-    const bool live = t < a.T;
+    const int nch = (d + rows - 1) / rows;
+    const int dpad = nch * rows;
+    float* ring = s_dyn;                                   // [kRouteSlots][chunk]
+    float* s_hrow = s_dyn + kRouteSlots * chunk;           // [TT][dpad]
+    uint64_t* full = reinterpret_cast<uint64_t*>(s_hrow + TT * dpad);
+    uint64_t* empty = full + kRouteSlots;
+    const int64_t t = int64_t(blockIdx.x) * TT + (warp < TT ? warp : 0);
+    const bool live = warp < TT && t < a.T;
     for (int e = threadIdx.x; e < E; e += blockDim.x) s_hist[e] = 0;
-    for (int p = lane; p < dpad; p += 32)
-        s_hrow[warp * dpad + p] = (live && p < d) ? load_act(a.h, a.h_f16, t * d + p) : 0.0f;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kRouteSlots; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], TT); }
+        fence_barrier_init();
+    }
+    __syncthreads();
 
-    float acc[EPL];
-#pragma unroll
-    for (int e = 0; e < EPL; ++e) acc[e] = 0.0f;
-    // EFIX: chunk == 4096 floats (E <= 128) or 32*E; each thread moves chunk/NT floats as float4
-    constexpr int V4 = EFIX ? (route_chunk_rows(EFIX) * EFIX) / (4 * NT) : 1;
-    float4 pre[V4];
-    const int64_t lim = int64_t(d) * E;
-    auto load_chunk = [&](int c) {
-        const int64_t base = int64_t(c) * chunk;
-        if constexpr (EFIX != 0) {
-#pragma unroll
-            for (int i = 0; i < V4; ++i) {
-                const int64_t idx = base + 4 * (int64_t(i) * NT + threadIdx.x);
-                pre[i] = idx + 3 < lim ? __ldg(reinterpret_cast<const float4*>(a.wg + idx)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (warp == TT) {
+        // ===== producer: Wg chunks -> ring (bulk copies need 16-byte aligned sources)
+        if (lane == 0) {
+            const bool bulk = (reinterpret_cast<uintptr_t>(a.wg) & 15) == 0;
+            for (int c = 0; c < nch; ++c) {
+                const int s = c % kRouteSlots;
+                if (c >= kRouteSlots) mbar_wait(&empty[s], ((c / kRouteSlots) - 1) & 1);
+                const int nr = min(rows, d - c * rows);
+                const float* src = a.wg + int64_t(c) * chunk;
+                if (bulk && ((nr * E) & 3) == 0) {
+                    mbar_arrive_expect_tx(&full[s], uint32_t(nr * E * 4));
+                    bulk_g2s(ring + s * chunk, src, uint32_t(nr * E * 4), &full[s]);
+                } else {
+                    for (int i = 0; i < nr * E; ++i) ring[s * chunk + i] = __ldg(src + i);
+                    mbar_arrive(&full[s]);
+                }
             }
         }
-    };
-    auto store_chunk = [&](int c, float* buf) {
-        if constexpr (EFIX != 0) {
-#pragma unroll
-            for (int i = 0; i < V4; ++i) reinterpret_cast<float4*>(buf)[i * NT + threadIdx.x] = pre[i];
+    } else {
+        // ===== token warps: row -> smem (fp32, zero padded), then the exact chain
+        float* hr = s_hrow + warp * dpad;
+        if (live && a.h_f16 && (d % 8) == 0 && (reinterpret_cast<uintptr_t>(a.h) & 15) == 0) {
+            const uint4* src = reinterpret_cast<const uint4*>(static_cast<const __half*>(a.h) + t * d);
+            for (int j = lane; j < d / 8; j += 32) {
+                const uint4 v = __ldg(src + j);
+                const __half2* h2 = reinterpret_cast<const __half2*>(&v);
+                float4 lo, hi;
+                float2 f;
+                f = __half22float2(h2[0]); lo.x = f.x; lo.y = f.y;
+                f = __half22float2(h2[1]); lo.z = f.x; lo.w = f.y;
+                f = __half22float2(h2[2]); hi.x = f.x; hi.y = f.y;
+                f = __half22float2(h2[3]); hi.z = f.x; hi.w = f.y;
+                reinterpret_cast<float4*>(hr)[2 * j] = lo;
+                reinterpret_cast<float4*>(hr)[2 * j + 1] = hi;
+            }
+            for (int p = d + lane; p < dpad; p += 32) hr[p] = 0.0f;
         } else {
-            const int64_t base = int64_t(c) * chunk;
-            for (int i = threadIdx.x; i < chunk; i += NT) buf[i] = base + i < lim ? __ldg(a.wg + base + i) : 0.0f;
+            for (int p = lane; p < dpad; p += 32) hr[p] = (live && p < d) ? load_act(a.h, a.h_f16, t * d + p) : 0.0f;
         }
-    };
-    load_chunk(0);
-    for (int c = 0; c < nchunks; ++c) {
-        float* buf = s_w + (c & 1) * chunk;
-        store_chunk(c, buf);
-        __syncthreads();
-        if (c + 1 < nchunks) load_chunk(c + 1);
-        if (live) {
-            const float* hr = s_hrow + warp * dpad + c * rows;
-            for (int q0 = 0; q0 < rows; q0 += 32) {
-                const float* wb = buf + q0 * E + lane;
+        __syncwarp();
+        if (tr && threadIdx.x == 0) tr[1] = gtime_ns();
+        float acc[EPL];
 #pragma unroll
-                for (int q = 0; q < 32; ++q) {
-                    const float av = hr[q0 + q];  // smem broadcast; 0 beyond d
+        for (int e = 0; e < EPL; ++e) acc[e] = 0.0f;
+        for (int c = 0; c < nch; ++c) {
+            const int s = c % kRouteSlots;
+            mbar_wait(&full[s], (c / kRouteSlots) & 1);
+            if (live) {
+                const float* wb = ring + s * chunk + lane;
+                const float* hc = hr + c * rows;
+                const int nr = min(rows, d - c * rows);  // rows beyond d are never read
+                // software pipeline: the next 16 rows' operands load while the
+                // current 16-step dependent FADD chain runs
+                constexpr int U = EPL >= 4 ? 4 : 16 / EPL;
+                int q = 0;
+                if (nr >= U) {
+                    float a_c[U], w_c[U][EPL];
+                    auto fetch = [&](int q0, float (&av)[U], float (&wv)[U][EPL]) {
+#pragma unroll
+                        for (int u = 0; u < U; u += 4) {
+                            const float4 t4 = *reinterpret_cast<const float4*>(hc + q0 + u);
+                            av[u] = t4.x; av[u + 1] = t4.y; av[u + 2] = t4.z; av[u + 3] = t4.w;
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; ++u)
+#pragma unroll
+                            for (int e = 0; e < EPL; ++e)
+                                wv[u][e] = (EFIX || lane + 32 * e < E) ? wb[(q0 + u) * E + 32 * e] : 0.0f;
+                    };
+                    fetch(0, a_c, w_c);
+                    for (; q + U <= nr; q += U) {
+                        float a_n[U], w_n[U][EPL];
+                        if (q + 2 * U <= nr) fetch(q + U, a_n, w_n);
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+#pragma unroll
+                            for (int e = 0; e < EPL; ++e) {
+                                // reference: `if (av == 0.0f) continue; orow[j] += av * brow[j];`
+                                const float pr = __fmul_rn(a_c[u], w_c[u][e]);
+                                if (a_c[u] != 0.0f) acc[e] = __fadd_rn(acc[e], pr);
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            a_c[u] = a_n[u];
+#pragma unroll
+                            for (int e = 0; e < EPL; ++e) w_c[u][e] = w_n[u][e];
+                        }
+                    }
+                }
+                for (; q < nr; ++q) {
+                    const float av = hc[q];
 #pragma unroll
                     for (int e = 0; e < EPL; ++e) {
                         const float w = (EFIX || lane + 32 * e < E) ? wb[q * E + 32 * e] : 0.0f;
-                        // reference: `if (av == 0.0f) continue; orow[j] += av * brow[j];`
                         const float pr = __fmul_rn(av, w);
                         if (av != 0.0f) acc[e] = __fadd_rn(acc[e], pr);
                     }
                 }
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            if (tr && threadIdx.x == 0 && c < 8) tr[2 + c] = gtime_ns();
         }
-        // buffer (c&1) is rewritten at c+2, after the next iteration's barrier
+        if (live) finish_token<EPL>(a, P, acc, t, warp, s_exp);
+        else if (lane == 0) { s_exp[warp * a.topk] = -1; if (a.topk == 2) s_exp[warp * a.topk + 1] = -1; }
+        if (tr && threadIdx.x == 0) tr[10] = gtime_ns();
     }
-    if (live) finish_token<EPL>(a, P, acc, t, warp, s_exp);
-    else if (lane == 0) { s_exp[warp * a.topk] = -1; if (a.topk == 2) s_exp[warp * a.topk + 1] = -1; }
-    ranks_hist_plan(a, P, s_exp, s_hist, TT);
+    // the Wg ring is free now: it stages the per-CTA histograms for the plan
+    __syncthreads();
+    ranks_hist_plan(a, P, s_exp, s_hist, TT, reinterpret_cast<int*>(ring), kRouteSlots * chunk, tr);
 }
 
 // ---- large T (prefill) ----------------------------------------------------------------
@@ -510,13 +614,11 @@ cudaError_t launch_route(const RouteArgs& a, const Plan& P, cudaStream_t st) {
         k_route_select<<<grid, kRouteSelWarps * 32, 0, st>>>(a, P);
         return cudaGetLastError();
     }
-    const int rows = route_chunk_rows(a.E);
-    const int dpad = (a.d + rows - 1) / rows * rows;
-    const size_t smem = (size_t(2) * rows * a.E + size_t(kRouteSmallWarps) * dpad) * sizeof(float);
-    if (smem > 200 * 1024) return cudaErrorInvalidValue;
+    const size_t smem = route_small_smem(a.d, a.E);
+    if (smem > 220 * 1024) return cudaErrorInvalidValue;
     static bool configured = false;
     if (!configured) {
-        const int mx = 200 * 1024;
+        const int mx = 220 * 1024;
         cudaFuncSetAttribute(k_route_small<1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(k_route_small<2, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(k_route_small<4, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
@@ -524,14 +626,15 @@ cudaError_t launch_route(const RouteArgs& a, const Plan& P, cudaStream_t st) {
         cudaFuncSetAttribute(k_route_small<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         configured = true;
     }
+    constexpr int nthr = (kRouteSmallWarps + 1) * 32;
     switch (a.E) {
-        case 32: k_route_small<1, 32><<<grid, kRouteSmallWarps * 32, smem, st>>>(a, P); return cudaGetLastError();
-        case 64: k_route_small<2, 64><<<grid, kRouteSmallWarps * 32, smem, st>>>(a, P); return cudaGetLastError();
-        case 128: k_route_small<4, 128><<<grid, kRouteSmallWarps * 32, smem, st>>>(a, P); return cudaGetLastError();
-        case 256: k_route_small<8, 256><<<grid, kRouteSmallWarps * 32, smem, st>>>(a, P); return cudaGetLastError();
-        default: k_route_small<8, 0><<<grid, kRouteSmallWarps * 32, smem, st>>>(a, P); return cudaGetLastError();
+        case 32: k_route_small<1, 32><<<grid, nthr, smem, st>>>(a, P); break;
+        case 64: k_route_small<2, 64><<<grid, nthr, smem, st>>>(a, P); break;
+        case 128: k_route_small<4, 128><<<grid, nthr, smem, st>>>(a, P); break;
+        case 256: k_route_small<8, 256><<<grid, nthr, smem, st>>>(a, P); break;
+        default: k_route_small<8, 0><<<grid, nthr, smem, st>>>(a, P); break;
     }
-    return cudaErrorInvalidValue;
+    return cudaGetLastError();
 }
 
 cudaError_t launch_scatter(const void* h, int h_f16, int64_t T, int d, int topk, int E, int path, int tt,
