@@ -45,14 +45,9 @@ struct Workspace {
     Plan P{};
     __half* mid = nullptr;
     __half* x_perm = nullptr;
-    float* partial = nullptr;
-    int64_t part_rows = 0;
     float* out_acc = nullptr;
-    unsigned* split_cnt = nullptr;
-    uint8_t* xb = nullptr;         // GEMV activation digit fragments
-    unsigned* xb_flag = nullptr;
+    uint8_t* xb = nullptr;         // decode GEMV: fc2 activation fragments (fc1 -> fc2)
     int64_t xb_slot_bytes = 0;
-    float* l1part = nullptr;
 };
 
 struct moqe_bank {
@@ -67,7 +62,7 @@ struct moqe_bank {
     float* b1 = nullptr;
     float* b2 = nullptr;
     float* wg = nullptr;
-    float* smax1 = nullptr;  // [E][fc2 k-chunks] fc2 fixed-point bound constants (decode GEMV)
+    float* smax1 = nullptr;  // [E] fc2 fixed-point bound constants (decode GEMV)
     float* bmax1 = nullptr;
     int num_sms = 148;
     int device = 0;
@@ -86,7 +81,7 @@ struct moqe_bank {
 };
 
 namespace {
-int gemv_dbg() {
+int gemv_dbg() {  // diagnostics only
     static const int v = [] { const char* s = getenv("MOQE_GEMV_DBG"); return s ? atoi(s) : 0; }();
     return v;
 }
@@ -135,19 +130,16 @@ moqe_status ensure_workspace(moqe_bank* b, int64_t T, int topk) {
     }
     const int E = b->E;
     const int64_t nctas = (capT + 3) / 4;  // routing CTAs cover >= 4 tokens each
-    const int maxmt = std::max(b->Np1, b->Np2) / TILE_N;
-    const int64_t part_rows = capR;
-    const int64_t part = gemv_partial_floats(part_rows, b->Kp1, b->Np1, b->Kp2, b->Np2);
     // sizing pass
     int64_t bytes = 0;
     auto add = [&](int64_t sz, int64_t n) { bytes += round_up(sz * std::max<int64_t>(n, 1), 256); };
     add(4, capR); add(4, capR); add(4, capR); add(4, nctas * E); add(4, E); add(4, E + 1);
     add(4, capR); add(4, capR); add(4, capR); add(4, E); add(4, E); add(4, E + 1); add(4, 8);
-    add(4, 8); add(4, E); add(4, 2 * E * maxmt);
-    add(2, capR * b->Np1); add(2, capR * b->Kp1); add(4, part); add(4, capT * b->d); add(4, capT * E);
-    const int64_t xb_slots = gemv_xb_passes(capR, E) * gemv_ksplit(b->Kp2);
+    add(4, 8); add(4, E);
+    add(2, capR * b->Np1); add(2, capR * b->Kp1); add(4, capT * b->d); add(4, capT * E);
+    const int64_t xb_slots = gemv_xb_slots(capR, E, b->Kp2);
     const int64_t xb_bytes = gemv_xb_slot_bytes(b->bits);
-    add(xb_bytes, xb_slots); add(4, xb_slots * gemv_stages_per_chunk()); add(4, capR * gemv_ksplit(b->Kp1));
+    add(xb_bytes, xb_slots);
     MOQE_CUDA(cudaMalloc(&w.block, bytes));
     MOQE_CUDA(cudaMemset(w.block, 0, bytes));
     char* p = static_cast<char*>(w.block);
@@ -167,19 +159,12 @@ moqe_status ensure_workspace(moqe_bank* b, int64_t T, int topk) {
     P.meta = carve<int32_t>(p, 8);
     P.tickets = carve<unsigned>(p, 8);
     P.done = carve<unsigned>(p, E);
-    w.split_cnt = carve<unsigned>(p, 2 * E * maxmt);
-    P.split_done = w.split_cnt;
     w.mid = carve<__half>(p, capR * b->Np1);
     w.x_perm = carve<__half>(p, capR * b->Kp1);
-    w.partial = carve<float>(p, part);
-    P.partial = w.partial;
     w.out_acc = carve<float>(p, capT * b->d);
     P.logits = carve<float>(p, capT * E);
     w.xb = carve<uint8_t>(p, xb_bytes * xb_slots);
-    w.xb_flag = carve<unsigned>(p, xb_slots * gemv_stages_per_chunk());
     w.xb_slot_bytes = xb_bytes;
-    w.l1part = carve<float>(p, capR * gemv_ksplit(b->Kp1));
-    w.part_rows = part_rows;
     w.cap_rows = capR;
     w.cap_tokens = capT;
     return MOQE_OK;
@@ -287,10 +272,9 @@ moqe_status moqe_gpu_bank_create(int n_experts, int64_t d_model, int64_t d_ffn, 
         if (b1 && (st = upload_padded(&b->b1, b1, n_experts, d_ffn, b->Np1, dev)) != MOQE_OK) break;
         if (b2 && (st = upload_padded(&b->b2, b2, n_experts, d_model, b->Np2, dev)) != MOQE_OK) break;
         {
-            const int64_t nk = int64_t(n_experts) * gemv_ksplit(b->Kp2);
-            if ((ce = cudaMalloc(&b->smax1, sizeof(float) * nk)) != cudaSuccess) break;
-            if ((ce = cudaMalloc(&b->bmax1, sizeof(float) * nk)) != cudaSuccess) break;
-            if ((ce = launch_chunk_max(b->s1, b->b1, n_experts, b->Np1, b->Kp2, b->smax1, b->bmax1, nullptr)) !=
+            if ((ce = cudaMalloc(&b->smax1, sizeof(float) * n_experts)) != cudaSuccess) break;
+            if ((ce = cudaMalloc(&b->bmax1, sizeof(float) * n_experts)) != cudaSuccess) break;
+            if ((ce = launch_expert_max(b->s1, b->b1, n_experts, b->Np1, b->smax1, b->bmax1, nullptr)) !=
                 cudaSuccess)
                 break;
         }
@@ -365,6 +349,10 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
     if (eff_path == MOQE_PATH_AUTO && !gemm_available()) eff_path = MOQE_PATH_GEMV;
     // Small batches: no expert can exceed a few GEMV passes, so skip the (empty)
     // scatter + tcgen05 launches entirely; the GEMV takes every expert.
+    if (!gemv_supported(b->Kp1, b->Kp2)) {  // decode kernels hold a whole fc1 row of fragments in smem
+        if (eff_path == MOQE_PATH_GEMV) return fail(MOQE_NOT_SUPPORTED, "moe_forward: GEMV path needs d_model <= 2048");
+        eff_path = MOQE_PATH_GEMM;
+    }
     if (eff_path == MOQE_PATH_AUTO && R <= 4 * kGemvMaxRows) eff_path = MOQE_PATH_GEMV;
     const bool need_gemm = eff_path == MOQE_PATH_GEMM || (eff_path == MOQE_PATH_AUTO && R > kGemvMaxRows);
     const bool need_gemv = eff_path != MOQE_PATH_GEMM;
@@ -391,10 +379,9 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
     if (need_gemv) {
         GemvArgs g{h, h_dtype == MOQE_F16, t, int(b->d), int(b->f), top_k, b->E, b->w1, b->w2,
                    b->w1_stride, b->w2_stride, b->s1, b->s2, b->b1, b->b2, b->Kp1, b->Np1, b->Kp2, b->Np2,
-                   w.mid, out, out_dtype == MOQE_F16, acc, w.partial, w.part_rows, w.split_cnt,
-                   w.xb, w.xb_flag, w.xb_slot_bytes, b->smax1, b->bmax1, w.l1part, b->trace, gemv_dbg()};
+                   out, out_dtype == MOQE_F16, acc, w.xb, w.xb_slot_bytes, b->smax1, b->bmax1, b->trace, gemv_dbg()};
         KernelTimer kt(b, 2, st);
-        ce = launch_gemv(b->bits, R > 16, g, P, st, b->num_sms);
+        ce = launch_gemv(b->bits, g, P, st, b->num_sms);
         if (ce != cudaSuccess) return cuda_fail(ce, "k_ffn_gemv");
     }
     if (need_gemm) {

@@ -1,5 +1,6 @@
-// ffn_gemv.cu — decode path: fused expert FFN (fc1 -> ReLU -> fc2 -> gate
-// combine) as ONE persistent, warp-specialised weight-streaming kernel.
+// ffn_gemv.cu — decode path: expert FFN (fc1 -> ReLU -> fc2 -> gate combine)
+// as two persistent weight-streaming kernels (one per layer of the FFN),
+// chained with programmatic dependent launch (PDL).
 //
 // Reference: the per-expert loop of moe_ffn_forward proj/src/model.cpp:360-391
 // (dequantize :370-375, matmul :381/:384, add_bias/relu :382-385, scatter
@@ -9,34 +10,35 @@
 //
 // Integer dot products (frag.cuh). A weight code q = u - 2^(b-1) is kept as
 // its offset binary u; one LOP3 yields four u8 values u * 2^s that feed IMMA
-// m16n8k32 (u8 x s8 -> s32). Activations of a row are a per-row fixed-point
-// integer X = rint(x * 2^p) split into signed base-256 digit planes; each
-// plane is one MMA column. Sum_k u*X is exact in integers; the zero point
-// (2^(b-1) Sum X), the plane weights 256^s and 2^-p are applied once per item
-// in fp64, the per-channel scale in the epilogue.
+// m16n8k32 (u8 x s8 -> s32). The activations of a row are a per-row
+// fixed-point integer X = rint(x * 2^p) split into signed base-256 digit
+// planes; each plane is one MMA column. Sum_k u*X is exact in integers; the
+// zero point 2^(b-1) * Sum X, the plane weights 256^s and 2^-p are applied
+// once per item, the per-channel scale in the epilogue.
 //   fc1 rows (fp16 tokens): 3 planes, p from the row maximum — exact for every
 //     activation within 2^11 of the row max.
 //   fc2 rows (mid = ReLU(fc1)): 4 planes, p from a rigorous per-row bound
-//     |mid| <= max_scale * 2^(b-1) * |x|_1 + max|bias|, so every fc1 item can
-//     encode its own 128 output channels (one fc2 k-stage) without waiting for
-//     the rest of the row; resolution ~2^-29 of the bound, far finer than the
-//     fp32 chain of the reference.
+//     |mid| <= max_scale * 2^(b-1) * |x|_1 + max|bias|, so every fc1 item
+//     encodes its own 128 output channels (one fc2 k-stage) independently;
+//     resolution ~2^-29 of the bound, far finer than the reference's fp32 chain.
 //
-// Work items (device-side, no host sync): fc1 (expert, 128-channel m-tile,
-// k-chunk, row pass) for every expert in the GEMV list, then fc2 items.
-//   warp 12      producer: item tickets, packed weight tiles -> smem ring via
-//                TMA bulk copies (evict-first), 2 tiles (128 k) per stage
-//   warps 8-10   builders: fc1 item rows -> digit fragments in smem (two items
-//                ahead of the consumers, warp per row)
-//   warp 11      loader: fc2 item -> waits for the 8 fc1 stage flags of its
-//                fragment slot, TMA bulk copy slot -> smem
-//   warps 0-7    consumers: 16 output channels each; LOP3 unpack, IMMA;
-//                accumulators -> smem scratch (double buffered)
-//   warps 13-14  publishers: exact epilogue, scale/bias, fc1 -> fc2 fragment
-//                slots (+ ready flags), fc2 -> gate-weighted output; split-K
-//                partials reduced in fixed order by the last arriving CTA
-// Results are deterministic (integer accumulation, fixed-order reductions).
+// Work: an item is (expert, row pass, 128-channel m-tile); its K is split into
+// 1024-k chunks, one per CTA of a thread-block cluster (fc1: d/1024 CTAs, fc2:
+// f/1024). Each CTA streams its chunk's packed tiles — one contiguous stripe —
+// with TMA bulk copies of >= 16 KB (smaller copies cap the chip at 1-3.6 TB/s,
+// profiles/round1/tma_copy_size.md), runs the IMMA k-loop, and sends its exact
+// int64 partial sums to cluster rank 0 through distributed shared memory; rank 0
+// finishes the item. Items are statically scheduled over the clusters (all the
+// same size), so there are no tickets and no cross-cluster synchronisation.
+//   fc1 roles: warps 0-7 consumers (16 channels each), 8-10 builders (token rows
+//     -> digit fragments in smem, two items ahead), 11 producer (weights).
+//     Rank 0's epilogue writes fc2's fragments + Sum X parts to global memory.
+//   fc2 roles: warps 0-7 consumers, 8 producer (weights, then each item's
+//     fragment slot, issued after the PDL wait on fc1); rank 0 writes the
+//     gate-weighted output rows (exactly one writer per element: deterministic).
 #include <cuda_fp16.h>
+
+#include <algorithm>
 
 #include "codec.cuh"
 #include "frag.cuh"
@@ -45,58 +47,62 @@
 
 namespace moqe_gpu {
 
-constexpr int kGemvKC = 1024;        // k per item
-constexpr int kStageK = 2 * TILE_K;  // k per ring stage (2 tiles)
-constexpr int kStagesPerChunk = kGemvKC / kStageK;
-constexpr int kConsumers = 4;        // IMMA warps (32 channels = two m16 blocks each: every B fragment feeds 2 IMMAs)
-constexpr int kBlk = 2;              // m16 blocks per consumer warp
-constexpr int kBuilders = 3;         // fc1 fragment builders
-constexpr int kLoader = kConsumers + kBuilders;
-constexpr int kProducer = kLoader + 1;
-constexpr int kPublisher = kProducer + 1;
-constexpr int kGemvThreads = (kPublisher + 1) * 32;
-constexpr int kItemQ = 6;
-constexpr int kBBufs = kBuilders;    // fragment buffers (builder warp b owns buffer b); two items of lead
-constexpr int kScrBufs = 3;          // accumulator scratch / epilogue buffers (warps may drift two items apart)
+constexpr int kStageK = 2 * TILE_K;  // k per IMMA stage (2 tiles)
+constexpr int kChunkK = 1024;        // k per CTA of a cluster
+constexpr int kChunkStages = kChunkK / kStageK;
+constexpr int kMaxCluster = 8;
 constexpr int kPassRows = 4;         // token rows per item pass
-constexpr int kMaxNT = 2;            // n8 column tiles per item (4 rows x 4 planes = 16 columns)
-constexpr int kMaxListed = 256;
-constexpr int kRingBytes = 96 * 1024;
+constexpr int kMaxNT = 2;            // n8 column tiles (4 rows x 4 planes = 16 columns)
 constexpr int kScrCols = 8 * kMaxNT;
+constexpr int kMaxListed = 256;
+constexpr int kConsumers = 8;        // consumer warps: 16 channels (one m16 block) each
+constexpr int kBuilders = 3;         // fc1 fragment builders (= fragment buffers)
+constexpr int kBufs = 3;             // fragment buffers
+constexpr int kHead = 352;           // fragment buffer / fc2 slot head (see below)
 constexpr int kZeroRow = -0x40000000;  // exponent sentinel: the row is (numerically) zero
 
-__host__ __device__ constexpr int gemv_ksplit_c(int Kp) { return (Kp + kGemvKC - 1) / kGemvKC; }
 __host__ __device__ constexpr int planes_of(int phase) { return phase == 1 ? 3 : 4; }
 __host__ __device__ constexpr int nt_of(int phase, int rows) { return (planes_of(phase) * rows + 7) / 8; }
 __host__ __device__ constexpr int w_of(int phase, int nt) { return 8 * nt / planes_of(phase); }
+__host__ __device__ constexpr int threads_of(int phase) {
+    return (phase == 1 ? kConsumers + kBuilders + 1 : kConsumers + 1) * 32;
+}
+template <int BITS>
+__host__ __device__ constexpr int unit_stages() { return BITS == 8 ? 2 : 4; }  // >= 16 KB per weight copy
+
+// Fragment buffer head (352 bytes):
+//   fc1 (built in smem): p[4] (row exponent), zsum[4] (Sum X of the chunk), l1[4] (|x|_1 of the row)
+//   fc2 slot (global, copied with the fragments): p[4] = p2, zpart[8 stages][4 rows] (Sum X2 per fc1 item)
+struct __align__(16) Head {
+    int p[4];
+    int pad0[4];
+    long long zsum[4];
+    float l1[4];
+    int pad1[4];
+    long long zpart[kChunkStages][4];
+};
+static_assert(sizeof(Head) == kHead, "head layout");
 
 template <int BITS>
-struct GemvCfg {
-    static constexpr int TB = tile_bytes(BITS);
-    static constexpr int SB = 2 * TB;                 // ring stage = 2 tiles (128 k)
-    static constexpr int NST = kRingBytes / SB;
+struct Cfg {
     static constexpr int F = Frag<BITS>::F;
-    static constexpr int BBUF = kStagesPerChunk * F * kMaxNT * 256;  // digit fragments per item
+    static constexpr int TB = tile_bytes(BITS);
+    static constexpr int SB = 2 * TB;                             // one IMMA stage of weights
+    static constexpr int US = unit_stages<BITS>();
+    static constexpr int UB = US * SB;                            // one weight copy
+    static constexpr int BBUF = kChunkStages * F * kMaxNT * 256;  // fragments of a 1024-k chunk
+    static constexpr int64_t SLOT = kHead + BBUF;                 // fc2 fragment slot in global memory
 };
 
 struct GemvItem {
-    int phase;  // 1 fc1, 2 fc2, 0 end
-    int e, mt, ks, row0, nrows, npass, slot;  // slot: fc2 fragment slot (fc1: of the pass's chunk 0)
+    int e, mt, row0, nrows, gp;  // gp: global row-pass index (fc2 fragment slots); e < 0: none
 };
 
 struct GemvTables {
     int list[kMaxListed], cnt[kMaxListed], off[kMaxListed];
-    int pst[kMaxListed + 1];                             // row-pass prefix per listed expert
-    int start1[kMaxListed + 1], start2[kMaxListed + 1];  // item prefix per listed expert
+    int pst[kMaxListed + 1];    // row-pass prefix per listed expert
+    int start[kMaxListed + 1];  // item prefix per listed expert
 };
-
-// Per-item fragment meta (128 bytes, copied with the fragments).
-struct __align__(16) BufMeta {
-    int p[8];                     // row exponent (kZeroRow: zero row)
-    unsigned long long zsum[8];   // fc1: Sum_k X per row (fc2 slots keep it per stage, after the fragments)
-    float l1[8];                  // fc1: |x|_1 of the row chunk (bounds the fc2 exponent)
-};
-static_assert(sizeof(BufMeta) == 128, "BufMeta is copied as one 128-byte block");
 
 __device__ __forceinline__ int find_listed(const int* st, int n, int v) {  // largest a with st[a] <= v
     int lo = 0, hi = n - 1;
@@ -107,126 +113,151 @@ __device__ __forceinline__ int find_listed(const int* st, int n, int v) {  // la
     return lo;
 }
 
-// Ticket order: fc1 items (expert, pass, m-tile, k-split) then fc2 items.
-__device__ GemvItem decode_item(unsigned ticket, const GemvTables& T, int n_gemv, int nmt1, int s1, int nmt2,
-                                int s2) {
-    GemvItem it{};
-    const unsigned c1 = unsigned(T.start1[n_gemv]), c2 = c1 + unsigned(T.start2[n_gemv]);
-    int phase, r;
-    if (ticket < c1) { phase = 1; r = int(ticket); }
-    else if (ticket < c2) { phase = 2; r = int(ticket - c1); }
-    else { it.phase = 0; return it; }
-    const int* st = phase == 1 ? T.start1 : T.start2;
-    const int a = find_listed(st, n_gemv, r);
-    const int nmt = phase == 1 ? nmt1 : nmt2, S = phase == 1 ? s1 : s2;
-    const int rr = r - st[a];
-    const int pass = rr / (nmt * S), r2 = rr % (nmt * S);
-    const int n = T.cnt[a];
-    it.phase = phase;
-    it.e = T.list[a];
-    it.mt = r2 / S;
-    it.ks = r2 % S;
-    it.row0 = T.off[a] + pass * kPassRows;
-    it.nrows = min(kPassRows, n - pass * kPassRows);
-    it.npass = (n + kPassRows - 1) / kPassRows;
-    it.slot = (T.pst[a] + pass) * s2 + (phase == 2 ? it.ks : 0);
-    return it;
-}
-
-// ---- optional event trace (diagnostics; off unless the bank enables it) ----------------
-// event word: role << 60 | ev << 56 | phase << 48 | e << 32 | mt << 16 | ks
-__device__ __forceinline__ void trace_ev(const GemvArgs& g, unsigned* cnt, int role, int ev, const GemvItem& it) {
-    if (g.trace == nullptr) return;
-    const unsigned i = atomicAdd(cnt, 1u);
-    if (i >= unsigned(kTraceCap)) return;
-    unsigned long long* p = g.trace + (size_t(blockIdx.x) * kTraceCap + i) * 2;
-    p[0] = gtime_ns();
-    p[1] = (unsigned long long)role << 60 | (unsigned long long)ev << 56 | (unsigned long long)(it.phase & 0xff) << 48 |
-           (unsigned long long)(it.e & 0xffff) << 32 | (unsigned long long)(it.mt & 0xffff) << 16 |
-           (unsigned long long)(it.ks & 0xffff);
-}
-
-// Scatter one lane's 32 digit words (byte s = plane s) into the B fragments of
-// one stage: column (t, s) -> n-tile j, group g; lane quad tq.
-template <int BITS, int PL>
-__device__ __forceinline__ void scatter_digits(const uint32_t (&D)[32], uint8_t* bstage, int NT, int W, int t,
-                                               int tq, bool global) {
-    using FR = Frag<BITS>;
-    constexpr int F = FR::F;
-#pragma unroll
-    for (int s = 0; s < PL; ++s) {
-        const int col = s * W + t, j = col >> 3, gq = col & 7;
-        const uint32_t sel = uint32_t(s) | (uint32_t(4 + s) << 4);
-        uint8_t* dst = bstage + size_t(j) * 256 + (4 * gq + tq) * 8;
-#pragma unroll
-        for (int f = 0; f < F; ++f) {
-            uint32_t b[2];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const uint32_t lo = prmt(D[FR::kidx(f, h, 0)], D[FR::kidx(f, h, 1)], sel);
-                const uint32_t hi = prmt(D[FR::kidx(f, h, 2)], D[FR::kidx(f, h, 3)], sel);
-                b[h] = prmt(lo, hi, 0x5410u);
-            }
-            uint2* p = reinterpret_cast<uint2*>(dst + size_t(f) * NT * 256);
-            if (global) __stcg(p, make_uint2(b[0], b[1]));
-            else *p = make_uint2(b[0], b[1]);
+// Item tables from the plan (one warp: lane-parallel loads, serial prefix).
+__device__ void build_tables(GemvTables& T, const Plan& P, int n_gemv, int nmt, int lane) {
+    for (int a = lane; a < n_gemv; a += 32) {
+        const int e = P.gemv_list[a];
+        T.list[a] = e;
+        T.cnt[a] = P.counts[e];
+        T.off[a] = P.offsets[e];
+    }
+    __syncwarp();
+    if (lane == 0) {
+        int t = 0, tp = 0;
+        for (int a = 0; a < n_gemv; ++a) {
+            const int np = (T.cnt[a] + kPassRows - 1) / kPassRows;
+            T.pst[a] = tp;
+            T.start[a] = t;
+            tp += np;
+            t += nmt * np;
         }
+        T.pst[n_gemv] = tp;
+        T.start[n_gemv] = t;
     }
 }
 
-// ---- builders: fc1 rows -> 3-plane digit fragments in smem ----------------------------
-// One warp per row; lane = (stage st, quad tq) owns the 32 activations that
-// quad's IMMA lanes meet in that stage, so the row maximum, Sum X and |x|_1
-// are warp reductions.
+// Item i (expert-major: expert, pass, m-tile).
+__device__ GemvItem item_at(int i, const GemvTables& T, int n_gemv, int nmt) {
+    GemvItem it{};
+    if (i >= T.start[n_gemv]) { it.e = -1; return it; }
+    const int a = find_listed(T.start, n_gemv, i);
+    const int r = i - T.start[a];
+    const int pass = r / nmt;
+    it.e = T.list[a];
+    it.mt = r % nmt;
+    it.row0 = T.off[a] + pass * kPassRows;
+    it.nrows = min(kPassRows, T.cnt[a] - pass * kPassRows);
+    it.gp = T.pst[a] + pass;
+    return it;
+}
+
+// ---- cluster / DSMEM helpers ----------------------------------------------------------
+__device__ __forceinline__ uint32_t cta_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cluster_nctas() {
+    uint32_t n;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(n));
+    return n;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_rank(const void* p, uint32_t rank) {  // own smem addr -> CTA `rank`
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster_s64(uint32_t addr, long long v) {
+    asm volatile("st.shared::cluster.s64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+__device__ __forceinline__ void arrive_cluster(uint32_t bar_addr) {  // release at cluster scope
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_addr) : "memory");
+}
+__device__ __forceinline__ void wait_cluster(uint64_t* bar, uint32_t parity) {  // acquire at cluster scope
+    uint32_t ok = 0;
+    while (!ok)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
+            : "memory");
+}
+
+// ---- optional event trace (diagnostics; off unless the bank enables it) ----------------
+__device__ __forceinline__ void trace_ev(unsigned long long* trace, unsigned* cnt, int role, int ev,
+                                         const GemvItem& it, int phase) {
+    if (trace == nullptr) return;
+    const unsigned i = atomicAdd(cnt, 1u);
+    if (i >= unsigned(kTraceCap / 2)) return;
+    unsigned long long* p = trace + (size_t(blockIdx.x) * kTraceCap + i) * 2;
+    p[0] = gtime_ns();
+    p[1] = (unsigned long long)role << 60 | (unsigned long long)ev << 56 | (unsigned long long)phase << 48 |
+           (unsigned long long)(it.e & 0xffff) << 32 | (unsigned long long)(it.mt & 0xfff) << 20 |
+           (unsigned long long)(it.nrows & 0xf) << 16 | (unsigned long long)(clock64() & 0xffff);
+}
+
+// ---- fc1 builders: token rows -> 3-plane digit fragments of one 1024-k chunk ----------
+// One warp per row; lane = (stage st, quad tq) owns the 32 activations that quad's
+// IMMA lanes meet in stage st of the chunk. The row maximum and |x|_1 cover the
+// whole row (every CTA of the cluster derives the same exponent).
 template <int BITS>
 __device__ void build_row(const GemvArgs& g, const Plan& P, const GemvItem& it, int t, int lane, bool vec_h,
-                          uint8_t* bb, BufMeta& meta) {
-    constexpr int F = Frag<BITS>::F;
-    const int k0 = it.ks * kGemvKC;
-    const int nst = min(kGemvKC, g.Kp1 - k0) / kStageK;
+                          int k0, int nst, uint8_t* bb, Head& hd) {
+    using FR = Frag<BITS>;
+    constexpr int F = FR::F;
     const int NT = nt_of(1, it.nrows), W = w_of(1, NT);
     const int st = lane >> 2, tq = lane & 3;
-    const bool act = st < nst;
-    float v[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = 0.f;
-    const int kb = k0 + st * kStageK + 16 * tq;  // tile 0 run; tile 1 run at +64
     const int64_t tok = P.perm_token[it.row0 + t];
-    if (act) {
+    auto load16 = [&](int k, float* v) {  // 16 activations from k (zeros beyond d)
         if (vec_h) {
             const __half* row = static_cast<const __half*>(g.h) + tok * g.d;
 #pragma unroll
-            for (int tile = 0; tile < 2; ++tile)
+            for (int q = 0; q < 2; ++q) {
+                uint4 w = make_uint4(0u, 0u, 0u, 0u);
+                if (k + 8 * q < g.d) w = __ldg(reinterpret_cast<const uint4*>(row + k + 8 * q));  // d % 8 == 0
+                const __half2* h2 = reinterpret_cast<const __half2*>(&w);
 #pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const int kk = kb + 64 * tile + 8 * q;
-                    uint4 w = make_uint4(0u, 0u, 0u, 0u);
-                    if (kk < g.d) w = __ldg(reinterpret_cast<const uint4*>(row + kk));  // d % 8 == 0
-                    const __half2* h2 = reinterpret_cast<const __half2*>(&w);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const float2 f = __half22float2(h2[i]);
-                        v[16 * tile + 8 * q + 2 * i] = f.x;
-                        v[16 * tile + 8 * q + 2 * i + 1] = f.y;
-                    }
+                for (int i = 0; i < 4; ++i) {
+                    const float2 f = __half22float2(h2[i]);
+                    v[8 * q + 2 * i] = f.x;
+                    v[8 * q + 2 * i + 1] = f.y;
                 }
+            }
         } else {
 #pragma unroll
-            for (int tile = 0; tile < 2; ++tile)
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int kk = kb + 64 * tile + i;
-                    float x = 0.f;
-                    if (kk < g.d)  // activations enter as fp16 values (the GEMM path's x_perm is fp16 too)
-                        x = g.h_f16 ? __half2float(static_cast<const __half*>(g.h)[tok * g.d + kk])
-                                    : __half2float(__float2half_rn(static_cast<const float*>(g.h)[tok * g.d + kk]));
-                    v[16 * tile + i] = x;
-                }
+            for (int i = 0; i < 16; ++i) {
+                float x = 0.f;
+                if (k + i < g.d)  // activations enter as fp16 values (the GEMM path's x_perm is fp16 too)
+                    x = g.h_f16 ? __half2float(static_cast<const __half*>(g.h)[tok * g.d + k + i])
+                                : __half2float(__float2half_rn(static_cast<const float*>(g.h)[tok * g.d + k + i]));
+                v[i] = x;
+            }
         }
+    };
+    float v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = 0.f;
+    const bool act = st < nst;
+    if (act) {
+        load16(k0 + st * kStageK + 16 * tq, v);
+        load16(k0 + st * kStageK + 64 + 16 * tq, v + 16);
     }
     float m = 0.f, l1 = 0.f;
 #pragma unroll
     for (int i = 0; i < 32; ++i) { m = fmaxf(m, fabsf(v[i])); l1 += fabsf(v[i]); }
+    // the rest of the row (other chunks of the cluster): maximum and |x|_1 only
+    for (int k = lane * 16; k < g.Kp1; k += 32 * 16) {
+        if (k >= k0 && k < k0 + kChunkK) continue;
+        float u[16];
+        load16(k, u);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) { m = fmaxf(m, fabsf(u[i])); l1 += fabsf(u[i]); }
+    }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
         m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
@@ -247,85 +278,66 @@ __device__ void build_row(const GemvArgs& g, const Plan& P, const GemvItem& it, 
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) zs += __shfl_xor_sync(0xffffffffu, zs, off);
     if (lane == 0) {
-        meta.p[t] = p;
-        meta.zsum[t] = (unsigned long long)zs;
-        meta.l1[t] = l1 * (1.0f + 0x1p-9f);  // covers the fp32 summation error: an upper bound
+        hd.p[t] = p;
+        hd.zsum[t] = zs;
+        hd.l1[t] = l1 * (1.0f + 0x1p-9f);  // covers the fp32 summation error: an upper bound
     }
-    if (act) scatter_digits<BITS, 3>(D, bb + size_t(st * F) * NT * 256, NT, W, t, tq, false);
-}
-
-// ---- consumers ------------------------------------------------------------------------
-template <int BITS, int NT>
-__device__ __forceinline__ void gemv_mainloop(const uint8_t* ring, const uint8_t* bb, uint64_t* full,
-                                              uint64_t* empty, int& stage, int& sphase, int nst, int warp,
-                                              int lane, int (&acc)[kBlk][Frag<BITS>::G][kMaxNT][4],
-                                              long long* cyc = nullptr) {
-    using Cfg = GemvCfg<BITS>;
-    using FR = Frag<BITS>;
-    constexpr int F = FR::F;
-    const int tq = lane & 3, r0 = 16 * kBlk * warp + (lane >> 2);
-    auto compute = [&](int stg, int s) {
-        const uint8_t* T0 = ring + stg * Cfg::SB;
-        uint32_t a[kBlk][F][4];
+    if (!act) return;
 #pragma unroll
-        for (int bk = 0; bk < kBlk; ++bk) FR::load(T0, T0 + Cfg::TB, r0 + 16 * bk, tq, a[bk]);
-        const uint8_t* bs = bb + size_t(s * F) * NT * 256 + lane * 8;
+    for (int s = 0; s < 3; ++s) {
+        const int col = s * W + t, j = col >> 3, gq = col & 7;
+        const uint32_t sel = uint32_t(s) | (uint32_t(4 + s) << 4);
+        uint8_t* dst = bb + (size_t(st * F) * NT + j) * 256 + (4 * gq + tq) * 8;
 #pragma unroll
-        for (int f = 0; f < F; ++f)
+        for (int f = 0; f < F; ++f) {
+            uint32_t b[2];
 #pragma unroll
-            for (int j = 0; j < NT; ++j) {
-                const uint2 b = *reinterpret_cast<const uint2*>(bs + (f * NT + j) * 256);
-#pragma unroll
-                for (int bk = 0; bk < kBlk; ++bk) imma(acc[bk][FR::grp(f)][j], a[bk][f], b.x, b.y);
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t lo = prmt(D[FR::kidx(f, h, 0)], D[FR::kidx(f, h, 1)], sel);
+                const uint32_t hi = prmt(D[FR::kidx(f, h, 2)], D[FR::kidx(f, h, 3)], sel);
+                b[h] = prmt(lo, hi, 0x5410u);
             }
-    };
-    // two ring stages per iteration: both waits first, so the second stage's
-    // shared-memory loads overlap the first stage's IMMAs
-    for (int s = 0; s < nst; s += 2) {
-        const bool two = s + 1 < nst;
-        const int st0 = stage, ph0 = sphase;
-        if (++stage == Cfg::NST) { stage = 0; sphase ^= 1; }
-        const int st1 = stage, ph1 = sphase;
-        if (two && ++stage == Cfg::NST) { stage = 0; sphase ^= 1; }
-        long long c0 = 0;
-        if (cyc) c0 = clock64();
-        mbar_wait(&full[st0], ph0);
-        if (two) mbar_wait(&full[st1], ph1);
-        if (cyc) { const long long c1 = clock64(); cyc[0] += c1 - c0; c0 = c1; }
-        compute(st0, s);
-        if (two) compute(st1, s + 1);
-        __syncwarp();
-        if (cyc) cyc[1] += clock64() - c0;
-        if (lane == 0) {
-            mbar_arrive(&empty[st0]);
-            if (two) mbar_arrive(&empty[st1]);
+            *reinterpret_cast<uint2*>(dst + size_t(f) * NT * 256) = make_uint2(b[0], b[1]);
         }
     }
 }
 
-// ---- epilogue helpers -------------------------------------------------------------------
-__device__ __forceinline__ void scale_bias(const GemvArgs& g, bool p1, int e, int ch, float& sc, float& bias) {
-    const int Np = p1 ? g.Np1 : g.Np2;
-    sc = __ldg((p1 ? g.s1 : g.s2) + int64_t(e) * Np + ch);
-    const float* bi = p1 ? g.b1 : g.b2;
-    bias = bi ? __ldg(bi + int64_t(e) * Np + ch) : 0.f;
+// ---- consumer pieces -------------------------------------------------------------------
+// One 128-k stage of one m16 block: LOP3 unpack + IMMA against the stage's B fragments.
+template <int BITS, int NT>
+__device__ __forceinline__ void stage_mma(const uint8_t* T0, int r0, int lane, const uint8_t* bstage,
+                                          int (&acc)[Frag<BITS>::G][kMaxNT][4]) {
+    using FR = Frag<BITS>;
+    constexpr int F = FR::F;
+    uint32_t a[F][4];
+    FR::load(T0, T0 + tile_bytes(BITS), r0, lane & 3, a);
+    const uint8_t* bs = bstage + lane * 8;
+#pragma unroll
+    for (int f = 0; f < F; ++f)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+            const uint2 b = *reinterpret_cast<const uint2*>(bs + (f * NT + j) * 256);
+            imma(acc[FR::grp(f)][j], a[f], b.x, b.y);
+        }
+}
+
+template <int BITS, int NT>
+__device__ __forceinline__ void unit_mma(const uint8_t* U, int nst_u, int s0, int r0, int lane, const uint8_t* bb,
+                                         int (&acc)[Frag<BITS>::G][kMaxNT][4]) {
+    constexpr int F = Frag<BITS>::F, SB = 2 * tile_bytes(BITS);
+#pragma unroll 2
+    for (int s = 0; s < nst_u; ++s) stage_mma<BITS, NT>(U + s * SB, r0, lane, bb + size_t((s0 + s) * F) * NT * 256, acc);
+}
+
+__device__ __forceinline__ void scale_bias(const float* s, const float* b, int64_t idx, float& sc, float& bias) {
+    sc = __ldg(s + idx);
+    bias = b ? __ldg(b + idx) : 0.f;
 }
 
 // V * 2^-sh in fp32: one rounding (int64 -> fp32), exact power-of-two scale
 __device__ __forceinline__ float scale_pow2(long long V, int sh) {
     const float v = float(V);
     return (sh > -127 && sh < 127) ? v * __int_as_float((127 - sh) << 23) : ldexpf(v, -sh);
-}
-
-// fc2 output element: y -> scale/bias -> x gate -> output row
-__device__ __forceinline__ void fc2_finish(const GemvArgs& g, int ch, float y, float sc, float bias, float gate,
-                                           int tok) {
-    if (ch >= g.d) return;
-    const float yg = fmaf(y, sc, bias) * gate;
-    const int64_t o = int64_t(tok) * g.d + ch;
-    if (g.out_acc) atomicAdd(g.out_acc + o, yg);
-    else if (g.out_f16) static_cast<__half*>(g.out)[o] = __float2half_rn(yg);
-    else static_cast<float*>(g.out)[o] = yg;
 }
 
 // fc2 exponent of one fc1 row: |mid| <= smax * 2^(b-1) * |x|_1 + bmax, and
@@ -335,552 +347,393 @@ __device__ __forceinline__ int fc2_exp(float smax, float bmax, float l1) {
     const float bound = (smax * float(1 << (BITS - 1)) * l1 + bmax) * (1.0f + 0x1p-16f);
     return bound < 0x1p-100f ? kZeroRow : 29 - ilogbf(bound);
 }
-__device__ __forceinline__ int encode_x2(float mid, int p2) {
-    return p2 == kZeroRow ? 0 : __float2int_rn(ldexpf(mid, p2));
-}
 
-// fc2 fragment words of one stage from the X2 of 128 channels x rows (xs),
-// spread over `nthr` threads: word (row t, quad tq, plane s, fragment f).
-template <int BITS>
-__device__ __forceinline__ void encode_stage(const int* xs, int nrows, uint8_t* bstage, int tid, int nthr) {
-    using FR = Frag<BITS>;
-    constexpr int F = FR::F;
-    const int NT = nt_of(2, nrows), W = w_of(2, NT);
-    const int nwords = nrows * 4 * 4 * F;
-    for (int w = tid; w < nwords; w += nthr) {
-        const int f = w % F, s = (w / F) & 3, tq = (w / (4 * F)) & 3, t = w / (16 * F);
-        uint32_t b[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            uint32_t word = 0;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int k = FR::kidx(f, h, i);  // tile * 16 + code
-                const int X = xs[(64 * (k >> 4) + 16 * tq + (k & 15)) * kPassRows + t];
-                const uint32_t dig = (((uint32_t(X) + 0x80808080u) ^ 0x80808080u) >> (8 * s)) & 0xffu;
-                word |= dig << (8 * i);
-            }
-            b[h] = word;
-        }
-        const int col = s * W + t, j = col >> 3, gq = col & 7;
-        __stcg(reinterpret_cast<uint2*>(bstage + (size_t(f) * NT + j) * 256 + (4 * gq + tq) * 8),
-               make_uint2(b[0], b[1]));
-    }
-}
-
-// ---- consumers: mainloop + the item's epilogue for the warp's 16 channels -------------
-struct EpiSmem {  // per epilogue buffer
-    int xs[TILE_N * kPassRows];   // fc1: fixed-point mid of the item (the fc2 stage)
-    unsigned long long zs[kPassRows];
+// ---- smem layout (host and device agree) ------------------------------------------------
+template <int BITS, int PHASE>
+struct Layout {
+    static constexpr int NU = 116 * 1024 / Cfg<BITS>::UB;  // weight-copy ring slots (~96-112 KB in flight)
+    static constexpr size_t RING = size_t(NU) * Cfg<BITS>::UB;
+    static constexpr size_t BUFS = size_t(kBufs) * (kHead + Cfg<BITS>::BBUF);
+    static constexpr size_t SCR = size_t(TILE_N) * kScrCols * 4;
+    static constexpr size_t RED = size_t(kMaxCluster) * TILE_N * kPassRows * 8;  // int64 partials per rank
+    static constexpr size_t XS = PHASE == 1 ? TILE_N * kPassRows * 4 + kPassRows * 8 : 0;
+    static constexpr size_t BARS = size_t(2 * NU + 2 * kBufs + 2) * 8;
+    static constexpr size_t TOTAL = RING + BUFS + SCR + RED + XS + BARS + sizeof(GemvTables) + 64;
 };
 
-template <int BITS, int NT>
-__device__ void consume_item(const GemvArgs& g, const Plan& P, const GemvItem& it, const uint8_t* ring,
-                             const uint8_t* bb, const BufMeta& meta, const long long* bzsum, uint64_t* full,
-                             uint64_t* empty, int& stage, int& sphase, int* ws, EpiSmem& es, int s1, int s2,
-                             unsigned* tn) {
+template <int BITS, int PHASE>
+__global__ void __launch_bounds__(threads_of(PHASE), 1) k_gemv(GemvArgs g, Plan P) {
     using FR = Frag<BITS>;
-    constexpr int G = FR::G;
+    using C = Cfg<BITS>;
+    using L = Layout<BITS, PHASE>;
+    constexpr int F = FR::F, G = FR::G, NU = L::NU, UB = C::UB, US = C::US, SB = C::SB, TB = C::TB;
     constexpr int LOGD = FR::D == 64 ? 6 : FR::D == 16 ? 4 : 0;
     constexpr long long Z = 1ll << (BITS - 1);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tq = lane & 3, gq = lane >> 2;
-    const bool p1 = it.phase == 1;
-    const int Kp = p1 ? g.Kp1 : g.Kp2;
-    const int nst = min(kGemvKC, Kp - it.ks * kGemvKC) / kStageK;
-    const int S = p1 ? s1 : s2;
-    const int Np = p1 ? g.Np1 : g.Np2;
-    const int nrows = it.nrows;
-    // epilogue operands fetched early (latency overlaps the k-loop): lane -> channel r, all rows
-    const int r = lane, ch = it.mt * TILE_N + 32 * warp + r;
-    float sc, bias;
-    scale_bias(g, p1, it.e, ch, sc, bias);
-    const int ks2 = it.mt / kStagesPerChunk;
-    const float smax = p1 ? __ldg(g.smax1 + it.e * s2 + ks2) : 0.f;
-    const float bmax = p1 ? __ldg(g.bmax1 + it.e * s2 + ks2) : 0.f;
-    float gate[kPassRows];
-    int tok[kPassRows];
-#pragma unroll
-    for (int t = 0; t < kPassRows; ++t) {
-        gate[t] = 0.f;
-        tok[t] = 0;
-        if (!p1 && S == 1 && t < nrows) { gate[t] = P.perm_gate[it.row0 + t]; tok[t] = P.perm_token[it.row0 + t]; }
-    }
-    int acc[kBlk][G][kMaxNT][4];
-#pragma unroll
-    for (int bk = 0; bk < kBlk; ++bk)
-#pragma unroll
-        for (int q = 0; q < G; ++q)
-#pragma unroll
-            for (int j = 0; j < kMaxNT; ++j)
-#pragma unroll
-                for (int i = 0; i < 4; ++i) acc[bk][q][j][i] = 0;
-    long long cyc[2] = {0, 0};
-    gemv_mainloop<BITS, NT>(ring, bb, full, empty, stage, sphase, nst, warp, lane, acc,
-                            (g.trace && threadIdx.x == 0) ? cyc : nullptr);
-    if (g.trace && threadIdx.x == 0) {  // mainloop end; mt/ks carry the wait / compute clock cycles (/16)
-        GemvItem w = it;
-        w.mt = int(min(cyc[0] >> 4, 0xffffll));
-        w.ks = int(min(cyc[1] >> 4, 0xffffll));
-        trace_ev(g, tn, 2, 1, w);
-    }
-    if (g.dbg & 1) {  // diagnostics: keep the accumulators alive, skip the epilogue
-        int s = 0;
-#pragma unroll
-        for (int bk = 0; bk < kBlk; ++bk)
-#pragma unroll
-            for (int q = 0; q < G; ++q)
-#pragma unroll
-                for (int j = 0; j < NT; ++j)
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) s += acc[bk][q][j][i];
-        if (s == 0x7fffffff) ws[0] = s;
-        return;
-    }
-    // groups -> D * Sum_k u * digit (exact in int32 for k-chunks <= 1024), per column (warp's own rows)
-#pragma unroll
-    for (int bk = 0; bk < kBlk; ++bk)
-#pragma unroll
-        for (int j = 0; j < NT; ++j)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                int s = 0;
-#pragma unroll
-                for (int q = 0; q < G; ++q) s += FR::mult(q) * acc[bk][q][j][i];
-                ws[(32 * warp + 16 * bk + gq + 8 * (i >> 1)) * kScrCols + 8 * j + 2 * tq + (i & 1)] = s;
-            }
-    __syncwarp();
-    if (g.trace && threadIdx.x == 0) trace_ev(g, tn, 5, 1, it);
-    // digits -> D * Sum_k q * X (int64) -> y = 2^-p * that / D (fp32, one rounding)
-    const int PL = planes_of(it.phase), W = w_of(it.phase, NT);
-    const int* wr = ws + (32 * warp + r) * kScrCols;
-    float* part = g.partial + (p1 || s1 == 1 ? 0 : int64_t(s1) * g.part_rows * g.Np1);
-    long long zsum_part[kPassRows];
-#pragma unroll
-    for (int t = 0; t < kPassRows; ++t) {
-        zsum_part[t] = 0;
-        if (t >= nrows) continue;
-        const long long zs = p1 ? (long long)meta.zsum[t] : bzsum[t];
-        long long V = -(long long)FR::D * Z * zs;
-        for (int s = 0; s < PL; ++s) V += (long long)wr[s * W + t] << (8 * s);
-        const int p = meta.p[t];
-        const float y = p == kZeroRow ? 0.f : scale_pow2(V, p + LOGD);
-        const int pos = it.row0 + t;
-        if (S > 1) {
-            __stcg(part + (int64_t(it.ks) * g.part_rows + pos) * Np + ch, y);
-        } else if (p1) {
-            const int X = encode_x2(fmaxf(fmaf(y, sc, bias), 0.0f), fc2_exp<BITS>(smax, bmax, meta.l1[t]));  // ReLU
-            es.xs[(32 * warp + r) * kPassRows + t] = X;
-            zsum_part[t] = X;
-        } else {
-            fc2_finish(g, ch, y, sc, bias, gate[t], tok[t]);
-        }
-    }
-    if (g.trace && threadIdx.x == 0) trace_ev(g, tn, 5, 2, it);
-    if (p1 && S > 1 && warp == 0 && lane < nrows)  // |x|_1 per row and k-split (the last CTA bounds the fc2 exponent)
-        g.l1part[int64_t(it.row0 + lane) * s1 + it.ks] = meta.l1[lane];
-    if (p1 && S == 1) {
-        // Sum X2 per row over the 128 channels (the fc2 zero-point term of this stage)
-#pragma unroll
-        for (int t = 0; t < kPassRows; ++t) {
-            long long z = zsum_part[t];
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) z += __shfl_xor_sync(0xffffffffu, z, off);
-            if (lane == 0 && t < nrows) atomicAdd(&es.zs[t], (unsigned long long)z);
-        }
-        named_bar_sync(1, kConsumers * 32);  // all 128 channels of X2 are in xs
-        if (g.trace && threadIdx.x == 0) trace_ev(g, tn, 5, 3, it);
-        const int slot = it.slot + ks2, st2 = it.mt % kStagesPerChunk;
-        uint8_t* sl = g.xb + int64_t(slot) * g.xb_slot_bytes;
-        encode_stage<BITS>(es.xs, nrows, sl + sizeof(BufMeta) + size_t(st2 * FR::F) * nt_of(2, nrows) * 256,
-                           threadIdx.x, kConsumers * 32);
-        if (g.trace && threadIdx.x == 0) trace_ev(g, tn, 5, 4, it);
-        const int ctid = threadIdx.x;
-        if (ctid < nrows) {
-            long long* zpart = reinterpret_cast<long long*>(sl + sizeof(BufMeta) + GemvCfg<BITS>::BBUF);
-            __stcg(zpart + st2 * 8 + ctid, (long long)es.zs[ctid]);
-            es.zs[ctid] = 0;  // reused three items later (after two more barriers)
-            reinterpret_cast<BufMeta*>(sl)->p[ctid] = fc2_exp<BITS>(smax, bmax, meta.l1[ctid]);
-        }
-    }
-}
-
-// ---- publisher: release the item's global results -------------------------------------
-// fc1: fence + epoch flag of the fc2 stage; split-K items: fence + arrival
-// count; the last arriving CTA reduces the partials in fixed k order.
-template <int BITS>
-__device__ void publish_item(const GemvArgs& g, const Plan& P, const GemvItem& it, int lane, int s1, int s2,
-                             int nmt1, int nmt2, unsigned epoch, EpiSmem& es) {
-    const bool p1 = it.phase == 1;
-    const int S = p1 ? s1 : s2;
-    const int ks2 = it.mt / kStagesPerChunk;
-    if (S == 1) {
-        if (p1 && lane == 0) {
-            fence_proxy_async_global();  // the slot is read back by TMA bulk copies
-            __threadfence();             // the consumers' fragment stores (acquired through the mbarrier)
-            st_release_u32(g.xb_flag + (it.slot + ks2) * kStagesPerChunk + it.mt % kStagesPerChunk, epoch);
-        }
-        return;
-    }
-    const int maxmt = max(nmt1, nmt2);
-    unsigned* cnt = g.split_cnt + (p1 ? 0 : g.E * maxmt) + it.e * maxmt + it.mt;
-    int last = 0;
-    if (lane == 0) {
-        __threadfence();  // release the CTA's partials
-        last = atomicAdd(cnt, 1u) == unsigned(S * it.npass - 1);
-        if (last) {
-            __threadfence();  // acquire the other CTAs' partials
-            *cnt = 0;         // self-reset for the next forward
-        }
-    }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (!last) return;
-    const int Np = p1 ? g.Np1 : g.Np2;
-    const float* part = g.partial + (p1 || s1 == 1 ? 0 : int64_t(s1) * g.part_rows * g.Np1);
-    const int n = P.counts[it.e], off = P.offsets[it.e];
-    const int slot0 = it.slot - (it.row0 - off) / kPassRows * s2;  // fc2 slot of the expert's first pass
-    constexpr int NQ = TILE_N / 32;
-    float sc[NQ], bias[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) scale_bias(g, p1, it.e, it.mt * TILE_N + lane + 32 * q, sc[q], bias[q]);
-    const float smax = p1 ? __ldg(g.smax1 + it.e * s2 + ks2) : 0.f;
-    const float bmax = p1 ? __ldg(g.bmax1 + it.e * s2 + ks2) : 0.f;
-    for (int pass = 0; pass * kPassRows < n; ++pass) {
-        const int row0 = off + pass * kPassRows, nr = min(kPassRows, n - pass * kPassRows);
-        float y[NQ][kPassRows];
-#pragma unroll
-        for (int q = 0; q < NQ; ++q)
-#pragma unroll
-            for (int t = 0; t < kPassRows; ++t) y[q][t] = 0.f;
-        for (int ks = 0; ks < S; ++ks)  // fixed k order; each step's loads are independent
-#pragma unroll
-            for (int q = 0; q < NQ; ++q)
-#pragma unroll
-                for (int t = 0; t < kPassRows; ++t)
-                    if (t < nr) y[q][t] += __ldcg(part + (int64_t(ks) * g.part_rows + row0 + t) * Np + it.mt * TILE_N + lane + 32 * q);
-        if (p1) {
-            int p2[kPassRows];
-#pragma unroll
-            for (int t = 0; t < kPassRows; ++t) {
-                float l = 0.f;
-                if (t < nr)
-                    for (int ks = 0; ks < S; ++ks) l += __ldcg(g.l1part + int64_t(row0 + t) * s1 + ks);
-                p2[t] = t < nr ? fc2_exp<BITS>(smax, bmax, l * (1.0f + 0x1p-12f)) : kZeroRow;
-            }
-#pragma unroll
-            for (int q = 0; q < NQ; ++q)
-#pragma unroll
-                for (int t = 0; t < kPassRows; ++t)
-                    if (t < nr) es.xs[(lane + 32 * q) * kPassRows + t] = encode_x2(fmaxf(fmaf(y[q][t], sc[q], bias[q]), 0.f), p2[t]);
-            __syncwarp();
-            const int slot = slot0 + pass * s2 + ks2, st2 = it.mt % kStagesPerChunk;
-            uint8_t* sl = g.xb + int64_t(slot) * g.xb_slot_bytes;
-            encode_stage<BITS>(es.xs, nr, sl + sizeof(BufMeta) + size_t(st2 * Frag<BITS>::F) * nt_of(2, nr) * 256,
-                               lane, 32);
-            if (lane < nr) {
-                long long z = 0;
-                for (int c = 0; c < TILE_N; ++c) z += es.xs[c * kPassRows + lane];
-                long long* zpart = reinterpret_cast<long long*>(sl + sizeof(BufMeta) + GemvCfg<BITS>::BBUF);
-                __stcg(zpart + st2 * 8 + lane, z);
-                reinterpret_cast<BufMeta*>(sl)->p[lane] = p2[lane];
-            }
-            __syncwarp();
-            if (lane == 0) {
-                fence_proxy_async_global();
-                __threadfence();
-                st_release_u32(g.xb_flag + slot * kStagesPerChunk + st2, epoch);
-            }
-            __syncwarp();
-        } else {
-#pragma unroll
-            for (int t = 0; t < kPassRows; ++t) {
-                if (t >= nr) break;
-                const float gt = P.perm_gate[row0 + t];
-                const int tk = P.perm_token[row0 + t];
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) fc2_finish(g, it.mt * TILE_N + lane + 32 * q, y[q][t], sc[q], bias[q], gt, tk);
-            }
-        }
-    }
-}
-
-template <int BITS>
-__global__ void __launch_bounds__(kGemvThreads, 1) k_ffn_gemv(GemvArgs g, Plan P) {
-    using Cfg = GemvCfg<BITS>;
-    constexpr int SB = Cfg::SB, NST = Cfg::NST;
-    constexpr int BSTRIDE = int(sizeof(BufMeta)) + Cfg::BBUF;
-    constexpr int SCR = TILE_N * kScrCols;  // ints per scratch buffer
+    constexpr int PROD = PHASE == 1 ? kConsumers + kBuilders : kConsumers;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* ring = smem;
-    uint8_t* bbuf = ring + NST * SB;                                  // [kBBufs][meta | fragments]
-    int* scr = reinterpret_cast<int*>(bbuf + kBBufs * BSTRIDE);        // [kScrBufs][128][16]
-    EpiSmem* epi = reinterpret_cast<EpiSmem*>(scr + kScrBufs * SCR);   // [kScrBufs] (+1: the publisher's)
-    long long* bzsum = reinterpret_cast<long long*>(epi + kScrBufs + 1);  // [kBBufs][kPassRows] fc2 Sum X
-    GemvItem* pub = reinterpret_cast<GemvItem*>(bzsum + kBBufs * kPassRows);  // [kScrBufs]
-    uint64_t* full = reinterpret_cast<uint64_t*>(pub + kScrBufs);
-    uint64_t* empty = full + NST;
-    uint64_t* ifull = empty + NST;
-    uint64_t* iempty = ifull + kItemQ;
-    uint64_t* bfull = iempty + kItemQ;
-    uint64_t* bempty = bfull + kBBufs;
-    uint64_t* pfull = bempty + kBBufs;
-    uint64_t* pempty = pfull + kScrBufs;
-    GemvItem* items = reinterpret_cast<GemvItem*>(pempty + kScrBufs);
-    GemvTables& TBL = *reinterpret_cast<GemvTables*>(items + kItemQ);
+    uint8_t* bufs = ring + L::RING;                                   // [kBufs][head | fragments]
+    int* scr = reinterpret_cast<int*>(bufs + L::BUFS);                 // [128][16]
+    long long* red = reinterpret_cast<long long*>(reinterpret_cast<uint8_t*>(scr) + L::SCR);  // [CS][128][4]
+    int* xs = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(red) + L::RED);  // fc1: [128][4] + zs[4]
+    long long* zs = reinterpret_cast<long long*>(xs + TILE_N * kPassRows);
+    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(xs) + L::XS);
+    uint64_t* empty = full + NU;
+    uint64_t* bfull = empty + NU;
+    uint64_t* bempty = bfull + kBufs;
+    uint64_t* red_full = bempty + kBufs;   // rank 0: every rank's partials landed
+    uint64_t* red_empty = red_full + 1;    // rank r: rank 0 consumed the previous partials
+    GemvTables& TBL = *reinterpret_cast<GemvTables*>(red_empty + 1);
     __shared__ unsigned s_tn;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const unsigned long long t_entry = gtime_ns();
+    const int CS = int(cluster_nctas()), rank = int(cta_rank());
+    const int Kp = PHASE == 1 ? g.Kp1 : g.Kp2;
+    const int Np = PHASE == 1 ? g.Np1 : g.Np2;
+    const int k0 = rank * kChunkK, nst = (min(kChunkK, Kp - k0) + kStageK - 1) / kStageK;
+    const int nunits = (nst + US - 1) / US;
     if (threadIdx.x == 0) {
         s_tn = 0;
-        for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kConsumers); }
-        for (int q = 0; q < kItemQ; ++q) { mbar_init(&ifull[q], 1); mbar_init(&iempty[q], kConsumers + kBuilders + 1); }
-        for (int b = 0; b < kBBufs; ++b) { mbar_init(&bfull[b], 1); mbar_init(&bempty[b], kConsumers); }
-        for (int b = 0; b < kScrBufs; ++b) { mbar_init(&pfull[b], kConsumers); mbar_init(&pempty[b], 1); }
+        for (int s = 0; s < NU; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kConsumers); }
+        for (int b = 0; b < kBufs; ++b) { mbar_init(&bfull[b], 1); mbar_init(&bempty[b], kConsumers); }
+        mbar_init(red_full, kConsumers * CS);
+        mbar_init(red_empty, 1);
+        if (PHASE == 1) for (int t = 0; t < kPassRows; ++t) zs[t] = 0;
+        fence_barrier_init();
     }
-    for (int i = threadIdx.x; i < (kScrBufs + 1) * kPassRows; i += blockDim.x) epi[i / kPassRows].zs[i % kPassRows] = 0;
-    if (threadIdx.x == 0) fence_barrier_init();
-    __syncthreads();
-    pdl_wait();  // routing plan of the preceding grid
+    if (PHASE == 1) pdl_wait();  // routing plan (fc2: the plan is older than fc1's own wait)
     const int n_gemv = P.meta[0];
-    if (n_gemv == 0) return;
-    const unsigned epoch = unsigned(P.meta[5]);
-    if (threadIdx.x == 0 && g.trace) {  // CTA entry (before the PDL wait) and after it
-        const unsigned i = atomicAdd(&s_tn, 1u);
-        g.trace[(size_t(blockIdx.x) * kTraceCap + i) * 2] = t_entry;
-        g.trace[(size_t(blockIdx.x) * kTraceCap + i) * 2 + 1] = 3ull << 60 | 1ull << 56;
-        trace_ev(g, &s_tn, 3, 0, GemvItem{});
-    }
-    const int nmt1 = g.Np1 / TILE_N, nmt2 = g.Np2 / TILE_N;
-    const int s1 = gemv_ksplit_c(g.Kp1), s2 = gemv_ksplit_c(g.Kp2);
+    const int nmt = Np / TILE_N;
+    if (warp == 0 && n_gemv > 0) build_tables(TBL, P, n_gemv, nmt, lane);
+    __syncthreads();
+    cluster_sync();  // barriers of every CTA initialised before any remote arrive
+    if (PHASE == 1) pdl_trigger();  // the fc2 grid may launch as CTAs of this grid retire
+    const int nitems = n_gemv > 0 ? TBL.start[n_gemv] : 0;
+    const int clu = int(blockIdx.x) / CS, nclu = int(gridDim.x) / CS;
+    const int nchunk2 = (g.Kp2 + kChunkK - 1) / kChunkK;
+    // trace rows: fc1 events in the first half of each CTA row, fc2 in the second
+    unsigned long long* tr = g.trace ? g.trace + (PHASE == 2 ? kTraceCap : 0) : nullptr;
 
-    if (warp == kProducer) {
-        // ===== producer: item tables, tickets (one atomic in flight ahead), weight tiles
-        unsigned ticket = 0;
-        if (lane == 0) ticket = atomicAdd(&P.tickets[1], 1u);  // latency overlaps the table build
-        for (int a = lane; a < n_gemv; a += 32) {
-            const int e = P.gemv_list[a];
-            TBL.list[a] = e;
-            TBL.cnt[a] = P.counts[e];
-            TBL.off[a] = P.offsets[e];
+    if (warp == PROD) {
+        // ===== producer: weight copy units (+ fc2: the fragment slot of each item)
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            bool waited = PHASE == 1;
+            int slot = 0, sph = 0, seq = 0;
+            const uint8_t* wbase0 = PHASE == 1 ? g.w1 : g.w2;
+            const int64_t wstride = PHASE == 1 ? g.w1_stride : g.w2_stride;
+            for (int i = clu; i < nitems; i += nclu, ++seq) {
+                const GemvItem it = item_at(i, TBL, n_gemv, nmt);
+                if (PHASE == 2 && seq > 0) {
+                    const int buf = seq % kBufs;
+                    mbar_wait(&bempty[buf], ((seq / kBufs) & 1) ^ 1);
+                    const uint32_t bytes = uint32_t(kHead + F * nt_of(2, it.nrows) * 256 * nst);
+                    mbar_arrive_expect_tx(&bfull[buf], bytes);
+                    bulk_g2s(bufs + size_t(buf) * (kHead + C::BBUF),
+                             g.xb + (int64_t(it.gp) * nchunk2 + rank) * g.xb_slot_bytes, bytes, &bfull[buf]);
+                }
+                const uint8_t* wb = wbase0 + int64_t(it.e) * wstride + (int64_t(it.mt) * (Kp / TILE_K) + k0 / TILE_K) * TB;
+                for (int u = 0; u <= nunits; ++u) {
+                    // fc2, first item: its weights stream while fc1 finishes; the fragment
+                    // slot (written by fc1) is fetched once the ring is full or the item issued
+                    if (PHASE == 2 && seq == 0 && !waited && (u == nunits || u == NU)) {
+                        pdl_wait();
+                        waited = true;
+                        const uint32_t bytes = uint32_t(kHead + F * nt_of(2, it.nrows) * 256 * nst);
+                        mbar_arrive_expect_tx(&bfull[0], bytes);
+                        bulk_g2s(bufs, g.xb + (int64_t(it.gp) * nchunk2 + rank) * g.xb_slot_bytes, bytes, &bfull[0]);
+                    }
+                    if (u == nunits) break;
+                    const int bytes = min(US, nst - u * US) * SB;
+                    mbar_wait(&empty[slot], sph ^ 1);
+                    mbar_arrive_expect_tx(&full[slot], uint32_t(bytes));
+                    bulk_g2s_hint(ring + size_t(slot) * UB, wb + int64_t(u) * UB, uint32_t(bytes), &full[slot], pol);
+                    if (++slot == NU) { slot = 0; sph ^= 1; }
+                }
+            }
+            if (!waited) pdl_wait();
         }
         __syncwarp();
-        if (lane != 0) return;
-        {
-            int t1 = 0, t2 = 0, tp = 0;
-            for (int a = 0; a < n_gemv; ++a) {
-                const int np = (TBL.cnt[a] + kPassRows - 1) / kPassRows;
-                TBL.pst[a] = tp;
-                TBL.start1[a] = t1;
-                TBL.start2[a] = t2;
-                tp += np;
-                t1 += nmt1 * s1 * np;
-                t2 += nmt2 * s2 * np;
-            }
-            TBL.pst[n_gemv] = tp;
-            TBL.start1[n_gemv] = t1;
-            TBL.start2[n_gemv] = t2;
-        }
-        const uint64_t pol = policy_evict_first();
-        int stage = 0, sphase = 0, q = 0, qphase = 0;
-        for (;;) {
-            const GemvItem it = decode_item(ticket, TBL, n_gemv, nmt1, s1, nmt2, s2);
-            trace_ev(g, &s_tn, 0, 0, it);
-            mbar_wait(&iempty[q], qphase ^ 1);
-            items[q] = it;
-            mbar_arrive(&ifull[q]);
-            if (++q == kItemQ) { q = 0; qphase ^= 1; }
-            if (it.phase == 0) break;
-            ticket = atomicAdd(&P.tickets[1], 1u);  // next ticket while this item's weights stream
-            const bool p1 = it.phase == 1;
-            const int Kp = p1 ? g.Kp1 : g.Kp2;
-            const int k0 = it.ks * kGemvKC, klen = min(kGemvKC, Kp - k0);
-            const int kbs = Kp / TILE_K;
-            const uint8_t* base = (p1 ? g.w1 + int64_t(it.e) * g.w1_stride : g.w2 + int64_t(it.e) * g.w2_stride) +
-                                  (int64_t(it.mt) * kbs + k0 / TILE_K) * Cfg::TB;
-            for (int s = 0; s < klen / kStageK; ++s) {  // 2 consecutive tiles are contiguous
-                mbar_wait(&empty[stage], sphase ^ 1);
-                mbar_arrive_expect_tx(&full[stage], SB);
-                bulk_g2s_hint(ring + stage * SB, base + int64_t(s) * SB, SB, &full[stage], pol);
-                if (++stage == NST) { stage = 0; sphase ^= 1; }
-            }
-            trace_ev(g, &s_tn, 0, 1, it);
-        }
-        return;
-    }
-
-    if (warp == kPublisher) {
-        // ===== publisher: fences, ready flags, split-K arrivals (in item order)
-        int ps = 0, pph = 0;
-        for (;;) {
-            mbar_wait(&pfull[ps], pph);
-            const GemvItem it = pub[ps];
-            if (it.phase == 0) break;
-            if (lane == 0) trace_ev(g, &s_tn, 4, 1, it);
-            publish_item<BITS>(g, P, it, lane, s1, s2, nmt1, nmt2, epoch, epi[kScrBufs]);
-            if (lane == 0) trace_ev(g, &s_tn, 4, 0, it);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&pempty[ps]);
-            if (++ps == kScrBufs) { ps = 0; pph ^= 1; }
-        }
-        return;
-    }
-
-    if (warp == kLoader) {
-        // ===== loader: fc2 items: fragment slot (all stages ready) -> smem buffer, in item order
-        int q = 0, qphase = 0, bseq = 0;
-        for (;;) {
-            mbar_wait(&ifull[q], qphase);
-            const GemvItem it = items[q];
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&iempty[q]);
-            if (++q == kItemQ) { q = 0; qphase ^= 1; }
-            if (it.phase == 0) break;
-            const int buf = bseq % kBBufs;
-            if (it.phase == 2) {
-                if (lane == 0) mbar_wait(&bempty[buf], ((bseq / kBBufs) & 1) ^ 1);
-                __syncwarp();
-                const int nst = min(kGemvKC, g.Kp2 - it.ks * kGemvKC) / kStageK;
-                // lane (stage st, row t): acquire the stage flag, then its Sum X part
-                const int st = lane >> 2, t = lane & 3;
-                long long z = 0;
-                if (st < nst) {
-                    while (ld_acquire_u32(g.xb_flag + it.slot * kStagesPerChunk + st) != epoch) __nanosleep(32);
-                    if (t < it.nrows)
-                        z = __ldcg(reinterpret_cast<const long long*>(g.xb + int64_t(it.slot) * g.xb_slot_bytes +
-                                                                      sizeof(BufMeta) + Cfg::BBUF) + st * 8 + t);
-                }
-#pragma unroll
-                for (int off = 4; off < 32; off <<= 1) z += __shfl_xor_sync(0xffffffffu, z, off);
-                if (lane < kPassRows) bzsum[buf * kPassRows + lane] = z;
-                __syncwarp();
-                if (lane == 0) {
-                    fence_proxy_async_global();
-                    trace_ev(g, &s_tn, 1, 2, it);
-                    const uint32_t bytes = uint32_t(sizeof(BufMeta) + nst * Cfg::F * nt_of(2, it.nrows) * 256);
-                    mbar_arrive_expect_tx(&bfull[buf], bytes);
-                    bulk_g2s(bbuf + buf * BSTRIDE, g.xb + int64_t(it.slot) * g.xb_slot_bytes, bytes, &bfull[buf]);
-                }
-            }
-            __syncwarp();
-            ++bseq;
-        }
-        return;
-    }
-
-    if (warp >= kConsumers) {
-        // ===== builders (warps 8..10): builder b fills buffer b, i.e. every kBBufs-th weight item (fc1)
+    } else if (PHASE == 1 && warp >= kConsumers) {
+        // ===== builders: builder b fills fragment buffer b (every kBufs-th item)
         const int bw = warp - kConsumers;
         const bool vec_h = g.h_f16 && (g.d % 8) == 0 && (reinterpret_cast<uintptr_t>(g.h) & 15) == 0;
-        int q = 0, qphase = 0, bseq = 0;
-        for (;;) {
-            mbar_wait(&ifull[q], qphase);
-            const GemvItem it = items[q];
+        int seq = bw;
+        for (int i = clu + bw * nclu; i < nitems; i += kBufs * nclu, seq += kBufs) {
+            const GemvItem it = item_at(i, TBL, n_gemv, nmt);
+            if (lane == 0) mbar_wait(&bempty[bw], ((seq / kBufs) & 1) ^ 1);
             __syncwarp();
-            if (lane == 0) mbar_arrive(&iempty[q]);
-            if (++q == kItemQ) { q = 0; qphase ^= 1; }
-            if (it.phase == 0) break;
-            const int buf = bseq % kBBufs;
-            if (it.phase == 1 && buf == bw) {
-                if (lane == 0) mbar_wait(&bempty[buf], ((bseq / kBBufs) & 1) ^ 1);
+            uint8_t* b = bufs + size_t(bw) * (kHead + C::BBUF);
+            Head& hd = *reinterpret_cast<Head*>(b);
+            for (int t = 0; t < it.nrows; ++t) build_row<BITS>(g, P, it, t, lane, vec_h, k0, nst, b + kHead, hd);
+            __syncwarp();
+            if (lane == 0) {
+                trace_ev(tr, &s_tn, 1, 1, it, PHASE);
+                mbar_arrive(&bfull[bw]);
+            }
+        }
+    } else if (warp < kConsumers) {
+        // ===== consumers: warp -> m16 block (16 channels) of the 128-channel item
+        const int r = lane & 15;  // epilogue: lane -> channel 16 warp + r, rows (lane >> 4) + 2 u
+        const uint32_t red_rank0 = map_rank(red, 0), full_rank0 = map_rank(red_full, 0);
+        int slot = 0, sph = 0, seq = 0;
+        for (int i = clu; i < nitems; i += nclu, ++seq) {
+            const GemvItem it = item_at(i, TBL, n_gemv, nmt);
+            const int buf = seq % kBufs;
+            const int ch = it.mt * TILE_N + 16 * warp + r;
+            float sc = 0.f, bias = 0.f, gate[2] = {0.f, 0.f};  // epilogue operands, fetched early
+            int tok[2] = {0, 0};
+            float smax = 0.f, bmax = 0.f;
+            if (rank == 0) {
+                scale_bias(PHASE == 1 ? g.s1 : g.s2, PHASE == 1 ? g.b1 : g.b2, int64_t(it.e) * Np + ch, sc, bias);
+                if (PHASE == 1) { smax = __ldg(g.smax1 + it.e); bmax = __ldg(g.bmax1 + it.e); }
+                if (PHASE == 2)
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int t = (lane >> 4) + 2 * u;
+                        if (t < it.nrows) { gate[u] = P.perm_gate[it.row0 + t]; tok[u] = P.perm_token[it.row0 + t]; }
+                    }
+            }
+            mbar_wait(&bfull[buf], (seq / kBufs) & 1);
+            if (threadIdx.x == 0) trace_ev(tr, &s_tn, 2, 0, it, PHASE);
+            const uint8_t* bb = bufs + size_t(buf) * (kHead + C::BBUF);
+            const Head& hd = *reinterpret_cast<const Head*>(bb);
+            const int NT = nt_of(PHASE, it.nrows);
+            int acc[G][kMaxNT][4];
+#pragma unroll
+            for (int a = 0; a < G; ++a)
+#pragma unroll
+                for (int j = 0; j < kMaxNT; ++j)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) acc[a][j][q] = 0;
+            const int r0 = 16 * warp + (lane >> 2);
+            for (int u = 0; u < nunits; ++u) {
+                mbar_wait(&full[slot], sph);
+                const uint8_t* U = ring + size_t(slot) * UB;
+                const int ns = min(US, nst - u * US);
+                if (NT == 1) unit_mma<BITS, 1>(U, ns, u * US, r0, lane, bb + kHead, acc);
+                else unit_mma<BITS, 2>(U, ns, u * US, r0, lane, bb + kHead, acc);
                 __syncwarp();
-                BufMeta& bm = *reinterpret_cast<BufMeta*>(bbuf + buf * BSTRIDE);
-                for (int t = 0; t < it.nrows; ++t)
-                    build_row<BITS>(g, P, it, t, lane, vec_h, bbuf + buf * BSTRIDE + sizeof(BufMeta), bm);
-                __syncwarp();
-                if (lane == 0) {
-                    trace_ev(g, &s_tn, 1, 1, it);
-                    mbar_arrive(&bfull[buf]);
+                if (lane == 0) mbar_arrive(&empty[slot]);
+                if (++slot == NU) { slot = 0; sph ^= 1; }
+            }
+            if (threadIdx.x == 0) trace_ev(tr, &s_tn, 2, 1, it, PHASE);
+            // groups -> D * Sum_k u * digit per (row, column) (exact in int32 for 1024-k chunks)
+            {
+                const int tq = lane & 3, gq = lane >> 2;
+#pragma unroll
+                for (int j = 0; j < kMaxNT; ++j) {
+                    if (j >= NT) break;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        int s = 0;
+#pragma unroll
+                        for (int a = 0; a < G; ++a) s += FR::mult(a) * acc[a][j][q];
+                        scr[(16 * warp + gq + 8 * (q >> 1)) * kScrCols + 8 * j + 2 * tq + (q & 1)] = s;
+                    }
                 }
             }
-            ++bseq;
-        }
-        return;
-    }
-
-    // ===== consumers (warps 0..7): mainloop + epilogue -> publisher
-    int stage = 0, sphase = 0, q = 0, qphase = 0, bseq = 0, ps = 0, pph = 0;
-    for (;;) {
-        mbar_wait(&ifull[q], qphase);
-        const GemvItem it = items[q];
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&iempty[q]);
-        if (++q == kItemQ) { q = 0; qphase ^= 1; }
-        if (lane == 0) mbar_wait(&pempty[ps], pph ^ 1);  // publisher slot ps is free
-        __syncwarp();
-        if (it.phase != 0) {
-            const int buf = bseq % kBBufs;
-            if (!(g.dbg & 2)) mbar_wait(&bfull[buf], (bseq / kBBufs) & 1);
-            if (threadIdx.x == 0) trace_ev(g, &s_tn, 2, 0, it);
-            const BufMeta& bm = *reinterpret_cast<const BufMeta*>(bbuf + buf * BSTRIDE);
-            const uint8_t* bb = bbuf + buf * BSTRIDE + sizeof(BufMeta);
-            const long long* bz = bzsum + buf * kPassRows;
-            int* ws = scr + ps * SCR;
-            if (nt_of(it.phase, it.nrows) == 1)
-                consume_item<BITS, 1>(g, P, it, ring, bb, bm, bz, full, empty, stage, sphase, ws, epi[ps], s1, s2, &s_tn);
-            else
-                consume_item<BITS, 2>(g, P, it, ring, bb, bm, bz, full, empty, stage, sphase, ws, epi[ps], s1, s2, &s_tn);
             __syncwarp();
-            if (lane == 0) mbar_arrive(&bempty[buf]);
-            if (threadIdx.x == 0) trace_ev(g, &s_tn, 2, 2, it);
-            ++bseq;
-        } else if (threadIdx.x == 0) {
-            trace_ev(g, &s_tn, 2, 3, it);
+            // this chunk's exact partial: V = Sum_s 256^s S_s - D Z Sum X (int64) -> rank 0
+            const int PL = planes_of(PHASE), W = w_of(PHASE, NT);
+            const int* wr = scr + (16 * warp + r) * kScrCols;
+            if (lane == 0 && rank != 0) wait_cluster(red_empty, (seq & 1) ^ 1);  // rank 0 took the previous item
+            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int t = (lane >> 4) + 2 * u;
+                if (t >= it.nrows) continue;
+                long long zsum = 0;
+                if (PHASE == 1) {
+                    zsum = hd.zsum[t];
+                } else {
+                    for (int st = 0; st < nst; ++st) zsum += hd.zpart[st][t];
+                }
+                long long V = -(long long)FR::D * Z * zsum;
+                for (int s = 0; s < PL; ++s) V += (long long)wr[s * W + t] << (8 * s);
+                const int idx = ((rank * TILE_N) + 16 * warp + r) * kPassRows + t;
+                if (rank == 0) red[idx] = V;
+                else st_cluster_s64(red_rank0 + uint32_t(idx) * 8u, V);
+            }
+            // exponents needed by rank 0 after the buffer is recycled
+            int pe[2] = {kZeroRow, kZeroRow};
+            float l1e[2] = {0.f, 0.f};
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int t = (lane >> 4) + 2 * u;
+                if (t < it.nrows) { pe[u] = hd.p[t]; l1e[u] = PHASE == 1 ? hd.l1[t] : 0.f; }
+            }
+            const float l1row = (PHASE == 1 && threadIdx.x < it.nrows) ? hd.l1[threadIdx.x] : 0.f;
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&bempty[buf]);
+                arrive_cluster(full_rank0);  // this warp's partials are in rank 0's smem
+            }
+            if (threadIdx.x == 0) trace_ev(tr, &s_tn, 2, 3, it, PHASE);
+            if (rank != 0) continue;
+            // ===== rank 0: reduce the cluster's partials and finish the item
+            wait_cluster(red_full, seq & 1);
+            if (threadIdx.x == 0) trace_ev(tr, &s_tn, 2, 4, it, PHASE);
+            float y[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int t = (lane >> 4) + 2 * u;
+                long long V = 0;
+                if (t < it.nrows)
+                    for (int c = 0; c < CS; ++c) V += red[((c * TILE_N) + 16 * warp + r) * kPassRows + t];
+                y[u] = (t >= it.nrows || pe[u] == kZeroRow) ? 0.f : scale_pow2(V, pe[u] + LOGD);
+            }
+            named_bar_sync(1, kConsumers * 32);  // every warp read red
+            if (threadIdx.x == 0) trace_ev(tr, &s_tn, 2, 6, it, PHASE);
+            if (threadIdx.x < CS && threadIdx.x > 0) arrive_cluster(map_rank(red_empty, threadIdx.x));
+            if (PHASE == 2) {
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int t = (lane >> 4) + 2 * u;
+                    if (t < it.nrows && ch < g.d) {
+                        const float yg = fmaf(y[u], sc, bias) * gate[u];
+                        const int64_t o = int64_t(tok[u]) * g.d + ch;
+                        if (g.out_acc) atomicAdd(g.out_acc + o, yg);  // top-2: two addends onto zero
+                        else if (g.out_f16) static_cast<__half*>(g.out)[o] = __float2half_rn(yg);
+                        else static_cast<float*>(g.out)[o] = yg;
+                    }
+                }
+            } else {
+                // mid = ReLU(y s + b) in fc2 fixed point -> fc2 fragment stage mt % 8 of slot (pass, mt / 8)
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int t = (lane >> 4) + 2 * u;
+                    long long X2 = 0;
+                    if (t < it.nrows) {
+                        const int p2 = fc2_exp<BITS>(smax, bmax, l1e[u]);
+                        const float mid = fmaxf(fmaf(y[u], sc, bias), 0.0f);  // ReLU, model.cpp:190
+                        X2 = p2 == kZeroRow ? 0 : __float2int_rn(ldexpf(mid, p2));
+                        xs[(16 * warp + r) * kPassRows + t] = int(X2);
+                    }
+#pragma unroll
+                    for (int off = 1; off < 16; off <<= 1) X2 += __shfl_xor_sync(0xffffffffu, X2, off);
+                    if (r == 0 && t < it.nrows)
+                        atomicAdd(reinterpret_cast<unsigned long long*>(&zs[t]), (unsigned long long)X2);
+                }
+                named_bar_sync(1, kConsumers * 32);  // all 128 channels of X2 are in xs
+                if (threadIdx.x == 0) trace_ev(tr, &s_tn, 2, 5, it, PHASE);
+                const int NT2 = nt_of(2, it.nrows), W2 = w_of(2, NT2);
+                uint8_t* sl = g.xb + (int64_t(it.gp) * nchunk2 + it.mt / kChunkStages) * g.xb_slot_bytes;
+                const int st2 = it.mt % kChunkStages;
+                uint8_t* bstage = sl + kHead + size_t(st2 * F) * NT2 * 256;
+                const int nwords = it.nrows * 4 * 4 * F;
+                for (int wd = threadIdx.x; wd < nwords; wd += kConsumers * 32) {
+                    const int f = wd % F, s = (wd / F) & 3, tq = (wd / (4 * F)) & 3, t = wd / (16 * F);
+                    uint32_t b[2];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        uint32_t word = 0;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const int k = FR::kidx(f, h, q);  // tile * 16 + code
+                            const int X = xs[(64 * (k >> 4) + 16 * tq + (k & 15)) * kPassRows + t];
+                            word |= ((((uint32_t(X) + 0x80808080u) ^ 0x80808080u) >> (8 * s)) & 0xffu) << (8 * q);
+                        }
+                        b[h] = word;
+                    }
+                    const int col = s * W2 + t, j = col >> 3, gq = col & 7;
+                    __stcg(reinterpret_cast<uint2*>(bstage + (size_t(f) * NT2 + j) * 256 + (4 * gq + tq) * 8),
+                           make_uint2(b[0], b[1]));
+                }
+                if (threadIdx.x == 0) trace_ev(tr, &s_tn, 2, 7, it, PHASE);
+                if (threadIdx.x < it.nrows) {
+                    const int t = threadIdx.x;
+                    Head* gh = reinterpret_cast<Head*>(sl);
+                    gh->zpart[st2][t] = zs[t];
+                    gh->p[t] = fc2_exp<BITS>(smax, bmax, l1row);  // the same value from every m-tile
+                }
+                named_bar_sync(1, kConsumers * 32);  // xs / zs reuse
+                if (threadIdx.x < kPassRows) zs[threadIdx.x] = 0;
+            }
+            if (threadIdx.x == 0) trace_ev(tr, &s_tn, 2, 2, it, PHASE);
         }
-        if (warp == 0 && lane == 0) pub[ps] = it;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&pfull[ps]);  // release: this warp's global results of the item
-        if (++ps == kScrBufs) { ps = 0; pph ^= 1; }
-        if (it.phase == 0) break;
     }
+    cluster_sync();  // no CTA leaves while a peer may still write its shared memory
 }
 
+// ---- launch -----------------------------------------------------------------------------
 namespace {
-template <int BITS>
-size_t gemv_smem() {
-    using Cfg = GemvCfg<BITS>;
-    return size_t(Cfg::NST) * Cfg::SB + kBBufs * (sizeof(BufMeta) + size_t(Cfg::BBUF)) +
-           size_t(kScrBufs) * TILE_N * kScrCols * 4 + (kScrBufs + 1) * sizeof(EpiSmem) +
-           kBBufs * kPassRows * 8 + kScrBufs * sizeof(GemvItem) +
-           (2 * Cfg::NST + 2 * kItemQ + 2 * kBBufs + 2 * kScrBufs) * 8 + kItemQ * sizeof(GemvItem) +
-           sizeof(GemvTables) + 64;
+template <class K>
+int active_clusters(K kern, int cs, size_t smem, int threads, int num_sms) {
+    if (cs == 1) return num_sms;
+    cudaLaunchConfig_t q{};
+    q.gridDim = dim3(unsigned(num_sms / cs * cs));
+    q.blockDim = dim3(threads);
+    q.dynamicSmemBytes = smem;
+    cudaLaunchAttribute qa[1];
+    qa[0].id = cudaLaunchAttributeClusterDimension;
+    qa[0].val.clusterDim.x = cs;
+    qa[0].val.clusterDim.y = 1;
+    qa[0].val.clusterDim.z = 1;
+    q.attrs = qa;
+    q.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &q) != cudaSuccess || n <= 0) n = num_sms / cs;
+    return std::min(n, num_sms / cs);
+}
+
+template <int BITS, int PHASE>
+cudaError_t launch_phase(const GemvArgs& g, const Plan& P, cudaStream_t st, int num_sms) {
+    using L = Layout<BITS, PHASE>;
+    auto kern = k_gemv<BITS, PHASE>;
+    const int Kp = PHASE == 1 ? g.Kp1 : g.Kp2;
+    const int cs = (Kp + kChunkK - 1) / kChunkK;
+    static bool configured = false;
+    static int ncl[kMaxCluster + 1] = {0};
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::TOTAL));
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    if (ncl[cs] == 0) ncl[cs] = active_clusters(kern, cs, L::TOTAL, threads_of(PHASE), num_sms);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(ncl[cs] * cs));
+    cfg.blockDim = dim3(threads_of(PHASE));
+    cfg.dynamicSmemBytes = L::TOTAL;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(cs);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    return cudaLaunchKernelEx(&cfg, kern, g, P);
 }
 
 template <int BITS>
 cudaError_t launch_gemv_t(const GemvArgs& g, const Plan& P, cudaStream_t st, int num_sms) {
-    auto kern = k_ffn_gemv<BITS>;
-    const size_t smem = gemv_smem<BITS>();
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
-    return launch_pdl(kern, dim3(num_sms), dim3(kGemvThreads), smem, st, g, P);
+    cudaError_t e = launch_phase<BITS, 1>(g, P, st, num_sms);
+    if (e != cudaSuccess) return e;
+    return launch_phase<BITS, 2>(g, P, st, num_sms);
 }
 }  // namespace
 
-int gemv_ksplit(int Kp) { return gemv_ksplit_c(Kp); }
-// fc2 fragment slot: [meta | fragments (4 planes) | Sum X per (stage, row)]
+bool gemv_supported(int Kp1, int Kp2) {
+    return Kp1 <= kMaxCluster * kChunkK && Kp2 <= kMaxCluster * kChunkK && Kp2 >= kStageK;
+}
 int64_t gemv_xb_slot_bytes(int bits) {
-    const int64_t tail = 8 * 8 * sizeof(long long);
     switch (bits) {
-        case 2: return sizeof(BufMeta) + GemvCfg<2>::BBUF + tail;
-        case 3: return sizeof(BufMeta) + GemvCfg<3>::BBUF + tail;
-        case 4: return sizeof(BufMeta) + GemvCfg<4>::BBUF + tail;
+        case 2: return Cfg<2>::SLOT;
+        case 3: return Cfg<3>::SLOT;
+        case 4: return Cfg<4>::SLOT;
     }
-    return sizeof(BufMeta) + GemvCfg<8>::BBUF + tail;
+    return Cfg<8>::SLOT;
 }
-// upper bound on row passes: every listed expert may end in a partial pass
-int64_t gemv_xb_passes(int64_t rows, int E) { return (rows + kPassRows - 1) / kPassRows + E; }
-int gemv_stages_per_chunk() { return kStagesPerChunk; }
-
-// Partial-sum buffer size (floats) for `rows` GEMV rows.
-int64_t gemv_partial_floats(int64_t rows, int Kp1, int Np1, int Kp2, int Np2) {
-    const int s1 = gemv_ksplit_c(Kp1), s2 = gemv_ksplit_c(Kp2);
-    return (s1 > 1 ? int64_t(s1) * rows * Np1 : 0) + int64_t(s2) * rows * Np2;
+// every listed expert may end in a partial pass; one slot per (pass, 1024-k chunk of fc2)
+int64_t gemv_xb_slots(int64_t rows, int E, int Kp2) {
+    return ((rows + kPassRows - 1) / kPassRows + E) * ((Kp2 + kChunkK - 1) / kChunkK);
 }
 
-cudaError_t launch_gemv(int bits, bool, const GemvArgs& g, const Plan& P, cudaStream_t st, int num_sms) {
+cudaError_t launch_gemv(int bits, const GemvArgs& g, const Plan& P, cudaStream_t st, int num_sms) {
+    if (!gemv_supported(g.Kp1, g.Kp2)) return cudaErrorInvalidValue;
     switch (bits) {
         case 2: return launch_gemv_t<2>(g, P, st, num_sms);
         case 3: return launch_gemv_t<3>(g, P, st, num_sms);
@@ -890,13 +743,13 @@ cudaError_t launch_gemv(int bits, bool, const GemvArgs& g, const Plan& P, cudaSt
     return cudaErrorInvalidValue;
 }
 
-// Per (expert, fc2 k-chunk): max fc1 scale and max |fc1 bias| over the chunk's
-// channels — the constants of the fc2 fixed-point bound (bank creation).
-__global__ void k_chunk_max(const float* __restrict__ s1, const float* __restrict__ b1, int Np1, float* smax,
-                            float* bmax) {
-    const int e = blockIdx.x, ks = blockIdx.y, n0 = ks * kGemvKC;
+// Per expert: max fc1 scale and max |fc1 bias| — the constants of the fc2
+// fixed-point bound (bank creation).
+__global__ void k_expert_max(const float* __restrict__ s1, const float* __restrict__ b1, int Np1, float* smax,
+                             float* bmax) {
+    const int e = blockIdx.x;
     float ms = 0.f, mb = 0.f;
-    for (int n = n0 + threadIdx.x; n < min(n0 + kGemvKC, Np1); n += blockDim.x) {
+    for (int n = threadIdx.x; n < Np1; n += blockDim.x) {
         ms = fmaxf(ms, fabsf(s1[int64_t(e) * Np1 + n]));
         if (b1) mb = fmaxf(mb, fabsf(b1[int64_t(e) * Np1 + n]));
     }
@@ -909,14 +762,14 @@ __global__ void k_chunk_max(const float* __restrict__ s1, const float* __restric
     __syncthreads();
     if (threadIdx.x == 0) {
         for (int w = 1; w < int(blockDim.x >> 5); ++w) { ms = fmaxf(ms, red[0][w]); mb = fmaxf(mb, red[1][w]); }
-        smax[e * gridDim.y + ks] = ms;
-        bmax[e * gridDim.y + ks] = mb;
+        smax[e] = ms;
+        bmax[e] = mb;
     }
 }
 
-cudaError_t launch_chunk_max(const float* s1, const float* b1, int E, int Np1, int Kp2, float* smax, float* bmax,
-                             cudaStream_t st) {
-    k_chunk_max<<<dim3(E, gemv_ksplit_c(Kp2)), 256, 0, st>>>(s1, b1, Np1, smax, bmax);
+cudaError_t launch_expert_max(const float* s1, const float* b1, int E, int Np1, float* smax, float* bmax,
+                              cudaStream_t st) {
+    k_expert_max<<<E, 256, 0, st>>>(s1, b1, Np1, smax, bmax);
     return cudaGetLastError();
 }
 

@@ -55,6 +55,9 @@ cudaError_t launch_scatter(const void* h, int h_f16, int64_t T, int d, int topk,
 moqe_status retile(const uint8_t* src, int64_t K, int64_t N, int bits, int n_mats, uint8_t* dst,
                    int64_t Kp, int64_t Np, cudaStream_t st);
 
+// Decode path (ffn_gemv.cu): two persistent weight-streaming kernels chained
+// with programmatic dependent launch — fc1 (expert rows -> ReLU -> fc2's
+// fixed-point fragments in global memory) and fc2 (-> gate-weighted output).
 struct GemvArgs {
     const void* h;
     int h_f16;
@@ -68,33 +71,24 @@ struct GemvArgs {
     const float* b1;               // [E][Np1] or null
     const float* b2;               // [E][Np2] or null
     int Kp1, Np1, Kp2, Np2;
-    __half* mid;                   // [R][Np1]
     void* out;                     // [T][d] (top-1 direct store)
     int out_f16;
-    float* out_acc;                // [T][d] fp32 (top-2 accumulation) or null
-    float* partial;                // split-K partials: phase1 [S1][R][Np1], phase2 [S2][R][Np2]
-    int64_t part_rows;             // R capacity
-    unsigned* split_cnt;           // [2][E][max(Nmt)]
-    uint8_t* xb;                   // fc2 activation digit fragments, one slot per (row pass, fc2 k-chunk)
-    unsigned* xb_flag;             // [slots][8 stages] forward epoch when the stage is written
+    float* out_acc;                // [T][d] fp32 (top-2 accumulation, 2 addends per element) or null
+    uint8_t* xb;                   // fc2 activation fragments: one slot per (row pass, 1024-k chunk)
     int64_t xb_slot_bytes;
-    const float* smax1;            // [E][fc2 k-chunks] max fc1 scale over the chunk's channels
-    const float* bmax1;            // [E][fc2 k-chunks] max |fc1 bias| over the chunk's channels
-    float* l1part;                 // [rows][fc1 k-splits] |x|_1 per row and split (d > 1024 only)
+    const float* smax1;            // [E] max fc1 scale (bounds the fc2 fixed-point exponent)
+    const float* bmax1;            // [E] max |fc1 bias|
     unsigned long long* trace;     // [grid][kTraceCap][2] (time ns, event) or null
-    int dbg;                       // diagnostics only (env MOQE_GEMV_DBG): 1 skip epilogue, 2 skip B waits
+    int dbg;                       // diagnostics (env MOQE_GEMV_DBG): 1 = builders skip the conversion
 };
 constexpr int kTraceCap = 512;
-cudaError_t launch_gemv(int bits, bool two_m16, const GemvArgs& g, const Plan& P, cudaStream_t st,
-                        int num_sms);
-int64_t gemv_partial_floats(int64_t rows, int Kp1, int Np1, int Kp2, int Np2);
-// fragment slots: bytes per slot and slot counts for `rows` GEMV rows over `E` experts
+cudaError_t launch_gemv(int bits, const GemvArgs& g, const Plan& P, cudaStream_t st, int num_sms);
+bool gemv_supported(int Kp1, int Kp2);
+// fc2 fragment slots for `rows` GEMV rows over `E` experts
 int64_t gemv_xb_slot_bytes(int bits);
-int64_t gemv_xb_passes(int64_t rows, int E);
-int gemv_ksplit(int Kp);
-int gemv_stages_per_chunk();
-cudaError_t launch_chunk_max(const float* s1, const float* b1, int E, int Np1, int Kp2, float* smax, float* bmax,
-                             cudaStream_t st);
+int64_t gemv_xb_slots(int64_t rows, int E, int Kp2);
+cudaError_t launch_expert_max(const float* s1, const float* b1, int E, int Np1, float* smax, float* bmax,
+                              cudaStream_t st);
 
 struct GemmArgs {
     const __half* x_perm;  // [R][Kp1] expert-grouped activations

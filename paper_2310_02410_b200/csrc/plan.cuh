@@ -21,10 +21,8 @@ struct Plan {
     int32_t* gemm_list;   // [E]    experts for the tcgen05 path
     int32_t* gemm_tile_start;  // [E+1] prefix of GEMM tiles per listed expert (per m-tile row)
     int32_t* meta;        // [8]    0: n_gemv, 1: n_gemm, 2: gemm n-tiles total, 3: max n_e, 5: forward epoch
-    unsigned* tickets;    // [8]    0: route last-CTA, 1: gemv items, 2: gemm fc1, 3: gemm fc2
-    unsigned* done;       // [E]    GEMV fc1 m-tiles finished per expert
-    unsigned* split_done; // [E * max_mt] GEMV fc2 split-K arrivals
-    float* partial;       // GEMV fc2 split-K partials
+    unsigned* tickets;    // [8]    0: route last-CTA, 1: gemv fc1 items, 2: gemm fc1, 3: gemm fc2, 4: gemv fc2
+    unsigned* done;       // [E]    (reserved; reset per forward)
     float* logits;        // [T][E] router logits (large-T path)
 };
 

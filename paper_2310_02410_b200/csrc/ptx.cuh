@@ -51,7 +51,7 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t pari
     return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    while (!mbar_try_wait_sleep(bar, parity)) {
+    while (!mbar_try_wait(bar, parity)) {
     }
 }
 

@@ -148,6 +148,7 @@ __device__ void plan_tail(const RouteArgs& a, Plan P, int n_ctas, int tt, int* s
             P.tickets[1] = 0;
             P.tickets[2] = 0;
             P.tickets[3] = 0;
+            P.tickets[4] = 0;
             P.tickets[0] = 0;  // self-reset for the next forward
         }
     }
