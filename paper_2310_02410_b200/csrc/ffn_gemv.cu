@@ -151,43 +151,6 @@ __device__ GemvItem item_at(int i, const GemvTables& T, int n_gemv, int nmt) {
     return it;
 }
 
-// ---- cluster / DSMEM helpers ----------------------------------------------------------
-__device__ __forceinline__ uint32_t cta_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ uint32_t cluster_nctas() {
-    uint32_t n;
-    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(n));
-    return n;
-}
-__device__ __forceinline__ void cluster_sync() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t map_rank(const void* p, uint32_t rank) {  // own smem addr -> CTA `rank`
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void st_cluster_s64(uint32_t addr, long long v) {
-    asm volatile("st.shared::cluster.s64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
-}
-__device__ __forceinline__ void arrive_cluster(uint32_t bar_addr) {  // release at cluster scope
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_addr) : "memory");
-}
-__device__ __forceinline__ void wait_cluster(uint64_t* bar, uint32_t parity) {  // acquire at cluster scope
-    uint32_t ok = 0;
-    while (!ok)
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
-            : "memory");
-}
-
 // ---- optional event trace (diagnostics; off unless the bank enables it) ----------------
 __device__ __forceinline__ void trace_ev(unsigned long long* trace, unsigned* cnt, int role, int ev,
                                          const GemvItem& it, int phase) {

@@ -49,6 +49,69 @@ __device__ __forceinline__ void warp_argmax(const float (&l)[EPL], int E, int sk
     bi = __shfl_sync(0xffffffffu, bi, 0);
 }
 
+// Offsets, per-path expert lists, GEMM tile prefix, meta and scheduler resets
+// from per-expert counts `cnt` (global or shared); the first warp works, the
+// others return. `s_off` (optional, shared) receives a copy of the offsets.
+__device__ void plan_lists(const RouteArgs& a, Plan& P, const int* cnt, int* s_off) {
+    const int E = a.E, lane = threadIdx.x & 31;
+    if (threadIdx.x < 32) {
+        int run = 0, ngemv = 0, ngemm = 0, tiles = 0, mx = 0;
+        for (int e0 = 0; e0 < E; e0 += 32) {
+            const int e = e0 + lane;
+            const int n = e < E ? cnt[e] : 0;
+            int incl = n;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += y;
+            }
+            if (e < E) {
+                P.offsets[e] = run + incl - n;
+                if (s_off) s_off[e] = run + incl - n;
+            }
+            run += __shfl_sync(0xffffffffu, incl, 31);
+            int m = n;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
+            mx = max(mx, m);
+            const bool gemv = n > 0 && (a.path == 1 || (a.path == 0 && n <= kGemvMaxRows));
+            const bool gemm = n > 0 && !gemv;
+            const unsigned bg = __ballot_sync(0xffffffffu, gemv), bm = __ballot_sync(0xffffffffu, gemm);
+            const unsigned lt = (1u << lane) - 1u;
+            if (gemv) P.gemv_list[ngemv + __popc(bg & lt)] = e;
+            const int nt = gemm ? (n + a.gemm_bn - 1) / a.gemm_bn : 0;
+            int tincl = nt;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, tincl, off);
+                if (lane >= off) tincl += y;
+            }
+            if (gemm) {
+                const int slot = ngemm + __popc(bm & lt);
+                P.gemm_list[slot] = e;
+                P.gemm_tile_start[slot] = tiles + tincl - nt;
+            }
+            tiles += __shfl_sync(0xffffffffu, tincl, 31);
+            ngemv += __popc(bg);
+            ngemm += __popc(bm);
+        }
+        if (lane == 0) {
+            P.offsets[E] = run;
+            P.gemm_tile_start[ngemm] = tiles;
+            P.meta[0] = ngemv;
+            P.meta[1] = ngemm;
+            P.meta[2] = tiles;
+            P.meta[3] = mx;
+            P.meta[5] += 1;  // forward epoch (GEMV fragment-ready flags compare against it)
+            P.tickets[1] = 0;
+            P.tickets[2] = 0;
+            P.tickets[3] = 0;
+            P.tickets[4] = 0;
+            P.tickets[0] = 0;  // self-reset for the next forward
+        }
+    }
+}
+
 // Last-CTA planning: per-CTA bases, counts, offsets, expert lists, resets.
 // `scr` (optional, >= n_ctas*E ints of smem) stages the per-CTA histograms so
 // the cross-CTA scan costs one L2 round trip instead of one per expert.
@@ -99,59 +162,7 @@ __device__ void plan_tail(const RouteArgs& a, Plan P, int n_ctas, int tt, int* s
     }
     __syncthreads();
     // 2. offsets + expert lists (warp 0, expert order)
-    if (warp == 0) {
-        int run = 0, ngemv = 0, ngemm = 0, tiles = 0, mx = 0;
-        for (int e0 = 0; e0 < E; e0 += 32) {
-            const int e = e0 + lane;
-            const int n = e < E ? P.counts[e] : 0;
-            int incl = n;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, incl, off);
-                if (lane >= off) incl += y;
-            }
-            if (e < E) P.offsets[e] = run + incl - n;
-            run += __shfl_sync(0xffffffffu, incl, 31);
-            int m = n;
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
-            mx = max(mx, m);
-            const bool gemv = n > 0 && (a.path == 1 || (a.path == 0 && n <= kGemvMaxRows));
-            const bool gemm = n > 0 && !gemv;
-            const unsigned bg = __ballot_sync(0xffffffffu, gemv), bm = __ballot_sync(0xffffffffu, gemm);
-            const unsigned lt = (1u << lane) - 1u;
-            if (gemv) P.gemv_list[ngemv + __popc(bg & lt)] = e;
-            const int nt = gemm ? (n + a.gemm_bn - 1) / a.gemm_bn : 0;
-            int tincl = nt;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, tincl, off);
-                if (lane >= off) tincl += y;
-            }
-            if (gemm) {
-                const int slot = ngemm + __popc(bm & lt);
-                P.gemm_list[slot] = e;
-                P.gemm_tile_start[slot] = tiles + tincl - nt;
-            }
-            tiles += __shfl_sync(0xffffffffu, tincl, 31);
-            ngemv += __popc(bg);
-            ngemm += __popc(bm);
-        }
-        if (lane == 0) {
-            P.offsets[E] = run;
-            P.gemm_tile_start[ngemm] = tiles;
-            P.meta[0] = ngemv;
-            P.meta[1] = ngemm;
-            P.meta[2] = tiles;
-            P.meta[3] = mx;
-            P.meta[5] += 1;  // forward epoch (GEMV fragment-ready flags compare against it)
-            P.tickets[1] = 0;
-            P.tickets[2] = 0;
-            P.tickets[3] = 0;
-            P.tickets[4] = 0;
-            P.tickets[0] = 0;  // self-reset for the next forward
-        }
-    }
+    plan_lists(a, P, P.counts, nullptr);
     for (int e = threadIdx.x; e < E; e += blockDim.x) P.done[e] = 0;
     __syncthreads();
     // 3. small problems: scatter routing metadata here (no extra launch)
@@ -410,6 +421,235 @@ __global__ void __launch_bounds__((kRouteSmallWarps + 1) * 32, 1) k_route_small(
     ranks_hist_plan(a, P, s_exp, s_hist, TT, reinterpret_cast<int*>(ring), kRouteSlots * chunk, tr);
 }
 
+// ---- decode (T <= 32): one cluster, plan built in the leader CTA's shared memory ----
+// Same per-token exact chain as k_route_small (warp = token, lane j <-> experts
+// j, j+32, ...), with the operands of the next BK rows loaded ahead of the
+// current BK-step dependent FADD chain (ping-pong register blocks, clamped
+// addresses so the loads are unconditional). Each token's choice and gate go
+// straight into cluster rank 0's shared memory (DSMEM); after one cluster
+// barrier rank 0 builds counts, offsets, lists and the permutation from shared
+// memory — no tickets, no global round trips before the plan is written.
+constexpr int kRouteDecMaxCtas = 8;
+constexpr int kRouteDecMaxT = kRouteDecMaxCtas * kRouteSmallWarps;
+constexpr int kRouteDecMaxE = 256;
+
+template <int BK, int EPL, int EFIX>
+__device__ __forceinline__ void chain_load(const float* hc, const float* wb, int q0, int E, int lane,
+                                           float (&x)[BK], float (&w)[BK][EPL]) {
+#pragma unroll
+    for (int u = 0; u < BK; u += 4) {
+        const float4 t4 = *reinterpret_cast<const float4*>(hc + q0 + u);
+        x[u] = t4.x; x[u + 1] = t4.y; x[u + 2] = t4.z; x[u + 3] = t4.w;
+    }
+#pragma unroll
+    for (int u = 0; u < BK; ++u)
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) w[u][e] = (EFIX || lane + 32 * e < E) ? wb[(q0 + u) * E + 32 * e] : 0.0f;
+}
+template <int BK, int EPL>
+__device__ __forceinline__ void chain_run(float (&acc)[EPL], const float (&x)[BK], const float (&w)[BK][EPL]) {
+#pragma unroll
+    for (int u = 0; u < BK; ++u)
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+            // reference: `if (av == 0.0f) continue; orow[j] += av * brow[j];`
+            const float pr = __fmul_rn(x[u], w[u][e]);
+            if (x[u] != 0.0f) acc[e] = __fadd_rn(acc[e], pr);
+        }
+}
+
+template <int EPL, int EFIX>
+__global__ void __launch_bounds__((kRouteSmallWarps + 1) * 32, 1) k_route_decode(RouteArgs a, Plan P) {
+    constexpr int TT = kRouteSmallWarps;
+    constexpr int BK = EPL <= 2 ? 16 : EPL <= 4 ? 8 : 4;  // rows per pipelined block
+    extern __shared__ __align__(128) float s_dyn[];
+    __shared__ int s_exp[kRouteDecMaxT * 2];
+    __shared__ float s_gate[kRouteDecMaxT * 2];
+    __shared__ int s_cnt[kRouteDecMaxE];
+    __shared__ int s_off[kRouteDecMaxE];
+    pdl_trigger();  // the expert-FFN grid may launch and run its prologue now
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rank = int(cta_rank());
+    unsigned long long* tr = (a.trace && blockIdx.x < kTraceRouteCtas) ? a.trace + blockIdx.x * 16 : nullptr;
+    if (tr && threadIdx.x == 0) tr[0] = gtime_ns();
+    const int E = EFIX ? EFIX : a.E, d = a.d, k = a.topk;
+    const int rows = route_chunk_rows(E);
+    const int chunk = rows * E;
+    const int nch = (d + rows - 1) / rows;
+    const int dpad = nch * rows;
+    float* ring = s_dyn;
+    float* s_hrow = s_dyn + kRouteSlots * chunk;
+    uint64_t* full = reinterpret_cast<uint64_t*>(s_hrow + TT * dpad);
+    uint64_t* empty = full + kRouteSlots;
+    const int64_t t = int64_t(blockIdx.x) * TT + (warp < TT ? warp : 0);
+    const bool live = warp < TT && t < a.T;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kRouteSlots; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], TT); }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    cluster_arrive_release();  // rank 0 has started before anyone writes its shared memory (wait below)
+
+    if (warp == TT) {
+        if (lane == 0) {
+            const bool bulk = (reinterpret_cast<uintptr_t>(a.wg) & 15) == 0;
+            for (int c = 0; c < nch; ++c) {
+                const int s = c % kRouteSlots;
+                if (c >= kRouteSlots) mbar_wait(&empty[s], ((c / kRouteSlots) - 1) & 1);
+                const int nr = min(rows, d - c * rows);
+                const float* src = a.wg + int64_t(c) * chunk;
+                if (bulk && ((nr * E) & 3) == 0) {
+                    mbar_arrive_expect_tx(&full[s], uint32_t(nr * E * 4));
+                    bulk_g2s(ring + s * chunk, src, uint32_t(nr * E * 4), &full[s]);
+                } else {
+                    for (int i = 0; i < nr * E; ++i) ring[s * chunk + i] = __ldg(src + i);
+                    mbar_arrive(&full[s]);
+                }
+            }
+        }
+        __syncwarp();
+        cluster_wait_acquire();
+    } else {
+        float* hr = s_hrow + warp * dpad;
+        if (live && a.h_f16 && (d % 8) == 0 && (reinterpret_cast<uintptr_t>(a.h) & 15) == 0) {
+            const uint4* src = reinterpret_cast<const uint4*>(static_cast<const __half*>(a.h) + t * d);
+            for (int j = lane; j < d / 8; j += 32) {
+                const uint4 v = __ldg(src + j);
+                const __half2* h2 = reinterpret_cast<const __half2*>(&v);
+                float4 lo, hi;
+                float2 f;
+                f = __half22float2(h2[0]); lo.x = f.x; lo.y = f.y;
+                f = __half22float2(h2[1]); lo.z = f.x; lo.w = f.y;
+                f = __half22float2(h2[2]); hi.x = f.x; hi.y = f.y;
+                f = __half22float2(h2[3]); hi.z = f.x; hi.w = f.y;
+                reinterpret_cast<float4*>(hr)[2 * j] = lo;
+                reinterpret_cast<float4*>(hr)[2 * j + 1] = hi;
+            }
+            for (int p = d + lane; p < dpad; p += 32) hr[p] = 0.0f;
+        } else {
+            for (int p = lane; p < dpad; p += 32) hr[p] = (live && p < d) ? load_act(a.h, a.h_f16, t * d + p) : 0.0f;
+        }
+        if (live && a.inline_scatter && a.zero_out)  // top-2: fp32 accumulation rows start at zero
+            for (int j = lane; j < d; j += 32) a.zero_out[t * d + j] = 0.f;
+        __syncwarp();
+        if (tr && threadIdx.x == 0) tr[1] = gtime_ns();
+        float acc[EPL];
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) acc[e] = 0.0f;
+        for (int c = 0; c < nch; ++c) {
+            const int s = c % kRouteSlots;
+            mbar_wait(&full[s], (c / kRouteSlots) & 1);
+            if (live) {
+                const float* wb = ring + s * chunk + lane;
+                const float* hc = hr + c * rows;
+                const int nr = min(rows, d - c * rows);
+                int q = 0;
+                if (nr >= 2 * BK) {
+                    const int qlast = (nr - BK) & ~3;  // clamp target: in range and 16-byte aligned
+                    float xa[BK], wa[BK][EPL], xb[BK], wbk[BK][EPL];
+                    chain_load<BK, EPL, EFIX>(hc, wb, 0, E, lane, xa, wa);
+                    for (; q + 2 * BK <= nr; q += 2 * BK) {
+                        chain_load<BK, EPL, EFIX>(hc, wb, q + BK, E, lane, xb, wbk);
+                        chain_run<BK, EPL>(acc, xa, wa);
+                        chain_load<BK, EPL, EFIX>(hc, wb, min(q + 2 * BK, qlast), E, lane, xa, wa);
+                        chain_run<BK, EPL>(acc, xb, wbk);
+                    }
+                }
+                for (; q < nr; ++q) {
+                    const float av = hc[q];
+#pragma unroll
+                    for (int e = 0; e < EPL; ++e) {
+                        const float w = (EFIX || lane + 32 * e < E) ? wb[q * E + 32 * e] : 0.0f;
+                        const float pr = __fmul_rn(av, w);
+                        if (av != 0.0f) acc[e] = __fadd_rn(acc[e], pr);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            if (tr && threadIdx.x == 0 && c < 8) tr[2 + c] = gtime_ns();
+        }
+        // argmax / gate (reference tie rule, fp64 softmax) -> rank 0's shared memory
+        float b1v = 0.f, b2v = 0.f, g1 = 0.f, g2 = 0.f;
+        int b1i = 0, b2i = 0;
+        if (live) {
+            warp_argmax<EPL>(acc, E, -1, b1v, b1i);
+            if (k == 1) {
+                const double mx = double(b1v);
+                double sm = 0.0;
+#pragma unroll
+                for (int e = 0; e < EPL; ++e)
+                    if (lane + 32 * e < E) sm += exp(double(acc[e]) - mx);
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, off);
+                const float eb = float(exp(double(b1v) - mx));
+                g1 = float(double(eb) / sm);
+            } else {
+                warp_argmax<EPL>(acc, E, b1i, b2v, b2i);
+                const double z = exp(double(b2v) - double(b1v));
+                g1 = float(1.0 / (1.0 + z));
+                g2 = float(z / (1.0 + z));
+            }
+        }
+        if (tr && threadIdx.x == 0) tr[10] = gtime_ns();
+        cluster_wait_acquire();  // rank 0 is running
+        if (live && lane == 0) {
+            st_cluster_u32(map_rank(&s_exp[t * k], 0), uint32_t(b1i));
+            st_cluster_u32(map_rank(&s_gate[t * k], 0), __float_as_uint(g1));
+            if (k == 2) {
+                st_cluster_u32(map_rank(&s_exp[t * k + 1], 0), uint32_t(b2i));
+                st_cluster_u32(map_rank(&s_gate[t * k + 1], 0), __float_as_uint(g2));
+            }
+        }
+    }
+    cluster_arrive_release();
+    cluster_wait_acquire();  // every token's choice is in rank 0's shared memory
+    if (tr && threadIdx.x == 0) tr[11] = gtime_ns();
+    if (rank != 0) return;
+
+    // ===== rank 0: the whole plan from shared memory
+    const int n = int(a.T) * k;
+    const int nct = int((a.T + TT - 1) / TT);
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        int c = 0;
+        for (int i = 0; i < n; ++i) c += s_exp[i] == e;
+        s_cnt[e] = c;
+        P.counts[e] = c;
+        P.done[e] = 0;
+    }
+    __syncthreads();
+    plan_lists(a, P, s_cnt, s_off);
+    if (threadIdx.x == 0) P.tickets[0] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int e = s_exp[i];
+        const int c0 = (i / k) / TT * TT * k;  // first (token, slot) of this row's route group
+        int r = 0, base = 0;
+        for (int j = 0; j < i; ++j)
+            if (s_exp[j] == e) { ++r; base += j < c0; }
+        const int pos = s_off[e] + r;
+        const float gt = s_gate[i];
+        P.expert[i] = e;
+        P.gate[i] = gt;
+        P.lrank[i] = r - base;
+        if (a.inline_scatter) {
+            P.perm_token[pos] = i / k;
+            P.perm_gate[pos] = gt;
+            P.inv_pos[i] = pos;
+        }
+    }
+    for (int idx = threadIdx.x; idx < nct * E; idx += blockDim.x) {  // route-group bases (k_scatter)
+        const int c = idx / E, e = idx - c * E, lim = min(c * TT * k, n);
+        int b = 0;
+        for (int j = 0; j < lim; ++j) b += s_exp[j] == e;
+        P.cta_counts[idx] = b;
+    }
+    if (tr) {
+        __syncthreads();
+        if (threadIdx.x == 0) tr[12] = gtime_ns();
+    }
+}
+
 // ---- large T (prefill) ----------------------------------------------------------------
 // k_route_logits: one warp = 32 tokens (lane = token) x 8 experts; a CTA = 4
 // warps = 32 tokens x 32 experts, grid (T/32, E/32). Each Wg row is a smem
@@ -599,6 +839,41 @@ __global__ void __launch_bounds__(256) k_scatter(const void* h, int h_f16, int64
     for (int j = d + lane; j < ldx; j += 32) dst[j] = __float2half_rn(0.f);
 }
 
+namespace {
+template <int EPL, int EFIX>
+cudaError_t launch_dec(const RouteArgs& a, const Plan& P, size_t smem, cudaStream_t st) {
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_route_decode<EPL, EFIX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        configured = true;
+    }
+    const unsigned nct = unsigned((a.T + kRouteSmallWarps - 1) / kRouteSmallWarps);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(nct);
+    cfg.blockDim = dim3((kRouteSmallWarps + 1) * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = nct;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_route_decode<EPL, EFIX>, a, P);
+}
+}  // namespace
+
+cudaError_t launch_route_decode(const RouteArgs& a, const Plan& P, size_t smem, cudaStream_t st) {
+    switch (a.E) {
+        case 32: return launch_dec<1, 32>(a, P, smem, st);
+        case 64: return launch_dec<2, 64>(a, P, smem, st);
+        case 128: return launch_dec<4, 128>(a, P, smem, st);
+        case 256: return launch_dec<8, 256>(a, P, smem, st);
+        default: return launch_dec<8, 0>(a, P, smem, st);
+    }
+}
+
 // Route tile: tokens per routing CTA for a given T (must match scatter's tt).
 constexpr int64_t kRouteBigThreshold = 512;
 int route_tokens_per_cta(int64_t T) { return T <= kRouteBigThreshold ? kRouteSmallWarps : kRouteSelWarps; }
@@ -617,6 +892,7 @@ cudaError_t launch_route(const RouteArgs& a, const Plan& P, cudaStream_t st) {
     }
     const size_t smem = route_small_smem(a.d, a.E);
     if (smem > 220 * 1024) return cudaErrorInvalidValue;
+    if (a.T <= kRouteDecMaxT && a.E <= kRouteDecMaxE) return launch_route_decode(a, P, smem, st);
     static bool configured = false;
     if (!configured) {
         const int mx = 220 * 1024;
