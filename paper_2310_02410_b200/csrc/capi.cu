@@ -46,8 +46,8 @@ struct Workspace {
     __half* mid = nullptr;
     __half* x_perm = nullptr;
     float* out_acc = nullptr;
-    uint8_t* xb = nullptr;         // decode GEMV: fc2 activation fragments (fc1 -> fc2)
-    int64_t xb_slot_bytes = 0;
+    uint8_t* xr = nullptr;         // decode GEMV: fc1 row blocks (k_xrows)
+    uint8_t* xb = nullptr;         // decode GEMV: fc2 row blocks (fc1 epilogue -> fc2)
 };
 
 struct moqe_bank {
@@ -137,9 +137,10 @@ moqe_status ensure_workspace(moqe_bank* b, int64_t T, int topk) {
     add(4, capR); add(4, capR); add(4, capR); add(4, E); add(4, E); add(4, E + 1); add(4, 8);
     add(4, 8); add(4, E);
     add(2, capR * b->Np1); add(2, capR * b->Kp1); add(4, capT * b->d); add(4, capT * E);
-    const int64_t xb_slots = gemv_xb_slots(capR, E, b->Kp2);
-    const int64_t xb_bytes = gemv_xb_slot_bytes(b->bits);
-    add(xb_bytes, xb_slots);
+    const int64_t xr_bytes = gemv_xr_bytes(b->bits) * gemv_chunks(b->Kp1) * capT;
+    const int64_t xb_bytes = gemv_xb_bytes(b->bits) * gemv_chunks(b->Kp2) * capR;
+    add(xr_bytes, 1);
+    add(xb_bytes, 1);
     MOQE_CUDA(cudaMalloc(&w.block, bytes));
     MOQE_CUDA(cudaMemset(w.block, 0, bytes));
     char* p = static_cast<char*>(w.block);
@@ -163,8 +164,8 @@ moqe_status ensure_workspace(moqe_bank* b, int64_t T, int topk) {
     w.x_perm = carve<__half>(p, capR * b->Kp1);
     w.out_acc = carve<float>(p, capT * b->d);
     P.logits = carve<float>(p, capT * E);
-    w.xb = carve<uint8_t>(p, xb_bytes * xb_slots);
-    w.xb_slot_bytes = xb_bytes;
+    w.xr = carve<uint8_t>(p, xr_bytes);
+    w.xb = carve<uint8_t>(p, xb_bytes);
     w.cap_rows = capR;
     w.cap_tokens = capT;
     return MOQE_OK;
@@ -366,6 +367,12 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
     cudaError_t ce;
     {
         KernelTimer kt(b, 0, st);
+        if (need_gemv) {  // token rows -> fc1 row blocks; the decode router overlaps it (PDL)
+            XrowArgs xa{h, h_dtype == MOQE_F16, t, int(b->d), gemv_chunks(b->Kp1), w.xr};
+            ce = launch_xrows(b->bits, xa, st);
+            if (ce != cudaSuccess) return cuda_fail(ce, "k_xrows");
+            ra.pdl = 1;
+        }
         ce = pre ? launch_plan_from_ids(ra, P, st) : launch_route(ra, P, st);
     }
     if (ce != cudaSuccess) return cuda_fail(ce, pre ? "k_plan_from_ids" : "k_route");
@@ -379,7 +386,7 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
     if (need_gemv) {
         GemvArgs g{h, h_dtype == MOQE_F16, t, int(b->d), int(b->f), top_k, b->E, b->w1, b->w2,
                    b->w1_stride, b->w2_stride, b->s1, b->s2, b->b1, b->b2, b->Kp1, b->Np1, b->Kp2, b->Np2,
-                   out, out_dtype == MOQE_F16, acc, w.xb, w.xb_slot_bytes, b->smax1, b->bmax1, b->trace, gemv_dbg()};
+                   out, out_dtype == MOQE_F16, acc, w.xr, gemv_chunks(b->Kp1), w.xb, b->smax1, b->bmax1, b->trace, gemv_dbg()};
         KernelTimer kt(b, 2, st);
         ce = launch_gemv(b->bits, g, P, st, b->num_sms);
         if (ce != cudaSuccess) return cuda_fail(ce, "k_ffn_gemv");

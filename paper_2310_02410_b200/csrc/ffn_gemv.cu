@@ -1,6 +1,7 @@
 // ffn_gemv.cu — decode path: expert FFN (fc1 -> ReLU -> fc2 -> gate combine)
 // as two persistent weight-streaming kernels (one per layer of the FFN),
-// chained with programmatic dependent launch (PDL).
+// chained with programmatic dependent launch (PDL), plus the token-row encoder
+// k_xrows that runs beside the router.
 //
 // Reference: the per-expert loop of moe_ffn_forward proj/src/model.cpp:360-391
 // (dequantize :370-375, matmul :381/:384, add_bias/relu :382-385, scatter
@@ -22,20 +23,29 @@
 //     encodes its own 128 output channels (one fc2 k-stage) independently;
 //     resolution ~2^-29 of the bound, far finer than the reference's fp32 chain.
 //
+// Row blocks. The B operand of an item is up to 4 rows; each row's digits of
+// one 1024-k chunk live in a self-contained "row block" (header + one plane
+// per digit, every plane already in the k-order the IMMA B fragments want), so
+// the producer fetches a row with a single TMA bulk copy and a consumer lane
+// reads its B registers with one LDS.64 per fragment. fc1 row blocks are
+// written once per token by k_xrows (not once per item), fc2 row blocks by the
+// fc1 epilogue (one 128-k stage per fc1 item).
+//
 // Work: an item is (expert, row pass, 128-channel m-tile); its K is split into
 // 1024-k chunks, one per CTA of a thread-block cluster (fc1: d/1024 CTAs, fc2:
 // f/1024). Each CTA streams its chunk's packed tiles — one contiguous stripe —
 // with TMA bulk copies of >= 16 KB (smaller copies cap the chip at 1-3.6 TB/s,
-// profiles/round1/tma_copy_size.md), runs the IMMA k-loop, and sends its exact
-// int64 partial sums to cluster rank 0 through distributed shared memory; rank 0
-// finishes the item. Items are statically scheduled over the clusters (all the
-// same size), so there are no tickets and no cross-cluster synchronisation.
-//   fc1 roles: warps 0-7 consumers (16 channels each), 8-10 builders (token rows
-//     -> digit fragments in smem, two items ahead), 11 producer (weights).
-//     Rank 0's epilogue writes fc2's fragments + Sum X parts to global memory.
-//   fc2 roles: warps 0-7 consumers, 8 producer (weights, then each item's
-//     fragment slot, issued after the PDL wait on fc1); rank 0 writes the
-//     gate-weighted output rows (exactly one writer per element: deterministic).
+// profiles/round1/tma_copy_size.md). Items are statically scheduled over the
+// clusters (all the same size): no tickets, no cross-cluster synchronisation.
+//   warps 0-7   consumers: 16 channels each; LOP3 unpack + IMMA; per item the
+//               exact group sums go to a double-buffered scratch and the warp
+//               moves straight on to the next item (the stream never waits
+//               for an epilogue)
+//   warps 8-11  epilogue: thread = channel; exact int64 partials, split-K
+//               reduction into cluster rank 0 over DSMEM, scale/bias, and
+//               fc1: ReLU -> fc2 fixed point -> fc2 row blocks in global memory
+//               fc2: gate-weighted output rows (one writer per element)
+//   warp 12     producer: row blocks + weight copy units (TMA, evict-first)
 #include <cuda_fp16.h>
 
 #include <algorithm>
@@ -51,57 +61,68 @@ constexpr int kStageK = 2 * TILE_K;  // k per IMMA stage (2 tiles)
 constexpr int kChunkK = 1024;        // k per CTA of a cluster
 constexpr int kChunkStages = kChunkK / kStageK;
 constexpr int kMaxCluster = 8;
-constexpr int kPassRows = 4;         // token rows per item pass
+constexpr int kPassRows = 4;         // rows per item pass
 constexpr int kMaxNT = 2;            // n8 column tiles (4 rows x 4 planes = 16 columns)
-constexpr int kScrCols = 8 * kMaxNT;
 constexpr int kMaxListed = 256;
-constexpr int kConsumers = 8;        // consumer warps: 16 channels (one m16 block) each
-constexpr int kBuilders = 3;         // fc1 fragment builders (= fragment buffers)
-constexpr int kBufs = 3;             // fragment buffers
-constexpr int kHead = 352;           // fragment buffer / fc2 slot head (see below)
+constexpr int kConsumers = 8;        // MMA warps: 16 channels (one m16 block) each
+constexpr int kEpiWarps = 4;         // epilogue warps: one thread per channel
+constexpr int kProdWarp = kConsumers + kEpiWarps;
+constexpr int kGemvThreads = (kProdWarp + 1) * 32;
+constexpr int kBufs = 3;             // row-block buffers (B operands of 3 items in flight)
+constexpr int kScrBufs = 2;          // accumulator scratch buffers (consumer -> epilogue)
+constexpr int kScrStride = 20;       // ints per channel row of the scratch (16 columns; conflict-free LDS.128)
+constexpr int kSmemMax = 227 * 1024;
 constexpr int kZeroRow = -0x40000000;  // exponent sentinel: the row is (numerically) zero
 
 __host__ __device__ constexpr int planes_of(int phase) { return phase == 1 ? 3 : 4; }
 __host__ __device__ constexpr int nt_of(int phase, int rows) { return (planes_of(phase) * rows + 7) / 8; }
-__host__ __device__ constexpr int w_of(int phase, int nt) { return 8 * nt / planes_of(phase); }
-__host__ __device__ constexpr int threads_of(int phase) {
-    return (phase == 1 ? kConsumers + kBuilders + 1 : kConsumers + 1) * 32;
-}
+__host__ __device__ constexpr int rup(int x, int a) { return (x + a - 1) / a * a; }
 template <int BITS>
 __host__ __device__ constexpr int unit_stages() { return BITS == 8 ? 2 : 4; }  // >= 16 KB per weight copy
 
-// Fragment buffer head (352 bytes):
-//   fc1 (built in smem): p[4] (row exponent), zsum[4] (Sum X of the chunk), l1[4] (|x|_1 of the row)
-//   fc2 slot (global, copied with the fragments): p[4] = p2, zpart[8 stages][4 rows] (Sum X2 per fc1 item)
-struct __align__(16) Head {
-    int p[4];
-    int pad0[4];
-    long long zsum[4];
-    float l1[4];
-    int pad1[4];
-    long long zpart[kChunkStages][4];
+// Row block geometry. A plane holds 8 stages of STG bytes: stage st, fragment
+// f, quad tq, register h -> the u32 at st*STG + f*32 + tq*8 + h*4 whose byte i
+// is the digit of activation Frag::kidx(f, h, i) of that quad (codec order).
+// Planes are PB bytes apart (PB = 32 mod 128) and row blocks XR bytes apart
+// (XR = 64 mod 128), so the 8 column groups of a warp's LDS.64 hit distinct
+// bank groups (two wavefronts, the minimum for 256 bytes).
+template <int BITS>
+struct RB {
+    static constexpr int F = Frag<BITS>::F;
+    static constexpr int STG = F * 32;
+    static constexpr int PB = kChunkStages * STG + 32;
+    static constexpr int HDR1 = 32;   // fc1: int p, float l1 (whole row), int64 Sum X (this chunk)
+    static constexpr int HDR2 = 128;  // fc2: int p2 at 0, int64 Sum X2 of stage st at 64 + 8 st
+    static constexpr int XR1 = rup(HDR1 + 3 * PB, 128) + 64;
+    static constexpr int XR2 = rup(HDR2 + 4 * PB, 128) + 64;
 };
-static_assert(sizeof(Head) == kHead, "head layout");
+struct XHead1 {
+    int p;
+    float l1;
+    long long zsum;
+};
 
 template <int BITS>
 struct Cfg {
     static constexpr int F = Frag<BITS>::F;
     static constexpr int TB = tile_bytes(BITS);
-    static constexpr int SB = 2 * TB;                             // one IMMA stage of weights
+    static constexpr int SB = 2 * TB;          // one IMMA stage of weights
     static constexpr int US = unit_stages<BITS>();
-    static constexpr int UB = US * SB;                            // one weight copy
-    static constexpr int BBUF = kChunkStages * F * kMaxNT * 256;  // fragments of a 1024-k chunk
-    static constexpr int64_t SLOT = kHead + BBUF;                 // fc2 fragment slot in global memory
+    static constexpr int UB = US * SB;         // one weight copy
 };
 
 struct GemvItem {
-    int e, mt, row0, nrows, gp;  // gp: global row-pass index (fc2 fragment slots); e < 0: none
+    int e, mt, row0, nrows;  // e < 0: none
 };
+
+constexpr int kTokCache = 512;       // routed rows whose token ids the producer keeps in smem
+constexpr int kItemCache = 64;       // this CTA's first items, decoded once at kernel start
 
 struct GemvTables {
     int list[kMaxListed], cnt[kMaxListed], off[kMaxListed];
-    int pst[kMaxListed + 1];    // row-pass prefix per listed expert
     int start[kMaxListed + 1];  // item prefix per listed expert
+    int tok[kTokCache];         // perm_token[0, kTokCache) (fc1 row-block sources)
+    int4 items[kItemCache];     // (e, mt, row0, nrows) of this CTA's k-th item
 };
 
 __device__ __forceinline__ int find_listed(const int* st, int n, int v) {  // largest a with st[a] <= v
@@ -114,7 +135,9 @@ __device__ __forceinline__ int find_listed(const int* st, int n, int v) {  // la
 }
 
 // Item tables from the plan (one warp: lane-parallel loads, serial prefix).
-__device__ void build_tables(GemvTables& T, const Plan& P, int n_gemv, int nmt, int lane) {
+__device__ void build_tables(GemvTables& T, const Plan& P, int n_gemv, int nmt, int lane, int64_t rows) {
+    const int nr = rows < kTokCache ? int(rows) : kTokCache;
+    for (int r = lane; r < nr; r += 32) T.tok[r] = P.perm_token[r];
     for (int a = lane; a < n_gemv; a += 32) {
         const int e = P.gemv_list[a];
         T.list[a] = e;
@@ -123,101 +146,119 @@ __device__ void build_tables(GemvTables& T, const Plan& P, int n_gemv, int nmt, 
     }
     __syncwarp();
     if (lane == 0) {
-        int t = 0, tp = 0;
+        int t = 0;
         for (int a = 0; a < n_gemv; ++a) {
-            const int np = (T.cnt[a] + kPassRows - 1) / kPassRows;
-            T.pst[a] = tp;
             T.start[a] = t;
-            tp += np;
-            t += nmt * np;
+            t += nmt * ((T.cnt[a] + kPassRows - 1) / kPassRows);
         }
-        T.pst[n_gemv] = tp;
         T.start[n_gemv] = t;
     }
 }
 
 // Item i (expert-major: expert, pass, m-tile).
-__device__ GemvItem item_at(int i, const GemvTables& T, int n_gemv, int nmt) {
+__device__ __forceinline__ GemvItem item_at(int i, const GemvTables& T, int n_gemv, int nmt) {
     GemvItem it{};
     if (i >= T.start[n_gemv]) { it.e = -1; return it; }
     const int a = find_listed(T.start, n_gemv, i);
     const int r = i - T.start[a];
     const int pass = r / nmt;
     it.e = T.list[a];
-    it.mt = r % nmt;
+    it.mt = r - pass * nmt;
     it.row0 = T.off[a] + pass * kPassRows;
     it.nrows = min(kPassRows, T.cnt[a] - pass * kPassRows);
-    it.gp = T.pst[a] + pass;
     return it;
 }
 
-// ---- optional event trace (diagnostics; off unless the bank enables it) ----------------
-__device__ __forceinline__ void trace_ev(unsigned long long* trace, unsigned* cnt, int role, int ev,
-                                         const GemvItem& it, int phase) {
-    if (trace == nullptr) return;
-    const unsigned i = atomicAdd(cnt, 1u);
-    if (i >= unsigned(kTraceCap / 2)) return;
-    unsigned long long* p = trace + (size_t(blockIdx.x) * kTraceCap + i) * 2;
-    p[0] = gtime_ns();
-    p[1] = (unsigned long long)role << 60 | (unsigned long long)ev << 56 | (unsigned long long)phase << 48 |
-           (unsigned long long)(it.e & 0xffff) << 32 | (unsigned long long)(it.mt & 0xfff) << 20 |
-           (unsigned long long)(it.nrows & 0xf) << 16 | (unsigned long long)(clock64() & 0xffff);
+// k-th item of this CTA (global index i): the cached decode, else the table lookup
+__device__ __forceinline__ GemvItem item_of(int k, int i, const GemvTables& T, int n_gemv, int nmt) {
+    if (k < kItemCache) {
+        const int4 v = T.items[k];
+        GemvItem it;
+        it.e = v.x; it.mt = v.y; it.row0 = v.z; it.nrows = v.w;
+        return it;
+    }
+    return item_at(i, T, n_gemv, nmt);
 }
 
-// ---- fc1 builders: token rows -> 3-plane digit fragments of one 1024-k chunk ----------
-// One warp per row; lane = (stage st, quad tq) owns the 32 activations that quad's
-// IMMA lanes meet in stage st of the chunk. The row maximum and |x|_1 cover the
-// whole row (every CTA of the cluster derives the same exponent).
-template <int BITS>
-__device__ void build_row(const GemvArgs& g, const Plan& P, const GemvItem& it, int t, int lane, bool vec_h,
-                          int k0, int nst, uint8_t* bb, Head& hd) {
-    using FR = Frag<BITS>;
-    constexpr int F = FR::F;
-    const int NT = nt_of(1, it.nrows), W = w_of(1, NT);
-    const int st = lane >> 2, tq = lane & 3;
-    const int64_t tok = P.perm_token[it.row0 + t];
-    auto load16 = [&](int k, float* v) {  // 16 activations from k (zeros beyond d)
-        if (vec_h) {
-            const __half* row = static_cast<const __half*>(g.h) + tok * g.d;
+// ---- optional event trace (diagnostics; off unless the bank enables it) ----------------
+// Per CTA and phase a row of kTraceCap/2 slots: slot 0 / last = (globaltimer, clock64)
+// anchors at start / end; consumers log into [1, 128), epilogue [128, 192), producer
+// [192, last). Events carry clock64 (cheap, no atomics); the reader maps them to ns.
+// role 2 = consumers (3 top, 0 row blocks in, 1 mainloop end, 4 scratch free),
+// 3 = epilogue (0 start, 2 end), 4 = producer (0/1 unit issued), 5 = unit landed.
+struct Tracer {
+    unsigned long long* p;
+    int n, cap;
+    __device__ __forceinline__ void ev(int role, int e, const GemvItem& it, int phase) {
+        if (p == nullptr || n >= cap) return;
+        unsigned long long* q = p + 2 * n++;
+        q[0] = clock64();
+        q[1] = (unsigned long long)role << 60 | (unsigned long long)e << 56 | (unsigned long long)phase << 48 |
+               (unsigned long long)(it.e & 0xffff) << 32 | (unsigned long long)(it.mt & 0xfff) << 20 |
+               (unsigned long long)(it.nrows & 0xf) << 16 | 1ull;
+    }
+};
+__device__ __forceinline__ Tracer tracer(unsigned long long* row, int lo, int hi) {
+    Tracer t;
+    t.p = row ? row + 2 * lo : nullptr;
+    t.n = 0;
+    t.cap = hi - lo;
+    return t;
+}
+
+// ---- k_xrows: token rows -> fc1 row blocks ------------------------------------------------
+// Warp per (token, 1024-k chunk); lane = (stage st, quad tq) owns the 32
+// activations that quad's IMMA lanes meet in stage st. The row maximum and
+// |x|_1 cover the whole row, so every chunk of a row derives the same exponent.
+__device__ __forceinline__ float act16(const XrowArgs& a, int64_t t, int k) {  // fp16 value of h[t][k] (0 beyond d)
+    if (k >= a.d) return 0.f;
+    return a.h_f16 ? __half2float(static_cast<const __half*>(a.h)[t * a.d + k])
+                   : __half2float(__float2half_rn(static_cast<const float*>(a.h)[t * a.d + k]));
+}
+__device__ __forceinline__ void load16(const XrowArgs& a, int64_t t, int k, bool vec, float* v) {
+    if (vec) {
+        const __half* row = static_cast<const __half*>(a.h) + t * a.d;
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                uint4 w = make_uint4(0u, 0u, 0u, 0u);
-                if (k + 8 * q < g.d) w = __ldg(reinterpret_cast<const uint4*>(row + k + 8 * q));  // d % 8 == 0
-                const __half2* h2 = reinterpret_cast<const __half2*>(&w);
+        for (int q = 0; q < 2; ++q) {
+            uint4 w = make_uint4(0u, 0u, 0u, 0u);
+            if (k + 8 * q < a.d) w = __ldg(reinterpret_cast<const uint4*>(row + k + 8 * q));  // d % 8 == 0
+            const __half2* h2 = reinterpret_cast<const __half2*>(&w);
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const float2 f = __half22float2(h2[i]);
-                    v[8 * q + 2 * i] = f.x;
-                    v[8 * q + 2 * i + 1] = f.y;
-                }
-            }
-        } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                float x = 0.f;
-                if (k + i < g.d)  // activations enter as fp16 values (the GEMM path's x_perm is fp16 too)
-                    x = g.h_f16 ? __half2float(static_cast<const __half*>(g.h)[tok * g.d + k + i])
-                                : __half2float(__float2half_rn(static_cast<const float*>(g.h)[tok * g.d + k + i]));
-                v[i] = x;
+            for (int i = 0; i < 4; ++i) {
+                const float2 f = __half22float2(h2[i]);
+                v[8 * q + 2 * i] = f.x;
+                v[8 * q + 2 * i + 1] = f.y;
             }
         }
-    };
-    float v[32];
+    } else {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = 0.f;
-    const bool act = st < nst;
-    if (act) {
-        load16(k0 + st * kStageK + 16 * tq, v);
-        load16(k0 + st * kStageK + 64 + 16 * tq, v + 16);
+        for (int i = 0; i < 16; ++i) v[i] = act16(a, t, k + i);
     }
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(128) k_xrows(XrowArgs a) {
+    pdl_trigger();  // the decode router may launch now (it does not read row blocks)
+    using FR = Frag<BITS>;
+    using R = RB<BITS>;
+    constexpr int F = FR::F;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t w = int64_t(blockIdx.x) * 4 + warp;
+    const int64_t t = w / a.nch1;
+    const int c = int(w - t * a.nch1);
+    if (t >= a.T) return;
+    const bool vec = a.h_f16 && (a.d % 8) == 0 && (reinterpret_cast<uintptr_t>(a.h) & 15) == 0;
+    const int st = lane >> 2, tq = lane & 3, k0 = c * kChunkK;
+    float v[32];
+    load16(a, t, k0 + st * kStageK + 16 * tq, vec, v);
+    load16(a, t, k0 + st * kStageK + 64 + 16 * tq, vec, v + 16);
     float m = 0.f, l1 = 0.f;
 #pragma unroll
     for (int i = 0; i < 32; ++i) { m = fmaxf(m, fabsf(v[i])); l1 += fabsf(v[i]); }
-    // the rest of the row (other chunks of the cluster): maximum and |x|_1 only
-    for (int k = lane * 16; k < g.Kp1; k += 32 * 16) {
+    for (int k = lane * 16; k < a.d; k += 32 * 16) {  // the other chunks of the row: max and |x|_1 only
         if (k >= k0 && k < k0 + kChunkK) continue;
         float u[16];
-        load16(k, u);
+        load16(a, t, k, vec, u);
 #pragma unroll
         for (int i = 0; i < 16; ++i) { m = fmaxf(m, fabsf(u[i])); l1 += fabsf(u[i]); }
     }
@@ -240,17 +281,18 @@ __device__ void build_row(const GemvArgs& g, const Plan& P, const GemvItem& it, 
     long long zs = sum;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) zs += __shfl_xor_sync(0xffffffffu, zs, off);
+    uint8_t* blk = a.xr + (t * a.nch1 + c) * int64_t(R::XR1);
     if (lane == 0) {
-        hd.p[t] = p;
-        hd.zsum[t] = zs;
-        hd.l1[t] = l1 * (1.0f + 0x1p-9f);  // covers the fp32 summation error: an upper bound
+        XHead1 hd;
+        hd.p = p;
+        hd.l1 = l1 * (1.0f + 0x1p-9f);  // covers the fp32 summation error: an upper bound
+        hd.zsum = zs;
+        *reinterpret_cast<XHead1*>(blk) = hd;
     }
-    if (!act) return;
 #pragma unroll
     for (int s = 0; s < 3; ++s) {
-        const int col = s * W + t, j = col >> 3, gq = col & 7;
         const uint32_t sel = uint32_t(s) | (uint32_t(4 + s) << 4);
-        uint8_t* dst = bb + (size_t(st * F) * NT + j) * 256 + (4 * gq + tq) * 8;
+        uint8_t* dst = blk + R::HDR1 + s * R::PB + st * R::STG + tq * 8;
 #pragma unroll
         for (int f = 0; f < F; ++f) {
             uint32_t b[2];
@@ -260,41 +302,60 @@ __device__ void build_row(const GemvArgs& g, const Plan& P, const GemvItem& it, 
                 const uint32_t hi = prmt(D[FR::kidx(f, h, 2)], D[FR::kidx(f, h, 3)], sel);
                 b[h] = prmt(lo, hi, 0x5410u);
             }
-            *reinterpret_cast<uint2*>(dst + size_t(f) * NT * 256) = make_uint2(b[0], b[1]);
+            *reinterpret_cast<uint2*>(dst + f * 32) = make_uint2(b[0], b[1]);
         }
     }
 }
 
 // ---- consumer pieces -------------------------------------------------------------------
-// One 128-k stage of one m16 block: LOP3 unpack + IMMA against the stage's B fragments.
+// One 128-k stage of one m16 block: LOP3 unpack + IMMA against the stage's B words.
 template <int BITS, int NT>
-__device__ __forceinline__ void stage_mma(const uint8_t* T0, int r0, int lane, const uint8_t* bstage,
-                                          int (&acc)[Frag<BITS>::G][kMaxNT][4]) {
+__device__ __forceinline__ void stage_mma(const uint8_t* T0, int r0, int tq, const uint8_t* const (&bp)[kMaxNT],
+                                          int soff, int (&acc)[Frag<BITS>::G][kMaxNT][4]) {
     using FR = Frag<BITS>;
     constexpr int F = FR::F;
     uint32_t a[F][4];
-    FR::load(T0, T0 + tile_bytes(BITS), r0, lane & 3, a);
-    const uint8_t* bs = bstage + lane * 8;
+    FR::load(T0, T0 + tile_bytes(BITS), r0, tq, a);
 #pragma unroll
     for (int f = 0; f < F; ++f)
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
-            const uint2 b = *reinterpret_cast<const uint2*>(bs + (f * NT + j) * 256);
+            const uint2 b = *reinterpret_cast<const uint2*>(bp[j] + soff + f * 32);
             imma(acc[FR::grp(f)][j], a[f], b.x, b.y);
         }
 }
 
 template <int BITS, int NT>
-__device__ __forceinline__ void unit_mma(const uint8_t* U, int nst_u, int s0, int r0, int lane, const uint8_t* bb,
-                                         int (&acc)[Frag<BITS>::G][kMaxNT][4]) {
-    constexpr int F = Frag<BITS>::F, SB = 2 * tile_bytes(BITS);
-#pragma unroll 2
-    for (int s = 0; s < nst_u; ++s) stage_mma<BITS, NT>(U + s * SB, r0, lane, bb + size_t((s0 + s) * F) * NT * 256, acc);
-}
-
-__device__ __forceinline__ void scale_bias(const float* s, const float* b, int64_t idx, float& sc, float& bias) {
-    sc = __ldg(s + idx);
-    bias = b ? __ldg(b + idx) : 0.f;
+__device__ __forceinline__ void unit_mma(const uint8_t* U, int nst_u, int s0, int r0, int tq,
+                                         const uint8_t* const (&bp)[kMaxNT], int (&acc)[Frag<BITS>::G][kMaxNT][4]) {
+    using FR = Frag<BITS>;
+    constexpr int F = FR::F, US = unit_stages<BITS>();
+    constexpr int SB = 2 * tile_bytes(BITS), STG = RB<BITS>::STG;
+    if (nst_u == US) {
+        // full unit: every stage's A and B words are loaded before the first IMMA
+        // (two consumer warps per SM sub-partition cannot hide the LDS -> IMMA chain)
+        uint32_t a[US][F][4];
+        uint2 b[US][F][NT];
+#pragma unroll
+        for (int s = 0; s < US; ++s) {
+            const uint8_t* T0 = U + s * SB;
+            FR::load(T0, T0 + tile_bytes(BITS), r0, tq, a[s]);
+#pragma unroll
+            for (int f = 0; f < F; ++f)
+#pragma unroll
+                for (int j = 0; j < NT; ++j)
+                    b[s][f][j] = *reinterpret_cast<const uint2*>(bp[j] + (s0 + s) * STG + f * 32);
+        }
+#pragma unroll
+        for (int s = 0; s < US; ++s)
+#pragma unroll
+            for (int f = 0; f < F; ++f)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) imma(acc[FR::grp(f)][j], a[s][f], b[s][f][j].x, b[s][f][j].y);
+        return;
+    }
+#pragma unroll 1
+    for (int s = 0; s < nst_u; ++s) stage_mma<BITS, NT>(U + s * SB, r0, tq, bp, (s0 + s) * STG, acc);
 }
 
 // V * 2^-sh in fp32: one rounding (int64 -> fp32), exact power-of-two scale
@@ -312,103 +373,136 @@ __device__ __forceinline__ int fc2_exp(float smax, float bmax, float l1) {
 }
 
 // ---- smem layout (host and device agree) ------------------------------------------------
+// Fixed parts first, then the split-K partials (only for clusters of >= 2 CTAs,
+// sized by the cluster), then the weight ring takes everything that is left:
+// the in-flight bytes per SM are what bounds the stream at loaded HBM latency.
 template <int BITS, int PHASE>
 struct Layout {
-    static constexpr int NU = 116 * 1024 / Cfg<BITS>::UB;  // weight-copy ring slots (~96-112 KB in flight)
-    static constexpr size_t RING = size_t(NU) * Cfg<BITS>::UB;
-    static constexpr size_t BUFS = size_t(kBufs) * (kHead + Cfg<BITS>::BBUF);
-    static constexpr size_t SCR = size_t(TILE_N) * kScrCols * 4;
-    static constexpr size_t RED = size_t(kMaxCluster) * TILE_N * kPassRows * 8;  // int64 partials per rank
-    static constexpr size_t XS = PHASE == 1 ? TILE_N * kPassRows * 4 + kPassRows * 8 : 0;
-    static constexpr size_t BARS = size_t(2 * NU + 2 * kBufs + 2) * 8;
-    static constexpr size_t TOTAL = RING + BUFS + SCR + RED + XS + BARS + sizeof(GemvTables) + 64;
+    using R = RB<BITS>;
+    static constexpr int kMaxNU = 8;
+    static constexpr int XR = PHASE == 1 ? R::XR1 : R::XR2;
+    static constexpr int HDR = PHASE == 1 ? R::HDR1 : R::HDR2;
+    static constexpr int BUFS = kBufs * kPassRows * XR;
+    static constexpr int ZERO = rup(R::PB, 128);                               // all-zero plane (idle columns)
+    static constexpr int SCR = kScrBufs * TILE_N * kScrStride * 4;
+    static constexpr int STG = PHASE == 1 ? rup(kPassRows * 4 * R::STG + kEpiWarps * kPassRows * 8, 128) : 0;
+    static constexpr int TABLES = rup(int(sizeof(GemvTables)), 128);
+    static constexpr int BARS = rup((2 * kMaxNU + 2 * kBufs + 2 * kScrBufs + 2) * 8, 128);
+    static constexpr int O_ZERO = BUFS, O_SCR = O_ZERO + ZERO, O_STG = O_SCR + SCR, O_TAB = O_STG + STG;
+    static constexpr int O_BARS = O_TAB + TABLES, O_RED = O_BARS + BARS;
+    __host__ __device__ static constexpr int red_bytes(int cs) { return cs > 1 ? cs * TILE_N * kPassRows * 8 : 0; }
+    __host__ __device__ static constexpr int ring_off(int cs) { return rup(O_RED + red_bytes(cs), 128); }
+    __host__ __device__ static constexpr int nu(int cs) {
+        return (kSmemMax - ring_off(cs)) / Cfg<BITS>::UB < kMaxNU ? (kSmemMax - ring_off(cs)) / Cfg<BITS>::UB : kMaxNU;
+    }
+    __host__ __device__ static constexpr int total(int cs) { return ring_off(cs) + nu(cs) * Cfg<BITS>::UB; }
+    static_assert(nu(kMaxCluster) >= 2, "weight ring needs two slots");
 };
 
 template <int BITS, int PHASE>
-__global__ void __launch_bounds__(threads_of(PHASE), 1) k_gemv(GemvArgs g, Plan P) {
+__global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
     using FR = Frag<BITS>;
     using C = Cfg<BITS>;
+    using R = RB<BITS>;
     using L = Layout<BITS, PHASE>;
-    constexpr int F = FR::F, G = FR::G, NU = L::NU, UB = C::UB, US = C::US, SB = C::SB, TB = C::TB;
+    constexpr int F = FR::F, G = FR::G, UB = C::UB, US = C::US, SB = C::SB, TB = C::TB;
+    constexpr int XR = L::XR, HDR = L::HDR, PL = planes_of(PHASE);
     constexpr int LOGD = FR::D == 64 ? 6 : FR::D == 16 ? 4 : 0;
     constexpr long long Z = 1ll << (BITS - 1);
-    constexpr int PROD = PHASE == 1 ? kConsumers + kBuilders : kConsumers;
     extern __shared__ __align__(128) uint8_t smem[];
-    uint8_t* ring = smem;
-    uint8_t* bufs = ring + L::RING;                                   // [kBufs][head | fragments]
-    int* scr = reinterpret_cast<int*>(bufs + L::BUFS);                 // [128][16]
-    long long* red = reinterpret_cast<long long*>(reinterpret_cast<uint8_t*>(scr) + L::SCR);  // [CS][128][4]
-    int* xs = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(red) + L::RED);  // fc1: [128][4] + zs[4]
-    long long* zs = reinterpret_cast<long long*>(xs + TILE_N * kPassRows);
-    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(xs) + L::XS);
+    const int CS = int(cluster_nctas()), rank = int(cta_rank());
+    const int NU = L::nu(CS);
+    uint8_t* bufs = smem;                                                      // [kBufs][4 rows][XR]
+    const uint8_t* zero = smem + L::O_ZERO;                                    // zero plane
+    int* scr = reinterpret_cast<int*>(smem + L::O_SCR);                        // [2][128][kScrStride]
+    uint8_t* stg = smem + L::O_STG;                                            // fc1: [4 rows][4 planes][STG] + zred
+    GemvTables& TBL = *reinterpret_cast<GemvTables*>(smem + L::O_TAB);
+    long long* red = reinterpret_cast<long long*>(smem + L::O_RED);            // [CS][128][4]
+    uint8_t* ring = smem + L::ring_off(CS);                                    // [NU][UB]
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::O_BARS);
     uint64_t* empty = full + NU;
     uint64_t* bfull = empty + NU;
     uint64_t* bempty = bfull + kBufs;
-    uint64_t* red_full = bempty + kBufs;   // rank 0: every rank's partials landed
-    uint64_t* red_empty = red_full + 1;    // rank r: rank 0 consumed the previous partials
-    GemvTables& TBL = *reinterpret_cast<GemvTables*>(red_empty + 1);
-    __shared__ unsigned s_tn;
+    uint64_t* sfull = bempty + kBufs;
+    uint64_t* sempty = sfull + kScrBufs;
+    uint64_t* red_full = sempty + kScrBufs;  // rank 0: every other rank's partials landed
+    uint64_t* red_empty = red_full + 1;      // rank r: rank 0 consumed the previous partials
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int CS = int(cluster_nctas()), rank = int(cta_rank());
     const int Kp = PHASE == 1 ? g.Kp1 : g.Kp2;
     const int Np = PHASE == 1 ? g.Np1 : g.Np2;
     const int k0 = rank * kChunkK, nst = (min(kChunkK, Kp - k0) + kStageK - 1) / kStageK;
     const int nunits = (nst + US - 1) / US;
     if (threadIdx.x == 0) {
-        s_tn = 0;
         for (int s = 0; s < NU; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kConsumers); }
-        for (int b = 0; b < kBufs; ++b) { mbar_init(&bfull[b], 1); mbar_init(&bempty[b], kConsumers); }
-        mbar_init(red_full, kConsumers * CS);
+        for (int b = 0; b < kBufs; ++b) { mbar_init(&bfull[b], 1); mbar_init(&bempty[b], kConsumers + kEpiWarps); }
+        for (int b = 0; b < kScrBufs; ++b) { mbar_init(&sfull[b], kConsumers); mbar_init(&sempty[b], kEpiWarps); }
+        mbar_init(red_full, kEpiWarps * max(CS - 1, 1));
         mbar_init(red_empty, 1);
-        if (PHASE == 1) for (int t = 0; t < kPassRows; ++t) zs[t] = 0;
         fence_barrier_init();
     }
-    if (PHASE == 1) pdl_wait();  // routing plan (fc2: the plan is older than fc1's own wait)
+    for (int i = threadIdx.x; i < L::ZERO / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(const_cast<uint8_t*>(zero))[i] = make_uint4(0u, 0u, 0u, 0u);
+    if (PHASE == 1) pdl_wait();  // routing plan and fc1 row blocks (fc2: the plan is older than fc1's wait)
     const int n_gemv = P.meta[0];
     const int nmt = Np / TILE_N;
-    if (warp == 0 && n_gemv > 0) build_tables(TBL, P, n_gemv, nmt, lane);
+    if (warp == 0 && n_gemv > 0) build_tables(TBL, P, n_gemv, nmt, lane, PHASE == 1 ? g.T * g.topk : 0);
+    __syncthreads();
+    const int nitems = n_gemv > 0 ? TBL.start[n_gemv] : 0;
+    const int clu = int(blockIdx.x) / CS, nclu = int(gridDim.x) / CS;
+    for (int k = threadIdx.x; k < kItemCache; k += blockDim.x) {
+        const int i = clu + k * nclu;
+        if (i >= nitems) break;
+        const GemvItem it = item_at(i, TBL, n_gemv, nmt);
+        TBL.items[k] = make_int4(it.e, it.mt, it.row0, it.nrows);
+    }
     __syncthreads();
     cluster_sync();  // barriers of every CTA initialised before any remote arrive
     if (PHASE == 1) pdl_trigger();  // the fc2 grid may launch as CTAs of this grid retire
-    const int nitems = n_gemv > 0 ? TBL.start[n_gemv] : 0;
-    const int clu = int(blockIdx.x) / CS, nclu = int(gridDim.x) / CS;
-    const int nchunk2 = (g.Kp2 + kChunkK - 1) / kChunkK;
+    const int nch2 = (g.Kp2 + kChunkK - 1) / kChunkK;
     // trace rows: fc1 events in the first half of each CTA row, fc2 in the second
-    unsigned long long* tr = g.trace ? g.trace + (PHASE == 2 ? kTraceCap : 0) : nullptr;
+    constexpr int kSlots = kTraceCap / 2;
+    unsigned long long* tr = g.trace ? g.trace + size_t(blockIdx.x) * kTraceCap * 2 + (PHASE == 2 ? kTraceCap : 0) : nullptr;
+    if (tr && threadIdx.x == 0) { tr[0] = gtime_ns(); tr[1] = clock64(); }
 
-    if (warp == PROD) {
-        // ===== producer: weight copy units (+ fc2: the fragment slot of each item)
+    if (warp == kProdWarp) {
+        // ===== producer: each item's row blocks, then its weight copy units
         if (lane == 0) {
+            Tracer T = tracer(tr, 192, kSlots - 1);
             const uint64_t pol = policy_evict_first();
             bool waited = PHASE == 1;
             int slot = 0, sph = 0, seq = 0;
             const uint8_t* wbase0 = PHASE == 1 ? g.w1 : g.w2;
             const int64_t wstride = PHASE == 1 ? g.w1_stride : g.w2_stride;
             for (int i = clu; i < nitems; i += nclu, ++seq) {
-                const GemvItem it = item_at(i, TBL, n_gemv, nmt);
-                if (PHASE == 2 && seq > 0) {
-                    const int buf = seq % kBufs;
-                    mbar_wait(&bempty[buf], ((seq / kBufs) & 1) ^ 1);
-                    const uint32_t bytes = uint32_t(kHead + F * nt_of(2, it.nrows) * 256 * nst);
-                    mbar_arrive_expect_tx(&bfull[buf], bytes);
-                    bulk_g2s(bufs + size_t(buf) * (kHead + C::BBUF),
-                             g.xb + (int64_t(it.gp) * nchunk2 + rank) * g.xb_slot_bytes, bytes, &bfull[buf]);
-                }
+                const GemvItem it = item_of(seq, i, TBL, n_gemv, nmt);
+                const int b = seq % kBufs;
+                auto issue_rows = [&]() {
+                    mbar_wait(&bempty[b], ((seq / kBufs) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&bfull[b], uint32_t(it.nrows * XR));
+                    for (int t = 0; t < it.nrows; ++t) {
+                        const uint8_t* src =
+                            PHASE == 1 ? g.xr + (int64_t(it.row0 + t < kTokCache ? TBL.tok[it.row0 + t]
+                                                                                  : __ldg(P.perm_token + it.row0 + t)) *
+                                                     g.nch1 + rank) * XR
+                                       : g.xb + (int64_t(it.row0 + t) * nch2 + rank) * XR;
+                        bulk_g2s(bufs + (b * kPassRows + t) * XR, src, uint32_t(XR), &bfull[b]);
+                    }
+                };
+                if (!(PHASE == 2 && seq == 0)) issue_rows();
                 const uint8_t* wb = wbase0 + int64_t(it.e) * wstride + (int64_t(it.mt) * (Kp / TILE_K) + k0 / TILE_K) * TB;
                 for (int u = 0; u <= nunits; ++u) {
-                    // fc2, first item: its weights stream while fc1 finishes; the fragment
-                    // slot (written by fc1) is fetched once the ring is full or the item issued
+                    // fc2, first item: its weights stream while fc1 finishes; its row blocks
+                    // (written by fc1) are fetched once the ring is full or the item issued
                     if (PHASE == 2 && seq == 0 && !waited && (u == nunits || u == NU)) {
                         pdl_wait();
                         waited = true;
-                        const uint32_t bytes = uint32_t(kHead + F * nt_of(2, it.nrows) * 256 * nst);
-                        mbar_arrive_expect_tx(&bfull[0], bytes);
-                        bulk_g2s(bufs, g.xb + (int64_t(it.gp) * nchunk2 + rank) * g.xb_slot_bytes, bytes, &bfull[0]);
+                        issue_rows();
                     }
                     if (u == nunits) break;
                     const int bytes = min(US, nst - u * US) * SB;
                     mbar_wait(&empty[slot], sph ^ 1);
+                    T.ev(4, u == 0 ? 0 : 1, it, PHASE);
                     mbar_arrive_expect_tx(&full[slot], uint32_t(bytes));
                     bulk_g2s_hint(ring + size_t(slot) * UB, wb + int64_t(u) * UB, uint32_t(bytes), &full[slot], pol);
                     if (++slot == NU) { slot = 0; sph ^= 1; }
@@ -417,51 +511,29 @@ __global__ void __launch_bounds__(threads_of(PHASE), 1) k_gemv(GemvArgs g, Plan 
             if (!waited) pdl_wait();
         }
         __syncwarp();
-    } else if (PHASE == 1 && warp >= kConsumers) {
-        // ===== builders: builder b fills fragment buffer b (every kBufs-th item)
-        const int bw = warp - kConsumers;
-        const bool vec_h = g.h_f16 && (g.d % 8) == 0 && (reinterpret_cast<uintptr_t>(g.h) & 15) == 0;
-        int seq = bw;
-        for (int i = clu + bw * nclu; i < nitems; i += kBufs * nclu, seq += kBufs) {
-            const GemvItem it = item_at(i, TBL, n_gemv, nmt);
-            if (lane == 0) mbar_wait(&bempty[bw], ((seq / kBufs) & 1) ^ 1);
-            __syncwarp();
-            uint8_t* b = bufs + size_t(bw) * (kHead + C::BBUF);
-            Head& hd = *reinterpret_cast<Head*>(b);
-            for (int t = 0; t < it.nrows; ++t) build_row<BITS>(g, P, it, t, lane, vec_h, k0, nst, b + kHead, hd);
-            __syncwarp();
-            if (lane == 0) {
-                trace_ev(tr, &s_tn, 1, 1, it, PHASE);
-                mbar_arrive(&bfull[bw]);
-            }
-        }
     } else if (warp < kConsumers) {
         // ===== consumers: warp -> m16 block (16 channels) of the 128-channel item
-        const int r = lane & 15;  // epilogue: lane -> channel 16 warp + r, rows (lane >> 4) + 2 u
-        const uint32_t red_rank0 = map_rank(red, 0), full_rank0 = map_rank(red_full, 0);
+        const int gq = lane >> 2, tq = lane & 3;
+        const int r0 = 16 * warp + gq;
+        Tracer T = tracer(threadIdx.x == 0 ? tr : nullptr, 1, 128);
         int slot = 0, sph = 0, seq = 0;
         for (int i = clu; i < nitems; i += nclu, ++seq) {
-            const GemvItem it = item_at(i, TBL, n_gemv, nmt);
-            const int buf = seq % kBufs;
-            const int ch = it.mt * TILE_N + 16 * warp + r;
-            float sc = 0.f, bias = 0.f, gate[2] = {0.f, 0.f};  // epilogue operands, fetched early
-            int tok[2] = {0, 0};
-            float smax = 0.f, bmax = 0.f;
-            if (rank == 0) {
-                scale_bias(PHASE == 1 ? g.s1 : g.s2, PHASE == 1 ? g.b1 : g.b2, int64_t(it.e) * Np + ch, sc, bias);
-                if (PHASE == 1) { smax = __ldg(g.smax1 + it.e); bmax = __ldg(g.bmax1 + it.e); }
-                if (PHASE == 2)
+            const GemvItem it = item_of(seq, i, TBL, n_gemv, nmt);
+            const int b = seq % kBufs, sb = seq & 1;
+            const int NT = nt_of(PHASE, it.nrows), ncol = PL * it.nrows;
+            // B column c = s * nrows + t (plane s of row t); idle columns read the zero plane
+            const uint8_t* bp[kMaxNT];
 #pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const int t = (lane >> 4) + 2 * u;
-                        if (t < it.nrows) { gate[u] = P.perm_gate[it.row0 + t]; tok[u] = P.perm_token[it.row0 + t]; }
-                    }
+            const int inv = it.nrows == 1 ? 65536 : it.nrows == 2 ? 32768 : it.nrows == 3 ? 21846 : 16384;
+            for (int j = 0; j < kMaxNT; ++j) {
+                const int c = 8 * j + gq;
+                const int sq = (c * inv) >> 16;  // c / nrows (exact for c < 16)
+                const int t = c < ncol ? c - sq * it.nrows : 0, s = c < ncol ? sq : 0;
+                bp[j] = c < ncol ? bufs + (b * kPassRows + t) * XR + HDR + s * R::PB + tq * 8 : zero + tq * 8;
             }
-            mbar_wait(&bfull[buf], (seq / kBufs) & 1);
-            if (threadIdx.x == 0) trace_ev(tr, &s_tn, 2, 0, it, PHASE);
-            const uint8_t* bb = bufs + size_t(buf) * (kHead + C::BBUF);
-            const Head& hd = *reinterpret_cast<const Head*>(bb);
-            const int NT = nt_of(PHASE, it.nrows);
+            T.ev(2, 3, it, PHASE);
+            mbar_wait(&bfull[b], (seq / kBufs) & 1);
+            T.ev(2, 0, it, PHASE);
             int acc[G][kMaxNT][4];
 #pragma unroll
             for (int a = 0; a < G; ++a)
@@ -469,154 +541,202 @@ __global__ void __launch_bounds__(threads_of(PHASE), 1) k_gemv(GemvArgs g, Plan 
                 for (int j = 0; j < kMaxNT; ++j)
 #pragma unroll
                     for (int q = 0; q < 4; ++q) acc[a][j][q] = 0;
-            const int r0 = 16 * warp + (lane >> 2);
             for (int u = 0; u < nunits; ++u) {
                 mbar_wait(&full[slot], sph);
+                T.ev(5, u == 0 ? 0 : 1, it, PHASE);
                 const uint8_t* U = ring + size_t(slot) * UB;
                 const int ns = min(US, nst - u * US);
-                if (NT == 1) unit_mma<BITS, 1>(U, ns, u * US, r0, lane, bb + kHead, acc);
-                else unit_mma<BITS, 2>(U, ns, u * US, r0, lane, bb + kHead, acc);
+                if (g.dbg == 1) {
+                } else if (NT == 1) unit_mma<BITS, 1>(U, ns, u * US, r0, tq, bp, acc);
+                else unit_mma<BITS, 2>(U, ns, u * US, r0, tq, bp, acc);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[slot]);
                 if (++slot == NU) { slot = 0; sph ^= 1; }
             }
-            if (threadIdx.x == 0) trace_ev(tr, &s_tn, 2, 1, it, PHASE);
-            // groups -> D * Sum_k u * digit per (row, column) (exact in int32 for 1024-k chunks)
-            {
-                const int tq = lane & 3, gq = lane >> 2;
+            T.ev(2, 1, it, PHASE);
+            if (lane == 0) {
+                mbar_arrive(&bempty[b]);
+                mbar_wait(&sempty[sb], ((seq >> 1) & 1) ^ 1);
+            }
+            T.ev(2, 4, it, PHASE);
+            __syncwarp();
+            // groups -> D * Sum_k u * digit per (channel, column): exact in int32 for 1024-k chunks
+            int* sc = scr + sb * TILE_N * kScrStride;
 #pragma unroll
-                for (int j = 0; j < kMaxNT; ++j) {
-                    if (j >= NT) break;
+            for (int j = 0; j < kMaxNT; ++j) {
+                if (j >= NT) break;
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        int s = 0;
+                for (int hq = 0; hq < 2; ++hq) {
+                    int s0 = 0, s1 = 0;
 #pragma unroll
-                        for (int a = 0; a < G; ++a) s += FR::mult(a) * acc[a][j][q];
-                        scr[(16 * warp + gq + 8 * (q >> 1)) * kScrCols + 8 * j + 2 * tq + (q & 1)] = s;
+                    for (int a = 0; a < G; ++a) {
+                        s0 += FR::mult(a) * acc[a][j][2 * hq];
+                        s1 += FR::mult(a) * acc[a][j][2 * hq + 1];
                     }
+                    *reinterpret_cast<int2*>(sc + (r0 + 8 * hq) * kScrStride + 8 * j + 2 * tq) = make_int2(s0, s1);
                 }
             }
             __syncwarp();
-            // this chunk's exact partial: V = Sum_s 256^s S_s - D Z Sum X (int64) -> rank 0
-            const int PL = planes_of(PHASE), W = w_of(PHASE, NT);
-            const int* wr = scr + (16 * warp + r) * kScrCols;
-            if (lane == 0 && rank != 0) wait_cluster(red_empty, (seq & 1) ^ 1);  // rank 0 took the previous item
-            __syncwarp();
+            if (lane == 0) mbar_arrive(&sfull[sb]);
+        }
+    } else {
+        // ===== epilogue: thread = channel of the item's 128-channel tile
+        const int ch = threadIdx.x - kConsumers * 32;
+        const int ew = warp - kConsumers;
+        const uint32_t red_rank0 = map_rank(red, 0), full_rank0 = map_rank(red_full, 0);
+        Tracer T = tracer(ch == 0 ? tr : nullptr, 128, 192);
+        // fc1: this channel's byte positions in a fc2 stage block (k = ch within the stage)
+        int pos0 = 0, pos1 = -1;
+        if (PHASE == 1) {
+            const int q = (ch & 63) >> 4, kid = (ch >> 6) * 16 + (ch & 15);
+            bool first = true;
+            for (int f = 0; f < F; ++f)
+                for (int h = 0; h < 2; ++h)
+                    for (int i = 0; i < 4; ++i)
+                        if (FR::kidx(f, h, i) == kid) {
+                            const int o = f * 32 + q * 8 + h * 4 + i;
+                            if (first) { pos0 = o; first = false; } else pos1 = o;
+                        }
+        }
+        int seq = 0;
+        for (int i = clu; i < nitems; i += nclu, ++seq) {
+            const GemvItem it = item_of(seq, i, TBL, n_gemv, nmt);
+            const int b = seq % kBufs, sb = seq & 1;
+            const int chg = it.mt * TILE_N + ch;
+            float sc = 0.f, bias = 0.f, gate[kPassRows] = {0.f, 0.f, 0.f, 0.f};
+            int tok[kPassRows] = {0, 0, 0, 0};
+            float es = 0.f, eb = 0.f;
+            if (rank == 0) {  // epilogue operands, fetched before the wait
+                sc = __ldg((PHASE == 1 ? g.s1 : g.s2) + int64_t(it.e) * Np + chg);
+                const float* bb = PHASE == 1 ? g.b1 : g.b2;
+                bias = bb ? __ldg(bb + int64_t(it.e) * Np + chg) : 0.f;
+                if (PHASE == 1) { es = __ldg(g.smax1 + it.e); eb = __ldg(g.bmax1 + it.e); }
+                if (PHASE == 2)
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int t = (lane >> 4) + 2 * u;
+                    for (int t = 0; t < kPassRows; ++t)
+                        if (t < it.nrows) { gate[t] = __ldg(P.perm_gate + it.row0 + t); tok[t] = __ldg(P.perm_token + it.row0 + t); }
+            }
+            mbar_wait(&sfull[sb], (seq >> 1) & 1);
+            T.ev(3, 0, it, PHASE);
+            // exact partial of this chunk: V = Sum_s 256^s S_s - D Z Sum X (int64)
+            const uint8_t* rb = bufs + b * kPassRows * XR;
+            const int* srow = scr + sb * TILE_N * kScrStride + ch * kScrStride;
+            long long V[kPassRows];
+            int pe[kPassRows];
+            float l1[kPassRows];
+#pragma unroll
+            for (int t = 0; t < kPassRows; ++t) {
+                V[t] = 0;
+                pe[t] = kZeroRow;
+                l1[t] = 0.f;
                 if (t >= it.nrows) continue;
-                long long zsum = 0;
+                const uint8_t* hb = rb + t * XR;
+                long long zs = 0;
                 if (PHASE == 1) {
-                    zsum = hd.zsum[t];
+                    const XHead1 hd = *reinterpret_cast<const XHead1*>(hb);
+                    pe[t] = hd.p;
+                    l1[t] = hd.l1;
+                    zs = hd.zsum;
                 } else {
-                    for (int st = 0; st < nst; ++st) zsum += hd.zpart[st][t];
+                    pe[t] = *reinterpret_cast<const int*>(hb);
+                    for (int s = 0; s < nst; ++s) zs += *reinterpret_cast<const long long*>(hb + 64 + 8 * s);
                 }
-                long long V = -(long long)FR::D * Z * zsum;
-                for (int s = 0; s < PL; ++s) V += (long long)wr[s * W + t] << (8 * s);
-                const int idx = ((rank * TILE_N) + 16 * warp + r) * kPassRows + t;
-                if (rank == 0) red[idx] = V;
-                else st_cluster_s64(red_rank0 + uint32_t(idx) * 8u, V);
-            }
-            // exponents needed by rank 0 after the buffer is recycled
-            int pe[2] = {kZeroRow, kZeroRow};
-            float l1e[2] = {0.f, 0.f};
+                long long v = -(long long)FR::D * Z * zs;
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int t = (lane >> 4) + 2 * u;
-                if (t < it.nrows) { pe[u] = hd.p[t]; l1e[u] = PHASE == 1 ? hd.l1[t] : 0.f; }
+                for (int s = 0; s < PL; ++s) v += (long long)srow[s * it.nrows + t] << (8 * s);
+                V[t] = v;
             }
-            const float l1row = (PHASE == 1 && threadIdx.x < it.nrows) ? hd.l1[threadIdx.x] : 0.f;
             __syncwarp();
             if (lane == 0) {
-                mbar_arrive(&bempty[buf]);
-                arrive_cluster(full_rank0);  // this warp's partials are in rank 0's smem
+                mbar_arrive(&sempty[sb]);
+                mbar_arrive(&bempty[b]);
             }
-            if (threadIdx.x == 0) trace_ev(tr, &s_tn, 2, 3, it, PHASE);
-            if (rank != 0) continue;
-            // ===== rank 0: reduce the cluster's partials and finish the item
-            wait_cluster(red_full, seq & 1);
-            if (threadIdx.x == 0) trace_ev(tr, &s_tn, 2, 4, it, PHASE);
-            float y[2];
+            if (CS > 1) {  // split-K: every rank's partial into rank 0 (DSMEM), fixed-order sum there
+                if (rank != 0) {
+                    if (lane == 0) wait_cluster(red_empty, (seq & 1) ^ 1);  // rank 0 took the previous item
+                    __syncwarp();
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int t = (lane >> 4) + 2 * u;
-                long long V = 0;
-                if (t < it.nrows)
-                    for (int c = 0; c < CS; ++c) V += red[((c * TILE_N) + 16 * warp + r) * kPassRows + t];
-                y[u] = (t >= it.nrows || pe[u] == kZeroRow) ? 0.f : scale_pow2(V, pe[u] + LOGD);
+                    for (int t = 0; t < kPassRows; ++t)
+                        if (t < it.nrows) st_cluster_s64(red_rank0 + uint32_t(((rank * TILE_N + ch) * kPassRows + t) * 8), V[t]);
+                    __syncwarp();
+                    if (lane == 0) arrive_cluster(full_rank0);
+                    T.ev(3, 2, it, PHASE);
+                    continue;
+                }
+                if (lane == 0) wait_cluster(red_full, seq & 1);
+                __syncwarp();
+#pragma unroll
+                for (int t = 0; t < kPassRows; ++t)
+                    if (t < it.nrows)
+                        for (int r = 1; r < CS; ++r) V[t] += red[(r * TILE_N + ch) * kPassRows + t];
+                named_bar_sync(2, kEpiWarps * 32);  // every epilogue warp read red
+                if (ch >= 1 && ch < CS) arrive_cluster(map_rank(red_empty, ch));
             }
-            named_bar_sync(1, kConsumers * 32);  // every warp read red
-            if (threadIdx.x == 0) trace_ev(tr, &s_tn, 2, 6, it, PHASE);
-            if (threadIdx.x < CS && threadIdx.x > 0) arrive_cluster(map_rank(red_empty, threadIdx.x));
             if (PHASE == 2) {
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const int t = (lane >> 4) + 2 * u;
-                    if (t < it.nrows && ch < g.d) {
-                        const float yg = fmaf(y[u], sc, bias) * gate[u];
-                        const int64_t o = int64_t(tok[u]) * g.d + ch;
-                        if (g.out_acc) atomicAdd(g.out_acc + o, yg);  // top-2: two addends onto zero
-                        else if (g.out_f16) static_cast<__half*>(g.out)[o] = __float2half_rn(yg);
-                        else static_cast<float*>(g.out)[o] = yg;
-                    }
+                for (int t = 0; t < kPassRows; ++t) {
+                    if (t >= it.nrows || chg >= g.d) continue;
+                    const float y = pe[t] == kZeroRow ? 0.f : scale_pow2(V[t], pe[t] + LOGD);
+                    const float yg = fmaf(y, sc, bias) * gate[t];
+                    const int64_t o = int64_t(tok[t]) * g.d + chg;
+                    if (g.out_acc) atomicAdd(g.out_acc + o, yg);  // top-2: two addends onto zero
+                    else if (g.out_f16) static_cast<__half*>(g.out)[o] = __float2half_rn(yg);
+                    else static_cast<float*>(g.out)[o] = yg;
                 }
             } else {
-                // mid = ReLU(y s + b) in fc2 fixed point -> fc2 fragment stage mt % 8 of slot (pass, mt / 8)
+                // mid = ReLU(y s + b) in fc2 fixed point -> stage mt % 8 of the rows' fc2 blocks
+                long long* zred = reinterpret_cast<long long*>(stg + kPassRows * 4 * R::STG);  // [4 warps][4 rows]
+                int p2[kPassRows];
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const int t = (lane >> 4) + 2 * u;
+                for (int t = 0; t < kPassRows; ++t) {
+                    p2[t] = kZeroRow;
                     long long X2 = 0;
                     if (t < it.nrows) {
-                        const int p2 = fc2_exp<BITS>(smax, bmax, l1e[u]);
-                        const float mid = fmaxf(fmaf(y[u], sc, bias), 0.0f);  // ReLU, model.cpp:190
-                        X2 = p2 == kZeroRow ? 0 : __float2int_rn(ldexpf(mid, p2));
-                        xs[(16 * warp + r) * kPassRows + t] = int(X2);
-                    }
+                        p2[t] = fc2_exp<BITS>(es, eb, l1[t]);
+                        const float y = pe[t] == kZeroRow ? 0.f : scale_pow2(V[t], pe[t] + LOGD);
+                        const float mid = fmaxf(fmaf(y, sc, bias), 0.0f);  // ReLU, model.cpp:190
+                        X2 = p2[t] == kZeroRow ? 0 : __float2int_rn(ldexpf(mid, p2[t]));
+                        const uint32_t dg = (uint32_t(int(X2)) + 0x80808080u) ^ 0x80808080u;  // 4 signed digits
 #pragma unroll
-                    for (int off = 1; off < 16; off <<= 1) X2 += __shfl_xor_sync(0xffffffffu, X2, off);
-                    if (r == 0 && t < it.nrows)
-                        atomicAdd(reinterpret_cast<unsigned long long*>(&zs[t]), (unsigned long long)X2);
-                }
-                named_bar_sync(1, kConsumers * 32);  // all 128 channels of X2 are in xs
-                if (threadIdx.x == 0) trace_ev(tr, &s_tn, 2, 5, it, PHASE);
-                const int NT2 = nt_of(2, it.nrows), W2 = w_of(2, NT2);
-                uint8_t* sl = g.xb + (int64_t(it.gp) * nchunk2 + it.mt / kChunkStages) * g.xb_slot_bytes;
-                const int st2 = it.mt % kChunkStages;
-                uint8_t* bstage = sl + kHead + size_t(st2 * F) * NT2 * 256;
-                const int nwords = it.nrows * 4 * 4 * F;
-                for (int wd = threadIdx.x; wd < nwords; wd += kConsumers * 32) {
-                    const int f = wd % F, s = (wd / F) & 3, tq = (wd / (4 * F)) & 3, t = wd / (16 * F);
-                    uint32_t b[2];
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        uint32_t word = 0;
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const int k = FR::kidx(f, h, q);  // tile * 16 + code
-                            const int X = xs[(64 * (k >> 4) + 16 * tq + (k & 15)) * kPassRows + t];
-                            word |= ((((uint32_t(X) + 0x80808080u) ^ 0x80808080u) >> (8 * s)) & 0xffu) << (8 * q);
+                        for (int s = 0; s < 4; ++s) {
+                            uint8_t* pl = stg + (t * 4 + s) * R::STG;
+                            const uint8_t byte = uint8_t(dg >> (8 * s));
+                            pl[pos0] = byte;
+                            if (pos1 >= 0) pl[pos1] = byte;
                         }
-                        b[h] = word;
                     }
-                    const int col = s * W2 + t, j = col >> 3, gq = col & 7;
-                    __stcg(reinterpret_cast<uint2*>(bstage + (size_t(f) * NT2 + j) * 256 + (4 * gq + tq) * 8),
-                           make_uint2(b[0], b[1]));
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) X2 += __shfl_xor_sync(0xffffffffu, X2, off);
+                    if (lane == 0) zred[ew * kPassRows + t] = X2;
                 }
-                if (threadIdx.x == 0) trace_ev(tr, &s_tn, 2, 7, it, PHASE);
-                if (threadIdx.x < it.nrows) {
-                    const int t = threadIdx.x;
-                    Head* gh = reinterpret_cast<Head*>(sl);
-                    gh->zpart[st2][t] = zs[t];
-                    gh->p[t] = fc2_exp<BITS>(smax, bmax, l1row);  // the same value from every m-tile
+                named_bar_sync(2, kEpiWarps * 32);  // the stage blocks and warp sums are complete
+                const int st2 = it.mt % kChunkStages, c2 = it.mt / kChunkStages;
+                constexpr int V16 = R::STG / 16;
+                for (int idx = ch; idx < it.nrows * 4 * V16; idx += kEpiWarps * 32) {
+                    const int t = idx / (4 * V16), s = (idx / V16) & 3, u = idx % V16;
+                    uint8_t* dst = g.xb + (int64_t(it.row0 + t) * nch2 + c2) * R::XR2 + R::HDR2 + s * R::PB +
+                                   st2 * R::STG + 16 * u;
+                    *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(stg + (t * 4 + s) * R::STG + 16 * u);
                 }
-                named_bar_sync(1, kConsumers * 32);  // xs / zs reuse
-                if (threadIdx.x < kPassRows) zs[threadIdx.x] = 0;
+                if (ch < it.nrows) {
+                    const int t = ch;
+                    int p2t = kZeroRow;
+#pragma unroll
+                    for (int u = 0; u < kPassRows; ++u)
+                        if (u == t) p2t = p2[u];
+                    uint8_t* hb = g.xb + (int64_t(it.row0 + t) * nch2 + c2) * R::XR2;
+                    long long z = 0;
+                    for (int w = 0; w < kEpiWarps; ++w) z += zred[w * kPassRows + t];
+                    *reinterpret_cast<long long*>(hb + 64 + 8 * st2) = z;
+                    *reinterpret_cast<int*>(hb) = p2t;  // the same value from every m-tile of the pass
+                }
+                named_bar_sync(2, kEpiWarps * 32);  // stage blocks / warp sums reused by the next item
             }
-            if (threadIdx.x == 0) trace_ev(tr, &s_tn, 2, 2, it, PHASE);
+            T.ev(3, 2, it, PHASE);
         }
     }
     cluster_sync();  // no CTA leaves while a peer may still write its shared memory
+    if (tr && threadIdx.x == 0) { tr[2 * (kSlots - 1)] = gtime_ns(); tr[2 * (kSlots - 1) + 1] = clock64(); }
 }
 
 // ---- launch -----------------------------------------------------------------------------
@@ -646,18 +766,19 @@ cudaError_t launch_phase(const GemvArgs& g, const Plan& P, cudaStream_t st, int 
     auto kern = k_gemv<BITS, PHASE>;
     const int Kp = PHASE == 1 ? g.Kp1 : g.Kp2;
     const int cs = (Kp + kChunkK - 1) / kChunkK;
+    const int smem = L::total(cs);
     static bool configured = false;
     static int ncl[kMaxCluster + 1] = {0};
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::TOTAL));
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    if (ncl[cs] == 0) ncl[cs] = active_clusters(kern, cs, L::TOTAL, threads_of(PHASE), num_sms);
+    if (ncl[cs] == 0) ncl[cs] = active_clusters(kern, cs, smem, kGemvThreads, num_sms);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(ncl[cs] * cs));
-    cfg.blockDim = dim3(threads_of(PHASE));
-    cfg.dynamicSmemBytes = L::TOTAL;
+    cfg.blockDim = dim3(kGemvThreads);
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -682,18 +803,23 @@ cudaError_t launch_gemv_t(const GemvArgs& g, const Plan& P, cudaStream_t st, int
 bool gemv_supported(int Kp1, int Kp2) {
     return Kp1 <= kMaxCluster * kChunkK && Kp2 <= kMaxCluster * kChunkK && Kp2 >= kStageK;
 }
-int64_t gemv_xb_slot_bytes(int bits) {
+int64_t gemv_xr_bytes(int bits) {
     switch (bits) {
-        case 2: return Cfg<2>::SLOT;
-        case 3: return Cfg<3>::SLOT;
-        case 4: return Cfg<4>::SLOT;
+        case 2: return RB<2>::XR1;
+        case 3: return RB<3>::XR1;
+        case 4: return RB<4>::XR1;
     }
-    return Cfg<8>::SLOT;
+    return RB<8>::XR1;
 }
-// every listed expert may end in a partial pass; one slot per (pass, 1024-k chunk of fc2)
-int64_t gemv_xb_slots(int64_t rows, int E, int Kp2) {
-    return ((rows + kPassRows - 1) / kPassRows + E) * ((Kp2 + kChunkK - 1) / kChunkK);
+int64_t gemv_xb_bytes(int bits) {
+    switch (bits) {
+        case 2: return RB<2>::XR2;
+        case 3: return RB<3>::XR2;
+        case 4: return RB<4>::XR2;
+    }
+    return RB<8>::XR2;
 }
+int gemv_chunks(int Kp) { return (Kp + kChunkK - 1) / kChunkK; }
 
 cudaError_t launch_gemv(int bits, const GemvArgs& g, const Plan& P, cudaStream_t st, int num_sms) {
     if (!gemv_supported(g.Kp1, g.Kp2)) return cudaErrorInvalidValue;
@@ -704,6 +830,19 @@ cudaError_t launch_gemv(int bits, const GemvArgs& g, const Plan& P, cudaStream_t
         case 8: return launch_gemv_t<8>(g, P, st, num_sms);
     }
     return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_xrows(int bits, const XrowArgs& a, cudaStream_t st) {
+    if (a.T <= 0) return cudaSuccess;
+    const unsigned grid = unsigned((a.T * a.nch1 + 3) / 4);
+    switch (bits) {
+        case 2: k_xrows<2><<<grid, 128, 0, st>>>(a); break;
+        case 3: k_xrows<3><<<grid, 128, 0, st>>>(a); break;
+        case 4: k_xrows<4><<<grid, 128, 0, st>>>(a); break;
+        case 8: k_xrows<8><<<grid, 128, 0, st>>>(a); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
 }
 
 // Per expert: max fc1 scale and max |fc1 bias| — the constants of the fc2

@@ -42,6 +42,7 @@ struct RouteArgs {
     int gemm_bn;         // GEMM n-tile rows, for tile counting
     float* zero_out;     // top-2 fp32 accumulation rows to zero (inline scatter), or null
     unsigned long long* trace;  // router phase stamps [kTraceRouteCtas][16] or null (diagnostics)
+    int pdl;                    // launched behind k_xrows: the decode router may start early (PDL)
 };
 constexpr int kTraceRouteCtas = 64;
 cudaError_t launch_route(const RouteArgs& a, const Plan& P, cudaStream_t st);
@@ -74,19 +75,30 @@ struct GemvArgs {
     void* out;                     // [T][d] (top-1 direct store)
     int out_f16;
     float* out_acc;                // [T][d] fp32 (top-2 accumulation, 2 addends per element) or null
-    uint8_t* xb;                   // fc2 activation fragments: one slot per (row pass, 1024-k chunk)
-    int64_t xb_slot_bytes;
+    const uint8_t* xr;             // fc1 row blocks [T][nch1][xr bytes] (k_xrows)
+    int nch1;                      // 1024-k chunks of fc1
+    uint8_t* xb;                   // fc2 row blocks [T*k][nch2][xb bytes] (written by the fc1 epilogue)
     const float* smax1;            // [E] max fc1 scale (bounds the fc2 fixed-point exponent)
     const float* bmax1;            // [E] max |fc1 bias|
     unsigned long long* trace;     // [grid][kTraceCap][2] (time ns, event) or null
-    int dbg;                       // diagnostics (env MOQE_GEMV_DBG): 1 = builders skip the conversion
+    int dbg;                       // diagnostics (env MOQE_GEMV_DBG; 1 = consumers skip the MMA work)
 };
 constexpr int kTraceCap = 512;
 cudaError_t launch_gemv(int bits, const GemvArgs& g, const Plan& P, cudaStream_t st, int num_sms);
 bool gemv_supported(int Kp1, int Kp2);
-// fc2 fragment slots for `rows` GEMV rows over `E` experts
-int64_t gemv_xb_slot_bytes(int bits);
-int64_t gemv_xb_slots(int64_t rows, int E, int Kp2);
+// Token rows -> fc1 row blocks (fixed-point digit planes in IMMA fragment order).
+struct XrowArgs {
+    const void* h;
+    int h_f16;
+    int64_t T;
+    int d;
+    int nch1;
+    uint8_t* xr;
+};
+cudaError_t launch_xrows(int bits, const XrowArgs& a, cudaStream_t st);
+int64_t gemv_xr_bytes(int bits);  // one fc1 row block (per token and 1024-k chunk)
+int64_t gemv_xb_bytes(int bits);  // one fc2 row block (per routed row and 1024-k chunk)
+int gemv_chunks(int Kp);
 cudaError_t launch_expert_max(const float* s1, const float* b1, int E, int Np1, float* smax, float* bmax,
                               cudaStream_t st);
 

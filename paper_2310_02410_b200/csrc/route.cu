@@ -648,6 +648,9 @@ __global__ void __launch_bounds__((kRouteSmallWarps + 1) * 32, 1) k_route_decode
         __syncthreads();
         if (threadIdx.x == 0) tr[12] = gtime_ns();
     }
+    // launched behind k_xrows (PDL): finish only after it, so the expert-FFN grid's
+    // own dependency wait on this grid covers the row blocks too
+    if (threadIdx.x == 0) pdl_wait();
 }
 
 // ---- large T (prefill) ----------------------------------------------------------------
@@ -853,13 +856,15 @@ cudaError_t launch_dec(const RouteArgs& a, const Plan& P, size_t smem, cudaStrea
     cfg.blockDim = dim3((kRouteSmallWarps + 1) * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = nct;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = a.pdl ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, k_route_decode<EPL, EFIX>, a, P);
 }
 }  // namespace

@@ -43,7 +43,18 @@ m.moe_ffn_forward(h, bank, top_k=1)
 tr, rt = bank.trace_read()
 if a.dump:
     np.save(a.dump, tr)
-t = tr[:, :, 0].astype(np.int64)
+# each CTA row: two halves (fc1, fc2) of S slots; slot 0 / S-1 = (globaltimer, clock64) anchors
+S = tr.shape[1] // 2
+raw = tr.astype(np.int64)
+t = np.zeros(tr.shape[:2], dtype=np.int64)
+for hlf in range(2):
+    blk = raw[:, hlf * S:(hlf + 1) * S]
+    g0, c0_, g1, c1_ = blk[:, 0, 0], blk[:, 0, 1], blk[:, S - 1, 0], blk[:, S - 1, 1]
+    ok = (g0 > 0) & (g1 > g0) & (c1_ > c0_)
+    rate = np.where(ok, (g1 - g0) / np.maximum(c1_ - c0_, 1), 0.0)  # ns per clock
+    ev_ok = (blk[:, 1:S - 1, 1] & 1) == 1
+    tt = g0[:, None] + (blk[:, 1:S - 1, 0] - c0_[:, None]) * rate[:, None]
+    t[:, hlf * S + 1:(hlf + 1) * S - 1] = np.where(ev_ok & ok[:, None], tt, 0).astype(np.int64)
 w = tr[:, :, 1]
 valid = t > 0
 t0 = t[valid].min()
@@ -60,39 +71,46 @@ us = (t - t0) / 1e3
 print(f"CTAs {tr.shape[0]}, events {valid.sum()}, span {us[valid].max():.2f} us")
 
 for phase in (1, 2):
-    sel_s = valid & (role == 2) & (ev == 0) & (ph == phase)
-    sel_e = valid & (role == 2) & (ev == 2) & (ph == phase)
-    if sel_s.any():
-        print(f"phase {phase}: items {sel_s.sum()}  first start {us[sel_s].min():.2f}  last start {us[sel_s].max():.2f}  "
-              f"first end {us[sel_e].min():.2f}  last end {us[sel_e].max():.2f} us")
-        durs = []
-        for c in range(tr.shape[0]):
-            st = sorted(us[c][sel_s[c]]); en = sorted(us[c][sel_e[c]])
-            durs += [b - a for a, b in zip(st, en)]
-        if durs:
-            print(f"   item start->end: mean {np.mean(durs):.2f} p50 {np.median(durs):.2f} max {np.max(durs):.2f} us (rank-0 CTAs incl. reduction)")
-        sel_m = valid & (role == 2) & (ev == 1) & (ph == phase)
-        ml = []
-        gaps = []
-        for c in range(tr.shape[0]):
-            st = sorted(us[c][sel_s[c]]); mm = sorted(us[c][sel_m[c]]); en = sorted(us[c][sel_e[c]])
-            ml += [b - a for a, b in zip(st, mm)]
-            gaps += [b - a for a, b in zip(en[:-1], st[1:])]
-        if ml:
-            print(f"   mainloop: mean {np.mean(ml):.2f} us; gap end->next start: mean {np.mean(gaps) if gaps else 0:.2f} max {np.max(gaps) if gaps else 0:.2f}")
-        evs = {}
-        cyc = {}
-        for c in range(tr.shape[0]):
-            sel = valid[c] & (role[c] == 2) & (ph[c] == phase)
-            tt = us[c][sel]; ee = ev[c][sel]; cc = (w[c][sel] & np.uint64(0xffff)).astype(np.int64)
-            order = np.argsort(tt, kind="stable")
-            tt = tt[order]; ee = ee[order]; cc = cc[order]
-            for k in range(1, len(tt)):
-                if ee[k] != 0:
-                    evs.setdefault((ee[k - 1], ee[k]), []).append(tt[k] - tt[k - 1])
-                    cyc.setdefault((ee[k - 1], ee[k]), []).append((cc[k] - cc[k - 1]) % 65536)
-        print("   segments: " + "  ".join(f"{a}->{b}: {np.mean(v):.2f}" for (a, b), v in sorted(evs.items())))
-        print("   cycles:   " + "  ".join(f"{a}->{b}: {np.mean(v):.0f}" for (a, b), v in sorted(cyc.items())))
-        sel_b = valid & (role == 1) & (ev == 1) & (ph == phase)
-        if sel_b.any():
-            print(f"   builder done: first {us[sel_b].min():.2f} median {np.median(us[sel_b]):.2f} last {us[sel_b].max():.2f}")
+    c0 = valid & (role == 2) & (ev == 0) & (ph == phase)
+    c1 = valid & (role == 2) & (ev == 1) & (ph == phase)
+    e0 = valid & (role == 3) & (ev == 0) & (ph == phase)
+    e2 = valid & (role == 3) & (ev == 2) & (ph == phase)
+    if not c0.any():
+        continue
+    print(f"phase {phase}: items {c0.sum()}  consumer first start {us[c0].min():.2f} last mainloop end {us[c1].max():.2f}  "
+          f"epilogue first end {us[e2].min():.2f} last end {us[e2].max():.2f} us")
+    ml, ep, gap, lag = [], [], [], []
+    for c in range(tr.shape[0]):
+        a = sorted(us[c][c0[c]]); b = sorted(us[c][c1[c]]); x = sorted(us[c][e0[c]]); y = sorted(us[c][e2[c]])
+        ml += [q - p for p, q in zip(a, b)]
+        gap += [q - p for p, q in zip(b[:-1], a[1:])]
+        ep += [q - p for p, q in zip(x, y)]
+        lag += [q - p for p, q in zip(b, y)]
+    f = lambda v: f"{np.mean(v):.2f}" if v else "-"
+    print(f"   per item: mainloop {f(ml)}  consumer gap {f(gap)}  epilogue {f(ep)}  mainloop-end -> epilogue-end {f(lag)} us")
+    # unit latency: k-th issue (role 4) -> k-th landed (role 5), per CTA in order
+    lat, bw, top, sw = [], [], [], []
+    for c in range(tr.shape[0]):
+        iss = sorted(us[c][valid[c] & (role[c] == 4) & (ph[c] == phase)])
+        lnd = sorted(us[c][valid[c] & (role[c] == 5) & (ph[c] == phase)])
+        lat += [q - p for p, q in zip(iss, lnd)]
+        w3 = sorted(us[c][valid[c] & (role[c] == 2) & (ev[c] == 3) & (ph[c] == phase)])
+        w0 = sorted(us[c][c0[c]])
+        bw += [q - p for p, q in zip(w3, w0)]
+        if iss: top.append(iss[0])
+        w4 = sorted(us[c][valid[c] & (role[c] == 2) & (ev[c] == 4) & (ph[c] == phase)])
+        sw.extend([q - p for p, q in zip(b, w4)])
+    print(f"   unit issue->landed {f(lat)} (max {max(lat) if lat else 0:.2f})  consumer bfull wait {f(bw)}  first issue {min(top) if top else 0:.2f} us  scratch wait {f(sw)}")
+
+if os.environ.get("TRACE_CTA"):
+    c = int(os.environ["TRACE_CTA"])
+    names = {(2, 3): "C top", (2, 0): "C bfull ok", (5, 0): "C unit0 in", (5, 1): "C unit+ in", (2, 1): "C mloop end",
+             (2, 4): "C scr ok", (3, 0): "E start", (3, 2): "E end", (4, 0): "P unit0 iss", (4, 1): "P unit+ iss"}
+    sel = valid[c]
+    order = np.argsort(us[c][sel], kind="stable")
+    rr, ee, pp, tt = role[c][sel][order], ev[c][sel][order], ph[c][sel][order], us[c][sel][order]
+    mt = ((w[c][sel][order] >> np.uint64(20)) & np.uint64(0xfff)).astype(int)
+    ex = ((w[c][sel][order] >> np.uint64(32)) & np.uint64(0xffff)).astype(int)
+    for a, b, p_, t_, m_, e_ in zip(rr, ee, pp, tt, mt, ex):
+        if p_ == 1:
+            print(f"{t_:8.2f}  {names.get((a, b), (a, b))!s:12s} e{e_} mt{m_}")
