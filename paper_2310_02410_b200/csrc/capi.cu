@@ -355,6 +355,9 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
         eff_path = MOQE_PATH_GEMM;
     }
     if (eff_path == MOQE_PATH_AUTO && R <= 4 * kGemvMaxRows) eff_path = MOQE_PATH_GEMV;
+    // Large batches: experts almost never stay within GEMV size, and the GEMV
+    // launches (+ token-row encoding) would cost ~15 us of empty work.
+    if (eff_path == MOQE_PATH_AUTO && R > 1024) eff_path = MOQE_PATH_GEMM;
     const bool need_gemm = eff_path == MOQE_PATH_GEMM || (eff_path == MOQE_PATH_AUTO && R > kGemvMaxRows);
     const bool need_gemv = eff_path != MOQE_PATH_GEMM;
     const bool inline_scatter = !need_gemm && R <= 256;

@@ -118,18 +118,30 @@ __device__ void plan_lists(const RouteArgs& a, Plan& P, const int* cnt, int* s_o
 __device__ void plan_tail(const RouteArgs& a, Plan P, int n_ctas, int tt, int* scr, int scr_ints) {
     const int E = a.E, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nw = blockDim.x >> 5;
-    const bool staged = scr != nullptr && int64_t(n_ctas) * E <= scr_ints;
+    const bool staged = scr != nullptr && int64_t(n_ctas) * E + E <= scr_ints;
+    int* s_cnt = staged ? scr + n_ctas * E : nullptr;
     if (staged) {
         for (int i = threadIdx.x; i < n_ctas * E; i += blockDim.x) scr[i] = __ldcg(P.cta_counts + i);
         __syncthreads();
-        for (int e = threadIdx.x; e < E; e += blockDim.x) {
-            int run = 0;
-            for (int c = 0; c < n_ctas; ++c) {
-                const int v = scr[c * E + e];
-                scr[c * E + e] = run;
-                run += v;
+        // 1. exclusive scan over CTAs per expert: warp per expert, shuffle scans
+        for (int e = warp; e < E; e += nw) {
+            int running = 0;
+            for (int c0 = 0; c0 < n_ctas; c0 += 32) {
+                const int c = c0 + lane;
+                const int v = c < n_ctas ? scr[c * E + e] : 0;
+                int incl = v;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, off);
+                    if (lane >= off) incl += y;
+                }
+                if (c < n_ctas) scr[c * E + e] = running + incl - v;
+                running += __shfl_sync(0xffffffffu, incl, 31);
             }
-            P.counts[e] = run;
+            if (lane == 0) {
+                s_cnt[e] = running;
+                P.counts[e] = running;
+            }
         }
         __syncthreads();
         for (int i = threadIdx.x; i < n_ctas * E; i += blockDim.x) P.cta_counts[i] = scr[i];
@@ -162,7 +174,7 @@ __device__ void plan_tail(const RouteArgs& a, Plan P, int n_ctas, int tt, int* s
     }
     __syncthreads();
     // 2. offsets + expert lists (warp 0, expert order)
-    plan_lists(a, P, P.counts, nullptr);
+    plan_lists(a, P, staged ? s_cnt : P.counts, nullptr);
     for (int e = threadIdx.x; e < E; e += blockDim.x) P.done[e] = 0;
     __syncthreads();
     // 3. small problems: scatter routing metadata here (no extra launch)
@@ -653,6 +665,122 @@ __global__ void __launch_bounds__((kRouteSmallWarps + 1) * 32, 1) k_route_decode
     if (threadIdx.x == 0) pdl_wait();
 }
 
+// ---- large T, E in {32, 64}, fp16 rows with d % 8 == 0 (the prefill shapes) ----------
+// CTA = 32 tokens x all E experts; 8 compute warps, warp w owns experts
+// [w*EPL, (w+1)*EPL) (EPL = E/8) for the 32 tokens of its lanes, so each lane runs
+// EPL independent exact chains (FMUL then FADD, ascending k, zero activations
+// skipped) and the FADD latency is covered without CTA-wide barriers. A producer
+// warp stages the 32 token rows once (TMA, padded rows: conflict-free LDS.128) and
+// streams Wg through an mbarrier ring in 128-row chunks.
+constexpr int kRL2Warps = 8, kRL2Rows = 128;
+__host__ __device__ constexpr int rl2_hstride(int d) { return d * 2 + 16; }
+__host__ __device__ constexpr int rl2_slots(int E) { return E <= 32 ? 6 : 4; }
+size_t rl2_smem(int d, int E) {
+    return size_t((32 * rl2_hstride(d) + 127) / 128 * 128) + size_t(rl2_slots(E)) * kRL2Rows * E * 4 + 256 +
+           size_t(32) * (E + 1) * 4;
+}
+
+template <int EPL>
+__global__ void __launch_bounds__((kRL2Warps + 1) * 32, 1) k_route_logits2(RouteArgs a, Plan P) {
+    constexpr int E = 8 * EPL, NS = rl2_slots(8 * EPL);
+    extern __shared__ __align__(128) uint8_t sm[];
+    const int d = a.d, hs = rl2_hstride(d);
+    float* ring = reinterpret_cast<float*>(sm + (32 * hs + 127) / 128 * 128);
+    uint64_t* hbar = reinterpret_cast<uint64_t*>(ring + NS * kRL2Rows * E);
+    uint64_t* full = hbar + 1;
+    uint64_t* empty = full + NS;
+    float* s_l = reinterpret_cast<float*>(empty + NS);  // [32 tokens][E + 1] logits of this CTA
+    __shared__ int s_exp[64];
+    __shared__ int s_hist[256];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t t0 = int64_t(blockIdx.x) * 32;
+    for (int e = threadIdx.x; e < E; e += blockDim.x) s_hist[e] = 0;
+    const int ntok = a.T - t0 < 32 ? int(a.T - t0) : 32;
+    const int nch = (d + kRL2Rows - 1) / kRL2Rows;
+    if (threadIdx.x == 0) {
+        mbar_init(hbar, 1);
+        for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kRL2Warps); }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (warp == kRL2Warps) {
+        if (lane == 0) {
+            const __half* h = static_cast<const __half*>(a.h);
+            mbar_arrive_expect_tx(hbar, uint32_t(ntok * d * 2));
+            for (int r = 0; r < ntok; ++r) bulk_g2s(sm + r * hs, h + (t0 + r) * d, uint32_t(d * 2), hbar);
+            for (int c = 0; c < nch; ++c) {
+                const int s = c % NS;
+                if (c >= NS) mbar_wait(&empty[s], ((c / NS) - 1) & 1);
+                const int nr = min(kRL2Rows, d - c * kRL2Rows);
+                mbar_arrive_expect_tx(&full[s], uint32_t(nr * E * 4));
+                bulk_g2s(ring + s * kRL2Rows * E, a.wg + int64_t(c) * kRL2Rows * E, uint32_t(nr * E * 4), &full[s]);
+            }
+        }
+        __syncwarp();
+    } else {
+    const bool live = lane < ntok;
+    const uint8_t* hr = sm + lane * hs;
+    float acc[EPL];
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) acc[e] = 0.0f;
+    mbar_wait(hbar, 0);
+    for (int c = 0; c < nch; ++c) {
+        const int s = c % NS;
+        mbar_wait(&full[s], (c / NS) & 1);
+        const float* wc = ring + s * kRL2Rows * E + warp * EPL;
+        const int nr = min(kRL2Rows, d - c * kRL2Rows);  // a multiple of 8
+        const uint8_t* hc = hr + c * kRL2Rows * 2;
+#pragma unroll 2
+        for (int q = 0; q < nr; q += 8) {
+            const uint4 hv = *reinterpret_cast<const uint4*>(hc + q * 2);
+            const __half2* h2 = reinterpret_cast<const __half2*>(&hv);
+            float x[8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float2 f = __half22float2(h2[i]);
+                x[2 * i] = f.x;
+                x[2 * i + 1] = f.y;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                float w[EPL];
+#pragma unroll
+                for (int e = 0; e < EPL; e += 4) {
+                    const float4 v = *reinterpret_cast<const float4*>(wc + (q + u) * E + e);
+                    w[e] = v.x; w[e + 1] = v.y; w[e + 2] = v.z; w[e + 3] = v.w;
+                }
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) {
+                    // reference: `if (av == 0.0f) continue; orow[j] += av * brow[j];`
+                    const float pr = __fmul_rn(x[u], w[e]);
+                    if (x[u] != 0.0f) acc[e] = __fadd_rn(acc[e], pr);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) s_l[lane * (E + 1) + warp * EPL + e] = acc[e];
+    named_bar_sync(1, kRL2Warps * 32);  // all 32 x E logits of the CTA in smem
+    // selection: warp w finishes tokens 4w .. 4w+3 (lane j <-> experts j, j + 32)
+    for (int lt = 4 * warp; lt < 4 * warp + 4; ++lt) {
+        if (lt < ntok) {
+            float l[E / 32];
+#pragma unroll
+            for (int e = 0; e < E / 32; ++e) l[e] = s_l[lt * (E + 1) + lane + 32 * e];
+            finish_token<E / 32>(a, P, l, t0 + lt, lt, s_exp);
+        } else if (lane == 0) {
+            s_exp[lt * a.topk] = -1;
+            if (a.topk == 2) s_exp[lt * a.topk + 1] = -1;
+        }
+    }
+    }
+    // ranks, CTA histogram, last-CTA plan (every thread of the CTA takes part;
+    // the drained Wg ring stages the per-CTA histograms)
+    ranks_hist_plan(a, P, s_exp, s_hist, 32, reinterpret_cast<int*>(ring), NS * kRL2Rows * E);
+}
+
 // ---- large T (prefill) ----------------------------------------------------------------
 // k_route_logits: one warp = 32 tokens (lane = token) x 8 experts; a CTA = 4
 // warps = 32 tokens x 32 experts, grid (T/32, E/32). Each Wg row is a smem
@@ -890,7 +1018,19 @@ cudaError_t launch_route(const RouteArgs& a, const Plan& P, cudaStream_t st) {
         if (P.logits == nullptr) return cudaErrorInvalidValue;
         dim3 lg(unsigned((a.T + kRLTok - 1) / kRLTok), unsigned((a.E + kRLExp - 1) / kRLExp));
         const bool vec = a.h_f16 && (a.d % 8) == 0 && (a.E % 32) == 0 && (reinterpret_cast<uintptr_t>(a.h) & 15) == 0;
-        if (vec) k_route_logits<true><<<lg, 128, 0, st>>>(a, P.logits);
+        const size_t sm2 = rl2_smem(a.d, a.E);
+        if (vec && (a.E == 32 || a.E == 64) && sm2 <= 220 * 1024 && (reinterpret_cast<uintptr_t>(a.wg) & 15) == 0) {
+            static bool cfg32 = false, cfg64 = false;
+            const unsigned g2 = unsigned((a.T + 31) / 32);
+            if (a.E == 32) {
+                if (!cfg32) { cudaFuncSetAttribute(k_route_logits2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); cfg32 = true; }
+                k_route_logits2<4><<<g2, (kRL2Warps + 1) * 32, sm2, st>>>(a, P);
+            } else {
+                if (!cfg64) { cudaFuncSetAttribute(k_route_logits2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); cfg64 = true; }
+                k_route_logits2<8><<<g2, (kRL2Warps + 1) * 32, sm2, st>>>(a, P);
+            }
+            return cudaGetLastError();  // selection and plan are fused into the logits kernel
+        } else if (vec) k_route_logits<true><<<lg, 128, 0, st>>>(a, P.logits);
         else k_route_logits<false><<<lg, 128, 0, st>>>(a, P.logits);
         k_route_select<<<grid, kRouteSelWarps * 32, 0, st>>>(a, P);
         return cudaGetLastError();
