@@ -266,7 +266,7 @@ def run_point(m, torch, E, d, f, bits, T, top_k, steps, warmup, dev, hbm_peak, t
         achieved = per_launch / (avg_launch_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(achieved / hbm_peak, 4), "traffic": None,
-                "kernel": "k_ffn_gemv", "bytes_per_launch": int(per_launch),
+                "kernel": "k_gemv fc1+fc2", "bytes_per_launch": int(per_launch),
                 "avg_launch_us": round(avg_launch_ms * 1e3, 3)}
     else:
         # each tcgen05 phase is half of the expert-FFN FLOPs (2*d*f*T*k per phase)
@@ -293,7 +293,9 @@ def run_point(m, torch, E, d, f, bits, T, top_k, steps, warmup, dev, hbm_peak, t
         "touched_experts": touched, "roofline": roof,
         "kernel_share": {KINDS[k]: round(float(prof_ms[k] / max(prof_ms.sum(), 1e-12)), 4)
                          for k in range(6) if prof_n[k]},
-        "launches_per_step": int(round(prof_n.sum() / max(1, -(-steps // len(layers)) * len(layers)))),
+        # kernels per forward: a "gemv" scope launches k_gemv fc1 + fc2 and is preceded by
+        # k_xrows (token-row encoding, timed inside the "route" scope)
+        "launches_per_step": int(round((prof_n.sum() + 2 * prof_n[2]) / max(1, -(-steps // len(layers)) * len(layers)))),
     }
     return res, layers
 

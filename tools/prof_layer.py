@@ -1,6 +1,6 @@
 """Profiling driver (ncu target): one MoE layer, a few forwards, nothing else.
 
-usage: python tools/prof_layer.py [--bits 3] [--tokens 24] [--experts 32] [--d 1024] [--f 4096]
+usage: python tools/prof_layer.py [--bits 3] [--tokens 24] [--experts 32] [--d 1024] [--f 4096] [--banks 1]
                                   [--top-k 1] [--iters 3] [--path auto]
 Weights are random fp32 N(0, 0.02) quantized on the GPU; activations N(0,1) fp16.
 """
@@ -22,15 +22,17 @@ ap.add_argument("--f", type=int, default=4096)
 ap.add_argument("--top-k", type=int, default=1)
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--path", default="auto")
+ap.add_argument("--banks", type=int, default=1, help="rotate over N weight copies (N x weights > L2 = cold)")
 a = ap.parse_args()
 g = torch.Generator(device="cuda").manual_seed(1)
 w1 = torch.randn(a.experts, a.d, a.f, device="cuda", generator=g) * 0.02
 w2 = torch.randn(a.experts, a.f, a.d, device="cuda", generator=g) * 0.02
 wg = torch.randn(a.d, a.experts, device="cuda", generator=g) * 0.02
-bank = m.ExpertBank.from_float(w1, w2, a.bits, router=wg)
+banks = [m.ExpertBank.from_float(w1 + 1e-6 * i, w2, a.bits, router=wg) for i in range(a.banks)]
 del w1, w2
 h = torch.randn(a.tokens, a.d, device="cuda", generator=g).half()
 for _ in range(a.iters):
-    out = m.moe_ffn_forward(h, bank, top_k=a.top_k, path=a.path)
+    for bank in banks:
+        out = m.moe_ffn_forward(h, bank, top_k=a.top_k, path=a.path)
 torch.cuda.synchronize()
 print("ok", out.float().abs().mean().item())

@@ -104,8 +104,8 @@ for phase in (1, 2):
 
 if os.environ.get("TRACE_CTA"):
     c = int(os.environ["TRACE_CTA"])
-    names = {(2, 3): "C top", (2, 0): "C bfull ok", (5, 0): "C unit0 in", (5, 1): "C unit+ in", (2, 1): "C mloop end",
-             (2, 4): "C scr ok", (3, 0): "E start", (3, 2): "E end", (4, 0): "P unit0 iss", (4, 1): "P unit+ iss"}
+    names = {(2, 5): "U B tile", (6, 0): "M item start", (6, 1): "M item issued", (6, 2): "M unit A ok", (6, 3): "M unit issued", (2, 3): "C top", (2, 0): "C bfull ok", (5, 0): "C unit0 in", (5, 1): "C unit+ in", (2, 1): "C mloop end",
+             (2, 4): "C scr ok/U B done", (3, 0): "E start", (3, 2): "E end", (4, 0): "P unit0 iss", (4, 1): "P unit+ iss"}
     sel = valid[c]
     order = np.argsort(us[c][sel], kind="stable")
     rr, ee, pp, tt = role[c][sel][order], ev[c][sel][order], ph[c][sel][order], us[c][sel][order]
