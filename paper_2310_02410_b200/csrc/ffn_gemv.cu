@@ -49,13 +49,11 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
-#include <cstdlib>
 
 #include "codec.cuh"
 #include "frag.cuh"
 #include "kernels.cuh"
 #include "ptx.cuh"
-#include "tc.cuh"
 
 namespace moqe_gpu {
 
@@ -66,8 +64,7 @@ constexpr int kMaxCluster = 8;
 constexpr int kPassRows = 4;         // rows per item pass
 constexpr int kMaxNT = 2;            // n8 column tiles (4 rows x 4 planes = 16 columns)
 constexpr int kMaxListed = 256;
-constexpr int kConsumers = 8;        // MMA warps: (m16 block of 16 channels) x (stage residue mod kKSplit)
-constexpr int kKSplit = kConsumers / 8;  // warps per m16 block, splitting every unit's stages (1 or 2)
+constexpr int kConsumers = 8;        // MMA warps: 16 channels (one m16 block) each
 constexpr int kEpiWarps = 4;         // epilogue warps: one thread per channel
 constexpr int kProdWarp = kConsumers + kEpiWarps;
 constexpr int kGemvThreads = (kProdWarp + 1) * 32;
@@ -83,26 +80,21 @@ __host__ __device__ constexpr int rup(int x, int a) { return (x + a - 1) / a * a
 template <int BITS>
 __host__ __device__ constexpr int unit_stages() { return BITS == 8 ? 2 : 4; }  // >= 16 KB per weight copy
 
-// Row block geometry. The digits of one row and 1024-k chunk, for stage st and
-// fragment f, are 32 bytes per plane s — byte j is the digit of activation
-// Frag::kidx(f, (j >> 2) & 1, j & 3) of quad j >> 3 (the k-order both MMA paths
-// use) — stored K-chunk-interleaved: off(pl, st, f, s, j) = (st F + f) 32 pl +
-// (j / 16) 16 pl + 16 s + j % 16. So the pl planes of one K-chunk are pl
-// consecutive 16-byte rows, i.e. rows 0..pl-1 of a K-major no-swizzle UMMA core
-// matrix (LBO = 16 pl): a single row block is a tcgen05 B operand in place (the
-// core-matrix rows >= pl read the bytes that follow; their accumulator columns
-// are never used — hence the tail pad). Row blocks are XR bytes apart (64 mod 128).
+// Row block geometry. A plane holds 8 stages of STG bytes: stage st, fragment
+// f, quad tq, register h -> the u32 at st*STG + f*32 + tq*8 + h*4 whose byte i
+// is the digit of activation Frag::kidx(f, h, i) of that quad (codec order).
+// Planes are PB bytes apart (PB = 32 mod 128) and row blocks XR bytes apart
+// (XR = 64 mod 128), so the 8 column groups of a warp's LDS.64 hit distinct
+// bank groups (two wavefronts, the minimum for 256 bytes).
 template <int BITS>
 struct RB {
     static constexpr int F = Frag<BITS>::F;
+    static constexpr int STG = F * 32;
+    static constexpr int PB = kChunkStages * STG + 32;
     static constexpr int HDR1 = 32;   // fc1: int p, float l1 (whole row), int64 Sum X (this chunk)
     static constexpr int HDR2 = 128;  // fc2: int p2 at 0, int64 Sum X2 of stage st at 64 + 8 st
-    __host__ __device__ static constexpr int stage_bytes(int pl) { return F * 32 * pl; }
-    __host__ __device__ static constexpr int off(int pl, int st, int f, int s, int j) {
-        return (st * F + f) * 32 * pl + (j >> 4) * 16 * pl + s * 16 + (j & 15);
-    }
-    static constexpr int XR1 = rup(HDR1 + kChunkStages * stage_bytes(3) + 128, 128) + 64;
-    static constexpr int XR2 = rup(HDR2 + kChunkStages * stage_bytes(4) + 128, 128) + 64;
+    static constexpr int XR1 = rup(HDR1 + 3 * PB, 128) + 64;
+    static constexpr int XR2 = rup(HDR2 + 4 * PB, 128) + 64;
 };
 struct XHead1 {
     int p;
@@ -300,7 +292,7 @@ __global__ void __launch_bounds__(128) k_xrows(XrowArgs a) {
 #pragma unroll
     for (int s = 0; s < 3; ++s) {
         const uint32_t sel = uint32_t(s) | (uint32_t(4 + s) << 4);
-        uint8_t* dst = blk + R::HDR1 + R::off(3, st, 0, s, tq * 8);
+        uint8_t* dst = blk + R::HDR1 + s * R::PB + st * R::STG + tq * 8;
 #pragma unroll
         for (int f = 0; f < F; ++f) {
             uint32_t b[2];
@@ -310,16 +302,16 @@ __global__ void __launch_bounds__(128) k_xrows(XrowArgs a) {
                 const uint32_t hi = prmt(D[FR::kidx(f, h, 2)], D[FR::kidx(f, h, 3)], sel);
                 b[h] = prmt(lo, hi, 0x5410u);
             }
-            *reinterpret_cast<uint2*>(dst + f * 32 * 3) = make_uint2(b[0], b[1]);
+            *reinterpret_cast<uint2*>(dst + f * 32) = make_uint2(b[0], b[1]);
         }
     }
 }
 
 // ---- consumer pieces -------------------------------------------------------------------
 // One 128-k stage of one m16 block: LOP3 unpack + IMMA against the stage's B words.
-template <int BITS, int NT, int PL>
+template <int BITS, int NT>
 __device__ __forceinline__ void stage_mma(const uint8_t* T0, int r0, int tq, const uint8_t* const (&bp)[kMaxNT],
-                                          int st, int (&acc)[Frag<BITS>::G][kMaxNT][4]) {
+                                          int soff, int (&acc)[Frag<BITS>::G][kMaxNT][4]) {
     using FR = Frag<BITS>;
     constexpr int F = FR::F;
     uint32_t a[F][4];
@@ -328,45 +320,42 @@ __device__ __forceinline__ void stage_mma(const uint8_t* T0, int r0, int tq, con
     for (int f = 0; f < F; ++f)
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
-            const uint2 b = *reinterpret_cast<const uint2*>(bp[j] + (st * F + f) * 32 * PL);
+            const uint2 b = *reinterpret_cast<const uint2*>(bp[j] + soff + f * 32);
             imma(acc[FR::grp(f)][j], a[f], b.x, b.y);
         }
 }
 
-// The stages s = kpar, kpar + kKSplit, ... of one weight unit (with kKSplit = 2
-// the two warps of a pair split every unit by stage parity; measured slower on
-// B200 than one warp per m16 block, so kKSplit = 1 is the default).
-template <int BITS, int NT, int PL>
-__device__ __forceinline__ void unit_mma(const uint8_t* U, int nst_u, int s0, int kpar, int r0, int tq,
+template <int BITS, int NT>
+__device__ __forceinline__ void unit_mma(const uint8_t* U, int nst_u, int s0, int r0, int tq,
                                          const uint8_t* const (&bp)[kMaxNT], int (&acc)[Frag<BITS>::G][kMaxNT][4]) {
     using FR = Frag<BITS>;
-    constexpr int F = FR::F, US = unit_stages<BITS>(), H = US / kKSplit;
-    constexpr int SB = 2 * tile_bytes(BITS);
+    constexpr int F = FR::F, US = unit_stages<BITS>();
+    constexpr int SB = 2 * tile_bytes(BITS), STG = RB<BITS>::STG;
     if (nst_u == US) {
-        // full unit: this warp's stages' A and B words are loaded before the first IMMA
-        uint32_t a[H][F][4];
-        uint2 b[H][F][NT];
+        // full unit: every stage's A and B words are loaded before the first IMMA
+        // (two consumer warps per SM sub-partition cannot hide the LDS -> IMMA chain)
+        uint32_t a[US][F][4];
+        uint2 b[US][F][NT];
 #pragma unroll
-        for (int i = 0; i < H; ++i) {
-            const int s = kpar + kKSplit * i;
+        for (int s = 0; s < US; ++s) {
             const uint8_t* T0 = U + s * SB;
-            FR::load(T0, T0 + tile_bytes(BITS), r0, tq, a[i]);
+            FR::load(T0, T0 + tile_bytes(BITS), r0, tq, a[s]);
 #pragma unroll
             for (int f = 0; f < F; ++f)
 #pragma unroll
                 for (int j = 0; j < NT; ++j)
-                    b[i][f][j] = *reinterpret_cast<const uint2*>(bp[j] + ((s0 + s) * F + f) * 32 * PL);
+                    b[s][f][j] = *reinterpret_cast<const uint2*>(bp[j] + (s0 + s) * STG + f * 32);
         }
 #pragma unroll
-        for (int i = 0; i < H; ++i)
+        for (int s = 0; s < US; ++s)
 #pragma unroll
             for (int f = 0; f < F; ++f)
 #pragma unroll
-                for (int j = 0; j < NT; ++j) imma(acc[FR::grp(f)][j], a[i][f], b[i][f][j].x, b[i][f][j].y);
+                for (int j = 0; j < NT; ++j) imma(acc[FR::grp(f)][j], a[s][f], b[s][f][j].x, b[s][f][j].y);
         return;
     }
 #pragma unroll 1
-    for (int s = kpar; s < nst_u; s += kKSplit) stage_mma<BITS, NT, PL>(U + s * SB, r0, tq, bp, s0 + s, acc);
+    for (int s = 0; s < nst_u; ++s) stage_mma<BITS, NT>(U + s * SB, r0, tq, bp, (s0 + s) * STG, acc);
 }
 
 // V * 2^-sh in fp32: one rounding (int64 -> fp32), exact power-of-two scale
@@ -394,9 +383,9 @@ struct Layout {
     static constexpr int XR = PHASE == 1 ? R::XR1 : R::XR2;
     static constexpr int HDR = PHASE == 1 ? R::HDR1 : R::HDR2;
     static constexpr int BUFS = kBufs * kPassRows * XR;
-    static constexpr int ZERO = 0;
-    static constexpr int SCR = kScrBufs * kKSplit * TILE_N * kScrStride * 4;  // [buffer][stage residue][channel]
-    static constexpr int STG = PHASE == 1 ? rup(kPassRows * R::stage_bytes(4) + kEpiWarps * kPassRows * 8, 128) : 0;
+    static constexpr int ZERO = rup(R::PB, 128);                               // all-zero plane (idle columns)
+    static constexpr int SCR = kScrBufs * TILE_N * kScrStride * 4;
+    static constexpr int STG = PHASE == 1 ? rup(kPassRows * 4 * R::STG + kEpiWarps * kPassRows * 8, 128) : 0;
     static constexpr int TABLES = rup(int(sizeof(GemvTables)), 128);
     static constexpr int BARS = rup((2 * kMaxNU + 2 * kBufs + 2 * kScrBufs + 2) * 8, 128);
     static constexpr int O_ZERO = BUFS, O_SCR = O_ZERO + ZERO, O_STG = O_SCR + SCR, O_TAB = O_STG + STG;
@@ -409,137 +398,6 @@ struct Layout {
     __host__ __device__ static constexpr int total(int cs) { return ring_off(cs) + nu(cs) * Cfg<BITS>::UB; }
     static_assert(nu(kMaxCluster) >= 2, "weight ring needs two slots");
 };
-
-// ---- epilogue of one item (both decode kernels) ----------------------------------------
-// srow: this channel's 16 column sums (D * Sum_k u * digit, exact int32); rb: the
-// item's row blocks (headers). rel0 / rel1: barriers to arrive on (lane 0) once
-// srow and the headers are read. Ranks != 0 return after handing their partials to rank 0.
-template <int BITS, int PHASE>
-__device__ __forceinline__ void epi_item(const GemvArgs& g, const Plan& P, const GemvItem& it, int seq, int ch, int lane,
-                                 int ew, int rank, int CS, int nst, int nch2, int Np, const int* srow,
-                                 const uint8_t* rb, long long* red, uint32_t red_rank0, uint32_t full_rank0,
-                                 uint64_t* red_full, uint64_t* red_empty, uint8_t* stg, int pos0, int pos1,
-                                 uint64_t* rel0, uint64_t* rel1, float sc, float bias, float es, float eb,
-                                 const float (&gate)[kPassRows], const int (&tok)[kPassRows]) {
-    using FR = Frag<BITS>;
-    using R = RB<BITS>;
-    using L = Layout<BITS, PHASE>;
-    constexpr int XR = L::XR, PL = planes_of(PHASE);
-    constexpr int LOGD = FR::D == 64 ? 6 : FR::D == 16 ? 4 : 0;
-    constexpr long long Z = 1ll << (BITS - 1);
-    const int chg = it.mt * TILE_N + ch;
-    // exact partial of this chunk: V = Sum_s 256^s S_s - D Z Sum X (int64)
-    long long V[kPassRows];
-    int pe[kPassRows];
-    float l1[kPassRows];
-#pragma unroll
-    for (int t = 0; t < kPassRows; ++t) {
-        V[t] = 0;
-        pe[t] = kZeroRow;
-        l1[t] = 0.f;
-        if (t >= it.nrows) continue;
-        const uint8_t* hb = rb + t * XR;
-        long long zs = 0;
-        if (PHASE == 1) {
-            const XHead1 hd = *reinterpret_cast<const XHead1*>(hb);
-            pe[t] = hd.p;
-            l1[t] = hd.l1;
-            zs = hd.zsum;
-        } else {
-            pe[t] = *reinterpret_cast<const int*>(hb);
-            for (int s = 0; s < nst; ++s) zs += *reinterpret_cast<const long long*>(hb + 64 + 8 * s);
-        }
-        long long v = -(long long)FR::D * Z * zs;
-#pragma unroll
-        for (int s = 0; s < PL; ++s) v += (long long)srow[s * it.nrows + t] << (8 * s);
-        V[t] = v;
-    }
-    __syncwarp();
-    if (lane == 0) {
-        if (rel0) mbar_arrive(rel0);
-        if (rel1) mbar_arrive(rel1);
-    }
-    if (CS > 1) {  // split-K: every rank's partial into rank 0 (DSMEM), fixed-order sum there
-        if (rank != 0) {
-            if (lane == 0) wait_cluster(red_empty, (seq & 1) ^ 1);  // rank 0 took the previous item
-            __syncwarp();
-#pragma unroll
-            for (int t = 0; t < kPassRows; ++t)
-                if (t < it.nrows) st_cluster_s64(red_rank0 + uint32_t(((rank * TILE_N + ch) * kPassRows + t) * 8), V[t]);
-            __syncwarp();
-            if (lane == 0) arrive_cluster(full_rank0);
-            return;
-        }
-        if (lane == 0) wait_cluster(red_full, seq & 1);
-        __syncwarp();
-#pragma unroll
-        for (int t = 0; t < kPassRows; ++t)
-            if (t < it.nrows)
-                for (int r = 1; r < CS; ++r) V[t] += red[(r * TILE_N + ch) * kPassRows + t];
-        named_bar_sync(2, kEpiWarps * 32);  // every epilogue warp read red
-        if (ch >= 1 && ch < CS) arrive_cluster(map_rank(red_empty, ch));
-    }
-    if (PHASE == 2) {
-#pragma unroll
-        for (int t = 0; t < kPassRows; ++t) {
-            if (t >= it.nrows || chg >= g.d) continue;
-            const float y = pe[t] == kZeroRow ? 0.f : scale_pow2(V[t], pe[t] + LOGD);
-            const float yg = fmaf(y, sc, bias) * gate[t];
-            const int64_t o = int64_t(tok[t]) * g.d + chg;
-            if (g.out_acc) atomicAdd(g.out_acc + o, yg);  // top-2: two addends onto zero
-            else if (g.out_f16) static_cast<__half*>(g.out)[o] = __float2half_rn(yg);
-            else static_cast<float*>(g.out)[o] = yg;
-        }
-    } else {
-        // mid = ReLU(y s + b) in fc2 fixed point -> stage mt % 8 of the rows' fc2 blocks
-        constexpr int SB2 = R::stage_bytes(4);
-        long long* zred = reinterpret_cast<long long*>(stg + kPassRows * SB2);  // [4 warps][4 rows]
-        int p2[kPassRows];
-#pragma unroll
-        for (int t = 0; t < kPassRows; ++t) {
-            p2[t] = kZeroRow;
-            long long X2 = 0;
-            if (t < it.nrows) {
-                p2[t] = fc2_exp<BITS>(es, eb, l1[t]);
-                const float y = pe[t] == kZeroRow ? 0.f : scale_pow2(V[t], pe[t] + LOGD);
-                const float mid = fmaxf(fmaf(y, sc, bias), 0.0f);  // ReLU, model.cpp:190
-                X2 = p2[t] == kZeroRow ? 0 : __float2int_rn(ldexpf(mid, p2[t]));
-                const uint32_t dg = (uint32_t(int(X2)) + 0x80808080u) ^ 0x80808080u;  // 4 signed digits
-#pragma unroll
-                for (int s = 0; s < 4; ++s) {
-                    uint8_t* pl = stg + t * SB2 + s * 16;  // this row's fc2 stage block, plane s
-                    const uint8_t byte = uint8_t(dg >> (8 * s));
-                    pl[pos0] = byte;
-                    if (pos1 >= 0) pl[pos1] = byte;
-                }
-            }
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) X2 += __shfl_xor_sync(0xffffffffu, X2, off);
-            if (lane == 0) zred[ew * kPassRows + t] = X2;
-        }
-        named_bar_sync(2, kEpiWarps * 32);  // the stage blocks and warp sums are complete
-        const int st2 = it.mt % kChunkStages, c2 = it.mt / kChunkStages;
-        constexpr int V16 = SB2 / 16;
-        for (int idx = ch; idx < it.nrows * V16; idx += kEpiWarps * 32) {
-            const int t = idx / V16, u = idx - t * V16;
-            uint8_t* dst = g.xb + (int64_t(it.row0 + t) * nch2 + c2) * R::XR2 + R::HDR2 + st2 * SB2 + 16 * u;
-            *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(stg + t * SB2 + 16 * u);
-        }
-        if (ch < it.nrows) {
-            const int t = ch;
-            int p2t = kZeroRow;
-#pragma unroll
-            for (int u = 0; u < kPassRows; ++u)
-                if (u == t) p2t = p2[u];
-            uint8_t* hb = g.xb + (int64_t(it.row0 + t) * nch2 + c2) * R::XR2;
-            long long z = 0;
-            for (int w = 0; w < kEpiWarps; ++w) z += zred[w * kPassRows + t];
-            *reinterpret_cast<long long*>(hb + 64 + 8 * st2) = z;
-            *reinterpret_cast<int*>(hb) = p2t;  // the same value from every m-tile of the pass
-        }
-        named_bar_sync(2, kEpiWarps * 32);  // stage blocks / warp sums reused by the next item
-    }
-}
 
 template <int BITS, int PHASE>
 __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
@@ -555,6 +413,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
     const int CS = int(cluster_nctas()), rank = int(cta_rank());
     const int NU = L::nu(CS);
     uint8_t* bufs = smem;                                                      // [kBufs][4 rows][XR]
+    const uint8_t* zero = smem + L::O_ZERO;                                    // zero plane
     int* scr = reinterpret_cast<int*>(smem + L::O_SCR);                        // [2][128][kScrStride]
     uint8_t* stg = smem + L::O_STG;                                            // fc1: [4 rows][4 planes][STG] + zred
     GemvTables& TBL = *reinterpret_cast<GemvTables*>(smem + L::O_TAB);
@@ -582,6 +441,8 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
         mbar_init(red_empty, 1);
         fence_barrier_init();
     }
+    for (int i = threadIdx.x; i < L::ZERO / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(const_cast<uint8_t*>(zero))[i] = make_uint4(0u, 0u, 0u, 0u);
     if (PHASE == 1) pdl_wait();  // routing plan and fc1 row blocks (fc2: the plan is older than fc1's wait)
     const int n_gemv = P.meta[0];
     const int nmt = Np / TILE_N;
@@ -653,24 +514,22 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
     } else if (warp < kConsumers) {
         // ===== consumers: warp -> m16 block (16 channels) of the 128-channel item
         const int gq = lane >> 2, tq = lane & 3;
-        const int kpar = warp >> 3;  // stage residue (kKSplit = 2: even / odd stages of every unit)
-        const int r0 = 16 * (warp & 7) + gq;
+        const int r0 = 16 * warp + gq;
         Tracer T = tracer(threadIdx.x == 0 ? tr : nullptr, 1, 128);
         int slot = 0, sph = 0, seq = 0;
         for (int i = clu; i < nitems; i += nclu, ++seq) {
             const GemvItem it = item_of(seq, i, TBL, n_gemv, nmt);
             const int b = seq % kBufs, sb = seq & 1;
             const int NT = nt_of(PHASE, it.nrows), ncol = PL * it.nrows;
-            // B column c = s * nrows + t (plane s of row t)
+            // B column c = s * nrows + t (plane s of row t); idle columns read the zero plane
             const uint8_t* bp[kMaxNT];
-            const int inv = it.nrows == 1 ? 65536 : it.nrows == 2 ? 32768 : it.nrows == 3 ? 21846 : 16384;
 #pragma unroll
+            const int inv = it.nrows == 1 ? 65536 : it.nrows == 2 ? 32768 : it.nrows == 3 ? 21846 : 16384;
             for (int j = 0; j < kMaxNT; ++j) {
                 const int c = 8 * j + gq;
                 const int sq = (c * inv) >> 16;  // c / nrows (exact for c < 16)
                 const int t = c < ncol ? c - sq * it.nrows : 0, s = c < ncol ? sq : 0;
-                // idle columns read any valid bytes: their MMA output columns are never used
-                bp[j] = bufs + (b * kPassRows + t) * XR + HDR + R::off(PL, 0, 0, s, tq * 8);
+                bp[j] = c < ncol ? bufs + (b * kPassRows + t) * XR + HDR + s * R::PB + tq * 8 : zero + tq * 8;
             }
             T.ev(2, 3, it, PHASE);
             mbar_wait(&bfull[b], (seq / kBufs) & 1);
@@ -683,13 +542,13 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
 #pragma unroll
                     for (int q = 0; q < 4; ++q) acc[a][j][q] = 0;
             for (int u = 0; u < nunits; ++u) {
-                if (g.dbg != 2) mbar_wait(&full[slot], sph);  // dbg 2 (timing only): compute on stale data
+                mbar_wait(&full[slot], sph);
                 T.ev(5, u == 0 ? 0 : 1, it, PHASE);
                 const uint8_t* U = ring + size_t(slot) * UB;
                 const int ns = min(US, nst - u * US);
                 if (g.dbg == 1) {
-                } else if (NT == 1) unit_mma<BITS, 1, PL>(U, ns, u * US, kpar, r0, tq, bp, acc);
-                else unit_mma<BITS, 2, PL>(U, ns, u * US, kpar, r0, tq, bp, acc);
+                } else if (NT == 1) unit_mma<BITS, 1>(U, ns, u * US, r0, tq, bp, acc);
+                else unit_mma<BITS, 2>(U, ns, u * US, r0, tq, bp, acc);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[slot]);
                 if (++slot == NU) { slot = 0; sph ^= 1; }
@@ -702,7 +561,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
             T.ev(2, 4, it, PHASE);
             __syncwarp();
             // groups -> D * Sum_k u * digit per (channel, column): exact in int32 for 1024-k chunks
-            int* sc = scr + (sb * kKSplit + kpar) * TILE_N * kScrStride;
+            int* sc = scr + sb * TILE_N * kScrStride;
 #pragma unroll
             for (int j = 0; j < kMaxNT; ++j) {
                 if (j >= NT) break;
@@ -735,7 +594,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
                 for (int h = 0; h < 2; ++h)
                     for (int i = 0; i < 4; ++i)
                         if (FR::kidx(f, h, i) == kid) {
-                            const int o = R::off(4, 0, f, 0, q * 8 + h * 4 + i);
+                            const int o = f * 32 + q * 8 + h * 4 + i;
                             if (first) { pos0 = o; first = false; } else pos1 = o;
                         }
         }
@@ -759,337 +618,124 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
             }
             mbar_wait(&sfull[sb], (seq >> 1) & 1);
             T.ev(3, 0, it, PHASE);
-            int* srow = scr + sb * kKSplit * TILE_N * kScrStride + ch * kScrStride;
-            if (kKSplit == 2) {  // add the odd stages' sums
-                const int* odd = srow + TILE_N * kScrStride;
+            // exact partial of this chunk: V = Sum_s 256^s S_s - D Z Sum X (int64)
+            const uint8_t* rb = bufs + b * kPassRows * XR;
+            const int* srow = scr + sb * TILE_N * kScrStride + ch * kScrStride;
+            long long V[kPassRows];
+            int pe[kPassRows];
+            float l1[kPassRows];
 #pragma unroll
-                for (int c = 0; c < 16; c += 4) {
-                    const int4 x = *reinterpret_cast<const int4*>(srow + c), y = *reinterpret_cast<const int4*>(odd + c);
-                    *reinterpret_cast<int4*>(srow + c) = make_int4(x.x + y.x, x.y + y.y, x.z + y.z, x.w + y.w);
+            for (int t = 0; t < kPassRows; ++t) {
+                V[t] = 0;
+                pe[t] = kZeroRow;
+                l1[t] = 0.f;
+                if (t >= it.nrows) continue;
+                const uint8_t* hb = rb + t * XR;
+                long long zs = 0;
+                if (PHASE == 1) {
+                    const XHead1 hd = *reinterpret_cast<const XHead1*>(hb);
+                    pe[t] = hd.p;
+                    l1[t] = hd.l1;
+                    zs = hd.zsum;
+                } else {
+                    pe[t] = *reinterpret_cast<const int*>(hb);
+                    for (int s = 0; s < nst; ++s) zs += *reinterpret_cast<const long long*>(hb + 64 + 8 * s);
                 }
-            }
-            epi_item<BITS, PHASE>(g, P, it, seq, ch, lane, ew, rank, CS, nst, nch2, Np,
-                                  srow, bufs + b * kPassRows * XR, red,
-                                  red_rank0, full_rank0, red_full, red_empty, stg, pos0, pos1, &sempty[sb], &bempty[b],
-                                  sc, bias, es, eb, gate, tok);
-            T.ev(3, 2, it, PHASE);
-        }
-    }
-    cluster_sync();  // no CTA leaves while a peer may still write its shared memory
-    if (tr && threadIdx.x == 0) { tr[2 * (kSlots - 1)] = gtime_ns(); tr[2 * (kSlots - 1) + 1] = clock64(); }
-}
-
-// ==== tcgen05 decode kernel ===============================================================
-// Same items, row blocks, producer and epilogue as k_gemv; the integer dot
-// products run on the 5th-generation tensor cores instead of mma.sync:
-//   warps 0-3  unpackers (thread = channel): per weight unit (4 stages), the
-//              channel's packed codes -> F x 32 u8 per stage (u * 2^s, the same
-//              LOP3 masks as the IMMA path) -> tcgen05.st into one of two TMEM A
-//              unit slots; one wait::st + one barrier arrive per unit
-//   warp 8     MMA issuer: per stage, fragment and row: tcgen05.mma.kind::i8
-//              (M 128, N 8, K 32; A from TMEM, B = the row block in smem, in
-//              place) into per-(group, row) s32 accumulators in TMEM
-//   warps 4-7  epilogue: tcgen05.ld of the accumulators, then epi_item
-//   warp 9     producer (as k_gemv)
-constexpr int kTcUnpack = 4, kTcEpi = 4, kTcMmaWarp = 8, kTcProdWarp = 9;
-constexpr int kTcThreads = 10 * 32;
-static_assert(kEpiWarps == kTcEpi, "epilogue barrier count");
-
-template <int BITS, int PHASE>
-struct LayoutTC {
-    using R = RB<BITS>;
-    static constexpr int kMaxNU = 8;
-    static constexpr int F = Frag<BITS>::F, G = Frag<BITS>::G, US = unit_stages<BITS>();
-    static constexpr int XR = PHASE == 1 ? R::XR1 : R::XR2;
-    static constexpr int HDR = PHASE == 1 ? R::HDR1 : R::HDR2;
-    // TMEM: accumulators [G][4 rows][8 columns] at 0; two A unit slots at the top
-    static constexpr int ACC_COLS = G * kPassRows * 8;
-    static constexpr int A_UNIT = US * F * 8;
-    static constexpr int A_BASE = 512 - 2 * A_UNIT;
-    static_assert(A_BASE >= ACC_COLS, "TMEM budget");
-    static constexpr int BUFS = kBufs * kPassRows * XR;
-    static constexpr int SCR = TILE_N * kScrStride * 4;
-    static constexpr int STG = PHASE == 1 ? rup(kPassRows * R::stage_bytes(4) + kEpiWarps * kPassRows * 8, 128) : 0;
-    static constexpr int TABLES = rup(int(sizeof(GemvTables)), 128);
-    static constexpr int BARS = rup((2 * kMaxNU + 2 * kBufs + 4 + 2 + 2) * 8 + 16, 128);
-    static constexpr int O_BUFS = 0, O_SCR = O_BUFS + BUFS, O_STG = O_SCR + SCR;
-    static constexpr int O_TAB = O_STG + STG, O_BARS = O_TAB + TABLES, O_RED = O_BARS + BARS;
-    __host__ __device__ static constexpr int red_bytes(int cs) { return cs > 1 ? cs * TILE_N * kPassRows * 8 : 0; }
-    __host__ __device__ static constexpr int ring_off(int cs) { return rup(O_RED + red_bytes(cs), 128); }
-    __host__ __device__ static constexpr int nu(int cs) {
-        return (kSmemMax - ring_off(cs)) / Cfg<BITS>::UB < kMaxNU ? (kSmemMax - ring_off(cs)) / Cfg<BITS>::UB : kMaxNU;
-    }
-    __host__ __device__ static constexpr int total(int cs) { return ring_off(cs) + nu(cs) * Cfg<BITS>::UB; }
-    static_assert(nu(kMaxCluster) >= 2, "weight ring needs two slots");
-};
-
-template <int BITS, int PHASE>
-__global__ void __launch_bounds__(kTcThreads, 1) k_gemv_tc(GemvArgs g, Plan P) {
-    using FR = Frag<BITS>;
-    using C = Cfg<BITS>;
-    using R = RB<BITS>;
-    using L = LayoutTC<BITS, PHASE>;
-    constexpr int F = FR::F, G = FR::G, UB = C::UB, US = C::US, SB = C::SB, TB = C::TB;
-    constexpr int XR = L::XR, HDR = L::HDR, PL = planes_of(PHASE);
-    extern __shared__ __align__(128) uint8_t smem[];
-    const int CS = int(cluster_nctas()), rank = int(cta_rank());
-    const int NU = L::nu(CS);
-    uint8_t* bufs = smem + L::O_BUFS;                                          // [kBufs][4 rows][XR]
-    int* scr = reinterpret_cast<int*>(smem + L::O_SCR);                        // [128][kScrStride]
-    uint8_t* stg = smem + L::O_STG;
-    GemvTables& TBL = *reinterpret_cast<GemvTables*>(smem + L::O_TAB);
-    long long* red = reinterpret_cast<long long*>(smem + L::O_RED);
-    uint8_t* ring = smem + L::ring_off(CS);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::O_BARS);
-    uint64_t* empty = full + NU;
-    uint64_t* bfull = empty + NU;
-    uint64_t* bempty = bfull + kBufs;
-    uint64_t* afull = bempty + kBufs;   // [2] A unit slots
-    uint64_t* aempty = afull + 2;
-    uint64_t* accfull = aempty + 2;
-    uint64_t* accempty = accfull + 1;
-    uint64_t* red_full = accempty + 1;
-    uint64_t* red_empty = red_full + 1;
-    uint32_t* s_tmem = reinterpret_cast<uint32_t*>(red_empty + 1);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int Kp = PHASE == 1 ? g.Kp1 : g.Kp2;
-    const int Np = PHASE == 1 ? g.Np1 : g.Np2;
-    const int k0 = rank * kChunkK, nst = (min(kChunkK, Kp - k0) + kStageK - 1) / kStageK;
-    const int nunits = (nst + US - 1) / US;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < NU; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kTcUnpack); }
-        for (int b = 0; b < kBufs; ++b) { mbar_init(&bfull[b], 1); mbar_init(&bempty[b], 1 + kTcEpi); }
-        for (int a = 0; a < 2; ++a) { mbar_init(&afull[a], kTcUnpack); mbar_init(&aempty[a], 1); }
-        mbar_init(accfull, 1);
-        mbar_init(accempty, kTcEpi);
-        mbar_init(red_full, kTcEpi * max(CS - 1, 1));
-        mbar_init(red_empty, 1);
-        fence_barrier_init();
-    }
-    if (warp == kTcMmaWarp) tm_alloc(s_tmem, 512);
-    if (PHASE == 1) pdl_wait();  // routing plan and fc1 row blocks
-    const int n_gemv = P.meta[0];
-    const int nmt = Np / TILE_N;
-    if (warp == 0 && n_gemv > 0) build_tables(TBL, P, n_gemv, nmt, lane, PHASE == 1 ? g.T * g.topk : 0);
-    __syncthreads();
-    const int nitems = n_gemv > 0 ? TBL.start[n_gemv] : 0;
-    const int clu = int(blockIdx.x) / CS, nclu = int(gridDim.x) / CS;
-    for (int k = threadIdx.x; k < kItemCache; k += blockDim.x) {
-        const int i = clu + k * nclu;
-        if (i >= nitems) break;
-        const GemvItem it = item_at(i, TBL, n_gemv, nmt);
-        TBL.items[k] = make_int4(it.e, it.mt, it.row0, it.nrows);
-    }
-    tm_fence_before();
-    __syncthreads();
-    tm_fence_after();
-    cluster_sync();  // barriers of every CTA initialised before any remote arrive
-    if (PHASE == 1) pdl_trigger();
-    const uint32_t tmem = *s_tmem;
-    const int nch2 = (g.Kp2 + kChunkK - 1) / kChunkK;
-    constexpr int kSlots = kTraceCap / 2;
-    unsigned long long* tr = g.trace ? g.trace + size_t(blockIdx.x) * kTraceCap * 2 + (PHASE == 2 ? kTraceCap : 0) : nullptr;
-    if (tr && threadIdx.x == 0) { tr[0] = gtime_ns(); tr[1] = clock64(); }
-
-    if (warp == kTcProdWarp) {
-        if (lane == 0) {
-            Tracer T = tracer(tr, 192, kSlots - 1);
-            const uint64_t pol = policy_evict_first();
-            bool waited = PHASE == 1;
-            int slot = 0, sph = 0, seq = 0;
-            const uint8_t* wbase0 = PHASE == 1 ? g.w1 : g.w2;
-            const int64_t wstride = PHASE == 1 ? g.w1_stride : g.w2_stride;
-            for (int i = clu; i < nitems; i += nclu, ++seq) {
-                const GemvItem it = item_of(seq, i, TBL, n_gemv, nmt);
-                const int b = seq % kBufs;
-                auto issue_rows = [&]() {
-                    mbar_wait(&bempty[b], ((seq / kBufs) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&bfull[b], uint32_t(it.nrows * XR));
-                    for (int t = 0; t < it.nrows; ++t) {
-                        const uint8_t* src =
-                            PHASE == 1 ? g.xr + (int64_t(it.row0 + t < kTokCache ? TBL.tok[it.row0 + t]
-                                                                                  : __ldg(P.perm_token + it.row0 + t)) *
-                                                     g.nch1 + rank) * XR
-                                       : g.xb + (int64_t(it.row0 + t) * nch2 + rank) * XR;
-                        bulk_g2s(bufs + (b * kPassRows + t) * XR, src, uint32_t(XR), &bfull[b]);
-                    }
-                };
-                if (!(PHASE == 2 && seq == 0)) issue_rows();
-                const uint8_t* wb = wbase0 + int64_t(it.e) * wstride + (int64_t(it.mt) * (Kp / TILE_K) + k0 / TILE_K) * TB;
-                for (int u = 0; u <= nunits; ++u) {
-                    if (PHASE == 2 && seq == 0 && !waited && (u == nunits || u == NU)) {
-                        pdl_wait();
-                        waited = true;
-                        issue_rows();
-                    }
-                    if (u == nunits) break;
-                    const int bytes = min(US, nst - u * US) * SB;
-                    mbar_wait(&empty[slot], sph ^ 1);
-                    T.ev(4, u == 0 ? 0 : 1, it, PHASE);
-                    mbar_arrive_expect_tx(&full[slot], uint32_t(bytes));
-                    bulk_g2s_hint(ring + size_t(slot) * UB, wb + int64_t(u) * UB, uint32_t(bytes), &full[slot], pol);
-                    if (++slot == NU) { slot = 0; sph ^= 1; }
-                }
-            }
-            if (!waited) pdl_wait();
-        }
-        __syncwarp();
-    } else if (warp == kTcMmaWarp) {
-        if (lane == 0) {
-            Tracer T = tracer(tr, 160, 192);
-            const uint32_t idesc = idesc_i8(8);
-            int ua = 0, seq = 0;  // A unit counter (slot ua & 1)
-            for (int i = clu; i < nitems; i += nclu, ++seq) {
-                const GemvItem it = item_of(seq, i, TBL, n_gemv, nmt);
-                const int b = seq % kBufs;
-                mbar_wait(&bfull[b], (seq / kBufs) & 1);    // row blocks = B operands, in place
-                mbar_wait(accempty, (seq & 1) ^ 1);        // the epilogue read the previous accumulators
-                T.ev(6, 0, it, PHASE);
-                tm_fence_after();
-                const uint32_t rb = smem_u32(bufs + b * kPassRows * XR) + HDR;
-                for (int u = 0; u < nunits; ++u, ++ua) {
-                    const int a = ua & 1;
-                    mbar_wait(&afull[a], (ua >> 1) & 1);
-                    T.ev(6, 2, it, PHASE);
-                    tm_fence_after();
-                    const int ns = min(US, nst - u * US);
-                    for (int s = 0; s < ns; ++s) {
-                        const int st = u * US + s;
+                long long v = -(long long)FR::D * Z * zs;
 #pragma unroll
-                        for (int f = 0; f < F; ++f) {
-                            bool first = true;
-#pragma unroll
-                            for (int ff = 0; ff < f; ++ff) first = first && FR::grp(ff) != FR::grp(f);
-                            const uint32_t ad = tmem + L::A_BASE + a * L::A_UNIT + (s * F + f) * 8;
-                            for (int t = 0; t < it.nrows; ++t)
-                                tm_mma_i8(tmem + (FR::grp(f) * kPassRows + t) * 8, ad,
-                                          desc_kmajor(rb + t * XR + R::off(PL, st, f, 0, 0), 16 * PL, 256), idesc,
-                                          (st > 0 || !first) ? 1 : 0);
-                        }
-                    }
-                    tm_commit(&aempty[a]);
-                    T.ev(6, 3, it, PHASE);
-                }
-                tm_commit(&bempty[b]);
-                tm_commit(accfull);
-                T.ev(6, 1, it, PHASE);
+                for (int s = 0; s < PL; ++s) v += (long long)srow[s * it.nrows + t] << (8 * s);
+                V[t] = v;
             }
-        }
-        __syncwarp();
-    } else if (warp < kTcUnpack) {
-        // ===== unpackers: thread = channel m (TMEM lane m); a stream of weight units
-        const int m = threadIdx.x;
-        const uint32_t tl = tmem + (uint32_t(32 * warp) << 16) + L::A_BASE;
-        Tracer T = tracer(threadIdx.x == 0 ? tr : nullptr, 1, 128);
-        int slot = 0, sph = 0, ua = 0, seq = 0;
-        for (int i = clu; i < nitems; i += nclu, ++seq) {
-            const GemvItem it = item_of(seq, i, TBL, n_gemv, nmt);
-            T.ev(2, 3, it, PHASE);
-            for (int u = 0; u < nunits; ++u, ++ua) {
-                const int a = ua & 1;
-                mbar_wait(&full[slot], sph);
-                T.ev(5, u == 0 ? 0 : 1, it, PHASE);
-                mbar_wait(&aempty[a], ((ua >> 1) & 1) ^ 1);
-                tm_fence_after();
-                const uint8_t* U = ring + size_t(slot) * UB;
-                const int ns = min(US, nst - u * US);
-                for (int s = 0; s < ns; ++s) {
-                    uint32_t w[F][8];
-                    FR::row_words(U + s * SB, U + s * SB + TB, m, w);
-#pragma unroll
-                    for (int f = 0; f < F; ++f) tm_st8(tl + a * L::A_UNIT + (s * F + f) * 8, w[f]);
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[slot]);  // the packed codes are in registers / TMEM
-                if (++slot == NU) { slot = 0; sph ^= 1; }
-                tm_wait_st();
-                tm_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&afull[a]);
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&sempty[sb]);
+                mbar_arrive(&bempty[b]);
             }
-            T.ev(2, 1, it, PHASE);
-        }
-    } else {
-        // ===== epilogue (warps 4-7): thread = channel (TMEM lane quarter warp % 4)
-        const int ch = threadIdx.x - kTcUnpack * 32;
-        const int ew = warp - kTcUnpack;
-        const uint32_t tl = tmem + (uint32_t(32 * (warp & 3)) << 16);
-        const uint32_t red_rank0 = map_rank(red, 0), full_rank0 = map_rank(red_full, 0);
-        int pos0 = 0, pos1 = -1;
-        if (PHASE == 1) {
-            const int q = (ch & 63) >> 4, kid = (ch >> 6) * 16 + (ch & 15);
-            bool first = true;
-            for (int f = 0; f < F; ++f)
-                for (int h = 0; h < 2; ++h)
-                    for (int i = 0; i < 4; ++i)
-                        if (FR::kidx(f, h, i) == kid) {
-                            const int o = R::off(4, 0, f, 0, q * 8 + h * 4 + i);
-                            if (first) { pos0 = o; first = false; } else pos1 = o;
-                        }
-        }
-        int* srow = scr + ch * kScrStride;
-        Tracer T = tracer(ch == 0 ? tr : nullptr, 128, 160);
-        int seq = 0;
-        for (int i = clu; i < nitems; i += nclu, ++seq) {
-            const GemvItem it = item_of(seq, i, TBL, n_gemv, nmt);
-            const int b = seq % kBufs;
-            const int chg = it.mt * TILE_N + ch;
-            float sc = 0.f, bias = 0.f, gate[kPassRows] = {0.f, 0.f, 0.f, 0.f};
-            int tok[kPassRows] = {0, 0, 0, 0};
-            float es = 0.f, eb = 0.f;
-            if (rank == 0) {
-                sc = __ldg((PHASE == 1 ? g.s1 : g.s2) + int64_t(it.e) * Np + chg);
-                const float* bbp = PHASE == 1 ? g.b1 : g.b2;
-                bias = bbp ? __ldg(bbp + int64_t(it.e) * Np + chg) : 0.f;
-                if (PHASE == 1) { es = __ldg(g.smax1 + it.e); eb = __ldg(g.bmax1 + it.e); }
-                if (PHASE == 2)
+            if (CS > 1) {  // split-K: every rank's partial into rank 0 (DSMEM), fixed-order sum there
+                if (rank != 0) {
+                    if (lane == 0) wait_cluster(red_empty, (seq & 1) ^ 1);  // rank 0 took the previous item
+                    __syncwarp();
 #pragma unroll
                     for (int t = 0; t < kPassRows; ++t)
-                        if (t < it.nrows) { gate[t] = __ldg(P.perm_gate + it.row0 + t); tok[t] = __ldg(P.perm_token + it.row0 + t); }
-            }
-            mbar_wait(accfull, seq & 1);
-            T.ev(3, 0, it, PHASE);
-            tm_fence_after();
-            // column sums S[t][s] = Sum_g mult(g) acc[g][t][s]  (exact int32)
-            int S[kPassRows][4];
-#pragma unroll
-            for (int t = 0; t < kPassRows; ++t)
-#pragma unroll
-                for (int s = 0; s < 4; ++s) S[t][s] = 0;
-#pragma unroll
-            for (int gg = 0; gg < G; ++gg) {
-                int v[2][16];
-                tm_ld16(tl + gg * kPassRows * 8, v[0]);
-                tm_ld16(tl + gg * kPassRows * 8 + 16, v[1]);
-                tm_wait_ld();
+                        if (t < it.nrows) st_cluster_s64(red_rank0 + uint32_t(((rank * TILE_N + ch) * kPassRows + t) * 8), V[t]);
+                    __syncwarp();
+                    if (lane == 0) arrive_cluster(full_rank0);
+                    T.ev(3, 2, it, PHASE);
+                    continue;
+                }
+                if (lane == 0) wait_cluster(red_full, seq & 1);
+                __syncwarp();
 #pragma unroll
                 for (int t = 0; t < kPassRows; ++t)
-#pragma unroll
-                    for (int s = 0; s < PL; ++s) S[t][s] += FR::mult(gg) * v[t >> 1][(t & 1) * 8 + s];
+                    if (t < it.nrows)
+                        for (int r = 1; r < CS; ++r) V[t] += red[(r * TILE_N + ch) * kPassRows + t];
+                named_bar_sync(2, kEpiWarps * 32);  // every epilogue warp read red
+                if (ch >= 1 && ch < CS) arrive_cluster(map_rank(red_empty, ch));
             }
-            tm_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(accempty);
-            // to the column layout epi_item reads: column c = s * nrows + t
+            if (PHASE == 2) {
 #pragma unroll
-            for (int t = 0; t < kPassRows; ++t)
+                for (int t = 0; t < kPassRows; ++t) {
+                    if (t >= it.nrows || chg >= g.d) continue;
+                    const float y = pe[t] == kZeroRow ? 0.f : scale_pow2(V[t], pe[t] + LOGD);
+                    const float yg = fmaf(y, sc, bias) * gate[t];
+                    const int64_t o = int64_t(tok[t]) * g.d + chg;
+                    if (g.out_acc) atomicAdd(g.out_acc + o, yg);  // top-2: two addends onto zero
+                    else if (g.out_f16) static_cast<__half*>(g.out)[o] = __float2half_rn(yg);
+                    else static_cast<float*>(g.out)[o] = yg;
+                }
+            } else {
+                // mid = ReLU(y s + b) in fc2 fixed point -> stage mt % 8 of the rows' fc2 blocks
+                long long* zred = reinterpret_cast<long long*>(stg + kPassRows * 4 * R::STG);  // [4 warps][4 rows]
+                int p2[kPassRows];
 #pragma unroll
-                for (int s = 0; s < PL; ++s)
-                    if (t < it.nrows) srow[s * it.nrows + t] = S[t][s];
-            mbar_wait(&bfull[b], (seq / kBufs) & 1);  // acquire the row-block headers
-            epi_item<BITS, PHASE>(g, P, it, seq, ch, lane, ew, rank, CS, nst, nch2, Np, srow, bufs + b * kPassRows * XR,
-                                  red, red_rank0, full_rank0, red_full, red_empty, stg, pos0, pos1, &bempty[b], nullptr,
-                                  sc, bias, es, eb, gate, tok);
+                for (int t = 0; t < kPassRows; ++t) {
+                    p2[t] = kZeroRow;
+                    long long X2 = 0;
+                    if (t < it.nrows) {
+                        p2[t] = fc2_exp<BITS>(es, eb, l1[t]);
+                        const float y = pe[t] == kZeroRow ? 0.f : scale_pow2(V[t], pe[t] + LOGD);
+                        const float mid = fmaxf(fmaf(y, sc, bias), 0.0f);  // ReLU, model.cpp:190
+                        X2 = p2[t] == kZeroRow ? 0 : __float2int_rn(ldexpf(mid, p2[t]));
+                        const uint32_t dg = (uint32_t(int(X2)) + 0x80808080u) ^ 0x80808080u;  // 4 signed digits
+#pragma unroll
+                        for (int s = 0; s < 4; ++s) {
+                            uint8_t* pl = stg + (t * 4 + s) * R::STG;
+                            const uint8_t byte = uint8_t(dg >> (8 * s));
+                            pl[pos0] = byte;
+                            if (pos1 >= 0) pl[pos1] = byte;
+                        }
+                    }
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) X2 += __shfl_xor_sync(0xffffffffu, X2, off);
+                    if (lane == 0) zred[ew * kPassRows + t] = X2;
+                }
+                named_bar_sync(2, kEpiWarps * 32);  // the stage blocks and warp sums are complete
+                const int st2 = it.mt % kChunkStages, c2 = it.mt / kChunkStages;
+                constexpr int V16 = R::STG / 16;
+                for (int idx = ch; idx < it.nrows * 4 * V16; idx += kEpiWarps * 32) {
+                    const int t = idx / (4 * V16), s = (idx / V16) & 3, u = idx % V16;
+                    uint8_t* dst = g.xb + (int64_t(it.row0 + t) * nch2 + c2) * R::XR2 + R::HDR2 + s * R::PB +
+                                   st2 * R::STG + 16 * u;
+                    *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(stg + (t * 4 + s) * R::STG + 16 * u);
+                }
+                if (ch < it.nrows) {
+                    const int t = ch;
+                    int p2t = kZeroRow;
+#pragma unroll
+                    for (int u = 0; u < kPassRows; ++u)
+                        if (u == t) p2t = p2[u];
+                    uint8_t* hb = g.xb + (int64_t(it.row0 + t) * nch2 + c2) * R::XR2;
+                    long long z = 0;
+                    for (int w = 0; w < kEpiWarps; ++w) z += zred[w * kPassRows + t];
+                    *reinterpret_cast<long long*>(hb + 64 + 8 * st2) = z;
+                    *reinterpret_cast<int*>(hb) = p2t;  // the same value from every m-tile of the pass
+                }
+                named_bar_sync(2, kEpiWarps * 32);  // stage blocks / warp sums reused by the next item
+            }
             T.ev(3, 2, it, PHASE);
         }
     }
-    tm_fence_before();
     cluster_sync();  // no CTA leaves while a peer may still write its shared memory
-    if (warp == kTcMmaWarp) {
-        tm_fence_after();
-        tm_dealloc(tmem, 512);
-    }
     if (tr && threadIdx.x == 0) { tr[2 * (kSlots - 1)] = gtime_ns(); tr[2 * (kSlots - 1) + 1] = clock64(); }
 }
 
@@ -1146,56 +792,11 @@ cudaError_t launch_phase(const GemvArgs& g, const Plan& P, cudaStream_t st, int 
     return cudaLaunchKernelEx(&cfg, kern, g, P);
 }
 
-template <int BITS, int PHASE>
-cudaError_t launch_phase_tc(const GemvArgs& g, const Plan& P, cudaStream_t st, int num_sms) {
-    using L = LayoutTC<BITS, PHASE>;
-    auto kern = k_gemv_tc<BITS, PHASE>;
-    const int Kp = PHASE == 1 ? g.Kp1 : g.Kp2;
-    const int cs = (Kp + kChunkK - 1) / kChunkK;
-    const int smem = L::total(cs);
-    static bool configured = false;
-    static int ncl[kMaxCluster + 1] = {0};
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
-    if (ncl[cs] == 0) ncl[cs] = active_clusters(kern, cs, smem, kTcThreads, num_sms);
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(unsigned(ncl[cs] * cs));
-    cfg.blockDim = dim3(kTcThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = unsigned(cs);
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 2;
-    return cudaLaunchKernelEx(&cfg, kern, g, P);
-}
-
-// MOQE_GEMV_TC=1: the tcgen05 kernel. Parity-green, but slower for decode shapes:
-// an N=8 kind::i8 MMA is bound by its 4 KB A-operand read (~64 cycles, measured by
-// tools/probe_umma_rate.cu), which exceeds what mma.sync needs per 128-k stage.
-bool use_imma() {
-    static const bool v = [] { const char* s = getenv("MOQE_GEMV_TC"); return !(s && atoi(s) != 0); }();
-    return v;
-}
-
 template <int BITS>
 cudaError_t launch_gemv_t(const GemvArgs& g, const Plan& P, cudaStream_t st, int num_sms) {
-    if (use_imma()) {
-        cudaError_t e = launch_phase<BITS, 1>(g, P, st, num_sms);
-        if (e != cudaSuccess) return e;
-        return launch_phase<BITS, 2>(g, P, st, num_sms);
-    }
-    cudaError_t e = launch_phase_tc<BITS, 1>(g, P, st, num_sms);
+    cudaError_t e = launch_phase<BITS, 1>(g, P, st, num_sms);
     if (e != cudaSuccess) return e;
-    return launch_phase_tc<BITS, 2>(g, P, st, num_sms);
+    return launch_phase<BITS, 2>(g, P, st, num_sms);
 }
 }  // namespace
 

@@ -28,20 +28,6 @@ struct Frag<2> {
     __host__ __device__ static constexpr int kidx(int f, int h, int i) {
         return 16 * h + (i == 0 ? 2 * f : i == 1 ? 8 + 2 * f : i == 2 ? 2 * f + 1 : 9 + 2 * f);
     }
-    // One channel row of a stage (tcgen05 path): w[f][2 tq + h] = the word lane tq holds in register h.
-    __device__ static __forceinline__ void row_words(const uint8_t* T0, const uint8_t* T1, int m, uint32_t (&w)[F][8]) {
-        const uint4 r0 = *reinterpret_cast<const uint4*>(T0 + m * 16);
-        const uint4 r1 = *reinterpret_cast<const uint4*>(T1 + m * 16);
-        const uint32_t a0[4] = {r0.x, r0.y, r0.z, r0.w}, a1[4] = {r1.x, r1.y, r1.z, r1.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int tq = 0; tq < 4; ++tq) {
-                const uint32_t M = 0x03030303u << (2 * j);
-                w[j][2 * tq] = a0[tq] & M;
-                w[j][2 * tq + 1] = a1[tq] & M;
-            }
-    }
     __device__ static __forceinline__ void load(const uint8_t* T0, const uint8_t* T1, int r0, int tq,
                                                 uint32_t (&a)[F][4]) {
         const uint32_t w00 = *reinterpret_cast<const uint32_t*>(T0 + r0 * 16 + 4 * tq);
@@ -67,23 +53,6 @@ struct Frag<3> {
              : f == 2 ? 16 * h + (i == 0 ? 8 : i == 1 ? 10 : i == 2 ? 9 : 11)
              : f == 3 ? 16 * (i >> 1) + 12 + 2 * h + (i & 1)
                       : 16 * (i >> 1) + 8 + 2 * h + (i & 1);
-    }
-    __device__ static __forceinline__ void row_words(const uint8_t* T0, const uint8_t* T1, int m, uint32_t (&w)[F][8]) {
-        const uint2* p0 = reinterpret_cast<const uint2*>(T0 + m * 24);
-        const uint2* p1 = reinterpret_cast<const uint2*>(T1 + m * 24);
-        const uint2 x0 = p0[0], y0 = p0[1], z0 = p0[2], x1 = p1[0], y1 = p1[1], z1 = p1[2];
-        const uint32_t A0[4] = {x0.x, x0.y, y0.x, y0.y}, A1[4] = {x1.x, x1.y, y1.x, y1.y};
-        const uint32_t B0[4] = {z0.x & 0xFFFFu, z0.x >> 16, z0.y & 0xFFFFu, z0.y >> 16};
-        const uint32_t B1[4] = {z1.x & 0xFFFFu, z1.x >> 16, z1.y & 0xFFFFu, z1.y >> 16};
-#pragma unroll
-        for (int tq = 0; tq < 4; ++tq) {
-            const uint32_t Bc = B0[tq] | (B1[tq] << 16);
-            w[0][2 * tq] = A0[tq] & 0x07070707u; w[0][2 * tq + 1] = A1[tq] & 0x07070707u;
-            w[1][2 * tq] = A0[tq] & 0x38383838u; w[1][2 * tq + 1] = A1[tq] & 0x38383838u;
-            w[2][2 * tq] = A0[tq] & 0xC0C0C0C0u; w[2][2 * tq + 1] = A1[tq] & 0xC0C0C0C0u;
-            w[3][2 * tq] = Bc & 0x07070707u; w[3][2 * tq + 1] = (Bc >> 3) & 0x07070707u;
-            w[4][2 * tq] = Bc & 0x40404040u; w[4][2 * tq + 1] = (Bc >> 1) & 0x40404040u;
-        }
     }
     __device__ static __forceinline__ void load(const uint8_t* T0, const uint8_t* T1, int r0, int tq,
                                                 uint32_t (&a)[F][4]) {
@@ -115,22 +84,6 @@ struct Frag<4> {
     __host__ __device__ static constexpr int kidx(int f, int h, int i) {
         return 16 * (f >> 1) + 8 * h + 2 * (f & 1) + (i == 0 ? 0 : i == 1 ? 4 : i == 2 ? 1 : 5);
     }
-    __device__ static __forceinline__ void row_words(const uint8_t* T0, const uint8_t* T1, int m, uint32_t (&w)[F][8]) {
-        const uint4* p0 = reinterpret_cast<const uint4*>(T0 + m * 32);
-        const uint4* p1 = reinterpret_cast<const uint4*>(T1 + m * 32);
-        const uint4 a = p0[0], b = p0[1], c = p1[0], d = p1[1];
-        const uint2 X0[4] = {make_uint2(a.x, a.y), make_uint2(a.z, a.w), make_uint2(b.x, b.y), make_uint2(b.z, b.w)};
-        const uint2 X1[4] = {make_uint2(c.x, c.y), make_uint2(c.z, c.w), make_uint2(d.x, d.y), make_uint2(d.z, d.w)};
-#pragma unroll
-        for (int g = 0; g < 2; ++g) {
-            const uint32_t M = g ? 0xF0F0F0F0u : 0x0F0F0F0Fu;
-#pragma unroll
-            for (int tq = 0; tq < 4; ++tq) {
-                w[g][2 * tq] = X0[tq].x & M; w[g][2 * tq + 1] = X0[tq].y & M;
-                w[2 + g][2 * tq] = X1[tq].x & M; w[2 + g][2 * tq + 1] = X1[tq].y & M;
-            }
-        }
-    }
     __device__ static __forceinline__ void load(const uint8_t* T0, const uint8_t* T1, int r0, int tq,
                                                 uint32_t (&a)[F][4]) {
         const uint2 w00 = *reinterpret_cast<const uint2*>(T0 + r0 * 32 + 8 * tq);
@@ -152,18 +105,6 @@ struct Frag<8> {
     __host__ __device__ static constexpr int grp(int) { return 0; }
     __host__ __device__ static constexpr int mult(int) { return 1; }
     __host__ __device__ static constexpr int kidx(int f, int h, int i) { return 16 * (f >> 1) + 8 * (f & 1) + 4 * h + i; }
-    __device__ static __forceinline__ void row_words(const uint8_t* T0, const uint8_t* T1, int m, uint32_t (&w)[F][8]) {
-        const uint4* p0 = reinterpret_cast<const uint4*>(T0 + m * 64);
-        const uint4* p1 = reinterpret_cast<const uint4*>(T1 + m * 64);
-#pragma unroll
-        for (int tq = 0; tq < 4; ++tq) {
-            const uint4 q0 = p0[tq], q1 = p1[tq];
-            w[0][2 * tq] = q0.x; w[0][2 * tq + 1] = q0.y;
-            w[1][2 * tq] = q0.z; w[1][2 * tq + 1] = q0.w;
-            w[2][2 * tq] = q1.x; w[2][2 * tq + 1] = q1.y;
-            w[3][2 * tq] = q1.z; w[3][2 * tq + 1] = q1.w;
-        }
-    }
     __device__ static __forceinline__ void load(const uint8_t* T0, const uint8_t* T1, int r0, int tq,
                                                 uint32_t (&a)[F][4]) {
         const uint4 w00 = *reinterpret_cast<const uint4*>(T0 + r0 * 64 + 16 * tq);
