@@ -135,7 +135,7 @@ moqe_status ensure_workspace(moqe_bank* b, int64_t T, int topk) {
     auto add = [&](int64_t sz, int64_t n) { bytes += round_up(sz * std::max<int64_t>(n, 1), 256); };
     add(4, capR); add(4, capR); add(4, capR); add(4, nctas * E); add(4, E); add(4, E + 1);
     add(4, capR); add(4, capR); add(4, capR); add(4, E); add(4, E); add(4, E + 1); add(4, 8);
-    add(4, 8); add(4, E);
+    add(4, 8); add(4, E); add(16, std::max(E + 1, 64));
     add(2, capR * b->Np1); add(2, capR * b->Kp1); add(4, capT * b->d); add(4, capT * E);
     const int64_t xr_bytes = gemv_xr_bytes(b->bits) * gemv_chunks(b->Kp1) * capT;
     const int64_t xb_bytes = gemv_xb_bytes(b->bits) * gemv_chunks(b->Kp2) * capR;
@@ -160,6 +160,7 @@ moqe_status ensure_workspace(moqe_bank* b, int64_t T, int topk) {
     P.meta = carve<int32_t>(p, 8);
     P.tickets = carve<unsigned>(p, 8);
     P.done = carve<unsigned>(p, E);
+    P.gtab = carve<int4>(p, std::max(E + 1, 64));  // >= 33: the GEMV's speculative first load round
     w.mid = carve<__half>(p, capR * b->Np1);
     w.x_perm = carve<__half>(p, capR * b->Kp1);
     w.out_acc = carve<float>(p, capT * b->d);
@@ -525,7 +526,7 @@ moqe_status moqe_gpu_route(const void* h, moqe_dtype h_dtype, int64_t t, int64_t
     auto sz = [&](int64_t n) { int64_t r = bytes; bytes += round_up(4 * std::max<int64_t>(n, 1), 256); return r; };
     const int64_t o_lrank = sz(R), o_cta = sz(nctas * E), o_counts = sz(E), o_off = sz(E + 1),
                   o_pt = sz(R), o_pg = sz(R), o_inv = sz(R), o_gl = sz(E), o_ml = sz(E), o_ts = sz(E + 1),
-                  o_meta = sz(8), o_tk = sz(8), o_done = sz(E), o_log = sz(t * E);
+                  o_meta = sz(8), o_tk = sz(8), o_done = sz(E), o_log = sz(t * E), o_gt = sz(4 * (E + 1));
     char* blk = nullptr;
     MOQE_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&blk), bytes, st));
     MOQE_CUDA(cudaMemsetAsync(blk, 0, bytes, st));
@@ -546,6 +547,7 @@ moqe_status moqe_gpu_route(const void* h, moqe_dtype h_dtype, int64_t t, int64_t
     P.tickets = reinterpret_cast<unsigned*>(blk + o_tk);
     P.done = reinterpret_cast<unsigned*>(blk + o_done);
     P.logits = reinterpret_cast<float*>(blk + o_log);
+    P.gtab = reinterpret_cast<int4*>(blk + o_gt);
     RouteArgs ra{h, h_dtype == MOQE_F16, t, int(d), wg, E, top_k, 0, 0, 128, nullptr};
     cudaError_t ce = launch_route(ra, P, st);
     cudaFreeAsync(blk, st);

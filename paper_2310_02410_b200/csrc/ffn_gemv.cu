@@ -123,6 +123,7 @@ struct GemvTables {
     int start[kMaxListed + 1];  // item prefix per listed expert
     int tok[kTokCache];         // perm_token[0, kTokCache) (fc1 row-block sources)
     int4 items[kItemCache];     // (e, mt, row0, nrows) of this CTA's k-th item
+    int n;                      // n_gemv
 };
 
 __device__ __forceinline__ int find_listed(const int* st, int n, int v) {  // largest a with st[a] <= v
@@ -134,24 +135,37 @@ __device__ __forceinline__ int find_listed(const int* st, int n, int v) {  // la
     return lo;
 }
 
-// Item tables from the plan (one warp: lane-parallel loads, serial prefix).
-__device__ void build_tables(GemvTables& T, const Plan& P, int n_gemv, int nmt, int lane, int64_t rows) {
+// Item tables from the plan's GEMV table (one warp, ONE load round: the header and
+// the first 32 entries are fetched together; prefix by a warp scan). Returns n_gemv
+// in T.n.
+__device__ void build_tables(GemvTables& T, const Plan& P, int nmt, int lane, int64_t rows) {
     const int nr = rows < kTokCache ? int(rows) : kTokCache;
+    const int n = P.gtab[0].x;
+    int4 v = P.gtab[1 + lane];  // speculative: valid if lane < n
     for (int r = lane; r < nr; r += 32) T.tok[r] = P.perm_token[r];
-    for (int a = lane; a < n_gemv; a += 32) {
-        const int e = P.gemv_list[a];
-        T.list[a] = e;
-        T.cnt[a] = P.counts[e];
-        T.off[a] = P.offsets[e];
-    }
-    __syncwarp();
-    if (lane == 0) {
-        int t = 0;
-        for (int a = 0; a < n_gemv; ++a) {
-            T.start[a] = t;
-            t += nmt * ((T.cnt[a] + kPassRows - 1) / kPassRows);
+    int running = 0;
+    for (int a0 = 0; a0 < n; a0 += 32) {
+        if (a0 > 0) v = P.gtab[1 + a0 + lane];
+        const int a = a0 + lane;
+        const bool ok = a < n;
+        const int np = ok ? nmt * ((v.y + kPassRows - 1) / kPassRows) : 0;
+        int incl = np;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += y;
         }
-        T.start[n_gemv] = t;
+        if (ok) {
+            T.list[a] = v.x;
+            T.cnt[a] = v.y;
+            T.off[a] = v.z;
+            T.start[a] = running + incl - np;
+        }
+        running += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) {
+        T.start[n] = running;
+        T.n = n;
     }
 }
 
@@ -387,10 +401,10 @@ struct Layout {
     static constexpr int SCR = kScrBufs * TILE_N * kScrStride * 4;
     static constexpr int STG = PHASE == 1 ? rup(kPassRows * 4 * R::STG + kEpiWarps * kPassRows * 8, 128) : 0;
     static constexpr int TABLES = rup(int(sizeof(GemvTables)), 128);
-    static constexpr int BARS = rup((2 * kMaxNU + 2 * kBufs + 2 * kScrBufs + 2) * 8, 128);
+    static constexpr int BARS = rup((2 * kMaxNU + 2 * kBufs + 2 * kScrBufs + 4) * 8, 128);
     static constexpr int O_ZERO = BUFS, O_SCR = O_ZERO + ZERO, O_STG = O_SCR + SCR, O_TAB = O_STG + STG;
     static constexpr int O_BARS = O_TAB + TABLES, O_RED = O_BARS + BARS;
-    __host__ __device__ static constexpr int red_bytes(int cs) { return cs > 1 ? cs * TILE_N * kPassRows * 8 : 0; }
+    __host__ __device__ static constexpr int red_bytes(int cs) { return cs > 1 ? 2 * (cs - 1) * TILE_N * kPassRows * 8 : 0; }
     __host__ __device__ static constexpr int ring_off(int cs) { return rup(O_RED + red_bytes(cs), 128); }
     __host__ __device__ static constexpr int nu(int cs) {
         return (kSmemMax - ring_off(cs)) / Cfg<BITS>::UB < kMaxNU ? (kSmemMax - ring_off(cs)) / Cfg<BITS>::UB : kMaxNU;
@@ -425,10 +439,13 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
     uint64_t* bempty = bfull + kBufs;
     uint64_t* sfull = bempty + kBufs;
     uint64_t* sempty = sfull + kScrBufs;
-    uint64_t* red_full = sempty + kScrBufs;  // rank 0: every other rank's partials landed
-    uint64_t* red_empty = red_full + 1;      // rank r: rank 0 consumed the previous partials
+    uint64_t* red_full = sempty + kScrBufs;  // [2] rank 0: every other rank's partials of the item landed
+    uint64_t* red_empty = red_full + 2;      // [2] rank r: rank 0 consumed that buffer
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int kSlots = kTraceCap / 2;
+    unsigned long long* tr = g.trace ? g.trace + size_t(blockIdx.x) * kTraceCap * 2 + (PHASE == 2 ? kTraceCap : 0) : nullptr;
+    if (tr && threadIdx.x == 0) { tr[0] = gtime_ns(); tr[1] = clock64(); }  // anchor: kernel entry
     const int Kp = PHASE == 1 ? g.Kp1 : g.Kp2;
     const int Np = PHASE == 1 ? g.Np1 : g.Np2;
     const int k0 = rank * kChunkK, nst = (min(kChunkK, Kp - k0) + kStageK - 1) / kStageK;
@@ -437,17 +454,20 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
         for (int s = 0; s < NU; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kConsumers); }
         for (int b = 0; b < kBufs; ++b) { mbar_init(&bfull[b], 1); mbar_init(&bempty[b], kConsumers + kEpiWarps); }
         for (int b = 0; b < kScrBufs; ++b) { mbar_init(&sfull[b], kConsumers); mbar_init(&sempty[b], kEpiWarps); }
-        mbar_init(red_full, kEpiWarps * max(CS - 1, 1));
-        mbar_init(red_empty, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&red_full[b], kEpiWarps * max(CS - 1, 1));
+            mbar_init(&red_empty[b], 1);
+        }
         fence_barrier_init();
     }
     for (int i = threadIdx.x; i < L::ZERO / 16; i += blockDim.x)
         reinterpret_cast<uint4*>(const_cast<uint8_t*>(zero))[i] = make_uint4(0u, 0u, 0u, 0u);
     if (PHASE == 1) pdl_wait();  // routing plan and fc1 row blocks (fc2: the plan is older than fc1's wait)
-    const int n_gemv = P.meta[0];
+    if (tr && threadIdx.x == 0) { tr[2] = clock64(); tr[3] = 7ull << 60 | 0ull << 56 | (unsigned long long)PHASE << 48 | 1ull; }
     const int nmt = Np / TILE_N;
-    if (warp == 0 && n_gemv > 0) build_tables(TBL, P, n_gemv, nmt, lane, PHASE == 1 ? g.T * g.topk : 0);
+    if (warp == 0) build_tables(TBL, P, nmt, lane, PHASE == 1 ? g.T * g.topk : 0);
     __syncthreads();
+    const int n_gemv = TBL.n;
     const int nitems = n_gemv > 0 ? TBL.start[n_gemv] : 0;
     const int clu = int(blockIdx.x) / CS, nclu = int(gridDim.x) / CS;
     for (int k = threadIdx.x; k < kItemCache; k += blockDim.x) {
@@ -461,9 +481,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
     if (PHASE == 1) pdl_trigger();  // the fc2 grid may launch as CTAs of this grid retire
     const int nch2 = (g.Kp2 + kChunkK - 1) / kChunkK;
     // trace rows: fc1 events in the first half of each CTA row, fc2 in the second
-    constexpr int kSlots = kTraceCap / 2;
-    unsigned long long* tr = g.trace ? g.trace + size_t(blockIdx.x) * kTraceCap * 2 + (PHASE == 2 ? kTraceCap : 0) : nullptr;
-    if (tr && threadIdx.x == 0) { tr[0] = gtime_ns(); tr[1] = clock64(); }
+        if (tr && threadIdx.x == 0) { tr[4] = clock64(); tr[5] = 7ull << 60 | 1ull << 56 | (unsigned long long)PHASE << 48 | 1ull; }
 
     if (warp == kProdWarp) {
         // ===== producer: each item's row blocks, then its weight copy units
@@ -515,7 +533,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
         // ===== consumers: warp -> m16 block (16 channels) of the 128-channel item
         const int gq = lane >> 2, tq = lane & 3;
         const int r0 = 16 * warp + gq;
-        Tracer T = tracer(threadIdx.x == 0 ? tr : nullptr, 1, 128);
+        Tracer T = tracer(threadIdx.x == 0 ? tr : nullptr, 3, 128);
         int slot = 0, sph = 0, seq = 0;
         for (int i = clu; i < nitems; i += nclu, ++seq) {
             const GemvItem it = item_of(seq, i, TBL, n_gemv, nmt);
@@ -652,25 +670,29 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
                 mbar_arrive(&bempty[b]);
             }
             if (CS > 1) {  // split-K: every rank's partial into rank 0 (DSMEM), fixed-order sum there
+                // partials double-buffered by item parity: rank r may run one item ahead of rank 0
+                const int rbuf = seq & 1;
+                const long long* redb = red + rbuf * (CS - 1) * TILE_N * kPassRows;
                 if (rank != 0) {
-                    if (lane == 0) wait_cluster(red_empty, (seq & 1) ^ 1);  // rank 0 took the previous item
+                    if (lane == 0) wait_cluster(&red_empty[rbuf], ((seq >> 1) & 1) ^ 1);  // rank 0 took item seq - 2
                     __syncwarp();
+                    const uint32_t dst = red_rank0 + uint32_t((rbuf * (CS - 1) + rank - 1) * TILE_N * kPassRows * 8);
 #pragma unroll
                     for (int t = 0; t < kPassRows; ++t)
-                        if (t < it.nrows) st_cluster_s64(red_rank0 + uint32_t(((rank * TILE_N + ch) * kPassRows + t) * 8), V[t]);
+                        if (t < it.nrows) st_cluster_s64(dst + uint32_t((ch * kPassRows + t) * 8), V[t]);
                     __syncwarp();
-                    if (lane == 0) arrive_cluster(full_rank0);
+                    if (lane == 0) arrive_cluster(full_rank0 + uint32_t(rbuf * 8));
                     T.ev(3, 2, it, PHASE);
                     continue;
                 }
-                if (lane == 0) wait_cluster(red_full, seq & 1);
+                if (lane == 0) wait_cluster(&red_full[rbuf], (seq >> 1) & 1);
                 __syncwarp();
 #pragma unroll
                 for (int t = 0; t < kPassRows; ++t)
                     if (t < it.nrows)
-                        for (int r = 1; r < CS; ++r) V[t] += red[(r * TILE_N + ch) * kPassRows + t];
-                named_bar_sync(2, kEpiWarps * 32);  // every epilogue warp read red
-                if (ch >= 1 && ch < CS) arrive_cluster(map_rank(red_empty, ch));
+                        for (int r = 1; r < CS; ++r) V[t] += redb[((r - 1) * TILE_N + ch) * kPassRows + t];
+                named_bar_sync(2, kEpiWarps * 32);  // every epilogue warp read this buffer
+                if (ch >= 1 && ch < CS) arrive_cluster(map_rank(&red_empty[rbuf], ch));
             }
             if (PHASE == 2) {
 #pragma unroll

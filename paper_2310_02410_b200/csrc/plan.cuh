@@ -1,6 +1,7 @@
 // plan.cuh — device workspace shared by route -> permute -> expert FFN kernels.
 #pragma once
 #include <stdint.h>
+#include <vector_types.h>
 
 namespace moqe_gpu {
 
@@ -24,6 +25,7 @@ struct Plan {
     unsigned* tickets;    // [8]    0: route last-CTA, 1: gemv fc1 items, 2: gemm fc1, 3: gemm fc2, 4: gemv fc2
     unsigned* done;       // [E]    (reserved; reset per forward)
     float* logits;        // [T][E] router logits (large-T path)
+    int4* gtab;           // [E+1] GEMV table: [0].x = n_gemv, [1+a] = {expert, rows, row offset, 0} (one load round)
 };
 
 }  // namespace moqe_gpu

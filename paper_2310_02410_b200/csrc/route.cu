@@ -65,9 +65,10 @@ __device__ void plan_lists(const RouteArgs& a, Plan& P, const int* cnt, int* s_o
                 const int y = __shfl_up_sync(0xffffffffu, incl, off);
                 if (lane >= off) incl += y;
             }
+            const int off_e = run + incl - n;
             if (e < E) {
-                P.offsets[e] = run + incl - n;
-                if (s_off) s_off[e] = run + incl - n;
+                P.offsets[e] = off_e;
+                if (s_off) s_off[e] = off_e;
             }
             run += __shfl_sync(0xffffffffu, incl, 31);
             int m = n;
@@ -78,7 +79,10 @@ __device__ void plan_lists(const RouteArgs& a, Plan& P, const int* cnt, int* s_o
             const bool gemm = n > 0 && !gemv;
             const unsigned bg = __ballot_sync(0xffffffffu, gemv), bm = __ballot_sync(0xffffffffu, gemm);
             const unsigned lt = (1u << lane) - 1u;
-            if (gemv) P.gemv_list[ngemv + __popc(bg & lt)] = e;
+            if (gemv) {
+                P.gemv_list[ngemv + __popc(bg & lt)] = e;
+                P.gtab[1 + ngemv + __popc(bg & lt)] = make_int4(e, n, off_e, 0);
+            }
             const int nt = gemm ? (n + a.gemm_bn - 1) / a.gemm_bn : 0;
             int tincl = nt;
 #pragma unroll
@@ -99,6 +103,7 @@ __device__ void plan_lists(const RouteArgs& a, Plan& P, const int* cnt, int* s_o
             P.offsets[E] = run;
             P.gemm_tile_start[ngemm] = tiles;
             P.meta[0] = ngemv;
+            P.gtab[0] = make_int4(ngemv, 0, 0, 0);
             P.meta[1] = ngemm;
             P.meta[2] = tiles;
             P.meta[3] = mx;

@@ -1,0 +1,36 @@
+// probe_imma_rate.cu — mma.sync.m16n8k32.u8.s8 throughput on B200: cycles per IMMA per
+// SM sub-partition for W warps per SMSP, 8 independent accumulators per warp.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -o tools/probe_imma_rate tools/probe_imma_rate.cu
+#include <cstdio>
+#include <cstdint>
+__device__ __forceinline__ void imma(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                 : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3]) : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__global__ void k(int n, int* out, long long* cyc) {
+    int acc[8][4] = {};
+    uint32_t a = threadIdx.x * 0x01010101u, b = threadIdx.x * 0x00010001u;
+    __syncthreads();
+    long long t0 = clock64();
+    for (int i = 0; i < n; ++i) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) imma(acc[j], a + j, a ^ j, a + 2 * j, a ^ (3 * j), b + j, b ^ j);
+    }
+    long long t1 = clock64();
+    int s = 0;
+    for (int j = 0; j < 8; ++j) s += acc[j][0] + acc[j][1] + acc[j][2] + acc[j][3];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+    if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = t1 - t0;
+}
+int main() {
+    int* o; long long* c; cudaMalloc(&o, 1 << 20); cudaMalloc(&c, 8);
+    const int n = 256;
+    for (int warps : {4, 8, 16, 32}) {
+        k<<<148, warps * 32>>>(n, o, c); k<<<148, warps * 32>>>(n, o, c);
+        long long h; cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
+        const double per_smsp = double(n) * 8 * (warps / 4);
+        printf("%2d warps/SM (%d per SMSP): %.1f cycles per IMMA per SMSP  (%.0f int8 MAC/clk/SM)\n", warps, warps / 4,
+               double(h) / per_smsp, 4 * 4096.0 * per_smsp / double(h));
+    }
+    return 0;
+}

@@ -9,13 +9,14 @@
 using namespace moqe_gpu;
 
 __global__ void __launch_bounds__(160, 1) k_stream(const uint8_t* src, int64_t bytes_per_cta, int copy, int nst,
-                                                   int issuers, int hint, int* out) {
+                                                   int issuers, int hint, int* out, unsigned long long* span) {
+    if (threadIdx.x == 0 && span) span[2 * blockIdx.x] = gtime_ns();
     extern __shared__ __align__(128) uint8_t sm[];
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + size_t(nst) * copy);
     uint64_t* empty = full + nst;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < nst; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 4); }
+        for (int s = 0; s < nst; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
         fence_barrier_init();
     }
     __syncthreads();
@@ -37,6 +38,7 @@ __global__ void __launch_bounds__(160, 1) k_stream(const uint8_t* src, int64_t b
         return;
     }
     int acc = 0;
+    if (warp > 0) return;  // one consumer warp suffices to wait / release (count 4 below)
     for (int64_t c = 0; c < n; ++c) {
         const int s = int(c % nst);
         mbar_wait(&full[s], int((c / nst) & 1));
@@ -45,6 +47,8 @@ __global__ void __launch_bounds__(160, 1) k_stream(const uint8_t* src, int64_t b
         if (lane == 0) mbar_arrive(&empty[s]);
     }
     if (acc == 0x12345678) out[0] = acc;
+    __syncwarp();
+    if (threadIdx.x == 0 && span) span[2 * blockIdx.x + 1] = gtime_ns();
 }
 
 int main() {
@@ -61,14 +65,33 @@ int main() {
     for (auto c : cfgs) {
         const int nst = c.ring_kb * 1024 / c.copy;
         const size_t smem = size_t(nst) * c.copy + 2 * nst * 8;
-        k_stream<<<sms, 160, smem>>>(src, per_cta, c.copy, nst, c.issuers, c.hint, out);
+        k_stream<<<sms, 160, smem>>>(src, per_cta, c.copy, nst, c.issuers, c.hint, out, nullptr);
         cudaEventRecord(a);
-        k_stream<<<sms, 160, smem>>>(src, per_cta, c.copy, nst, c.issuers, c.hint, out);
+        k_stream<<<sms, 160, smem>>>(src, per_cta, c.copy, nst, c.issuers, c.hint, out, nullptr);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms; cudaEventElapsedTime(&ms, a, b);
         printf("copy %6d B ring %3d KB (%2d slots) issuers %d hint %d: %7.1f GB/s\n", c.copy, c.ring_kb, nst, c.issuers,
                c.hint, double(per_cta) * sms / (ms * 1e-3) / 1e9);
+    }
+    // short streams (the decode GEMV's per-CTA volume): in-kernel span (first start .. last end)
+    unsigned long long* span; cudaMalloc(&span, sms * 16);
+    struct S { int copy, nst, units; };
+    S ss[] = {{24576, 6, 7}, {24576, 6, 28}, {24576, 6, 112}, {16384, 8, 10}, {49152, 3, 4}, {24576, 4, 7}};
+    for (auto c : ss) {
+        const size_t smem = size_t(c.nst) * c.copy + 2 * c.nst * 8;
+        const int64_t per = int64_t(c.copy) * c.units;
+        for (int rep = 0; rep < 3; ++rep) {
+            // rotate the source so every run reads cold data
+            k_stream<<<sms, 160, smem>>>(src + int64_t(rep) * per * sms, per, c.copy, c.nst, 1, 1, out, span);
+        }
+        cudaDeviceSynchronize();
+        unsigned long long h[2 * 160];
+        cudaMemcpy(h, span, sms * 16, cudaMemcpyDeviceToHost);
+        unsigned long long lo = ~0ull, hi = 0; double mean = 0;
+        for (int i = 0; i < sms; ++i) { lo = h[2 * i] < lo ? h[2 * i] : lo; hi = h[2 * i + 1] > hi ? h[2 * i + 1] : hi; mean += double(h[2 * i + 1] - h[2 * i]); }
+        printf("short: copy %6d x %3d units (%4lld KB/CTA), ring %d: span %.2f us, mean CTA %.2f us -> %.0f GB/s\n", c.copy,
+               c.units, (long long)(per >> 10), c.nst, (hi - lo) / 1e3, mean / sms / 1e3, double(per) * sms / double(hi - lo));
     }
     printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
 }

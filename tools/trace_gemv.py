@@ -104,7 +104,7 @@ for phase in (1, 2):
 
 if os.environ.get("TRACE_CTA"):
     c = int(os.environ["TRACE_CTA"])
-    names = {(2, 5): "U B tile", (6, 0): "M item start", (6, 1): "M item issued", (6, 2): "M unit A ok", (6, 3): "M unit issued", (2, 3): "C top", (2, 0): "C bfull ok", (5, 0): "C unit0 in", (5, 1): "C unit+ in", (2, 1): "C mloop end",
+    names = {(7, 0): "K pdl_wait done", (7, 1): "K tables+cluster ok", (2, 5): "U B tile", (6, 0): "M item start", (6, 1): "M item issued", (6, 2): "M unit A ok", (6, 3): "M unit issued", (2, 3): "C top", (2, 0): "C bfull ok", (5, 0): "C unit0 in", (5, 1): "C unit+ in", (2, 1): "C mloop end",
              (2, 4): "C scr ok/U B done", (3, 0): "E start", (3, 2): "E end", (4, 0): "P unit0 iss", (4, 1): "P unit+ iss"}
     sel = valid[c]
     order = np.argsort(us[c][sel], kind="stable")
@@ -112,5 +112,5 @@ if os.environ.get("TRACE_CTA"):
     mt = ((w[c][sel][order] >> np.uint64(20)) & np.uint64(0xfff)).astype(int)
     ex = ((w[c][sel][order] >> np.uint64(32)) & np.uint64(0xffff)).astype(int)
     for a, b, p_, t_, m_, e_ in zip(rr, ee, pp, tt, mt, ex):
-        if p_ == 1:
+        if p_ == int(os.environ.get("TRACE_PHASE", "1")):
             print(f"{t_:8.2f}  {names.get((a, b), (a, b))!s:12s} e{e_} mt{m_}")
