@@ -450,26 +450,74 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
     const int Np = PHASE == 1 ? g.Np1 : g.Np2;
     const int k0 = rank * kChunkK, nst = (min(kChunkK, Kp - k0) + kStageK - 1) / kStageK;
     const int nunits = (nst + US - 1) / US;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < NU; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kConsumers); }
-        for (int b = 0; b < kBufs; ++b) { mbar_init(&bfull[b], 1); mbar_init(&bempty[b], kConsumers + kEpiWarps); }
-        for (int b = 0; b < kScrBufs; ++b) { mbar_init(&sfull[b], kConsumers); mbar_init(&sempty[b], kEpiWarps); }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(&red_full[b], kEpiWarps * max(CS - 1, 1));
-            mbar_init(&red_empty[b], 1);
-        }
-        fence_barrier_init();
-    }
+    const int nmt = Np / TILE_N;
+    const int clu = int(blockIdx.x) / CS, nclu = int(gridDim.x) / CS;
+    const uint8_t* wbase0 = PHASE == 1 ? g.w1 : g.w2;
+    const int64_t wstride = PHASE == 1 ? g.w1_stride : g.w2_stride;
+    int early_units = 0;     // producer: weight units of this CTA's first item issued before the table build
+    bool early_rows = false; // producer: its fc1 row blocks too
     for (int i = threadIdx.x; i < L::ZERO / 16; i += blockDim.x)
         reinterpret_cast<uint4*>(const_cast<uint8_t*>(zero))[i] = make_uint4(0u, 0u, 0u, 0u);
-    if (PHASE == 1) pdl_wait();  // routing plan and fc1 row blocks (fc2: the plan is older than fc1's wait)
+    if (warp == kProdWarp) {
+        // The producer owns the barriers' initialisation and starts its first item straight
+        // from the plan's GEMV table (one load round + a warp scan), before the CTA-wide table
+        // build and synchronisation: the weight stream starts ~2 us earlier.
+        if (lane == 0) {
+            for (int s = 0; s < NU; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kConsumers); }
+            for (int b = 0; b < kBufs; ++b) { mbar_init(&bfull[b], 1); mbar_init(&bempty[b], kConsumers + kEpiWarps); }
+            for (int b = 0; b < kScrBufs; ++b) { mbar_init(&sfull[b], kConsumers); mbar_init(&sempty[b], kEpiWarps); }
+            for (int b = 0; b < 2; ++b) {
+                mbar_init(&red_full[b], kEpiWarps * max(CS - 1, 1));
+                mbar_init(&red_empty[b], 1);
+            }
+            fence_barrier_init();
+        }
+        __syncwarp();
+        if (PHASE == 1) pdl_wait();  // routing plan and fc1 row blocks
+        const int n = P.gtab[0].x;
+        const int4 v = P.gtab[1 + lane];
+        if (n > 0 && n <= 32) {
+            const int np = lane < n ? nmt * ((v.y + kPassRows - 1) / kPassRows) : 0;
+            int incl = np;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += y;
+            }
+            const unsigned own = __ballot_sync(0xffffffffu, lane < n && incl - np <= clu && clu < incl);
+            if (own) {
+                const int src = __ffs(own) - 1;
+                const int e = __shfl_sync(0xffffffffu, v.x, src), cnt = __shfl_sync(0xffffffffu, v.y, src);
+                const int off0 = __shfl_sync(0xffffffffu, v.z, src), st0 = __shfl_sync(0xffffffffu, incl - np, src);
+                const int r = clu - st0, pass = r / nmt, mt = r - pass * nmt;
+                const int row0 = off0 + pass * kPassRows, nrows = min(kPassRows, cnt - pass * kPassRows);
+                const uint8_t* wb = wbase0 + int64_t(e) * wstride + (int64_t(mt) * (Kp / TILE_K) + k0 / TILE_K) * TB;
+                early_units = min(nunits, NU);
+                if (lane == 0) {
+                    const uint64_t pol = policy_evict_first();
+                    for (int u = 0; u < early_units; ++u) {
+                        const int bytes = min(US, nst - u * US) * SB;
+                        mbar_arrive_expect_tx(&full[u], uint32_t(bytes));
+                        bulk_g2s_hint(ring + size_t(u) * UB, wb + int64_t(u) * UB, uint32_t(bytes), &full[u], pol);
+                    }
+                }
+                if (PHASE == 1) {
+                    const int tok = lane < nrows ? P.perm_token[row0 + lane] : 0;
+                    if (lane == 0) mbar_arrive_expect_tx(&bfull[0], uint32_t(nrows * XR));
+                    __syncwarp();
+                    if (lane < nrows)
+                        bulk_g2s(bufs + lane * XR, g.xr + (int64_t(tok) * g.nch1 + rank) * XR, uint32_t(XR), &bfull[0]);
+                    early_rows = true;
+                }
+            }
+        }
+    }
+    if (PHASE == 1 && warp != kProdWarp) pdl_wait();  // every thread that reads the plan waits for it
     if (tr && threadIdx.x == 0) { tr[2] = clock64(); tr[3] = 7ull << 60 | 0ull << 56 | (unsigned long long)PHASE << 48 | 1ull; }
-    const int nmt = Np / TILE_N;
     if (warp == 0) build_tables(TBL, P, nmt, lane, PHASE == 1 ? g.T * g.topk : 0);
     __syncthreads();
     const int n_gemv = TBL.n;
     const int nitems = n_gemv > 0 ? TBL.start[n_gemv] : 0;
-    const int clu = int(blockIdx.x) / CS, nclu = int(gridDim.x) / CS;
     for (int k = threadIdx.x; k < kItemCache; k += blockDim.x) {
         const int i = clu + k * nclu;
         if (i >= nitems) break;
@@ -489,9 +537,8 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
             Tracer T = tracer(tr, 192, kSlots - 1);
             const uint64_t pol = policy_evict_first();
             bool waited = PHASE == 1;
-            int slot = 0, sph = 0, seq = 0;
-            const uint8_t* wbase0 = PHASE == 1 ? g.w1 : g.w2;
-            const int64_t wstride = PHASE == 1 ? g.w1_stride : g.w2_stride;
+            int slot = early_units, sph = 0, seq = 0;
+            if (slot == NU) { slot = 0; sph = 1; }
             for (int i = clu; i < nitems; i += nclu, ++seq) {
                 const GemvItem it = item_of(seq, i, TBL, n_gemv, nmt);
                 const int b = seq % kBufs;
@@ -507,9 +554,9 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
                         bulk_g2s(bufs + (b * kPassRows + t) * XR, src, uint32_t(XR), &bfull[b]);
                     }
                 };
-                if (!(PHASE == 2 && seq == 0)) issue_rows();
+                if (!(PHASE == 2 && seq == 0) && !(seq == 0 && early_rows)) issue_rows();
                 const uint8_t* wb = wbase0 + int64_t(it.e) * wstride + (int64_t(it.mt) * (Kp / TILE_K) + k0 / TILE_K) * TB;
-                for (int u = 0; u <= nunits; ++u) {
+                for (int u = seq == 0 ? early_units : 0; u <= nunits; ++u) {
                     // fc2, first item: its weights stream while fc1 finishes; its row blocks
                     // (written by fc1) are fetched once the ring is full or the item issued
                     if (PHASE == 2 && seq == 0 && !waited && (u == nunits || u == NU)) {
