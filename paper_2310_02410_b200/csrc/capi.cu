@@ -369,8 +369,13 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
                  gemm_block_n(), inline_scatter ? acc : nullptr,
                  b->trace ? b->trace + int64_t(b->num_sms) * kTraceCap * 2 : nullptr};
     cudaError_t ce;
+    bool self_plan = false;
     {
         KernelTimer kt(b, 0, st);
+        // decode, every expert on the GEMV path: the router writes only the choices and the
+        // GEMV kernels build the plan themselves (no serial plan step between them)
+        self_plan = !pre && !need_gemm && R <= kSelfPlanRows && t <= 32 && b->E <= 256;
+        ra.no_plan = self_plan ? 1 : 0;
         if (need_gemv) {  // token rows -> fc1 row blocks; the decode router overlaps it (PDL)
             XrowArgs xa{h, h_dtype == MOQE_F16, t, int(b->d), gemv_chunks(b->Kp1), w.xr};
             ce = launch_xrows(b->bits, xa, st);
@@ -390,7 +395,7 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
     if (need_gemv) {
         GemvArgs g{h, h_dtype == MOQE_F16, t, int(b->d), int(b->f), top_k, b->E, b->w1, b->w2,
                    b->w1_stride, b->w2_stride, b->s1, b->s2, b->b1, b->b2, b->Kp1, b->Np1, b->Kp2, b->Np2,
-                   out, out_dtype == MOQE_F16, acc, w.xr, gemv_chunks(b->Kp1), w.xb, b->smax1, b->bmax1, b->trace, gemv_dbg()};
+                   out, out_dtype == MOQE_F16, acc, w.xr, gemv_chunks(b->Kp1), w.xb, b->smax1, b->bmax1, b->trace, gemv_dbg(), self_plan ? 1 : 0};
         KernelTimer kt(b, 2, st);
         ce = launch_gemv(b->bits, g, P, st, b->num_sms);
         if (ce != cudaSuccess) return cuda_fail(ce, "k_ffn_gemv");

@@ -124,6 +124,10 @@ struct GemvTables {
     int tok[kTokCache];         // perm_token[0, kTokCache) (fc1 row-block sources)
     int4 items[kItemCache];     // (e, mt, row0, nrows) of this CTA's k-th item
     int n;                      // n_gemv
+    // self plan (decode, GEMV only): the router's raw choices -> positions
+    int rexp[kSelfPlanRows];    // expert of routed row i = (token, slot)
+    int eoff[kMaxListed];       // first permuted row of expert e
+    float gate[kSelfPlanRows];  // gate of permuted row (fc2 epilogue)
 };
 
 __device__ __forceinline__ int find_listed(const int* st, int n, int v) {  // largest a with st[a] <= v
@@ -167,6 +171,78 @@ __device__ void build_tables(GemvTables& T, const Plan& P, int nmt, int lane, in
         T.start[n] = running;
         T.n = n;
     }
+}
+
+// Self plan (decode, every routed expert on the GEMV path, T*k <= kSelfPlanRows):
+// the same counts, expert-order offsets, item prefix and stable row order as the
+// router's plan (route.cu plan_lists / the decode router's leader), built by one
+// warp from P.expert / P.gate in one load round — the router then only writes the
+// choices and never serialises a plan step.
+__device__ void build_tables_self(GemvTables& T, const Plan& P, int nr, int E, int k, int nmt, int lane) {
+    // rows i = lane and lane + 32; per-expert counts by smem atomics, stable ranks by
+    // __match_any (no per-lane loops over the rows)
+    const int i0 = lane, i1 = lane + 32;
+    const int e0 = i0 < nr ? P.expert[i0] : -1, e1 = i1 < nr ? P.expert[i1] : -1;
+    const float g0 = i0 < nr ? P.gate[i0] : 0.f, g1 = i1 < nr ? P.gate[i1] : 0.f;
+    int* h1 = T.rexp;  // scratch: [E] counts of rows 0..31 (E <= kSelfPlanRows handled below)
+    int* cnt = T.eoff;  // [E] total counts; the scan below reads each and overwrites it with the offset
+    for (int e = lane; e < E; e += 32) cnt[e] = 0;
+    const bool small = E <= kSelfPlanRows;
+    if (small) for (int e = lane; e < E; e += 32) h1[e] = 0;
+    __syncwarp();
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned m0 = __match_any_sync(0xffffffffu, e0), m1 = __match_any_sync(0xffffffffu, e1);
+    if (e0 >= 0 && (m0 & lt) == 0) atomicAdd(&cnt[e0], __popc(m0));   // leader of each group adds its size
+    if (e1 >= 0 && (m1 & lt) == 0) atomicAdd(&cnt[e1], __popc(m1));
+    if (small && e0 >= 0 && (m0 & lt) == 0) h1[e0] = __popc(m0);
+    __syncwarp();
+    int running = 0, nlisted = 0, items = 0;
+    for (int eb = 0; eb < E; eb += 32) {
+        const int e = eb + lane;
+        const int c = e < E ? cnt[e] : 0;
+        int incl = c;
+        const int np = c > 0 ? nmt * ((c + kPassRows - 1) / kPassRows) : 0;
+        int inp = np;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, off);
+            const int z = __shfl_up_sync(0xffffffffu, inp, off);
+            if (lane >= off) { incl += y; inp += z; }
+        }
+        if (e < E) T.eoff[e] = running + incl - c;
+        const unsigned bl = __ballot_sync(0xffffffffu, c > 0);
+        if (c > 0) {
+            const int a = nlisted + __popc(bl & lt);
+            T.list[a] = e;
+            T.cnt[a] = c;
+            T.off[a] = running + incl - c;
+            T.start[a] = items + inp - np;
+        }
+        running += __shfl_sync(0xffffffffu, incl, 31);
+        items += __shfl_sync(0xffffffffu, inp, 31);
+        nlisted += __popc(bl);
+    }
+    if (lane == 0) {
+        T.start[nlisted] = items;
+        T.n = nlisted;
+    }
+    __syncwarp();
+    // stable positions: row i -> eoff[e] + #{j < i : e_j == e}
+    if (e0 >= 0) {
+        const int pos = T.eoff[e0] + __popc(m0 & lt);
+        T.tok[pos] = i0 / k;
+        T.gate[pos] = g0;
+    }
+    if (e1 >= 0) {
+        int before = 0;  // rows 0..31 with the same expert
+        if (small) before = h1[e1];
+        else
+            for (int j = 0; j < 32; ++j) before += __shfl_sync(0xffffffffu, e0, j) == e1;
+        const int pos = T.eoff[e1] + before + __popc(m1 & lt);
+        T.tok[pos] = i1 / k;
+        T.gate[pos] = g1;
+    }
+    __syncwarp();
 }
 
 // Item i (expert-major: expert, pass, m-tile).
@@ -474,6 +550,37 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
         }
         __syncwarp();
         if (PHASE == 1) pdl_wait();  // routing plan and fc1 row blocks
+        if (g.self_plan) {
+            build_tables_self(TBL, P, int(g.T * g.topk), g.E, g.topk, nmt, lane);
+            if (tr && lane == 0) { tr[6] = clock64(); tr[7] = 7ull << 60 | 2ull << 56 | (unsigned long long)PHASE << 48 | 1ull; }
+            if (g.dbg == 3) {  // diagnostics: the same build again (warm instruction cache, warm data)
+                build_tables_self(TBL, P, int(g.T * g.topk), g.E, g.topk, nmt, lane);
+                if (tr && lane == 0) { tr[10] = clock64(); tr[11] = 7ull << 60 | 4ull << 56 | (unsigned long long)PHASE << 48 | 1ull; }
+            }
+            const int n = TBL.n;
+            if (clu < TBL.start[n]) {
+                const GemvItem it = item_at(clu, TBL, n, nmt);
+                const uint8_t* wb = wbase0 + int64_t(it.e) * wstride + (int64_t(it.mt) * (Kp / TILE_K) + k0 / TILE_K) * TB;
+                early_units = min(nunits, NU);
+                if (lane == 0) {
+                    const uint64_t pol = policy_evict_first();
+                    for (int u = 0; u < early_units; ++u) {
+                        const int bytes = min(US, nst - u * US) * SB;
+                        mbar_arrive_expect_tx(&full[u], uint32_t(bytes));
+                        bulk_g2s_hint(ring + size_t(u) * UB, wb + int64_t(u) * UB, uint32_t(bytes), &full[u], pol);
+                    }
+                    if (PHASE == 1) mbar_arrive_expect_tx(&bfull[0], uint32_t(it.nrows * XR));
+                }
+                if (PHASE == 1) {
+                    __syncwarp();
+                    if (lane < it.nrows)
+                        bulk_g2s(bufs + lane * XR, g.xr + (int64_t(TBL.tok[it.row0 + lane]) * g.nch1 + rank) * XR,
+                                 uint32_t(XR), &bfull[0]);
+                    early_rows = true;
+                }
+                if (tr && lane == 0) { tr[8] = clock64(); tr[9] = 7ull << 60 | 3ull << 56 | (unsigned long long)PHASE << 48 | 1ull; }
+            }
+        } else {
         const int n = P.gtab[0].x;
         const int4 v = P.gtab[1 + lane];
         if (n > 0 && n <= 32) {
@@ -511,10 +618,11 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
                 }
             }
         }
+        }
     }
     if (PHASE == 1 && warp != kProdWarp) pdl_wait();  // every thread that reads the plan waits for it
     if (tr && threadIdx.x == 0) { tr[2] = clock64(); tr[3] = 7ull << 60 | 0ull << 56 | (unsigned long long)PHASE << 48 | 1ull; }
-    if (warp == 0) build_tables(TBL, P, nmt, lane, PHASE == 1 ? g.T * g.topk : 0);
+    if (warp == 0 && !g.self_plan) build_tables(TBL, P, nmt, lane, PHASE == 1 ? g.T * g.topk : 0);
     __syncthreads();
     const int n_gemv = TBL.n;
     const int nitems = n_gemv > 0 ? TBL.start[n_gemv] : 0;
@@ -526,7 +634,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
     }
     __syncthreads();
     cluster_sync();  // barriers of every CTA initialised before any remote arrive
-    if (PHASE == 1) pdl_trigger();  // the fc2 grid may launch as CTAs of this grid retire
+    if (PHASE == 1 && threadIdx.x == 0) pdl_trigger();  // the fc2 grid may launch as CTAs retire (one thread per CTA)
     const int nch2 = (g.Kp2 + kChunkK - 1) / kChunkK;
     // trace rows: fc1 events in the first half of each CTA row, fc2 in the second
         if (tr && threadIdx.x == 0) { tr[4] = clock64(); tr[5] = 7ull << 60 | 1ull << 56 | (unsigned long long)PHASE << 48 | 1ull; }
@@ -538,6 +646,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
             const uint64_t pol = policy_evict_first();
             bool waited = PHASE == 1;
             int slot = early_units, sph = 0, seq = 0;
+            bool rows0 = false;  // fc2: the first item's row blocks are issued after its weights
             if (slot == NU) { slot = 0; sph = 1; }
             for (int i = clu; i < nitems; i += nclu, ++seq) {
                 const GemvItem it = item_of(seq, i, TBL, n_gemv, nmt);
@@ -559,9 +668,10 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
                 for (int u = seq == 0 ? early_units : 0; u <= nunits; ++u) {
                     // fc2, first item: its weights stream while fc1 finishes; its row blocks
                     // (written by fc1) are fetched once the ring is full or the item issued
-                    if (PHASE == 2 && seq == 0 && !waited && (u == nunits || u == NU)) {
-                        pdl_wait();
+                    if (PHASE == 2 && seq == 0 && !rows0 && (u == nunits || u == NU)) {
+                        if (!waited) pdl_wait();
                         waited = true;
+                        rows0 = true;
                         issue_rows();
                     }
                     if (u == nunits) break;
@@ -580,7 +690,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
         // ===== consumers: warp -> m16 block (16 channels) of the 128-channel item
         const int gq = lane >> 2, tq = lane & 3;
         const int r0 = 16 * warp + gq;
-        Tracer T = tracer(threadIdx.x == 0 ? tr : nullptr, 3, 128);
+        Tracer T = tracer(threadIdx.x == 0 ? tr : nullptr, 6, 128);
         int slot = 0, sph = 0, seq = 0;
         for (int i = clu; i < nitems; i += nclu, ++seq) {
             const GemvItem it = item_of(seq, i, TBL, n_gemv, nmt);
@@ -679,7 +789,10 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
                 if (PHASE == 2)
 #pragma unroll
                     for (int t = 0; t < kPassRows; ++t)
-                        if (t < it.nrows) { gate[t] = __ldg(P.perm_gate + it.row0 + t); tok[t] = __ldg(P.perm_token + it.row0 + t); }
+                        if (t < it.nrows) {
+                            if (g.self_plan) { gate[t] = TBL.gate[it.row0 + t]; tok[t] = TBL.tok[it.row0 + t]; }
+                            else { gate[t] = __ldg(P.perm_gate + it.row0 + t); tok[t] = __ldg(P.perm_token + it.row0 + t); }
+                        }
             }
             mbar_wait(&sfull[sb], (seq >> 1) & 1);
             T.ev(3, 0, it, PHASE);

@@ -43,6 +43,7 @@ struct RouteArgs {
     float* zero_out;     // top-2 fp32 accumulation rows to zero (inline scatter), or null
     unsigned long long* trace;  // router phase stamps [kTraceRouteCtas][16] or null (diagnostics)
     int pdl;                    // launched behind k_xrows: the decode router may start early (PDL)
+    int no_plan;                // decode GEMV-only: write expert / gate only (the GEMV kernels plan themselves)
 };
 constexpr int kTraceRouteCtas = 64;
 cudaError_t launch_route(const RouteArgs& a, const Plan& P, cudaStream_t st);
@@ -82,7 +83,9 @@ struct GemvArgs {
     const float* bmax1;            // [E] max |fc1 bias|
     unsigned long long* trace;     // [grid][kTraceCap][2] (time ns, event) or null
     int dbg;                       // diagnostics (env MOQE_GEMV_DBG; 1 = consumers skip the MMA work)
+    int self_plan;                 // plan built in each CTA from P.expert / P.gate (T*k <= kSelfPlanRows)
 };
+constexpr int kSelfPlanRows = 64;
 constexpr int kTraceCap = 512;
 cudaError_t launch_gemv(int bits, const GemvArgs& g, const Plan& P, cudaStream_t st, int num_sms);
 bool gemv_supported(int Kp1, int Kp2);

@@ -505,7 +505,8 @@ __global__ void __launch_bounds__((kRouteSmallWarps + 1) * 32, 1) k_route_decode
         fence_barrier_init();
     }
     __syncthreads();
-    cluster_arrive_release();  // rank 0 has started before anyone writes its shared memory (wait below)
+    const bool plan = !a.no_plan;  // uniform: with no_plan the CTAs never touch each other
+    if (plan) cluster_arrive_release();  // rank 0 has started before anyone writes its shared memory (wait below)
 
     if (warp == TT) {
         if (lane == 0) {
@@ -525,7 +526,7 @@ __global__ void __launch_bounds__((kRouteSmallWarps + 1) * 32, 1) k_route_decode
             }
         }
         __syncwarp();
-        cluster_wait_acquire();
+        if (plan) cluster_wait_acquire();
     } else {
         float* hr = s_hrow + warp * dpad;
         if (live && a.h_f16 && (d % 8) == 0 && (reinterpret_cast<uintptr_t>(a.h) & 15) == 0) {
@@ -609,6 +610,16 @@ __global__ void __launch_bounds__((kRouteSmallWarps + 1) * 32, 1) k_route_decode
             }
         }
         if (tr && threadIdx.x == 0) tr[10] = gtime_ns();
+        if (!plan) {  // the GEMV kernels build the plan themselves: expert / gate only
+            if (live && lane == 0) {
+                P.expert[t * k] = b1i;
+                P.gate[t * k] = g1;
+                if (k == 2) {
+                    P.expert[t * k + 1] = b2i;
+                    P.gate[t * k + 1] = g2;
+                }
+            }
+        } else {
         cluster_wait_acquire();  // rank 0 is running
         if (live && lane == 0) {
             st_cluster_u32(map_rank(&s_exp[t * k], 0), uint32_t(b1i));
@@ -618,6 +629,12 @@ __global__ void __launch_bounds__((kRouteSmallWarps + 1) * 32, 1) k_route_decode
                 st_cluster_u32(map_rank(&s_gate[t * k + 1], 0), __float_as_uint(g2));
             }
         }
+        }
+    }
+    if (!plan) {
+        // launched behind k_xrows (PDL): the grid completes only after it (see below)
+        if (blockIdx.x == 0 && threadIdx.x == 0) pdl_wait();
+        return;
     }
     cluster_arrive_release();
     cluster_wait_acquire();  // every token's choice is in rank 0's shared memory
@@ -635,9 +652,11 @@ __global__ void __launch_bounds__((kRouteSmallWarps + 1) * 32, 1) k_route_decode
         P.done[e] = 0;
     }
     __syncthreads();
+    if (tr && threadIdx.x == 0) tr[13] = gtime_ns();
     plan_lists(a, P, s_cnt, s_off);
     if (threadIdx.x == 0) P.tickets[0] = 0;
     __syncthreads();
+    if (tr && threadIdx.x == 0) tr[14] = gtime_ns();
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const int e = s_exp[i];
         const int c0 = (i / k) / TT * TT * k;  // first (token, slot) of this row's route group
@@ -655,6 +674,7 @@ __global__ void __launch_bounds__((kRouteSmallWarps + 1) * 32, 1) k_route_decode
             P.inv_pos[i] = pos;
         }
     }
+    if (tr && threadIdx.x == 0) tr[15] = gtime_ns();
     for (int idx = threadIdx.x; idx < nct * E; idx += blockDim.x) {  // route-group bases (k_scatter)
         const int c = idx / E, e = idx - c * E, lim = min(c * TT * k, n);
         int b = 0;

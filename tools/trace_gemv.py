@@ -63,7 +63,7 @@ if rv.any():
     r = (rt[rv].astype(np.int64) - t0) / 1e3
     print(f"router CTAs {rv.sum()} (us rel. to GEMV first stamp): start {r[:, 0].min():.2f}  row {r[:, 1].max():.2f}  "
           f"chunks " + " ".join(f"{r[:, 2 + c].max():.2f}" for c in range(8)) +
-          f"  chain {r[:, 10].max():.2f}  ticket {r[:, 11].max():.2f}  plan {r[:, 12].max():.2f}")
+          f"  chain {r[:, 10].max():.2f}  ticket {r[:, 11].max():.2f}  counts {r[:, 13].max():.2f}  lists {r[:, 14].max():.2f}  perm {r[:, 15].max():.2f}  plan {r[:, 12].max():.2f}")
 role = (w >> np.uint64(60)).astype(int)
 ev = ((w >> np.uint64(56)) & np.uint64(0xF)).astype(int)
 ph = ((w >> np.uint64(48)) & np.uint64(0xFF)).astype(int)
@@ -104,7 +104,7 @@ for phase in (1, 2):
 
 if os.environ.get("TRACE_CTA"):
     c = int(os.environ["TRACE_CTA"])
-    names = {(7, 0): "K pdl_wait done", (7, 1): "K tables+cluster ok", (2, 5): "U B tile", (6, 0): "M item start", (6, 1): "M item issued", (6, 2): "M unit A ok", (6, 3): "M unit issued", (2, 3): "C top", (2, 0): "C bfull ok", (5, 0): "C unit0 in", (5, 1): "C unit+ in", (2, 1): "C mloop end",
+    names = {(7, 0): "K pdl_wait done", (7, 1): "K tables+cluster ok", (7, 2): "P self plan done", (7, 3): "P first item issued", (7, 4): "P self plan again", (2, 5): "U B tile", (6, 0): "M item start", (6, 1): "M item issued", (6, 2): "M unit A ok", (6, 3): "M unit issued", (2, 3): "C top", (2, 0): "C bfull ok", (5, 0): "C unit0 in", (5, 1): "C unit+ in", (2, 1): "C mloop end",
              (2, 4): "C scr ok/U B done", (3, 0): "E start", (3, 2): "E end", (4, 0): "P unit0 iss", (4, 1): "P unit+ iss"}
     sel = valid[c]
     order = np.argsort(us[c][sel], kind="stable")
