@@ -81,6 +81,10 @@ struct moqe_bank {
 };
 
 namespace {
+int route_dbg() {  // diagnostics only
+    static const int v = [] { const char* s = getenv("MOQE_ROUTE_DBG"); return s ? atoi(s) : 0; }();
+    return v;
+}
 int gemv_dbg() {  // diagnostics only
     static const int v = [] { const char* s = getenv("MOQE_GEMV_DBG"); return s ? atoi(s) : 0; }();
     return v;
@@ -376,6 +380,7 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
         // GEMV kernels build the plan themselves (no serial plan step between them)
         self_plan = !pre && !need_gemm && R <= kSelfPlanRows && t <= 32 && b->E <= 256;
         ra.no_plan = self_plan ? 1 : 0;
+        ra.dbg = route_dbg();
         if (need_gemv) {  // token rows -> fc1 row blocks; the decode router overlaps it (PDL)
             XrowArgs xa{h, h_dtype == MOQE_F16, t, int(b->d), gemv_chunks(b->Kp1), w.xr};
             ce = launch_xrows(b->bits, xa, st);

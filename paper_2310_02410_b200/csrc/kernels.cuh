@@ -44,6 +44,7 @@ struct RouteArgs {
     unsigned long long* trace;  // router phase stamps [kTraceRouteCtas][16] or null (diagnostics)
     int pdl;                    // launched behind k_xrows: the decode router may start early (PDL)
     int no_plan;                // decode GEMV-only: write expert / gate only (the GEMV kernels plan themselves)
+    int dbg;                    // diagnostics (env MOQE_ROUTE_DBG; 1 = skip the logit chain, timing only)
 };
 constexpr int kTraceRouteCtas = 64;
 cudaError_t launch_route(const RouteArgs& a, const Plan& P, cudaStream_t st);

@@ -469,15 +469,20 @@ __device__ __forceinline__ void chain_run(float (&acc)[EPL], const float (&x)[BK
     for (int u = 0; u < BK; ++u)
 #pragma unroll
         for (int e = 0; e < EPL; ++e) {
-            // reference: `if (av == 0.0f) continue; orow[j] += av * brow[j];`
-            const float pr = __fmul_rn(x[u], w[u][e]);
-            if (x[u] != 0.0f) acc[e] = __fadd_rn(acc[e], pr);
+            // reference: `if (av == 0.0f) continue; orow[j] += av * brow[j];` — the skip is
+            // folded into the addend (+0 leaves a round-to-nearest sum that started at +0
+            // unchanged, and 0 * inf never forms), so the dependent FADD chain carries no
+            // predicate from the ALU pipe: bit-identical, shorter critical path
+            const float pr = x[u] != 0.0f ? __fmul_rn(x[u], w[u][e]) : 0.0f;
+            acc[e] = __fadd_rn(acc[e], pr);
         }
 }
 
-template <int EPL, int EFIX>
-__global__ void __launch_bounds__((kRouteSmallWarps + 1) * 32, 1) k_route_decode(RouteArgs a, Plan P) {
-    constexpr int TT = kRouteSmallWarps;
+// TT tokens (warps) per CTA: 4 with the in-cluster plan; 1 in no_plan mode, where
+// the CTAs are independent — one token warp per SM keeps the chain off the shared-
+// memory wavefront limit (~1.25 wavefronts per step per warp, ~1 per cycle per SM).
+template <int EPL, int EFIX, int TT>
+__global__ void __launch_bounds__((TT + 1) * 32, 1) k_route_decode(RouteArgs a, Plan P) {
     constexpr int BK = EPL <= 2 ? 16 : EPL <= 4 ? 8 : 4;  // rows per pipelined block
     extern __shared__ __align__(128) float s_dyn[];
     __shared__ int s_exp[kRouteDecMaxT * 2];
@@ -551,13 +556,14 @@ __global__ void __launch_bounds__((kRouteSmallWarps + 1) * 32, 1) k_route_decode
             for (int j = lane; j < d; j += 32) a.zero_out[t * d + j] = 0.f;
         __syncwarp();
         if (tr && threadIdx.x == 0) tr[1] = gtime_ns();
+        const long long clk0 = clock64();
         float acc[EPL];
 #pragma unroll
         for (int e = 0; e < EPL; ++e) acc[e] = 0.0f;
         for (int c = 0; c < nch; ++c) {
             const int s = c % kRouteSlots;
             mbar_wait(&full[s], (c / kRouteSlots) & 1);
-            if (live) {
+            if (live && a.dbg != 1) {
                 const float* wb = ring + s * chunk + lane;
                 const float* hc = hr + c * rows;
                 const int nr = min(rows, d - c * rows);
@@ -609,7 +615,7 @@ __global__ void __launch_bounds__((kRouteSmallWarps + 1) * 32, 1) k_route_decode
                 g2 = float(z / (1.0 + z));
             }
         }
-        if (tr && threadIdx.x == 0) tr[10] = gtime_ns();
+        if (tr && threadIdx.x == 0) { tr[10] = gtime_ns(); tr[13] = clock64() - clk0; }
         if (!plan) {  // the GEMV kernels build the plan themselves: expert / gate only
             if (live && lane == 0) {
                 P.expert[t * k] = b1i;
@@ -996,29 +1002,33 @@ __global__ void __launch_bounds__(256) k_scatter(const void* h, int h_f16, int64
 }
 
 namespace {
-template <int EPL, int EFIX>
-cudaError_t launch_dec(const RouteArgs& a, const Plan& P, size_t smem, cudaStream_t st) {
+template <int EPL, int EFIX, int TT>
+cudaError_t launch_dec_tt(const RouteArgs& a, const Plan& P, size_t smem, cudaStream_t st) {
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(k_route_decode<EPL, EFIX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        cudaFuncSetAttribute(k_route_decode<EPL, EFIX, TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         configured = true;
     }
-    const unsigned nct = unsigned((a.T + kRouteSmallWarps - 1) / kRouteSmallWarps);
+    const unsigned nct = unsigned((a.T + TT - 1) / TT);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(nct);
-    cfg.blockDim = dim3((kRouteSmallWarps + 1) * 32);
+    cfg.blockDim = dim3((TT + 1) * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = nct;
+    at[0].val.clusterDim.x = TT == 1 ? 1 : nct;  // no_plan: independent CTAs
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = a.pdl ? 2 : 1;
-    return cudaLaunchKernelEx(&cfg, k_route_decode<EPL, EFIX>, a, P);
+    return cudaLaunchKernelEx(&cfg, k_route_decode<EPL, EFIX, TT>, a, P);
+}
+template <int EPL, int EFIX>
+cudaError_t launch_dec(const RouteArgs& a, const Plan& P, size_t smem, cudaStream_t st) {
+    return a.no_plan ? launch_dec_tt<EPL, EFIX, 1>(a, P, smem, st) : launch_dec_tt<EPL, EFIX, kRouteSmallWarps>(a, P, smem, st);
 }
 }  // namespace
 

@@ -60,6 +60,7 @@ valid = t > 0
 t0 = t[valid].min()
 rv = rt[:, 0] > 0
 if rv.any():
+    print("router chain cycles (clock64, per CTA thread 0): mean %.0f" % rt[rv][:, 13].astype(np.float64).mean())
     r = (rt[rv].astype(np.int64) - t0) / 1e3
     print(f"router CTAs {rv.sum()} (us rel. to GEMV first stamp): start {r[:, 0].min():.2f}  row {r[:, 1].max():.2f}  "
           f"chunks " + " ".join(f"{r[:, 2 + c].max():.2f}" for c in range(8)) +
