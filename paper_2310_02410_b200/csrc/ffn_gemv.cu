@@ -65,8 +65,10 @@ constexpr int kPassRows = 4;         // rows per item pass
 constexpr int kMaxNT = 2;            // n8 column tiles (4 rows x 4 planes = 16 columns)
 constexpr int kMaxListed = 256;
 constexpr int kConsumers = 8;        // MMA warps: 16 channels (one m16 block) each
-constexpr int kEpiWarps = 4;         // epilogue warps: one thread per channel
-constexpr int kProdWarp = kConsumers + kEpiWarps;
+constexpr int kEpiWarps = 4;         // warps per epilogue group: one thread per channel
+constexpr int kEpiGroups = 2;        // epilogue groups, alternating items (an item's epilogue may take
+                                     // longer than its mainloop without stalling the consumers)
+constexpr int kProdWarp = kConsumers + kEpiGroups * kEpiWarps;
 constexpr int kGemvThreads = (kProdWarp + 1) * 32;
 constexpr int kBufs = 3;             // row-block buffers (B operands of 3 items in flight)
 constexpr int kScrBufs = 2;          // accumulator scratch buffers (consumer -> epilogue)
@@ -475,7 +477,8 @@ struct Layout {
     static constexpr int BUFS = kBufs * kPassRows * XR;
     static constexpr int ZERO = rup(R::PB, 128);                               // all-zero plane (idle columns)
     static constexpr int SCR = kScrBufs * TILE_N * kScrStride * 4;
-    static constexpr int STG = PHASE == 1 ? rup(kPassRows * 4 * R::STG + kEpiWarps * kPassRows * 8, 128) : 0;
+    static constexpr int STG1 = PHASE == 1 ? rup(kPassRows * 4 * R::STG + kEpiWarps * kPassRows * 8, 128) : 0;
+    static constexpr int STG = kEpiGroups * STG1;  // per epilogue group
     static constexpr int TABLES = rup(int(sizeof(GemvTables)), 128);
     static constexpr int BARS = rup((2 * kMaxNU + 2 * kBufs + 2 * kScrBufs + 4) * 8, 128);
     static constexpr int O_ZERO = BUFS, O_SCR = O_ZERO + ZERO, O_STG = O_SCR + SCR, O_TAB = O_STG + STG;
@@ -755,11 +758,14 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
             if (lane == 0) mbar_arrive(&sfull[sb]);
         }
     } else {
-        // ===== epilogue: thread = channel of the item's 128-channel tile
-        const int ch = threadIdx.x - kConsumers * 32;
-        const int ew = warp - kConsumers;
+        // ===== epilogue: group grp takes items seq = grp, grp + 2, ...; thread = channel
+        const int grp = (warp - kConsumers) / kEpiWarps;
+        const int ew = (warp - kConsumers) % kEpiWarps;
+        const int ch = threadIdx.x - (kConsumers + grp * kEpiWarps) * 32;
+        const int ebar = 2 + grp;  // this group's named barrier
+        stg += grp * L::STG1;
         const uint32_t red_rank0 = map_rank(red, 0), full_rank0 = map_rank(red_full, 0);
-        Tracer T = tracer(ch == 0 ? tr : nullptr, 128, 192);
+        Tracer T = tracer(ch == 0 && grp == 0 ? tr : nullptr, 128, 192);
         // fc1: this channel's byte positions in a fc2 stage block (k = ch within the stage)
         int pos0 = 0, pos1 = -1;
         if (PHASE == 1) {
@@ -773,8 +779,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
                             if (first) { pos0 = o; first = false; } else pos1 = o;
                         }
         }
-        int seq = 0;
-        for (int i = clu; i < nitems; i += nclu, ++seq) {
+        for (int i = clu + grp * nclu, seq = grp; i < nitems; i += kEpiGroups * nclu, seq += kEpiGroups) {
             const GemvItem it = item_of(seq, i, TBL, n_gemv, nmt);
             const int b = seq % kBufs, sb = seq & 1;
             const int chg = it.mt * TILE_N + ch;
@@ -851,7 +856,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
                 for (int t = 0; t < kPassRows; ++t)
                     if (t < it.nrows)
                         for (int r = 1; r < CS; ++r) V[t] += redb[((r - 1) * TILE_N + ch) * kPassRows + t];
-                named_bar_sync(2, kEpiWarps * 32);  // every epilogue warp read this buffer
+                named_bar_sync(ebar, kEpiWarps * 32);  // every epilogue warp read this buffer
                 if (ch >= 1 && ch < CS) arrive_cluster(map_rank(&red_empty[rbuf], ch));
             }
             if (PHASE == 2) {
@@ -891,7 +896,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
                     for (int off = 16; off > 0; off >>= 1) X2 += __shfl_xor_sync(0xffffffffu, X2, off);
                     if (lane == 0) zred[ew * kPassRows + t] = X2;
                 }
-                named_bar_sync(2, kEpiWarps * 32);  // the stage blocks and warp sums are complete
+                named_bar_sync(ebar, kEpiWarps * 32);  // the stage blocks and warp sums are complete
                 const int st2 = it.mt % kChunkStages, c2 = it.mt / kChunkStages;
                 constexpr int V16 = R::STG / 16;
                 for (int idx = ch; idx < it.nrows * 4 * V16; idx += kEpiWarps * 32) {
@@ -912,7 +917,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
                     *reinterpret_cast<long long*>(hb + 64 + 8 * st2) = z;
                     *reinterpret_cast<int*>(hb) = p2t;  // the same value from every m-tile of the pass
                 }
-                named_bar_sync(2, kEpiWarps * 32);  // stage blocks / warp sums reused by the next item
+                named_bar_sync(ebar, kEpiWarps * 32);  // stage blocks / warp sums reused by the next item
             }
             T.ev(3, 2, it, PHASE);
         }
