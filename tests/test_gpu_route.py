@@ -50,3 +50,21 @@ def test_route_vs_oracle(gpu, orc, T, d, E, topk):
         ex, g = gpu.route(hh, _t(wg), topk)
         assert np.array_equal(ex.cpu().numpy(), ex_o), dt
         assert np.allclose(g.cpu().numpy(), g_o, rtol=1e-6, atol=0), dt
+
+
+def test_route_nonfinite_weights_under_zero_activations(gpu, orc):
+    # the reference skips zero activations (model.cpp:160-162), so an inf weight met only
+    # by zeros never reaches the sum: the decode router's unguarded fast chain must fall
+    # back to the exact skip when its Wg scan finds a non-finite value
+    rng = np.random.default_rng(11)
+    for T, d, E in ((4, 256, 32), (24, 1024, 32)):
+        h = fp16_valued(rng.standard_normal((T, d)))
+        h[:, 5] = 0.0
+        wg = (rng.standard_normal((d, E)) * 0.02).astype(np.float32)
+        wg[5, 3] = np.inf
+        wg[5, 7] = -np.inf
+        ex_o, g_o = orc.route(h, wg, 1)
+        import torch
+        ex, g = gpu.route(_t(h).half(), _t(wg), 1)
+        assert np.array_equal(ex.cpu().numpy(), ex_o)
+        assert np.allclose(g.cpu().numpy(), g_o, rtol=1e-6, atol=0)
