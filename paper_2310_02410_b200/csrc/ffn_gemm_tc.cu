@@ -51,6 +51,9 @@ constexpr int kTmemCols = 512;
 
 bool gemm_available() { return true; }
 int gemm_block_n() { return kBN; }
+// UMMA N of a 2-SM tile with `nvalid` tokens: a multiple of 32 (N/2 rows per CTA, whole
+// 8-row swizzle atoms), at most kBN
+__host__ __device__ constexpr int tile_n(int nvalid) { return nvalid >= kBN ? kBN : (nvalid + 31) / 32 * 32; }
 
 struct GemmParams {
     CUtensorMap tmap_b;  // activation matrix (x_perm for fc1, mid for fc2)
@@ -556,7 +559,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     mbar_arrive_expect_tx(&pfull[s], TB);
                     bulk_g2s(sP + s * TB, wt + int64_t(kb) * TB, TB, &pfull[s]);
                     if (rank == 0) mbar_arrive_expect_tx(&bfull[s], 2 * kBHalf);
-                    tma_load_2d_2sm(sB + s * kBHalf, &prm.tmap_b, kb * kBK, tl.row0 + rank * (kBN / 2),
+                    // the pair splits the tile's N = tile_n(nvalid) rows: CTA r holds rows [r N/2, (r+1) N/2)
+                    // (the fixed kBN/2-row box is a superset; the MMA reads the first N/2 rows)
+                    tma_load_2d_2sm(sB + s * kBHalf, &prm.tmap_b, kb * kBK, tl.row0 + rank * (tile_n(tl.nvalid) / 2),
                                     leader_addr(&bfull[s]));
                     if (++s == kStages) { s = 0; ph ^= 1; }
                 }
@@ -565,9 +570,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     } else if (warp == 1) {
         // ===== MMA issuer (leader only) =====
         if (rank == 0 && lane == 0) {
-            constexpr uint32_t idesc = idesc_f16(2 * kBM, kBN);
             int s = 0, ph = 0, a = 0, aph2 = 0, as = 0, aph = 0;
             for (int t = cid; t < ntiles; t += ncl) {
+                // UMMA N sized to the tile's tokens (a 130-token expert no longer pays for 256)
+                const GemmTile tl = decode_tile(t, s_list, s_off, s_cnt, s_tstart, n_gemm, nmg, 2, rank);
+                const uint32_t idesc = idesc_f16(2 * kBM, tile_n(tl.nvalid));
                 mbar_wait(&acce[as], aph ^ 1);
                 tc_fence_after();
                 const uint32_t dt = tmem + uint32_t(as * kBN);
