@@ -635,8 +635,12 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
         const GemvItem it = item_at(i, TBL, n_gemv, nmt);
         TBL.items[k] = make_int4(it.e, it.mt, it.row0, it.nrows);
     }
-    __syncthreads();
-    cluster_sync();  // barriers of every CTA initialised before any remote arrive
+    if (CS > 1) {
+        __syncthreads();
+        cluster_sync();  // barriers of every CTA initialised before any remote arrive
+    } else {
+        __syncthreads();  // one-CTA "cluster": no remote arrives, a CTA barrier suffices
+    }
     if (PHASE == 1 && threadIdx.x == 0) pdl_trigger();  // the fc2 grid may launch as CTAs retire (one thread per CTA)
     const int nch2 = (g.Kp2 + kChunkK - 1) / kChunkK;
     // trace rows: fc1 events in the first half of each CTA row, fc2 in the second
@@ -922,7 +926,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
             T.ev(3, 2, it, PHASE);
         }
     }
-    cluster_sync();  // no CTA leaves while a peer may still write its shared memory
+    if (CS > 1) cluster_sync();  // no CTA leaves while a peer may still write its shared memory
     if (tr && threadIdx.x == 0) { tr[2 * (kSlots - 1)] = gtime_ns(); tr[2 * (kSlots - 1) + 1] = clock64(); }
 }
 
