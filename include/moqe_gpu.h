@@ -156,19 +156,24 @@ moqe_status moqe_gpu_expert_ffn(moqe_bank_t bank, const void* x, moqe_dtype x_dt
  * profile_read synchronises and returns milliseconds and launch counts per
  * kernel kind for the events recorded since the last clearing read; with
  * keep != 0 the recorded events are kept (read again after the next graph
- * replay). Kinds: 0 route(+plan), 1 scatter, 2 gemv (fused fc1+fc2),
- * 3 gemm fc1, 4 gemm fc2, 5 convert. */
+ * replay). Kinds: 0 route (+ plan, + the k_xrows token-row encoding when the
+ * GEMV runs), 1 scatter, 2 gemv (k_gemv fc1 + k_gemv fc2), 3 gemm fc1,
+ * 4 gemm fc2, 5 convert. */
 #define MOQE_PROFILE_KINDS 6
 moqe_status moqe_gpu_bank_profile(moqe_bank_t bank, int enable);
 moqe_status moqe_gpu_bank_profile_read(moqe_bank_t bank, double* ms, int64_t* launches, int keep);
 
-/* Device event trace of the decode GEMV (diagnostics; off by default).
- * trace(bank, 1) allocates a [num_sms][512][2] u64 buffer of (globaltimer ns,
- * event word) pairs, filled by later forwards (word: role<<60 | event<<56 |
- * phase<<48 | expert<<32 | m-tile<<16 | k-split; roles 0 producer, 1 converter,
- * 2 consumer, 3 kernel start). trace_read synchronises, copies up to `cap`
- * words (out may be NULL to query the size), clears the buffer and returns the
- * word count, or -1 when tracing is off. */
+/* Device event trace of the decode path (diagnostics; off by default).
+ * trace(bank, 1) allocates, per SM, 512 slots of two u64: slots 0..255 for the
+ * fc1 kernel, 256..511 for fc2. In each half, the first and last slot hold
+ * (globaltimer ns, clock64) anchors at kernel entry / exit; the others hold
+ * events (clock64, word) with word = role<<60 | event<<56 | phase<<48 |
+ * expert<<32 | m-tile<<20 | rows<<16 | 1 (roles 2 consumer, 3 epilogue,
+ * 4 producer, 5 weight unit landed, 7 prologue). After them, 64 x 16 u64
+ * router stamps (globaltimer ns; 0 start, 1 row loaded, 10 chain done, 13 chain
+ * clock64 cycles). tools/trace_gemv.py decodes both. trace_read synchronises,
+ * copies up to `cap` words (out may be NULL to query the size), clears the
+ * buffer and returns the word count, or -1 when tracing is off. */
 moqe_status moqe_gpu_bank_trace(moqe_bank_t bank, int enable);
 int64_t moqe_gpu_bank_trace_read(moqe_bank_t bank, uint64_t* out, int64_t cap);
 
