@@ -35,6 +35,13 @@ SEED = 20231004
 N_LAYERS = 8
 
 
+def gemv_extra(d, T, top_k):
+    """Kernels beside the timed "gemv" scope's first: k_xrows, plus the fc2 grid unless
+    fc1 and fc2 run as one fused grid (capi.cu: self plan, fc1 in one 1024-k chunk)."""
+    fused = (T * top_k <= 64 and T <= 32 and d <= 1024 and os.environ.get("MOQE_GEMV_FUSED", "1") != "0")
+    return 1 if fused else 2
+
+
 def packed_bytes(bits: int, n: int) -> int:
     return 3 * ((n + 7) // 8) if bits == 3 else (n * bits + 7) // 8
 
@@ -293,9 +300,11 @@ def run_point(m, torch, E, d, f, bits, T, top_k, steps, warmup, dev, hbm_peak, t
         "touched_experts": touched, "roofline": roof,
         "kernel_share": {KINDS[k]: round(float(prof_ms[k] / max(prof_ms.sum(), 1e-12)), 4)
                          for k in range(6) if prof_n[k]},
-        # kernels per forward: a "gemv" scope launches k_gemv fc1 + fc2 and is preceded by
-        # k_xrows (token-row encoding, timed inside the "route" scope)
-        "launches_per_step": int(round((prof_n.sum() + 2 * prof_n[2]) / max(1, -(-steps // len(layers)) * len(layers)))),
+        # kernels per forward: a "gemv" scope launches k_gemv (one fused fc1+fc2 grid for
+        # decode batches of <= 64 routed rows, else fc1 + fc2) and is preceded by k_xrows
+        # (token-row encoding, timed inside the "route" scope)
+        "launches_per_step": int(round((prof_n.sum() + gemv_extra(d, T, top_k) * prof_n[2]) /
+                                       max(1, -(-steps // len(layers)) * len(layers)))),
     }
     return res, layers
 

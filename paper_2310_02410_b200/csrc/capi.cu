@@ -48,6 +48,7 @@ struct Workspace {
     float* out_acc = nullptr;
     uint8_t* xr = nullptr;         // decode GEMV: fc1 row blocks (k_xrows)
     uint8_t* xb = nullptr;         // decode GEMV: fc2 row blocks (fc1 epilogue -> fc2)
+    unsigned* ready = nullptr;     // decode GEMV, fused grid: fc1 m-tiles done per pass
 };
 
 struct moqe_bank {
@@ -83,6 +84,10 @@ struct moqe_bank {
 namespace {
 int route_dbg() {  // diagnostics only
     static const int v = [] { const char* s = getenv("MOQE_ROUTE_DBG"); return s ? atoi(s) : 0; }();
+    return v;
+}
+bool gemv_fused() {  // MOQE_GEMV_FUSED=0: decode as two grids (fc1, fc2) even when one would do
+    static const bool v = [] { const char* s = getenv("MOQE_GEMV_FUSED"); return !(s && atoi(s) == 0); }();
     return v;
 }
 int gemv_dbg() {  // diagnostics only
@@ -145,6 +150,7 @@ moqe_status ensure_workspace(moqe_bank* b, int64_t T, int topk) {
     const int64_t xb_bytes = gemv_xb_bytes(b->bits) * gemv_chunks(b->Kp2) * capR;
     add(xr_bytes, 1);
     add(xb_bytes, 1);
+    add(4, kSelfPlanRows);
     MOQE_CUDA(cudaMalloc(&w.block, bytes));
     MOQE_CUDA(cudaMemset(w.block, 0, bytes));
     char* p = static_cast<char*>(w.block);
@@ -171,6 +177,7 @@ moqe_status ensure_workspace(moqe_bank* b, int64_t T, int topk) {
     P.logits = carve<float>(p, capT * E);
     w.xr = carve<uint8_t>(p, xr_bytes);
     w.xb = carve<uint8_t>(p, xb_bytes);
+    w.ready = carve<unsigned>(p, kSelfPlanRows);
     w.cap_rows = capR;
     w.cap_tokens = capT;
     return MOQE_OK;
@@ -382,7 +389,8 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
         ra.no_plan = self_plan ? 1 : 0;
         ra.dbg = route_dbg();
         if (need_gemv) {  // token rows -> fc1 row blocks; the decode router overlaps it (PDL)
-            XrowArgs xa{h, h_dtype == MOQE_F16, t, int(b->d), gemv_chunks(b->Kp1), w.xr};
+            XrowArgs xa{h, h_dtype == MOQE_F16, t, int(b->d), gemv_chunks(b->Kp1), w.xr,
+                        self_plan && gemv_fused() ? w.ready : nullptr};
             ce = launch_xrows(b->bits, xa, st);
             if (ce != cudaSuccess) return cuda_fail(ce, "k_xrows");
             ra.pdl = 1;
@@ -400,7 +408,8 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
     if (need_gemv) {
         GemvArgs g{h, h_dtype == MOQE_F16, t, int(b->d), int(b->f), top_k, b->E, b->w1, b->w2,
                    b->w1_stride, b->w2_stride, b->s1, b->s2, b->b1, b->b2, b->Kp1, b->Np1, b->Kp2, b->Np2,
-                   out, out_dtype == MOQE_F16, acc, w.xr, gemv_chunks(b->Kp1), w.xb, b->smax1, b->bmax1, b->trace, gemv_dbg(), self_plan ? 1 : 0};
+                   out, out_dtype == MOQE_F16, acc, w.xr, gemv_chunks(b->Kp1), w.xb, b->smax1, b->bmax1, b->trace, gemv_dbg(), self_plan ? 1 : 0,
+                   self_plan && gemv_fused() ? w.ready : nullptr};
         KernelTimer kt(b, 2, st);
         ce = launch_gemv(b->bits, g, P, st, b->num_sms);
         if (ce != cudaSuccess) return cuda_fail(ce, "k_ffn_gemv");

@@ -1,7 +1,11 @@
 // ffn_gemv.cu — decode path: expert FFN (fc1 -> ReLU -> fc2 -> gate combine)
-// as two persistent weight-streaming kernels (one per layer of the FFN),
-// chained with programmatic dependent launch (PDL), plus the token-row encoder
-// k_xrows that runs beside the router.
+// as persistent weight-streaming kernels, plus the token-row encoder k_xrows
+// that runs beside the router. Decode batches (<= 64 routed rows, d <= 1024)
+// run fc1 and fc2 in ONE grid: every CTA streams its fc1 items, then its
+// cluster's fc2 items; an fc2 item waits only for its own pass's readiness
+// counter (release by the fc1 epilogues), so fc2 weights stream while fc1
+// finishes. Larger batches chain an fc1 and an fc2 grid with programmatic
+// dependent launch (PDL).
 //
 // Reference: the per-expert loop of moe_ffn_forward proj/src/model.cpp:360-391
 // (dequantize :370-375, matmul :381/:384, add_bias/relu :382-385, scatter
@@ -132,11 +136,11 @@ struct GemvTables {
     float gate[kSelfPlanRows];  // gate of permuted row (fc2 epilogue)
 };
 
-__device__ __forceinline__ int find_listed(const int* st, int n, int v) {  // largest a with st[a] <= v
+__device__ __forceinline__ int find_listed(const int* st, int n, int v, int sc) {  // largest a with st[a] * sc <= v
     int lo = 0, hi = n - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (st[mid] <= v) lo = mid; else hi = mid - 1;
+        if (st[mid] * sc <= v) lo = mid; else hi = mid - 1;
     }
     return lo;
 }
@@ -247,12 +251,13 @@ __device__ void build_tables_self(GemvTables& T, const Plan& P, int nr, int E, i
     __syncwarp();
 }
 
-// Item i (expert-major: expert, pass, m-tile).
-__device__ __forceinline__ GemvItem item_at(int i, const GemvTables& T, int n_gemv, int nmt) {
+// Item i (expert-major: expert, pass, m-tile). T.start counts items (sc = 1) or, for the
+// fused kernel whose two phases differ in m-tiles, passes (sc = nmt).
+__device__ __forceinline__ GemvItem item_at(int i, const GemvTables& T, int n_gemv, int nmt, int sc) {
     GemvItem it{};
-    if (i >= T.start[n_gemv]) { it.e = -1; return it; }
-    const int a = find_listed(T.start, n_gemv, i);
-    const int r = i - T.start[a];
+    if (i >= T.start[n_gemv] * sc) { it.e = -1; return it; }
+    const int a = find_listed(T.start, n_gemv, i, sc);
+    const int r = i - T.start[a] * sc;
     const int pass = r / nmt;
     it.e = T.list[a];
     it.mt = r - pass * nmt;
@@ -261,15 +266,25 @@ __device__ __forceinline__ GemvItem item_at(int i, const GemvTables& T, int n_ge
     return it;
 }
 
-// k-th item of this CTA (global index i): the cached decode, else the table lookup
-__device__ __forceinline__ GemvItem item_of(int k, int i, const GemvTables& T, int n_gemv, int nmt) {
-    if (k < kItemCache) {
-        const int4 v = T.items[k];
+// One phase (fc1 or fc2) as this CTA sees it.
+struct PhaseGeo {
+    int CS, rank, clu, nclu;  // split-K cluster of this phase (fused fc1: one CTA)
+    int Kp, Np, k0, nst, nunits, nmt;
+    int n, nitems, sc;        // listed experts, items, unit of T.start (see item_at)
+    int cbase, ccap;          // this phase's slice of T.items
+    const uint8_t* wbase0;
+    int64_t wstride;
+};
+
+// k-th item of this CTA in phase Q (global index i): the cached decode, else the table lookup
+__device__ __forceinline__ GemvItem item_of(int k, int i, const GemvTables& T, const PhaseGeo& Q) {
+    if (k < Q.ccap) {
+        const int4 v = T.items[Q.cbase + k];
         GemvItem it;
         it.e = v.x; it.mt = v.y; it.row0 = v.z; it.nrows = v.w;
         return it;
     }
-    return item_at(i, T, n_gemv, nmt);
+    return item_at(i, T, Q.n, Q.nmt, Q.sc);
 }
 
 // ---- optional event trace (diagnostics; off unless the bank enables it) ----------------
@@ -338,6 +353,7 @@ __global__ void __launch_bounds__(128) k_xrows(XrowArgs a) {
     const int64_t w = int64_t(blockIdx.x) * 4 + warp;
     const int64_t t = w / a.nch1;
     const int c = int(w - t * a.nch1);
+    if (a.ready && blockIdx.x == 0 && threadIdx.x < kSelfPlanRows) a.ready[threadIdx.x] = 0u;
     if (t >= a.T) return;
     const bool vec = a.h_f16 && (a.d % 8) == 0 && (reinterpret_cast<uintptr_t>(a.h) & 15) == 0;
     const int st = lane >> 2, tq = lane & 3, k0 = c * kChunkK;
@@ -468,16 +484,16 @@ __device__ __forceinline__ int fc2_exp(float smax, float bmax, float l1) {
 // Fixed parts first, then the split-K partials (only for clusters of >= 2 CTAs,
 // sized by the cluster), then the weight ring takes everything that is left:
 // the in-flight bytes per SM are what bounds the stream at loaded HBM latency.
-template <int BITS, int PHASE>
+template <int BITS, int PHASE>  // PHASE 0: the fused kernel (both phases share the carve-up)
 struct Layout {
     using R = RB<BITS>;
+    static_assert(R::XR2 >= R::XR1, "fc2 row blocks are the larger");
     static constexpr int kMaxNU = 8;
-    static constexpr int XR = PHASE == 1 ? R::XR1 : R::XR2;
-    static constexpr int HDR = PHASE == 1 ? R::HDR1 : R::HDR2;
+    static constexpr int XR = PHASE == 1 ? R::XR1 : R::XR2;                    // row-block buffer stride
     static constexpr int BUFS = kBufs * kPassRows * XR;
     static constexpr int ZERO = rup(R::PB, 128);                               // all-zero plane (idle columns)
     static constexpr int SCR = kScrBufs * TILE_N * kScrStride * 4;
-    static constexpr int STG1 = PHASE == 1 ? rup(kPassRows * 4 * R::STG + kEpiWarps * kPassRows * 8, 128) : 0;
+    static constexpr int STG1 = PHASE != 2 ? rup(kPassRows * 4 * R::STG + kEpiWarps * kPassRows * 8, 128) : 0;
     static constexpr int STG = kEpiGroups * STG1;  // per epilogue group
     static constexpr int TABLES = rup(int(sizeof(GemvTables)), 128);
     static constexpr int BARS = rup((2 * kMaxNU + 2 * kBufs + 2 * kScrBufs + 4) * 8, 128);
@@ -492,148 +508,508 @@ struct Layout {
     static_assert(nu(kMaxCluster) >= 2, "weight ring needs two slots");
 };
 
-template <int BITS, int PHASE>
-__global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
+// ---- per-phase pieces ---------------------------------------------------------------------
+// Shared-memory carve-up of one CTA (both phases of the fused kernel share it).
+struct GemvSmem {
+    uint8_t* bufs;        // [kBufs][4 rows][XRB]: row blocks of 3 items in flight
+    const uint8_t* zero;  // zero plane (idle B columns)
+    int* scr;             // [2][128][kScrStride]: exact group sums, consumers -> epilogue
+    uint8_t* stg;         // fc1: per epilogue group [4 rows][4 planes][STG] + zred
+    GemvTables* TBL;
+    long long* red;       // [2][CS-1][128][4]: split-K partials (rank 0)
+    uint8_t* ring;        // [NU][UB]: weight copy units
+    uint64_t *full, *empty, *bfull, *bempty, *sfull, *sempty, *red_full, *red_empty;
+    int NU, XRB;
+};
+
+template <int BITS, int PH>
+__device__ __forceinline__ PhaseGeo phase_geo(const GemvArgs& g, int CS, int rank, int clu, int nclu) {
+    PhaseGeo G;
+    G.CS = CS;
+    G.rank = rank;
+    G.clu = clu;
+    G.nclu = nclu;
+    G.Kp = PH == 1 ? g.Kp1 : g.Kp2;
+    G.Np = PH == 1 ? g.Np1 : g.Np2;
+    G.k0 = rank * kChunkK;
+    G.nst = (min(kChunkK, G.Kp - G.k0) + kStageK - 1) / kStageK;
+    G.nunits = (G.nst + Cfg<BITS>::US - 1) / Cfg<BITS>::US;
+    G.nmt = G.Np / TILE_N;
+    G.n = G.nitems = G.cbase = G.ccap = 0;
+    G.sc = 1;
+    G.wbase0 = PH == 1 ? g.w1 : g.w2;
+    G.wstride = PH == 1 ? g.w1_stride : g.w2_stride;
+    return G;
+}
+
+// ===== producer (one thread): each item's row blocks, then its weight copy units
+template <int BITS, int PH>
+__device__ __forceinline__ void produce(const GemvArgs& g, const Plan& P, const GemvSmem& S, const PhaseGeo& Q,
+                                        int& slot, int& sph, int& seq, int early_units, bool early_rows, bool fused,
+                                        bool& waited, Tracer& T) {
+    using C = Cfg<BITS>;
+    constexpr int XR = PH == 1 ? RB<BITS>::XR1 : RB<BITS>::XR2;
+    const GemvTables& TBL = *S.TBL;
+    const uint64_t pol = policy_evict_first();
+    const int nch2 = (g.Kp2 + kChunkK - 1) / kChunkK;
+    for (int k = 0, i = Q.clu; i < Q.nitems; i += Q.nclu, ++k, ++seq) {
+        const GemvItem it = item_of(k, i, TBL, Q);
+        const int b = seq % kBufs, bph = ((seq / kBufs) & 1) ^ 1;
+        auto issue_rows = [&]() {
+            if (PH == 2 && fused) {  // the pass's fc2 row blocks come from fc1 items of every CTA
+                const unsigned need = unsigned(g.Np1 / TILE_N);
+                while (ld_acquire_u32(g.ready + it.row0) < need) {
+                }
+                fence_proxy_async_global();  // generic writes (fc1 epilogues) -> this CTA's TMA reads
+            }
+            mbar_wait(&S.bempty[b], bph);
+            mbar_arrive_expect_tx(&S.bfull[b], uint32_t(it.nrows * XR));
+            for (int t = 0; t < it.nrows; ++t) {
+                const uint8_t* src =
+                    PH == 1 ? g.xr + (int64_t(it.row0 + t < kTokCache ? TBL.tok[it.row0 + t]
+                                                                      : __ldg(P.perm_token + it.row0 + t)) *
+                                          g.nch1 + Q.rank) * XR
+                            : g.xb + (int64_t(it.row0 + t) * nch2 + Q.rank) * XR;
+                bulk_g2s(S.bufs + (b * kPassRows + t) * S.XRB, src, uint32_t(XR), &S.bfull[b]);
+            }
+        };
+        // fc2 (first item of the fc2 kernel; every item of the fused one): the weights do not
+        // depend on fc1 and are queued first; the row blocks follow once the ring is full or
+        // the item is issued
+        const bool late = PH == 2 && (fused || k == 0);
+        if (!late && !(k == 0 && early_rows)) issue_rows();
+        const uint8_t* wb =
+            Q.wbase0 + int64_t(it.e) * Q.wstride + (int64_t(it.mt) * (Q.Kp / TILE_K) + Q.k0 / TILE_K) * C::TB;
+        bool rows_due = late;
+        for (int u = k == 0 ? early_units : 0; u <= Q.nunits; ++u) {
+            if (rows_due && (u == Q.nunits || u == S.NU)) {
+                if (!waited) pdl_wait();
+                waited = true;
+                rows_due = false;
+                issue_rows();
+            }
+            if (u == Q.nunits) break;
+            const int bytes = min(C::US, Q.nst - u * C::US) * C::SB;
+            mbar_wait(&S.empty[slot], sph ^ 1);
+            T.ev(4, u == 0 ? 0 : 1, it, PH);
+            mbar_arrive_expect_tx(&S.full[slot], uint32_t(bytes));
+            bulk_g2s_hint(S.ring + size_t(slot) * C::UB, wb + int64_t(u) * C::UB, uint32_t(bytes), &S.full[slot], pol);
+            if (++slot == S.NU) { slot = 0; sph ^= 1; }
+        }
+    }
+}
+
+// ===== consumers: warp -> m16 block (16 channels) of the 128-channel item
+template <int BITS, int PH>
+__device__ __forceinline__ void consume(const GemvArgs& g, const GemvSmem& S, const PhaseGeo& Q, int& slot, int& sph,
+                                        int& seq, int warp, int lane, Tracer& T) {
     using FR = Frag<BITS>;
     using C = Cfg<BITS>;
     using R = RB<BITS>;
-    using L = Layout<BITS, PHASE>;
-    constexpr int F = FR::F, G = FR::G, UB = C::UB, US = C::US, SB = C::SB, TB = C::TB;
-    constexpr int XR = L::XR, HDR = L::HDR, PL = planes_of(PHASE);
+    constexpr int G = FR::G, HDR = PH == 1 ? R::HDR1 : R::HDR2, PL = planes_of(PH);
+    const int gq = lane >> 2, tq = lane & 3;
+    const int r0 = 16 * warp + gq;
+    for (int k = 0, i = Q.clu; i < Q.nitems; i += Q.nclu, ++k, ++seq) {
+        const GemvItem it = item_of(k, i, *S.TBL, Q);
+        const int b = seq % kBufs, sb = seq & 1;
+        const int NT = nt_of(PH, it.nrows), ncol = PL * it.nrows;
+        // B column c = s * nrows + t (plane s of row t); idle columns read the zero plane
+        const uint8_t* bp[kMaxNT];
+        const int inv = it.nrows == 1 ? 65536 : it.nrows == 2 ? 32768 : it.nrows == 3 ? 21846 : 16384;
+#pragma unroll
+        for (int j = 0; j < kMaxNT; ++j) {
+            const int c = 8 * j + gq;
+            const int sq = (c * inv) >> 16;  // c / nrows (exact for c < 16)
+            const int t = c < ncol ? c - sq * it.nrows : 0, s = c < ncol ? sq : 0;
+            bp[j] = c < ncol ? S.bufs + (b * kPassRows + t) * S.XRB + HDR + s * R::PB + tq * 8 : S.zero + tq * 8;
+        }
+        T.ev(2, 3, it, PH);
+        mbar_wait(&S.bfull[b], (seq / kBufs) & 1);
+        T.ev(2, 0, it, PH);
+        int acc[G][kMaxNT][4];
+#pragma unroll
+        for (int a = 0; a < G; ++a)
+#pragma unroll
+            for (int j = 0; j < kMaxNT; ++j)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[a][j][q] = 0;
+        for (int u = 0; u < Q.nunits; ++u) {
+            mbar_wait(&S.full[slot], sph);
+            T.ev(5, u == 0 ? 0 : 1, it, PH);
+            const uint8_t* U = S.ring + size_t(slot) * C::UB;
+            const int ns = min(C::US, Q.nst - u * C::US);
+            if (g.dbg == 1) {
+            } else if (NT == 1) unit_mma<BITS, 1>(U, ns, u * C::US, r0, tq, bp, acc);
+            else unit_mma<BITS, 2>(U, ns, u * C::US, r0, tq, bp, acc);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.empty[slot]);
+            if (++slot == S.NU) { slot = 0; sph ^= 1; }
+        }
+        T.ev(2, 1, it, PH);
+        if (lane == 0) {
+            mbar_arrive(&S.bempty[b]);
+            mbar_wait(&S.sempty[sb], ((seq >> 1) & 1) ^ 1);
+        }
+        T.ev(2, 4, it, PH);
+        __syncwarp();
+        // groups -> D * Sum_k u * digit per (channel, column): exact in int32 for 1024-k chunks
+        int* sc = S.scr + sb * TILE_N * kScrStride;
+#pragma unroll
+        for (int j = 0; j < kMaxNT; ++j) {
+            if (j >= NT) break;
+#pragma unroll
+            for (int hq = 0; hq < 2; ++hq) {
+                int s0 = 0, s1 = 0;
+#pragma unroll
+                for (int a = 0; a < G; ++a) {
+                    s0 += FR::mult(a) * acc[a][j][2 * hq];
+                    s1 += FR::mult(a) * acc[a][j][2 * hq + 1];
+                }
+                *reinterpret_cast<int2*>(sc + (r0 + 8 * hq) * kScrStride + 8 * j + 2 * tq) = make_int2(s0, s1);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.sfull[sb]);
+    }
+}
+
+// ===== epilogue: group grp takes the items whose CTA sequence number is grp mod 2;
+// thread = channel. seq0 = sequence number of this phase's first item.
+template <int BITS, int PH>
+__device__ __forceinline__ void epilogue(const GemvArgs& g, const Plan& P, const GemvSmem& S, const PhaseGeo& Q,
+                                         int seq0, int grp, uint8_t* stg, bool fused, Tracer& T) {
+    using FR = Frag<BITS>;
+    using R = RB<BITS>;
+    constexpr int F = FR::F, PL = planes_of(PH);
     constexpr int LOGD = FR::D == 64 ? 6 : FR::D == 16 ? 4 : 0;
     constexpr long long Z = 1ll << (BITS - 1);
+    const GemvTables& TBL = *S.TBL;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ew = (warp - kConsumers) % kEpiWarps;
+    const int ch = threadIdx.x - (kConsumers + grp * kEpiWarps) * 32;
+    const int ebar = 2 + grp;  // this group's named barrier
+    const int CS = Q.CS, rank = Q.rank;
+    const int nch2 = (g.Kp2 + kChunkK - 1) / kChunkK;
+    const uint32_t red_rank0 = CS > 1 ? map_rank(S.red, 0) : 0u, full_rank0 = CS > 1 ? map_rank(S.red_full, 0) : 0u;
+    // fc1: this channel's byte positions in a fc2 stage block (k = ch within the stage)
+    int pos0 = 0, pos1 = -1;
+    if (PH == 1) {
+        const int q = (ch & 63) >> 4, kid = (ch >> 6) * 16 + (ch & 15);
+        bool first = true;
+        for (int f = 0; f < F; ++f)
+            for (int h = 0; h < 2; ++h)
+                for (int i = 0; i < 4; ++i)
+                    if (FR::kidx(f, h, i) == kid) {
+                        const int o = f * 32 + q * 8 + h * 4 + i;
+                        if (first) { pos0 = o; first = false; } else pos1 = o;
+                    }
+    }
+    const int k1 = ((grp - seq0) % kEpiGroups + kEpiGroups) % kEpiGroups;
+    for (int k = k1, seq = seq0 + k1, i = Q.clu + k1 * Q.nclu; i < Q.nitems;
+         k += kEpiGroups, seq += kEpiGroups, i += kEpiGroups * Q.nclu) {
+        const GemvItem it = item_of(k, i, TBL, Q);
+        const int b = seq % kBufs, sb = seq & 1;
+        const int chg = it.mt * TILE_N + ch;
+        float sc = 0.f, bias = 0.f, gate[kPassRows] = {0.f, 0.f, 0.f, 0.f};
+        int tok[kPassRows] = {0, 0, 0, 0};
+        float es = 0.f, eb = 0.f;
+        if (rank == 0) {  // epilogue operands, fetched before the wait
+            sc = __ldg((PH == 1 ? g.s1 : g.s2) + int64_t(it.e) * Q.Np + chg);
+            const float* bb = PH == 1 ? g.b1 : g.b2;
+            bias = bb ? __ldg(bb + int64_t(it.e) * Q.Np + chg) : 0.f;
+            if (PH == 1) { es = __ldg(g.smax1 + it.e); eb = __ldg(g.bmax1 + it.e); }
+            if (PH == 2)
+#pragma unroll
+                for (int t = 0; t < kPassRows; ++t)
+                    if (t < it.nrows) {
+                        if (g.self_plan) { gate[t] = TBL.gate[it.row0 + t]; tok[t] = TBL.tok[it.row0 + t]; }
+                        else { gate[t] = __ldg(P.perm_gate + it.row0 + t); tok[t] = __ldg(P.perm_token + it.row0 + t); }
+                    }
+        }
+        mbar_wait(&S.sfull[sb], (seq >> 1) & 1);
+        T.ev(3, 0, it, PH);
+        // exact partial of this chunk: V = Sum_s 256^s S_s - D Z Sum X (int64)
+        const uint8_t* rb = S.bufs + b * kPassRows * S.XRB;
+        const int* srow = S.scr + sb * TILE_N * kScrStride + ch * kScrStride;
+        long long V[kPassRows];
+        int pe[kPassRows];
+        float l1[kPassRows];
+#pragma unroll
+        for (int t = 0; t < kPassRows; ++t) {
+            V[t] = 0;
+            pe[t] = kZeroRow;
+            l1[t] = 0.f;
+            if (t >= it.nrows) continue;
+            const uint8_t* hb = rb + t * S.XRB;
+            long long zs = 0;
+            if (PH == 1) {
+                const XHead1 hd = *reinterpret_cast<const XHead1*>(hb);
+                pe[t] = hd.p;
+                l1[t] = hd.l1;
+                zs = hd.zsum;
+            } else {
+                pe[t] = *reinterpret_cast<const int*>(hb);
+                for (int s = 0; s < Q.nst; ++s) zs += *reinterpret_cast<const long long*>(hb + 64 + 8 * s);
+            }
+            long long v = -(long long)FR::D * Z * zs;
+#pragma unroll
+            for (int s = 0; s < PL; ++s) v += (long long)srow[s * it.nrows + t] << (8 * s);
+            V[t] = v;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive(&S.sempty[sb]);
+            mbar_arrive(&S.bempty[b]);
+        }
+        if (CS > 1) {  // split-K: every rank's partial into rank 0 (DSMEM), fixed-order sum there
+            // partials double-buffered by item parity: rank r may run one item ahead of rank 0
+            const int q = seq - seq0, rbuf = q & 1;
+            const long long* redb = S.red + rbuf * (CS - 1) * TILE_N * kPassRows;
+            if (rank != 0) {
+                if (lane == 0) wait_cluster(&S.red_empty[rbuf], ((q >> 1) & 1) ^ 1);  // rank 0 took item q - 2
+                __syncwarp();
+                const uint32_t dst = red_rank0 + uint32_t((rbuf * (CS - 1) + rank - 1) * TILE_N * kPassRows * 8);
+#pragma unroll
+                for (int t = 0; t < kPassRows; ++t)
+                    if (t < it.nrows) st_cluster_s64(dst + uint32_t((ch * kPassRows + t) * 8), V[t]);
+                __syncwarp();
+                if (lane == 0) arrive_cluster(full_rank0 + uint32_t(rbuf * 8));
+                T.ev(3, 2, it, PH);
+                continue;
+            }
+            if (lane == 0) wait_cluster(&S.red_full[rbuf], (q >> 1) & 1);
+            __syncwarp();
+#pragma unroll
+            for (int t = 0; t < kPassRows; ++t)
+                if (t < it.nrows)
+                    for (int r = 1; r < CS; ++r) V[t] += redb[((r - 1) * TILE_N + ch) * kPassRows + t];
+            named_bar_sync(ebar, kEpiWarps * 32);  // every epilogue warp read this buffer
+            if (ch >= 1 && ch < CS) arrive_cluster(map_rank(&S.red_empty[rbuf], ch));
+        }
+        if (PH == 2) {
+#pragma unroll
+            for (int t = 0; t < kPassRows; ++t) {
+                if (t >= it.nrows || chg >= g.d) continue;
+                const float y = pe[t] == kZeroRow ? 0.f : scale_pow2(V[t], pe[t] + LOGD);
+                const float yg = fmaf(y, sc, bias) * gate[t];
+                const int64_t o = int64_t(tok[t]) * g.d + chg;
+                if (g.out_acc) atomicAdd(g.out_acc + o, yg);  // top-2: two addends onto zero
+                else if (g.out_f16) static_cast<__half*>(g.out)[o] = __float2half_rn(yg);
+                else static_cast<float*>(g.out)[o] = yg;
+            }
+        } else {
+            // mid = ReLU(y s + b) in fc2 fixed point -> stage mt % 8 of the rows' fc2 blocks
+            long long* zred = reinterpret_cast<long long*>(stg + kPassRows * 4 * R::STG);  // [4 warps][4 rows]
+            int p2[kPassRows];
+#pragma unroll
+            for (int t = 0; t < kPassRows; ++t) {
+                p2[t] = kZeroRow;
+                long long X2 = 0;
+                if (t < it.nrows) {
+                    p2[t] = fc2_exp<BITS>(es, eb, l1[t]);
+                    const float y = pe[t] == kZeroRow ? 0.f : scale_pow2(V[t], pe[t] + LOGD);
+                    const float mid = fmaxf(fmaf(y, sc, bias), 0.0f);  // ReLU, model.cpp:190
+                    X2 = p2[t] == kZeroRow ? 0 : __float2int_rn(ldexpf(mid, p2[t]));
+                    const uint32_t dg = (uint32_t(int(X2)) + 0x80808080u) ^ 0x80808080u;  // 4 signed digits
+#pragma unroll
+                    for (int s = 0; s < 4; ++s) {
+                        uint8_t* pl = stg + (t * 4 + s) * R::STG;
+                        const uint8_t byte = uint8_t(dg >> (8 * s));
+                        pl[pos0] = byte;
+                        if (pos1 >= 0) pl[pos1] = byte;
+                    }
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) X2 += __shfl_xor_sync(0xffffffffu, X2, off);
+                if (lane == 0) zred[ew * kPassRows + t] = X2;
+            }
+            named_bar_sync(ebar, kEpiWarps * 32);  // the stage blocks and warp sums are complete
+            const int st2 = it.mt % kChunkStages, c2 = it.mt / kChunkStages;
+            constexpr int V16 = R::STG / 16;
+            for (int idx = ch; idx < it.nrows * 4 * V16; idx += kEpiWarps * 32) {
+                const int t = idx / (4 * V16), s = (idx / V16) & 3, u = idx % V16;
+                uint8_t* dst = g.xb + (int64_t(it.row0 + t) * nch2 + c2) * R::XR2 + R::HDR2 + s * R::PB +
+                               st2 * R::STG + 16 * u;
+                *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(stg + (t * 4 + s) * R::STG + 16 * u);
+            }
+            if (ch < it.nrows) {
+                const int t = ch;
+                int p2t = kZeroRow;
+#pragma unroll
+                for (int u = 0; u < kPassRows; ++u)
+                    if (u == t) p2t = p2[u];
+                uint8_t* hb = g.xb + (int64_t(it.row0 + t) * nch2 + c2) * R::XR2;
+                long long z = 0;
+                for (int w = 0; w < kEpiWarps; ++w) z += zred[w * kPassRows + t];
+                *reinterpret_cast<long long*>(hb + 64 + 8 * st2) = z;
+                *reinterpret_cast<int*>(hb) = p2t;  // the same value from every m-tile of the pass
+            }
+            named_bar_sync(ebar, kEpiWarps * 32);  // stage blocks / warp sums reused by the next item
+            if (fused && ch == 0) {
+                // publish: this m-tile's stage of the pass's fc2 row blocks is in global memory
+                // (the barrier orders the group's stores before this thread's release)
+                __threadfence();
+                fence_proxy_async_global();
+                atomicAdd(g.ready + it.row0, 1u);
+            }
+        }
+        T.ev(3, 2, it, PH);
+    }
+}
+
+// MODE 1: fc1, 2: fc2 (two grids chained by PDL), 3: fc1 then fc2 in one persistent grid
+// (decode with the self plan and a one-CTA fc1 chunk: no second launch, no second
+// prologue; a cluster starts fc2 as soon as its own fc1 items are done, each fc2 item
+// waiting only for its pass's readiness counter).
+template <int BITS, int MODE>
+__global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
+    constexpr bool FUSED = MODE == 3;
+    constexpr int PH0 = MODE == 2 ? 2 : 1;  // the first (or only) phase
+    using C = Cfg<BITS>;
+    using L = Layout<BITS, FUSED ? 0 : MODE>;
+    constexpr int XR0 = PH0 == 1 ? RB<BITS>::XR1 : RB<BITS>::XR2;
     extern __shared__ __align__(128) uint8_t smem[];
     const int CS = int(cluster_nctas()), rank = int(cta_rank());
-    const int NU = L::nu(CS);
-    uint8_t* bufs = smem;                                                      // [kBufs][4 rows][XR]
-    const uint8_t* zero = smem + L::O_ZERO;                                    // zero plane
-    int* scr = reinterpret_cast<int*>(smem + L::O_SCR);                        // [2][128][kScrStride]
-    uint8_t* stg = smem + L::O_STG;                                            // fc1: [4 rows][4 planes][STG] + zred
-    GemvTables& TBL = *reinterpret_cast<GemvTables*>(smem + L::O_TAB);
-    long long* red = reinterpret_cast<long long*>(smem + L::O_RED);            // [CS][128][4]
-    uint8_t* ring = smem + L::ring_off(CS);                                    // [NU][UB]
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::O_BARS);
-    uint64_t* empty = full + NU;
-    uint64_t* bfull = empty + NU;
-    uint64_t* bempty = bfull + kBufs;
-    uint64_t* sfull = bempty + kBufs;
-    uint64_t* sempty = sfull + kScrBufs;
-    uint64_t* red_full = sempty + kScrBufs;  // [2] rank 0: every other rank's partials of the item landed
-    uint64_t* red_empty = red_full + 2;      // [2] rank r: rank 0 consumed that buffer
+    GemvSmem S;
+    S.NU = L::nu(CS);
+    S.XRB = L::XR;
+    S.bufs = smem;
+    S.zero = smem + L::O_ZERO;
+    S.scr = reinterpret_cast<int*>(smem + L::O_SCR);
+    S.stg = smem + L::O_STG;
+    S.TBL = reinterpret_cast<GemvTables*>(smem + L::O_TAB);
+    S.red = reinterpret_cast<long long*>(smem + L::O_RED);
+    S.ring = smem + L::ring_off(CS);
+    S.full = reinterpret_cast<uint64_t*>(smem + L::O_BARS);
+    S.empty = S.full + S.NU;
+    S.bfull = S.empty + S.NU;
+    S.bempty = S.bfull + kBufs;
+    S.sfull = S.bempty + kBufs;
+    S.sempty = S.sfull + kScrBufs;
+    S.red_full = S.sempty + kScrBufs;  // [2] rank 0: every other rank's partials of the item landed
+    S.red_empty = S.red_full + 2;      // [2] rank r: rank 0 consumed that buffer
+    GemvTables& TBL = *S.TBL;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int kSlots = kTraceCap / 2;
-    unsigned long long* tr = g.trace ? g.trace + size_t(blockIdx.x) * kTraceCap * 2 + (PHASE == 2 ? kTraceCap : 0) : nullptr;
-    if (tr && threadIdx.x == 0) { tr[0] = gtime_ns(); tr[1] = clock64(); }  // anchor: kernel entry
-    const int Kp = PHASE == 1 ? g.Kp1 : g.Kp2;
-    const int Np = PHASE == 1 ? g.Np1 : g.Np2;
-    const int k0 = rank * kChunkK, nst = (min(kChunkK, Kp - k0) + kStageK - 1) / kStageK;
-    const int nunits = (nst + US - 1) / US;
-    const int nmt = Np / TILE_N;
-    const int clu = int(blockIdx.x) / CS, nclu = int(gridDim.x) / CS;
-    const uint8_t* wbase0 = PHASE == 1 ? g.w1 : g.w2;
-    const int64_t wstride = PHASE == 1 ? g.w1_stride : g.w2_stride;
+    // trace rows: fc1 events in the first half of each CTA row, fc2 in the second
+    unsigned long long* trow = g.trace ? g.trace + size_t(blockIdx.x) * kTraceCap * 2 : nullptr;
+    unsigned long long* tr = trow ? trow + (PH0 == 2 ? kTraceCap : 0) : nullptr;
+    unsigned long long* tr2 = FUSED && trow ? trow + kTraceCap : nullptr;
+    if (threadIdx.x == 0) {  // anchors: kernel entry
+        if (tr) { tr[0] = gtime_ns(); tr[1] = clock64(); }
+        if (tr2) { tr2[0] = gtime_ns(); tr2[1] = clock64(); }
+    }
+    // first phase: its split-K cluster (fused fc1: every CTA on its own); fused fc2: the cluster
+    PhaseGeo G1 = phase_geo<BITS, PH0>(g, FUSED ? 1 : CS, FUSED ? 0 : rank, FUSED ? int(blockIdx.x) : int(blockIdx.x) / CS,
+                                       FUSED ? int(gridDim.x) : int(gridDim.x) / CS);
+    PhaseGeo G2 = phase_geo<BITS, 2>(g, CS, rank, int(blockIdx.x) / CS, int(gridDim.x) / CS);
+    const int tsc = FUSED ? G1.nmt : 1;  // fused: TBL.start counts passes (the phases differ in m-tiles)
     int early_units = 0;     // producer: weight units of this CTA's first item issued before the table build
     bool early_rows = false; // producer: its fc1 row blocks too
     for (int i = threadIdx.x; i < L::ZERO / 16; i += blockDim.x)
-        reinterpret_cast<uint4*>(const_cast<uint8_t*>(zero))[i] = make_uint4(0u, 0u, 0u, 0u);
+        reinterpret_cast<uint4*>(const_cast<uint8_t*>(S.zero))[i] = make_uint4(0u, 0u, 0u, 0u);
     if (warp == kProdWarp) {
         // The producer owns the barriers' initialisation and starts its first item straight
         // from the plan's GEMV table (one load round + a warp scan), before the CTA-wide table
         // build and synchronisation: the weight stream starts ~2 us earlier.
         if (lane == 0) {
-            for (int s = 0; s < NU; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kConsumers); }
-            for (int b = 0; b < kBufs; ++b) { mbar_init(&bfull[b], 1); mbar_init(&bempty[b], kConsumers + kEpiWarps); }
-            for (int b = 0; b < kScrBufs; ++b) { mbar_init(&sfull[b], kConsumers); mbar_init(&sempty[b], kEpiWarps); }
+            for (int s = 0; s < S.NU; ++s) { mbar_init(&S.full[s], 1); mbar_init(&S.empty[s], kConsumers); }
+            for (int b = 0; b < kBufs; ++b) { mbar_init(&S.bfull[b], 1); mbar_init(&S.bempty[b], kConsumers + kEpiWarps); }
+            for (int b = 0; b < kScrBufs; ++b) { mbar_init(&S.sfull[b], kConsumers); mbar_init(&S.sempty[b], kEpiWarps); }
             for (int b = 0; b < 2; ++b) {
-                mbar_init(&red_full[b], kEpiWarps * max(CS - 1, 1));
-                mbar_init(&red_empty[b], 1);
+                mbar_init(&S.red_full[b], kEpiWarps * max(CS - 1, 1));
+                mbar_init(&S.red_empty[b], 1);
             }
             fence_barrier_init();
         }
         __syncwarp();
-        if (PHASE == 1) pdl_wait();  // routing plan and fc1 row blocks
+        if (PH0 == 1) pdl_wait();  // routing plan and fc1 row blocks
+        int e0 = -1, mt0 = 0, row00 = 0, nrows0 = 0;  // this CTA's first item, if any
         if (g.self_plan) {
-            build_tables_self(TBL, P, int(g.T * g.topk), g.E, g.topk, nmt, lane);
-            if (tr && lane == 0) { tr[6] = clock64(); tr[7] = 7ull << 60 | 2ull << 56 | (unsigned long long)PHASE << 48 | 1ull; }
+            build_tables_self(TBL, P, int(g.T * g.topk), g.E, g.topk, FUSED ? 1 : G1.nmt, lane);
+            if (tr && lane == 0) { tr[6] = clock64(); tr[7] = 7ull << 60 | 2ull << 56 | (unsigned long long)PH0 << 48 | 1ull; }
             if (g.dbg == 3) {  // diagnostics: the same build again (warm instruction cache, warm data)
-                build_tables_self(TBL, P, int(g.T * g.topk), g.E, g.topk, nmt, lane);
-                if (tr && lane == 0) { tr[10] = clock64(); tr[11] = 7ull << 60 | 4ull << 56 | (unsigned long long)PHASE << 48 | 1ull; }
+                build_tables_self(TBL, P, int(g.T * g.topk), g.E, g.topk, FUSED ? 1 : G1.nmt, lane);
+                if (tr && lane == 0) { tr[10] = clock64(); tr[11] = 7ull << 60 | 4ull << 56 | (unsigned long long)PH0 << 48 | 1ull; }
             }
             const int n = TBL.n;
-            if (clu < TBL.start[n]) {
-                const GemvItem it = item_at(clu, TBL, n, nmt);
-                const uint8_t* wb = wbase0 + int64_t(it.e) * wstride + (int64_t(it.mt) * (Kp / TILE_K) + k0 / TILE_K) * TB;
-                early_units = min(nunits, NU);
-                if (lane == 0) {
-                    const uint64_t pol = policy_evict_first();
-                    for (int u = 0; u < early_units; ++u) {
-                        const int bytes = min(US, nst - u * US) * SB;
-                        mbar_arrive_expect_tx(&full[u], uint32_t(bytes));
-                        bulk_g2s_hint(ring + size_t(u) * UB, wb + int64_t(u) * UB, uint32_t(bytes), &full[u], pol);
-                    }
-                    if (PHASE == 1) mbar_arrive_expect_tx(&bfull[0], uint32_t(it.nrows * XR));
-                }
-                if (PHASE == 1) {
-                    __syncwarp();
-                    if (lane < it.nrows)
-                        bulk_g2s(bufs + lane * XR, g.xr + (int64_t(TBL.tok[it.row0 + lane]) * g.nch1 + rank) * XR,
-                                 uint32_t(XR), &bfull[0]);
-                    early_rows = true;
-                }
-                if (tr && lane == 0) { tr[8] = clock64(); tr[9] = 7ull << 60 | 3ull << 56 | (unsigned long long)PHASE << 48 | 1ull; }
+            if (G1.clu < TBL.start[n] * tsc) {
+                const GemvItem it = item_at(G1.clu, TBL, n, G1.nmt, tsc);
+                e0 = it.e; mt0 = it.mt; row00 = it.row0; nrows0 = it.nrows;
             }
         } else {
-        const int n = P.gtab[0].x;
-        const int4 v = P.gtab[1 + lane];
-        if (n > 0 && n <= 32) {
-            const int np = lane < n ? nmt * ((v.y + kPassRows - 1) / kPassRows) : 0;
-            int incl = np;
+            const int n = P.gtab[0].x;
+            const int4 v = P.gtab[1 + lane];
+            if (n > 0 && n <= 32) {
+                const int np = lane < n ? G1.nmt * ((v.y + kPassRows - 1) / kPassRows) : 0;
+                int incl = np;
 #pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, incl, off);
-                if (lane >= off) incl += y;
-            }
-            const unsigned own = __ballot_sync(0xffffffffu, lane < n && incl - np <= clu && clu < incl);
-            if (own) {
-                const int src = __ffs(own) - 1;
-                const int e = __shfl_sync(0xffffffffu, v.x, src), cnt = __shfl_sync(0xffffffffu, v.y, src);
-                const int off0 = __shfl_sync(0xffffffffu, v.z, src), st0 = __shfl_sync(0xffffffffu, incl - np, src);
-                const int r = clu - st0, pass = r / nmt, mt = r - pass * nmt;
-                const int row0 = off0 + pass * kPassRows, nrows = min(kPassRows, cnt - pass * kPassRows);
-                const uint8_t* wb = wbase0 + int64_t(e) * wstride + (int64_t(mt) * (Kp / TILE_K) + k0 / TILE_K) * TB;
-                early_units = min(nunits, NU);
-                if (lane == 0) {
-                    const uint64_t pol = policy_evict_first();
-                    for (int u = 0; u < early_units; ++u) {
-                        const int bytes = min(US, nst - u * US) * SB;
-                        mbar_arrive_expect_tx(&full[u], uint32_t(bytes));
-                        bulk_g2s_hint(ring + size_t(u) * UB, wb + int64_t(u) * UB, uint32_t(bytes), &full[u], pol);
-                    }
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, off);
+                    if (lane >= off) incl += y;
                 }
-                if (PHASE == 1) {
-                    const int tok = lane < nrows ? P.perm_token[row0 + lane] : 0;
-                    if (lane == 0) mbar_arrive_expect_tx(&bfull[0], uint32_t(nrows * XR));
-                    __syncwarp();
-                    if (lane < nrows)
-                        bulk_g2s(bufs + lane * XR, g.xr + (int64_t(tok) * g.nch1 + rank) * XR, uint32_t(XR), &bfull[0]);
-                    early_rows = true;
+                const unsigned own = __ballot_sync(0xffffffffu, lane < n && incl - np <= G1.clu && G1.clu < incl);
+                if (own) {
+                    const int src = __ffs(own) - 1;
+                    const int cnt = __shfl_sync(0xffffffffu, v.y, src);
+                    const int off0 = __shfl_sync(0xffffffffu, v.z, src), st0 = __shfl_sync(0xffffffffu, incl - np, src);
+                    const int r = G1.clu - st0, pass = r / G1.nmt;
+                    e0 = __shfl_sync(0xffffffffu, v.x, src);
+                    mt0 = r - pass * G1.nmt;
+                    row00 = off0 + pass * kPassRows;
+                    nrows0 = min(kPassRows, cnt - pass * kPassRows);
                 }
             }
         }
+        if (e0 >= 0) {
+            const uint8_t* wb = G1.wbase0 + int64_t(e0) * G1.wstride +
+                                (int64_t(mt0) * (G1.Kp / TILE_K) + G1.k0 / TILE_K) * C::TB;
+            early_units = min(G1.nunits, S.NU);
+            if (lane == 0) {
+                const uint64_t pol = policy_evict_first();
+                for (int u = 0; u < early_units; ++u) {
+                    const int bytes = min(C::US, G1.nst - u * C::US) * C::SB;
+                    mbar_arrive_expect_tx(&S.full[u], uint32_t(bytes));
+                    bulk_g2s_hint(S.ring + size_t(u) * C::UB, wb + int64_t(u) * C::UB, uint32_t(bytes), &S.full[u], pol);
+                }
+            }
+            if (PH0 == 1) {
+                const int tok = lane < nrows0 ? (g.self_plan ? TBL.tok[row00 + lane] : P.perm_token[row00 + lane]) : 0;
+                if (lane == 0) mbar_arrive_expect_tx(&S.bfull[0], uint32_t(nrows0 * XR0));
+                __syncwarp();
+                if (lane < nrows0)
+                    bulk_g2s(S.bufs + lane * S.XRB, g.xr + (int64_t(tok) * g.nch1 + G1.rank) * XR0, uint32_t(XR0),
+                             &S.bfull[0]);
+                early_rows = true;
+            }
+            if (tr && lane == 0) { tr[8] = clock64(); tr[9] = 7ull << 60 | 3ull << 56 | (unsigned long long)PH0 << 48 | 1ull; }
         }
     }
-    if (PHASE == 1 && warp != kProdWarp) pdl_wait();  // every thread that reads the plan waits for it
-    if (tr && threadIdx.x == 0) { tr[2] = clock64(); tr[3] = 7ull << 60 | 0ull << 56 | (unsigned long long)PHASE << 48 | 1ull; }
-    if (warp == 0 && !g.self_plan) build_tables(TBL, P, nmt, lane, PHASE == 1 ? g.T * g.topk : 0);
+    if (PH0 == 1 && warp != kProdWarp) pdl_wait();  // every thread that reads the plan waits for it
+    if (tr && threadIdx.x == 0) { tr[2] = clock64(); tr[3] = 7ull << 60 | 0ull << 56 | (unsigned long long)PH0 << 48 | 1ull; }
+    if (warp == 0 && !g.self_plan) build_tables(TBL, P, G1.nmt, lane, PH0 == 1 ? g.T * g.topk : 0);
     __syncthreads();
     const int n_gemv = TBL.n;
-    const int nitems = n_gemv > 0 ? TBL.start[n_gemv] : 0;
-    for (int k = threadIdx.x; k < kItemCache; k += blockDim.x) {
-        const int i = clu + k * nclu;
-        if (i >= nitems) break;
-        const GemvItem it = item_at(i, TBL, n_gemv, nmt);
-        TBL.items[k] = make_int4(it.e, it.mt, it.row0, it.nrows);
+    G1.n = G2.n = n_gemv;
+    G1.sc = tsc;
+    G1.nitems = n_gemv > 0 ? TBL.start[n_gemv] * tsc : 0;
+    G1.ccap = FUSED ? kItemCache / 2 : kItemCache;
+    G2.sc = G2.nmt;
+    G2.nitems = n_gemv > 0 ? TBL.start[n_gemv] * G2.nmt : 0;
+    G2.cbase = kItemCache / 2;
+    G2.ccap = FUSED ? kItemCache / 2 : 0;
+    for (int k = threadIdx.x; k < G1.ccap; k += blockDim.x) {
+        const int i = G1.clu + k * G1.nclu;
+        if (i >= G1.nitems) break;
+        const GemvItem it = item_at(i, TBL, n_gemv, G1.nmt, G1.sc);
+        TBL.items[G1.cbase + k] = make_int4(it.e, it.mt, it.row0, it.nrows);
+    }
+    for (int k = threadIdx.x; k < G2.ccap; k += blockDim.x) {
+        const int i = G2.clu + k * G2.nclu;
+        if (i >= G2.nitems) break;
+        const GemvItem it = item_at(i, TBL, n_gemv, G2.nmt, G2.sc);
+        TBL.items[G2.cbase + k] = make_int4(it.e, it.mt, it.row0, it.nrows);
     }
     if (CS > 1) {
         __syncthreads();
@@ -641,293 +1017,47 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
     } else {
         __syncthreads();  // one-CTA "cluster": no remote arrives, a CTA barrier suffices
     }
-    if (PHASE == 1 && threadIdx.x == 0) pdl_trigger();  // the fc2 grid may launch as CTAs retire (one thread per CTA)
-    const int nch2 = (g.Kp2 + kChunkK - 1) / kChunkK;
-    // trace rows: fc1 events in the first half of each CTA row, fc2 in the second
-        if (tr && threadIdx.x == 0) { tr[4] = clock64(); tr[5] = 7ull << 60 | 1ull << 56 | (unsigned long long)PHASE << 48 | 1ull; }
+    if (MODE == 1 && threadIdx.x == 0) pdl_trigger();  // the fc2 grid may launch as CTAs retire (one thread per CTA)
+    if (tr && threadIdx.x == 0) { tr[4] = clock64(); tr[5] = 7ull << 60 | 1ull << 56 | (unsigned long long)PH0 << 48 | 1ull; }
 
     if (warp == kProdWarp) {
-        // ===== producer: each item's row blocks, then its weight copy units
         if (lane == 0) {
-            Tracer T = tracer(tr, 192, kSlots - 1);
-            const uint64_t pol = policy_evict_first();
-            bool waited = PHASE == 1;
             int slot = early_units, sph = 0, seq = 0;
-            bool rows0 = false;  // fc2: the first item's row blocks are issued after its weights
-            if (slot == NU) { slot = 0; sph = 1; }
-            for (int i = clu; i < nitems; i += nclu, ++seq) {
-                const GemvItem it = item_of(seq, i, TBL, n_gemv, nmt);
-                const int b = seq % kBufs;
-                auto issue_rows = [&]() {
-                    mbar_wait(&bempty[b], ((seq / kBufs) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&bfull[b], uint32_t(it.nrows * XR));
-                    for (int t = 0; t < it.nrows; ++t) {
-                        const uint8_t* src =
-                            PHASE == 1 ? g.xr + (int64_t(it.row0 + t < kTokCache ? TBL.tok[it.row0 + t]
-                                                                                  : __ldg(P.perm_token + it.row0 + t)) *
-                                                     g.nch1 + rank) * XR
-                                       : g.xb + (int64_t(it.row0 + t) * nch2 + rank) * XR;
-                        bulk_g2s(bufs + (b * kPassRows + t) * XR, src, uint32_t(XR), &bfull[b]);
-                    }
-                };
-                if (!(PHASE == 2 && seq == 0) && !(seq == 0 && early_rows)) issue_rows();
-                const uint8_t* wb = wbase0 + int64_t(it.e) * wstride + (int64_t(it.mt) * (Kp / TILE_K) + k0 / TILE_K) * TB;
-                for (int u = seq == 0 ? early_units : 0; u <= nunits; ++u) {
-                    // fc2, first item: its weights stream while fc1 finishes; its row blocks
-                    // (written by fc1) are fetched once the ring is full or the item issued
-                    if (PHASE == 2 && seq == 0 && !rows0 && (u == nunits || u == NU)) {
-                        if (!waited) pdl_wait();
-                        waited = true;
-                        rows0 = true;
-                        issue_rows();
-                    }
-                    if (u == nunits) break;
-                    const int bytes = min(US, nst - u * US) * SB;
-                    mbar_wait(&empty[slot], sph ^ 1);
-                    T.ev(4, u == 0 ? 0 : 1, it, PHASE);
-                    mbar_arrive_expect_tx(&full[slot], uint32_t(bytes));
-                    bulk_g2s_hint(ring + size_t(slot) * UB, wb + int64_t(u) * UB, uint32_t(bytes), &full[slot], pol);
-                    if (++slot == NU) { slot = 0; sph ^= 1; }
-                }
+            if (slot == S.NU) { slot = 0; sph = 1; }
+            bool waited = PH0 == 1;
+            Tracer T1 = tracer(tr, 192, kSlots - 1);
+            produce<BITS, PH0>(g, P, S, G1, slot, sph, seq, early_units, early_rows, false, waited, T1);
+            if (FUSED) {
+                Tracer T2 = tracer(tr2, 192, kSlots - 1);
+                produce<BITS, 2>(g, P, S, G2, slot, sph, seq, 0, false, true, waited, T2);
             }
             if (!waited) pdl_wait();
         }
         __syncwarp();
     } else if (warp < kConsumers) {
-        // ===== consumers: warp -> m16 block (16 channels) of the 128-channel item
-        const int gq = lane >> 2, tq = lane & 3;
-        const int r0 = 16 * warp + gq;
-        Tracer T = tracer(threadIdx.x == 0 ? tr : nullptr, 6, 128);
         int slot = 0, sph = 0, seq = 0;
-        for (int i = clu; i < nitems; i += nclu, ++seq) {
-            const GemvItem it = item_of(seq, i, TBL, n_gemv, nmt);
-            const int b = seq % kBufs, sb = seq & 1;
-            const int NT = nt_of(PHASE, it.nrows), ncol = PL * it.nrows;
-            // B column c = s * nrows + t (plane s of row t); idle columns read the zero plane
-            const uint8_t* bp[kMaxNT];
-#pragma unroll
-            const int inv = it.nrows == 1 ? 65536 : it.nrows == 2 ? 32768 : it.nrows == 3 ? 21846 : 16384;
-            for (int j = 0; j < kMaxNT; ++j) {
-                const int c = 8 * j + gq;
-                const int sq = (c * inv) >> 16;  // c / nrows (exact for c < 16)
-                const int t = c < ncol ? c - sq * it.nrows : 0, s = c < ncol ? sq : 0;
-                bp[j] = c < ncol ? bufs + (b * kPassRows + t) * XR + HDR + s * R::PB + tq * 8 : zero + tq * 8;
-            }
-            T.ev(2, 3, it, PHASE);
-            mbar_wait(&bfull[b], (seq / kBufs) & 1);
-            T.ev(2, 0, it, PHASE);
-            int acc[G][kMaxNT][4];
-#pragma unroll
-            for (int a = 0; a < G; ++a)
-#pragma unroll
-                for (int j = 0; j < kMaxNT; ++j)
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) acc[a][j][q] = 0;
-            for (int u = 0; u < nunits; ++u) {
-                mbar_wait(&full[slot], sph);
-                T.ev(5, u == 0 ? 0 : 1, it, PHASE);
-                const uint8_t* U = ring + size_t(slot) * UB;
-                const int ns = min(US, nst - u * US);
-                if (g.dbg == 1) {
-                } else if (NT == 1) unit_mma<BITS, 1>(U, ns, u * US, r0, tq, bp, acc);
-                else unit_mma<BITS, 2>(U, ns, u * US, r0, tq, bp, acc);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[slot]);
-                if (++slot == NU) { slot = 0; sph ^= 1; }
-            }
-            T.ev(2, 1, it, PHASE);
-            if (lane == 0) {
-                mbar_arrive(&bempty[b]);
-                mbar_wait(&sempty[sb], ((seq >> 1) & 1) ^ 1);
-            }
-            T.ev(2, 4, it, PHASE);
-            __syncwarp();
-            // groups -> D * Sum_k u * digit per (channel, column): exact in int32 for 1024-k chunks
-            int* sc = scr + sb * TILE_N * kScrStride;
-#pragma unroll
-            for (int j = 0; j < kMaxNT; ++j) {
-                if (j >= NT) break;
-#pragma unroll
-                for (int hq = 0; hq < 2; ++hq) {
-                    int s0 = 0, s1 = 0;
-#pragma unroll
-                    for (int a = 0; a < G; ++a) {
-                        s0 += FR::mult(a) * acc[a][j][2 * hq];
-                        s1 += FR::mult(a) * acc[a][j][2 * hq + 1];
-                    }
-                    *reinterpret_cast<int2*>(sc + (r0 + 8 * hq) * kScrStride + 8 * j + 2 * tq) = make_int2(s0, s1);
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sfull[sb]);
+        Tracer T1 = tracer(threadIdx.x == 0 ? tr : nullptr, 6, 128);
+        consume<BITS, PH0>(g, S, G1, slot, sph, seq, warp, lane, T1);
+        if (FUSED) {
+            Tracer T2 = tracer(threadIdx.x == 0 ? tr2 : nullptr, 6, 128);
+            consume<BITS, 2>(g, S, G2, slot, sph, seq, warp, lane, T2);
         }
     } else {
-        // ===== epilogue: group grp takes items seq = grp, grp + 2, ...; thread = channel
         const int grp = (warp - kConsumers) / kEpiWarps;
-        const int ew = (warp - kConsumers) % kEpiWarps;
-        const int ch = threadIdx.x - (kConsumers + grp * kEpiWarps) * 32;
-        const int ebar = 2 + grp;  // this group's named barrier
-        stg += grp * L::STG1;
-        const uint32_t red_rank0 = map_rank(red, 0), full_rank0 = map_rank(red_full, 0);
-        Tracer T = tracer(ch == 0 && grp == 0 ? tr : nullptr, 128, 192);
-        // fc1: this channel's byte positions in a fc2 stage block (k = ch within the stage)
-        int pos0 = 0, pos1 = -1;
-        if (PHASE == 1) {
-            const int q = (ch & 63) >> 4, kid = (ch >> 6) * 16 + (ch & 15);
-            bool first = true;
-            for (int f = 0; f < F; ++f)
-                for (int h = 0; h < 2; ++h)
-                    for (int i = 0; i < 4; ++i)
-                        if (FR::kidx(f, h, i) == kid) {
-                            const int o = f * 32 + q * 8 + h * 4 + i;
-                            if (first) { pos0 = o; first = false; } else pos1 = o;
-                        }
-        }
-        for (int i = clu + grp * nclu, seq = grp; i < nitems; i += kEpiGroups * nclu, seq += kEpiGroups) {
-            const GemvItem it = item_of(seq, i, TBL, n_gemv, nmt);
-            const int b = seq % kBufs, sb = seq & 1;
-            const int chg = it.mt * TILE_N + ch;
-            float sc = 0.f, bias = 0.f, gate[kPassRows] = {0.f, 0.f, 0.f, 0.f};
-            int tok[kPassRows] = {0, 0, 0, 0};
-            float es = 0.f, eb = 0.f;
-            if (rank == 0) {  // epilogue operands, fetched before the wait
-                sc = __ldg((PHASE == 1 ? g.s1 : g.s2) + int64_t(it.e) * Np + chg);
-                const float* bb = PHASE == 1 ? g.b1 : g.b2;
-                bias = bb ? __ldg(bb + int64_t(it.e) * Np + chg) : 0.f;
-                if (PHASE == 1) { es = __ldg(g.smax1 + it.e); eb = __ldg(g.bmax1 + it.e); }
-                if (PHASE == 2)
-#pragma unroll
-                    for (int t = 0; t < kPassRows; ++t)
-                        if (t < it.nrows) {
-                            if (g.self_plan) { gate[t] = TBL.gate[it.row0 + t]; tok[t] = TBL.tok[it.row0 + t]; }
-                            else { gate[t] = __ldg(P.perm_gate + it.row0 + t); tok[t] = __ldg(P.perm_token + it.row0 + t); }
-                        }
-            }
-            mbar_wait(&sfull[sb], (seq >> 1) & 1);
-            T.ev(3, 0, it, PHASE);
-            // exact partial of this chunk: V = Sum_s 256^s S_s - D Z Sum X (int64)
-            const uint8_t* rb = bufs + b * kPassRows * XR;
-            const int* srow = scr + sb * TILE_N * kScrStride + ch * kScrStride;
-            long long V[kPassRows];
-            int pe[kPassRows];
-            float l1[kPassRows];
-#pragma unroll
-            for (int t = 0; t < kPassRows; ++t) {
-                V[t] = 0;
-                pe[t] = kZeroRow;
-                l1[t] = 0.f;
-                if (t >= it.nrows) continue;
-                const uint8_t* hb = rb + t * XR;
-                long long zs = 0;
-                if (PHASE == 1) {
-                    const XHead1 hd = *reinterpret_cast<const XHead1*>(hb);
-                    pe[t] = hd.p;
-                    l1[t] = hd.l1;
-                    zs = hd.zsum;
-                } else {
-                    pe[t] = *reinterpret_cast<const int*>(hb);
-                    for (int s = 0; s < nst; ++s) zs += *reinterpret_cast<const long long*>(hb + 64 + 8 * s);
-                }
-                long long v = -(long long)FR::D * Z * zs;
-#pragma unroll
-                for (int s = 0; s < PL; ++s) v += (long long)srow[s * it.nrows + t] << (8 * s);
-                V[t] = v;
-            }
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&sempty[sb]);
-                mbar_arrive(&bempty[b]);
-            }
-            if (CS > 1) {  // split-K: every rank's partial into rank 0 (DSMEM), fixed-order sum there
-                // partials double-buffered by item parity: rank r may run one item ahead of rank 0
-                const int rbuf = seq & 1;
-                const long long* redb = red + rbuf * (CS - 1) * TILE_N * kPassRows;
-                if (rank != 0) {
-                    if (lane == 0) wait_cluster(&red_empty[rbuf], ((seq >> 1) & 1) ^ 1);  // rank 0 took item seq - 2
-                    __syncwarp();
-                    const uint32_t dst = red_rank0 + uint32_t((rbuf * (CS - 1) + rank - 1) * TILE_N * kPassRows * 8);
-#pragma unroll
-                    for (int t = 0; t < kPassRows; ++t)
-                        if (t < it.nrows) st_cluster_s64(dst + uint32_t((ch * kPassRows + t) * 8), V[t]);
-                    __syncwarp();
-                    if (lane == 0) arrive_cluster(full_rank0 + uint32_t(rbuf * 8));
-                    T.ev(3, 2, it, PHASE);
-                    continue;
-                }
-                if (lane == 0) wait_cluster(&red_full[rbuf], (seq >> 1) & 1);
-                __syncwarp();
-#pragma unroll
-                for (int t = 0; t < kPassRows; ++t)
-                    if (t < it.nrows)
-                        for (int r = 1; r < CS; ++r) V[t] += redb[((r - 1) * TILE_N + ch) * kPassRows + t];
-                named_bar_sync(ebar, kEpiWarps * 32);  // every epilogue warp read this buffer
-                if (ch >= 1 && ch < CS) arrive_cluster(map_rank(&red_empty[rbuf], ch));
-            }
-            if (PHASE == 2) {
-#pragma unroll
-                for (int t = 0; t < kPassRows; ++t) {
-                    if (t >= it.nrows || chg >= g.d) continue;
-                    const float y = pe[t] == kZeroRow ? 0.f : scale_pow2(V[t], pe[t] + LOGD);
-                    const float yg = fmaf(y, sc, bias) * gate[t];
-                    const int64_t o = int64_t(tok[t]) * g.d + chg;
-                    if (g.out_acc) atomicAdd(g.out_acc + o, yg);  // top-2: two addends onto zero
-                    else if (g.out_f16) static_cast<__half*>(g.out)[o] = __float2half_rn(yg);
-                    else static_cast<float*>(g.out)[o] = yg;
-                }
-            } else {
-                // mid = ReLU(y s + b) in fc2 fixed point -> stage mt % 8 of the rows' fc2 blocks
-                long long* zred = reinterpret_cast<long long*>(stg + kPassRows * 4 * R::STG);  // [4 warps][4 rows]
-                int p2[kPassRows];
-#pragma unroll
-                for (int t = 0; t < kPassRows; ++t) {
-                    p2[t] = kZeroRow;
-                    long long X2 = 0;
-                    if (t < it.nrows) {
-                        p2[t] = fc2_exp<BITS>(es, eb, l1[t]);
-                        const float y = pe[t] == kZeroRow ? 0.f : scale_pow2(V[t], pe[t] + LOGD);
-                        const float mid = fmaxf(fmaf(y, sc, bias), 0.0f);  // ReLU, model.cpp:190
-                        X2 = p2[t] == kZeroRow ? 0 : __float2int_rn(ldexpf(mid, p2[t]));
-                        const uint32_t dg = (uint32_t(int(X2)) + 0x80808080u) ^ 0x80808080u;  // 4 signed digits
-#pragma unroll
-                        for (int s = 0; s < 4; ++s) {
-                            uint8_t* pl = stg + (t * 4 + s) * R::STG;
-                            const uint8_t byte = uint8_t(dg >> (8 * s));
-                            pl[pos0] = byte;
-                            if (pos1 >= 0) pl[pos1] = byte;
-                        }
-                    }
-#pragma unroll
-                    for (int off = 16; off > 0; off >>= 1) X2 += __shfl_xor_sync(0xffffffffu, X2, off);
-                    if (lane == 0) zred[ew * kPassRows + t] = X2;
-                }
-                named_bar_sync(ebar, kEpiWarps * 32);  // the stage blocks and warp sums are complete
-                const int st2 = it.mt % kChunkStages, c2 = it.mt / kChunkStages;
-                constexpr int V16 = R::STG / 16;
-                for (int idx = ch; idx < it.nrows * 4 * V16; idx += kEpiWarps * 32) {
-                    const int t = idx / (4 * V16), s = (idx / V16) & 3, u = idx % V16;
-                    uint8_t* dst = g.xb + (int64_t(it.row0 + t) * nch2 + c2) * R::XR2 + R::HDR2 + s * R::PB +
-                                   st2 * R::STG + 16 * u;
-                    *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(stg + (t * 4 + s) * R::STG + 16 * u);
-                }
-                if (ch < it.nrows) {
-                    const int t = ch;
-                    int p2t = kZeroRow;
-#pragma unroll
-                    for (int u = 0; u < kPassRows; ++u)
-                        if (u == t) p2t = p2[u];
-                    uint8_t* hb = g.xb + (int64_t(it.row0 + t) * nch2 + c2) * R::XR2;
-                    long long z = 0;
-                    for (int w = 0; w < kEpiWarps; ++w) z += zred[w * kPassRows + t];
-                    *reinterpret_cast<long long*>(hb + 64 + 8 * st2) = z;
-                    *reinterpret_cast<int*>(hb) = p2t;  // the same value from every m-tile of the pass
-                }
-                named_bar_sync(ebar, kEpiWarps * 32);  // stage blocks / warp sums reused by the next item
-            }
-            T.ev(3, 2, it, PHASE);
+        const bool lead = threadIdx.x == (kConsumers + grp * kEpiWarps) * 32 && grp == 0;
+        Tracer T1 = tracer(lead ? tr : nullptr, 128, 192);
+        epilogue<BITS, PH0>(g, P, S, G1, 0, grp, S.stg + grp * L::STG1, FUSED, T1);
+        if (FUSED) {
+            const int n1 = G1.clu < G1.nitems ? (G1.nitems - G1.clu + G1.nclu - 1) / G1.nclu : 0;
+            Tracer T2 = tracer(lead ? tr2 : nullptr, 128, 192);
+            epilogue<BITS, 2>(g, P, S, G2, n1, grp, nullptr, false, T2);
         }
     }
     if (CS > 1) cluster_sync();  // no CTA leaves while a peer may still write its shared memory
-    if (tr && threadIdx.x == 0) { tr[2 * (kSlots - 1)] = gtime_ns(); tr[2 * (kSlots - 1) + 1] = clock64(); }
+    if (threadIdx.x == 0) {
+        if (tr) { tr[2 * (kSlots - 1)] = gtime_ns(); tr[2 * (kSlots - 1) + 1] = clock64(); }
+        if (tr2) { tr2[2 * (kSlots - 1)] = gtime_ns(); tr2[2 * (kSlots - 1) + 1] = clock64(); }
+    }
 }
 
 // ---- launch -----------------------------------------------------------------------------
@@ -951,11 +1081,11 @@ int active_clusters(K kern, int cs, size_t smem, int threads, int num_sms) {
     return std::min(n, num_sms / cs);
 }
 
-template <int BITS, int PHASE>
+template <int BITS, int MODE>
 cudaError_t launch_phase(const GemvArgs& g, const Plan& P, cudaStream_t st, int num_sms) {
-    using L = Layout<BITS, PHASE>;
-    auto kern = k_gemv<BITS, PHASE>;
-    const int Kp = PHASE == 1 ? g.Kp1 : g.Kp2;
+    using L = Layout<BITS, MODE == 3 ? 0 : MODE>;
+    auto kern = k_gemv<BITS, MODE>;
+    const int Kp = MODE == 1 ? g.Kp1 : g.Kp2;
     const int cs = (Kp + kChunkK - 1) / kChunkK;
     const int smem = L::total(cs);
     static bool configured = false;
@@ -985,6 +1115,9 @@ cudaError_t launch_phase(const GemvArgs& g, const Plan& P, cudaStream_t st, int 
 
 template <int BITS>
 cudaError_t launch_gemv_t(const GemvArgs& g, const Plan& P, cudaStream_t st, int num_sms) {
+    // fused: every fc1 item must fit one CTA (its cluster is the fc2 one) and the per-pass
+    // readiness counters (indexed by the pass's first permuted row) cover the self plan
+    if (g.ready && g.self_plan && g.Kp1 <= kChunkK) return launch_phase<BITS, 3>(g, P, st, num_sms);
     cudaError_t e = launch_phase<BITS, 1>(g, P, st, num_sms);
     if (e != cudaSuccess) return e;
     return launch_phase<BITS, 2>(g, P, st, num_sms);

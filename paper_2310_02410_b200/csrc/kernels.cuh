@@ -85,6 +85,8 @@ struct GemvArgs {
     unsigned long long* trace;     // [grid][kTraceCap][2] (time ns, event) or null
     int dbg;                       // diagnostics (env MOQE_GEMV_DBG; 1 = consumers skip the MMA work)
     int self_plan;                 // plan built in each CTA from P.expert / P.gate (T*k <= kSelfPlanRows)
+    unsigned* ready;               // [kSelfPlanRows] fc1 m-tiles done per pass (by first row), zeroed by
+                                   // k_xrows; non-null selects the fused fc1+fc2 grid (self plan only)
 };
 constexpr int kSelfPlanRows = 64;
 constexpr int kTraceCap = 512;
@@ -98,6 +100,7 @@ struct XrowArgs {
     int d;
     int nch1;
     uint8_t* xr;
+    unsigned* ready;  // [kSelfPlanRows] zeroed here for the fused decode grid, or null
 };
 cudaError_t launch_xrows(int bits, const XrowArgs& a, cudaStream_t st);
 int64_t gemv_xr_bytes(int bits);  // one fc1 row block (per token and 1024-k chunk)
