@@ -184,12 +184,16 @@ __device__ void build_tables(GemvTables& T, const Plan& P, int nmt, int lane, in
 // router's plan (route.cu plan_lists / the decode router's leader), built by one
 // warp from P.expert / P.gate in one load round — the router then only writes the
 // choices and never serialises a plan step.
+// The loads go through L2 only (__ldcg): the GEMV grid also runs this as a dry pass while
+// the router still writes the choices, and must not keep stale lines in L1; ids are
+// clamped to [0, E) so a dry pass over stale data stays in bounds.
 __device__ void build_tables_self(GemvTables& T, const Plan& P, int nr, int E, int k, int nmt, int lane) {
     // rows i = lane and lane + 32; per-expert counts by smem atomics, stable ranks by
     // __match_any (no per-lane loops over the rows)
     const int i0 = lane, i1 = lane + 32;
-    const int e0 = i0 < nr ? P.expert[i0] : -1, e1 = i1 < nr ? P.expert[i1] : -1;
-    const float g0 = i0 < nr ? P.gate[i0] : 0.f, g1 = i1 < nr ? P.gate[i1] : 0.f;
+    const int e0 = i0 < nr ? int(min(unsigned(__ldcg(P.expert + i0)), unsigned(E - 1))) : -1;
+    const int e1 = i1 < nr ? int(min(unsigned(__ldcg(P.expert + i1)), unsigned(E - 1))) : -1;
+    const float g0 = i0 < nr ? __ldcg(P.gate + i0) : 0.f, g1 = i1 < nr ? __ldcg(P.gate + i1) : 0.f;
     int* h1 = T.rexp;  // scratch: [E] counts of rows 0..31 (E <= kSelfPlanRows handled below)
     int* cnt = T.eoff;  // [E] total counts; the scan below reads each and overwrites it with the offset
     for (int e = lane; e < E; e += 32) cnt[e] = 0;
@@ -540,6 +544,38 @@ __device__ __forceinline__ PhaseGeo phase_geo(const GemvArgs& g, int CS, int ran
     G.wbase0 = PH == 1 ? g.w1 : g.w2;
     G.wstride = PH == 1 ? g.w1_stride : g.w2_stride;
     return G;
+}
+
+// Finalise both phases' item counts and cache slices from the built tables (every thread).
+__device__ __forceinline__ void finish_geo(const GemvTables& T, PhaseGeo& G1, PhaseGeo& G2, int tsc, bool fused) {
+    const int n = T.n;
+    G1.n = G2.n = n;
+    G1.sc = tsc;
+    G1.nitems = n > 0 ? T.start[n] * tsc : 0;
+    G1.cbase = 0;
+    G1.ccap = fused ? kItemCache / 2 : kItemCache;  // fused: half per phase
+    G2.sc = G2.nmt;
+    G2.nitems = n > 0 ? T.start[n] * G2.nmt : 0;
+    G2.cbase = kItemCache / 2;
+    G2.ccap = fused ? kItemCache / 2 : 0;
+}
+// Decode this CTA's first items of both phases into T.items (threads tid < nthr of one warp
+// group, after the tables are built; read after the CTA barrier).
+__device__ __forceinline__ void fill_items(GemvTables& T, PhaseGeo G1, PhaseGeo G2, int tsc, bool fused, int tid,
+                                           int nthr) {
+    finish_geo(T, G1, G2, tsc, fused);
+    for (int k = tid; k < G1.ccap; k += nthr) {
+        const int i = G1.clu + k * G1.nclu;
+        if (i >= G1.nitems) break;
+        const GemvItem it = item_at(i, T, G1.n, G1.nmt, G1.sc);
+        T.items[G1.cbase + k] = make_int4(it.e, it.mt, it.row0, it.nrows);
+    }
+    for (int k = tid; k < G2.ccap; k += nthr) {
+        const int i = G2.clu + k * G2.nclu;
+        if (i >= G2.nitems) break;
+        const GemvItem it = item_at(i, T, G2.n, G2.nmt, G2.sc);
+        T.items[G2.cbase + k] = make_int4(it.e, it.mt, it.row0, it.nrows);
+    }
 }
 
 // ===== producer (one thread): each item's row blocks, then its weight copy units
@@ -905,14 +941,17 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
                                        FUSED ? int(gridDim.x) : int(gridDim.x) / CS);
     PhaseGeo G2 = phase_geo<BITS, 2>(g, CS, rank, int(blockIdx.x) / CS, int(gridDim.x) / CS);
     const int tsc = FUSED ? G1.nmt : 1;  // fused: TBL.start counts passes (the phases differ in m-tiles)
-    int early_units = 0;     // producer: weight units of this CTA's first item issued before the table build
+    int early_units = 0;     // producer: weight units of this CTA's first item issued before the CTA barrier
     bool early_rows = false; // producer: its fc1 row blocks too
     for (int i = threadIdx.x; i < L::ZERO / 16; i += blockDim.x)
         reinterpret_cast<uint4*>(const_cast<uint8_t*>(S.zero))[i] = make_uint4(0u, 0u, 0u, 0u);
     if (warp == kProdWarp) {
-        // The producer owns the barriers' initialisation and starts its first item straight
-        // from the plan's GEMV table (one load round + a warp scan), before the CTA-wide table
-        // build and synchronisation: the weight stream starts ~2 us earlier.
+        // The producer owns the barriers' initialisation, builds the item tables and starts
+        // its first item before the CTA-wide synchronisation. Self plan: the build, the
+        // first issue and the item cache run twice through the same code — a dry pass while
+        // the router still runs (this grid launched early, PDL), then the real one: the
+        // dry pass pulls the cold prologue code into the instruction cache (cold, the real
+        // pass took ~3x its warm time).
         if (lane == 0) {
             for (int s = 0; s < S.NU; ++s) { mbar_init(&S.full[s], 1); mbar_init(&S.empty[s], kConsumers); }
             for (int b = 0; b < kBufs; ++b) { mbar_init(&S.bfull[b], 1); mbar_init(&S.bempty[b], kConsumers + kEpiWarps); }
@@ -924,99 +963,86 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
             fence_barrier_init();
         }
         __syncwarp();
-        if (PH0 == 1) pdl_wait();  // routing plan and fc1 row blocks
-        int e0 = -1, mt0 = 0, row00 = 0, nrows0 = 0;  // this CTA's first item, if any
-        if (g.self_plan) {
-            build_tables_self(TBL, P, int(g.T * g.topk), g.E, g.topk, FUSED ? 1 : G1.nmt, lane);
-            if (tr && lane == 0) { tr[6] = clock64(); tr[7] = 7ull << 60 | 2ull << 56 | (unsigned long long)PH0 << 48 | 1ull; }
-            if (g.dbg == 3) {  // diagnostics: the same build again (warm instruction cache, warm data)
+#pragma unroll 1
+        for (int pass = g.self_plan ? 0 : 1; pass < 2; ++pass) {
+            const bool real = pass == 1;
+            if (real && PH0 == 1) pdl_wait();  // routing plan and fc1 row blocks
+            int e0 = -1, mt0 = 0, row00 = 0, nrows0 = 0;  // this CTA's first item, if any
+            if (g.self_plan) {
                 build_tables_self(TBL, P, int(g.T * g.topk), g.E, g.topk, FUSED ? 1 : G1.nmt, lane);
-                if (tr && lane == 0) { tr[10] = clock64(); tr[11] = 7ull << 60 | 4ull << 56 | (unsigned long long)PH0 << 48 | 1ull; }
-            }
-            const int n = TBL.n;
-            if (G1.clu < TBL.start[n] * tsc) {
-                const GemvItem it = item_at(G1.clu, TBL, n, G1.nmt, tsc);
-                e0 = it.e; mt0 = it.mt; row00 = it.row0; nrows0 = it.nrows;
-            }
-        } else {
-            const int n = P.gtab[0].x;
-            const int4 v = P.gtab[1 + lane];
-            if (n > 0 && n <= 32) {
-                const int np = lane < n ? G1.nmt * ((v.y + kPassRows - 1) / kPassRows) : 0;
-                int incl = np;
+                if (real && tr && lane == 0) { tr[6] = clock64(); tr[7] = 7ull << 60 | 2ull << 56 | (unsigned long long)PH0 << 48 | 1ull; }
+                const int n = TBL.n;
+                if (G1.clu < TBL.start[n] * tsc) {
+                    const GemvItem it = item_at(G1.clu, TBL, n, G1.nmt, tsc);
+                    e0 = it.e; mt0 = it.mt; row00 = it.row0; nrows0 = it.nrows;
+                }
+            } else {
+                const int n = P.gtab[0].x;
+                const int4 v = P.gtab[1 + lane];
+                if (n > 0 && n <= 32) {
+                    const int np = lane < n ? G1.nmt * ((v.y + kPassRows - 1) / kPassRows) : 0;
+                    int incl = np;
 #pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const int y = __shfl_up_sync(0xffffffffu, incl, off);
-                    if (lane >= off) incl += y;
-                }
-                const unsigned own = __ballot_sync(0xffffffffu, lane < n && incl - np <= G1.clu && G1.clu < incl);
-                if (own) {
-                    const int src = __ffs(own) - 1;
-                    const int cnt = __shfl_sync(0xffffffffu, v.y, src);
-                    const int off0 = __shfl_sync(0xffffffffu, v.z, src), st0 = __shfl_sync(0xffffffffu, incl - np, src);
-                    const int r = G1.clu - st0, pass = r / G1.nmt;
-                    e0 = __shfl_sync(0xffffffffu, v.x, src);
-                    mt0 = r - pass * G1.nmt;
-                    row00 = off0 + pass * kPassRows;
-                    nrows0 = min(kPassRows, cnt - pass * kPassRows);
-                }
-            }
-        }
-        if (e0 >= 0) {
-            const uint8_t* wb = G1.wbase0 + int64_t(e0) * G1.wstride +
-                                (int64_t(mt0) * (G1.Kp / TILE_K) + G1.k0 / TILE_K) * C::TB;
-            early_units = min(G1.nunits, S.NU);
-            if (lane == 0) {
-                const uint64_t pol = policy_evict_first();
-                for (int u = 0; u < early_units; ++u) {
-                    const int bytes = min(C::US, G1.nst - u * C::US) * C::SB;
-                    mbar_arrive_expect_tx(&S.full[u], uint32_t(bytes));
-                    bulk_g2s_hint(S.ring + size_t(u) * C::UB, wb + int64_t(u) * C::UB, uint32_t(bytes), &S.full[u], pol);
+                    for (int off = 1; off < 32; off <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, incl, off);
+                        if (lane >= off) incl += y;
+                    }
+                    const unsigned own = __ballot_sync(0xffffffffu, lane < n && incl - np <= G1.clu && G1.clu < incl);
+                    if (own) {
+                        const int src = __ffs(own) - 1;
+                        const int cnt = __shfl_sync(0xffffffffu, v.y, src);
+                        const int off0 = __shfl_sync(0xffffffffu, v.z, src), st0 = __shfl_sync(0xffffffffu, incl - np, src);
+                        const int r = G1.clu - st0, pass1 = r / G1.nmt;
+                        e0 = __shfl_sync(0xffffffffu, v.x, src);
+                        mt0 = r - pass1 * G1.nmt;
+                        row00 = off0 + pass1 * kPassRows;
+                        nrows0 = min(kPassRows, cnt - pass1 * kPassRows);
+                    }
                 }
             }
-            if (PH0 == 1) {
-                const int tok = lane < nrows0 ? (g.self_plan ? TBL.tok[row00 + lane] : P.perm_token[row00 + lane]) : 0;
-                if (lane == 0) mbar_arrive_expect_tx(&S.bfull[0], uint32_t(nrows0 * XR0));
+            if (e0 >= 0) {
+                const uint8_t* wb = G1.wbase0 + int64_t(e0) * G1.wstride +
+                                    (int64_t(mt0) * (G1.Kp / TILE_K) + G1.k0 / TILE_K) * C::TB;
+                early_units = min(G1.nunits, S.NU);
+                if (lane == 0 && real) {
+                    const uint64_t pol = policy_evict_first();
+                    for (int u = 0; u < early_units; ++u) {
+                        const int bytes = min(C::US, G1.nst - u * C::US) * C::SB;
+                        mbar_arrive_expect_tx(&S.full[u], uint32_t(bytes));
+                        bulk_g2s_hint(S.ring + size_t(u) * C::UB, wb + int64_t(u) * C::UB, uint32_t(bytes), &S.full[u], pol);
+                    }
+                }
+                if (PH0 == 1) {
+                    const int tok = lane < nrows0 ? (g.self_plan ? TBL.tok[row00 + lane] : P.perm_token[row00 + lane]) : 0;
+                    if (lane == 0 && real) mbar_arrive_expect_tx(&S.bfull[0], uint32_t(nrows0 * XR0));
+                    __syncwarp();
+                    if (lane < nrows0 && real)
+                        bulk_g2s(S.bufs + lane * S.XRB, g.xr + (int64_t(tok) * g.nch1 + G1.rank) * XR0, uint32_t(XR0),
+                                 &S.bfull[0]);
+                    early_rows = real;
+                }
+                if (real && tr && lane == 0) { tr[8] = clock64(); tr[9] = 7ull << 60 | 3ull << 56 | (unsigned long long)PH0 << 48 | 1ull; }
+            }
+            if (!real) early_units = 0;
+            if (g.self_plan) {
                 __syncwarp();
-                if (lane < nrows0)
-                    bulk_g2s(S.bufs + lane * S.XRB, g.xr + (int64_t(tok) * g.nch1 + G1.rank) * XR0, uint32_t(XR0),
-                             &S.bfull[0]);
-                early_rows = true;
+                fill_items(TBL, G1, G2, tsc, FUSED, lane, 32);
             }
-            if (tr && lane == 0) { tr[8] = clock64(); tr[9] = 7ull << 60 | 3ull << 56 | (unsigned long long)PH0 << 48 | 1ull; }
         }
     }
     if (PH0 == 1 && warp != kProdWarp) pdl_wait();  // every thread that reads the plan waits for it
     if (tr && threadIdx.x == 0) { tr[2] = clock64(); tr[3] = 7ull << 60 | 0ull << 56 | (unsigned long long)PH0 << 48 | 1ull; }
-    if (warp == 0 && !g.self_plan) build_tables(TBL, P, G1.nmt, lane, PH0 == 1 ? g.T * g.topk : 0);
+    if (warp == 0 && !g.self_plan) {
+        build_tables(TBL, P, G1.nmt, lane, PH0 == 1 ? g.T * g.topk : 0);
+        __syncwarp();
+        fill_items(TBL, G1, G2, tsc, FUSED, lane, 32);
+    }
     __syncthreads();
-    const int n_gemv = TBL.n;
-    G1.n = G2.n = n_gemv;
-    G1.sc = tsc;
-    G1.nitems = n_gemv > 0 ? TBL.start[n_gemv] * tsc : 0;
-    G1.ccap = FUSED ? kItemCache / 2 : kItemCache;
-    G2.sc = G2.nmt;
-    G2.nitems = n_gemv > 0 ? TBL.start[n_gemv] * G2.nmt : 0;
-    G2.cbase = kItemCache / 2;
-    G2.ccap = FUSED ? kItemCache / 2 : 0;
-    for (int k = threadIdx.x; k < G1.ccap; k += blockDim.x) {
-        const int i = G1.clu + k * G1.nclu;
-        if (i >= G1.nitems) break;
-        const GemvItem it = item_at(i, TBL, n_gemv, G1.nmt, G1.sc);
-        TBL.items[G1.cbase + k] = make_int4(it.e, it.mt, it.row0, it.nrows);
-    }
-    for (int k = threadIdx.x; k < G2.ccap; k += blockDim.x) {
-        const int i = G2.clu + k * G2.nclu;
-        if (i >= G2.nitems) break;
-        const GemvItem it = item_at(i, TBL, n_gemv, G2.nmt, G2.sc);
-        TBL.items[G2.cbase + k] = make_int4(it.e, it.mt, it.row0, it.nrows);
-    }
-    if (CS > 1) {
-        __syncthreads();
-        cluster_sync();  // barriers of every CTA initialised before any remote arrive
-    } else {
-        __syncthreads();  // one-CTA "cluster": no remote arrives, a CTA barrier suffices
-    }
+    finish_geo(TBL, G1, G2, tsc, FUSED);
+    // Split cluster barrier: this CTA's barriers are initialised (arrive here); a thread waits
+    // only before its first remote access (the split-K epilogue), so no role stalls on the
+    // slowest peer's prologue.
+    if (CS > 1) cluster_arrive_relaxed();
     if (MODE == 1 && threadIdx.x == 0) pdl_trigger();  // the fc2 grid may launch as CTAs retire (one thread per CTA)
     if (tr && threadIdx.x == 0) { tr[4] = clock64(); tr[5] = 7ull << 60 | 1ull << 56 | (unsigned long long)PH0 << 48 | 1ull; }
 
@@ -1034,6 +1060,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
             if (!waited) pdl_wait();
         }
         __syncwarp();
+        if (CS > 1) cluster_wait_acquire();
     } else if (warp < kConsumers) {
         int slot = 0, sph = 0, seq = 0;
         Tracer T1 = tracer(threadIdx.x == 0 ? tr : nullptr, 6, 128);
@@ -1042,11 +1069,14 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
             Tracer T2 = tracer(threadIdx.x == 0 ? tr2 : nullptr, 6, 128);
             consume<BITS, 2>(g, S, G2, slot, sph, seq, warp, lane, T2);
         }
+        if (CS > 1) cluster_wait_acquire();
     } else {
         const int grp = (warp - kConsumers) / kEpiWarps;
         const bool lead = threadIdx.x == (kConsumers + grp * kEpiWarps) * 32 && grp == 0;
         Tracer T1 = tracer(lead ? tr : nullptr, 128, 192);
+        if (!FUSED && CS > 1) cluster_wait_acquire();  // every peer's barriers initialised
         epilogue<BITS, PH0>(g, P, S, G1, 0, grp, S.stg + grp * L::STG1, FUSED, T1);
+        if (FUSED && CS > 1) cluster_wait_acquire();
         if (FUSED) {
             const int n1 = G1.clu < G1.nitems ? (G1.nitems - G1.clu + G1.nclu - 1) / G1.nclu : 0;
             Tracer T2 = tracer(lead ? tr2 : nullptr, 128, 192);

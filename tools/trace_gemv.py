@@ -47,13 +47,15 @@ if a.dump:
 S = tr.shape[1] // 2
 raw = tr.astype(np.int64)
 t = np.zeros(tr.shape[:2], dtype=np.int64)
+# globaltimer values are ~1.8e18 ns: convert relative to a base, or float64 rounds to 256 ns
+gbase = int(raw[:, 0, 0][raw[:, 0, 0] > 0].min()) - 1_000_000
 for hlf in range(2):
     blk = raw[:, hlf * S:(hlf + 1) * S]
     g0, c0_, g1, c1_ = blk[:, 0, 0], blk[:, 0, 1], blk[:, S - 1, 0], blk[:, S - 1, 1]
     ok = (g0 > 0) & (g1 > g0) & (c1_ > c0_)
     rate = np.where(ok, (g1 - g0) / np.maximum(c1_ - c0_, 1), 0.0)  # ns per clock
     ev_ok = (blk[:, 1:S - 1, 1] & 1) == 1
-    tt = g0[:, None] + (blk[:, 1:S - 1, 0] - c0_[:, None]) * rate[:, None]
+    tt = (g0 - gbase)[:, None] + (blk[:, 1:S - 1, 0] - c0_[:, None]) * rate[:, None]
     t[:, hlf * S + 1:(hlf + 1) * S - 1] = np.where(ev_ok & ok[:, None], tt, 0).astype(np.int64)
 w = tr[:, :, 1]
 valid = t > 0
@@ -61,7 +63,7 @@ t0 = t[valid].min()
 rv = rt[:, 0] > 0
 if rv.any():
     print("router chain cycles (clock64, per CTA thread 0): mean %.0f" % rt[rv][:, 13].astype(np.float64).mean())
-    r = (rt[rv].astype(np.int64) - t0) / 1e3
+    r = (rt[rv].astype(np.int64) - gbase - t0) / 1e3
     print(f"router CTAs {rv.sum()} (us rel. to GEMV first stamp): start {r[:, 0].min():.2f}  row {r[:, 1].max():.2f}  "
           f"chunks " + " ".join(f"{r[:, 2 + c].max():.2f}" for c in range(8)) +
           f"  chain {r[:, 10].max():.2f}  ticket {r[:, 11].max():.2f}  counts {r[:, 13].max():.2f}  lists {r[:, 14].max():.2f}  perm {r[:, 15].max():.2f}  plan {r[:, 12].max():.2f}")
@@ -70,6 +72,8 @@ ev = ((w >> np.uint64(56)) & np.uint64(0xF)).astype(int)
 ph = ((w >> np.uint64(48)) & np.uint64(0xFF)).astype(int)
 us = (t - t0) / 1e3
 print(f"CTAs {tr.shape[0]}, events {valid.sum()}, span {us[valid].max():.2f} us")
+ent = raw[:, 0, 0]
+print(f"kernel entry (globaltimer anchor) rel. first stamp: min {(ent[ent > 0].min() - gbase - t0) / 1e3:.2f} max {(ent[ent > 0].max() - gbase - t0) / 1e3:.2f} us")
 
 for phase in (1, 2):
     c0 = valid & (role == 2) & (ev == 0) & (ph == phase)
