@@ -63,6 +63,8 @@ struct moqe_bank {
     float* b1 = nullptr;
     float* b2 = nullptr;
     float* wg = nullptr;
+    float* wg_blk = nullptr;  // blocked transposed copy for the decode router (route_block_wg)
+    int wg_finite = 0;
     float* smax1 = nullptr;  // [E] fc2 fixed-point bound constants (decode GEMV)
     float* bmax1 = nullptr;
     int num_sms = 148;
@@ -192,6 +194,7 @@ void free_bank(moqe_bank* b) {
     cudaFree(b->b1);
     cudaFree(b->b2);
     cudaFree(b->wg);
+    cudaFree(b->wg_blk);
     cudaFree(b->smax1);
     cudaFree(b->bmax1);
     cudaFree(b->ws.block);
@@ -314,6 +317,9 @@ moqe_status moqe_gpu_bank_set_router(moqe_bank_t b, const float* wg, int on_devi
     if (!b->wg) MOQE_CUDA(cudaMalloc(&b->wg, sizeof(float) * b->d * b->E));
     MOQE_CUDA(cudaMemcpy(b->wg, wg, sizeof(float) * b->d * b->E,
                          on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+    if (!b->wg_blk) MOQE_CUDA(cudaMalloc(&b->wg_blk, sizeof(float) * route_wg_block_floats(int(b->d), b->E) + 16));
+    int* flag = reinterpret_cast<int*>(b->wg_blk + route_wg_block_floats(int(b->d), b->E));
+    MOQE_CUDA(route_block_wg(b->wg, int(b->d), b->E, b->wg_blk, flag, &b->wg_finite));
     return MOQE_OK;
 }
 
@@ -387,6 +393,7 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
         // GEMV kernels build the plan themselves (no serial plan step between them)
         self_plan = !pre && !need_gemm && R <= kSelfPlanRows && t <= 32 && b->E <= 256;
         ra.no_plan = self_plan ? 1 : 0;
+        if (wg == b->wg && b->wg_blk) { ra.wg_blk = b->wg_blk; ra.wg_finite = b->wg_finite; }
         ra.dbg = route_dbg();
         if (need_gemv) {  // token rows -> fc1 row blocks; the decode router overlaps it (PDL)
             XrowArgs xa{h, h_dtype == MOQE_F16, t, int(b->d), gemv_chunks(b->Kp1), w.xr,

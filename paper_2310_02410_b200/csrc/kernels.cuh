@@ -45,8 +45,13 @@ struct RouteArgs {
     int pdl;                    // launched behind k_xrows: the decode router may start early (PDL)
     int no_plan;                // decode GEMV-only: write expert / gate only (the GEMV kernels plan themselves)
     int dbg;                    // diagnostics (env MOQE_ROUTE_DBG; 1 = skip the logit chain, timing only)
+    const float* wg_blk;        // the bank's blocked copy of wg (route_block_wg) or null
+    int wg_finite;              // wg has no inf / NaN
 };
 constexpr int kTraceRouteCtas = 64;
+// Router weights -> blocked transposed copy for the decode chain; *finite = no inf / NaN.
+int64_t route_wg_block_floats(int d, int E);
+cudaError_t route_block_wg(const float* wg, int d, int E, float* out, int* d_flag, int* finite);
 cudaError_t launch_route(const RouteArgs& a, const Plan& P, cudaStream_t st);
 int route_tokens_per_cta(int64_t T);
 // rows already routed: plan with kRouteSelWarps rows per CTA (scatter must use that tile)

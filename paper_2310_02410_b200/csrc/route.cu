@@ -696,6 +696,246 @@ __global__ void __launch_bounds__((TT + 1) * 32, 1) k_route_decode(RouteArgs a, 
     if (threadIdx.x == 0) pdl_wait();
 }
 
+// ---- decode without a plan (the GEMV grid builds it): one chain warp, blocked Wg -------
+// The bank keeps a second copy of the router weights, transposed and blocked (built once by
+// route_block_wg): 16 KB chunks [chunk][expert][rows + 4] (a 16-byte pad per expert row, so
+// eight lanes' LDS.128 cover all 32 banks). One token per CTA. The chain warp (lane j <->
+// experts j, j + 32, ...) reads four consecutive k of its expert per LDS.128 and four
+// activations per broadcast LDS.128, and runs the reference's sequential fp32 chain (FMUL,
+// then FADD, ascending k; model.cpp matmul) — ~2.5 instructions per k instead of a strided
+// load per k. With an all-finite Wg (checked at bank creation) the zero-activation skip
+// needs no select: 0 * w is +-0, and adding +-0 leaves the sum unchanged (it starts at +0
+// and round-to-nearest never yields -0 from a nonzero sum); otherwise x != 0 selects. A TMA
+// warp on another SM sub-partition streams the chunks through a ring.
+constexpr int kRCSlots = 8;
+constexpr int kRCPad = 64;  // floats after the token row: the chain's look-ahead loads past a chunk stay in bounds
+__host__ __device__ constexpr int rc_ps(int rows) { return rows + 4; }
+size_t route_chain_smem(int d, int E) {
+    const int rows = route_chunk_rows(E);
+    return size_t(kRCSlots) * E * rc_ps(rows) * 4 + size_t(route_dpad(d, E) + kRCPad) * 4 + size_t(2 * kRCSlots) * 8;
+}
+
+template <int EPL, int EFIX, bool SEL>
+__global__ void __launch_bounds__(64, 1) k_route_chain(RouteArgs a, Plan P) {
+    extern __shared__ __align__(128) float s_dyn[];
+    pdl_trigger();  // the expert-FFN grid may launch and run its prologue now
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned long long* tr = (a.trace && blockIdx.x < kTraceRouteCtas && (a.dbg != 9 || blockIdx.x == 0))
+                                 ? a.trace + blockIdx.x * 16 : nullptr;
+    if (tr && threadIdx.x == 0) tr[0] = gtime_ns();
+    const int E = EFIX ? EFIX : a.E, d = a.d, k = a.topk;
+    const int rows = route_chunk_rows(E), PS = rc_ps(rows), cf = E * PS;  // floats per chunk
+    const int nch = (d + rows - 1) / rows, dpad = nch * rows;
+    float* ring = s_dyn;               // [kRCSlots][E][PS]
+    float* hr = ring + kRCSlots * cf;  // [dpad] the token row in fp32 (zero padded)
+    uint64_t* full = reinterpret_cast<uint64_t*>(hr + dpad + kRCPad);
+    uint64_t* empty = full + kRCSlots;
+    const int64_t t = blockIdx.x;
+    // dbg 9: per-chunk clock64 stamps of CTA 0 in the trace slots of CTAs 1.. (diagnostics)
+    unsigned long long* ds = a.dbg == 9 && a.trace && blockIdx.x == 0 ? a.trace + 16 : nullptr;
+    auto dstamp = [&](int c, int ev) { if (ds && c < 8) ds[c * 6 + ev] = clock64(); };
+    if (ds && threadIdx.x == 0) ds[60] = clock64();
+    auto issue = [&](int c) {  // chunk c -> slot c % kRCSlots
+        const int s = c % kRCSlots;
+        dstamp(c, 0);
+        mbar_arrive_expect_tx(&full[s], uint32_t(cf * 4));
+        bulk_g2s(ring + s * cf, a.wg_blk + int64_t(c) * cf, uint32_t(cf * 4), &full[s]);
+    };
+    if (warp == 1 && lane == 0) {  // barriers, then the first chunks while the row loads
+        for (int s = 0; s < kRCSlots; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        fence_barrier_init();
+        for (int c = 0; c < min(nch, kRCSlots); ++c) issue(c);
+    }
+    {  // token row -> fp32 (both warps)
+        const int tid = threadIdx.x, nthr = 64;
+        if (a.h_f16 && (d % 8) == 0 && (reinterpret_cast<uintptr_t>(a.h) & 15) == 0) {
+            const uint4* src = reinterpret_cast<const uint4*>(static_cast<const __half*>(a.h) + t * d);
+            for (int j = tid; j < d / 8; j += nthr) {
+                const uint4 v = __ldg(src + j);
+                const __half2* h2 = reinterpret_cast<const __half2*>(&v);
+                float4 lo, hi;
+                float2 f;
+                f = __half22float2(h2[0]); lo.x = f.x; lo.y = f.y;
+                f = __half22float2(h2[1]); lo.z = f.x; lo.w = f.y;
+                f = __half22float2(h2[2]); hi.x = f.x; hi.y = f.y;
+                f = __half22float2(h2[3]); hi.z = f.x; hi.w = f.y;
+                reinterpret_cast<float4*>(hr)[2 * j] = lo;
+                reinterpret_cast<float4*>(hr)[2 * j + 1] = hi;
+            }
+            for (int p = d + tid; p < dpad + kRCPad; p += nthr) hr[p] = 0.0f;
+        } else {
+            for (int p = tid; p < dpad + kRCPad; p += nthr) hr[p] = p < d ? load_act(a.h, a.h_f16, t * d + p) : 0.0f;
+        }
+        if (a.inline_scatter && a.zero_out)  // top-2: fp32 accumulation rows start at zero
+            for (int j = tid; j < d; j += nthr) a.zero_out[t * d + j] = 0.f;
+    }
+    __syncthreads();
+    if (tr && threadIdx.x == 0) tr[1] = gtime_ns();
+
+    if (warp == 1) {
+        if (lane == 0)
+            for (int c = kRCSlots; c < nch; ++c) {
+                while (!mbar_try_wait_sleep(&empty[c % kRCSlots], ((c / kRCSlots) - 1) & 1)) {
+                }
+                issue(c);
+            }
+        __syncwarp();
+    } else {
+        // ===== chain warp
+        const long long clk0 = clock64();
+        float acc[EPL];
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) acc[e] = 0.0f;
+        constexpr int V = EPL == 1 ? 4 : EPL <= 4 ? 2 : 1;  // 4-k groups per register block
+        int col[EPL];
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) col[e] = (EFIX || lane + 32 * e < E) ? lane + 32 * e : 0;
+        auto mul = [](float x, float w) { return SEL ? (x != 0.0f ? __fmul_rn(x, w) : 0.0f) : __fmul_rn(x, w); };
+        for (int c = 0; c < nch; ++c) {
+            const int s = c % kRCSlots;
+            mbar_wait(&full[s], (c / kRCSlots) & 1);
+            if (lane == 0) dstamp(c, 3);
+            const float* wc = ring + s * cf;
+            const float* hc = hr + c * rows;
+            const int ng = (min(rows, d - c * rows) + 3) / 4;
+            if (a.dbg != 1 && ng == rows / 4 && ng % (2 * V) == 0) {
+                // full chunk: ping-pong register blocks, the next block's loads in flight during
+                // this block's dependent FADDs; no clamps or guards (immediate-offset loads; the
+                // look-ahead past the chunk reads padding or the next slot, never used)
+                const float* wp[EPL];
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) wp[e] = wc + col[e] * PS;
+                float4 xa[V], xb[V], wa[V][EPL], wb[V][EPL];
+                auto ld = [&](float4 (&x)[V], float4 (&w)[V][EPL], int g0) {
+#pragma unroll
+                    for (int i = 0; i < V; ++i) {
+                        x[i] = *reinterpret_cast<const float4*>(hc + 4 * (g0 + i));
+#pragma unroll
+                        for (int e = 0; e < EPL; ++e) w[i][e] = *reinterpret_cast<const float4*>(wp[e] + 4 * (g0 + i));
+                    }
+                };
+                auto run = [&](const float4 (&x)[V], const float4 (&w)[V][EPL]) {
+#pragma unroll
+                    for (int i = 0; i < V; ++i)
+#pragma unroll
+                        for (int e = 0; e < EPL; ++e) {
+                            float v = __fadd_rn(acc[e], mul(x[i].x, w[i][e].x));
+                            v = __fadd_rn(v, mul(x[i].y, w[i][e].y));
+                            v = __fadd_rn(v, mul(x[i].z, w[i][e].z));
+                            acc[e] = __fadd_rn(v, mul(x[i].w, w[i][e].w));
+                        }
+                };
+                ld(xa, wa, 0);
+#pragma unroll 1
+                for (int g = 0; g < ng; g += 2 * V) {
+                    ld(xb, wb, g + V);
+                    run(xa, wa);
+                    ld(xa, wa, g + 2 * V);
+                    run(xb, wb);
+                }
+            } else if (a.dbg != 1) {
+                // partial chunk: the same with clamped addresses and guarded adds
+                float4 xa[V], xb[V], wa[V][EPL], wb[V][EPL];
+                auto ld = [&](float4 (&x)[V], float4 (&w)[V][EPL], int g0) {
+#pragma unroll
+                    for (int i = 0; i < V; ++i) {
+                        const int g = min(g0 + i, ng - 1);
+                        x[i] = *reinterpret_cast<const float4*>(hc + 4 * g);
+#pragma unroll
+                        for (int e = 0; e < EPL; ++e) w[i][e] = *reinterpret_cast<const float4*>(wc + col[e] * PS + 4 * g);
+                    }
+                };
+                auto run = [&](const float4 (&x)[V], const float4 (&w)[V][EPL], int g0) {
+#pragma unroll
+                    for (int i = 0; i < V; ++i)
+                        if (g0 + i < ng)
+#pragma unroll
+                            for (int e = 0; e < EPL; ++e) {
+                                float v = __fadd_rn(acc[e], mul(x[i].x, w[i][e].x));
+                                v = __fadd_rn(v, mul(x[i].y, w[i][e].y));
+                                v = __fadd_rn(v, mul(x[i].z, w[i][e].z));
+                                acc[e] = __fadd_rn(v, mul(x[i].w, w[i][e].w));
+                            }
+                };
+                ld(xa, wa, 0);
+                for (int g = 0; g < ng; g += 2 * V) {
+                    ld(xb, wb, g + V);
+                    run(xa, wa, g);
+                    ld(xa, wa, g + 2 * V);
+                    run(xb, wb, g + V);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) { dstamp(c, 4); mbar_arrive(&empty[s]); }
+            if (tr && threadIdx.x == 0 && c < 8) tr[2 + c] = gtime_ns();
+        }
+        // argmax / gate (reference tie rule, fp64 softmax)
+        float b1v = 0.f, b2v = 0.f, g1 = 0.f, g2 = 0.f;
+        int b1i = 0, b2i = 0;
+        warp_argmax<EPL>(acc, E, -1, b1v, b1i);
+        if (k == 1) {
+            const double mx = double(b1v);
+            double sm = 0.0;
+#pragma unroll
+            for (int e = 0; e < EPL; ++e)
+                if (lane + 32 * e < E) sm += exp(double(acc[e]) - mx);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, off);
+            const float eb = float(exp(double(b1v) - mx));
+            g1 = float(double(eb) / sm);
+        } else {
+            warp_argmax<EPL>(acc, E, b1i, b2v, b2i);
+            const double z = exp(double(b2v) - double(b1v));
+            g1 = float(1.0 / (1.0 + z));
+            g2 = float(z / (1.0 + z));
+        }
+        if (tr && threadIdx.x == 0) { tr[10] = gtime_ns(); tr[13] = clock64() - clk0; }
+        if (lane == 0) {  // the GEMV grid builds the plan from these
+            P.expert[t * k] = b1i;
+            P.gate[t * k] = g1;
+            if (k == 2) {
+                P.expert[t * k + 1] = b2i;
+                P.gate[t * k + 1] = g2;
+            }
+        }
+    }
+    // launched behind k_xrows (PDL): the grid completes only after it, so the expert-FFN
+    // grid's own dependency wait on this grid covers the row blocks too
+    if (blockIdx.x == 0 && threadIdx.x == 0) pdl_wait();
+}
+
+// Router weights [d][E] -> the blocked, transposed copy k_route_chain streams; flags any
+// non-finite weight (then the chain keeps the explicit zero-activation select).
+__global__ void k_wg_block(const float* __restrict__ wg, int d, int E, float* __restrict__ out, int* nonfinite) {
+    const int rows = route_chunk_rows(E), PS = rc_ps(rows);
+    const int nch = (d + rows - 1) / rows;
+    const int64_t n = int64_t(nch) * E * PS;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const int r = int(i % PS);
+        const int64_t ce = i / PS;
+        const int e = int(ce % E), c = int(ce / E);
+        const int kk = c * rows + r;
+        const float v = (r < rows && kk < d) ? wg[int64_t(kk) * E + e] : 0.0f;
+        if (!isfinite(v)) atomicOr(nonfinite, 1);
+        out[i] = v;
+    }
+}
+int64_t route_wg_block_floats(int d, int E) {
+    const int rows = route_chunk_rows(E);
+    return int64_t((d + rows - 1) / rows) * E * rc_ps(rows);
+}
+cudaError_t route_block_wg(const float* wg, int d, int E, float* out, int* d_flag, int* finite) {
+    cudaError_t e = cudaMemset(d_flag, 0, sizeof(int));
+    if (e != cudaSuccess) return e;
+    const int64_t n = route_wg_block_floats(d, E);
+    k_wg_block<<<unsigned(std::min<int64_t>((n + 255) / 256, 4096)), 256>>>(wg, d, E, out, d_flag);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    int h = 0;
+    if ((e = cudaMemcpy(&h, d_flag, sizeof(int), cudaMemcpyDeviceToHost)) != cudaSuccess) return e;
+    *finite = h == 0;
+    return cudaSuccess;
+}
+
 // ---- large T, E in {32, 64}, fp16 rows with d % 8 == 0 (the prefill shapes) ----------
 // CTA = 32 tokens x all E experts; 8 compute warps, warp w owns experts
 // [w*EPL, (w+1)*EPL) (EPL = E/8) for the 32 tokens of its lanes, so each lane runs
@@ -1026,9 +1266,34 @@ cudaError_t launch_dec_tt(const RouteArgs& a, const Plan& P, size_t smem, cudaSt
     cfg.numAttrs = a.pdl ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, k_route_decode<EPL, EFIX, TT>, a, P);
 }
+template <int EPL, int EFIX, bool SEL>
+cudaError_t launch_chain(const RouteArgs& a, const Plan& P, size_t smem, cudaStream_t st) {
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_route_chain<EPL, EFIX, SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        configured = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(a.T));
+    cfg.blockDim = dim3(64);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = a.pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k_route_chain<EPL, EFIX, SEL>, a, P);
+}
 template <int EPL, int EFIX>
 cudaError_t launch_dec(const RouteArgs& a, const Plan& P, size_t smem, cudaStream_t st) {
-    return a.no_plan ? launch_dec_tt<EPL, EFIX, 1>(a, P, smem, st) : launch_dec_tt<EPL, EFIX, kRouteSmallWarps>(a, P, smem, st);
+    if (a.no_plan) {
+        const size_t cs = route_chain_smem(a.d, EFIX ? EFIX : a.E);
+        if (a.wg_blk && cs <= 220 * 1024 && a.dbg != 7)  // dbg 7: the strided-Wg chain (comparison)
+            return a.wg_finite ? launch_chain<EPL, EFIX, false>(a, P, cs, st) : launch_chain<EPL, EFIX, true>(a, P, cs, st);
+        return launch_dec_tt<EPL, EFIX, 1>(a, P, smem, st);
+    }
+    return launch_dec_tt<EPL, EFIX, kRouteSmallWarps>(a, P, smem, st);
 }
 }  // namespace
 

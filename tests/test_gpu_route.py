@@ -68,3 +68,27 @@ def test_route_nonfinite_weights_under_zero_activations(gpu, orc):
         ex, g = gpu.route(_t(h).half(), _t(wg), 1)
         assert np.array_equal(ex.cpu().numpy(), ex_o)
         assert np.allclose(g.cpu().numpy(), g_o, rtol=1e-6, atol=0)
+
+
+@pytest.mark.parametrize("topk", [1, 2])
+def test_decode_forward_routing_finite_and_nonfinite_bank_router(gpu, orc, topk):
+    # decode forward (T*k <= 64): the bank's blocked router copy and the one-warp chain
+    # (ffn decode self plan). Finite Wg: the select-free chain; an inf weight met only by
+    # zero activations (model.cpp:160-162 skips them) must switch the bank to the exact skip.
+    import torch
+    rng = np.random.default_rng(5 + topk)
+    E, d, f, T = 32, 1024, 256, 24
+    w1 = torch.randn(E, d, f, device="cuda") * 0.02
+    w2 = torch.randn(E, f, d, device="cuda") * 0.02
+    for nonfinite in (False, True):
+        h = fp16_valued(rng.standard_normal((T, d)))
+        wg = (rng.standard_normal((d, E)) * 0.02).astype(np.float32)
+        if nonfinite:
+            h[:, 5] = 0.0
+            wg[5, 3] = np.inf
+            wg[5, 7] = -np.nan
+        bank = gpu.ExpertBank.from_float(w1, w2, 4, router=_t(wg))
+        _, ex, g = gpu.moe_ffn_forward(_t(h).half(), bank, top_k=topk, return_routing=True)
+        ex_o, g_o = orc.route(h, wg, topk)
+        assert np.array_equal(ex.cpu().numpy().reshape(ex_o.shape), ex_o)
+        assert np.allclose(g.cpu().numpy().reshape(g_o.shape), g_o, rtol=1e-6, atol=0)
