@@ -884,9 +884,8 @@ __device__ __forceinline__ void epilogue(const GemvArgs& g, const Plan& P, const
             if (fused && ch == 0) {
                 // publish: this m-tile's stage of the pass's fc2 row blocks is in global memory
                 // (the barrier orders the group's stores before this thread's release)
-                __threadfence();
                 fence_proxy_async_global();
-                atomicAdd(g.ready + it.row0, 1u);
+                red_release_add(g.ready + it.row0, 1u);
             }
         }
         T.ev(3, 2, it, PH);

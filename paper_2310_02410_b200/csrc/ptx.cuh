@@ -135,6 +135,10 @@ __device__ __forceinline__ unsigned long long gtime_ns() {
 __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// release-add at GPU scope (cumulative: covers writes this thread observed, e.g. through a barrier)
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 // order generic-proxy global writes/reads against async-proxy (TMA) accesses
 __device__ __forceinline__ void fence_proxy_async_global() {
     asm volatile("fence.proxy.async.global;" ::: "memory");
