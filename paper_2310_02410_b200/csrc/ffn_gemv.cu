@@ -349,7 +349,11 @@ __device__ __forceinline__ void load16(const XrowArgs& a, int64_t t, int k, bool
 
 template <int BITS>
 __global__ void __launch_bounds__(128) k_xrows(XrowArgs a) {
-    pdl_trigger();  // the decode router may launch now (it does not read row blocks)
+    // Launched with PDL behind the previous forward's expert-FFN grid, so this grid can be
+    // resident before that one drains: wait for the previous grid, then let the decode router
+    // launch (it reads the token rows, never the row blocks).
+    pdl_wait();
+    pdl_trigger();
     using FR = Frag<BITS>;
     using R = RB<BITS>;
     constexpr int F = FR::F;
@@ -904,6 +908,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_gemv(GemvArgs g, Plan P) {
     using L = Layout<BITS, FUSED ? 0 : MODE>;
     constexpr int XR0 = PH0 == 1 ? RB<BITS>::XR1 : RB<BITS>::XR2;
     extern __shared__ __align__(128) uint8_t smem[];
+    if (MODE != 1 && threadIdx.x == 0) pdl_trigger();  // the next forward's k_xrows may become resident
     const int CS = int(cluster_nctas()), rank = int(cta_rank());
     GemvSmem S;
     S.NU = L::nu(CS);
@@ -1187,15 +1192,22 @@ cudaError_t launch_gemv(int bits, const GemvArgs& g, const Plan& P, cudaStream_t
 
 cudaError_t launch_xrows(int bits, const XrowArgs& a, cudaStream_t st) {
     if (a.T <= 0) return cudaSuccess;
-    const unsigned grid = unsigned((a.T * a.nch1 + 3) / 4);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned((a.T * a.nch1 + 3) / 4));
+    cfg.blockDim = dim3(128);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
     switch (bits) {
-        case 2: k_xrows<2><<<grid, 128, 0, st>>>(a); break;
-        case 3: k_xrows<3><<<grid, 128, 0, st>>>(a); break;
-        case 4: k_xrows<4><<<grid, 128, 0, st>>>(a); break;
-        case 8: k_xrows<8><<<grid, 128, 0, st>>>(a); break;
+        case 2: return cudaLaunchKernelEx(&cfg, k_xrows<2>, a);
+        case 3: return cudaLaunchKernelEx(&cfg, k_xrows<3>, a);
+        case 4: return cudaLaunchKernelEx(&cfg, k_xrows<4>, a);
+        case 8: return cudaLaunchKernelEx(&cfg, k_xrows<8>, a);
         default: return cudaErrorInvalidValue;
     }
-    return cudaGetLastError();
 }
 
 // Per expert: max fc1 scale and max |fc1 bias| — the constants of the fc2
