@@ -706,17 +706,22 @@ __global__ void __launch_bounds__((TT + 1) * 32, 1) k_route_decode(RouteArgs a, 
 // load per k. With an all-finite Wg (checked at bank creation) the zero-activation skip
 // needs no select: 0 * w is +-0, and adding +-0 leaves the sum unchanged (it starts at +0
 // and round-to-nearest never yields -0 from a nonzero sum); otherwise x != 0 selects. A TMA
-// warp on another SM sub-partition streams the chunks through a ring.
+// warp streams the chunks through a ring. kRCTok tokens per CTA, one chain warp each (one per
+// SM sub-partition): the chains are latency-bound, so sharing the ring costs nothing, and the
+// router occupies T/4 SMs instead of T — fewer expert-FFN CTAs launch late behind it.
+constexpr int kRCTok = 2;
+static_assert(kRCTok <= 4, "row index math below covers up to 4 tokens");
 constexpr int kRCSlots = 8;
 constexpr int kRCPad = 64;  // floats after the token row: the chain's look-ahead loads past a chunk stay in bounds
 __host__ __device__ constexpr int rc_ps(int rows) { return rows + 4; }
 size_t route_chain_smem(int d, int E) {
     const int rows = route_chunk_rows(E);
-    return size_t(kRCSlots) * E * rc_ps(rows) * 4 + size_t(route_dpad(d, E) + kRCPad) * 4 + size_t(2 * kRCSlots) * 8;
+    return size_t(kRCSlots) * E * rc_ps(rows) * 4 + size_t(kRCTok) * (route_dpad(d, E) + kRCPad) * 4 +
+           size_t(2 * kRCSlots) * 8;
 }
 
 template <int EPL, int EFIX, bool SEL>
-__global__ void __launch_bounds__(64, 1) k_route_chain(RouteArgs a, Plan P) {
+__global__ void __launch_bounds__((kRCTok + 1) * 32, 1) k_route_chain(RouteArgs a, Plan P) {
     extern __shared__ __align__(128) float s_dyn[];
     pdl_trigger();  // the expert-FFN grid may launch and run its prologue now
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -726,11 +731,14 @@ __global__ void __launch_bounds__(64, 1) k_route_chain(RouteArgs a, Plan P) {
     const int E = EFIX ? EFIX : a.E, d = a.d, k = a.topk;
     const int rows = route_chunk_rows(E), PS = rc_ps(rows), cf = E * PS;  // floats per chunk
     const int nch = (d + rows - 1) / rows, dpad = nch * rows;
-    float* ring = s_dyn;               // [kRCSlots][E][PS]
-    float* hr = ring + kRCSlots * cf;  // [dpad] the token row in fp32 (zero padded)
-    uint64_t* full = reinterpret_cast<uint64_t*>(hr + dpad + kRCPad);
+    const int hs = dpad + kRCPad;         // floats per token row
+    float* ring = s_dyn;                  // [kRCSlots][E][PS]
+    float* hrow = ring + kRCSlots * cf;   // [kRCTok][hs] the token rows in fp32 (zero padded)
+    uint64_t* full = reinterpret_cast<uint64_t*>(hrow + kRCTok * hs);
     uint64_t* empty = full + kRCSlots;
-    const int64_t t = blockIdx.x;
+    const int64_t t0 = int64_t(blockIdx.x) * kRCTok;
+    const int ntok = int(min(int64_t(kRCTok), a.T - t0));
+    constexpr int kTma = kRCTok;  // the TMA warp
     // dbg 9: per-chunk clock64 stamps of CTA 0 in the trace slots of CTAs 1.. (diagnostics)
     unsigned long long* ds = a.dbg == 9 && a.trace && blockIdx.x == 0 ? a.trace + 16 : nullptr;
     auto dstamp = [&](int c, int ev) { if (ds && c < 8) ds[c * 6 + ev] = clock64(); };
@@ -741,17 +749,20 @@ __global__ void __launch_bounds__(64, 1) k_route_chain(RouteArgs a, Plan P) {
         mbar_arrive_expect_tx(&full[s], uint32_t(cf * 4));
         bulk_g2s(ring + s * cf, a.wg_blk + int64_t(c) * cf, uint32_t(cf * 4), &full[s]);
     };
-    if (warp == 1 && lane == 0) {  // barriers, then the first chunks while the row loads
-        for (int s = 0; s < kRCSlots; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    if (warp == kTma && lane == 0) {  // barriers, then the first chunks while the rows load
+        for (int s = 0; s < kRCSlots; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kRCTok); }
         fence_barrier_init();
         for (int c = 0; c < min(nch, kRCSlots); ++c) issue(c);
     }
-    {  // token row -> fp32 (both warps)
-        const int tid = threadIdx.x, nthr = 64;
+    {  // token rows -> fp32 (every warp)
+        const int tid = threadIdx.x, nthr = (kRCTok + 1) * 32;
         if (a.h_f16 && (d % 8) == 0 && (reinterpret_cast<uintptr_t>(a.h) & 15) == 0) {
-            const uint4* src = reinterpret_cast<const uint4*>(static_cast<const __half*>(a.h) + t * d);
-            for (int j = tid; j < d / 8; j += nthr) {
-                const uint4 v = __ldg(src + j);
+            const uint4* src = reinterpret_cast<const uint4*>(static_cast<const __half*>(a.h) + t0 * d);
+            const int d8 = d / 8;
+            for (int jj = tid; jj < ntok * d8; jj += nthr) {
+                const int r = jj >= d8 ? (jj >= 2 * d8 ? (jj >= 3 * d8 ? 3 : 2) : 1) : 0, j = jj - r * d8;
+                float* hr = hrow + r * hs;
+                const uint4 v = __ldg(src + jj);
                 const __half2* h2 = reinterpret_cast<const __half2*>(&v);
                 float4 lo, hi;
                 float2 f;
@@ -762,17 +773,21 @@ __global__ void __launch_bounds__(64, 1) k_route_chain(RouteArgs a, Plan P) {
                 reinterpret_cast<float4*>(hr)[2 * j] = lo;
                 reinterpret_cast<float4*>(hr)[2 * j + 1] = hi;
             }
-            for (int p = d + tid; p < dpad + kRCPad; p += nthr) hr[p] = 0.0f;
+            for (int r = 0; r < kRCTok; ++r)  // padding (and the rows of absent tokens)
+                for (int p = (r < ntok ? d : 0) + tid; p < hs; p += nthr) hrow[r * hs + p] = 0.0f;
         } else {
-            for (int p = tid; p < dpad + kRCPad; p += nthr) hr[p] = p < d ? load_act(a.h, a.h_f16, t * d + p) : 0.0f;
+            for (int pp = tid; pp < kRCTok * hs; pp += nthr) {
+                const int r = pp / hs, p = pp - r * hs;
+                hrow[pp] = (p < d && r < ntok) ? load_act(a.h, a.h_f16, (t0 + r) * d + p) : 0.0f;
+            }
         }
         if (a.inline_scatter && a.zero_out)  // top-2: fp32 accumulation rows start at zero
-            for (int j = tid; j < d; j += nthr) a.zero_out[t * d + j] = 0.f;
+            for (int j = tid; j < ntok * d; j += nthr) a.zero_out[t0 * d + j] = 0.f;
     }
     __syncthreads();
     if (tr && threadIdx.x == 0) tr[1] = gtime_ns();
 
-    if (warp == 1) {
+    if (warp == kTma) {
         if (lane == 0)
             for (int c = kRCSlots; c < nch; ++c) {
                 while (!mbar_try_wait_sleep(&empty[c % kRCSlots], ((c / kRCSlots) - 1) & 1)) {
@@ -781,7 +796,10 @@ __global__ void __launch_bounds__(64, 1) k_route_chain(RouteArgs a, Plan P) {
             }
         __syncwarp();
     } else {
-        // ===== chain warp
+        // ===== chain warp: token t0 + warp
+        const int64_t t = t0 + warp;
+        const bool live = warp < ntok;
+        const float* hr = hrow + warp * hs;
         const long long clk0 = clock64();
         float acc[EPL];
 #pragma unroll
@@ -794,11 +812,11 @@ __global__ void __launch_bounds__(64, 1) k_route_chain(RouteArgs a, Plan P) {
         for (int c = 0; c < nch; ++c) {
             const int s = c % kRCSlots;
             mbar_wait(&full[s], (c / kRCSlots) & 1);
-            if (lane == 0) dstamp(c, 3);
+            if (threadIdx.x == 0) dstamp(c, 3);
             const float* wc = ring + s * cf;
             const float* hc = hr + c * rows;
             const int ng = (min(rows, d - c * rows) + 3) / 4;
-            if (a.dbg != 1 && ng == rows / 4 && ng % (2 * V) == 0) {
+            if (live && a.dbg != 1 && ng == rows / 4 && ng % (2 * V) == 0) {
                 // full chunk: ping-pong register blocks, the next block's loads in flight during
                 // this block's dependent FADDs; no clamps or guards (immediate-offset loads; the
                 // look-ahead past the chunk reads padding or the next slot, never used)
@@ -833,7 +851,7 @@ __global__ void __launch_bounds__(64, 1) k_route_chain(RouteArgs a, Plan P) {
                     ld(xa, wa, g + 2 * V);
                     run(xb, wb);
                 }
-            } else if (a.dbg != 1) {
+            } else if (live && a.dbg != 1) {
                 // partial chunk: the same with clamped addresses and guarded adds
                 float4 xa[V], xb[V], wa[V][EPL], wb[V][EPL];
                 auto ld = [&](float4 (&x)[V], float4 (&w)[V][EPL], int g0) {
@@ -866,7 +884,10 @@ __global__ void __launch_bounds__(64, 1) k_route_chain(RouteArgs a, Plan P) {
                 }
             }
             __syncwarp();
-            if (lane == 0) { dstamp(c, 4); mbar_arrive(&empty[s]); }
+            if (lane == 0) {
+                if (warp == 0) dstamp(c, 4);
+                mbar_arrive(&empty[s]);
+            }
             if (tr && threadIdx.x == 0 && c < 8) tr[2 + c] = gtime_ns();
         }
         // argmax / gate (reference tie rule, fp64 softmax)
@@ -890,7 +911,7 @@ __global__ void __launch_bounds__(64, 1) k_route_chain(RouteArgs a, Plan P) {
             g2 = float(z / (1.0 + z));
         }
         if (tr && threadIdx.x == 0) { tr[10] = gtime_ns(); tr[13] = clock64() - clk0; }
-        if (lane == 0) {  // the GEMV grid builds the plan from these
+        if (live && lane == 0) {  // the GEMV grid builds the plan from these
             P.expert[t * k] = b1i;
             P.gate[t * k] = g1;
             if (k == 2) {
@@ -1274,8 +1295,8 @@ cudaError_t launch_chain(const RouteArgs& a, const Plan& P, size_t smem, cudaStr
         configured = true;
     }
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(unsigned(a.T));
-    cfg.blockDim = dim3(64);
+    cfg.gridDim = dim3(unsigned((a.T + kRCTok - 1) / kRCTok));
+    cfg.blockDim = dim3((kRCTok + 1) * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];

@@ -77,10 +77,10 @@ def test_decode_forward_routing_finite_and_nonfinite_bank_router(gpu, orc, topk)
     # zero activations (model.cpp:160-162 skips them) must switch the bank to the exact skip.
     import torch
     rng = np.random.default_rng(5 + topk)
-    E, d, f, T = 32, 1024, 256, 24
+    E, d, f = 32, 1024, 256
     w1 = torch.randn(E, d, f, device="cuda") * 0.02
     w2 = torch.randn(E, f, d, device="cuda") * 0.02
-    for nonfinite in (False, True):
+    for T, nonfinite in ((24, False), (24, True), (5, False), (1, True)):  # odd T: a half-used router CTA
         h = fp16_valued(rng.standard_normal((T, d)))
         wg = (rng.standard_normal((d, E)) * 0.02).astype(np.float32)
         if nonfinite:
