@@ -41,6 +41,20 @@ __global__ void k(float* out, long long* cyc) {
             ld(hc, wb, min(q + 2 * BK, ROWS - BK), xa, wa);
             run(acc, xb, wbk);
         }
+    } else if (V == 2) {  // the kernel's structure: 8 chunks of 128 rows, the pipeline restarts per chunk
+        for (int c = 0; c < ROWS / 128; ++c) {
+            const float* wc = wb + c * 128 * E;
+            const float* hcc = hc + c * 128;
+            float xa[BK], wa[BK], xb[BK], wbk[BK];
+            ld(hcc, wc, 0, xa, wa);
+            for (int q = 0; q + 2 * BK <= 128; q += 2 * BK) {
+                ld(hcc, wc, q + BK, xb, wbk);
+                run(acc, xa, wa);
+                ld(hcc, wc, min(q + 2 * BK, 128 - BK), xa, wa);
+                run(acc, xb, wbk);
+            }
+            __syncwarp();
+        }
     } else {  // deeper: 4 blocks in flight
         float x0[BK], w0[BK], x1[BK], w1[BK], x2[BK], w2[BK], x3[BK], w3[BK];
         ld(hc, wb, 0, x0, w0); ld(hc, wb, BK, x1, w1); ld(hc, wb, 2 * BK, x2, w2);
@@ -64,8 +78,13 @@ int main() {
     const int smem = (ROWS * E + 4 * ROWS) * 4;
     cudaFuncSetAttribute(k<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(k<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    for (int rep = 0; rep < 2; ++rep) { k<0><<<1, 128, smem>>>(o, c); k<1><<<1, 128, smem>>>(o, c); }
-    long long h[2]; cudaMemcpy(h, c, 16, cudaMemcpyDeviceToHost);
-    printf("ping-pong (router): %.2f cycles/step\n4-deep:             %.2f cycles/step\n", double(h[0]) / ROWS, double(h[1]) / ROWS);
+    cudaFuncSetAttribute(k<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int rep = 0; rep < 2; ++rep) {
+        k<0><<<1, 128, smem>>>(o, c); k<1><<<1, 128, smem>>>(o, c); k<2><<<1, 128, smem>>>(o, c);
+        k<0><<<1, 32, smem>>>(o, c + 4);
+    }
+    long long h[8]; cudaMemcpy(h, c, 64, cudaMemcpyDeviceToHost);
+    printf("ping-pong (router): %.2f cycles/step\n4-deep:             %.2f cycles/step\nchunked (kernel):   %.2f cycles/step\n1 warp ping-pong:   %.2f cycles/step\n",
+           double(h[0]) / ROWS, double(h[1]) / ROWS, double(h[2]) / ROWS, double(h[4]) / ROWS);
     return 0;
 }
