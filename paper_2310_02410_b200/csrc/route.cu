@@ -698,7 +698,7 @@ __global__ void __launch_bounds__((TT + 1) * 32, 1) k_route_decode(RouteArgs a, 
 
 // ---- decode without a plan (the GEMV grid builds it): one chain warp, blocked Wg -------
 // The bank keeps a second copy of the router weights, transposed and blocked (built once by
-// route_block_wg): 16 KB chunks [chunk][expert][rows + 4] (a 16-byte pad per expert row, so
+// route_block_wg): chunks [chunk][expert][rows + 4] (rc_rows; a 16-byte pad per expert row, so
 // eight lanes' LDS.128 cover all 32 banks). One token per CTA. The chain warp (lane j <->
 // experts j, j + 32, ...) reads four consecutive k of its expert per LDS.128 and four
 // activations per broadcast LDS.128, and runs the reference's sequential fp32 chain (FMUL,
@@ -711,13 +711,24 @@ __global__ void __launch_bounds__((TT + 1) * 32, 1) k_route_decode(RouteArgs a, 
 // router occupies T/4 SMs instead of T — fewer expert-FFN CTAs launch late behind it.
 constexpr int kRCTok = 2;
 static_assert(kRCTok <= 4, "row index math below covers up to 4 tokens");
-constexpr int kRCSlots = 8;
+// Chunking (measured: every chunk boundary restarts the register pipeline and costs the
+// chain more than the copy latency it hides): the whole Wg as ONE chunk when it fits
+// ~136 KB (E = 32, d = 1024: 128 KB), else ~64 KB chunks through two slots.
+constexpr int kRCOneChunk = 136 * 1024;
+__host__ __device__ constexpr int rc_ps(int rows);
+__host__ __device__ inline int rc_rows(int d, int E) {
+    const int whole = (d + 31) / 32 * 32;  // a multiple of 32: full chunks take the fast path
+    if (int64_t(E) * (whole + 4) * 4 <= kRCOneChunk) return whole;
+    return 4 * route_chunk_rows(E);
+}
+__host__ __device__ inline int rc_slots(int d, int E) { return rc_rows(d, E) >= d ? 1 : 2; }
+constexpr int kRCSlotsMax = 2;
 constexpr int kRCPad = 64;  // floats after the token row: the chain's look-ahead loads past a chunk stay in bounds
 __host__ __device__ constexpr int rc_ps(int rows) { return rows + 4; }
 size_t route_chain_smem(int d, int E) {
-    const int rows = route_chunk_rows(E);
-    return size_t(kRCSlots) * E * rc_ps(rows) * 4 + size_t(kRCTok) * (route_dpad(d, E) + kRCPad) * 4 +
-           size_t(2 * kRCSlots) * 8;
+    const int rows = rc_rows(d, E);
+    return size_t(rc_slots(d, E)) * E * rc_ps(rows) * 4 + size_t(kRCTok) * ((d + rows - 1) / rows * rows + kRCPad) * 4 +
+           size_t(2 * kRCSlotsMax) * 8;
 }
 
 template <int EPL, int EFIX, bool SEL>
@@ -729,13 +740,14 @@ __global__ void __launch_bounds__((kRCTok + 1) * 32, 1) k_route_chain(RouteArgs 
                                  ? a.trace + blockIdx.x * 16 : nullptr;
     if (tr && threadIdx.x == 0) tr[0] = gtime_ns();
     const int E = EFIX ? EFIX : a.E, d = a.d, k = a.topk;
-    const int rows = route_chunk_rows(E), PS = rc_ps(rows), cf = E * PS;  // floats per chunk
+    const int rows = rc_rows(d, E), PS = rc_ps(rows), cf = E * PS;  // floats per chunk
+    const int nslot = rc_slots(d, E), sh = nslot - 1;                 // 1 or 2 slots: c >> sh = use count
     const int nch = (d + rows - 1) / rows, dpad = nch * rows;
     const int hs = dpad + kRCPad;         // floats per token row
-    float* ring = s_dyn;                  // [kRCSlots][E][PS]
-    float* hrow = ring + kRCSlots * cf;   // [kRCTok][hs] the token rows in fp32 (zero padded)
+    float* ring = s_dyn;                  // [nslot][E][PS]
+    float* hrow = ring + nslot * cf;      // [kRCTok][hs] the token rows in fp32 (zero padded)
     uint64_t* full = reinterpret_cast<uint64_t*>(hrow + kRCTok * hs);
-    uint64_t* empty = full + kRCSlots;
+    uint64_t* empty = full + kRCSlotsMax;
     const int64_t t0 = int64_t(blockIdx.x) * kRCTok;
     const int ntok = int(min(int64_t(kRCTok), a.T - t0));
     constexpr int kTma = kRCTok;  // the TMA warp
@@ -743,16 +755,16 @@ __global__ void __launch_bounds__((kRCTok + 1) * 32, 1) k_route_chain(RouteArgs 
     unsigned long long* ds = a.dbg == 9 && a.trace && blockIdx.x == 0 ? a.trace + 16 : nullptr;
     auto dstamp = [&](int c, int ev) { if (ds && c < 8) ds[c * 6 + ev] = clock64(); };
     if (ds && threadIdx.x == 0) ds[60] = clock64();
-    auto issue = [&](int c) {  // chunk c -> slot c % kRCSlots
-        const int s = c % kRCSlots;
+    auto issue = [&](int c) {  // chunk c -> slot c & sh
+        const int s = c & sh;
         dstamp(c, 0);
         mbar_arrive_expect_tx(&full[s], uint32_t(cf * 4));
         bulk_g2s(ring + s * cf, a.wg_blk + int64_t(c) * cf, uint32_t(cf * 4), &full[s]);
     };
     if (warp == kTma && lane == 0) {  // barriers, then the first chunks while the rows load
-        for (int s = 0; s < kRCSlots; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kRCTok); }
+        for (int s = 0; s < nslot; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kRCTok); }
         fence_barrier_init();
-        for (int c = 0; c < min(nch, kRCSlots); ++c) issue(c);
+        for (int c = 0; c < min(nch, nslot); ++c) issue(c);
     }
     {  // token rows -> fp32 (every warp)
         const int tid = threadIdx.x, nthr = (kRCTok + 1) * 32;
@@ -789,8 +801,8 @@ __global__ void __launch_bounds__((kRCTok + 1) * 32, 1) k_route_chain(RouteArgs 
 
     if (warp == kTma) {
         if (lane == 0)
-            for (int c = kRCSlots; c < nch; ++c) {
-                while (!mbar_try_wait_sleep(&empty[c % kRCSlots], ((c / kRCSlots) - 1) & 1)) {
+            for (int c = nslot; c < nch; ++c) {
+                while (!mbar_try_wait_sleep(&empty[c & sh], ((c >> sh) - 1) & 1)) {
                 }
                 issue(c);
             }
@@ -810,8 +822,8 @@ __global__ void __launch_bounds__((kRCTok + 1) * 32, 1) k_route_chain(RouteArgs 
         for (int e = 0; e < EPL; ++e) col[e] = (EFIX || lane + 32 * e < E) ? lane + 32 * e : 0;
         auto mul = [](float x, float w) { return SEL ? (x != 0.0f ? __fmul_rn(x, w) : 0.0f) : __fmul_rn(x, w); };
         for (int c = 0; c < nch; ++c) {
-            const int s = c % kRCSlots;
-            mbar_wait(&full[s], (c / kRCSlots) & 1);
+            const int s = c & sh;
+            mbar_wait(&full[s], (c >> sh) & 1);
             if (threadIdx.x == 0) dstamp(c, 3);
             const float* wc = ring + s * cf;
             const float* hc = hr + c * rows;
@@ -928,7 +940,7 @@ __global__ void __launch_bounds__((kRCTok + 1) * 32, 1) k_route_chain(RouteArgs 
 // Router weights [d][E] -> the blocked, transposed copy k_route_chain streams; flags any
 // non-finite weight (then the chain keeps the explicit zero-activation select).
 __global__ void k_wg_block(const float* __restrict__ wg, int d, int E, float* __restrict__ out, int* nonfinite) {
-    const int rows = route_chunk_rows(E), PS = rc_ps(rows);
+    const int rows = rc_rows(d, E), PS = rc_ps(rows);
     const int nch = (d + rows - 1) / rows;
     const int64_t n = int64_t(nch) * E * PS;
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
@@ -942,7 +954,7 @@ __global__ void k_wg_block(const float* __restrict__ wg, int d, int E, float* __
     }
 }
 int64_t route_wg_block_floats(int d, int E) {
-    const int rows = route_chunk_rows(E);
+    const int rows = rc_rows(d, E);
     return int64_t((d + rows - 1) / rows) * E * rc_ps(rows);
 }
 cudaError_t route_block_wg(const float* wg, int d, int E, float* out, int* d_flag, int* finite) {
