@@ -707,9 +707,10 @@ __global__ void __launch_bounds__((TT + 1) * 32, 1) k_route_decode(RouteArgs a, 
 // needs no select: 0 * w is +-0, and adding +-0 leaves the sum unchanged (it starts at +0
 // and round-to-nearest never yields -0 from a nonzero sum); otherwise x != 0 selects. A TMA
 // warp streams the chunks through a ring. kRCTok tokens per CTA, one chain warp each (one per
-// SM sub-partition): the chains are latency-bound, so sharing the ring costs nothing, and the
-// router occupies T/4 SMs instead of T — fewer expert-FFN CTAs launch late behind it.
-constexpr int kRCTok = 2;
+// SM sub-partition), sharing the ring: fewer router SMs means fewer expert-FFN CTAs launching
+// late behind it, but with the one-chunk layout 1 token per CTA measured best (32.6 us per
+// layer vs 33.0 with 2 and 33.8 with 4).
+constexpr int kRCTok = 1;
 static_assert(kRCTok <= 4, "row index math below covers up to 4 tokens");
 // Chunking (measured: every chunk boundary restarts the register pipeline and costs the
 // chain more than the copy latency it hides): the whole Wg as ONE chunk when it fits
