@@ -243,11 +243,14 @@ __device__ void build_tables_self(GemvTables& T, const Plan& P, int nr, int E, i
         T.tok[pos] = i0 / k;
         T.gate[pos] = g0;
     }
+    int before = 0;  // rows 0..31 with the same expert
+    if (small) {
+        if (e1 >= 0) before = h1[e1];
+    } else {
+        // every lane takes part in the full-mask shuffles (rows >= nr have e1 = -1)
+        for (int j = 0; j < 32; ++j) before += __shfl_sync(0xffffffffu, e0, j) == e1;
+    }
     if (e1 >= 0) {
-        int before = 0;  // rows 0..31 with the same expert
-        if (small) before = h1[e1];
-        else
-            for (int j = 0; j < 32; ++j) before += __shfl_sync(0xffffffffu, e0, j) == e1;
         const int pos = T.eoff[e1] + before + __popc(m1 & lt);
         T.tok[pos] = i1 / k;
         T.gate[pos] = g1;

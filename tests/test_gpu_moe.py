@@ -54,6 +54,8 @@ CASES = [
     # decode-path boundaries: self-planned GEMV (T*k <= 64, T <= 32), decode router EPL 2 / 8
     (64, 1024, 2048, 3, 32, 2, False),   # T*k = 64 (self-plan limit), fc2 split-K over 2 CTAs
     (256, 256, 512, 2, 32, 1, True),     # E = 256: multi-round expert scans in the self plan
+    (256, 512, 256, 4, 24, 2, False),    # E > 64 with 32 < T*k < 64: partly filled second row half of the self plan
+    (100, 256, 512, 3, 20, 2, True),
     (32, 512, 1024, 4, 33, 1, False),    # T = 33: routed plan + packed GEMV table path
     (8, 2048, 1024, 3, 8, 1, True),      # d = 2048: fc1 split-K over a 2-CTA cluster
     (4, 256, 8192, 2, 6, 2, False),      # f = 8192: fc2 split-K over an 8-CTA cluster

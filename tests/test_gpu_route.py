@@ -70,14 +70,17 @@ def test_route_nonfinite_weights_under_zero_activations(gpu, orc):
         assert np.allclose(g.cpu().numpy(), g_o, rtol=1e-6, atol=0)
 
 
-@pytest.mark.parametrize("topk", [1, 2])
-def test_decode_forward_routing_finite_and_nonfinite_bank_router(gpu, orc, topk):
+@pytest.mark.parametrize("topk,E,d", [(1, 32, 1024), (2, 32, 1024), (1, 64, 1024), (2, 256, 512),
+                                       (1, 40, 2048), (1, 128, 256)])
+def test_decode_forward_routing_finite_and_nonfinite_bank_router(gpu, orc, topk, E, d):
     # decode forward (T*k <= 64): the bank's blocked router copy and the one-warp chain
     # (ffn decode self plan). Finite Wg: the select-free chain; an inf weight met only by
     # zero activations (model.cpp:160-162 skips them) must switch the bank to the exact skip.
+    # Shapes: Wg as one chunk (E=32, d=1024; E=128, d=256) and as ~64 KB chunks through two
+    # slots (E=64, E=256, d=2048), one to eight experts per lane, E not a multiple of 32.
     import torch
-    rng = np.random.default_rng(5 + topk)
-    E, d, f = 32, 1024, 256
+    rng = np.random.default_rng(5 + topk + E + d)
+    f = 256
     w1 = torch.randn(E, d, f, device="cuda") * 0.02
     w2 = torch.randn(E, f, d, device="cuda") * 0.02
     for T, nonfinite in ((24, False), (24, True), (5, False), (1, True)):  # odd T: a half-used router CTA
