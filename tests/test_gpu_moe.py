@@ -78,6 +78,14 @@ def test_moe_vs_oracle(gpu, orc, E, d, f, bits, T, topk, bias):
             assert np.allclose(g.cpu().numpy(), g_o, rtol=1e-6, atol=0)
             nbad, mx = allclose_report(out.cpu().numpy(), want, ATOL, RTOL)
             assert nbad == 0, (path, hdt, mx)
+    # the bank's router (set once; its blocked copy feeds the decode chain router)
+    bank.set_router(_t(L["wg"]))
+    for hdt in (torch.float32, torch.float16):
+        out, ex, g = gpu.moe_ffn_forward(_t(L["h"]).to(hdt), bank, top_k=topk, return_routing=True)
+        assert np.array_equal(ex.cpu().numpy(), ex_o), ("bank router", hdt)
+        assert np.allclose(g.cpu().numpy(), g_o, rtol=1e-6, atol=0)
+        nbad, mx = allclose_report(out.cpu().numpy(), want, ATOL, RTOL)
+        assert nbad == 0, ("bank router", hdt, mx)
 
 
 def _gemm_ok(gpu):
