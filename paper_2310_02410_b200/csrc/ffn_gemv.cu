@@ -45,11 +45,13 @@
 //               exact group sums go to a double-buffered scratch and the warp
 //               moves straight on to the next item (the stream never waits
 //               for an epilogue)
-//   warps 8-11  epilogue: thread = channel; exact int64 partials, split-K
-//               reduction into cluster rank 0 over DSMEM, scale/bias, and
+//   warps 8-15  epilogue, two groups of four taking alternate items: thread =
+//               channel; exact int64 partials, split-K reduction into cluster
+//               rank 0 over DSMEM, scale/bias, and
 //               fc1: ReLU -> fc2 fixed point -> fc2 row blocks in global memory
+//               (fused grid: then a per-pass readiness release)
 //               fc2: gate-weighted output rows (one writer per element)
-//   warp 12     producer: row blocks + weight copy units (TMA, evict-first)
+//   warp 16     producer: row blocks + weight copy units (TMA, evict-first)
 #include <cuda_fp16.h>
 
 #include <algorithm>
