@@ -36,10 +36,12 @@ N_LAYERS = 8
 
 
 def gemv_extra(d, T, top_k):
-    """Kernels beside the timed "gemv" scope's first: k_xrows, plus the fc2 grid unless
-    fc1 and fc2 run as one fused grid (capi.cu: self plan, fc1 in one 1024-k chunk)."""
+    """Kernels beside the timed "gemv" scope's first: the fc2 grid unless fc1 and fc2 run as
+    one fused grid (capi.cu: self plan, fc1 in one 1024-k chunk), plus k_xrows unless the
+    decode router writes the fc1 row blocks itself (self plan with the bank's router)."""
     fused = (T * top_k <= 64 and T <= 32 and d <= 1024 and os.environ.get("MOQE_GEMV_FUSED", "1") != "0")
-    return 1 if fused else 2
+    in_router = T * top_k <= 64 and T <= 32 and os.environ.get("MOQE_XROWS_IN_ROUTER", "1") != "0"
+    return (0 if fused else 1) + (0 if in_router else 1)
 
 
 def packed_bytes(bits: int, n: int) -> int:

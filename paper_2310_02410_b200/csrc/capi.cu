@@ -92,6 +92,10 @@ bool gemv_fused() {  // MOQE_GEMV_FUSED=0: decode as two grids (fc1, fc2) even w
     static const bool v = [] { const char* s = getenv("MOQE_GEMV_FUSED"); return !(s && atoi(s) == 0); }();
     return v;
 }
+bool xrows_in_router() {  // MOQE_XROWS_IN_ROUTER=0: decode keeps the separate k_xrows launch
+    static const bool v = [] { const char* s = getenv("MOQE_XROWS_IN_ROUTER"); return !(s && atoi(s) == 0); }();
+    return v;
+}
 int gemv_dbg() {  // diagnostics only
     static const int v = [] { const char* s = getenv("MOQE_GEMV_DBG"); return s ? atoi(s) : 0; }();
     return v;
@@ -395,7 +399,16 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
         ra.no_plan = self_plan ? 1 : 0;
         if (wg == b->wg && b->wg_blk) { ra.wg_blk = b->wg_blk; ra.wg_finite = b->wg_finite; }
         ra.dbg = route_dbg();
-        if (need_gemv) {  // token rows -> fc1 row blocks; the decode router overlaps it (PDL)
+        if (need_gemv && !pre && route_chain_used(ra) && xrows_in_router()) {
+            // decode: the router leads the chain (waits for the previous grid itself) and its
+            // copy warp writes the fc1 row blocks — two launches per forward
+            ra.first = 1;
+            ra.pdl = 1;
+            ra.xr = w.xr;
+            ra.nch1 = gemv_chunks(b->Kp1);
+            ra.xr_bits = b->bits;
+            ra.ready = self_plan && gemv_fused() ? w.ready : nullptr;
+        } else if (need_gemv) {  // token rows -> fc1 row blocks; the decode router overlaps it (PDL)
             XrowArgs xa{h, h_dtype == MOQE_F16, t, int(b->d), gemv_chunks(b->Kp1), w.xr,
                         self_plan && gemv_fused() ? w.ready : nullptr};
             ce = launch_xrows(b->bits, xa, st);

@@ -47,7 +47,14 @@ struct RouteArgs {
     int dbg;                    // diagnostics (env MOQE_ROUTE_DBG; 1 = skip the logit chain, timing only)
     const float* wg_blk;        // the bank's blocked copy of wg (route_block_wg) or null
     int wg_finite;              // wg has no inf / NaN
+    // decode chain led by the router (k_route_chain only): it waits for the previous grid
+    // itself, zeroes the GEMV readiness counters and writes the fc1 row blocks (no k_xrows)
+    int first;
+    uint8_t* xr;                // fc1 row blocks [T][nch1][xr bytes] or null
+    int nch1, xr_bits;
+    unsigned* ready;            // [kSelfPlanRows] or null
 };
+bool route_chain_used(const RouteArgs& a);  // launch_route will run k_route_chain
 constexpr int kTraceRouteCtas = 64;
 // Router weights -> blocked transposed copy for the decode chain; *finite = no inf / NaN.
 int64_t route_wg_block_floats(int d, int E);

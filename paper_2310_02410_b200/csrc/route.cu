@@ -20,6 +20,7 @@
 
 #include "kernels.cuh"
 #include "ptx.cuh"
+#include "xrow.cuh"
 
 namespace moqe_gpu {
 
@@ -732,10 +733,51 @@ size_t route_chain_smem(int d, int E) {
            size_t(2 * kRCSlotsMax) * 8;
 }
 
+// fc1 row blocks of a router CTA's tokens from their rows in smem (the decode router's
+// copy warp; out of line so the chain warp's code and registers are unaffected).
+__device__ __noinline__ void route_xrows(const RouteArgs& a, const float* hrow, int hs, int ntok, int64_t t0,
+                                         int lane) {
+    const int d = a.d;
+    for (int r = 0; r < ntok; ++r) {
+        const float* hr = hrow + r * hs;
+        auto q16 = [&](float x) { return a.h_f16 ? x : __half2float(__float2half_rn(x)); };
+        float m = 0.f, l1 = 0.f;
+        for (int kk = lane; kk < d; kk += 32) {
+            const float x = fabsf(q16(hr[kk]));
+            m = fmaxf(m, x);
+            l1 += x;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+            l1 += __shfl_xor_sync(0xffffffffu, l1, off);
+        }
+        const int st = lane >> 2, tq = lane & 3;
+        for (int c = 0; c < a.nch1; ++c) {
+            float v[32];
+            const int k0 = c * kChunkK + st * kStageK + 16 * tq;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                v[i] = k0 + i < d ? q16(hr[k0 + i]) : 0.f;
+                v[16 + i] = k0 + 64 + i < d ? q16(hr[k0 + 64 + i]) : 0.f;
+            }
+            const int64_t row = (t0 + r) * a.nch1 + c;
+            switch (a.xr_bits) {
+                case 2: xrow_encode<2>(v, m, l1, a.xr + row * RB<2>::XR1, lane); break;
+                case 3: xrow_encode<3>(v, m, l1, a.xr + row * RB<3>::XR1, lane); break;
+                case 4: xrow_encode<4>(v, m, l1, a.xr + row * RB<4>::XR1, lane); break;
+                default: xrow_encode<8>(v, m, l1, a.xr + row * RB<8>::XR1, lane); break;
+            }
+        }
+    }
+}
+
 template <int EPL, int EFIX, bool SEL>
 __global__ void __launch_bounds__((kRCTok + 1) * 32, 1) k_route_chain(RouteArgs a, Plan P) {
     extern __shared__ __align__(128) float s_dyn[];
-    pdl_trigger();  // the expert-FFN grid may launch and run its prologue now
+    if (a.first) pdl_wait();  // leads the decode chain: the previous grid made the token rows
+    pdl_trigger();            // the expert-FFN grid may launch and run its prologue now
+    if (a.first && a.ready && blockIdx.x == 0 && threadIdx.x < kSelfPlanRows) a.ready[threadIdx.x] = 0u;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned long long* tr = (a.trace && blockIdx.x < kTraceRouteCtas && (a.dbg != 9 || blockIdx.x == 0))
                                  ? a.trace + blockIdx.x * 16 : nullptr;
@@ -808,6 +850,9 @@ __global__ void __launch_bounds__((kRCTok + 1) * 32, 1) k_route_chain(RouteArgs 
                 issue(c);
             }
         __syncwarp();
+        // this warp is otherwise idle during the chain: the tokens' fc1 row blocks from the
+        // rows in smem (fp16-valued, as k_xrows reads them; same exponent, digits and planes)
+        if (a.xr) route_xrows(a, hrow, hs, ntok, t0, lane);
     } else {
         // ===== chain warp: token t0 + warp
         const int64_t t = t0 + warp;
@@ -935,7 +980,7 @@ __global__ void __launch_bounds__((kRCTok + 1) * 32, 1) k_route_chain(RouteArgs 
     }
     // launched behind k_xrows (PDL): the grid completes only after it, so the expert-FFN
     // grid's own dependency wait on this grid covers the row blocks too
-    if (blockIdx.x == 0 && threadIdx.x == 0) pdl_wait();
+    if (!a.first && blockIdx.x == 0 && threadIdx.x == 0) pdl_wait();
 }
 
 // Router weights [d][E] -> the blocked, transposed copy k_route_chain streams; flags any
@@ -1331,6 +1376,10 @@ cudaError_t launch_dec(const RouteArgs& a, const Plan& P, size_t smem, cudaStrea
 }
 }  // namespace
 
+bool route_chain_used(const RouteArgs& a) {
+    return a.no_plan && a.wg_blk && a.T <= kRouteDecMaxT && a.E <= kRouteDecMaxE && a.dbg != 7 &&
+           route_chain_smem(a.d, a.E) <= 220 * 1024 && route_small_smem(a.d, a.E) <= 220 * 1024;
+}
 cudaError_t launch_route_decode(const RouteArgs& a, const Plan& P, size_t smem, cudaStream_t st) {
     switch (a.E) {
         case 32: return launch_dec<1, 32>(a, P, smem, st);
