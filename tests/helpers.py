@@ -41,3 +41,40 @@ def allclose_report(got, ref, atol=2e-3, rtol=1e-2):
     diff = np.abs(got - ref)
     bad = diff > atol + rtol * np.abs(ref)
     return int(bad.sum()), float(diff.max() if diff.size else 0.0)
+
+
+def sampled_moe_expected(orc, h, wg, top_k, tokens, expert_codes, ex_all, g_all, b1=None, b2=None,
+                         threads=8):
+    """Oracle MoE outputs for a SAMPLE of tokens (rows are independent:
+    /root/reference/proj/src/model.cpp:360-391 touches a token only through its own
+    experts). expert_codes(e) -> (q1, s1, q2, s2) from the oracle quantizer; ex_all /
+    g_all are the oracle's routing of ALL tokens ([T] or [T, k]). out[t] = g0*y0
+    (+ g1*y1), fp32, in slot order like oracle/moqe_oracle.c run_shard."""
+    from concurrent.futures import ThreadPoolExecutor
+    ex = np.asarray(ex_all).reshape(len(ex_all), -1)
+    g = np.asarray(g_all, np.float32).reshape(len(g_all), -1)
+    need = {}
+    for i, t in enumerate(tokens):
+        for k in range(top_k):
+            need.setdefault(int(ex[t, k]), []).append((i, k))
+    ys = {}
+
+    def run(e):
+        q1, s1, q2, s2 = expert_codes(e)
+        rows = need[e]
+        x = np.stack([h[tokens[i]] for i, _ in rows]).astype(np.float32)
+        y = orc.expert_ffn(x, q1, s1, q2, s2, None if b1 is None else b1[e], None if b2 is None else b2[e])
+        return e, y
+
+    with ThreadPoolExecutor(threads) as pool:  # ctypes releases the GIL
+        for e, y in pool.map(run, sorted(need)):
+            for r, (i, k) in enumerate(need[e]):
+                ys[(i, k)] = y[r]
+    d = h.shape[1]
+    out = np.zeros((len(tokens), d), np.float32)
+    for i, t in enumerate(tokens):
+        o = g[t, 0] * ys[(i, 0)]
+        for k in range(1, top_k):
+            o = o + g[t, k] * ys[(i, k)]
+        out[i] = o
+    return out

@@ -1,0 +1,173 @@
+"""GPU parity at the BASELINE.json shapes bench.py reports (configs 1, 2, 4, 5).
+
+The GPU runs every token; the oracle (oracle/moqe_oracle.c) routes every token and
+computes the expert FFN for a seeded SAMPLE of tokens. That is exact for this path:
+a token's output depends only on its own experts
+(/root/reference/proj/src/model.cpp:360-391). Weights are drawn on the device
+(f32 ~N(0,0.02)) and quantized by the GPU quantizer; for every expert the sample
+touches, the oracle re-quantizes the same f32 weights and the packed bytes and
+scales must be bit-identical, and the oracle's own codes feed the expected values.
+
+Tolerances (BASELINE.json north_star): outputs |gpu - ref| <= 2e-3 + 1e-2*|ref|;
+expert ids bit-exact except tokens whose oracle top-(k+1) logit gap is < 1e-4;
+gates within 1e-5 relative.
+"""
+import numpy as np
+import pytest
+
+from helpers import allclose_report, fp16_valued, sampled_moe_expected
+
+pytestmark = pytest.mark.gpu
+ATOL, RTOL, GAP = 2e-3, 1e-2, 1e-4
+
+
+def _threaded(fn, h, chunks=8):
+    from concurrent.futures import ThreadPoolExecutor
+    parts = np.array_split(np.arange(h.shape[0]), chunks)
+    with ThreadPoolExecutor(chunks) as pool:
+        return list(pool.map(lambda ix: fn(h[ix[0]:ix[-1] + 1]) if len(ix) else None, parts))
+
+
+def oracle_routing(orc, h, wg, top_k):
+    """Oracle ids/gates of all tokens + each token's smallest gap among its top-(k+1) logits."""
+    res = [r for r in _threaded(lambda x: orc.route(x, wg, top_k), h) if r is not None]
+    ex = np.concatenate([r[0] for r in res])
+    g = np.concatenate([r[1] for r in res])
+    lg = np.concatenate([r for r in _threaded(lambda x: orc.router_logits(x, wg), h) if r is not None])
+    top = -np.sort(-lg, axis=1)[:, : top_k + 1]
+    gap = np.min(top[:, :-1] - top[:, 1:], axis=1) if lg.shape[1] > top_k else np.full(len(h), np.inf)
+    return ex, g, gap
+
+
+class GpuLayer:
+    """Expert weights drawn on the device, quantized by the GPU quantizer."""
+
+    def __init__(self, gpu, orc, seed, E, d, f, bits, T, zipf=False):
+        import torch
+        from paper_2310_02410_b200.workloads import apply_bias, zipf_bias
+        gen = torch.Generator(device="cuda").manual_seed(seed)
+        self.w1 = torch.randn((E, d, f), generator=gen, device="cuda") * 0.02
+        self.w2 = torch.randn((E, f, d), generator=gen, device="cuda") * 0.02
+        self.p1, self.s1 = gpu.quantize_pack(self.w1, bits)
+        self.p2, self.s2 = gpu.quantize_pack(self.w2, bits)
+        rng = np.random.default_rng(seed)
+        h = fp16_valued(rng.standard_normal((T, d), dtype=np.float32))
+        wg = (rng.standard_normal((d, E), dtype=np.float32) * 0.02).astype(np.float32)
+        if zipf:
+            h, wg = apply_bias(h, wg, zipf_bias(wg))
+        self.h, self.wg = h, wg
+        self.bank = gpu.ExpertBank(E, d, f, bits, self.p1, self.s1, self.p2, self.s2)
+        self.orc, self.bits = orc, bits
+        self.E, self.d, self.f, self.T = E, d, f, T
+
+    def codes(self, e):
+        """Oracle codes of expert e, pinned bit-exact to the GPU's packed bytes and scales."""
+        orc, b = self.orc, self.bits
+        q1, s1 = orc.quantize_linear(self.w1[e].cpu().numpy(), b)
+        q2, s2 = orc.quantize_linear(self.w2[e].cpu().numpy(), b)
+        assert np.array_equal(orc.pack(q1, b), self.p1[e].cpu().numpy()), f"W1 bytes, expert {e}"
+        assert np.array_equal(orc.pack(q2, b), self.p2[e].cpu().numpy()), f"W2 bytes, expert {e}"
+        assert np.array_equal(s1, self.s1[e].cpu().numpy()) and np.array_equal(s2, self.s2[e].cpu().numpy())
+        return q1, s1, q2, s2
+
+
+def pick_tokens(ex, gap, top_k, n, seed, experts=None):
+    """Seeded sample of well-separated tokens. Always includes tokens of the largest and
+    the smallest non-empty expert. experts: restrict to tokens whose every slot is in it."""
+    rng = np.random.default_rng(seed)
+    ex2 = ex.reshape(len(ex), -1)
+    ok = gap >= GAP
+    if experts is not None:
+        ok &= np.isin(ex2, list(experts)).all(axis=1)
+    cand = np.flatnonzero(ok)
+    counts = np.bincount(ex2[:, 0], minlength=int(ex2.max()) + 1)
+    must = []
+    for e in (int(np.argmax(counts)), int(np.argmin(np.where(counts > 0, counts, 1 << 30)))):
+        rows = cand[ex2[cand, 0] == e]
+        must += list(rows[:8]) + list(rows[-8:])
+    rest = rng.choice(cand, size=min(n, len(cand)), replace=False) if len(cand) else []
+    return np.unique(np.concatenate([np.asarray(must, np.int64), np.asarray(rest, np.int64)]))
+
+
+def check_layer(gpu, L, top_k, n_sample, paths, seed, experts=None, min_rows=None, want_empty=False):
+    import torch
+    ex_o, g_o, gap = oracle_routing(L.orc, L.h, L.wg, top_k)
+    counts = np.bincount(ex_o.reshape(-1), minlength=L.E)
+    if min_rows is not None:
+        assert counts.max() > min_rows, f"case must give an expert > {min_rows} rows (max {counts.max()})"
+    if want_empty:
+        assert (counts == 0).any(), "case must leave an expert empty"
+    tokens = pick_tokens(ex_o, gap, top_k, n_sample, seed, experts)
+    assert len(tokens) > 0
+    want = sampled_moe_expected(L.orc, L.h, L.wg, top_k, tokens, L.codes, ex_o, g_o)
+    h16 = torch.from_numpy(L.h).cuda().half()
+    wg = torch.from_numpy(L.wg).cuda()
+    sep = gap >= GAP
+    for path in paths:
+        out, ex, g = gpu.moe_ffn_forward(h16, L.bank, wg, top_k=top_k, path=path, return_routing=True)
+        ex = ex.cpu().numpy().reshape(ex_o.shape)
+        g = g.cpu().numpy().reshape(g_o.shape)
+        diff_ids = (ex != ex_o).reshape(len(ex), -1).any(axis=1)
+        assert not (diff_ids & sep).any(), (path, "routing differs on a well-separated token",
+                                            np.flatnonzero(diff_ids & sep)[:5])
+        gs = sep if g.ndim == 1 else sep[:, None]
+        gerr = np.abs(g.astype(np.float64) - g_o) / np.maximum(np.abs(g_o), 1e-30)
+        assert (np.where(gs, gerr, 0) <= 1e-5).all(), (path, float(np.where(gs, gerr, 0).max()))
+        got = out[torch.from_numpy(tokens).cuda()].float().cpu().numpy()
+        nbad, mx = allclose_report(got, want, ATOL, RTOL)
+        assert nbad == 0, (path, nbad, mx)
+        assert np.isfinite(out.float().cpu().numpy()).all(), path
+    return counts
+
+
+D1, F1 = 1024, 4096
+
+
+@pytest.mark.parametrize("bits,T", [(4, 512)])
+def test_config1(gpu, orc, bits, T):
+    """BASELINE config 1: 512 tokens, int4, E=32, top-1 (sample = every token)."""
+    L = GpuLayer(gpu, orc, 101, 32, D1, F1, bits, T)
+    check_layer(gpu, L, 1, T, ["auto", "gemm"], 1)
+
+
+@pytest.mark.parametrize("bits,T", [(8, 4096), (4, 4096), (3, 4096), (2, 4096), (3, 16384), (2, 16384)])
+def test_config2_prefill(gpu, orc, bits, T):
+    """BASELINE config 2 at the prefill sizes bench.py reports (T=16384: >256 rows per
+    expert, so the tcgen05 GEMM runs several N tiles per expert)."""
+    L = GpuLayer(gpu, orc, 200 + bits + T, 32, D1, F1, bits, T)
+    counts = check_layer(gpu, L, 1, 384, ["auto", "gemm"], bits, min_rows=256 if T >= 16384 else None)
+    assert counts.min() > 0
+
+
+def test_config4_ep_shape(gpu, orc):
+    """BASELINE config 4 at G=1: d=2048, f=8192, E=128, top-2 renormalised, int2,
+    16384 tokens (~256 rows per expert). The oracle checks the tokens whose both experts
+    fall in a 16-expert subset (incl. the busiest)."""
+    import torch
+    L = GpuLayer(gpu, orc, 400, 128, 2048, 8192, 2, 16384)
+    rng = np.random.default_rng(4)
+    _, ex, _ = gpu.moe_ffn_forward(torch.from_numpy(L.h).cuda().half(), L.bank,
+                                   torch.from_numpy(L.wg).cuda(), top_k=2, return_routing=True)
+    busiest = int(torch.bincount(ex.reshape(-1).long(), minlength=128).argmax())
+    subset = set(rng.choice(128, 15, replace=False).tolist()) | {busiest}
+    check_layer(gpu, L, 2, 512, ["auto", "gemm"], 4, experts=subset, min_rows=256)
+
+
+@pytest.mark.parametrize("T", [1, 8, 64, 512, 4096, 32768])
+def test_config5_zipf(gpu, orc, T):
+    """BASELINE config 5: Zipf(1.2) popularity over E=64 int4 experts (bias folded into
+    Wg[0,:] with h[:,0]=1). Small T leaves experts empty; T=32768 gives one expert
+    > 1024 rows (>10x the mean)."""
+    L = GpuLayer(gpu, orc, 500, 64, D1, F1, 4, T, zipf=True)
+    counts = check_layer(gpu, L, 1, 384, ["auto"] + (["gemm"] if T >= 512 else []), T,
+                         min_rows=1024 if T == 32768 else None, want_empty=T <= 512)
+    if T == 32768:
+        assert counts.max() > 10 * counts.mean()
+
+
+@pytest.mark.parametrize("E,d,f,bits,T,topk", [(4, 256, 512, 4, 2048, 1), (4, 256, 512, 3, 2048, 2),
+                                              (3, 128, 384, 2, 3000, 2)])
+def test_multi_tile_full_oracle(gpu, orc, E, d, f, bits, T, topk):
+    """Small layers with > 256 rows per expert, checked on EVERY token."""
+    L = GpuLayer(gpu, orc, E * 7 + T, E, d, f, bits, T)
+    check_layer(gpu, L, topk, T, ["auto", "gemm"], 9, min_rows=512)
