@@ -163,6 +163,16 @@ moqe_status moqe_gpu_expert_ffn(moqe_bank_t bank, const void* x, moqe_dtype x_dt
 moqe_status moqe_gpu_bank_profile(moqe_bank_t bank, int enable);
 moqe_status moqe_gpu_bank_profile_read(moqe_bank_t bank, double* ms, int64_t* launches, int keep);
 
+/* In-kernel launch spans of the decode path (measurement support, off by default):
+ * with span(bank, 1) each decode forward's router and expert-FFN kernels record,
+ * on the device, the time from the first CTA's start (after the programmatic-
+ * dependent-launch wait) to the last CTA's exit, without breaking the launch
+ * chain (no event nodes). span_read synchronises and returns, per kind
+ * (0 router, 1 expert FFN), the summed microseconds and the launch count since
+ * the last read, then clears them. */
+moqe_status moqe_gpu_bank_span(moqe_bank_t bank, int enable);
+moqe_status moqe_gpu_bank_span_read(moqe_bank_t bank, double* total_us, int64_t* launches);
+
 /* Device event trace of the decode path (diagnostics; off by default).
  * trace(bank, 1) allocates, per SM, 512 slots of two u64: slots 0..255 for the
  * fc1 kernel, 256..511 for fc2. In each half, the first and last slot hold

@@ -49,6 +49,18 @@ struct Workspace {
     uint8_t* xr = nullptr;         // decode GEMV: fc1 row blocks (k_xrows)
     uint8_t* xb = nullptr;         // decode GEMV: fc2 row blocks (fc1 epilogue -> fc2)
     unsigned* ready = nullptr;     // decode GEMV, fused grid: fc1 m-tiles done per pass
+    // decode path (dec.cu), fixed size: kDecMaxRows routed rows
+    void* dblock = nullptr;
+    int4* d_units = nullptr;
+    int* d_nunits = nullptr;
+    int32_t* d_perm_token = nullptr;
+    float* d_perm_gate = nullptr;
+    int32_t* d_row_of = nullptr;
+    __half* d_xperm = nullptr;
+    long long* d_acc = nullptr;
+    unsigned* d_unit_done = nullptr;
+    float* d_ybuf = nullptr;
+    unsigned* d_tok_cnt = nullptr;
 };
 
 struct moqe_bank {
@@ -67,6 +79,10 @@ struct moqe_bank {
     int wg_finite = 0;
     float* smax1 = nullptr;  // [E] fc2 fixed-point bound constants (decode GEMV)
     float* bmax1 = nullptr;
+    uint8_t* wdec = nullptr;  // decode layout (dec_build_layout), d_model <= 1024 only
+    int64_t wdec_stride = 0, dec_slice = 0;
+    DecSpan* spans = nullptr;  // [2] router / expert-FFN launch spans (moqe_gpu_bank_span)
+    bool span_on = false;
     int num_sms = 148;
     int device = 0;
     cudaStream_t host_stream = nullptr;
@@ -90,6 +106,10 @@ int route_dbg() {  // diagnostics only
 }
 bool gemv_fused() {  // MOQE_GEMV_FUSED=0: decode as two grids (fc1, fc2) even when one would do
     static const bool v = [] { const char* s = getenv("MOQE_GEMV_FUSED"); return !(s && atoi(s) == 0); }();
+    return v;
+}
+bool dec_enabled() {  // MOQE_DEC=0: decode batches take the round-1 GEMV path instead
+    static const bool v = [] { const char* s = getenv("MOQE_DEC"); return !(s && atoi(s) == 0); }();
     return v;
 }
 bool xrows_in_router() {  // MOQE_XROWS_IN_ROUTER=0: decode keeps the separate k_xrows launch
@@ -189,6 +209,31 @@ moqe_status ensure_workspace(moqe_bank* b, int64_t T, int topk) {
     return MOQE_OK;
 }
 
+moqe_status ensure_dec_workspace(moqe_bank* b) {
+    Workspace& w = b->ws;
+    if (w.dblock) return MOQE_OK;
+    const int64_t R = kDecMaxRows, xpitch = int64_t(b->Kp1) * 2 + 16;
+    int64_t bytes = 0;
+    auto add = [&](int64_t n) { int64_t o = bytes; bytes += round_up(std::max<int64_t>(n, 1), 256); return o; };
+    const int64_t o_units = add(16 * R), o_nu = add(16), o_pt = add(4 * R), o_pg = add(4 * R), o_ro = add(4 * R),
+                  o_x = add(xpitch * R), o_acc = add(8 * R * b->Np2), o_ud = add(4 * R), o_yb = add(4 * R * b->d),
+                  o_tc = add(4 * R);
+    MOQE_CUDA(cudaMalloc(&w.dblock, bytes));
+    MOQE_CUDA(cudaMemset(w.dblock, 0, bytes));
+    char* p = static_cast<char*>(w.dblock);
+    w.d_units = reinterpret_cast<int4*>(p + o_units);
+    w.d_nunits = reinterpret_cast<int*>(p + o_nu);
+    w.d_perm_token = reinterpret_cast<int32_t*>(p + o_pt);
+    w.d_perm_gate = reinterpret_cast<float*>(p + o_pg);
+    w.d_row_of = reinterpret_cast<int32_t*>(p + o_ro);
+    w.d_xperm = reinterpret_cast<__half*>(p + o_x);
+    w.d_acc = reinterpret_cast<long long*>(p + o_acc);
+    w.d_unit_done = reinterpret_cast<unsigned*>(p + o_ud);
+    w.d_ybuf = reinterpret_cast<float*>(p + o_yb);
+    w.d_tok_cnt = reinterpret_cast<unsigned*>(p + o_tc);
+    return MOQE_OK;
+}
+
 void free_bank(moqe_bank* b) {
     if (!b) return;
     cudaFree(b->w1);
@@ -202,6 +247,9 @@ void free_bank(moqe_bank* b) {
     cudaFree(b->smax1);
     cudaFree(b->bmax1);
     cudaFree(b->ws.block);
+    cudaFree(b->ws.dblock);
+    cudaFree(b->wdec);
+    cudaFree(b->spans);
     cudaFree(b->h_dev);
     cudaFree(b->o_dev);
     cudaFree(b->trace);
@@ -298,6 +346,20 @@ moqe_status moqe_gpu_bank_create(int n_experts, int64_t d_model, int64_t d_ffn, 
                 cudaSuccess)
                 break;
         }
+        if (b->Kp1 <= 1024 && b->Np2 <= 1024) {
+            b->dec_slice = dec_slice_bytes(bits, b->Kp1, b->Np2);
+            b->wdec_stride = b->dec_slice * (b->Np1 / 64);
+            if ((ce = cudaMalloc(&b->wdec, b->wdec_stride * n_experts)) != cudaSuccess) break;
+            if ((ce = dec_build_layout(b->w1, b->w2, b->w1_stride, b->w2_stride, n_experts, b->Kp1, b->Np1, b->Np2,
+                                       bits, b->wdec, nullptr)) != cudaSuccess)
+                break;
+        }
+        if ((ce = cudaMalloc(&b->spans, 2 * sizeof(DecSpan))) != cudaSuccess) break;
+        {
+            DecSpan z[2];
+            for (auto& x : z) { x.start_min = ~0ull; x.ticket = x.pad = 0; x.total_ns = x.count = 0; }
+            if ((ce = cudaMemcpy(b->spans, z, sizeof(z), cudaMemcpyHostToDevice)) != cudaSuccess) break;
+        }
         if ((ce = cudaDeviceSynchronize()) != cudaSuccess) break;
     } while (false);
     if (stage) cudaFree(stage);
@@ -354,6 +416,55 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
     if (!h || !out) return fail(MOQE_INVALID_ARGUMENT, "moe_forward: null buffer");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     (void)cudaGetLastError();  // launch checks below must not see a stale error from unrelated calls
+    if (!pre && b->wdec && dec_enabled() && (path == MOQE_PATH_AUTO || path == MOQE_PATH_GEMV) &&
+        dec_supported(t, top_k, int(b->d), b->E, b->Kp1, b->Np1, b->Np2)) {
+        moqe_status s = ensure_dec_workspace(b);
+        if (s != MOQE_OK) return s;
+        s = ensure_workspace(b, t, top_k);  // routing outputs when the caller passes none
+        if (s != MOQE_OK) return s;
+        Workspace& w = b->ws;
+        DecArgs a{};
+        a.h = h;
+        a.h_f16 = h_dtype == MOQE_F16;
+        a.T = int(t);
+        a.d = int(b->d);
+        a.wg = wg;
+        a.E = b->E;
+        a.topk = top_k;
+        a.bits = b->bits;
+        a.expert = expert_out ? expert_out : w.P.expert;
+        a.gate = gate_out ? gate_out : w.P.gate;
+        a.units = w.d_units;
+        a.n_units = w.d_nunits;
+        a.perm_token = w.d_perm_token;
+        a.perm_gate = w.d_perm_gate;
+        a.row_of = w.d_row_of;
+        a.xperm = w.d_xperm;
+        a.xpitch = b->Kp1 * 2 + 16;
+        a.Kp1 = b->Kp1;
+        a.Np1 = b->Np1;
+        a.Np2 = b->Np2;
+        a.S = b->Np1 / 64;
+        a.wdec = b->wdec;
+        a.wdec_stride = b->wdec_stride;
+        a.slice_bytes = b->dec_slice;
+        a.s1 = b->s1;
+        a.b1 = b->b1;
+        a.s2 = b->s2;
+        a.b2 = b->b2;
+        a.acc = w.d_acc;
+        a.unit_done = w.d_unit_done;
+        a.ybuf = w.d_ybuf;
+        a.tok_cnt = w.d_tok_cnt;
+        a.out = out;
+        a.out_f16 = out_dtype == MOQE_F16;
+        a.span_route = b->span_on ? b->spans : nullptr;
+        a.span_ffn = b->span_on ? b->spans + 1 : nullptr;
+        a.trace = b->trace;
+        cudaError_t ce = launch_dec(b->bits, a, st, b->num_sms);
+        if (ce != cudaSuccess) return cuda_fail(ce, "k_dec");
+        return MOQE_OK;
+    }
     moqe_status s = ensure_workspace(b, t, top_k);
     if (s != MOQE_OK) return s;
     Workspace& w = b->ws;
@@ -495,6 +606,28 @@ int64_t moqe_gpu_bank_trace_read(moqe_bank_t b, uint64_t* out, int64_t cap) {
         cudaMemset(b->trace, 0, sizeof(uint64_t) * n);
     }
     return n;
+}
+
+moqe_status moqe_gpu_bank_span(moqe_bank_t b, int enable) {
+    if (!b) return fail(MOQE_INVALID_ARGUMENT, "span: null bank");
+    b->span_on = enable != 0;
+    return MOQE_OK;
+}
+
+moqe_status moqe_gpu_bank_span_read(moqe_bank_t b, double* total_us, int64_t* launches) {
+    if (!b) return fail(MOQE_INVALID_ARGUMENT, "span: null bank");
+    MOQE_CUDA(cudaDeviceSynchronize());
+    DecSpan sp[2];
+    MOQE_CUDA(cudaMemcpy(sp, b->spans, sizeof(sp), cudaMemcpyDeviceToHost));
+    for (int k = 0; k < 2; ++k) {
+        if (total_us) total_us[k] = double(sp[k].total_ns) * 1e-3;
+        if (launches) launches[k] = int64_t(sp[k].count);
+        sp[k].total_ns = sp[k].count = 0;
+        sp[k].start_min = ~0ull;
+        sp[k].ticket = 0;
+    }
+    MOQE_CUDA(cudaMemcpy(b->spans, sp, sizeof(sp), cudaMemcpyHostToDevice));
+    return MOQE_OK;
 }
 
 moqe_status moqe_gpu_bank_profile(moqe_bank_t b, int enable) {

@@ -1,0 +1,1094 @@
+// dec.cu — decode path (T*k <= 64 routed rows, d_model <= 1024): two launches.
+//
+//   k_dec_route  one thread-block cluster. Each CTA owns a slice of d_model: it stages its
+//                rows of Wg (before the PDL wait, so the copy overlaps the previous grid) and
+//                its columns of h, and forms partial logits with FFMA; the partials are summed
+//                over DSMEM in CTA-rank order (a fixed order: deterministic). Each token's
+//                (expert, gate) is broadcast to every CTA, every CTA builds the same plan
+//                (stable expert-grouped row order, units of <= 16 rows) and writes its share
+//                of the permuted fp16 activation rows.
+//   k_dec<BITS>  persistent weight-streaming expert FFN, one CTA per SM. The work is the
+//                sequence (unit u, f-slice j) over every routed unit and the S = d_ffn/64
+//                slices of its expert; CTA c takes a contiguous range of it (stream-K).
+//                A slice is self-contained: fc1 for 64 channels (all of d_model) -> ReLU ->
+//                fp16 mid -> fc2 partial over those 64 k. fc2 partials accumulate in registers
+//                while the CTA stays on one unit and are flushed as 2^-24 fixed point with
+//                integer atomics (order-independent, so the sum is deterministic). The CTA
+//                whose flush completes a unit's S slices applies scale, bias and gate and
+//                stores the rows (top-2: the second finisher of a token adds the two slots).
+//                No grid-wide waits, so partial residency cannot deadlock.
+//
+// Reference path replaced: moqe::top1_route + moe_ffn_forward (proj/src/model.cpp:328-393);
+// top-2 renormalisation per BASELINE config 4 (oracle/moqe_oracle.c orc_route).
+// Numerics: logits in parallel FFMA order (north_star allows different routing for tokens
+// whose top-2 logit gap is < 1e-4); the reference's zero-activation skip is kept (a zero
+// activation never multiplies a weight). Codes x fp16 activations are exact products,
+// fp32 accumulation, scale in the epilogue, fp16 mid (as the prefill GEMM).
+#include <cuda_fp16.h>
+
+#include <algorithm>
+#include <type_traits>
+
+#include "codec.cuh"
+#include "kernels.cuh"
+
+namespace moqe_gpu {
+
+namespace {
+
+constexpr int kDecThreads = 256;     // router CTA
+constexpr int kMidPitch = 64 * 2 + 16;  // bytes per mid row (pitch = 16 mod 128: conflict-free LDS.128)
+constexpr float kFix = 16777216.0f;     // 2^24 fixed-point scale of the fc2 partials
+constexpr int kMaxRouteSmem = 200 * 1024;
+
+__device__ __forceinline__ void red_add_s64(long long* p, long long v) {
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ float ld_cluster_f32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+
+// ---- span profiler: first CTA's start (after the PDL wait) to the last CTA's exit ----
+__device__ __forceinline__ void span_begin(DecSpan* s) {
+    if (s) atomicMin(&s->start_min, gtime_ns());
+}
+__device__ __forceinline__ void span_end(DecSpan* s, unsigned nctas) {
+    if (!s) return;
+    const unsigned long long t = gtime_ns();
+    __threadfence();
+    if (atomicAdd(&s->ticket, 1u) == nctas - 1) {
+        __threadfence();
+        const unsigned long long t0 = atomicExch(&s->start_min, ~0ull);
+        if (t > t0) atomicAdd(&s->total_ns, t - t0);
+        atomicAdd(&s->count, 1ull);
+        s->ticket = 0;
+    }
+}
+
+// Strict '>' argmax with the reference's sequential semantics (model.cpp:339-341,
+// oracle argmax_excluding): ties -> lowest index, a NaN never wins unless it sits at the
+// scan's first index. Warp-wide; lane owns experts lane, lane+32, ...
+__device__ __forceinline__ int warp_argmax(const float* l, int E, int skip) {
+    const int lane = threadIdx.x & 31;
+    const int first = skip == 0 ? 1 : 0;
+    if (l[first] != l[first]) return first;  // NaN at the scan start stays the best
+    float bv = -__int_as_float(0x7f800000);
+    int bi = 1 << 30;
+    for (int e = lane; e < E; e += 32) {
+        const float v = l[e];
+        if (e == skip || v != v) continue;
+        if (bi == (1 << 30) || v > bv) { bv = v; bi = e; }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (oi != (1 << 30) && (bi == (1 << 30) || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; }
+    }
+    return bi == (1 << 30) ? first : bi;
+}
+
+}  // namespace
+
+// power of two of the codec field holding code position p (0..15) of a 16-code chunk
+// (codec.cuh / unpack_chunk_raw)
+__device__ __forceinline__ int dec_field_shift(int bits, int p) {
+    // one nibble per code pair (p / 2): int2 0,2,4,6,8,0,2,4; int3 0,3,0,3,6,6,0,3; int4 0,4,...
+    const uint32_t tab = bits == 2 ? 0x42086420u : bits == 3 ? 0x30663030u : bits == 4 ? 0x40404040u : 0u;
+    return int((tab >> (4 * (p >> 1))) & 0xFu);
+}
+
+// diagnostics: per-CTA event log (a.trace: [grid][kDecTrace][2] = (event, globaltimer ns)),
+// slots [base, base + 21) per role
+__device__ __forceinline__ void dec_trace(const DecArgs& a, int base, int& n, int ev) {
+    if (a.trace && n < 21) {
+        unsigned long long* p = a.trace + (size_t(blockIdx.x) * kDecTrace + base + n) * 2;
+        p[0] = unsigned(ev);
+        p[1] = gtime_ns();
+        ++n;
+    }
+}
+
+// router events: absolute slots after the FFN kernel's [grid][kDecTrace] block
+__device__ __forceinline__ void route_trace(const DecArgs& a, int rank, int& n, int ev) {
+    if (a.trace && n < 32 && threadIdx.x == 0) {
+        unsigned long long* p = a.trace + (size_t(160 + rank) * kDecTrace + n) * 2;
+        p[0] = unsigned(ev) | (static_cast<unsigned long long>(clock64()) << 8);
+        p[1] = gtime_ns();
+        ++n;
+    }
+}
+
+// =====================================================================================
+// Router + plan (one cluster)
+// =====================================================================================
+__global__ void __launch_bounds__(kDecThreads) k_dec_route(const DecArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int C = int(cluster_nctas());
+    const int rank = int(cta_rank());
+    const int T = a.T, E = a.E, K = a.topk, R = T * K, d = a.d;
+    const int rpc = ((d + C - 1) / C + 3) & ~3;  // rows of Wg per CTA (multiple of 4: 16-B aligned rows)
+    const int r0 = rank * rpc, nr = max(0, min(d, r0 + rpc) - r0);
+    const int Tp = (T + 7) & ~7;
+    const int ntile = (Tp / 8) * ((E + 31) / 32);               // 8-token x 32-expert output tiles
+    const int ks = ntile >= 8 ? 1 : (ntile >= 4 ? 2 : (ntile >= 2 ? 4 : 8));  // row splits per tile
+    float* wgs = reinterpret_cast<float*>(smem);                 // [rpc][E]
+    float* hsT = wgs + rpc * E;                                   // [rpc][Tp] (token-minor)
+    float* part = hsT + rpc * Tp;                                 // [ks][T][E], later per-warp logit rows
+    float* plog = part + max(ks * T * E, 8 * 256);                // [T][E]
+    int* ch_e = reinterpret_cast<int*>(plog + T * E);             // [64] (token, slot) choices
+    float* ch_g = reinterpret_cast<float*>(ch_e + 64);            // [64]
+    int* cnt = reinterpret_cast<int*>(ch_g + 64);                 // [E]
+    int* off = cnt + E;                                           // [E + 1] row offsets
+    int* ubase = off + E + 1;                                     // [E + 1] unit offsets
+    int* pos = ubase + E + 1;                                     // [64]
+    uint64_t* bar = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(pos + 64) + 15) & ~uintptr_t(15));
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    // Wg rows [r0, r0+nr) are contiguous (Wg is [d][E] row-major): one bulk copy, issued
+    // before the PDL wait (the gate weights are not produced by the previous grid).
+    const uint32_t wbytes = uint32_t(nr) * E * 4;
+    const bool bulk = (wbytes % 16 == 0) && ((reinterpret_cast<uintptr_t>(a.wg + size_t(r0) * E) & 15) == 0);
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (tid == 0 && bulk && nr > 0) {
+        mbar_arrive_expect_tx(bar, wbytes);
+        for (uint32_t o = 0; o < wbytes; o += 32768u)
+            bulk_g2s(reinterpret_cast<unsigned char*>(wgs) + o, reinterpret_cast<const unsigned char*>(a.wg + size_t(r0) * E) + o,
+                     min(32768u, wbytes - o), bar);
+    }
+    if (!bulk)
+        for (int i = tid; i < nr * E; i += kDecThreads) wgs[i] = a.wg[size_t(r0) * E + i];
+    pdl_trigger();
+    pdl_wait();
+    int rtr = 0;
+    route_trace(a, rank, rtr, 20);
+    span_begin(tid == 0 ? a.span_route : nullptr);
+    // token columns [r0, r0+nr) of h -> f32, transposed (8 consecutive tokens per LDS.128 pair).
+    // 8-column chunks with one vector load each (rows of fp16 h are 16-B aligned when d % 8 == 0)
+    const bool vec = a.h_f16 && (d % 8 == 0) && ((reinterpret_cast<uintptr_t>(a.h) & 15) == 0);
+    if (vec) {
+        const int nc = rpc / 4;  // 4-column units (rpc is a multiple of 4); load 8 when both halves exist
+        for (int i = tid; i < Tp * (nc / 2 + (nc & 1)); i += kDecThreads) {
+            const int per = nc / 2 + (nc & 1);
+            const int t = i / per, k = (i - t * per) * 8;
+            float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            if (t < T && k < nr) {
+                const __half* src = static_cast<const __half*>(a.h) + size_t(t) * d + r0 + k;
+                if (k + 8 <= nr) {
+                    const uint4 q = *reinterpret_cast<const uint4*>(src);
+                    const __half2* hp = reinterpret_cast<const __half2*>(&q);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float2 f = __half22float2(hp[e]);
+                        v[2 * e] = f.x;
+                        v[2 * e + 1] = f.y;
+                    }
+                } else {
+                    for (int e = 0; k + e < nr && e < 8; ++e) v[e] = __half2float(src[e]);
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                if (k + e < rpc) hsT[(k + e) * Tp + t] = v[e];
+        }
+    } else {
+        for (int i = tid; i < Tp * rpc; i += kDecThreads) {
+            const int t = i / rpc, k = i - t * rpc;
+            float v = 0.f;
+            if (t < T && k < nr) {
+                const size_t gi = size_t(t) * d + r0 + k;
+                v = a.h_f16 ? __half2float(static_cast<const __half*>(a.h)[gi]) : static_cast<const float*>(a.h)[gi];
+            }
+            hsT[k * Tp + t] = v;
+        }
+    }
+    route_trace(a, rank, rtr, 21);
+    if (bulk && nr > 0) mbar_wait(bar, 0);
+    route_trace(a, rank, rtr, 22);
+    // non-finite gate weights: keep the reference's zero-activation skip (0 * inf must not
+    // reach the sum, model.cpp:160); otherwise a plain FMA is the same sum
+    bool nonfinite = false;
+    for (int i = tid; i < nr * E; i += kDecThreads) nonfinite |= !isfinite(wgs[i]);
+    nonfinite = __syncthreads_or(nonfinite);
+    // partial logits: warp = (8-token x 32-expert tile, row split); lane = expert; 8 FMA chains
+    {
+        const int rps = (nr + ks - 1) / ks;
+        for (int wi = warp; wi < ntile * ks; wi += kDecThreads / 32) {
+            const int tile = wi / ks, sp = wi - tile * ks;
+            const int tb = tile % (Tp / 8), eg = tile / (Tp / 8);
+            const int e = eg * 32 + lane;
+            const int k0 = sp * rps, k1 = min(nr, k0 + rps);
+            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            if (e < E) {
+                if (!nonfinite) {
+#pragma unroll 4
+                    for (int k = k0; k < k1; ++k) {
+                        const float w = wgs[k * E + e];
+                        const float4 x0 = *reinterpret_cast<const float4*>(hsT + k * Tp + tb * 8);
+                        const float4 x1 = *reinterpret_cast<const float4*>(hsT + k * Tp + tb * 8 + 4);
+                        acc[0] = fmaf(x0.x, w, acc[0]); acc[1] = fmaf(x0.y, w, acc[1]);
+                        acc[2] = fmaf(x0.z, w, acc[2]); acc[3] = fmaf(x0.w, w, acc[3]);
+                        acc[4] = fmaf(x1.x, w, acc[4]); acc[5] = fmaf(x1.y, w, acc[5]);
+                        acc[6] = fmaf(x1.z, w, acc[6]); acc[7] = fmaf(x1.w, w, acc[7]);
+                    }
+                } else {
+                    for (int k = k0; k < k1; ++k) {
+                        const float w = wgs[k * E + e];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const float x = hsT[k * Tp + tb * 8 + i];
+                            if (x != 0.f) acc[i] = fmaf(x, w, acc[i]);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int t = tb * 8 + i;
+                    if (t < T) part[(sp * T + t) * E + e] = acc[i];
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (int o = tid; o < T * E; o += kDecThreads) {  // row splits summed in a fixed order
+        float v = part[o];
+        for (int sp = 1; sp < ks; ++sp) v += part[sp * T * E + o];
+        plog[o] = v;
+    }
+    route_trace(a, rank, rtr, 23);
+    cluster_sync();
+    route_trace(a, rank, rtr, 24);
+    // reduce partials in rank order; this CTA owns tokens t = rank, rank + C, ...
+    for (int t = rank + warp * C; t < T; t += C * (kDecThreads / 32)) {
+        float* lt = part + warp * 256;  // per-warp logit row (the partials are consumed)
+        for (int e = lane; e < E; e += 32) {
+            float v[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
+                if (c < C) v[c] = ld_cluster_f32(map_rank(plog + t * E + e, uint32_t(c)));
+            float s = v[0];
+#pragma unroll
+            for (int c = 1; c < 16; ++c)
+                if (c < C) s += v[c];
+            lt[e] = s;
+        }
+        __syncwarp();
+        const int b1 = warp_argmax(lt, E, -1);
+        int b2 = -1;
+        if (K == 2) b2 = warp_argmax(lt, E, b1);
+        float g1 = 1.f, g2 = 0.f;
+        if (K == 1) {
+            // softmax probability of the winner in double (model.cpp:214-227, :343)
+            double mx = -1e300;
+            for (int e = lane; e < E; e += 32)
+                if (double(lt[e]) > mx) mx = double(lt[e]);
+            for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            double s = 0.0;
+            for (int e = lane; e < E; e += 32) s += exp(double(lt[e]) - mx);
+            for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            g1 = float(double(float(exp(double(lt[b1]) - mx))) / s);
+        } else {
+            const double z = exp(double(lt[b2]) - double(lt[b1]));
+            g1 = float(1.0 / (1.0 + z));
+            g2 = float(z / (1.0 + z));
+        }
+        if (lane < C) {  // broadcast the choice to every CTA of the cluster
+            st_cluster_u32(map_rank(ch_e + t * K, uint32_t(lane)), uint32_t(b1));
+            st_cluster_u32(map_rank(ch_g + t * K, uint32_t(lane)), __float_as_uint(g1));
+            if (K == 2) {
+                st_cluster_u32(map_rank(ch_e + t * K + 1, uint32_t(lane)), uint32_t(b2));
+                st_cluster_u32(map_rank(ch_g + t * K + 1, uint32_t(lane)), __float_as_uint(g2));
+            }
+        }
+        if (lane == 0) {
+            a.expert[t * K] = b1;
+            a.gate[t * K] = g1;
+            if (K == 2) {
+                a.expert[t * K + 1] = b2;
+                a.gate[t * K + 1] = g2;
+            }
+        }
+        __syncwarp();
+    }
+    route_trace(a, rank, rtr, 23);
+    cluster_sync();
+    route_trace(a, rank, rtr, 24);
+    // every CTA builds the same plan: rows grouped by expert, ascending (token, slot) inside
+    for (int e = tid; e < E; e += kDecThreads) {
+        int c = 0;
+        for (int i = 0; i < R; ++i) c += ch_e[i] == e;
+        cnt[e] = c;
+    }
+    __syncthreads();
+    if (warp == 0) {  // exclusive scans of rows and of units (<= 16 rows each), E <= 256
+        const int per = (E + 31) / 32, e0 = lane * per;
+        int sr = 0, su = 0;
+        for (int e = e0; e < min(E, e0 + per); ++e) { sr += cnt[e]; su += (cnt[e] + kDecUnitRows - 1) / kDecUnitRows; }
+        int ir = sr, iu = su;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int vr = __shfl_up_sync(0xffffffffu, ir, o), vu = __shfl_up_sync(0xffffffffu, iu, o);
+            if (lane >= o) { ir += vr; iu += vu; }
+        }
+        int pr = ir - sr, pu = iu - su;
+        for (int e = e0; e < min(E, e0 + per); ++e) {
+            off[e] = pr;
+            ubase[e] = pu;
+            pr += cnt[e];
+            pu += (cnt[e] + kDecUnitRows - 1) / kDecUnitRows;
+        }
+        if (lane == 31) { off[E] = ir; ubase[E] = iu; }
+    }
+    __syncthreads();
+    for (int i = tid; i < R; i += kDecThreads) {
+        const int e = ch_e[i];
+        int r = 0;
+        for (int j = 0; j < i; ++j) r += ch_e[j] == e;
+        pos[i] = off[e] + r;
+    }
+    __syncthreads();
+    if (rank == 0) {
+        for (int i = tid; i < R; i += kDecThreads) {
+            a.perm_token[pos[i]] = i / K;
+            a.perm_gate[pos[i]] = ch_g[i];
+            a.row_of[i] = pos[i];
+        }
+        for (int e = tid; e < E; e += kDecThreads) {
+            const int n = cnt[e];
+            for (int p = 0; p * kDecUnitRows < n; ++p)
+                a.units[ubase[e] + p] = make_int4(e, off[e] + p * kDecUnitRows, min(kDecUnitRows, n - p * kDecUnitRows), 0);
+        }
+        if (tid == 0) *a.n_units = ubase[E];
+    }
+    route_trace(a, rank, rtr, 25);
+    // permuted fp16 rows (zero padded to Kp1), one warp per row, rows split over the CTAs.
+    // Value k is stored as fp16(x_k) * 2^-s(k mod 16) (the fc1 weight field's power of two,
+    // see unpack_chunk_raw) and Z = Sum_k (1024 + bias * 2^s) * stored_k goes behind the row.
+    const int bias = 1 << (a.bits - 1);
+    for (int i = rank + warp * C; i < R; i += C * (kDecThreads / 32)) {
+        const int t = i / K;
+        unsigned char* rowp = reinterpret_cast<unsigned char*>(a.xperm) + size_t(pos[i]) * a.xpitch;
+        double z = 0.0;
+        // 8 values per lane step: all loads of the row first, then scale / store / Z
+        for (int k0 = lane * 8; k0 < a.Kp1; k0 += 32 * 8) {
+            float v[8];
+            if (vec && k0 + 8 <= d) {
+                const uint4 q = __ldg(reinterpret_cast<const uint4*>(static_cast<const __half*>(a.h) + size_t(t) * d + k0));
+                const __half2* hp = reinterpret_cast<const __half2*>(&q);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 f = __half22float2(hp[e]);
+                    v[2 * e] = f.x;
+                    v[2 * e + 1] = f.y;
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const int k = k0 + e;
+                    const size_t gi = size_t(t) * d + k;
+                    v[e] = k >= d ? 0.f
+                                  : a.h_f16 ? __half2float(static_cast<const __half*>(a.h)[gi])
+                                            : __half2float(__float2half_rn(static_cast<const float*>(a.h)[gi]));
+                }
+            }
+            uint4 o;
+            __half2* op = reinterpret_cast<__half2*>(&o);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int sh = dec_field_shift(a.bits, (k0 + 2 * e) & 15);  // one shift per code pair
+                const __half2 hv = __floats2half2_rn(ldexpf(v[2 * e], -sh), ldexpf(v[2 * e + 1], -sh));
+                op[e] = hv;
+                const double m = 1024.0 + double(bias) * double(1 << sh);
+                z += m * (double(__low2float(hv)) + double(__high2float(hv)));
+            }
+            *reinterpret_cast<uint4*>(rowp + size_t(k0) * 2) = o;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+        if (lane == 0) *reinterpret_cast<float*>(rowp + a.Kp1 * 2) = float(z);
+    }
+    __syncthreads();
+    route_trace(a, rank, rtr, 26);
+    span_end(tid == 0 ? a.span_route : nullptr, gridDim.x);
+    cluster_sync();  // no CTA exits while a peer may still read its plog / write its choices
+}
+
+// =====================================================================================
+// Expert FFN, stream-K over (unit, f-slice)
+// =====================================================================================
+namespace {
+
+template <int BITS>
+struct DecGeom {
+    static constexpr int RB = 8 * BITS;  // tile-row bytes (64 codes)
+};
+
+// fc1 weights without the fp16 magic subtraction: pair p of a 16-code chunk becomes
+// (1024 + u * 2^s_p) exactly (codec.cuh field positions; u = code + 2^(bits-1)). The MMA's
+// B values carry 2^-s_k instead (the router writes x_k * 2^-s_k), so each product is
+// 1024 * 2^-s_k * x_k + u_k * x_k and Sum q_k x_k = acc - Z with the per-token constant
+// Z = Sum_k (1024 + bias * 2^s_k) * B_k (k_dec_route). No HFMA2, no constants.
+template <int BITS>
+__device__ __forceinline__ void unpack_chunk_raw(const uint8_t* row, int t, uint32_t (&o)[8]) {
+    const uint32_t mg = magic_reg();
+    if constexpr (BITS == 4) {
+        const uint2 w = *reinterpret_cast<const uint2*>(row + 8 * t);
+        const uint32_t ws[2] = {w.x, w.y};
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const uint32_t a = ws[q], a8 = ws[q] >> 8;
+            o[4 * q + 0] = lop_magic<0x000F000Fu>(a, mg);
+            o[4 * q + 1] = lop_magic<0x00F000F0u>(a, mg);
+            o[4 * q + 2] = lop_magic<0x000F000Fu>(a8, mg);
+            o[4 * q + 3] = lop_magic<0x00F000F0u>(a8, mg);
+        }
+    } else if constexpr (BITS == 2) {
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(row + 4 * t);
+        const uint32_t w10 = w >> 10;
+        o[0] = lop_magic<0x00030003u>(w, mg);
+        o[1] = lop_magic<0x000C000Cu>(w, mg);
+        o[2] = lop_magic<0x00300030u>(w, mg);
+        o[3] = lop_magic<0x00C000C0u>(w, mg);
+        o[4] = lop_magic<0x03000300u>(w, mg);
+        o[5] = lop_magic<0x00030003u>(w10, mg);
+        o[6] = lop_magic<0x000C000Cu>(w10, mg);
+        o[7] = lop_magic<0x00300030u>(w10, mg);
+    } else if constexpr (BITS == 3) {
+        const uint32_t A = *reinterpret_cast<const uint32_t*>(row + 4 * t);
+        const uint32_t B = *reinterpret_cast<const uint16_t*>(row + 16 + 2 * t);
+        const uint32_t A8 = A >> 8;
+        const uint32_t Bx = prmt(B, 0u, 0x4140u);  // (B.lo, 0, B.hi, 0)
+        o[0] = lop_magic<0x00070007u>(A, mg);
+        o[1] = lop_magic<0x00380038u>(A, mg);
+        o[2] = lop_magic<0x00070007u>(A8, mg);
+        o[3] = lop_magic<0x00380038u>(A8, mg);
+        o[4] = lop_magic<0x00C000C0u>(A, mg) | ((Bx << 2) & 0x01000100u);
+        o[5] = lop_magic<0x00C000C0u>(A8, mg) | ((Bx << 1) & 0x01000100u);
+        o[6] = lop_magic<0x00070007u>(Bx, mg);
+        o[7] = lop_magic<0x00380038u>(Bx, mg);
+    } else {  // 8
+        const uint4 w = *reinterpret_cast<const uint4*>(row + 16 * t);
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            o[2 * q] = prmt(ws[q], 0x64646464u, 0x4140u);
+            o[2 * q + 1] = prmt(ws[q], 0x64646464u, 0x4342u);
+        }
+    }
+}
+
+template <int BITS>
+constexpr int kBias = 1 << (BITS - 1);
+template <int BITS>
+__device__ __forceinline__ int field_shift_c(int p) {  // p = code position mod 16 (see dec_field_shift)
+    constexpr uint32_t tab = BITS == 2 ? 0x42086420u : BITS == 3 ? 0x30663030u : BITS == 4 ? 0x40404040u : 0u;
+    return int((tab >> (4 * ((p & 15) >> 1))) & 0xFu);
+}
+
+// ---- warp roles of k_dec -------------------------------------------------------------
+constexpr int kF1Warps = 8;   // fc1: (16-channel group of the slice's 64, half of Kp1) each
+constexpr int kF2Warps = 8;   // fc2: Np2 / 8 channels each, the slice's 64 k
+constexpr int kDecFfnWarps = kF1Warps + kF2Warps + 1;  // + the TMA producer
+
+// fc1 of one slice for one warp: channels gw*16 .. +15, k-tiles [p*KP, (p+1)*KP) of piece p.
+// Two accumulator sets (even / odd k-tiles) halve the HMMA dependency chain.
+template <int BITS, int KP, int NB>
+__device__ __forceinline__ void dec_fc1_piece(const unsigned char* piece, int kt0, int gw, int g, int t,
+                                              const unsigned char* xs, int xpitch, float (&ca)[2][4],
+                                              float (&cb)[2][4]) {
+    constexpr int RB = DecGeom<BITS>::RB;
+    const unsigned char* ra = piece + (gw * 16 + g) * RB;
+    const unsigned char* xr = xs + g * xpitch + kt0 * 128 + t * 32;
+#pragma unroll
+    for (int i = 0; i < KP; ++i) {
+        uint32_t oa[8], ob[8];
+        unpack_chunk_raw<BITS>(ra + i * 64 * RB, t, oa);
+        unpack_chunk_raw<BITS>(ra + i * 64 * RB + 8 * RB, t, ob);
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) {
+            float(&c)[4] = (i & 1) ? cb[nb] : ca[nb];
+            const uint4 x0 = *reinterpret_cast<const uint4*>(xr + i * 128 + nb * 8 * xpitch);
+            const uint4 x1 = *reinterpret_cast<const uint4*>(xr + i * 128 + nb * 8 * xpitch + 16);
+            mma_16816(c, oa[0], ob[0], oa[1], ob[1], x0.x, x0.y);
+            mma_16816(c, oa[2], ob[2], oa[3], ob[3], x0.z, x0.w);
+            mma_16816(c, oa[4], ob[4], oa[5], ob[5], x1.x, x1.y);
+            mma_16816(c, oa[6], ob[6], oa[7], ob[7], x1.z, x1.w);
+        }
+    }
+}
+
+// fc2 partial of one slice for one warp: QW channel groups starting at group q0 of a piece.
+// mid >= 0 (ReLU) makes a magic-offset trick accumulate a one-signed offset over the slices, so
+// fc2 converts exactly (codec.cuh unpack_chunk: LOP3 + HFMA2 per code pair).
+template <int BITS, int QW, int NB>
+__device__ __forceinline__ void dec_fc2_piece(const unsigned char* piece, int q0, int g, int t,
+                                              const unsigned char* mid, float (&c2)[QW][NB][4]) {
+    constexpr int RB = DecGeom<BITS>::RB;
+    uint4 m0[NB], m1[NB];
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+        const unsigned char* mr = mid + (nb * 8 + g) * kMidPitch + t * 32;
+        m0[nb] = *reinterpret_cast<const uint4*>(mr);
+        m1[nb] = *reinterpret_cast<const uint4*>(mr + 16);
+    }
+#pragma unroll
+    for (int q = 0; q < QW; ++q) {
+        const unsigned char* ra = piece + size_t((q0 + q) * 16 + g) * RB;
+        uint32_t oa[8], ob[8];
+        unpack_chunk<BITS>(ra, t, oa);
+        unpack_chunk<BITS>(ra + 8 * RB, t, ob);
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) {
+            mma_16816(c2[q][nb], oa[0], ob[0], oa[1], ob[1], m0[nb].x, m0[nb].y);
+            mma_16816(c2[q][nb], oa[2], ob[2], oa[3], ob[3], m0[nb].z, m0[nb].w);
+            mma_16816(c2[q][nb], oa[4], ob[4], oa[5], ob[5], m1[nb].x, m1[nb].y);
+            mma_16816(c2[q][nb], oa[6], ob[6], oa[7], ob[7], m1[nb].z, m1[nb].w);
+        }
+    }
+}
+
+}  // namespace
+
+// Warp-specialised stream-K decode FFN. Warps 0-3 (fc1) and 4-11 (fc2) work on different
+// slices at once: fc1 of slice n+1 overlaps fc2 of slice n through a double-buffered mid.
+// QN = Kp1 / 256, GQ = Np2 / 256, NP = pieces per weight part (2 for int8: smaller stages).
+template <int BITS, int QN, int GQ, int NP>
+__global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
+    constexpr int RB = DecGeom<BITS>::RB;
+    constexpr int Kt = 4 * QN;          // fc1 k-tiles
+    constexpr int KP = Kt / NP;         // k-tiles per W1 piece
+    constexpr int QW = 2 * GQ;          // fc2 groups per warp (Np2 / 16 / kF2Warps)
+    constexpr int KH = KP / 2;          // k-tiles per fc1 warp per piece
+    constexpr int WPP = kF2Warps / NP;  // fc2 warps per W2 piece
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int S = a.S, Np2 = a.Np2, d = a.d;
+    const uint32_t sb1 = a.stage_bytes, sb2 = a.stage2_bytes;
+    const int n1 = a.n_stages, n2 = a.n_stages2;
+    unsigned char* ring1 = smem;
+    unsigned char* ring2 = ring1 + size_t(n1) * sb1;
+    unsigned char* xsb = ring2 + size_t(n2) * sb2;                    // 2 x [16 rows][xpitch]
+    unsigned char* midb = xsb + 2 * size_t(kDecUnitRows) * a.xpitch;  // 2 x [16][kMidPitch]
+    float* z2b = reinterpret_cast<float*>(midb + 2 * kDecUnitRows * kMidPitch);  // [2][4 warps][16 cols]
+    float* redb = z2b + 2 * 64;                                                  // [2][4 groups][32][8]
+    uint64_t* full1 = reinterpret_cast<uint64_t*>(redb + 2 * 4 * 32 * 8);
+    uint64_t* empty1 = full1 + n1;
+    uint64_t* full2 = empty1 + n1;
+    uint64_t* empty2 = full2 + n2;
+    uint64_t* xfull = empty2 + n2;
+    uint64_t* xempty = xfull + 2;
+    uint64_t* mfull = xempty + 2;
+    uint64_t* mempty = mfull + 2;
+    int* flag = reinterpret_cast<int*>(mempty + 2);
+    int* comb = flag + 2;  // [kDecUnitRows] tokens to combine (top-2)
+
+    if (tid == 0) {
+        for (int s = 0; s < n1; ++s) {
+            mbar_init(full1 + s, 1);
+            mbar_init(empty1 + s, kF1Warps);
+        }
+        for (int s = 0; s < n2; ++s) {
+            mbar_init(full2 + s, 1);
+            mbar_init(empty2 + s, WPP);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(xfull + b, 1);
+            mbar_init(xempty + b, kF1Warps);
+            mbar_init(mfull + b, kF1Warps / 2);  // the epilogue warps (kh = 0)
+            mbar_init(mempty + b, kF2Warps);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    pdl_trigger();
+    pdl_wait();
+    if (tid == 0) span_begin(a.span_ffn);
+    const int U = *a.n_units;
+    const int W = U * S;
+    const int w0 = int((long long)W * blockIdx.x / gridDim.x), w1 = int((long long)W * (blockIdx.x + 1) / gridDim.x);
+    const int u0 = w0 / S, j0 = w0 - u0 * S;
+
+    if (warp == kF1Warps + kF2Warps) {
+        // ------------------------------ producer ------------------------------
+        if (lane == 0 && w0 < w1) {
+            const uint64_t pol = policy_evict_first();
+            int s1 = 0, s2 = 0, nu = 0, ntr = 0;
+            uint32_t p1 = 0, p2 = 0;
+            int u = u0, j = j0;
+            int4 un = a.units[u];
+            for (int w = w0; w < w1; ++w) {
+                if (w == w0 || j == 0) {
+                    if (w != w0) un = a.units[u];
+                    const int b = nu & 1;
+                    mbar_wait(xempty + b, ((nu >> 1) & 1) ^ 1);
+                    const uint32_t xb = uint32_t(un.z) * a.xpitch;
+                    mbar_arrive_expect_tx(xfull + b, xb);
+                    bulk_g2s(xsb + size_t(b) * kDecUnitRows * a.xpitch,
+                             reinterpret_cast<const unsigned char*>(a.xperm) + size_t(un.y) * a.xpitch, xb, xfull + b);
+                    ++nu;
+                }
+                const uint8_t* sl = a.wdec + size_t(un.x) * a.wdec_stride + size_t(j) * a.slice_bytes;
+                dec_trace(a, 42, ntr, 10);
+#pragma unroll
+                for (int p = 0; p < NP; ++p) {  // W1 pieces; the last one carries the slice's s1 / b1
+                    const uint32_t bytes = uint32_t(KP) * 64 * RB;
+                    const uint32_t extra = p == NP - 1 ? (a.b1 ? 512u : 256u) : 0u;
+                    mbar_wait(empty1 + s1, p1 ^ 1);
+                    mbar_arrive_expect_tx(full1 + s1, bytes + extra);
+                    unsigned char* dst = ring1 + size_t(s1) * sb1;
+                    bulk_g2s_hint(dst, sl + size_t(p) * bytes, bytes, full1 + s1, pol);
+                    if (p == NP - 1) {
+                        bulk_g2s(dst + sb1 - 512, a.s1 + size_t(un.x) * a.Np1 + j * 64, 256u, full1 + s1);
+                        if (a.b1) bulk_g2s(dst + sb1 - 256, a.b1 + size_t(un.x) * a.Np1 + j * 64, 256u, full1 + s1);
+                    }
+                    if (++s1 == n1) { s1 = 0; p1 ^= 1; }
+                }
+                dec_trace(a, 42, ntr, 11);
+#pragma unroll
+                for (int p = 0; p < NP; ++p) {  // W2 pieces
+                    const uint32_t bytes = uint32_t(Np2 / NP) * RB;
+                    mbar_wait(empty2 + s2, p2 ^ 1);
+                    mbar_arrive_expect_tx(full2 + s2, bytes);
+                    bulk_g2s_hint(ring2 + size_t(s2) * sb2, sl + size_t(Kt) * 64 * RB + size_t(p) * bytes, bytes,
+                                  full2 + s2, pol);
+                    if (++s2 == n2) { s2 = 0; p2 ^= 1; }
+                }
+                if (++j == S) { j = 0; ++u; }
+            }
+        }
+        return;
+    }
+
+    if (warp < kF1Warps) {
+        // ------------------------------ fc1 warps ------------------------------
+        const int gw = warp & 3, kh = warp >> 2;
+        int s1 = 0, nu = 0, n = 0, ntr = 0;
+        uint32_t p1 = 0;
+        int u = u0, j = j0;
+        int4 un = a.units[u];
+        const unsigned char* xs = xsb;
+        const bool has_b1 = a.b1 != nullptr;
+        for (int w = w0; w < w1; ++w, ++n) {
+            if (w == w0 || j == 0) {
+                if (w != w0) un = a.units[u];
+                const int b = nu & 1;
+                xs = xsb + size_t(b) * kDecUnitRows * a.xpitch;
+                mbar_wait(xfull + b, (nu >> 1) & 1);
+            }
+            const int NBr = un.z > 8 ? 2 : 1;
+            float ca[2][4], cb[2][4];
+#pragma unroll
+            for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) ca[nb][i] = cb[nb][i] = 0.f;
+            int sl1 = s1;
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                sl1 = s1;
+                mbar_wait(full1 + s1, p1);
+                if (lane == 0 && warp == 0) dec_trace(a, 0, ntr, 1);
+                const unsigned char* piece = ring1 + size_t(s1) * sb1 + size_t(kh * KH) * 64 * RB;
+                if (NBr == 1) dec_fc1_piece<BITS, KH, 1>(piece, p * KP + kh * KH, gw, g, t, xs, a.xpitch, ca, cb);
+                else dec_fc1_piece<BITS, KH, 2>(piece, p * KP + kh * KH, gw, g, t, xs, a.xpitch, ca, cb);
+                if (p < NP - 1 || kh == 1) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(empty1 + s1);
+                }
+                if (++s1 == n1) { s1 = 0; p1 ^= 1; }
+            }
+            // the K halves meet in smem (double-buffered by slice parity): kh = 1 hands over,
+            // kh = 0 adds (fixed order) and runs the epilogue
+            float* rw = redb + ((n & 1) * 4 + gw) * 32 * 8 + lane * 8;
+            if (kh == 1) {
+#pragma unroll
+                for (int nb = 0; nb < 2; ++nb)
+                    if (nb < NBr)
+                        *reinterpret_cast<float4*>(rw + nb * 4) =
+                            make_float4(ca[nb][0] + cb[nb][0], ca[nb][1] + cb[nb][1], ca[nb][2] + cb[nb][2], ca[nb][3] + cb[nb][3]);
+                named_bar_sync(3 + gw, 64);
+                if (++j == S) { j = 0; ++u; }
+                if (w + 1 == w1 || j == 0) {  // this CTA's run on the unit ends: release its rows
+                    if (lane == 0) mbar_arrive(xempty + (nu & 1));
+                    ++nu;
+                }
+                continue;
+            }
+            named_bar_sync(3 + gw, 64);
+#pragma unroll
+            for (int nb = 0; nb < 2; ++nb)
+                if (nb < NBr) {
+                    const float4 o = *reinterpret_cast<const float4*>(rw + nb * 4);
+                    ca[nb][0] += cb[nb][0]; ca[nb][1] += cb[nb][1]; ca[nb][2] += cb[nb][2]; ca[nb][3] += cb[nb][3];
+                    cb[nb][0] = o.x; cb[nb][1] = o.y; cb[nb][2] = o.z; cb[nb][3] = o.w;
+                }
+            // epilogue: (acc - Z) * s1 + b1 -> ReLU -> fp16 mid[n & 1]
+            const int mb = n & 1;
+            mbar_wait(mempty + mb, ((n >> 1) & 1) ^ 1);
+            unsigned char* mid = midb + mb * kDecUnitRows * kMidPitch;
+            const unsigned char* last = ring1 + size_t(sl1) * sb1;
+            const float* sc1 = reinterpret_cast<const float*>(last + sb1 - 512);
+            const float* bi1 = reinterpret_cast<const float*>(last + sb1 - 256);
+#pragma unroll
+            for (int nb = 0; nb < 2; ++nb) {
+                if (nb < NBr) {
+                    float z[2];
+#pragma unroll
+                    for (int lo = 0; lo < 2; ++lo)
+                        z[lo] = *reinterpret_cast<const float*>(xs + (nb * 8 + 2 * t + lo) * a.xpitch + QN * 512);
+#pragma unroll
+                    for (int hi = 0; hi < 2; ++hi) {
+                        const int ch = gw * 16 + g + 8 * hi;
+                        const float sc = sc1[ch], bi = has_b1 ? bi1[ch] : 0.f;
+#pragma unroll
+                        for (int lo = 0; lo < 2; ++lo) {
+                            const int i = hi * 2 + lo;
+                            float v = ((ca[nb][i] + cb[nb][i]) - z[lo]) * sc + bi;
+                            v = v > 0.f ? v : 0.f;  // ReLU (model.cpp:189-191)
+                            *reinterpret_cast<__half*>(mid + (nb * 8 + 2 * t + lo) * kMidPitch + ch * 2) = __float2half_rn(v);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(mfull + mb);
+                mbar_arrive(empty1 + sl1);  // last W1 piece (and its scales) consumed
+                if (gw == 0) dec_trace(a, 0, ntr, 2);
+            }
+            if (++j == S) { j = 0; ++u; }
+            if (w + 1 == w1 || j == 0) {  // this CTA's run on the unit ends: release its rows
+                if (lane == 0) mbar_arrive(xempty + (nu & 1));
+                ++nu;
+            }
+        }
+        return;
+    }
+
+    // ------------------------------ fc2 warps ------------------------------
+    constexpr int NT2 = kF2Warps * 32;
+    const int v = warp - kF1Warps, tid2 = tid - kF1Warps * 32;
+    const int vp = v / WPP, q0 = (v % WPP) * QW;  // W2 piece of this warp, first group in it
+    int s2 = 0, n = 0, ntr = 0;
+    uint32_t p2 = 0;
+    int u = u0, j = j0;
+    int w = w0;
+    while (w < w1) {
+        // one run: this CTA's consecutive slices of unit u, accumulated in registers
+        const int4 un = a.units[u];
+        const int ulo = j, len = min(S - j, w1 - w);
+        long long* acc = a.acc + size_t(un.y) * Np2;
+        auto wait_slice = [&](int& myst) {
+            int st = s2;  // skip the W2 pieces of the other warps, wait for this warp's piece
+            uint32_t ph = p2;
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                if (p == vp) { st = s2; ph = p2; }
+                if (++s2 == n2) { s2 = 0; p2 ^= 1; }
+            }
+            myst = st;
+            mbar_wait(full2 + st, ph);
+            if (tid2 == 0) dec_trace(a, 21, ntr, 3);
+            mbar_wait(mfull + (n & 1), (n >> 1) & 1);
+            if (tid2 == 0) dec_trace(a, 21, ntr, 4);
+        };
+        auto release_slice = [&](int myst) {
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(empty2 + myst);
+                mbar_arrive(mempty + (n & 1));
+            }
+        };
+        if (un.z <= 8) {
+            // <= 8 rows: the run's fc2 partials stay in registers, one flush at the end
+            float c2[QW][1][4];
+#pragma unroll
+            for (int q = 0; q < QW; ++q)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) c2[q][0][i] = 0.f;
+            for (int r = 0; r < len; ++r, ++n) {
+                int myst;
+                wait_slice(myst);
+                dec_fc2_piece<BITS, QW, 1>(ring2 + size_t(myst) * sb2, q0, g, t, midb + (n & 1) * kDecUnitRows * kMidPitch, c2);
+                release_slice(myst);
+            }
+#pragma unroll
+            for (int q = 0; q < QW; ++q) {
+                const int gi = vp * (QW * WPP) + q0 + q;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int col = 2 * t + (i & 1);
+                    const int ch = gi * 16 + g + 8 * (i >> 1);
+                    if (col < un.z) red_add_s64(acc + size_t(col) * Np2 + ch, __float2ll_rn(c2[q][0][i] * kFix));
+                }
+            }
+        } else {
+            // 9..16 rows: flush every slice, QW/2 groups at a time (bounded registers)
+            constexpr int QH = QW / 2 > 0 ? QW / 2 : 1;
+            for (int r = 0; r < len; ++r, ++n) {
+                int myst;
+                wait_slice(myst);
+#pragma unroll
+                for (int hb = 0; hb < QW / QH; ++hb) {
+                    float c2[QH][2][4];
+#pragma unroll
+                    for (int q = 0; q < QH; ++q)
+#pragma unroll
+                        for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) c2[q][nb][i] = 0.f;
+                    dec_fc2_piece<BITS, QH, 2>(ring2 + size_t(myst) * sb2, q0 + hb * QH, g, t,
+                                               midb + (n & 1) * kDecUnitRows * kMidPitch, c2);
+#pragma unroll
+                    for (int q = 0; q < QH; ++q) {
+                        const int gi = vp * (QW * WPP) + q0 + hb * QH + q;
+#pragma unroll
+                        for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                const int col = nb * 8 + 2 * t + (i & 1);
+                                const int ch = gi * 16 + g + 8 * (i >> 1);
+                                if (col < un.z)
+                                    red_add_s64(acc + size_t(col) * Np2 + ch, __float2ll_rn(c2[q][nb][i] * kFix));
+                            }
+                    }
+                }
+                release_slice(myst);
+            }
+        }
+        const int uu = u, ju = j + len - 1;
+        w += len;
+        j += len;
+        if (j == S) { j = 0; ++u; }
+        {
+            __threadfence();
+            named_bar_sync(2, NT2);
+            if (tid2 == 0) {
+                const unsigned mine = unsigned(ju + 1 - ulo);
+                const unsigned old = atomicAdd(a.unit_done + uu, mine);
+                const int fin = old + mine == unsigned(S);
+                if (fin) a.unit_done[uu] = 0;
+                flag[0] = fin;
+                __threadfence();
+            }
+            named_bar_sync(2, NT2);
+            if (tid2 == 0) dec_trace(a, 21, ntr, 5);
+            if (flag[0]) {
+                // final epilogue of the unit: y = s2 * acc * 2^-24 + b2, gated (model.cpp:385-390)
+                const float* s2p = a.s2 + size_t(un.x) * Np2;
+                const float* b2p = a.b2 ? a.b2 + size_t(un.x) * Np2 : nullptr;
+                for (int idx = tid2; idx < un.z * d; idx += NT2) {
+                    const int r = idx / d, ch = idx - r * d;
+                    long long* ap = acc + size_t(r) * Np2 + ch;
+                    const long long vv = __ldcg(ap);
+                    *ap = 0;  // self-cleaning for the next forward
+                    float y = float(vv) * (1.0f / kFix) * s2p[ch];
+                    if (b2p) y = y + b2p[ch];
+                    const int row = un.y + r;
+                    const float gy = a.perm_gate[row] * y;
+                    if (a.topk == 1) {
+                        const size_t o = size_t(a.perm_token[row]) * d + ch;
+                        if (a.out_f16) static_cast<__half*>(a.out)[o] = __float2half_rn(gy);
+                        else static_cast<float*>(a.out)[o] = gy;
+                    } else {
+                        a.ybuf[size_t(row) * d + ch] = gy;
+                    }
+                }
+                if (a.topk == 2) {
+                    __threadfence();
+                    named_bar_sync(2, NT2);
+                    if (tid2 < un.z) {
+                        const int tok = a.perm_token[un.y + tid2];
+                        const unsigned old = atomicAdd(a.tok_cnt + tok, 1u);
+                        comb[tid2] = old == 1 ? tok : -1;
+                        if (old == 1) a.tok_cnt[tok] = 0;
+                        __threadfence();
+                    }
+                    named_bar_sync(2, NT2);
+                    for (int idx = tid2; idx < un.z * d; idx += NT2) {
+                        const int r = idx / d, ch = idx - r * d;
+                        const int tok = comb[r];
+                        if (tok < 0) continue;
+                        // o = g0*y0; o = o + g1*y1 (slot order, like the oracle's combine)
+                        const float y0 = __ldcg(a.ybuf + size_t(a.row_of[2 * tok]) * d + ch);
+                        const float y1 = __ldcg(a.ybuf + size_t(a.row_of[2 * tok + 1]) * d + ch);
+                        const float o = y0 + y1;
+                        const size_t oi = size_t(tok) * d + ch;
+                        if (a.out_f16) static_cast<__half*>(a.out)[oi] = __float2half_rn(o);
+                        else static_cast<float*>(a.out)[oi] = o;
+                    }
+                }
+                named_bar_sync(2, NT2);
+            }
+        }
+    }
+    named_bar_sync(2, NT2);
+    if (tid2 == 0) span_end(a.span_ffn, gridDim.x);
+}
+
+// Bank layout for the decode kernel: per expert, per 64-channel f-slice j, contiguous
+// [W1 part: Kp1/64 k-tiles x 64 channel rows][W2 part: Np2/128 x 128 channel rows] of
+// tile rows (64 codes each, the codec of codec.cuh), copied from the tiled bank.
+__global__ void k_dec_layout(const uint8_t* __restrict__ w1, const uint8_t* __restrict__ w2, int64_t w1_stride,
+                             int64_t w2_stride, int Kp1, int Np1, int Np2, int bits, uint8_t* __restrict__ out,
+                             int64_t out_stride, int64_t slice_bytes) {
+    const int e = blockIdx.z, j = blockIdx.y;
+    const int RB = 8 * bits, Kt = Kp1 / 64, Kt2 = Np1 / 64;
+    const int tb = 128 * RB;
+    const int nblk = Kt + Np2 / 128;  // Kt half-tiles of W1, Np2/128 tiles of W2
+    for (int b = blockIdx.x; b < nblk; b += gridDim.x) {
+        const uint8_t* src;
+        uint8_t* dst = out + size_t(e) * out_stride + size_t(j) * slice_bytes;
+        int bytes;
+        if (b < Kt) {  // W1 tile (nt = j/2, kb = b), rows (j%2)*64 .. +63
+            src = w1 + size_t(e) * w1_stride + (size_t(j / 2) * Kt + b) * tb + (j & 1) * 64 * RB;
+            dst += size_t(b) * 64 * RB;
+            bytes = 64 * RB;
+        } else {  // W2 tile (nt = b - Kt, kb = j)
+            const int nt = b - Kt;
+            src = w2 + size_t(e) * w2_stride + (size_t(nt) * Kt2 + j) * tb;
+            dst += size_t(Kt) * 64 * RB + size_t(nt) * tb;
+            bytes = tb;
+        }
+        for (int i = threadIdx.x * 16; i < bytes; i += blockDim.x * 16)
+            *reinterpret_cast<uint4*>(dst + i) = *reinterpret_cast<const uint4*>(src + i);
+    }
+}
+
+// =====================================================================================
+// host side
+// =====================================================================================
+namespace {
+constexpr int kMaxDev = 64;
+
+int route_cluster(int d, int E) {
+    return (int64_t(((d + 7) / 8 + 3) & ~3) * E * 4 <= 64 * 1024) ? 8 : 16;
+}
+size_t route_smem(int T, int d, int E, int C) {
+    const int rpc = ((d + C - 1) / C + 3) & ~3;
+    const int Tp = (T + 7) & ~7;
+    const int ntile = (Tp / 8) * ((E + 31) / 32);
+    const int ks = ntile >= 8 ? 1 : (ntile >= 4 ? 2 : (ntile >= 2 ? 4 : 8));
+    size_t s = size_t(rpc) * E * 4 + size_t(rpc) * Tp * 4 + size_t(std::max(ks * T * E, 8 * 256)) * 4 +
+               size_t(T) * E * 4;
+    s += 64 * 4 * 2 + size_t(3 * E + 2 + 64) * 4 + 32;
+    return s;
+}
+}  // namespace
+
+int64_t dec_slice_bytes(int bits, int Kp1, int Np2) { return int64_t(Kp1 + Np2) * 8 * bits; }
+
+bool dec_supported(int64_t T, int topk, int d, int E, int Kp1, int Np1, int Np2) {
+    if (T * topk > kDecMaxRows || T < 1) return false;
+    // compile-time warp tiling: fc1 k-tiles a multiple of 4 (Kp1 in {256, 512, 768, 1024}),
+    // fc2 channel groups a multiple of 16 (Np2 in {256, 512, 768, 1024})
+    if (Kp1 > 1024 || Kp1 % 256 || Np2 > 1024 || Np2 % 256 || Np1 % 64 || E > 256) return false;
+    const int C = route_cluster(d, E);
+    return route_smem(int(T), d, E, C) <= size_t(kMaxRouteSmem);
+}
+
+cudaError_t dec_build_layout(const uint8_t* w1, const uint8_t* w2, int64_t w1_stride, int64_t w2_stride, int E,
+                             int Kp1, int Np1, int Np2, int bits, uint8_t* out, cudaStream_t st) {
+    const int64_t sb = dec_slice_bytes(bits, Kp1, Np2);
+    dim3 grid(8, Np1 / 64, E);
+    k_dec_layout<<<grid, 256, 0, st>>>(w1, w2, w1_stride, w2_stride, Kp1, Np1, Np2, bits, out, sb * (Np1 / 64), sb);
+    return cudaGetLastError();
+}
+
+template <int BITS, int QN, int GQ, int NP>
+static cudaError_t launch_dec_t(const DecArgs& a, cudaStream_t st, int num_sms, size_t smem) {
+    static bool configured[kMaxDev] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto kern = k_dec<BITS, QN, GQ, NP>;
+    if (dev < kMaxDev && !configured[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(227 * 1024));
+        if (e != cudaSuccess) return e;
+        configured[dev] = true;
+    }
+    return launch_pdl(kern, dim3(num_sms), dim3(kDecFfnWarps * 32), smem, st, a);
+}
+
+template <int BITS, int QN>
+static cudaError_t launch_dec_q(const DecArgs& a, cudaStream_t st, int num_sms, size_t smem) {
+    constexpr int NP = BITS == 8 ? 2 : 1;
+    switch (a.Np2 / 256) {
+        case 1: return launch_dec_t<BITS, QN, 1, NP>(a, st, num_sms, smem);
+        case 2: return launch_dec_t<BITS, QN, 2, NP>(a, st, num_sms, smem);
+        case 3: return launch_dec_t<BITS, QN, 3, NP>(a, st, num_sms, smem);
+        case 4: return launch_dec_t<BITS, QN, 4, NP>(a, st, num_sms, smem);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <int BITS>
+static cudaError_t launch_dec_b(const DecArgs& a, cudaStream_t st, int num_sms, size_t smem) {
+    switch (a.Kp1 / 256) {
+        case 1: return launch_dec_q<BITS, 1>(a, st, num_sms, smem);
+        case 2: return launch_dec_q<BITS, 2>(a, st, num_sms, smem);
+        case 3: return launch_dec_q<BITS, 3>(a, st, num_sms, smem);
+        case 4: return launch_dec_q<BITS, 4>(a, st, num_sms, smem);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_dec(int bits, const DecArgs& a0, cudaStream_t st, int num_sms) {
+    DecArgs a = a0;
+    // ---- router (one cluster) ----
+    const int C = route_cluster(a.d, a.E);
+    const size_t rs = route_smem(int(a.T), a.d, a.E, C);
+    {
+        static bool configured[kMaxDev] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < kMaxDev && !configured[dev]) {
+            cudaError_t e = cudaFuncSetAttribute(k_dec_route, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxRouteSmem);
+            if (e != cudaSuccess) return e;
+            e = cudaFuncSetAttribute(k_dec_route, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            if (e != cudaSuccess) return e;
+            configured[dev] = true;
+        }
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(C);
+        cfg.blockDim = dim3(kDecThreads);
+        cfg.dynamicSmemBytes = rs;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[2];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = C;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 2;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, k_dec_route, a);
+        if (e != cudaSuccess) return e;
+    }
+    // ---- expert FFN ----
+    const int RB = 8 * bits, NP = bits == 8 ? 2 : 1;
+    a.stage_bytes = uint32_t(a.Kp1 / NP) * RB + 512;  // W1 piece + the slice's fc1 scales / biases
+    a.stage2_bytes = uint32_t(a.Np2 / NP) * RB;
+    const size_t fixed = 2 * size_t(kDecUnitRows) * a.xpitch + 2 * kDecUnitRows * kMidPitch + 512 + 512 + 2 * 4 * 32 * 8 * 4;
+    const size_t budget = 227 * 1024 - fixed;
+    // stages split evenly between the W1 and W2 rings (both parts have the same bytes)
+    const int pairs = int(std::min<size_t>(8, budget / (a.stage_bytes + a.stage2_bytes + 32)));
+    if (pairs < 2) return cudaErrorInvalidConfiguration;
+    a.n_stages = a.n_stages2 = pairs;
+    const size_t smem = size_t(pairs) * (a.stage_bytes + a.stage2_bytes) + fixed + size_t(pairs) * 32;
+    switch (bits) {
+        case 2: return launch_dec_b<2>(a, st, num_sms, smem);
+        case 3: return launch_dec_b<3>(a, st, num_sms, smem);
+        case 4: return launch_dec_b<4>(a, st, num_sms, smem);
+        case 8: return launch_dec_b<8>(a, st, num_sms, smem);
+    }
+
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace moqe_gpu

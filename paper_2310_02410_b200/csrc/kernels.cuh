@@ -142,4 +142,54 @@ bool gemm_available();
 int gemm_block_n();
 cudaError_t launch_gemm(int bits, int phase, const GemmArgs& g, const Plan& P, cudaStream_t st, int num_sms);
 
+// Decode path (dec.cu): k_dec_route (one cluster: parallel-order logits, top-k, plan,
+// permuted fp16 rows) -> PDL -> k_dec<BITS> (stream-K over (unit, 64-channel f-slice)).
+constexpr int kDecMaxRows = 64;   // T * top_k handled by the decode path
+constexpr int kDecTrace = 64;
+constexpr int kDecUnitRows = 16;  // rows per unit (an expert with more rows has several units)
+struct DecSpan {                  // in-kernel launch span: first CTA start (after PDL wait) -> last CTA exit
+    unsigned long long start_min;
+    unsigned ticket, pad;
+    unsigned long long total_ns, count;
+};
+struct DecArgs {
+    const void* h;
+    int h_f16;
+    int T, d;
+    const float* wg;
+    int E, topk, bits;
+    int32_t* expert;       // [T*k] routing outputs
+    float* gate;
+    int4* units;           // [kDecMaxRows] {expert, first permuted row, rows, 0}
+    int* n_units;
+    int32_t* perm_token;   // [T*k] token of permuted row
+    float* perm_gate;      // [T*k]
+    int32_t* row_of;       // [T*k] permuted row of (token, slot)
+    __half* xperm;         // [T*k][xpitch bytes] fp16 rows * 2^-field shift, zero padded to Kp1; float Z behind
+    int xpitch;
+    int Kp1, Np1, Np2, S;  // S = Np1 / 64 f-slices
+    const uint8_t* wdec;   // decode bank layout (dec_build_layout)
+    int64_t wdec_stride, slice_bytes;
+    const float* s1;
+    const float* b1;
+    const float* s2;
+    const float* b2;
+    long long* acc;        // [T*k][Np2] fixed-point fc2 accumulators (zero between forwards)
+    unsigned* unit_done;   // [kDecMaxRows] (zero between forwards)
+    float* ybuf;           // [T*k][d] gated rows (top-2)
+    unsigned* tok_cnt;     // [T] (top-2; zero between forwards)
+    void* out;
+    int out_f16;
+    DecSpan* span_route;   // or null
+    DecSpan* span_ffn;     // or null
+    unsigned long long* trace;  // diagnostics: [grid][kDecTrace][2] (event, globaltimer ns) or null
+    uint32_t stage_bytes, stage2_bytes;  // set by launch_dec: W1 / W2 ring stage sizes
+    int n_stages, n_stages2;
+};
+bool dec_supported(int64_t T, int topk, int d, int E, int Kp1, int Np1, int Np2);
+int64_t dec_slice_bytes(int bits, int Kp1, int Np2);
+cudaError_t dec_build_layout(const uint8_t* w1, const uint8_t* w2, int64_t w1_stride, int64_t w2_stride, int E,
+                             int Kp1, int Np1, int Np2, int bits, uint8_t* out, cudaStream_t st);
+cudaError_t launch_dec(int bits, const DecArgs& a, cudaStream_t st, int num_sms);
+
 }  // namespace moqe_gpu

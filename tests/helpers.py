@@ -78,3 +78,24 @@ def sampled_moe_expected(orc, h, wg, top_k, tokens, expert_codes, ex_all, g_all,
             o = o + g[t, k] * ys[(i, k)]
         out[i] = o
     return out
+
+
+def check_routing(orc, h, wg, top_k, ex, g, gap_tol=1e-4, gate_rtol=1e-5):
+    """Routing parity (BASELINE.json north_star): expert ids equal the oracle's except for
+    tokens whose oracle top-(k+1) logit gap is below 1e-4 (the GPU sums the logits in a
+    parallel order); gates of the other tokens within gate_rtol."""
+    ex_o, g_o = orc.route(h, wg, top_k)
+    lg = orc.router_logits(h, wg)
+    top = -np.sort(-lg, axis=1)[:, : top_k + 1]
+    gap = np.min(top[:, :-1] - top[:, 1:], axis=1) if lg.shape[1] > top_k else np.full(len(h), np.inf)
+    sep = ~(gap < gap_tol)  # NaN gaps (non-finite logits) count as separated
+    ex = np.asarray(ex).reshape(ex_o.shape)
+    g = np.asarray(g, np.float64).reshape(g_o.shape)
+    bad = (ex != ex_o).reshape(len(ex_o), -1).any(axis=1) & sep
+    assert not bad.any(), ("routing differs on well-separated tokens", np.flatnonzero(bad)[:8])
+    gs = sep if g.ndim == 1 else sep[:, None]
+    with np.errstate(invalid="ignore", divide="ignore"):
+        rel = np.abs(g - g_o) / np.abs(g_o)
+    ok = (rel <= gate_rtol) | (g == g_o) | (np.isnan(g) & np.isnan(g_o)) | ~gs
+    assert ok.all(), ("gate mismatch", float(np.nanmax(np.where(gs, rel, 0))))
+    return ex_o, g_o

@@ -5,7 +5,7 @@ import math
 import numpy as np
 import pytest
 
-from helpers import fp16_valued
+from helpers import check_routing, fp16_valued
 
 pytestmark = pytest.mark.gpu
 
@@ -92,6 +92,5 @@ def test_decode_forward_routing_finite_and_nonfinite_bank_router(gpu, orc, topk,
             wg[5, 7] = -np.nan
         bank = gpu.ExpertBank.from_float(w1, w2, 4, router=_t(wg))
         _, ex, g = gpu.moe_ffn_forward(_t(h).half(), bank, top_k=topk, return_routing=True)
-        ex_o, g_o = orc.route(h, wg, topk)
-        assert np.array_equal(ex.cpu().numpy().reshape(ex_o.shape), ex_o)
-        assert np.allclose(g.cpu().numpy().reshape(g_o.shape), g_o, rtol=1e-6, atol=0)
+        # the decode forward sums logits in a parallel order: near-tie exemption (north_star)
+        check_routing(orc, h, wg, topk, ex.cpu().numpy(), g.cpu().numpy())
