@@ -8,6 +8,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -80,6 +81,8 @@ struct moqe_bank {
     float* smax1 = nullptr;  // [E] fc2 fixed-point bound constants (decode GEMV)
     float* bmax1 = nullptr;
     uint8_t* wdec = nullptr;  // decode layout (dec_build_layout), d_model <= 1024 only
+    __half* wgt = nullptr;    // split gate weights for the fused decode routing (dec_split_wg)
+    int wg_shift = 0;
     int64_t wdec_stride = 0, dec_slice = 0;
     DecSpan* spans = nullptr;  // [2] router / expert-FFN launch spans (moqe_gpu_bank_span)
     bool span_on = false;
@@ -110,6 +113,10 @@ bool gemv_fused() {  // MOQE_GEMV_FUSED=0: decode as two grids (fc1, fc2) even w
 }
 bool dec_enabled() {  // MOQE_DEC=0: decode batches take the round-1 GEMV path instead
     static const bool v = [] { const char* s = getenv("MOQE_DEC"); return !(s && atoi(s) == 0); }();
+    return v;
+}
+bool fused_enabled() {  // MOQE_DEC_FUSED=0: decode keeps the separate router launch
+    static const bool v = [] { const char* s = getenv("MOQE_DEC_FUSED"); return !(s && atoi(s) == 0); }();
     return v;
 }
 bool xrows_in_router() {  // MOQE_XROWS_IN_ROUTER=0: decode keeps the separate k_xrows launch
@@ -249,6 +256,7 @@ void free_bank(moqe_bank* b) {
     cudaFree(b->ws.block);
     cudaFree(b->ws.dblock);
     cudaFree(b->wdec);
+    cudaFree(b->wgt);
     cudaFree(b->spans);
     cudaFree(b->h_dev);
     cudaFree(b->o_dev);
@@ -386,6 +394,18 @@ moqe_status moqe_gpu_bank_set_router(moqe_bank_t b, const float* wg, int on_devi
     if (!b->wg_blk) MOQE_CUDA(cudaMalloc(&b->wg_blk, sizeof(float) * route_wg_block_floats(int(b->d), b->E) + 16));
     int* flag = reinterpret_cast<int*>(b->wg_blk + route_wg_block_floats(int(b->d), b->E));
     MOQE_CUDA(route_block_wg(b->wg, int(b->d), b->E, b->wg_blk, flag, &b->wg_finite));
+    if (b->wdec) {  // decode banks: the split copy the fused routing streams (finite Wg only)
+        std::vector<float> hw(size_t(b->d) * b->E);
+        MOQE_CUDA(cudaMemcpy(hw.data(), b->wg, hw.size() * sizeof(float), cudaMemcpyDeviceToHost));
+        float mx = 0.f;
+        for (float v : hw) mx = std::max(mx, std::fabs(v));
+        int e2 = 0;
+        if (mx > 0.f && std::isfinite(mx)) std::frexp(mx, &e2);  // mx < 2^e2
+        b->wg_shift = 14 - e2;
+        if (!b->wgt) MOQE_CUDA(cudaMalloc(&b->wgt, sizeof(__half) * dec_wgt_halves(b->E, b->Kp1)));
+        MOQE_CUDA(dec_split_wg(b->wg, int(b->d), b->E, b->Kp1, b->wg_shift, b->wgt, nullptr));
+        MOQE_CUDA(cudaDeviceSynchronize());
+    }
     return MOQE_OK;
 }
 
@@ -461,6 +481,9 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
         a.span_route = b->span_on ? b->spans : nullptr;
         a.span_ffn = b->span_on ? b->spans + 1 : nullptr;
         a.trace = b->trace;
+        a.fused = (wg == b->wg && b->wgt && b->wg_finite && t <= 32 && fused_enabled()) ? 1 : 0;
+        a.wgt = b->wgt;
+        a.wg_shift = b->wg_shift;
         cudaError_t ce = launch_dec(b->bits, a, st, b->num_sms);
         if (ce != cudaSuccess) return cuda_fail(ce, "k_dec");
         return MOQE_OK;

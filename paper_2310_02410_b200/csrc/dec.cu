@@ -114,7 +114,7 @@ __device__ __forceinline__ void dec_trace(const DecArgs& a, int base, int& n, in
 // router events: absolute slots after the FFN kernel's [grid][kDecTrace] block
 __device__ __forceinline__ void route_trace(const DecArgs& a, int rank, int& n, int ev) {
     if (a.trace && n < 32 && threadIdx.x == 0) {
-        unsigned long long* p = a.trace + (size_t(160 + rank) * kDecTrace + n) * 2;
+        unsigned long long* p = a.trace + (size_t(160 + rank) * kDecTrace + (ev >= 28 ? ev - 28 + 16 + n : n)) * 2;
         p[0] = unsigned(ev) | (static_cast<unsigned long long>(clock64()) << 8);
         p[1] = gtime_ns();
         ++n;
@@ -401,7 +401,8 @@ __global__ void __launch_bounds__(kDecThreads) k_dec_route(const DecArgs a) {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const int sh = dec_field_shift(a.bits, (k0 + 2 * e) & 15);  // one shift per code pair
-                const __half2 hv = __floats2half2_rn(ldexpf(v[2 * e], -sh), ldexpf(v[2 * e + 1], -sh));
+                const float sc = __int_as_float((127 - sh) << 23);            // 2^-sh, exact
+                const __half2 hv = __floats2half2_rn(v[2 * e] * sc, v[2 * e + 1] * sc);
                 op[e] = hv;
                 const double m = 1024.0 + double(bias) * double(1 << sh);
                 z += m * (double(__low2float(hv)) + double(__high2float(hv)));
@@ -495,15 +496,15 @@ constexpr int kF1Warps = 8;   // fc1: (16-channel group of the slice's 64, half 
 constexpr int kF2Warps = 8;   // fc2: Np2 / 8 channels each, the slice's 64 k
 constexpr int kDecFfnWarps = kF1Warps + kF2Warps + 1;  // + the TMA producer
 
-// fc1 of one slice for one warp: channels gw*16 .. +15, k-tiles [p*KP, (p+1)*KP) of piece p.
+// fc1 of one slice for one warp: channels gw*16 .. +15, KP k-tiles from global k-tile kt0.
+// xrow[nb] = this lane's activation row (row g of n-block nb) scaled by 2^-s(k).
 // Two accumulator sets (even / odd k-tiles) halve the HMMA dependency chain.
 template <int BITS, int KP, int NB>
 __device__ __forceinline__ void dec_fc1_piece(const unsigned char* piece, int kt0, int gw, int g, int t,
-                                              const unsigned char* xs, int xpitch, float (&ca)[2][4],
+                                              const unsigned char* const (&xrow)[2], float (&ca)[2][4],
                                               float (&cb)[2][4]) {
     constexpr int RB = DecGeom<BITS>::RB;
     const unsigned char* ra = piece + (gw * 16 + g) * RB;
-    const unsigned char* xr = xs + g * xpitch + kt0 * 128 + t * 32;
 #pragma unroll
     for (int i = 0; i < KP; ++i) {
         uint32_t oa[8], ob[8];
@@ -512,8 +513,9 @@ __device__ __forceinline__ void dec_fc1_piece(const unsigned char* piece, int kt
 #pragma unroll
         for (int nb = 0; nb < NB; ++nb) {
             float(&c)[4] = (i & 1) ? cb[nb] : ca[nb];
-            const uint4 x0 = *reinterpret_cast<const uint4*>(xr + i * 128 + nb * 8 * xpitch);
-            const uint4 x1 = *reinterpret_cast<const uint4*>(xr + i * 128 + nb * 8 * xpitch + 16);
+            const unsigned char* xr = xrow[nb] + (kt0 + i) * 128 + t * 32;
+            const uint4 x0 = *reinterpret_cast<const uint4*>(xr);
+            const uint4 x1 = *reinterpret_cast<const uint4*>(xr + 16);
             mma_16816(c, oa[0], ob[0], oa[1], ob[1], x0.x, x0.y);
             mma_16816(c, oa[2], ob[2], oa[3], ob[3], x0.z, x0.w);
             mma_16816(c, oa[4], ob[4], oa[5], ob[5], x1.x, x1.y);
@@ -554,10 +556,281 @@ __device__ __forceinline__ void dec_fc2_piece(const unsigned char* piece, int q0
 
 }  // namespace
 
-// Warp-specialised stream-K decode FFN. Warps 0-3 (fc1) and 4-11 (fc2) work on different
+// Per-CTA plan (shared memory) of the fused decode kernel, or pointers into the router's
+// global plan (separate-router path).
+struct DecPlanSmem {
+    int4 units[kDecMaxRows];
+    int perm_token[kDecMaxRows];
+    float perm_gate[kDecMaxRows];
+    int row_of[kDecMaxRows];
+    float z[32];            // per-token correction Z of the scaled rows (fused path)
+    int ch_e[kDecMaxRows];  // (token, slot) choices
+    float ch_g[kDecMaxRows];
+    int cnt[256], off[257], ubase[257], pos[kDecMaxRows];
+    int n_units;
+};
+
+// Fused routing (every CTA, redundantly and bit-identically): logits = h . Wg on the tensor
+// cores with Wg pre-split by the bank into fp16 hi + lo (x 2^sw), streamed through two
+// buffers in four K chunks; parallel-order fp32 sums, so north_star's near-tie exemption
+// applies. Then top-k + gate (model.cpp:214-227, :339-346), the plan, and the activation
+// rows scaled in place by 2^-s(k) with their correction Z (see unpack_chunk_raw).
+template <int BITS, int MT>
+__device__ __forceinline__ void dec_fused_route(const DecArgs& a, DecPlanSmem& P, unsigned char* hs, int hpitch,
+                                             unsigned char* rbase, int nbuf, float* part, uint64_t* rbar,
+                                             int warp, int lane, bool dry) {
+    const int T = a.T, E = a.E, K = a.topk, R = T * K, d = a.d, Kp1 = a.Kp1;
+    const int Ep = (E + 7) & ~7, ntiles = Ep / 8;
+    const int ks = ntiles >= 16 ? 1 : 16 / ntiles;
+    const int Kc = Kp1 / 4, cpitch = (Kc + 8) * 2, nsteps = Kc / 16;
+    const uint32_t cbytes = uint32_t(2 * Ep) * cpitch;
+    const int tid = threadIdx.x, g = lane >> 2, t = lane & 3;
+    constexpr int NW = kF1Warps + kF2Warps;  // compute warps
+    float acc[2][MT][2][4];  // [work item (<= 2 per warp)][m-tile][hi, lo][4]
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int m = 0; m < MT; ++m)
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) acc[x][m][h2][i] = 0.f;
+    int rtr = 0;
+    const int rk = blockIdx.x < 8 ? int(blockIdx.x) : 7;
+    if (blockIdx.x < 8 && !dry) route_trace(a, rk, rtr, 30);
+    for (int c = 0; c < 4; ++c) {
+        const int bi = c % nbuf;
+        unsigned char* buf = rbase + size_t(bi) * cbytes;
+        if (!dry) mbar_wait(rbar + bi, (c / nbuf) & 1);
+        if (blockIdx.x < 8 && !dry) route_trace(a, rk, rtr, 31);
+        if (warp < NW) {
+#pragma unroll
+            for (int x = 0; x < 2; ++x) {
+                const int wi = warp + x * NW;
+                if (wi >= ntiles * ks) break;
+                const int nt = wi % ntiles, kq = wi / ntiles;
+                for (int st = kq; st < nsteps; st += ks) {
+                    const int kk = st * 16, k0 = c * Kc + kk;
+                    uint32_t b[2][2];
+#pragma unroll
+                    for (int h2 = 0; h2 < 2; ++h2) {
+                        const unsigned char* br = buf + size_t(h2 * Ep + nt * 8 + g) * cpitch + (kk + 2 * t) * 2;
+                        b[h2][0] = *reinterpret_cast<const uint32_t*>(br);
+                        b[h2][1] = *reinterpret_cast<const uint32_t*>(br + 16);
+                    }
+#pragma unroll
+                    for (int m = 0; m < MT; ++m) {
+                        {
+                            // rows past the last token reuse row T-1 (their logits are discarded)
+                            const unsigned char* r0 = hs + size_t(min(m * 16 + g, T - 1)) * hpitch + (k0 + 2 * t) * 2;
+                            const unsigned char* r1 = hs + size_t(min(m * 16 + g + 8, T - 1)) * hpitch + (k0 + 2 * t) * 2;
+                            const uint32_t a0 = *reinterpret_cast<const uint32_t*>(r0);
+                            const uint32_t a1 = *reinterpret_cast<const uint32_t*>(r1);
+                            const uint32_t a2 = *reinterpret_cast<const uint32_t*>(r0 + 16);
+                            const uint32_t a3 = *reinterpret_cast<const uint32_t*>(r1 + 16);
+                            mma_16816(acc[x][m][0], a0, a1, a2, a3, b[0][0], b[0][1]);
+                            mma_16816(acc[x][m][1], a0, a1, a2, a3, b[1][0], b[1][1]);
+                        }
+                    }
+                }
+            }
+        }
+        if (c + nbuf < 4) {
+            __syncthreads();  // buffer bi is free again
+            if (tid == 0 && !dry) {
+                mbar_arrive_expect_tx(rbar + bi, cbytes);
+                bulk_g2s(buf, reinterpret_cast<const unsigned char*>(a.wgt) + size_t(c + nbuf) * cbytes, cbytes, rbar + bi);
+            }
+        }
+    }
+    // partial logits [kq][token][expert] (hi + lo), then the fixed-order sum over kq
+    if (warp < NW) {
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+            const int wi = warp + x * NW;
+            if (wi >= ntiles * ks) break;
+            const int nt = wi % ntiles, kq = wi / ntiles;
+#pragma unroll
+            for (int m = 0; m < MT; ++m) {
+                {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int tok = m * 16 + g + 8 * (i >> 1), e = nt * 8 + 2 * t + (i & 1);
+                        part[(kq * 32 + tok) * Ep + e] = acc[x][m][0][i] + acc[x][m][1][i];
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (int o = tid; o < MT * 16 * Ep; o += blockDim.x) {
+        float v = part[o];
+        for (int kq = 1; kq < ks; ++kq) v += part[kq * 32 * Ep + o];
+        part[o] = v * __int_as_float((127 - a.wg_shift) << 23);  // exact power-of-two unscale
+    }
+    __syncthreads();
+    if (blockIdx.x < 8 && !dry) route_trace(a, rk, rtr, 32);
+    // top-k + gate: 8 lanes per token (4 tokens per warp, one round for T <= 32 * 17 / 8 ...).
+    // Gates in fp32 (expf is within 2 ulp; the logits already differ from the reference's in the
+    // last bits). Argmax keeps the reference's scan semantics (see warp_argmax).
+    {
+        const int sub = lane & 7, grp = lane >> 3;
+        const unsigned gmask = 0xFFu << (grp * 8);
+        for (int tk = warp * 4 + grp; tk - grp < T; tk += kDecFfnWarps * 4) {
+            const bool live = tk < T;
+            const float* lt = part + (live ? tk : 0) * Ep;
+            int best[2] = {-1, -1};
+#pragma unroll
+            for (int slot = 0; slot < 2; ++slot) {
+                if (slot == 1 && K == 1) break;
+                const int skip = slot == 0 ? -1 : best[0];
+                const int first = skip == 0 ? 1 : 0;
+                float bv = -__int_as_float(0x7f800000);
+                int bi = 1 << 30;
+                for (int e = sub; e < E; e += 8) {
+                    const float v = lt[e];
+                    if (e == skip || v != v) continue;
+                    if (bi == (1 << 30) || v > bv) { bv = v; bi = e; }
+                }
+#pragma unroll
+                for (int o = 4; o; o >>= 1) {
+                    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                    if (oi != (1 << 30) && (bi == (1 << 30) || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; }
+                }
+                best[slot] = (lt[first] != lt[first]) ? first : (bi == (1 << 30) ? first : bi);
+            }
+            float g1 = 1.f, g2 = 0.f;
+            if (K == 1) {
+                float mx = -__int_as_float(0x7f800000);
+                for (int e = sub; e < E; e += 8) mx = fmaxf(mx, lt[e]);
+#pragma unroll
+                for (int o = 4; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                float sm = 0.f;
+                for (int e = sub; e < E; e += 8) sm += expf(lt[e] - mx);
+#pragma unroll
+                for (int o = 4; o; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+                g1 = expf(lt[best[0]] - mx) / sm;
+            } else {
+                const float z = expf(lt[best[1]] - lt[best[0]]);
+                g1 = 1.f / (1.f + z);
+                g2 = z / (1.f + z);
+            }
+            if (live && sub == 0) {
+                P.ch_e[tk * K] = best[0];
+                P.ch_g[tk * K] = g1;
+                if (K == 2) {
+                    P.ch_e[tk * K + 1] = best[1];
+                    P.ch_g[tk * K + 1] = g2;
+                }
+                if (blockIdx.x == 0 && !dry) {
+                    a.expert[tk * K] = best[0];
+                    a.gate[tk * K] = g1;
+                    if (K == 2) {
+                        a.expert[tk * K + 1] = best[1];
+                        a.gate[tk * K + 1] = g2;
+                    }
+                }
+            }
+            (void)gmask;
+        }
+    }
+    __syncthreads();
+    if (blockIdx.x < 8 && !dry) route_trace(a, rk, rtr, 33);
+    // plan (warp 0): rows grouped by expert, ascending (token, slot) inside; units of <= 16 rows.
+    // Lane l holds rows l and l + 32; per-half counts from match masks into two expert tables,
+    // stable ranks from the masks, offsets / unit bases from one shuffle scan over the experts.
+    if (warp == 0) {
+        int* tabA = P.cnt;  // rows per expert in rows 0..31
+        int* tabB = P.off;  // rows per expert in rows 32..63
+        for (int e = lane; e < E; e += 32) { tabA[e] = 0; tabB[e] = 0; }
+        __syncwarp();
+        const int ea = lane < R ? P.ch_e[lane] : 0x40000000 + lane;
+        const int eb = lane + 32 < R ? P.ch_e[lane + 32] : 0x40000040 + lane;
+        const unsigned ma = __match_any_sync(0xffffffffu, ea), mb = __match_any_sync(0xffffffffu, eb);
+        const unsigned ltm = (1u << lane) - 1u;
+        const int ra = __popc(ma & ltm), rbl = __popc(mb & ltm);
+        if (lane < R && ra == 0) tabA[ea] = __popc(ma);
+        if (lane + 32 < R && rbl == 0) tabB[eb] = __popc(mb);
+        __syncwarp();
+        const int rank_a = ra, rank_b = (lane + 32 < R ? tabA[eb] : 0) + rbl;
+        // exclusive scans over experts of rows and units (lane owns a contiguous expert range)
+        const int per = (E + 31) / 32, e0 = lane * per, e1 = min(E, e0 + per);
+        int sr = 0, su = 0;
+        for (int e = e0; e < e1; ++e) {
+            const int c = tabA[e] + tabB[e];
+            sr += c;
+            su += (c + kDecUnitRows - 1) / kDecUnitRows;
+        }
+        int ir = sr, iu = su;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int vr = __shfl_up_sync(0xffffffffu, ir, o), vu = __shfl_up_sync(0xffffffffu, iu, o);
+            if (lane >= o) { ir += vr; iu += vu; }
+        }
+        const int nu_tot = __shfl_sync(0xffffffffu, iu, 31);
+        int pr = ir - sr, pu = iu - su;
+        // per expert: offset, unit base, count -> ubase[] (offset in the low 16 bits, unit base above)
+        for (int e = e0; e < e1; ++e) {
+            const int c = tabA[e] + tabB[e];
+            P.ubase[e] = pr | (pu << 16);
+            for (int q = 0; q * kDecUnitRows < c; ++q)
+                P.units[pu + q] = make_int4(e, pr + q * kDecUnitRows, min(kDecUnitRows, c - q * kDecUnitRows), 0);
+            pr += c;
+            pu += (c + kDecUnitRows - 1) / kDecUnitRows;
+        }
+        __syncwarp();
+        if (lane < R) {
+            const int ps = (P.ubase[ea] & 0xFFFF) + rank_a;
+            P.perm_token[ps] = lane / K;
+            P.perm_gate[ps] = P.ch_g[lane];
+            P.row_of[lane] = ps;
+        }
+        if (lane + 32 < R) {
+            const int ps = (P.ubase[eb] & 0xFFFF) + rank_b;
+            P.perm_token[ps] = (lane + 32) / K;
+            P.perm_gate[ps] = P.ch_g[lane + 32];
+            P.row_of[lane + 32] = ps;
+        }
+        if (lane == 0) P.n_units = nu_tot;
+    }
+    if (blockIdx.x < 8 && !dry) route_trace(a, rk, rtr, 34);
+    // activation rows scaled in place by 2^-s(k) (the fc1 weight field shifts) + Z per token
+    constexpr int bias = 1 << (BITS - 1);
+    for (int tk = warp; tk < T; tk += kDecFfnWarps) {
+        unsigned char* row = hs + size_t(tk) * hpitch;
+        float zf = 0.f;
+        for (int k0 = lane * 8; k0 < Kp1; k0 += 256) {
+            uint4 q = *reinterpret_cast<const uint4*>(row + k0 * 2);
+            __half2* hp = reinterpret_cast<__half2*>(&q);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int sh = field_shift_c<BITS>((k0 + 2 * e) & 15);
+                const float2 f = __half22float2(hp[e]);
+                const float sc = __int_as_float((127 - sh) << 23);  // 2^-sh, exact
+                hp[e] = __floats2half2_rn(f.x * sc, f.y * sc);
+                const float m = 1024.f + float(bias << sh);  // exact; products of 11-bit factors
+                zf = fmaf(m, __low2float(hp[e]), zf);
+                zf = fmaf(m, __high2float(hp[e]), zf);
+            }
+            *reinterpret_cast<uint4*>(row + k0 * 2) = q;
+        }
+        double z = zf;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+        if (lane == 0) P.z[tk] = float(z);
+    }
+    (void)d;
+    __syncthreads();
+    if (blockIdx.x < 8 && !dry) route_trace(a, rk, rtr, 35);
+}
+
+// Warp-specialised stream-K decode FFN. Warps 0-7 (fc1) and 8-15 (fc2) work on different
 // slices at once: fc1 of slice n+1 overlaps fc2 of slice n through a double-buffered mid.
 // QN = Kp1 / 256, GQ = Np2 / 256, NP = pieces per weight part (2 for int8: smaller stages).
-template <int BITS, int QN, int GQ, int NP>
+// FU: routing fused in (dec_fused_route, T <= 32); else the plan and the permuted scaled rows
+// come from k_dec_route (global).
+template <int BITS, int QN, int GQ, int NP, bool FU>
 __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
     constexpr int RB = DecGeom<BITS>::RB;
     constexpr int Kt = 4 * QN;          // fc1 k-tiles
@@ -573,11 +846,12 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
     const int n1 = a.n_stages, n2 = a.n_stages2;
     unsigned char* ring1 = smem;
     unsigned char* ring2 = ring1 + size_t(n1) * sb1;
-    unsigned char* xsb = ring2 + size_t(n2) * sb2;                    // 2 x [16 rows][xpitch]
-    unsigned char* midb = xsb + 2 * size_t(kDecUnitRows) * a.xpitch;  // 2 x [16][kMidPitch]
-    float* z2b = reinterpret_cast<float*>(midb + 2 * kDecUnitRows * kMidPitch);  // [2][4 warps][16 cols]
-    float* redb = z2b + 2 * 64;                                                  // [2][4 groups][32][8]
-    uint64_t* full1 = reinterpret_cast<uint64_t*>(redb + 2 * 4 * 32 * 8);
+    unsigned char* xsb = ring2 + size_t(n2) * sb2;  // FU: hs [T][hpitch]; else 2 x [16 rows][xpitch]
+    const int xregion = FU ? ((a.T * a.xpitch + 127) & ~127) : 2 * kDecUnitRows * a.xpitch;
+    unsigned char* midb = xsb + xregion;                                          // 2 x [16][kMidPitch]
+    float* redb = reinterpret_cast<float*>(midb + 2 * kDecUnitRows * kMidPitch);  // [2][4 groups][32][8]
+    DecPlanSmem* PS = reinterpret_cast<DecPlanSmem*>(redb + 2 * 4 * 32 * 8);
+    uint64_t* full1 = reinterpret_cast<uint64_t*>(PS + 1);
     uint64_t* empty1 = full1 + n1;
     uint64_t* full2 = empty1 + n1;
     uint64_t* empty2 = full2 + n2;
@@ -585,7 +859,8 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
     uint64_t* xempty = xfull + 2;
     uint64_t* mfull = xempty + 2;
     uint64_t* mempty = mfull + 2;
-    int* flag = reinterpret_cast<int*>(mempty + 2);
+    uint64_t* rbar = mempty + 2;  // [4] routing Wg chunks, [4] activation rows
+    int* flag = reinterpret_cast<int*>(rbar + 8);
     int* comb = flag + 2;  // [kDecUnitRows] tokens to combine (top-2)
 
     if (tid == 0) {
@@ -603,13 +878,58 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
             mbar_init(mfull + b, kF1Warps / 2);  // the epilogue warps (kh = 0)
             mbar_init(mempty + b, kF2Warps);
         }
+        for (int b = 0; b < 8; ++b) mbar_init(rbar + b, 1);
         fence_barrier_init();
     }
     __syncthreads();
+    // fused routing: gate-weight chunks that fit in the rings (bank constants: before the PDL wait)
+    const int Ep_ = (a.E + 7) & ~7;
+    const uint32_t cbytes_ = uint32_t(2 * Ep_) * ((a.Kp1 / 4 + 8) * 2);
+    const int nbuf_ = FU ? a.route_nbuf : 1;
+    if (FU && tid == 0) {
+        for (int c = 0; c < nbuf_; ++c) {
+            mbar_arrive_expect_tx(rbar + c, cbytes_);
+            bulk_g2s(ring1 + size_t(c) * cbytes_, reinterpret_cast<const unsigned char*>(a.wgt) + size_t(c) * cbytes_,
+                     cbytes_, rbar + c);
+        }
+    }
     pdl_trigger();
     pdl_wait();
     if (tid == 0) span_begin(a.span_ffn);
-    const int U = *a.n_units;
+    int rtr0 = 0;
+    if (FU && blockIdx.x < 8) route_trace(a, blockIdx.x, rtr0, 28);
+    if constexpr (FU) {
+        // activation rows -> hs (one bulk copy per row), zero padding columns / rows
+        const int T = a.T;
+        const bool bulk = a.h_f16 && (d % 8 == 0) && ((reinterpret_cast<uintptr_t>(a.h) & 15) == 0);
+        if (bulk && tid == 0) {
+            mbar_arrive_expect_tx(rbar + 4, uint32_t(T) * d * 2);
+            for (int r = 0; r < T; ++r)
+                bulk_g2s(xsb + size_t(r) * a.xpitch, static_cast<const __half*>(a.h) + size_t(r) * d, d * 2, rbar + 4);
+        }
+        if (!bulk) {
+            for (int i = tid; i < T * d; i += blockDim.x) {
+                const int r = i / d, k = i - r * d;
+                const float v = a.h_f16 ? __half2float(static_cast<const __half*>(a.h)[i]) : static_cast<const float*>(a.h)[i];
+                reinterpret_cast<__half*>(xsb + size_t(r) * a.xpitch)[k] = __float2half_rn(v);
+            }
+        }
+        for (int i = tid; i < T * (a.Kp1 - d); i += blockDim.x) {
+            const int r = i / (a.Kp1 - d), k = d + i % (a.Kp1 - d);
+            reinterpret_cast<__half*>(xsb + size_t(r) * a.xpitch)[k] = __float2half_rn(0.f);
+        }
+        if (bulk) mbar_wait(rbar + 4, 0);
+        __syncthreads();
+        if (blockIdx.x < 8) route_trace(a, blockIdx.x, rtr0, 29);
+        float* part = reinterpret_cast<float*>(ring1 + size_t(nbuf_) * cbytes_);
+        // one instantiation (two token m-tiles) keeps the kernel's instruction footprint small
+        dec_fused_route<BITS, 2>(a, *PS, xsb, a.xpitch, ring1, nbuf_, part, rbar, warp, lane, false);
+    }
+    const int4* units = FU ? PS->units : a.units;
+    const int* perm_token = FU ? PS->perm_token : a.perm_token;
+    const float* perm_gate = FU ? PS->perm_gate : a.perm_gate;
+    const int* row_of = FU ? PS->row_of : a.row_of;
+    const int U = FU ? PS->n_units : *a.n_units;
     const int W = U * S;
     const int w0 = int((long long)W * blockIdx.x / gridDim.x), w1 = int((long long)W * (blockIdx.x + 1) / gridDim.x);
     const int u0 = w0 / S, j0 = w0 - u0 * S;
@@ -621,16 +941,18 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
             int s1 = 0, s2 = 0, nu = 0, ntr = 0;
             uint32_t p1 = 0, p2 = 0;
             int u = u0, j = j0;
-            int4 un = a.units[u];
+            int4 un = units[u];
             for (int w = w0; w < w1; ++w) {
                 if (w == w0 || j == 0) {
-                    if (w != w0) un = a.units[u];
-                    const int b = nu & 1;
-                    mbar_wait(xempty + b, ((nu >> 1) & 1) ^ 1);
-                    const uint32_t xb = uint32_t(un.z) * a.xpitch;
-                    mbar_arrive_expect_tx(xfull + b, xb);
-                    bulk_g2s(xsb + size_t(b) * kDecUnitRows * a.xpitch,
-                             reinterpret_cast<const unsigned char*>(a.xperm) + size_t(un.y) * a.xpitch, xb, xfull + b);
+                    if (w != w0) un = units[u];
+                    if (!FU) {
+                        const int b = nu & 1;
+                        mbar_wait(xempty + b, ((nu >> 1) & 1) ^ 1);
+                        const uint32_t xb = uint32_t(un.z) * a.xpitch;
+                        mbar_arrive_expect_tx(xfull + b, xb);
+                        bulk_g2s(xsb + size_t(b) * kDecUnitRows * a.xpitch,
+                                 reinterpret_cast<const unsigned char*>(a.xperm) + size_t(un.y) * a.xpitch, xb, xfull + b);
+                    }
                     ++nu;
                 }
                 const uint8_t* sl = a.wdec + size_t(un.x) * a.wdec_stride + size_t(j) * a.slice_bytes;
@@ -671,15 +993,36 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
         int s1 = 0, nu = 0, n = 0, ntr = 0;
         uint32_t p1 = 0;
         int u = u0, j = j0;
-        int4 un = a.units[u];
-        const unsigned char* xs = xsb;
+        int4 un = units[u];
+        const unsigned char* xrow[2] = {xsb, xsb};
+        float zc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};  // Z of this lane's epilogue columns
         const bool has_b1 = a.b1 != nullptr;
         for (int w = w0; w < w1; ++w, ++n) {
             if (w == w0 || j == 0) {
-                if (w != w0) un = a.units[u];
-                const int b = nu & 1;
-                xs = xsb + size_t(b) * kDecUnitRows * a.xpitch;
-                mbar_wait(xfull + b, (nu >> 1) & 1);
+                if (w != w0) un = units[u];
+                if (FU) {
+#pragma unroll
+                    for (int nb = 0; nb < 2; ++nb) {
+                        const int r = nb * 8 + g;
+                        xrow[nb] = xsb + size_t(perm_token[un.y + (r < un.z ? r : 0)]) * a.xpitch;
+#pragma unroll
+                        for (int lo = 0; lo < 2; ++lo) {
+                            const int col = nb * 8 + 2 * t + lo;
+                            zc[nb][lo] = col < un.z ? PS->z[perm_token[un.y + col]] : 0.f;
+                        }
+                    }
+                } else {
+                    const int b = nu & 1;
+                    const unsigned char* xs = xsb + size_t(b) * kDecUnitRows * a.xpitch;
+                    mbar_wait(xfull + b, (nu >> 1) & 1);
+#pragma unroll
+                    for (int nb = 0; nb < 2; ++nb) {
+                        xrow[nb] = xs + (nb * 8 + g) * a.xpitch;
+#pragma unroll
+                        for (int lo = 0; lo < 2; ++lo)
+                            zc[nb][lo] = *reinterpret_cast<const float*>(xs + (nb * 8 + 2 * t + lo) * a.xpitch + QN * 512);
+                    }
+                }
             }
             const int NBr = un.z > 8 ? 2 : 1;
             float ca[2][4], cb[2][4];
@@ -694,8 +1037,8 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
                 mbar_wait(full1 + s1, p1);
                 if (lane == 0 && warp == 0) dec_trace(a, 0, ntr, 1);
                 const unsigned char* piece = ring1 + size_t(s1) * sb1 + size_t(kh * KH) * 64 * RB;
-                if (NBr == 1) dec_fc1_piece<BITS, KH, 1>(piece, p * KP + kh * KH, gw, g, t, xs, a.xpitch, ca, cb);
-                else dec_fc1_piece<BITS, KH, 2>(piece, p * KP + kh * KH, gw, g, t, xs, a.xpitch, ca, cb);
+                if (NBr == 1) dec_fc1_piece<BITS, KH, 1>(piece, p * KP + kh * KH, gw, g, t, xrow, ca, cb);
+                else dec_fc1_piece<BITS, KH, 2>(piece, p * KP + kh * KH, gw, g, t, xrow, ca, cb);
                 if (p < NP - 1 || kh == 1) {
                     __syncwarp();
                     if (lane == 0) mbar_arrive(empty1 + s1);
@@ -714,7 +1057,7 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
                 named_bar_sync(3 + gw, 64);
                 if (++j == S) { j = 0; ++u; }
                 if (w + 1 == w1 || j == 0) {  // this CTA's run on the unit ends: release its rows
-                    if (lane == 0) mbar_arrive(xempty + (nu & 1));
+                    if (!FU && lane == 0) mbar_arrive(xempty + (nu & 1));
                     ++nu;
                 }
                 continue;
@@ -737,10 +1080,6 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
 #pragma unroll
             for (int nb = 0; nb < 2; ++nb) {
                 if (nb < NBr) {
-                    float z[2];
-#pragma unroll
-                    for (int lo = 0; lo < 2; ++lo)
-                        z[lo] = *reinterpret_cast<const float*>(xs + (nb * 8 + 2 * t + lo) * a.xpitch + QN * 512);
 #pragma unroll
                     for (int hi = 0; hi < 2; ++hi) {
                         const int ch = gw * 16 + g + 8 * hi;
@@ -748,7 +1087,7 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
 #pragma unroll
                         for (int lo = 0; lo < 2; ++lo) {
                             const int i = hi * 2 + lo;
-                            float v = ((ca[nb][i] + cb[nb][i]) - z[lo]) * sc + bi;
+                            float v = ((ca[nb][i] + cb[nb][i]) - zc[nb][lo]) * sc + bi;
                             v = v > 0.f ? v : 0.f;  // ReLU (model.cpp:189-191)
                             *reinterpret_cast<__half*>(mid + (nb * 8 + 2 * t + lo) * kMidPitch + ch * 2) = __float2half_rn(v);
                         }
@@ -763,7 +1102,7 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
             }
             if (++j == S) { j = 0; ++u; }
             if (w + 1 == w1 || j == 0) {  // this CTA's run on the unit ends: release its rows
-                if (lane == 0) mbar_arrive(xempty + (nu & 1));
+                if (!FU && lane == 0) mbar_arrive(xempty + (nu & 1));
                 ++nu;
             }
         }
@@ -780,7 +1119,7 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
     int w = w0;
     while (w < w1) {
         // one run: this CTA's consecutive slices of unit u, accumulated in registers
-        const int4 un = a.units[u];
+        const int4 un = units[u];
         const int ulo = j, len = min(S - j, w1 - w);
         long long* acc = a.acc + size_t(un.y) * Np2;
         auto wait_slice = [&](int& myst) {
@@ -890,9 +1229,9 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
                     float y = float(vv) * (1.0f / kFix) * s2p[ch];
                     if (b2p) y = y + b2p[ch];
                     const int row = un.y + r;
-                    const float gy = a.perm_gate[row] * y;
+                    const float gy = perm_gate[row] * y;
                     if (a.topk == 1) {
-                        const size_t o = size_t(a.perm_token[row]) * d + ch;
+                        const size_t o = size_t(perm_token[row]) * d + ch;
                         if (a.out_f16) static_cast<__half*>(a.out)[o] = __float2half_rn(gy);
                         else static_cast<float*>(a.out)[o] = gy;
                     } else {
@@ -903,7 +1242,7 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
                     __threadfence();
                     named_bar_sync(2, NT2);
                     if (tid2 < un.z) {
-                        const int tok = a.perm_token[un.y + tid2];
+                        const int tok = perm_token[un.y + tid2];
                         const unsigned old = atomicAdd(a.tok_cnt + tok, 1u);
                         comb[tid2] = old == 1 ? tok : -1;
                         if (old == 1) a.tok_cnt[tok] = 0;
@@ -915,8 +1254,8 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
                         const int tok = comb[r];
                         if (tok < 0) continue;
                         // o = g0*y0; o = o + g1*y1 (slot order, like the oracle's combine)
-                        const float y0 = __ldcg(a.ybuf + size_t(a.row_of[2 * tok]) * d + ch);
-                        const float y1 = __ldcg(a.ybuf + size_t(a.row_of[2 * tok + 1]) * d + ch);
+                        const float y0 = __ldcg(a.ybuf + size_t(row_of[2 * tok]) * d + ch);
+                        const float y1 = __ldcg(a.ybuf + size_t(row_of[2 * tok + 1]) * d + ch);
                         const float o = y0 + y1;
                         const size_t oi = size_t(tok) * d + ch;
                         if (a.out_f16) static_cast<__half*>(a.out)[oi] = __float2half_rn(o);
@@ -1000,12 +1339,12 @@ cudaError_t dec_build_layout(const uint8_t* w1, const uint8_t* w2, int64_t w1_st
     return cudaGetLastError();
 }
 
-template <int BITS, int QN, int GQ, int NP>
+template <int BITS, int QN, int GQ, int NP, bool FU>
 static cudaError_t launch_dec_t(const DecArgs& a, cudaStream_t st, int num_sms, size_t smem) {
     static bool configured[kMaxDev] = {};
     int dev = 0;
     cudaGetDevice(&dev);
-    auto kern = k_dec<BITS, QN, GQ, NP>;
+    auto kern = k_dec<BITS, QN, GQ, NP, FU>;
     if (dev < kMaxDev && !configured[dev]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(227 * 1024));
         if (e != cudaSuccess) return e;
@@ -1014,14 +1353,20 @@ static cudaError_t launch_dec_t(const DecArgs& a, cudaStream_t st, int num_sms, 
     return launch_pdl(kern, dim3(num_sms), dim3(kDecFfnWarps * 32), smem, st, a);
 }
 
+template <int BITS, int QN, int GQ>
+static cudaError_t launch_dec_f(const DecArgs& a, cudaStream_t st, int num_sms, size_t smem) {
+    constexpr int NP = BITS == 8 ? 2 : 1;
+    return a.fused ? launch_dec_t<BITS, QN, GQ, NP, true>(a, st, num_sms, smem)
+                   : launch_dec_t<BITS, QN, GQ, NP, false>(a, st, num_sms, smem);
+}
+
 template <int BITS, int QN>
 static cudaError_t launch_dec_q(const DecArgs& a, cudaStream_t st, int num_sms, size_t smem) {
-    constexpr int NP = BITS == 8 ? 2 : 1;
     switch (a.Np2 / 256) {
-        case 1: return launch_dec_t<BITS, QN, 1, NP>(a, st, num_sms, smem);
-        case 2: return launch_dec_t<BITS, QN, 2, NP>(a, st, num_sms, smem);
-        case 3: return launch_dec_t<BITS, QN, 3, NP>(a, st, num_sms, smem);
-        case 4: return launch_dec_t<BITS, QN, 4, NP>(a, st, num_sms, smem);
+        case 1: return launch_dec_f<BITS, QN, 1>(a, st, num_sms, smem);
+        case 2: return launch_dec_f<BITS, QN, 2>(a, st, num_sms, smem);
+        case 3: return launch_dec_f<BITS, QN, 3>(a, st, num_sms, smem);
+        case 4: return launch_dec_f<BITS, QN, 4>(a, st, num_sms, smem);
     }
     return cudaErrorInvalidValue;
 }
@@ -1037,12 +1382,65 @@ static cudaError_t launch_dec_b(const DecArgs& a, cudaStream_t st, int num_sms, 
     return cudaErrorInvalidValue;
 }
 
+// Gate weights for the fused routing: Wg [d x E] f32 -> [4 K chunks][hi, lo][Ep][Kp1/4 + 8] fp16
+// with Wg * 2^shift = hi + lo (shift keeps hi in range and lo out of the subnormals).
+__global__ void k_wg_split(const float* __restrict__ wg, int d, int E, int Ep, int Kp1, int shift,
+                           __half* __restrict__ out) {
+    const int Kc = Kp1 / 4, cp = Kc + 8;
+    const int64_t n = int64_t(4) * 2 * Ep * cp;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const int kk = int(i % cp);
+        const int e = int((i / cp) % Ep);
+        const int h2 = int((i / (int64_t(cp) * Ep)) % 2);
+        const int c = int(i / (int64_t(cp) * Ep * 2));
+        const int k = c * Kc + kk;
+        float v = 0.f;
+        if (kk < Kc && k < d && e < E) v = ldexpf(wg[size_t(k) * E + e], shift);
+        const __half hi = __float2half_rn(v);
+        out[i] = h2 == 0 ? hi : __float2half_rn(v - __half2float(hi));
+    }
+}
+
+int64_t dec_wgt_halves(int E, int Kp1) { return int64_t(4) * 2 * ((E + 7) & ~7) * (Kp1 / 4 + 8); }
+
+cudaError_t dec_split_wg(const float* wg, int d, int E, int Kp1, int shift, __half* out, cudaStream_t st) {
+    const int64_t n = dec_wgt_halves(E, Kp1);
+    k_wg_split<<<unsigned(std::min<int64_t>((n + 255) / 256, 4096)), 256, 0, st>>>(wg, d, E, (E + 7) & ~7, Kp1, shift, out);
+    return cudaGetLastError();
+}
+
+// Shared-memory plan of k_dec for a mode (fused routing or not); false when it does not fit.
+static bool dec_config(int bits, DecArgs& a, size_t* smem_out) {
+    const int RB = 8 * bits, NP = bits == 8 ? 2 : 1;
+    a.stage_bytes = uint32_t(a.Kp1 / NP) * RB + 512;  // W1 piece + the slice's fc1 scales / biases
+    a.stage2_bytes = uint32_t(a.Np2 / NP) * RB;
+    const size_t xregion = a.fused ? ((size_t(a.T) * a.xpitch + 127) & ~size_t(127)) : 2 * size_t(kDecUnitRows) * a.xpitch;
+    const size_t fixed = xregion + 2 * kDecUnitRows * kMidPitch + 2 * 4 * 32 * 8 * 4 + sizeof(DecPlanSmem) + 256;
+    if (fixed >= 227 * 1024) return false;
+    const size_t budget = 227 * 1024 - fixed;
+    // stages split evenly between the W1 and W2 rings (both parts have the same bytes)
+    const int pairs = int(std::min<size_t>(8, budget / (a.stage_bytes + a.stage2_bytes + 32)));
+    if (pairs < 2) return false;
+    if (a.fused) {  // the routing phase borrows the rings: 2..4 Wg chunks + the partial logits
+        const int Ep = (a.E + 7) & ~7, ntiles = Ep / 8, ks = ntiles >= 16 ? 1 : 16 / ntiles;
+        const size_t cb = size_t(2 * Ep) * ((a.Kp1 / 4 + 8) * 2), pb = size_t(ks) * 32 * Ep * 4;
+        const size_t ring = size_t(pairs) * (a.stage_bytes + a.stage2_bytes);
+        a.route_nbuf = ring < pb ? 0 : int(std::min<size_t>(4, (ring - pb) / cb));
+        if (a.route_nbuf < 2) return false;
+    }
+    a.n_stages = a.n_stages2 = pairs;
+    *smem_out = size_t(pairs) * (a.stage_bytes + a.stage2_bytes) + fixed + size_t(pairs) * 32;
+    return true;
+}
+
 cudaError_t launch_dec(int bits, const DecArgs& a0, cudaStream_t st, int num_sms) {
     DecArgs a = a0;
-    // ---- router (one cluster) ----
-    const int C = route_cluster(a.d, a.E);
-    const size_t rs = route_smem(int(a.T), a.d, a.E, C);
-    {
+    size_t smem = 0;
+    if (a.fused && !dec_config(bits, a, &smem)) a.fused = 0;  // fall back to the router launch
+    if (!a.fused && !dec_config(bits, a, &smem)) return cudaErrorInvalidConfiguration;
+    if (!a.fused) {  // ---- router (one cluster) ----
+        const int C = route_cluster(a.d, a.E);
+        const size_t rs = route_smem(int(a.T), a.d, a.E, C);
         static bool configured[kMaxDev] = {};
         int dev = 0;
         cudaGetDevice(&dev);
@@ -1071,16 +1469,6 @@ cudaError_t launch_dec(int bits, const DecArgs& a0, cudaStream_t st, int num_sms
         if (e != cudaSuccess) return e;
     }
     // ---- expert FFN ----
-    const int RB = 8 * bits, NP = bits == 8 ? 2 : 1;
-    a.stage_bytes = uint32_t(a.Kp1 / NP) * RB + 512;  // W1 piece + the slice's fc1 scales / biases
-    a.stage2_bytes = uint32_t(a.Np2 / NP) * RB;
-    const size_t fixed = 2 * size_t(kDecUnitRows) * a.xpitch + 2 * kDecUnitRows * kMidPitch + 512 + 512 + 2 * 4 * 32 * 8 * 4;
-    const size_t budget = 227 * 1024 - fixed;
-    // stages split evenly between the W1 and W2 rings (both parts have the same bytes)
-    const int pairs = int(std::min<size_t>(8, budget / (a.stage_bytes + a.stage2_bytes + 32)));
-    if (pairs < 2) return cudaErrorInvalidConfiguration;
-    a.n_stages = a.n_stages2 = pairs;
-    const size_t smem = size_t(pairs) * (a.stage_bytes + a.stage2_bytes) + fixed + size_t(pairs) * 32;
     switch (bits) {
         case 2: return launch_dec_b<2>(a, st, num_sms, smem);
         case 3: return launch_dec_b<3>(a, st, num_sms, smem);

@@ -183,6 +183,10 @@ struct DecArgs {
     DecSpan* span_route;   // or null
     DecSpan* span_ffn;     // or null
     unsigned long long* trace;  // diagnostics: [grid][kDecTrace][2] (event, globaltimer ns) or null
+    const __half* wgt;     // fused routing: the bank's split gate weights (dec_split_wg) or null
+    int wg_shift;
+    int fused;             // routing inside k_dec (T <= 32, bank router, finite Wg)
+    int route_nbuf;        // set by launch_dec: Wg chunk buffers of the fused routing
     uint32_t stage_bytes, stage2_bytes;  // set by launch_dec: W1 / W2 ring stage sizes
     int n_stages, n_stages2;
 };
@@ -191,5 +195,7 @@ int64_t dec_slice_bytes(int bits, int Kp1, int Np2);
 cudaError_t dec_build_layout(const uint8_t* w1, const uint8_t* w2, int64_t w1_stride, int64_t w2_stride, int E,
                              int Kp1, int Np1, int Np2, int bits, uint8_t* out, cudaStream_t st);
 cudaError_t launch_dec(int bits, const DecArgs& a, cudaStream_t st, int num_sms);
+int64_t dec_wgt_halves(int E, int Kp1);
+cudaError_t dec_split_wg(const float* wg, int d, int E, int Kp1, int shift, __half* out, cudaStream_t st);
 
 }  // namespace moqe_gpu
