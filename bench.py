@@ -136,7 +136,10 @@ class GpuLayer:
         self.touched, self.counts = touched, counts
 
 
-def build_gpu_layers(m, torch, E, d, f, bits, T, top_k, n_layers, dev):
+def build_gpu_layers(m, torch, E, d, f, bits, T, top_k, n_layers, dev, zipf=False):
+    """zipf: BASELINE config 5 popularity (bias folded into Wg[0,:] with h[:,0] = 1,
+    paper_2310_02410_b200.workloads.zipf_bias)."""
+    from paper_2310_02410_b200.workloads import zipf_bias
     layers = []
     w1n, w2n, wgn, rng = layer0_numpy(E, d, f)
     for li in range(n_layers):
@@ -151,6 +154,11 @@ def build_gpu_layers(m, torch, E, d, f, bits, T, top_k, n_layers, dev):
             w2 = torch.randn((E, f, d), generator=g, device=dev) * 0.02
             wg = torch.randn((d, E), generator=g, device=dev) * 0.02
             h = torch.randn((T, d), generator=g, device=dev).half()
+        if zipf:
+            wg = wg.clone()
+            wg[0, :] = torch.from_numpy(zipf_bias(wg.float().cpu().numpy())).to(dev)
+            h = h.clone()
+            h[:, 0] = 1.0
         bank = m.ExpertBank.from_float(w1, w2, bits, router=wg)
         del w1, w2
         _, ex, _ = m.moe_ffn_forward(h, bank, top_k=top_k, return_routing=True)
@@ -216,10 +224,40 @@ def time_steps(torch, fn, layers, steps, warmup, dist=None, graphs=True):
     return ms
 
 
+def profile_spans(m, torch, layers, steps, fwd):
+    """In-pipeline durations of the decode kernels, measured on the device (moqe_gpu_bank_span:
+    first CTA start after the programmatic-launch wait -> last CTA exit, summed by the kernel
+    itself), from a graph of one forward per layer replayed until >= `steps` forwards. No event
+    nodes, so the launch chain keeps its programmatic edges. Returns per kind (0 router, 1 expert
+    FFN incl. fused routing): (total us, launches)."""
+    import ctypes as C
+    lib = m.load_library()
+    for L in layers:
+        lib.moqe_gpu_bank_span(L.bank._h, 1)
+    g = capture(torch, fwd, layers, list(range(len(layers))))
+    for L in layers:
+        lib.moqe_gpu_bank_span(L.bank._h, 0)
+    tot = (C.c_double * 2)()
+    cnt = (C.c_int64 * 2)()
+    g.replay()
+    for L in layers:
+        lib.moqe_gpu_bank_span_read(L.bank._h, tot, cnt)  # discard the warm replay
+    us = np.zeros(2)
+    n = np.zeros(2, np.int64)
+    for _ in range(max(1, -(-steps // len(layers)))):
+        g.replay()
+    for L in layers:
+        lib.moqe_gpu_bank_span_read(L.bank._h, tot, cnt)
+        us += np.array(tot[:])
+        n += np.array(cnt[:])
+    del g
+    return us, n
+
+
 def profile_kernels(m, torch, layers, steps, fwd):
-    """Per-kernel CUDA-event durations on the launching stream: a graph of one
-    forward per layer with event nodes around every kernel, replayed until
-    >= `steps` steps have been measured."""
+    """Per-kernel CUDA-event durations on the launching stream (prefill kernels): a graph of one
+    forward per layer with event nodes around every kernel, replayed until >= `steps` steps have
+    been measured."""
     import ctypes as C
     lib = m.load_library()
     for L in layers:
@@ -254,8 +292,8 @@ KINDS = ["route", "scatter", "gemv", "gemm_fc1", "gemm_fc2", "convert"]
 
 
 def run_point(m, torch, E, d, f, bits, T, top_k, steps, warmup, dev, hbm_peak, tc_peak, dist=None,
-              n_layers=N_LAYERS, detail=False):
-    layers = build_gpu_layers(m, torch, E, d, f, bits, T, top_k, n_layers, dev)
+              n_layers=N_LAYERS, detail=False, zipf=False):
+    layers = build_gpu_layers(m, torch, E, d, f, bits, T, top_k, n_layers, dev, zipf=zipf)
     outs = [torch.empty((T, d), dtype=torch.float32, device=dev) for _ in layers]
 
     # reuse preallocated outputs to keep allocator traffic out of the loop
@@ -265,33 +303,59 @@ def run_point(m, torch, E, d, f, bits, T, top_k, steps, warmup, dev, hbm_peak, t
         m.moe_ffn_forward(L.h, L.bank, top_k=top_k, out=_o[id(L)])
 
     ms = time_steps(torch, fwd_out, layers, steps, warmup, dist)
-    prof_ms, prof_n, per_layer = profile_kernels(m, torch, layers, steps, fwd_out)
-    # dominant expert-FFN kernel (the path's hot loop; the router is reported in kernel_share)
-    ffn = [2, 3, 4]
-    dom = ffn[int(np.argmax(prof_ms[ffn]))]
-    avg_launch_ms = prof_ms[dom] / max(prof_n[dom], 1)
-    if KINDS[dom] == "gemv":
-        # bytes per launch averaged over the rotating layers (launch counts per layer)
-        tot_b = sum(kernel_bytes(L, d, f, bits, T, top_k) * n[2] for L, (_, n) in zip(layers, per_layer))
-        per_launch = tot_b / max(prof_n[2], 1)
-        achieved = per_launch / (avg_launch_ms * 1e-3) / 1e9
+    span_us, span_n = profile_spans(m, torch, layers, steps, fwd_out)
+    if span_n[1] > 0:
+        # decode path (dec.cu): one k_dec launch per forward (routing fused in, or behind the
+        # k_dec_route cluster); span = first CTA start after the PDL wait -> last CTA exit
+        avg_us = span_us[1] / span_n[1]
+        per_launch = float(np.mean([kernel_bytes(L, d, f, bits, T, top_k) + d * E * 4 for L in layers]))
+        achieved = per_launch / (avg_us * 1e-6) / 1e9
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(achieved / hbm_peak, 4), "traffic": None,
-                "kernel": "k_gemv fc1+fc2", "bytes_per_launch": int(per_launch),
-                "avg_launch_us": round(avg_launch_ms * 1e3, 3)}
+                "kernel": "k_dec (routing + expert FFN, one launch)" if span_n[0] == 0 else "k_dec expert FFN",
+                "bytes_per_launch": int(per_launch), "avg_launch_us": round(avg_us, 3),
+                "timing": "in-kernel globaltimer span (first CTA after PDL wait -> last CTA exit), inside the graph"}
+        if span_n[0] > 0:
+            roof["router_avg_us"] = round(span_us[0] / span_n[0], 3)
+        prof_ms = np.zeros(6)
+        prof_n = np.zeros(6, np.int64)
+        prof_ms[2] = span_us[1] * 1e-3
+        prof_n[2] = span_n[1]
+        if span_n[0] > 0:
+            prof_ms[0] = span_us[0] * 1e-3
+            prof_n[0] = span_n[0]
+        launches = (1 + (1 if span_n[0] > 0 else 0))
     else:
-        # each tcgen05 phase is half of the expert-FFN FLOPs (2*d*f*T*k per phase)
-        fl = 2 * d * f * T * top_k
-        achieved = fl / (avg_launch_ms * 1e-3) / 1e12
-        both_ms = (prof_ms[3] + prof_ms[4]) / max(prof_n[3], 1)
-        roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": tc_peak, "unit": "TFLOP/s",
-                "frac": round(achieved / tc_peak, 4), "traffic": None, "kernel": "k_ffn_gemm " + KINDS[dom],
-                "flops_per_launch": int(fl), "avg_launch_us": round(avg_launch_ms * 1e3, 3),
-                "fc1_plus_fc2_TFLOPs": round(2 * fl / (both_ms * 1e-3) / 1e12, 1)}
-    try:  # ncu-measured DRAM bytes per launch of this kernel/config (profiles/round1/traffic.json)
-        with open(os.path.join(ROOT, "profiles", "round1", "traffic.json")) as fh:
-            tr = json.load(fh).get(f"{roof['kernel']}/int{bits}/T{T}")
-        roof["traffic"] = tr
+        prof_ms, prof_n, per_layer = profile_kernels(m, torch, layers, steps, fwd_out)
+        # dominant expert-FFN kernel (the path's hot loop; the router is reported in kernel_share)
+        ffn = [2, 3, 4]
+        dom = ffn[int(np.argmax(prof_ms[ffn]))]
+        avg_launch_ms = prof_ms[dom] / max(prof_n[dom], 1)
+        if KINDS[dom] == "gemv":
+            tot_b = sum(kernel_bytes(L, d, f, bits, T, top_k) * n[2] for L, (_, n) in zip(layers, per_layer))
+            per_launch = tot_b / max(prof_n[2], 1)
+            achieved = per_launch / (avg_launch_ms * 1e-3) / 1e9
+            roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                    "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                    "kernel": "k_gemv fc1+fc2", "bytes_per_launch": int(per_launch),
+                    "avg_launch_us": round(avg_launch_ms * 1e3, 3)}
+        else:
+            # each tcgen05 phase is half of the expert-FFN FLOPs (2*d*f*T*k per phase)
+            fl = 2 * d * f * T * top_k
+            achieved = fl / (avg_launch_ms * 1e-3) / 1e12
+            both_ms = (prof_ms[3] + prof_ms[4]) / max(prof_n[3], 1)
+            roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": tc_peak, "unit": "TFLOP/s",
+                    "frac": round(achieved / tc_peak, 4), "traffic": None, "kernel": "k_ffn_gemm " + KINDS[dom],
+                    "flops_per_launch": int(fl), "avg_launch_us": round(avg_launch_ms * 1e3, 3),
+                    "fc1_plus_fc2_TFLOPs": round(2 * fl / (both_ms * 1e-3) / 1e12, 1),
+                    "timing": "CUDA event nodes around each kernel in the graph"}
+        launches = None
+    try:  # ncu-measured DRAM bytes per launch (dram__bytes_read+write.sum) of this kernel/config
+        with open(os.path.join(ROOT, "profiles", "round2", "traffic.json")) as fh:
+            tr = json.load(fh).get(f"int{bits}/T{T}/E{E}/k{top_k}")
+        if tr:
+            roof["traffic"] = tr["bytes_per_launch"]
+            roof["traffic_source"] = tr["source"]
     except Exception:
         pass
     touched = float(np.mean([L.touched for L in layers]))
@@ -307,8 +371,8 @@ def run_point(m, torch, E, d, f, bits, T, top_k, steps, warmup, dev, hbm_peak, t
         # kernels per forward: a "gemv" scope launches k_gemv (one fused fc1+fc2 grid for
         # decode batches of <= 64 routed rows, else fc1 + fc2) and is preceded by k_xrows
         # (token-row encoding, timed inside the "route" scope)
-        "launches_per_step": int(round((prof_n.sum() + gemv_extra(d, T, top_k) * prof_n[2]) /
-                                       max(1, -(-steps // len(layers)) * len(layers)))),
+        "launches_per_step": launches if launches is not None else
+        int(round((prof_n.sum() + gemv_extra(d, T, top_k) * prof_n[2]) / max(1, -(-steps // len(layers)) * len(layers)))),
     }
     return res, layers
 
@@ -324,6 +388,8 @@ def e2e_point(m, torch, layers, steps, warmup, top_k, d):
         i = idx[id(L)]
         m.moe_ffn_forward_host(hs[i], L.bank, top_k=top_k, out=outs[i])
 
+    for L in layers:  # every replica's first host call sizes its staging buffers: not timed
+        fn(L)
     ms = time_steps(torch, fn, layers, steps, warmup, graphs=False)
     return {"value": round(T / (ms * 1e-3), 1), "unit": "tokens/s",
             "h2d_bytes_per_step": int(T * d * 2), "d2h_bytes_per_step": int(T * d * 4),
@@ -360,39 +426,57 @@ def run_point_ep(m, torch, dist, E, d, f, bits, T, top_k, steps, warmup, dev, ra
 # ---------------------------------------------------------------------------------------
 # reference CPU arm
 
-def reference_baseline(E, d, f, bits, T, reps=3, threads=None):
-    """Time the reference moqe::moe_ffn_forward (oracle/_ref) on the host cores,
-    token-sharded over all threads (bit-identical to 1 thread)."""
+def reference_baseline(E, d, f, bits, T, reps=3, threads=None, one_thread=True):
+    """Time the reference moqe::moe_ffn_forward (oracle/_ref) on the host cores the way
+    BASELINE.md §2 / SURVEY.md §8(d) ask (bench.cpp:96-107 convention: 1 discarded warm-up,
+    median of `reps`): token-sharded over all host threads (bit-identical to 1 thread) and,
+    when one_thread, single-threaded as the reference runs. The one-time quantize-experts cost
+    (quantize_linear + pack of every expert matrix, 1 thread) is timed too."""
     import oracle
-    orc = oracle.orc()
     kind = "reference" if oracle.ref_available() else "port"
+    lib = oracle.ref() if kind == "reference" else oracle.orc()
+    orc = oracle.orc()
     w1, w2, wg, rng = layer0_numpy(E, d, f)
     h = tokens_numpy(rng, T, d).astype(np.float32)
     q1 = np.empty((E, d, f), np.int8)
     q2 = np.empty((E, f, d), np.int8)
     s1 = np.empty((E, f), np.float32)
     s2 = np.empty((E, d), np.float32)
-    for e in range(E):
-        q1[e], s1[e] = orc.quantize_linear(w1[e], bits)
-        q2[e], s2[e] = orc.quantize_linear(w2[e], bits)
+    t0 = time.perf_counter()
+    for e in range(E):  # quantize-experts (model.cpp:577-636), packed as write_checkpoint does
+        q1[e], s1[e] = lib.quantize_linear(w1[e], bits)
+        q2[e], s2[e] = lib.quantize_linear(w2[e], bits)
+        lib.pack(q1[e], bits)
+        lib.pack(q2[e], bits)
+    quant_s = time.perf_counter() - t0
     del w1, w2
     threads = threads or os.cpu_count() or 1
     if kind == "reference":
         bank = oracle.ref().bank(q1, s1, q2, s2, bits)
-        run = lambda: bank.forward(h, wg, threads)
+        run = lambda n: bank.forward(h, wg, n)
     else:
-        run = lambda: orc.moe_forward(h, wg, q1, s1, q2, s2, n_threads=threads)
-    run()  # discarded warm-up (bench.cpp:96-105 convention)
-    ts = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        run()
-        ts.append(time.perf_counter() - t0)
-    med = statistics.median(ts)
-    return {"value": round(T / med, 3), "unit": "tokens/s", "cores": threads, "kind": kind,
-            "sample": f"T={T} int{bits} E={E} d={d} f={f} top-1 layer; 1 warm-up + median of {reps} "
-                      f"timed moe_ffn_forward calls, token-sharded over {threads} threads",
-            "seconds_per_step": round(med, 4)}
+        run = lambda n: orc.moe_forward(h, wg, q1, s1, q2, s2, n_threads=n)
+
+    def timed(n):
+        run(n)  # discarded warm-up
+        ts = []
+        for _ in range(reps):
+            t1 = time.perf_counter()
+            run(n)
+            ts.append(time.perf_counter() - t1)
+        return statistics.median(ts)
+
+    med = timed(threads)
+    res = {"value": round(T / med, 3), "unit": "tokens/s", "cores": threads, "kind": kind,
+           "sample": f"T={T} int{bits} E={E} d={d} f={f} top-1 layer; 1 warm-up + median of {reps} "
+                     f"timed moe_ffn_forward calls, token-sharded over {threads} threads",
+           "seconds_per_step": round(med, 4),
+           "quantize_experts_s_1thread": round(quant_s, 3)}
+    if one_thread and threads > 1:
+        med1 = timed(1)
+        res["one_thread"] = {"value": round(T / med1, 3), "unit": "tokens/s", "cores": 1,
+                             "seconds_per_step": round(med1, 4)}
+    return res
 
 
 # ---------------------------------------------------------------------------------------
@@ -429,7 +513,7 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        base = reference_baseline(E, d, f, bits, T)
+        base = reference_baseline(E, d, f, bits, T, one_thread=False)
         line = {"metric": METRIC, "value": base["value"], "unit": "tokens/s", "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": base["seconds_per_step"] * 1e3,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
@@ -494,23 +578,32 @@ def main():
 
     sweep = []
     if rank == 0 and world == 1 and not args.no_sweep:
-        pts = [(b, t) for b in (8, 4, 3, 2) for t in (24, 4096)] + [(3, 16384), (2, 16384)]
-        for b, t in pts:
-            if (b, t) == (bits, T):
+        # (config, E, bits, T, zipf): BASELINE config 2 bit sweep (+ T=16384 tensor point), config 1,
+        # config 5 Zipf(1.2) skew over 64 experts
+        pts = [("config2", E, b, t, False) for b in (8, 4, 3, 2) for t in (24, 4096)]
+        pts += [("config2", E, 3, 16384, False), ("config2", E, 2, 16384, False), ("config1", 32, 4, 512, False)]
+        pts += [("config5", 64, 4, t, True) for t in (1, 8, 64, 512, 4096, 32768)]
+        for cfg, e_, b, t, zf in pts:
+            if (cfg, e_, b, t) == ("config2", E, bits, T):
                 continue
             try:
-                r, lay = run_point(m, torch, E, d, f, b, t, 1, max(min(args.steps, 60), 10), 5, dev,
-                                   hbm_peak, tc_peak, n_layers=4 if t >= 4096 else N_LAYERS)
+                r, lay = run_point(m, torch, e_, d, f, b, t, 1, max(min(args.steps, 60), 10), 5, dev,
+                                   hbm_peak, tc_peak, n_layers=4 if t >= 4096 else N_LAYERS, zipf=zf)
                 del lay
                 torch.cuda.empty_cache()
-                sweep.append({kk: (round(v, 5) if isinstance(v, float) else v) for kk, v in r.items()})
+                r = {kk: (round(v, 5) if isinstance(v, float) else v) for kk, v in r.items()}
+                r["config"] = cfg
+                r["experts"] = e_
+                sweep.append(r)
             except Exception as ex:  # report, never hide
-                sweep.append({"bits": b, "tokens": t, "error": str(ex)[:200]})
+                sweep.append({"config": cfg, "experts": e_, "bits": b, "tokens": t, "error": str(ex)[:200]})
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = reference_baseline(E, d, f, bits, T)
         cpu.pop("seconds_per_step", None)
+        if "one_thread" in cpu:
+            cpu["one_thread"].pop("seconds_per_step", None)
 
     if rank == 0:
         value = head["tokens_per_s"] * world
