@@ -396,6 +396,38 @@ def e2e_point(m, torch, layers, steps, warmup, top_k, d):
             "ms_per_step": round(ms, 5)}
 
 
+def run_config3(m, torch, steps, warmup, n_layers=36, T=768, seed=SEED):
+    """BASELINE config 3: 36-layer pre-LN residual FFN stack (even layers 32-expert top-1 int3
+    MoE, odd layers dense fp16 FFNs with 0.1 % outliers), 24 x 32 = 768 fp16 tokens. One step
+    = one forward of the whole stack, replayed from a CUDA graph (weights 1.8 GB >> L2)."""
+    from paper_2310_02410_b200.workloads import build_config3
+    stack, _ = build_config3(m, torch, seed, n_layers=n_layers)
+    g = torch.Generator(device="cuda").manual_seed(seed + 3)
+    h = torch.randn((T, 1024), generator=g, device="cuda").half()
+    stack.forward(h)
+    torch.cuda.synchronize()
+    st = torch.cuda.Stream()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(st):
+        with torch.cuda.graph(gr, stream=st):
+            stack.forward(h)
+    for _ in range(max(warmup, 3)):
+        gr.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        gr.replay()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    del gr, stack
+    torch.cuda.empty_cache()
+    return {"config": "config3", "layers": n_layers, "tokens": T, "ms_per_step": round(ms, 4),
+            "tokens_per_s": round(T / (ms * 1e-3), 1), "ms_per_layer": round(ms / n_layers, 5),
+            "launch": "CUDA graph of the whole stack forward"}
+
+
 # ---------------------------------------------------------------------------------------
 # expert parallelism (N > 1): experts sharded E/G, T tokens per rank (weak scaling)
 
@@ -597,6 +629,11 @@ def main():
                 sweep.append(r)
             except Exception as ex:  # report, never hide
                 sweep.append({"config": cfg, "experts": e_, "bits": b, "tokens": t, "error": str(ex)[:200]})
+
+        try:
+            sweep.append(run_config3(m, torch, max(min(args.steps // 20, 20), 5), 3))
+        except Exception as ex:  # report, never hide
+            sweep.append({"config": "config3", "error": str(ex)[:200]})
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -136,6 +136,8 @@ class Oracle(_Lib):
         self._sig("orc_moe_forward", i32, [fp, i64, i64, i64, i32, fp, i32, i8p, fp, i8p, fp,
                                            fp, fp, fp, ip, fp, i32])
         self._sig("orc_layer_norm", None, [fp, i64, i64, fp, fp, fp])
+        self._sig("orc_matmul", None, [fp, i64, i64, fp, i64, fp])
+        self._sig("orc_dense_ffn", None, [fp, i64, i64, i64, fp, fp, fp, fp, fp])
 
     def router_logits(self, h, wg):
         h = np.ascontiguousarray(h, np.float32)
@@ -192,6 +194,26 @@ class Oracle(_Lib):
                                 _p(arr(s1, np.float32), C.c_float), _p(arr(q2, np.int8), C.c_int8),
                                 _p(arr(s2, np.float32), C.c_float), _p(arr(b1, np.float32), C.c_float),
                                 _p(arr(b2, np.float32), C.c_float), _p(y, C.c_float))
+        return y[:m]
+
+    def matmul(self, a, b):
+        """Reference matmul (model.cpp:152-167)."""
+        a = np.ascontiguousarray(a, np.float32)
+        b = np.ascontiguousarray(b, np.float32)
+        out = np.zeros((a.shape[0], b.shape[1]), np.float32)
+        self.lib.orc_matmul(_p(a, C.c_float), a.shape[0], a.shape[1], _p(b, C.c_float), b.shape[1],
+                            _p(out, C.c_float))
+        return out
+
+    def dense_ffn(self, x, w1, w2, b1=None, b2=None):
+        """relu(x W1 + b1) W2 + b2 (model.cpp:315-322)."""
+        x = np.ascontiguousarray(x, np.float32)
+        m, d = x.shape
+        f = w1.shape[1]
+        y = np.zeros((max(m, 1), d), np.float32)
+        arr = lambda a: None if a is None else np.ascontiguousarray(a, np.float32)
+        self.lib.orc_dense_ffn(_p(x, C.c_float), m, d, f, _p(arr(w1), C.c_float), _p(arr(b1), C.c_float),
+                               _p(arr(w2), C.c_float), _p(arr(b2), C.c_float), _p(y, C.c_float))
         return y[:m]
 
     def layer_norm(self, x, gain, bias):

@@ -53,6 +53,11 @@ int orc_moe_forward(const float* h, int64_t t, int64_t d, int64_t f, int n_exper
 void orc_layer_norm(const float* x, int64_t rows, int64_t n, const float* gain,
                     const float* bias, float* out);
 
+/* Reference matmul (model.cpp:152-167) and dense_ffn (model.cpp:315-322), fp32. */
+void orc_matmul(const float* a, int64_t m, int64_t k, const float* b, int64_t n, float* out);
+void orc_dense_ffn(const float* x, int64_t m, int64_t d, int64_t f, const float* w1, const float* b1,
+                   const float* w2, const float* b2, float* y);
+
 #ifdef __cplusplus
 }
 #endif

@@ -17,3 +17,4 @@ __all__ = [
     "quantize_linear", "quantize_model", "quantize_pack", "route", "top1_route", "unpack",
     "valid_bits",
 ]
+from . import stack  # noqa: E402  (config-3 FFN stack: add_layer_norm, FfnStack)

@@ -41,6 +41,7 @@ SIGNATURES = {
     "moqe_gpu_expert_ffn": (_i32, [_vp, _vp, _i32, _i64, _vp, _vp, _vp, _i32, _i32, _vp]),
     "moqe_gpu_bank_profile": (_i32, [_vp, _i32]),
     "moqe_gpu_bank_profile_read": (_i32, [_vp, _vp, _vp, _i32]),
+    "moqe_gpu_add_layer_norm": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _i32, _vp]),
     "moqe_gpu_bank_span": (_i32, [_vp, _i32]),
     "moqe_gpu_bank_span_read": (_i32, [_vp, _vp, _vp]),
     "moqe_gpu_bank_trace": (_i32, [_vp, _i32]),

@@ -51,3 +51,43 @@ def apply_bias(h: np.ndarray, wg: np.ndarray, bias: np.ndarray):
     h[:, 0] = 1.0
     wg[0, :] = bias
     return h, wg
+
+
+def build_config3(m, torch, seed: int, n_layers: int = 36, E: int = 32, d: int = 1024, f: int = 4096,
+                  bits: int = 3, outlier_frac: float = 1e-3, keep_f32: bool = False):
+    """BASELINE config 3: a pre-LN residual FFN stack (no attention). Even layers are E-expert
+    top-1 MoE FFNs with `bits`-bit per-channel experts, odd layers dense fp16 FFNs
+    d -> f -> d with weights ~N(0,0.02) and `outlier_frac` of entries scaled x8. LayerNorm
+    gains ~1 + N(0,0.05), biases ~N(0,0.05); dense biases ~N(0,0.01); routers ~N(0,0.02).
+    Weights are drawn on the device from `seed`. keep_f32: also return the f32 expert weights
+    and the gate weights (the oracle re-quantizes them)."""
+    from .stack import DenseFFN, FfnStack, StackLayer
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(seed)
+    layers, raw = [], []
+    for i in range(n_layers):
+        gain = 1.0 + 0.05 * torch.randn(d, generator=g, device=dev)
+        bias = 0.05 * torch.randn(d, generator=g, device=dev)
+        if i % 2 == 0:
+            w1 = torch.randn((E, d, f), generator=g, device=dev) * 0.02
+            w2 = torch.randn((E, f, d), generator=g, device=dev) * 0.02
+            wg = torch.randn((d, E), generator=g, device=dev) * 0.02
+            bank = m.ExpertBank.from_float(w1, w2, bits, router=wg)
+            layers.append(StackLayer(gain, bias, moe=bank))
+            raw.append({"kind": "moe", "w1": w1 if keep_f32 else None, "w2": w2 if keep_f32 else None, "wg": wg})
+            if not keep_f32:
+                del w1, w2
+        else:
+            def dense_w(k, n):
+                w = torch.randn((k, n), generator=g, device=dev) * 0.02
+                mask = torch.rand((k, n), generator=g, device=dev) < outlier_frac
+                return torch.where(mask, w * 8.0, w).to(torch.float16)
+            w1 = dense_w(d, f)
+            w2 = dense_w(f, d)
+            b1 = 0.01 * torch.randn(f, generator=g, device=dev)
+            b2 = 0.01 * torch.randn(d, generator=g, device=dev)
+            layers.append(StackLayer(gain, bias, dense=DenseFFN(w1, w2, b1, b2)))
+            raw.append({"kind": "dense"})
+    fg = 1.0 + 0.05 * torch.randn(d, generator=g, device=dev)
+    fb = 0.05 * torch.randn(d, generator=g, device=dev)
+    return FfnStack(layers, fg, fb), raw
