@@ -40,7 +40,8 @@ typedef enum moqe_status {
     MOQE_RANGE_ERROR = 3,      /* std::range_error (tensor.cpp:101-104) */
     MOQE_CUDA_ERROR = 4,
     MOQE_NCCL_ERROR = 5,
-    MOQE_NOT_SUPPORTED = 6
+    MOQE_NOT_SUPPORTED = 6,
+    MOQE_CHECKPOINT_ERROR = 7  /* moqe::CheckpointError (checkpoint.hpp:14-30) */
 } moqe_status;
 
 typedef enum moqe_granularity { MOQE_PER_CHANNEL = 0, MOQE_PER_TENSOR = 1 } moqe_granularity;
@@ -113,6 +114,14 @@ moqe_status moqe_gpu_bank_create(int n_experts, int64_t d_model, int64_t d_ffn, 
                                  const uint8_t* packed_w2, const float* scales2,
                                  const float* b1, const float* b2, int inputs_on_device,
                                  moqe_bank_t* out);
+
+/* bank_create with the scales' granularity: MOQE_PER_CHANNEL (0: scales1 [E][d_ffn], scales2
+ * [E][d_model], as bank_create) or MOQE_PER_TENSOR (1: one scale per expert matrix, scales1 and
+ * scales2 [E]; Granularity::PerTensor, quant.cpp:53-55, broadcast to every channel). */
+moqe_status moqe_gpu_bank_create_g(int n_experts, int64_t d_model, int64_t d_ffn, int bits, int granularity,
+                                   const uint8_t* packed_w1, const float* scales1,
+                                   const uint8_t* packed_w2, const float* scales2, const float* b1,
+                                   const float* b2, int inputs_on_device, moqe_bank_t* out);
 moqe_status moqe_gpu_bank_destroy(moqe_bank_t bank);
 /* Router weights Wg [d_model x n_experts] f32 kept with the bank
  * (RouterState, include/moqe/model.hpp:56-58). Blocking. */
@@ -162,6 +171,34 @@ moqe_status moqe_gpu_expert_ffn(moqe_bank_t bank, const void* x, moqe_dtype x_dt
 #define MOQE_PROFILE_KINDS 6
 moqe_status moqe_gpu_bank_profile(moqe_bank_t bank, int enable);
 moqe_status moqe_gpu_bank_profile_read(moqe_bank_t bank, double* ms, int64_t* launches, int keep);
+
+/* ---- MQE1 container -> device bank (checkpoint.cpp:99-131 layout, :312-413 reader) ----
+ * open maps the file and validates the header and index like read_checkpoint (bad magic /
+ * version, truncation, inconsistent offsets, duplicate names -> MOQE_CHECKPOINT_ERROR).
+ * mqe1_bank_create builds the bank of "<layer>.expert.<e>.fc{1,2}.w" (q-lin; + optional
+ * ".fc{1,2}.b"), names as ffn_block (model.cpp:402-412), straight from the packed blobs (one
+ * host->device copy, no unpacking), and sets "<layer>.router.w" as its router when present. */
+typedef struct moqe_mqe1* moqe_mqe1_t;
+typedef struct moqe_mqe1_info {
+    char name[128], group[32], dtype[8];
+    int bits, per_tensor, ndim;
+    int64_t shape[4];
+    uint64_t data_offset, data_bytes, scale_offset, scale_bytes;
+} moqe_mqe1_info;
+moqe_status moqe_gpu_mqe1_open(const char* path, moqe_mqe1_t* out);
+moqe_status moqe_gpu_mqe1_close(moqe_mqe1_t m);
+int64_t moqe_gpu_mqe1_count(moqe_mqe1_t m);
+moqe_status moqe_gpu_mqe1_entry(moqe_mqe1_t m, int64_t i, moqe_mqe1_info* info);
+moqe_status moqe_gpu_mqe1_bank_create(moqe_mqe1_t m, const char* layer, int n_experts, moqe_bank_t* out);
+
+/* Pre-LN residual FFN stack support (BASELINE config 3):
+ * x [rows][n] f32 residual stream; when delta != NULL, x += delta first (in place, fp32 like
+ * add_inplace, proj/src/model.cpp:308-310); then out = layer_norm(x, gain, bias) per row, eps
+ * 1e-5, statistics in double (model.cpp:193-212). Replaces the layer_norm + add_inplace pair of
+ * run_stack (model.cpp:419-435). Stream-ordered. */
+moqe_status moqe_gpu_add_layer_norm(float* x, const float* delta, int64_t rows, int64_t n,
+                                    const float* gain, const float* bias, void* out,
+                                    moqe_dtype out_dtype, void* stream);
 
 /* In-kernel launch spans of the decode path (measurement support, off by default):
  * with span(bank, 1) each decode forward's router and expert-FFN kernels record,

@@ -242,6 +242,8 @@ class Ref(_Lib):
         self._sig("ref_bank_destroy", None, [vp])
         self._sig("ref_bank_forward", i32, [vp, fp, i64, fp, fp, i32])
         self._sig("ref_hardware_threads", i32, [])
+        self._sig("ref_write_moe_mqe1", i64, [C.c_char_p, C.c_char_p, i32, i64, i64, i32, i32, i8p, fp, i8p, fp,
+                                              fp, fp, fp])
 
     def linear_scales(self, a, bits, per_tensor=False):  # ref uses 0=channel,1=tensor too
         return super().linear_scales(a, bits, per_tensor)
@@ -281,6 +283,21 @@ class Ref(_Lib):
 
     def float_bank(self, w1, w2, b1=None, b2=None):
         return RefBank(self, w1, None, w2, None, 0, b1, b2, float_bank=True)
+
+    def write_moe_mqe1(self, path, layer, codes1, scales1, codes2, scales2, bits, per_tensor=False,
+                       b1=None, b2=None, wg=None) -> int:
+        """One MoE layer as an MQE1 container written by moqe::write_checkpoint_file."""
+        E, d, f = codes1.shape
+        arr = lambda a, dt: None if a is None else np.ascontiguousarray(a, dt)
+        c1, c2 = arr(codes1, np.int8), arr(codes2, np.int8)
+        s1, s2 = arr(scales1, np.float32), arr(scales2, np.float32)
+        bb1, bb2, w = arr(b1, np.float32), arr(b2, np.float32), arr(wg, np.float32)
+        n = self.lib.ref_write_moe_mqe1(str(path).encode(), layer.encode(), E, d, f, bits, int(per_tensor),
+                                        _p(c1, C.c_int8), _p(s1, C.c_float), _p(c2, C.c_int8), _p(s2, C.c_float),
+                                        _p(bb1, C.c_float), _p(bb2, C.c_float), _p(w, C.c_float))
+        if n < 0:
+            raise RuntimeError("write_checkpoint failed")
+        return int(n)
 
     def hardware_threads(self) -> int:
         return int(self.lib.ref_hardware_threads())

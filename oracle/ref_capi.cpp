@@ -15,6 +15,7 @@
 //   ref_top1_route           -> moqe::top1_route             proj/src/model.cpp:328-346
 //   ref_bank_* / ref_moe_ffn_forward -> moqe::moe_ffn_forward proj/src/model.cpp:348-393
 //   ref_matmul_dequant_fused -> moqe::matmul_dequant_fused   proj/src/bench.cpp:11-47
+//   ref_write_moe_mqe1       -> moqe::write_checkpoint_file  proj/src/checkpoint.cpp:239-290
 //
 // Status codes mirror include/moqe_gpu.h (0 ok, 1 invalid_argument,
 // 2 out_of_range, 3 range_error, 9 other).
@@ -27,6 +28,7 @@
 
 #include "moqe/bench.hpp"
 #include "moqe/bitpack.hpp"
+#include "moqe/checkpoint.hpp"
 #include "moqe/model.hpp"
 #include "moqe/quant.hpp"
 #include "moqe/tensor.hpp"
@@ -269,5 +271,40 @@ int ref_bank_forward(void* bank, const float* h, int64_t t, const float* wg, flo
 }
 
 int ref_hardware_threads(void) { return static_cast<int>(std::thread::hardware_concurrency()); }
+
+// An MQE1 container (written by the reference's own write_checkpoint_file) holding one MoE
+// layer the way ffn_block names it (model.cpp:402-412): "<layer>.expert.<e>.fc{1,2}.w" as
+// q-lin tensors (codes [E][rows*cols], scales [E][cols] or [E][1] when per_tensor), optional
+// f32 biases "<layer>.expert.<e>.fc{1,2}.b", and the f32 router "<layer>.router.w" [d x E].
+// Returns the file size, or -1 on an exception.
+int64_t ref_write_moe_mqe1(const char* path, const char* layer, int n_experts, int64_t d, int64_t f, int bits,
+                           int per_tensor, const int8_t* codes1, const float* scales1, const int8_t* codes2,
+                           const float* scales2, const float* b1, const float* b2, const float* wg) {
+    try {
+        moqe::Checkpoint ck;
+        ck.meta["format"] = "moqe-b200-test";
+        const std::string base = std::string(layer) + ".expert.";
+        const int64_t ns1 = per_tensor ? 1 : f, ns2 = per_tensor ? 1 : d;
+        for (int e = 0; e < n_experts; ++e) {
+            const std::string p = base + std::to_string(e);
+            ck.add(moqe::CheckpointEntry::quantized(p + ".fc1.w", moqe::LayerGroup::ExpertFFN,
+                                                    make_qt(codes1 + e * d * f, scales1 + e * ns1, d, f, bits, per_tensor)));
+            ck.add(moqe::CheckpointEntry::quantized(p + ".fc2.w", moqe::LayerGroup::ExpertFFN,
+                                                    make_qt(codes2 + e * f * d, scales2 + e * ns2, f, d, bits, per_tensor)));
+            if (b1)
+                ck.add(moqe::CheckpointEntry::f32(p + ".fc1.b", moqe::LayerGroup::ExpertFFN,
+                                                  moqe::Tensor({f}, std::vector<float>(b1 + e * f, b1 + (e + 1) * f))));
+            if (b2)
+                ck.add(moqe::CheckpointEntry::f32(p + ".fc2.b", moqe::LayerGroup::ExpertFFN,
+                                                  moqe::Tensor({d}, std::vector<float>(b2 + e * d, b2 + (e + 1) * d))));
+        }
+        if (wg)
+            ck.add(moqe::CheckpointEntry::f32(std::string(layer) + ".router.w", moqe::LayerGroup::Router,
+                                              make2d(wg, d, n_experts)));
+        return static_cast<int64_t>(moqe::write_checkpoint_file(ck, path));
+    } catch (...) {
+        return -1;
+    }
+}
 
 }  // extern "C"

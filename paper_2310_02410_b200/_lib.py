@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libmoqe_gpu.so")
 
 # status codes (moqe_status)
-OK, INVALID_ARGUMENT, OUT_OF_RANGE, RANGE_ERROR, CUDA_ERROR, NCCL_ERROR, NOT_SUPPORTED = range(7)
+OK, INVALID_ARGUMENT, OUT_OF_RANGE, RANGE_ERROR, CUDA_ERROR, NCCL_ERROR, NOT_SUPPORTED, CHECKPOINT_ERROR = range(8)
 PER_CHANNEL, PER_TENSOR = 0, 1
 F32, F16 = 0, 1
 PATH_AUTO, PATH_GEMV, PATH_GEMM = 0, 1, 2
@@ -33,6 +33,8 @@ SIGNATURES = {
     "moqe_gpu_route": (_i32, [_vp, _i32, _i64, _i64, _vp, _i32, _i32, _vp, _vp, _vp]),
     "moqe_gpu_bank_create": (_i32, [_i32, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32,
                                     C.POINTER(_vp)]),
+    "moqe_gpu_bank_create_g": (_i32, [_i32, _i64, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32,
+                                      C.POINTER(_vp)]),
     "moqe_gpu_bank_destroy": (_i32, [_vp]),
     "moqe_gpu_bank_set_router": (_i32, [_vp, _vp, _i32]),
     "moqe_gpu_bank_weight_bytes": (_i64, [_vp]),
@@ -41,6 +43,11 @@ SIGNATURES = {
     "moqe_gpu_expert_ffn": (_i32, [_vp, _vp, _i32, _i64, _vp, _vp, _vp, _i32, _i32, _vp]),
     "moqe_gpu_bank_profile": (_i32, [_vp, _i32]),
     "moqe_gpu_bank_profile_read": (_i32, [_vp, _vp, _vp, _i32]),
+    "moqe_gpu_mqe1_open": (_i32, [C.c_char_p, C.POINTER(_vp)]),
+    "moqe_gpu_mqe1_close": (_i32, [_vp]),
+    "moqe_gpu_mqe1_count": (_i64, [_vp]),
+    "moqe_gpu_mqe1_entry": (_i32, [_vp, _i64, _vp]),
+    "moqe_gpu_mqe1_bank_create": (_i32, [_vp, C.c_char_p, _i32, C.POINTER(_vp)]),
     "moqe_gpu_add_layer_norm": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _i32, _vp]),
     "moqe_gpu_bank_span": (_i32, [_vp, _i32]),
     "moqe_gpu_bank_span_read": (_i32, [_vp, _vp, _vp]),
@@ -66,6 +73,10 @@ class RangeError(MoqeError, ArithmeticError):
     """std::range_error in the reference (tensor.cpp:101-104)."""
 
 
+class CheckpointError(MoqeError, RuntimeError):
+    """moqe::CheckpointError in the reference (checkpoint.hpp:14-30)."""
+
+
 class CudaError(MoqeError):
     pass
 
@@ -75,7 +86,8 @@ class NotSupported(MoqeError):
 
 
 _EXC = {INVALID_ARGUMENT: InvalidArgument, OUT_OF_RANGE: OutOfRange, RANGE_ERROR: RangeError,
-        CUDA_ERROR: CudaError, NCCL_ERROR: MoqeError, NOT_SUPPORTED: NotSupported}
+        CUDA_ERROR: CudaError, NCCL_ERROR: MoqeError, NOT_SUPPORTED: NotSupported,
+        CHECKPOINT_ERROR: CheckpointError}
 
 _lib = None
 

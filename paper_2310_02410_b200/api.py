@@ -176,7 +176,10 @@ class ExpertBank:
     def __init__(self, n_experts: int, d_model: int, d_ffn: int, bits: int,
                  packed_w1: torch.Tensor, scales1: torch.Tensor, packed_w2: torch.Tensor,
                  scales2: torch.Tensor, b1: Optional[torch.Tensor] = None,
-                 b2: Optional[torch.Tensor] = None, router: Optional[torch.Tensor] = None):
+                 b2: Optional[torch.Tensor] = None, router: Optional[torch.Tensor] = None,
+                 granularity: str = PER_CHANNEL):
+        """granularity: PER_CHANNEL (scales1 [E, d_ffn], scales2 [E, d_model]) or PER_TENSOR
+        (one scale per expert matrix: scales [E] or [E, 1]; quant.cpp:53-55)."""
         self.E, self.d, self.f, self.bits = n_experts, d_model, d_ffn, bits
         lib = _lib.load()
         dev = packed_w1.is_cuda
@@ -186,8 +189,8 @@ class ExpertBank:
                 None if b1 is None else conv(b1, torch.float32),
                 None if b2 is None else conv(b2, torch.float32)]
         h = C.c_void_p()
-        check(lib.moqe_gpu_bank_create(n_experts, d_model, d_ffn, bits, *[_ptr(t) for t in keep],
-                                       1 if dev else 0, C.byref(h)))
+        check(lib.moqe_gpu_bank_create_g(n_experts, d_model, d_ffn, bits, _GRAN[granularity],
+                                         *[_ptr(t) for t in keep], 1 if dev else 0, C.byref(h)))
         self._h = h
         torch.cuda.synchronize()
         if router is not None:
@@ -196,12 +199,29 @@ class ExpertBank:
     @classmethod
     def from_float(cls, w1: torch.Tensor, w2: torch.Tensor, bits: int,
                    b1: Optional[torch.Tensor] = None, b2: Optional[torch.Tensor] = None,
-                   router: Optional[torch.Tensor] = None) -> "ExpertBank":
-        """Quantize-experts on the GPU (per-channel linear) then build the bank."""
+                   router: Optional[torch.Tensor] = None, granularity: str = PER_CHANNEL) -> "ExpertBank":
+        """Quantize-experts on the GPU (linear, per channel or per tensor) then build the bank."""
         E, d, f = w1.shape
-        p1, s1 = quantize_pack(w1, bits)
-        p2, s2 = quantize_pack(w2, bits)
-        return cls(E, d, f, bits, p1, s1, p2, s2, b1, b2, router)
+        p1, s1 = quantize_pack(w1, bits, granularity)
+        p2, s2 = quantize_pack(w2, bits, granularity)
+        return cls(E, d, f, bits, p1, s1, p2, s2, b1, b2, router, granularity)
+
+    @classmethod
+    def from_mqe1(cls, path: str, layer: str, n_experts: int) -> "ExpertBank":
+        """The bank of one MoE layer straight from an MQE1 container (checkpoint.cpp:312-413):
+        "<layer>.expert.<e>.fc{1,2}.w" q-lin blobs copied to the device as stored, optional biases,
+        and "<layer>.router.w" as the router when present."""
+        lib = _lib.load()
+        with Mqe1(path) as m:
+            h = C.c_void_p()
+            check(lib.moqe_gpu_mqe1_bank_create(m._h, layer.encode(), n_experts, C.byref(h)))
+        bank = cls.__new__(cls)
+        bank._h = h
+        info = {e["name"]: e for e in Mqe1(path).entries()}
+        w1 = info[f"{layer}.expert.0.fc1.w"]
+        bank.E, bank.d, bank.f, bank.bits = n_experts, int(w1["shape"][0]), int(w1["shape"][1]), int(w1["bits"])
+        torch.cuda.synchronize()
+        return bank
 
     def set_router(self, wg: torch.Tensor) -> None:
         wg = wg.to(torch.float32).contiguous()
@@ -242,6 +262,51 @@ class ExpertBank:
             if sys.is_finalizing():
                 return
             self.close()
+        except Exception:
+            pass
+
+
+class _Mqe1Info(C.Structure):
+    _fields_ = [("name", C.c_char * 128), ("group", C.c_char * 32), ("dtype", C.c_char * 8), ("bits", C.c_int),
+                ("per_tensor", C.c_int), ("ndim", C.c_int), ("shape", C.c_int64 * 4), ("data_offset", C.c_uint64),
+                ("data_bytes", C.c_uint64), ("scale_offset", C.c_uint64), ("scale_bytes", C.c_uint64)]
+
+
+class Mqe1:
+    """A mapped MQE1 container (read_checkpoint's index validation, checkpoint.cpp:312-392)."""
+
+    def __init__(self, path: str):
+        self._h = C.c_void_p()
+        check(_lib.load().moqe_gpu_mqe1_open(str(path).encode(), C.byref(self._h)))
+
+    def entries(self):
+        lib = _lib.load()
+        out = []
+        for i in range(int(lib.moqe_gpu_mqe1_count(self._h))):
+            inf = _Mqe1Info()
+            check(lib.moqe_gpu_mqe1_entry(self._h, i, C.byref(inf)))
+            out.append({"name": inf.name.decode(), "group": inf.group.decode(), "dtype": inf.dtype.decode(),
+                        "bits": inf.bits, "granularity": PER_TENSOR if inf.per_tensor else PER_CHANNEL,
+                        "shape": tuple(inf.shape[k] for k in range(inf.ndim)), "data_offset": inf.data_offset,
+                        "data_bytes": inf.data_bytes, "scale_offset": inf.scale_offset,
+                        "scale_bytes": inf.scale_bytes})
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            _lib.load().moqe_gpu_mqe1_close(self._h)
+            self._h = C.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            if not sys.is_finalizing():
+                self.close()
         except Exception:
             pass
 

@@ -289,6 +289,7 @@ const char* moqe_gpu_status_string(moqe_status st) {
         case MOQE_CUDA_ERROR: return "cuda_error";
         case MOQE_NCCL_ERROR: return "nccl_error";
         case MOQE_NOT_SUPPORTED: return "not_supported";
+        case MOQE_CHECKPOINT_ERROR: return "checkpoint_error";
     }
     return "unknown";
 }
@@ -378,6 +379,43 @@ moqe_status moqe_gpu_bank_create(int n_experts, int64_t d_model, int64_t d_ffn, 
     }
     *out = b;
     return MOQE_OK;
+}
+
+moqe_status moqe_gpu_bank_create_g(int n_experts, int64_t d_model, int64_t d_ffn, int bits, int granularity,
+                                   const uint8_t* packed_w1, const float* scales1, const uint8_t* packed_w2,
+                                   const float* scales2, const float* b1, const float* b2, int inputs_on_device,
+                                   moqe_bank_t* out) {
+    if (granularity == 0)
+        return moqe_gpu_bank_create(n_experts, d_model, d_ffn, bits, packed_w1, scales1, packed_w2, scales2, b1, b2,
+                                    inputs_on_device, out);
+    if (granularity != 1) return fail(MOQE_INVALID_ARGUMENT, "bank_create: bad granularity");
+    if (n_experts <= 0 || d_model <= 0 || d_ffn <= 0 || !scales1 || !scales2)
+        return moqe_gpu_bank_create(n_experts, d_model, d_ffn, bits, packed_w1, scales1, packed_w2, scales2, b1, b2,
+                                    inputs_on_device, out);
+    // per-tensor: one scale per matrix, broadcast to its channels (scale_index, quant.cpp:53-55)
+    std::vector<float> t1(n_experts), t2(n_experts);
+    const cudaMemcpyKind k = inputs_on_device ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost;
+    MOQE_CUDA(cudaMemcpy(t1.data(), scales1, sizeof(float) * n_experts, k));
+    MOQE_CUDA(cudaMemcpy(t2.data(), scales2, sizeof(float) * n_experts, k));
+    std::vector<float> e1(size_t(n_experts) * d_ffn), e2(size_t(n_experts) * d_model);
+    for (int e = 0; e < n_experts; ++e) {
+        std::fill(e1.begin() + size_t(e) * d_ffn, e1.begin() + size_t(e + 1) * d_ffn, t1[e]);
+        std::fill(e2.begin() + size_t(e) * d_model, e2.begin() + size_t(e + 1) * d_model, t2[e]);
+    }
+    if (!inputs_on_device)
+        return moqe_gpu_bank_create(n_experts, d_model, d_ffn, bits, packed_w1, e1.data(), packed_w2, e2.data(), b1, b2,
+                                    0, out);
+    float *d1 = nullptr, *d2 = nullptr;
+    MOQE_CUDA(cudaMalloc(&d1, e1.size() * sizeof(float)));
+    cudaError_t ce = cudaMalloc(&d2, e2.size() * sizeof(float));
+    if (ce == cudaSuccess) ce = cudaMemcpy(d1, e1.data(), e1.size() * sizeof(float), cudaMemcpyHostToDevice);
+    if (ce == cudaSuccess) ce = cudaMemcpy(d2, e2.data(), e2.size() * sizeof(float), cudaMemcpyHostToDevice);
+    moqe_status st = ce == cudaSuccess ? moqe_gpu_bank_create(n_experts, d_model, d_ffn, bits, packed_w1, d1, packed_w2,
+                                                              d2, b1, b2, 1, out)
+                                       : cuda_fail(ce, "bank_create_g");
+    cudaFree(d1);
+    cudaFree(d2);
+    return st;
 }
 
 moqe_status moqe_gpu_bank_destroy(moqe_bank_t bank) {

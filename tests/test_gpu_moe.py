@@ -153,3 +153,28 @@ def test_zero_input_gives_gated_bias(gpu):
                                      torch.zeros((d, E), device="cuda"), return_routing=True)
     assert (ex.cpu().numpy() == 0).all()
     assert np.allclose(out.cpu().numpy(), (np.arange(d) - 1.5) / 3.0, rtol=1e-6)
+
+
+@pytest.mark.parametrize("bits,T,topk", [(4, 24, 1), (3, 300, 2), (2, 2048, 1)])
+def test_moe_per_tensor_bank(gpu, orc, bits, T, topk):
+    """Per-tensor experts (Granularity::PerTensor, quant.cpp:53-55: one scale per matrix,
+    scale_index) through the forward, decode / mixed / tcgen05 paths."""
+    import torch
+    E, d, f = 8, 256, 512
+    rng = np.random.default_rng(bits * 13 + T)
+    w1 = (rng.standard_normal((E, d, f)) * 0.02).astype(np.float32)
+    w2 = (rng.standard_normal((E, f, d)) * 0.02).astype(np.float32)
+    wg = (rng.standard_normal((d, E)) * 0.02).astype(np.float32)
+    h = fp16_valued(rng.standard_normal((T, d)))
+    q1 = np.zeros(w1.shape, np.int8); q2 = np.zeros(w2.shape, np.int8)
+    s1 = np.zeros((E, f), np.float32); s2 = np.zeros((E, d), np.float32)
+    for e in range(E):
+        q1[e], t1 = orc.quantize_linear(w1[e], bits, per_tensor=True)
+        q2[e], t2 = orc.quantize_linear(w2[e], bits, per_tensor=True)
+        s1[e], s2[e] = t1[0], t2[0]
+    bank = gpu.ExpertBank.from_float(_t(w1), _t(w2), bits, router=_t(wg), granularity=gpu.PER_TENSOR)
+    want, ex_o, g_o = orc.moe_forward(h, wg, q1, s1, q2, s2, top_k=topk)
+    out, ex, g = gpu.moe_ffn_forward(_t(h).half(), bank, top_k=topk, return_routing=True)
+    check_routing(orc, h, wg, topk, ex.cpu().numpy(), g.cpu().numpy())
+    nbad, mx = allclose_report(out.cpu().numpy(), want, ATOL, RTOL)
+    assert nbad == 0, mx
