@@ -27,6 +27,8 @@ moqe_status cuda_fail(cudaError_t err, const char* what);
         if (e__ != cudaSuccess) return ::moqe_gpu::cuda_fail(e__, what); \
     } while (0)
 
+constexpr int kMaxDevices = 64;  // per-process launch caches are indexed by device ordinal
+
 inline bool valid_bits(int b) { return b == 2 || b == 3 || b == 4 || b == 8; }
 
 // bitpack.cpp:12-16

@@ -246,7 +246,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, bool p1, const 
 
 template <int BITS, int CS>
 __global__ void __launch_bounds__(kGemmThreads, 1)
-    k_ffn_gemm(const __grid_constant__ GemmParams prm, GemmArgs g, Plan P, int phase, int dbg) {
+    k_ffn_gemm(const __grid_constant__ GemmParams prm, GemmArgs g, Plan P, int phase) {
     constexpr int TB = tile_bytes(BITS);
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -375,18 +375,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 mbar_wait(&aempty[a], aph2 ^ 1);
                 const uint8_t* row = sP + s * TB + m * row_bytes(BITS);
                 uint8_t* arow = sA + a * kATile + m * 128;
-                if (dbg != 3 && dbg != 5)
 #pragma unroll
                 for (int cc = 0; cc < 2; ++cc) {
                     const int c = 2 * hc + cc;
                     uint32_t o[8];
-                    if (dbg == 2) { for (int i = 0; i < 8; ++i) o[i] = 0; } else
                     unpack_chunk<BITS>(row, c, o);
                     // 16-byte chunks 2c, 2c+1 of the 128-byte row, swizzled by (row % 8)
                     *reinterpret_cast<uint4*>(arow + (((2 * c) ^ (m & 7)) << 4)) = make_uint4(o[0], o[1], o[2], o[3]);
                     *reinterpret_cast<uint4*>(arow + (((2 * c + 1) ^ (m & 7)) << 4)) = make_uint4(o[4], o[5], o[6], o[7]);
                 }
-                if (dbg == 0) fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core
+                fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core
                 mbar_arrive(&afull[a]);
                 if (++s == kStages) { s = 0; ph ^= 1; }
                 if (++a == kAStages) { a = 0; aph2 ^= 1; }
@@ -712,7 +710,10 @@ cudaError_t launch_gemm_2sm(const GemmArgs& g, const Plan& P, int phase, cudaStr
     if (!ok) return cudaErrorInvalidValue;
     auto kern = k_ffn_gemm2<BITS>;
     const size_t smem = gemm2_smem<BITS>();
-    static int max_clusters = 0;
+    static int max_clusters_dev[kMaxDevices] = {};  // per device: attribute + co-resident clusters
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& max_clusters = max_clusters_dev[dev < kMaxDevices ? dev : 0];
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
@@ -749,14 +750,18 @@ cudaError_t launch_gemm_cs(const GemmArgs& g, const Plan& P, int phase, cudaStre
     if (!ok) return cudaErrorInvalidValue;
     auto kern = k_ffn_gemm<BITS, CS>;
     const size_t smem = gemm_smem<BITS>();
-    static bool configured = false;
-    if (!configured) {
+    static bool configured_dev[kMaxDevices] = {};
+    static int max_clusters_dev[kMaxDevices] = {};  // co-resident clusters (GPC packing leaves SMs idle for CS=4)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int di = dev < kMaxDevices ? dev : 0;
+    if (!configured_dev[di]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return e;
-        configured = true;
+        configured_dev[di] = true;
     }
     cudaLaunchConfig_t cfg{};
-    static int max_clusters = 0;  // co-resident clusters (GPC packing leaves SMs idle for CS=4)
+    int& max_clusters = max_clusters_dev[di];
     if (max_clusters == 0) {
         cudaLaunchConfig_t q{};
         q.gridDim = dim3(unsigned(num_sms / CS * CS));
@@ -784,8 +789,7 @@ cudaError_t launch_gemm_cs(const GemmArgs& g, const Plan& P, int phase, cudaStre
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    static const int dbg = [] { const char* v = getenv("MOQE_GEMM_DEBUG"); return v ? atoi(v) : 0; }();
-    return cudaLaunchKernelEx(&cfg, kern, prm, g, P, phase, dbg);
+    return cudaLaunchKernelEx(&cfg, kern, prm, g, P, phase);
 }
 
 template <int BITS>

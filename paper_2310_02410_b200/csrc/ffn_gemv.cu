@@ -1061,12 +1061,16 @@ cudaError_t launch_phase(const GemvArgs& g, const Plan& P, cudaStream_t st, int 
     const int Kp = MODE == 1 ? g.Kp1 : g.Kp2;
     const int cs = (Kp + kChunkK - 1) / kChunkK;
     const int smem = L::total(cs);
-    static bool configured = false;
-    static int ncl[kMaxCluster + 1] = {0};
-    if (!configured) {
+    static bool configured_dev[kMaxDevices] = {};
+    static int ncl_dev[kMaxDevices][kMaxCluster + 1] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int di = dev < kMaxDevices ? dev : 0;
+    int* ncl = ncl_dev[di];
+    if (!configured_dev[di]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
         if (e != cudaSuccess) return e;
-        configured = true;
+        configured_dev[di] = true;
     }
     if (ncl[cs] == 0) ncl[cs] = active_clusters(kern, cs, smem, kGemvThreads, num_sms);
     cudaLaunchConfig_t cfg{};

@@ -1323,7 +1323,10 @@ __global__ void __launch_bounds__(256) k_scatter(const void* h, int h_f16, int64
 namespace {
 template <int EPL, int EFIX, int TT>
 cudaError_t launch_dec_tt(const RouteArgs& a, const Plan& P, size_t smem, cudaStream_t st) {
-    static bool configured = false;
+    static bool configured_dev[kMaxDevices] = {};
+    int dev_ = 0;
+    cudaGetDevice(&dev_);
+    bool& configured = configured_dev[dev_ < kMaxDevices ? dev_ : 0];
     if (!configured) {
         cudaFuncSetAttribute(k_route_decode<EPL, EFIX, TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         configured = true;
@@ -1347,7 +1350,10 @@ cudaError_t launch_dec_tt(const RouteArgs& a, const Plan& P, size_t smem, cudaSt
 }
 template <int EPL, int EFIX, bool SEL>
 cudaError_t launch_chain(const RouteArgs& a, const Plan& P, size_t smem, cudaStream_t st) {
-    static bool configured = false;
+    static bool configured_dev[kMaxDevices] = {};
+    int dev_ = 0;
+    cudaGetDevice(&dev_);
+    bool& configured = configured_dev[dev_ < kMaxDevices ? dev_ : 0];
     if (!configured) {
         cudaFuncSetAttribute(k_route_chain<EPL, EFIX, SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         configured = true;
@@ -1421,7 +1427,10 @@ cudaError_t launch_route(const RouteArgs& a, const Plan& P, cudaStream_t st) {
     const size_t smem = route_small_smem(a.d, a.E);
     if (smem > 220 * 1024) return cudaErrorInvalidValue;
     if (a.T <= kRouteDecMaxT && a.E <= kRouteDecMaxE) return launch_route_decode(a, P, smem, st);
-    static bool configured = false;
+    static bool configured_dev[kMaxDevices] = {};
+    int dev_ = 0;
+    cudaGetDevice(&dev_);
+    bool& configured = configured_dev[dev_ < kMaxDevices ? dev_ : 0];
     if (!configured) {
         const int mx = 220 * 1024;
         cudaFuncSetAttribute(k_route_small<1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
