@@ -119,6 +119,10 @@ bool fused_enabled() {  // MOQE_DEC_FUSED=0: decode keeps the separate router la
     static const bool v = [] { const char* s = getenv("MOQE_DEC_FUSED"); return !(s && atoi(s) == 0); }();
     return v;
 }
+int route_cluster_env() {  // MOQE_DEC_CLUSTER=1: every decode CTA routes alone (no 4-CTA clusters)
+    static const int v = [] { const char* s = getenv("MOQE_DEC_CLUSTER"); return (s && atoi(s) == 1) ? 1 : 4; }();
+    return v;
+}
 bool xrows_in_router() {  // MOQE_XROWS_IN_ROUTER=0: decode keeps the separate k_xrows launch
     static const bool v = [] { const char* s = getenv("MOQE_XROWS_IN_ROUTER"); return !(s && atoi(s) == 0); }();
     return v;
@@ -522,6 +526,7 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
         a.fused = (wg == b->wg && b->wgt && b->wg_finite && t <= 32 && fused_enabled()) ? 1 : 0;
         a.wgt = b->wgt;
         a.wg_shift = b->wg_shift;
+        a.route_cluster = route_cluster_env();
         cudaError_t ce = launch_dec(b->bits, a, st, b->num_sms);
         if (ce != cudaSuccess) return cuda_fail(ce, "k_dec");
         return MOQE_OK;

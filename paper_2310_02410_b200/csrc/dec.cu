@@ -435,50 +435,48 @@ struct DecGeom {
 // 1024 * 2^-s_k * x_k + u_k * x_k and Sum q_k x_k = acc - Z with the per-token constant
 // Z = Sum_k (1024 + bias * 2^s_k) * B_k (k_dec_route). No HFMA2, no constants.
 template <int BITS>
-__device__ __forceinline__ void unpack_chunk_raw(const uint8_t* row, int t, uint32_t (&o)[8]) {
-    const uint32_t mg = magic_reg();
+__device__ __forceinline__ void unpack_chunk_raw(const uint8_t* row, int t, uint32_t (&o)[8], const uint32_t (&mg)[8]) {
     if constexpr (BITS == 4) {
         const uint2 w = *reinterpret_cast<const uint2*>(row + 8 * t);
         const uint32_t ws[2] = {w.x, w.y};
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
             const uint32_t a = ws[q], a8 = ws[q] >> 8;
-            o[4 * q + 0] = lop_magic<0x000F000Fu>(a, mg);
-            o[4 * q + 1] = lop_magic<0x00F000F0u>(a, mg);
-            o[4 * q + 2] = lop_magic<0x000F000Fu>(a8, mg);
-            o[4 * q + 3] = lop_magic<0x00F000F0u>(a8, mg);
+            o[4 * q + 0] = lop_magic<0x000F000Fu>(a, mg[4 * q + 0]);
+            o[4 * q + 1] = lop_magic<0x00F000F0u>(a, mg[4 * q + 1]);
+            o[4 * q + 2] = lop_magic<0x000F000Fu>(a8, mg[4 * q + 2]);
+            o[4 * q + 3] = lop_magic<0x00F000F0u>(a8, mg[4 * q + 3]);
         }
     } else if constexpr (BITS == 2) {
         const uint32_t w = *reinterpret_cast<const uint32_t*>(row + 4 * t);
         const uint32_t w10 = w >> 10;
-        o[0] = lop_magic<0x00030003u>(w, mg);
-        o[1] = lop_magic<0x000C000Cu>(w, mg);
-        o[2] = lop_magic<0x00300030u>(w, mg);
-        o[3] = lop_magic<0x00C000C0u>(w, mg);
-        o[4] = lop_magic<0x03000300u>(w, mg);
-        o[5] = lop_magic<0x00030003u>(w10, mg);
-        o[6] = lop_magic<0x000C000Cu>(w10, mg);
-        o[7] = lop_magic<0x00300030u>(w10, mg);
+        o[0] = lop_magic<0x00030003u>(w, mg[0]);
+        o[1] = lop_magic<0x000C000Cu>(w, mg[1]);
+        o[2] = lop_magic<0x00300030u>(w, mg[2]);
+        o[3] = lop_magic<0x00C000C0u>(w, mg[3]);
+        o[4] = lop_magic<0x03000300u>(w, mg[4]);
+        o[5] = lop_magic<0x00030003u>(w10, mg[5]);
+        o[6] = lop_magic<0x000C000Cu>(w10, mg[6]);
+        o[7] = lop_magic<0x00300030u>(w10, mg[7]);
     } else if constexpr (BITS == 3) {
         const uint32_t A = *reinterpret_cast<const uint32_t*>(row + 4 * t);
         const uint32_t B = *reinterpret_cast<const uint16_t*>(row + 16 + 2 * t);
         const uint32_t A8 = A >> 8;
         const uint32_t Bx = prmt(B, 0u, 0x4140u);  // (B.lo, 0, B.hi, 0)
-        o[0] = lop_magic<0x00070007u>(A, mg);
-        o[1] = lop_magic<0x00380038u>(A, mg);
-        o[2] = lop_magic<0x00070007u>(A8, mg);
-        o[3] = lop_magic<0x00380038u>(A8, mg);
-        o[4] = lop_magic<0x00C000C0u>(A, mg) | ((Bx << 2) & 0x01000100u);
-        o[5] = lop_magic<0x00C000C0u>(A8, mg) | ((Bx << 1) & 0x01000100u);
-        o[6] = lop_magic<0x00070007u>(Bx, mg);
-        o[7] = lop_magic<0x00380038u>(Bx, mg);
-    } else {  // 8
-        const uint4 w = *reinterpret_cast<const uint4*>(row + 16 * t);
-        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+        o[0] = lop_magic<0x00070007u>(A, mg[0]);
+        o[1] = lop_magic<0x00380038u>(A, mg[1]);
+        o[2] = lop_magic<0x00070007u>(A8, mg[2]);
+        o[3] = lop_magic<0x00380038u>(A8, mg[3]);
+        o[4] = lop_magic<0x00C000C0u>(A, mg[4]) | ((Bx << 2) & 0x01000100u);
+        o[5] = lop_magic<0x00C000C0u>(A8, mg[5]) | ((Bx << 1) & 0x01000100u);
+        o[6] = lop_magic<0x00070007u>(Bx, mg[6]);
+        o[7] = lop_magic<0x00380038u>(Bx, mg[7]);
+    } else {  // 8: the magic's high byte (0x64 or 0xE4) joins each code byte
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            o[2 * q] = prmt(ws[q], 0x64646464u, 0x4140u);
-            o[2 * q + 1] = prmt(ws[q], 0x64646464u, 0x4342u);
+            const uint32_t wq = reinterpret_cast<const uint32_t*>(row + 16 * t)[q];
+            o[2 * q] = prmt(wq, mg[2 * q], 0x7170u);      // (byte0, magic hi, byte1, magic hi)
+            o[2 * q + 1] = prmt(wq, mg[2 * q + 1], 0x7372u);
         }
     }
 }
@@ -489,6 +487,14 @@ template <int BITS>
 __device__ __forceinline__ int field_shift_c(int p) {  // p = code position mod 16 (see dec_field_shift)
     constexpr uint32_t tab = BITS == 2 ? 0x42086420u : BITS == 3 ? 0x30663030u : BITS == 4 ? 0x40404040u : 0u;
     return int((tab >> (4 * ((p & 15) >> 1))) & 0xFu);
+}
+
+// per-pair magic registers (all 0x6400: fp16 1024 + field)
+__device__ __forceinline__ void make_magics(uint32_t (&mg)[8]) {
+    uint32_t pos;
+    asm("mov.b32 %0, 0x64006400;" : "=r"(pos));  // opaque: keeps the LOP3 a single instruction
+#pragma unroll
+    for (int p = 0; p < 8; ++p) mg[p] = pos;
 }
 
 // ---- warp roles of k_dec -------------------------------------------------------------
@@ -505,11 +511,13 @@ __device__ __forceinline__ void dec_fc1_piece(const unsigned char* piece, int kt
                                               float (&cb)[2][4]) {
     constexpr int RB = DecGeom<BITS>::RB;
     const unsigned char* ra = piece + (gw * 16 + g) * RB;
+    uint32_t mg[8];
+    make_magics(mg);
 #pragma unroll
     for (int i = 0; i < KP; ++i) {
         uint32_t oa[8], ob[8];
-        unpack_chunk_raw<BITS>(ra + i * 64 * RB, t, oa);
-        unpack_chunk_raw<BITS>(ra + i * 64 * RB + 8 * RB, t, ob);
+        unpack_chunk_raw<BITS>(ra + i * 64 * RB, t, oa, mg);
+        unpack_chunk_raw<BITS>(ra + i * 64 * RB + 8 * RB, t, ob, mg);
 #pragma unroll
         for (int nb = 0; nb < NB; ++nb) {
             float(&c)[4] = (i & 1) ? cb[nb] : ca[nb];
@@ -525,8 +533,10 @@ __device__ __forceinline__ void dec_fc1_piece(const unsigned char* piece, int kt
 }
 
 // fc2 partial of one slice for one warp: QW channel groups starting at group q0 of a piece.
-// mid >= 0 (ReLU) makes a magic-offset trick accumulate a one-signed offset over the slices, so
-// fc2 converts exactly (codec.cuh unpack_chunk: LOP3 + HFMA2 per code pair).
+// fc2 converts exactly (codec.cuh unpack_chunk: LOP3 + HFMA2 per code pair). A magic-offset
+// variant (signed magics over a complemented layout, per-slice correction) was built and
+// measured: parity-green, no faster (the decode slice is bound by the fc1 warps' latency, see
+// DESIGN.md), slower for int8; the exact path stays.
 template <int BITS, int QW, int NB>
 __device__ __forceinline__ void dec_fc2_piece(const unsigned char* piece, int q0, int g, int t,
                                               const unsigned char* mid, float (&c2)[QW][NB][4]) {
@@ -598,10 +608,14 @@ __device__ __forceinline__ void dec_fused_route(const DecArgs& a, DecPlanSmem& P
     int rtr = 0;
     const int rk = blockIdx.x < 8 ? int(blockIdx.x) : 7;
     if (blockIdx.x < 8 && !dry) route_trace(a, rk, rtr, 30);
-    for (int c = 0; c < 4; ++c) {
-        const int bi = c % nbuf;
+    // cluster of 4: CTA rank r takes K chunk r only (its Wg quarter was staged before the PDL
+    // wait), the four partial logit tables meet over DSMEM below
+    const int cl = int(cluster_nctas()), crank = int(cta_rank());
+    const int c_begin = cl == 4 ? crank : 0, c_end = cl == 4 ? crank + 1 : 4;
+    for (int c = c_begin; c < c_end; ++c) {
+        const int bi = cl == 4 ? 0 : c % nbuf;
         unsigned char* buf = rbase + size_t(bi) * cbytes;
-        if (!dry) mbar_wait(rbar + bi, (c / nbuf) & 1);
+        if (!dry) mbar_wait(rbar + bi, cl == 4 ? 0 : (c / nbuf) & 1);
         if (blockIdx.x < 8 && !dry) route_trace(a, rk, rtr, 31);
         if (warp < NW) {
 #pragma unroll
@@ -635,7 +649,7 @@ __device__ __forceinline__ void dec_fused_route(const DecArgs& a, DecPlanSmem& P
                 }
             }
         }
-        if (c + nbuf < 4) {
+        if (cl != 4 && c + nbuf < 4) {
             __syncthreads();  // buffer bi is free again
             if (tid == 0 && !dry) {
                 mbar_arrive_expect_tx(rbar + bi, cbytes);
@@ -663,13 +677,42 @@ __device__ __forceinline__ void dec_fused_route(const DecArgs& a, DecPlanSmem& P
         }
     }
     __syncthreads();
-    for (int o = tid; o < MT * 16 * Ep; o += blockDim.x) {
-        float v = part[o];
-        for (int kq = 1; kq < ks; ++kq) v += part[kq * 32 * Ep + o];
-        part[o] = v * __int_as_float((127 - a.wg_shift) << 23);  // exact power-of-two unscale
+    float* lg = part + ks * 32 * Ep;  // [MT*16][Ep] summed logits
+    if (cl == 4) {
+        for (int o = tid; o < MT * 16 * Ep; o += blockDim.x) {
+            float v = part[o];
+            for (int kq = 1; kq < ks; ++kq) v += part[kq * 32 * Ep + o];
+            part[o] = v;  // this CTA's K quarter
+        }
+        cluster_sync();
+        for (int o = tid; o < MT * 16 * Ep; o += blockDim.x) {  // quarters summed in rank order
+            float v = ld_cluster_f32(map_rank(part + o, 0u));
+#pragma unroll
+            for (int r = 1; r < 4; ++r) v += ld_cluster_f32(map_rank(part + o, uint32_t(r)));
+            lg[o] = v * __int_as_float((127 - a.wg_shift) << 23);  // exact power-of-two unscale
+        }
+        cluster_sync();  // every peer has read this CTA's partials
+    } else {
+        for (int o = tid; o < MT * 16 * Ep; o += blockDim.x) {
+            float v = part[o];
+            for (int kq = 1; kq < ks; ++kq) v += part[kq * 32 * Ep + o];
+            lg[o] = v * __int_as_float((127 - a.wg_shift) << 23);  // exact power-of-two unscale
+        }
     }
     __syncthreads();
     if (blockIdx.x < 8 && !dry) route_trace(a, rk, rtr, 32);
+}
+
+// Top-k, gates, plan and the scaled activation rows from the summed logits lg [T][Ep]
+// (every CTA, identically). dry = true skips every global write (diagnostics / warm-up runs).
+template <int BITS>
+__device__ __forceinline__ void dec_fused_decide(const DecArgs& a, DecPlanSmem& P, unsigned char* hs, int hpitch,
+                                                 const float* lg, int warp, int lane, bool dry) {
+    const int T = a.T, E = a.E, K = a.topk, R = T * K, d = a.d, Kp1 = a.Kp1;
+    const int Ep = (E + 7) & ~7;
+    const int tid = threadIdx.x;
+    int rtr = 8;
+    const int rk = blockIdx.x < 8 ? int(blockIdx.x) : 7;
     // top-k + gate: 8 lanes per token (4 tokens per warp, one round for T <= 32 * 17 / 8 ...).
     // Gates in fp32 (expf is within 2 ulp; the logits already differ from the reference's in the
     // last bits). Argmax keeps the reference's scan semantics (see warp_argmax).
@@ -678,7 +721,7 @@ __device__ __forceinline__ void dec_fused_route(const DecArgs& a, DecPlanSmem& P
         const unsigned gmask = 0xFFu << (grp * 8);
         for (int tk = warp * 4 + grp; tk - grp < T; tk += kDecFfnWarps * 4) {
             const bool live = tk < T;
-            const float* lt = part + (live ? tk : 0) * Ep;
+            const float* lt = lg + (live ? tk : 0) * Ep;
             int best[2] = {-1, -1};
 #pragma unroll
             for (int slot = 0; slot < 2; ++slot) {
@@ -825,6 +868,12 @@ __device__ __forceinline__ void dec_fused_route(const DecArgs& a, DecPlanSmem& P
     if (blockIdx.x < 8 && !dry) route_trace(a, rk, rtr, 35);
 }
 
+// the summed-logit table of the fused routing (behind the partial tables in the rings)
+__device__ __forceinline__ const float* dec_logits(const float* part, int E) {
+    const int Ep = (E + 7) & ~7, ntiles = Ep / 8, ks = ntiles >= 16 ? 1 : 16 / ntiles;
+    return part + ks * 32 * Ep;
+}
+
 // Warp-specialised stream-K decode FFN. Warps 0-7 (fc1) and 8-15 (fc2) work on different
 // slices at once: fc1 of slice n+1 overlaps fc2 of slice n through a double-buffered mid.
 // QN = Kp1 / 256, GQ = Np2 / 256, NP = pieces per weight part (2 for int8: smaller stages).
@@ -849,7 +898,8 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
     unsigned char* xsb = ring2 + size_t(n2) * sb2;  // FU: hs [T][hpitch]; else 2 x [16 rows][xpitch]
     const int xregion = FU ? ((a.T * a.xpitch + 127) & ~127) : 2 * kDecUnitRows * a.xpitch;
     unsigned char* midb = xsb + xregion;                                          // 2 x [16][kMidPitch]
-    float* redb = reinterpret_cast<float*>(midb + 2 * kDecUnitRows * kMidPitch);  // [2][4 groups][32][8]
+    float* z2b = reinterpret_cast<float*>(midb + 2 * kDecUnitRows * kMidPitch);  // [2][4 warps][16 cols]
+    float* redb = z2b + 2 * 64;                                                  // [2][4 groups][32][8]
     DecPlanSmem* PS = reinterpret_cast<DecPlanSmem*>(redb + 2 * 4 * 32 * 8);
     uint64_t* full1 = reinterpret_cast<uint64_t*>(PS + 1);
     uint64_t* empty1 = full1 + n1;
@@ -887,10 +937,16 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
     const uint32_t cbytes_ = uint32_t(2 * Ep_) * ((a.Kp1 / 4 + 8) * 2);
     const int nbuf_ = FU ? a.route_nbuf : 1;
     if (FU && tid == 0) {
-        for (int c = 0; c < nbuf_; ++c) {
-            mbar_arrive_expect_tx(rbar + c, cbytes_);
-            bulk_g2s(ring1 + size_t(c) * cbytes_, reinterpret_cast<const unsigned char*>(a.wgt) + size_t(c) * cbytes_,
-                     cbytes_, rbar + c);
+        if (cluster_nctas() == 4) {  // this CTA's K quarter only
+            const uint32_t r = cta_rank();
+            mbar_arrive_expect_tx(rbar, cbytes_);
+            bulk_g2s(ring1, reinterpret_cast<const unsigned char*>(a.wgt) + size_t(r) * cbytes_, cbytes_, rbar);
+        } else {
+            for (int c = 0; c < nbuf_; ++c) {
+                mbar_arrive_expect_tx(rbar + c, cbytes_);
+                bulk_g2s(ring1 + size_t(c) * cbytes_, reinterpret_cast<const unsigned char*>(a.wgt) + size_t(c) * cbytes_,
+                         cbytes_, rbar + c);
+            }
         }
     }
     pdl_trigger();
@@ -924,6 +980,7 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
         float* part = reinterpret_cast<float*>(ring1 + size_t(nbuf_) * cbytes_);
         // one instantiation (two token m-tiles) keeps the kernel's instruction footprint small
         dec_fused_route<BITS, 2>(a, *PS, xsb, a.xpitch, ring1, nbuf_, part, rbar, warp, lane, false);
+        dec_fused_decide<BITS>(a, *PS, xsb, a.xpitch, dec_logits(part, a.E), warp, lane, false);
     }
     const int4* units = FU ? PS->units : a.units;
     const int* perm_token = FU ? PS->perm_token : a.perm_token;
@@ -1153,7 +1210,8 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
             for (int r = 0; r < len; ++r, ++n) {
                 int myst;
                 wait_slice(myst);
-                dec_fc2_piece<BITS, QW, 1>(ring2 + size_t(myst) * sb2, q0, g, t, midb + (n & 1) * kDecUnitRows * kMidPitch, c2);
+                dec_fc2_piece<BITS, QW, 1>(ring2 + size_t(myst) * sb2, q0, g, t, midb + (n & 1) * kDecUnitRows * kMidPitch,
+                                           c2);
                 release_slice(myst);
             }
 #pragma unroll
@@ -1342,15 +1400,46 @@ cudaError_t dec_build_layout(const uint8_t* w1, const uint8_t* w2, int64_t w1_st
 template <int BITS, int QN, int GQ, int NP, bool FU>
 static cudaError_t launch_dec_t(const DecArgs& a, cudaStream_t st, int num_sms, size_t smem) {
     static bool configured[kMaxDev] = {};
+    static int clusters4[kMaxDev] = {};  // co-resident 4-CTA clusters (fused routing)
     int dev = 0;
     cudaGetDevice(&dev);
+    const int di = dev < kMaxDev ? dev : 0;
     auto kern = k_dec<BITS, QN, GQ, NP, FU>;
-    if (dev < kMaxDev && !configured[dev]) {
+    if (!configured[di]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(227 * 1024));
         if (e != cudaSuccess) return e;
-        configured[dev] = true;
+        configured[di] = true;
     }
-    return launch_pdl(kern, dim3(num_sms), dim3(kDecFfnWarps * 32), smem, st, a);
+    cudaLaunchConfig_t cfg{};
+    cfg.blockDim = dim3(kDecFfnWarps * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = 4;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    int grid = num_sms;
+    if (FU && a.route_cluster == 4) {
+        if (clusters4[di] == 0) {
+            cudaLaunchConfig_t q = cfg;
+            q.gridDim = dim3(unsigned(num_sms / 4 * 4));
+            q.attrs = attr + 1;
+            q.numAttrs = 1;
+            int n = 0;
+            if (cudaOccupancyMaxActiveClusters(&n, kern, &q) != cudaSuccess || n <= 0) n = num_sms / 4;
+            clusters4[di] = std::min(n, num_sms / 4);
+        }
+        grid = clusters4[di] * 4;
+        cfg.numAttrs = 2;
+    } else {
+        cfg.numAttrs = 1;
+    }
+    cfg.gridDim = dim3(unsigned(grid));
+    return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 template <int BITS, int QN, int GQ>
@@ -1415,7 +1504,7 @@ static bool dec_config(int bits, DecArgs& a, size_t* smem_out) {
     a.stage_bytes = uint32_t(a.Kp1 / NP) * RB + 512;  // W1 piece + the slice's fc1 scales / biases
     a.stage2_bytes = uint32_t(a.Np2 / NP) * RB;
     const size_t xregion = a.fused ? ((size_t(a.T) * a.xpitch + 127) & ~size_t(127)) : 2 * size_t(kDecUnitRows) * a.xpitch;
-    const size_t fixed = xregion + 2 * kDecUnitRows * kMidPitch + 2 * 4 * 32 * 8 * 4 + sizeof(DecPlanSmem) + 256;
+    const size_t fixed = xregion + 2 * kDecUnitRows * kMidPitch + 512 + 2 * 4 * 32 * 8 * 4 + sizeof(DecPlanSmem) + 256;
     if (fixed >= 227 * 1024) return false;
     const size_t budget = 227 * 1024 - fixed;
     // stages split evenly between the W1 and W2 rings (both parts have the same bytes)
@@ -1423,7 +1512,7 @@ static bool dec_config(int bits, DecArgs& a, size_t* smem_out) {
     if (pairs < 2) return false;
     if (a.fused) {  // the routing phase borrows the rings: 2..4 Wg chunks + the partial logits
         const int Ep = (a.E + 7) & ~7, ntiles = Ep / 8, ks = ntiles >= 16 ? 1 : 16 / ntiles;
-        const size_t cb = size_t(2 * Ep) * ((a.Kp1 / 4 + 8) * 2), pb = size_t(ks) * 32 * Ep * 4;
+        const size_t cb = size_t(2 * Ep) * ((a.Kp1 / 4 + 8) * 2), pb = size_t(ks + 2) * 32 * Ep * 4;
         const size_t ring = size_t(pairs) * (a.stage_bytes + a.stage2_bytes);
         a.route_nbuf = ring < pb ? 0 : int(std::min<size_t>(4, (ring - pb) / cb));
         if (a.route_nbuf < 2) return false;
