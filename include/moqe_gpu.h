@@ -46,6 +46,7 @@ typedef enum moqe_status {
 
 typedef enum moqe_granularity { MOQE_PER_CHANNEL = 0, MOQE_PER_TENSOR = 1 } moqe_granularity;
 typedef enum moqe_dtype { MOQE_F32 = 0, MOQE_F16 = 1 } moqe_dtype;
+typedef enum moqe_scheme { MOQE_SCHEME_LINEAR = 0, MOQE_SCHEME_LOG = 1 } moqe_scheme; /* quant.hpp:11 */
 
 typedef struct moqe_bank* moqe_bank_t;
 
@@ -122,6 +123,15 @@ moqe_status moqe_gpu_bank_create_g(int n_experts, int64_t d_model, int64_t d_ffn
                                    const uint8_t* packed_w1, const float* scales1,
                                    const uint8_t* packed_w2, const float* scales2, const float* b1,
                                    const float* b2, int inputs_on_device, moqe_bank_t* out);
+
+/* bank_create with the quantization scheme (Scheme, quant.hpp:11): MOQE_SCHEME_LINEAR or
+ * MOQE_SCHEME_LOG (quantize_log, quant.cpp:179-224: field = sign bit + k, weight = +-s * 2^-k;
+ * the same packed byte stream, bitpack.cpp:18-39). Log banks run on the tcgen05 path, which
+ * decodes the fields to exact fp16 +-2^-k in staging; bits 2, 3, 4 (log int8 -> NOT_SUPPORTED). */
+moqe_status moqe_gpu_bank_create_ex(int n_experts, int64_t d_model, int64_t d_ffn, int bits, int scheme,
+                                    int granularity, const uint8_t* packed_w1, const float* scales1,
+                                    const uint8_t* packed_w2, const float* scales2, const float* b1,
+                                    const float* b2, int inputs_on_device, moqe_bank_t* out);
 moqe_status moqe_gpu_bank_destroy(moqe_bank_t bank);
 /* Router weights Wg [d_model x n_experts] f32 kept with the bank
  * (RouterState, include/moqe/model.hpp:56-58). Blocking. */

@@ -6,9 +6,9 @@
 // linked (or LD_PRELOADed) ahead of the reference's libmoqe.so. The reference library is built
 // -fPIC, so its own callers (ffn_block, model.cpp:399-417, and everything above it:
 // model_forward, run_sensitivity, the CLI) reach this definition through the PLT and link
-// unchanged. Banks of linear-quantized experts run on the GPU through the C-ABI
-// (include/moqe_gpu.h); everything else (float or log-scale experts, mixed banks, and the
-// reference's argument errors) goes to the reference implementation found with
+// unchanged. Banks of quantized experts (linear, or log-scale with 2..4 bits) run on the GPU
+// through the C-ABI (include/moqe_gpu.h); everything else (float experts, log int8, mixed
+// banks, and the reference's argument errors) goes to the reference implementation found with
 // dlsym(RTLD_NEXT), so results and exceptions stay the reference's.
 //
 // Device banks are cached by CONTENT, not by address: ffn_block builds a stack-local
@@ -117,8 +117,8 @@ bool gpu_eligible(const ExpertBank& bank) {
     for (const auto& ew : bank.experts) {
         const auto* a = ew.w1.q;
         const auto* b = ew.w2.q;
-        if (!a || !b || a->scheme != moqe::Scheme::LinearAbsMax || b->scheme != moqe::Scheme::LinearAbsMax)
-            return false;
+        if (!a || !b || a->scheme != q0->scheme || b->scheme != q0->scheme) return false;
+        if (q0->scheme == moqe::Scheme::LogScale && q0->bits == 8) return false;  // not a GPU scheme
         if (a->bits != q0->bits || b->bits != q0->bits || a->shape != q0->shape || b->shape != r0->shape ||
             a->granularity != q0->granularity || b->granularity != q0->granularity)
             return false;
@@ -168,9 +168,11 @@ DeviceBank& device_bank(const ExpertBank& bank) {
     DeviceBank db;
     db.addr = std::move(addr);
     db.fp = fp;
-    check(moqe_gpu_bank_create_g(E, d, f, bits, per_tensor ? MOQE_PER_TENSOR : MOQE_PER_CHANNEL, p1.data(), s1.data(),
-                                 p2.data(), s2.data(), b1.empty() ? nullptr : b1.data(),
-                                 b2.empty() ? nullptr : b2.data(), 0, &db.bank));
+    check(moqe_gpu_bank_create_ex(E, d, f, bits,
+                                  q0.scheme == moqe::Scheme::LogScale ? MOQE_SCHEME_LOG : MOQE_SCHEME_LINEAR,
+                                  per_tensor ? MOQE_PER_TENSOR : MOQE_PER_CHANNEL, p1.data(), s1.data(), p2.data(),
+                                  s2.data(), b1.empty() ? nullptr : b1.data(), b2.empty() ? nullptr : b2.data(), 0,
+                                  &db.bank));
     g_cache.push_front(std::move(db));
     return g_cache.front();
 }

@@ -23,9 +23,11 @@ int main() {
     spec.dec_layers = 2;
     Checkpoint ckpt = build_random_checkpoint(spec, 2310, 0.05f);
     int fails = 0;
-    for (int bits : {4, 3, 2}) {
-        Checkpoint q = quantize_model(ckpt, {LayerGroup::ExpertFFN}, bits, Scheme::LinearAbsMax,
-                                      Granularity::PerChannel, LayerSubset::All, LogScaleMode::MseOptimal, 4);
+    for (int variant = 0; variant < 4; ++variant) {
+        const int bits = variant == 3 ? 4 : 4 - variant;  // int4, int3, int2 linear; int4 log-scale
+        const Scheme scheme = variant == 3 ? Scheme::LogScale : Scheme::LinearAbsMax;
+        Checkpoint q = quantize_model(ckpt, {LayerGroup::ExpertFFN}, bits, scheme, Granularity::PerChannel,
+                                      LayerSubset::All, LogScaleMode::AbsMax, 4);
         std::vector<std::vector<int32_t>> probe = {{1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12}, {500, 400, 300, 7}};
         moqe_gpu_shim_enable(0);
         ForwardResult cpu = model_forward(probe, q, spec);
@@ -43,8 +45,9 @@ int main() {
             bad += dlt > 2e-3 + 1e-2 * std::fabs(r);
         }
         const bool det = gpu.final_hidden == gpu2.final_hidden;
-        std::printf("int%d: model_forward with %lld GPU moe_ffn_forward calls, final_hidden max |gpu - cpu| %.3e, "
-                    "%ld outside tolerance, repeat bit-identical %s\n", bits, calls, mx, bad, det ? "yes" : "no");
+        std::printf("%sint%d: model_forward with %lld GPU moe_ffn_forward calls, final_hidden max |gpu - cpu| %.3e, "
+                    "%ld outside tolerance, repeat bit-identical %s\n", scheme == Scheme::LogScale ? "log-" : "", bits,
+                    calls, mx, bad, det ? "yes" : "no");
         if (calls <= 0 || bad != 0 || !det) ++fails;
     }
     std::printf("%s\n", fails ? "FAIL" : "PASS");

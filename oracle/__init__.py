@@ -242,6 +242,9 @@ class Ref(_Lib):
         self._sig("ref_bank_destroy", None, [vp])
         self._sig("ref_bank_forward", i32, [vp, fp, i64, fp, fp, i32])
         self._sig("ref_hardware_threads", i32, [])
+        self._sig("ref_quantize_log", i32, [fp, i64, i64, i32, i32, i32, i8p, fp])
+        self._sig("ref_dequantize_log", i32, [i8p, fp, i64, i64, i32, i32, fp])
+        self._sig("ref_bank_create_log", vp, [i32, i64, i64, i32, i8p, fp, i8p, fp])
         self._sig("ref_write_moe_mqe1", i64, [C.c_char_p, C.c_char_p, i32, i64, i64, i32, i32, i8p, fp, i8p, fp,
                                               fp, fp, fp])
 
@@ -278,6 +281,27 @@ class Ref(_Lib):
                                                  _p(out, C.c_float)), "matmul_dequant_fused")
         return out
 
+    def quantize_log(self, a, bits, per_tensor=False, mse_optimal=True):
+        """moqe::quantize_log (quant.cpp:179-224): (codes [K,N] int8, scales f32)."""
+        a = np.ascontiguousarray(a, np.float32)
+        codes = np.zeros(a.shape, np.int8)
+        scales = np.zeros(1 if per_tensor else a.shape[1], np.float32)
+        _check(self.lib.ref_quantize_log(_p(a, C.c_float), a.shape[0], a.shape[1], bits, int(per_tensor),
+                                         int(mse_optimal), _p(codes, C.c_int8), _p(scales, C.c_float)),
+               "quantize_log")
+        return codes, scales
+
+    def dequantize_log(self, codes, scales, bits, per_tensor=False):
+        c = np.ascontiguousarray(codes, np.int8)
+        s = np.ascontiguousarray(scales, np.float32)
+        out = np.zeros(c.shape, np.float32)
+        _check(self.lib.ref_dequantize_log(_p(c, C.c_int8), _p(s, C.c_float), c.shape[0], c.shape[1], bits,
+                                           int(per_tensor), _p(out, C.c_float)), "dequantize")
+        return out
+
+    def log_bank(self, codes1, scales1, codes2, scales2, bits):
+        return RefBank(self, codes1, scales1, codes2, scales2, bits, None, None, log=True)
+
     def bank(self, codes1, scales1, codes2, scales2, bits, b1=None, b2=None):
         return RefBank(self, codes1, scales1, codes2, scales2, bits, b1, b2)
 
@@ -306,7 +330,7 @@ class Ref(_Lib):
 class RefBank:
     """Host-resident reference ExpertBank; forward = moqe::moe_ffn_forward."""
 
-    def __init__(self, ref: Ref, w1, s1, w2, s2, bits, b1, b2, float_bank=False):
+    def __init__(self, ref: Ref, w1, s1, w2, s2, bits, b1, b2, float_bank=False, log=False):
         self.ref = ref
         E, d, f = w1.shape
         self.E, self.d, self.f = E, d, f
@@ -319,7 +343,11 @@ class RefBank:
             keep.append(a)
             return a
 
-        if float_bank:
+        if log:
+            self.h = ref.lib.ref_bank_create_log(
+                E, d, f, bits, _p(arr(w1, np.int8), C.c_int8), _p(arr(s1, np.float32), C.c_float),
+                _p(arr(w2, np.int8), C.c_int8), _p(arr(s2, np.float32), C.c_float))
+        elif float_bank:
             self.h = ref.lib.ref_bank_create_float(
                 E, d, f, _p(arr(w1, np.float32), C.c_float), _p(arr(w2, np.float32), C.c_float),
                 _p(arr(b1, np.float32), C.c_float), _p(arr(b2, np.float32), C.c_float))

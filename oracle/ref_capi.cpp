@@ -16,6 +16,8 @@
 //   ref_bank_* / ref_moe_ffn_forward -> moqe::moe_ffn_forward proj/src/model.cpp:348-393
 //   ref_matmul_dequant_fused -> moqe::matmul_dequant_fused   proj/src/bench.cpp:11-47
 //   ref_write_moe_mqe1       -> moqe::write_checkpoint_file  proj/src/checkpoint.cpp:239-290
+//   ref_quantize_log / ref_dequantize_log / ref_bank_create_log -> moqe::quantize_log, dequantize,
+//                               moe_ffn_forward over log banks  proj/src/quant.cpp:97-243
 //
 // Status codes mirror include/moqe_gpu.h (0 ok, 1 invalid_argument,
 // 2 out_of_range, 3 range_error, 9 other).
@@ -137,6 +139,28 @@ int ref_dequantize(const int8_t* codes, const float* scales, int64_t rows, int64
     });
 }
 
+// log-scale scheme (quant.cpp:97-224): codes / scales of quantize_log (AbsMax or MseOptimal),
+// dequantize of log codes (quant.cpp:226-243)
+int ref_quantize_log(const float* a, int64_t rows, int64_t cols, int bits, int g, int mse_optimal,
+                     int8_t* codes_out, float* scales_out) {
+    return guarded([&] {
+        auto qt = moqe::quantize_log(make2d(a, rows, cols), bits, gran(g),
+                                     mse_optimal ? moqe::LogScaleMode::MseOptimal : moqe::LogScaleMode::AbsMax);
+        std::memcpy(codes_out, qt.codes.codes.data(), qt.codes.codes.size());
+        std::memcpy(scales_out, qt.scales.data(), qt.scales.size() * sizeof(float));
+    });
+}
+
+int ref_dequantize_log(const int8_t* codes, const float* scales, int64_t rows, int64_t cols, int bits, int g,
+                       float* out) {
+    return guarded([&] {
+        auto qt = make_qt(codes, scales, rows, cols, bits, g);
+        qt.scheme = moqe::Scheme::LogScale;
+        auto t = moqe::dequantize(qt);
+        std::memcpy(out, t.data.data(), t.data.size() * sizeof(float));
+    });
+}
+
 int64_t ref_packed_size(int bits, int64_t count) {
     int64_t r = -1;
     guarded([&] { r = static_cast<int64_t>(moqe::packed_size(bits, static_cast<size_t>(count))); });
@@ -178,6 +202,19 @@ int ref_matmul_dequant_fused(const int8_t* codes, const float* scales, int64_t k
         auto y = moqe::matmul_dequant_fused(make_qt(codes, scales, k, n, bits, g), make2d(x, m, k));
         std::memcpy(out, y.data.data(), y.data.size() * sizeof(float));
     });
+}
+
+// Log-scale bank (per-channel): as ref_bank_create with Scheme::LogScale tensors.
+void* ref_bank_create(int n_experts, int64_t d, int64_t f, int bits, const int8_t* codes1,
+                      const float* scales1, const int8_t* codes2, const float* scales2,
+                      const float* b1, const float* b2);
+void* ref_bank_create_log(int n_experts, int64_t d, int64_t f, int bits, const int8_t* codes1,
+                          const float* scales1, const int8_t* codes2, const float* scales2) {
+    auto* b = static_cast<RefBank*>(ref_bank_create(n_experts, d, f, bits, codes1, scales1, codes2, scales2,
+                                                    nullptr, nullptr));
+    for (auto& q : b->q1) q.scheme = moqe::Scheme::LogScale;
+    for (auto& q : b->q2) q.scheme = moqe::Scheme::LogScale;
+    return b;
 }
 
 // Quantized bank: codes1 [E][d*f] (W1 [d x f] row-major), scales1 [E][f];

@@ -15,6 +15,7 @@ LIB_PATH = os.path.join(HERE, "lib", "libmoqe_gpu.so")
 # status codes (moqe_status)
 OK, INVALID_ARGUMENT, OUT_OF_RANGE, RANGE_ERROR, CUDA_ERROR, NCCL_ERROR, NOT_SUPPORTED, CHECKPOINT_ERROR = range(8)
 PER_CHANNEL, PER_TENSOR = 0, 1
+SCHEME_LINEAR, SCHEME_LOG = 0, 1
 F32, F16 = 0, 1
 PATH_AUTO, PATH_GEMV, PATH_GEMM = 0, 1, 2
 
@@ -35,6 +36,8 @@ SIGNATURES = {
                                     C.POINTER(_vp)]),
     "moqe_gpu_bank_create_g": (_i32, [_i32, _i64, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32,
                                       C.POINTER(_vp)]),
+    "moqe_gpu_bank_create_ex": (_i32, [_i32, _i64, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32,
+                                       C.POINTER(_vp)]),
     "moqe_gpu_bank_destroy": (_i32, [_vp]),
     "moqe_gpu_bank_set_router": (_i32, [_vp, _vp, _i32]),
     "moqe_gpu_bank_weight_bytes": (_i64, [_vp]),

@@ -177,9 +177,12 @@ class ExpertBank:
                  packed_w1: torch.Tensor, scales1: torch.Tensor, packed_w2: torch.Tensor,
                  scales2: torch.Tensor, b1: Optional[torch.Tensor] = None,
                  b2: Optional[torch.Tensor] = None, router: Optional[torch.Tensor] = None,
-                 granularity: str = PER_CHANNEL):
+                 granularity: str = PER_CHANNEL, scheme: str = "linear"):
         """granularity: PER_CHANNEL (scales1 [E, d_ffn], scales2 [E, d_model]) or PER_TENSOR
-        (one scale per expert matrix: scales [E] or [E, 1]; quant.cpp:53-55)."""
+        (one scale per expert matrix: scales [E] or [E, 1]; quant.cpp:53-55). scheme: "linear"
+        (code * s) or "log" (quantize_log's sign + exponent fields, +-s * 2^-k; quant.cpp:97-243)."""
+        if scheme not in ("linear", "log"):
+            raise _lib.InvalidArgument("bank: scheme must be 'linear' or 'log'")
         self.E, self.d, self.f, self.bits = n_experts, d_model, d_ffn, bits
         lib = _lib.load()
         dev = packed_w1.is_cuda
@@ -189,8 +192,10 @@ class ExpertBank:
                 None if b1 is None else conv(b1, torch.float32),
                 None if b2 is None else conv(b2, torch.float32)]
         h = C.c_void_p()
-        check(lib.moqe_gpu_bank_create_g(n_experts, d_model, d_ffn, bits, _GRAN[granularity],
-                                         *[_ptr(t) for t in keep], 1 if dev else 0, C.byref(h)))
+        check(lib.moqe_gpu_bank_create_ex(n_experts, d_model, d_ffn, bits,
+                                          _lib.SCHEME_LOG if scheme == "log" else _lib.SCHEME_LINEAR,
+                                          _GRAN[granularity], *[_ptr(t) for t in keep], 1 if dev else 0,
+                                          C.byref(h)))
         self._h = h
         torch.cuda.synchronize()
         if router is not None:

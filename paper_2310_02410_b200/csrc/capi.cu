@@ -81,6 +81,7 @@ struct moqe_bank {
     float* smax1 = nullptr;  // [E] fc2 fixed-point bound constants (decode GEMV)
     float* bmax1 = nullptr;
     uint8_t* wdec = nullptr;  // decode layout (dec_build_layout), d_model <= 1024 only
+    int log = 0;              // log-scale experts (Scheme::LogScale): tcgen05 path only
     __half* wgt = nullptr;    // split gate weights for the fused decode routing (dec_split_wg)
     int wg_shift = 0;
     int64_t wdec_stride = 0, dec_slice = 0;
@@ -422,6 +423,20 @@ moqe_status moqe_gpu_bank_create_g(int n_experts, int64_t d_model, int64_t d_ffn
     return st;
 }
 
+moqe_status moqe_gpu_bank_create_ex(int n_experts, int64_t d_model, int64_t d_ffn, int bits, int scheme,
+                                    int granularity, const uint8_t* packed_w1, const float* scales1,
+                                    const uint8_t* packed_w2, const float* scales2, const float* b1, const float* b2,
+                                    int inputs_on_device, moqe_bank_t* out) {
+    if (scheme != MOQE_SCHEME_LINEAR && scheme != MOQE_SCHEME_LOG)
+        return fail(MOQE_INVALID_ARGUMENT, "bank_create: bad scheme");
+    if (scheme == MOQE_SCHEME_LOG && bits == 8)
+        return fail(MOQE_NOT_SUPPORTED, "bank_create: log-scale int8 (k up to 127) is not a GPU scheme");
+    moqe_status st = moqe_gpu_bank_create_g(n_experts, d_model, d_ffn, bits, granularity, packed_w1, scales1, packed_w2,
+                                            scales2, b1, b2, inputs_on_device, out);
+    if (st == MOQE_OK && scheme == MOQE_SCHEME_LOG) (*out)->log = 1;
+    return st;
+}
+
 moqe_status moqe_gpu_bank_destroy(moqe_bank_t bank) {
     if (bank) cudaDeviceSynchronize();
     free_bank(bank);
@@ -478,7 +493,11 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
     if (!h || !out) return fail(MOQE_INVALID_ARGUMENT, "moe_forward: null buffer");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     (void)cudaGetLastError();  // launch checks below must not see a stale error from unrelated calls
-    if (!pre && b->wdec && dec_enabled() && (path == MOQE_PATH_AUTO || path == MOQE_PATH_GEMV) &&
+    if (b->log) {  // log-scale codes: only the tcgen05 GEMM converts them (unpack_chunk_log)
+        if (path == MOQE_PATH_GEMV) return fail(MOQE_NOT_SUPPORTED, "moe_forward: log-scale banks take the GEMM path");
+        path = MOQE_PATH_GEMM;
+    }
+    if (!pre && !b->log && b->wdec && dec_enabled() && (path == MOQE_PATH_AUTO || path == MOQE_PATH_GEMV) &&
         dec_supported(t, top_k, int(b->d), b->E, b->Kp1, b->Np1, b->Np2)) {
         moqe_status s = ensure_dec_workspace(b);
         if (s != MOQE_OK) return s;
@@ -613,7 +632,7 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
     }
     if (need_gemm) {
         GemmArgs g{w.x_perm, w.mid, b->w1, b->w2, b->w1_stride, b->w2_stride, b->s1, b->s2, b->b1, b->b2,
-                   b->Kp1, b->Np1, b->Kp2, b->Np2, w.cap_rows, int(b->d), out, out_dtype == MOQE_F16, acc};
+                   b->Kp1, b->Np1, b->Kp2, b->Np2, w.cap_rows, int(b->d), out, out_dtype == MOQE_F16, acc, b->log};
         {
             KernelTimer kt(b, 3, st);
             ce = launch_gemm(b->bits, 1, g, P, st, b->num_sms);

@@ -132,3 +132,63 @@ __device__ __forceinline__ void unpack_chunk(const uint8_t* row, int t, uint32_t
 }
 
 }  // namespace moqe_gpu
+
+namespace moqe_gpu {
+
+// Log-scale codes (quant.cpp:18-27, :226-243): a field u = code + 2^(b-1) holds the sign in its
+// top bit and k = u & (2^(b-1) - 1); the weight is +-s * 2^-k. Two fields x (one per 16-bit
+// half, already shifted down to bit 0) become the exact fp16 pair (+-2^-k) as
+// (sign << 15) | ((15 - k) << 10); the per-channel s is applied in the epilogue like the
+// linear scale. b <= 4 (k <= 7: normal fp16).
+template <int BITS>
+__device__ __forceinline__ uint32_t log_pair(uint32_t x) {
+    constexpr uint32_t kmask = ((1u << (BITS - 1)) - 1u) * 0x00010001u;
+    const uint32_t sgn = (x >> (BITS - 1)) & 0x00010001u;
+    return (sgn << 15) | ((0x000F000Fu - (x & kmask)) << 10);
+}
+
+// Unpack chunk t of a tile row of log codes into 8 fp16 pairs (same field positions as
+// unpack_chunk; each field is shifted down by its position s before the exponent build).
+template <int BITS>
+__device__ __forceinline__ void unpack_chunk_log(const uint8_t* row, int t, uint32_t (&o)[8]) {
+    if constexpr (BITS == 4) {
+        const uint2 w = *reinterpret_cast<const uint2*>(row + 8 * t);
+        const uint32_t ws[2] = {w.x, w.y};
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const uint32_t a = ws[q], a8 = ws[q] >> 8;
+            o[4 * q + 0] = log_pair<4>(a & 0x000F000Fu);
+            o[4 * q + 1] = log_pair<4>((a >> 4) & 0x000F000Fu);
+            o[4 * q + 2] = log_pair<4>(a8 & 0x000F000Fu);
+            o[4 * q + 3] = log_pair<4>((a8 >> 4) & 0x000F000Fu);
+        }
+    } else if constexpr (BITS == 2) {
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(row + 4 * t);
+        const uint32_t w10 = w >> 10;
+        o[0] = log_pair<2>(w & 0x00030003u);
+        o[1] = log_pair<2>((w >> 2) & 0x00030003u);
+        o[2] = log_pair<2>((w >> 4) & 0x00030003u);
+        o[3] = log_pair<2>((w >> 6) & 0x00030003u);
+        o[4] = log_pair<2>((w >> 8) & 0x00030003u);
+        o[5] = log_pair<2>(w10 & 0x00030003u);
+        o[6] = log_pair<2>((w10 >> 2) & 0x00030003u);
+        o[7] = log_pair<2>((w10 >> 4) & 0x00030003u);
+    } else if constexpr (BITS == 3) {
+        const uint32_t A = *reinterpret_cast<const uint32_t*>(row + 4 * t);
+        const uint32_t B = *reinterpret_cast<const uint16_t*>(row + 16 + 2 * t);
+        const uint32_t A8 = A >> 8;
+        const uint32_t Bx = prmt(B, 0u, 0x4140u);  // (B.lo, 0, B.hi, 0)
+        o[0] = log_pair<3>(A & 0x00070007u);
+        o[1] = log_pair<3>((A >> 3) & 0x00070007u);
+        o[2] = log_pair<3>(A8 & 0x00070007u);
+        o[3] = log_pair<3>((A8 >> 3) & 0x00070007u);
+        o[4] = log_pair<3>(((A >> 6) & 0x00030003u) | ((Bx >> 4) & 0x00040004u));
+        o[5] = log_pair<3>(((A8 >> 6) & 0x00030003u) | ((Bx >> 5) & 0x00040004u));
+        o[6] = log_pair<3>(Bx & 0x00070007u);
+        o[7] = log_pair<3>((Bx >> 3) & 0x00070007u);
+    } else {
+        for (int i = 0; i < 8; ++i) o[i] = 0u;  // log8 is not a GPU scheme (k up to 127)
+    }
+}
+
+}  // namespace moqe_gpu

@@ -379,7 +379,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 for (int cc = 0; cc < 2; ++cc) {
                     const int c = 2 * hc + cc;
                     uint32_t o[8];
-                    unpack_chunk<BITS>(row, c, o);
+                    if (g.log_codes) unpack_chunk_log<BITS>(row, c, o);  // log-scale bank (quant.cpp:226-243)
+                    else unpack_chunk<BITS>(row, c, o);
                     // 16-byte chunks 2c, 2c+1 of the 128-byte row, swizzled by (row % 8)
                     *reinterpret_cast<uint4*>(arow + (((2 * c) ^ (m & 7)) << 4)) = make_uint4(o[0], o[1], o[2], o[3]);
                     *reinterpret_cast<uint4*>(arow + (((2 * c + 1) ^ (m & 7)) << 4)) = make_uint4(o[4], o[5], o[6], o[7]);
@@ -610,7 +611,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 for (int cc = 0; cc < 2; ++cc) {
                     const int c = 2 * hc + cc;
                     uint32_t o[8];
-                    unpack_chunk<BITS>(row, c, o);
+                    if (g.log_codes) unpack_chunk_log<BITS>(row, c, o);  // log-scale bank (quant.cpp:226-243)
+                    else unpack_chunk<BITS>(row, c, o);
                     *reinterpret_cast<uint4*>(arow + (((2 * c) ^ (m & 7)) << 4)) = make_uint4(o[0], o[1], o[2], o[3]);
                     *reinterpret_cast<uint4*>(arow + (((2 * c + 1) ^ (m & 7)) << 4)) = make_uint4(o[4], o[5], o[6], o[7]);
                 }

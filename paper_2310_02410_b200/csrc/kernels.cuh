@@ -137,6 +137,7 @@ struct GemmArgs {
     void* out;
     int out_f16;
     float* out_acc;
+    int log_codes;         // 1: log-scale bank (+-2^-k codes, unpack_chunk_log)
 };
 bool gemm_available();
 int gemm_block_n();
