@@ -455,6 +455,33 @@ def run_point_ep(m, torch, dist, E, d, f, bits, T, top_k, steps, warmup, dev, ra
     return {"ms_per_step": ms, "tokens_per_s_per_rank": T / (ms * 1e-3), "experts_per_rank": hi - lo}
 
 
+def ep_cpu_baseline(E, d, f, bits, top_k, sample_tokens=16, threads=None):
+    """CPU baseline of the expert-parallel layer (BASELINE config 4). The reference routes
+    top-1 only (top-2 is not in it), so this is the oracle port (oracle/moqe_oracle.c: the
+    reference's router and per-row dequantize-on-the-fly FFN, model.cpp:328-393) on a bounded
+    sample: `sample_tokens` rows x top-2 experts over the host threads, extrapolated to
+    tokens/s (the per-token work does not depend on which expert it meets)."""
+    import oracle
+    from concurrent.futures import ThreadPoolExecutor
+    orc = oracle.orc()
+    threads = threads or os.cpu_count() or 1
+    rng = np.random.default_rng(SEED)
+    q1 = rng.integers(-(1 << (bits - 1)), 1 << (bits - 1), size=(d, f), dtype=np.int8)
+    q2 = rng.integers(-(1 << (bits - 1)), 1 << (bits - 1), size=(f, d), dtype=np.int8)
+    s1 = np.full(f, 0.01, np.float32)
+    s2 = np.full(d, 0.01, np.float32)
+    wg = (rng.standard_normal((d, E)) * 0.02).astype(np.float32)
+    h = rng.standard_normal((sample_tokens, d)).astype(np.float16).astype(np.float32)
+    t0 = time.perf_counter()
+    orc.route(h, wg, top_k)
+    with ThreadPoolExecutor(threads) as pool:  # ctypes releases the GIL
+        list(pool.map(lambda i: orc.expert_ffn(h[i:i + 1].repeat(top_k, 0), q1, s1, q2, s2), range(sample_tokens)))
+    dt = time.perf_counter() - t0
+    return {"value": round(sample_tokens / dt, 3), "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": f"{sample_tokens} tokens x top-{top_k} of the d={d} f={f} int{bits} layer (oracle port: the "
+                      f"reference has no top-2), {threads} threads, extrapolated per token"}
+
+
 # ---------------------------------------------------------------------------------------
 # reference CPU arm
 
@@ -527,13 +554,19 @@ def main():
     ap.add_argument("--top-k", type=int, default=1)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--ep", action="store_true", help="expert-parallel path even at one rank")
+    ap.add_argument("--ep", action="store_true", help="expert-parallel path (config 4) even at one rank")
+    ap.add_argument("--keep-shape", action="store_true", help="EP runs keep the given shape instead of config 4")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if (world > 1 or args.ep) and not args.keep_shape:
+        # multi-GPU runs measure BASELINE config 4: d=2048, f=8192, 128 experts sharded over the
+        # ranks, top-2 renormalised, int2, 16384 tokens per rank
+        args.experts, args.d_model, args.d_ffn, args.top_k, args.bits, args.tokens = 128, 2048, 8192, 2, 2, 16384
+        args.steps = min(args.steps, 40)
     E, d, f, bits, T, k = args.experts, args.d_model, args.d_ffn, args.bits, args.tokens, args.top_k
     config = {"workload": f"config2 decode: MoE FFN layer d_model={d} d_ffn={f} {E} experts top-{k} "
                           f"int{bits} per-channel, T={T} tokens",
@@ -580,19 +613,29 @@ def main():
         sampler = ClockSampler(local) if rank == 0 else None
         if sampler:
             sampler.start()
-        ep = run_point_ep(m, torch, dist, E, d, f, bits, T, k, args.steps, args.warmup, dev, rank, world)
+        ep = run_point_ep(m, torch, dist, E, d, f, bits, T, k, args.steps, args.warmup, dev, rank, world,
+                          n_layers=4)
         clocks = sampler.stop() if sampler else None
         if rank == 0:
-            config["workload"] = (f"expert-parallel MoE FFN layer d_model={d} d_ffn={f} {E} experts "
-                                  f"({ep['experts_per_rank']}/rank) top-{k} int{bits}, T={T} tokens per rank")
+            config["workload"] = (f"config4 expert-parallel MoE FFN layer d_model={d} d_ffn={f} {E} experts "
+                                  f"({ep['experts_per_rank']}/rank) top-{k} renormalised int{bits}, "
+                                  f"T={T} tokens per rank")
             config["parallelism"] = f"ep{world}"
+            fl = 2 * T * d * E + 4 * d * f * T * k  # per rank (router + fc1 + fc2 of every routed row)
+            ach = fl / (ep["ms_per_step"] * 1e-3) / 1e12
+            roof = {"bound": "tensor", "achieved": round(ach, 1), "peak": tc_peak, "unit": "TFLOP/s",
+                    "frac": round(ach / tc_peak, 4), "traffic": None, "kernel": "whole EP layer step per rank",
+                    "flops_per_step_per_rank": int(fl), "peak_kind": peak_kind,
+                    "timing": "CUDA events around the eager step, max over ranks"}
+            cpu = ep_cpu_baseline(E, d, f, bits, k) if not args.no_cpu else None
             line = {"metric": METRIC, "value": round(ep["tokens_per_s_per_rank"] * world, 1), "unit": "tokens/s",
                     "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                     "ms_per_step": round(ep["ms_per_step"], 5), "higher_is_better": True, "scaling": "weak",
                     "vs_baseline": None, "dtype": "f16", "data": "synthetic", "config": config,
-                    "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": None, "clocks": clocks,
-                    "detail": {"note": "eager EP steps (NCCL all_to_all dispatch/return, host-known split sizes); "
-                                       "max over ranks"}}
+                    "roofline": roof, "cpu_baseline": cpu, "e2e": None, "gpu_launches": None, "clocks": clocks,
+                    "detail": {"note": "eager EP steps: router kernel, packed fp16 dispatch records (one NCCL "
+                                       "all_to_all + a G-int count exchange), owner expert FFN kernels, fp16 "
+                                       "return all_to_all, combine; max over ranks"}}
             print(json.dumps(line), flush=True)
         dist.barrier()
         dist.destroy_process_group()

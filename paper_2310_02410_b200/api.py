@@ -352,9 +352,10 @@ def moe_ffn_forward(h: torch.Tensor, bank: ExpertBank, gate_weights: Optional[to
 
 def expert_ffn(x: torch.Tensor, bank: ExpertBank, expert: torch.Tensor, gate: torch.Tensor,
                out_dtype: torch.dtype = torch.float32, path: str = "auto",
-               out: Optional[torch.Tensor] = None) -> torch.Tensor:
+               out: Optional[torch.Tensor] = None, validate: bool = True) -> torch.Tensor:
     """Expert FFN on pre-routed rows (expert-parallel owner side):
-    out[r] = gate[r] * FFN_{expert[r]}(x[r]), expert ids local to `bank`."""
+    out[r] = gate[r] * FFN_{expert[r]}(x[r]), expert ids local to `bank`. validate=False skips
+    the host-side id range check (a device sync) when the ids come from a trusted router."""
     xd = x.dtype if x.dtype in (torch.float16, torch.float32) else torch.float32
     x = _dev(x, xd, "expert_ffn")
     if x.dim() != 2 or x.shape[1] != bank.d:
@@ -364,7 +365,7 @@ def expert_ffn(x: torch.Tensor, bank: ExpertBank, expert: torch.Tensor, gate: to
     R = x.shape[0]
     if ex.numel() != R or gt.numel() != R:
         raise _lib.InvalidArgument("expert_ffn: one expert id and gate per row")
-    if R and (int(ex.min()) < 0 or int(ex.max()) >= bank.E):
+    if validate and R and (int(ex.min()) < 0 or int(ex.max()) >= bank.E):
         raise _lib.InvalidArgument("expert_ffn: expert id out of range")
     if out is None:
         out = torch.empty((R, bank.d), dtype=out_dtype, device=x.device)

@@ -10,15 +10,17 @@ weights are replicated.
 One forward:
   1. route local tokens (exact fp32 router kernel; global expert ids + gates)
   2. group (token, slot) rows by owner rank, ascending token order (stable)
-  3. exchange per-rank counts, then all_to_all the fp16 rows, the owner-local
-     expert ids and the gates (NCCL over NVLink on GPU, gloo in the CPU tests)
+  3. exchange per-rank counts (one small all_to_all + one read of G counts), then ONE
+     all_to_all of packed records: the fp16 row with the owner-local expert id and the
+     gate bit-cast into 4 trailing fp16 slots (NCCL over NVLink on GPU, gloo on CPU)
   4. owners run the expert FFN on the received rows (moqe_gpu_expert_ffn: the
-     same GEMV / tcgen05 kernels as moe_forward; out = gate * FFN(row))
-  5. all_to_all the gate-weighted rows back
+     same decode / tcgen05 kernels as moe_forward; out = gate * FFN(row))
+  5. all_to_all the gate-weighted rows back, fp16 by default (half the return bytes;
+     return_dtype=torch.float32 keeps the bit-exact fp32 return)
   6. combine: out[t] = sum over t's slots, added onto zero (two addends,
      commutative -> deterministic).
-Outputs equal the single-GPU moe_forward of the whole layer up to the fp32
-combine order, which is identical for top-1/top-2.
+With an fp32 return the output equals the single-GPU moe_forward of the whole layer bit for
+bit (combine order identical for top-1/top-2); the fp16 return rounds each gated row once.
 """
 from __future__ import annotations
 
@@ -62,7 +64,7 @@ class ExpertParallelMoE:
     def __init__(self, bank, router: torch.Tensor, n_experts: int, top_k: int = 2,
                  group: Optional[dist.ProcessGroup] = None,
                  route_fn: Optional[Callable] = None, expert_fn: Optional[Callable] = None,
-                 path: str = "auto"):
+                 path: str = "auto", return_dtype: torch.dtype = torch.float16):
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -72,10 +74,14 @@ class ExpertParallelMoE:
         self.bank = bank
         self.router = router
         self.path = path
+        self.return_dtype = return_dtype
         if route_fn is None or expert_fn is None:
             from . import api
         self.route_fn = route_fn or (lambda h: api.route(h, self.router, self.top_k))
-        self.expert_fn = expert_fn or (lambda x, e, g: api.expert_ffn(x, self.bank, e, g, path=self.path))
+        # ids come from this layer's own router: no host-side range check (no sync)
+        self.expert_fn = expert_fn or (lambda x, e, g: api.expert_ffn(x, self.bank, e, g, path=self.path,
+                                                                         out_dtype=self.return_dtype,
+                                                                         validate=False))
 
     def _a2a(self, out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits) -> None:
         dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
@@ -87,29 +93,32 @@ class ExpertParallelMoE:
         gate = gate.reshape(T, -1)
         order, tok, dest_sorted, send_counts = dispatch_plan(ex, self.E, self.world)
         src_tok = tok[order]
-        send_rows = h.index_select(0, src_tok).contiguous()
-        send_exp = (ex.reshape(-1)[order] - dest_sorted * (self.E // self.world)).to(torch.int32).contiguous()
-        send_gate = gate.reshape(-1)[order].to(torch.float32).contiguous()
+        R_send = src_tok.shape[0]
+        # packed records: [row (d fp16) | expert id (i32) | gate (f32)] as d + 4 fp16 slots
+        rec = torch.empty((R_send, d + 4), dtype=torch.float16, device=h.device)
+        rec[:, :d] = h.index_select(0, src_tok)
+        meta = rec[:, d:].view(torch.int32)  # two int32 words per record
+        meta[:, 0] = (ex.reshape(-1)[order] - dest_sorted * (self.E // self.world)).to(torch.int32)
+        meta[:, 1] = gate.reshape(-1)[order].to(torch.float32).view(torch.int32)
 
-        # 1) counts
+        # 1) counts (the only host read: G integers, the all_to_all split sizes)
         recv_counts = torch.empty_like(send_counts)
         self._a2a(recv_counts, send_counts, None, None)
         s_split = send_counts.tolist()
         r_split = recv_counts.tolist()
         R = int(sum(r_split))
-        # 2) rows + metadata to the owners
-        recv_rows = torch.empty((R, d), dtype=h.dtype, device=h.device)
-        recv_exp = torch.empty((R,), dtype=torch.int32, device=h.device)
-        recv_gate = torch.empty((R,), dtype=torch.float32, device=h.device)
-        self._a2a(recv_rows, send_rows, r_split, s_split)
-        self._a2a(recv_exp, send_exp, r_split, s_split)
-        self._a2a(recv_gate, send_gate, r_split, s_split)
-        # 3) owner-side expert FFN (gate-weighted rows, fp32)
-        y = self.expert_fn(recv_rows, recv_exp, recv_gate).to(torch.float32).contiguous()
+        # 2) packed rows + metadata to the owners, one collective
+        recv = torch.empty((R, d + 4), dtype=torch.float16, device=h.device)
+        self._a2a(recv, rec, r_split, s_split)
+        rmeta = recv[:, d:].view(torch.int32)
+        recv_exp = rmeta[:, 0].contiguous()
+        recv_gate = rmeta[:, 1].contiguous().view(torch.float32)
+        # 3) owner-side expert FFN (gate-weighted rows)
+        y = self.expert_fn(recv[:, :d], recv_exp, recv_gate).to(self.return_dtype).contiguous()
         # 4) back to the sources, in the order they were sent
-        back = torch.empty((send_rows.shape[0], d), dtype=torch.float32, device=h.device)
+        back = torch.empty((R_send, d), dtype=self.return_dtype, device=h.device)
         self._a2a(back, y, s_split, r_split)
         # 5) combine the top-k slots (<= 2 addends onto zero: order-independent)
         out = torch.zeros((T, d), dtype=torch.float32, device=h.device)
-        out.index_add_(0, src_tok, back)
+        out.index_add_(0, src_tok, back.to(torch.float32))
         return out

@@ -20,7 +20,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, E, d, f, bits, T, top_k, q):
+def _worker(rank, world, port, E, d, f, bits, T, top_k, q, ret16=False):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
@@ -51,29 +51,37 @@ def _worker(rank, world, port, E, d, f, bits, T, top_k, q):
                 out[r] = np.float32(g[r]) * y[0]
             return torch.from_numpy(out)
 
-        moe = ExpertParallelMoE(None, None, E, top_k=top_k, route_fn=route_fn, expert_fn=expert_fn)
+        moe = ExpertParallelMoE(None, None, E, top_k=top_k, route_fn=route_fn, expert_fn=expert_fn,
+                                return_dtype=torch.float16 if ret16 else torch.float32)
         got = moe.forward(torch.from_numpy(np.ascontiguousarray(h))).numpy()
         want = orc.moe_forward(h, L["wg"], L["q1"], L["s1"], L["q2"], L["s2"], top_k=top_k,
                                b1=L["b1"], b2=L["b2"])[0]
-        q.put((rank, bool(np.array_equal(got, want)), float(np.abs(got - want).max())))
+        if ret16:  # fp16 return rows: one rounding of each gated row (north_star tolerance)
+            ok = bool((np.abs(got - want) <= 2e-3 + 1e-2 * np.abs(want)).all())
+        else:
+            ok = bool(np.array_equal(got, want))
+        q.put((rank, ok, float(np.abs(got - want).max())))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("top_k", [1, 2])
-def test_ep_world2_matches_single_process(top_k):
+@pytest.mark.parametrize("world,top_k,ret16", [(2, 1, False), (2, 2, False), (4, 2, False), (4, 2, True)])
+def test_ep_matches_single_process(world, top_k, ret16):
+    """world 2 / 4 over gloo: fp32 return rows are bit-exact with the single-process oracle;
+    fp16 return rows (the GPU default) stay within the north_star tolerance."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    world, E, d, f, bits, T = 2, 8, 32, 64, 4, 13
-    procs = [ctx.Process(target=_worker, args=(r, world, port, E, d, f, bits, T, top_k, q)) for r in range(world)]
+    E, d, f, bits, T = 8, 32, 64, 4, 13
+    procs = [ctx.Process(target=_worker, args=(r, world, port, E, d, f, bits, T, top_k, q, ret16))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=180) for _ in range(world)]
     for p in procs:
         p.join(timeout=60)
-    for rank, exact, mx in sorted(res):
-        assert exact, f"rank {rank}: max abs diff {mx}"
+    for rank, ok, mx in sorted(res):
+        assert ok, f"rank {rank}: max abs diff {mx}"
 
 
 def test_dispatch_plan_stable_order():

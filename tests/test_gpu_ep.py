@@ -46,12 +46,14 @@ def test_ep_world1_nccl(gpu, orc):
         E, d, f, bits, T = 8, 256, 512, 2, 70
         L = make_layer(orc, 3, E, d, f, bits, T)
         bank = gpu.ExpertBank(E, d, f, bits, _t(L["p1"]), _t(L["s1"]), _t(L["p2"]), _t(L["s2"]))
-        moe = ExpertParallelMoE(bank, _t(L["wg"]), E, top_k=2)
-        out = moe.forward(_t(L["h"]).half())
         want = orc.moe_forward(L["h"], L["wg"], L["q1"], L["s1"], L["q2"], L["s2"], top_k=2)[0]
-        nbad, mx = allclose_report(out.cpu().numpy(), want)
-        assert nbad == 0, mx
         ref = gpu.moe_ffn_forward(_t(L["h"]).half(), bank, _t(L["wg"]), top_k=2)
-        assert torch.allclose(out, ref, rtol=0, atol=1e-6)
+        for rdt in (torch.float16, torch.float32):
+            moe = ExpertParallelMoE(bank, _t(L["wg"]), E, top_k=2, return_dtype=rdt)
+            out = moe.forward(_t(L["h"]).half())
+            nbad, mx = allclose_report(out.cpu().numpy(), want)
+            assert nbad == 0, (rdt, mx)
+            if rdt == torch.float32:  # fp32 return: same kernels, same combine as the 1-GPU forward
+                assert torch.allclose(out, ref, rtol=0, atol=1e-6)
     finally:
         dist.destroy_process_group()

@@ -33,8 +33,11 @@ def test_log_bank_vs_reference(gpu, orc, bits, E, d, f, T):
     q1 = np.zeros(w1.shape, np.int8); q2 = np.zeros(w2.shape, np.int8)
     s1 = np.zeros((E, f), np.float32); s2 = np.zeros((E, d), np.float32)
     for e in range(E):
-        q1[e], s1[e] = ref.quantize_log(w1[e], bits, mse_optimal=(E <= 8))
-        q2[e], s2[e] = ref.quantize_log(w2[e], bits, mse_optimal=(E <= 8))
+        # the reference's MSE-optimal scale search costs ~3.5 s per 256x512 matrix on one core:
+        # expert 0 takes it on the small shapes, the rest use the max-abs scale
+        mse = e == 0 and d * f <= 256 * 512
+        q1[e], s1[e] = ref.quantize_log(w1[e], bits, mse_optimal=mse)
+        q2[e], s2[e] = ref.quantize_log(w2[e], bits, mse_optimal=mse)
     p1 = np.stack([orc.pack(q1[e], bits) for e in range(E)])
     p2 = np.stack([orc.pack(q2[e], bits) for e in range(E)])
     bank = gpu.ExpertBank(E, d, f, bits, _t(p1), _t(s1), _t(p2), _t(s2), router=_t(wg), scheme="log")
