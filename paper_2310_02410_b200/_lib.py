@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libmoqe_gpu.so")
+# MOQE_GPU_LIB: an alternate build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("MOQE_GPU_LIB") or os.path.join(HERE, "lib", "libmoqe_gpu.so")
 
 # status codes (moqe_status)
 OK, INVALID_ARGUMENT, OUT_OF_RANGE, RANGE_ERROR, CUDA_ERROR, NCCL_ERROR, NOT_SUPPORTED, CHECKPOINT_ERROR = range(8)

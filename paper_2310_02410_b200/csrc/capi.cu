@@ -120,8 +120,12 @@ bool fused_enabled() {  // MOQE_DEC_FUSED=0: decode keeps the separate router la
     static const bool v = [] { const char* s = getenv("MOQE_DEC_FUSED"); return !(s && atoi(s) == 0); }();
     return v;
 }
-int route_cluster_env() {  // MOQE_DEC_CLUSTER=1: every decode CTA routes alone (no 4-CTA clusters)
-    static const int v = [] { const char* s = getenv("MOQE_DEC_CLUSTER"); return (s && atoi(s) == 1) ? 1 : 4; }();
+int route_cluster_env() {  // MOQE_DEC_CLUSTER=1|2|4: CTAs per routing cluster of the fused decode
+    static const int v = [] {
+        const char* s = getenv("MOQE_DEC_CLUSTER");
+        const int c = s ? atoi(s) : 2;
+        return (c == 1 || c == 4) ? c : 2;
+    }();
     return v;
 }
 bool xrows_in_router() {  // MOQE_XROWS_IN_ROUTER=0: decode keeps the separate k_xrows launch

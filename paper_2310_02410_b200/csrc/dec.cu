@@ -40,6 +40,13 @@ constexpr int kDecThreads = 256;     // router CTA
 constexpr int kMidPitch = 64 * 2 + 16;  // bytes per mid row (pitch = 16 mod 128: conflict-free LDS.128)
 constexpr float kFix = 16777216.0f;     // 2^24 fixed-point scale of the fc2 partials
 constexpr int kMaxRouteSmem = 200 * 1024;
+#ifndef DEC_ROLE_SPLIT
+#define DEC_ROLE_SPLIT 0
+#endif
+#ifndef DEC_F1_UNROLL
+#define DEC_F1_UNROLL 8
+#endif
+constexpr int kF1Unroll = DEC_F1_UNROLL;
 
 __device__ __forceinline__ void red_add_s64(long long* p, long long v) {
     asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -114,7 +121,7 @@ __device__ __forceinline__ void dec_trace(const DecArgs& a, int base, int& n, in
 // router events: absolute slots after the FFN kernel's [grid][kDecTrace] block
 __device__ __forceinline__ void route_trace(const DecArgs& a, int rank, int& n, int ev) {
     if (a.trace && n < 32 && threadIdx.x == 0) {
-        unsigned long long* p = a.trace + (size_t(160 + rank) * kDecTrace + (ev >= 28 ? ev - 28 + 16 + n : n)) * 2;
+        unsigned long long* p = a.trace + (size_t(160 + rank) * kDecTrace + (ev >= 28 ? ev - 28 + 16 : n)) * 2;
         p[0] = unsigned(ev) | (static_cast<unsigned long long>(clock64()) << 8);
         p[1] = gtime_ns();
         ++n;
@@ -513,7 +520,7 @@ __device__ __forceinline__ void dec_fc1_piece(const unsigned char* piece, int kt
     const unsigned char* ra = piece + (gw * 16 + g) * RB;
     uint32_t mg[8];
     make_magics(mg);
-#pragma unroll
+#pragma unroll kF1Unroll
     for (int i = 0; i < KP; ++i) {
         uint32_t oa[8], ob[8];
         unpack_chunk_raw<BITS>(ra + i * 64 * RB, t, oa, mg);
@@ -580,149 +587,190 @@ struct DecPlanSmem {
     int n_units;
 };
 
-// Fused routing (every CTA, redundantly and bit-identically): logits = h . Wg on the tensor
-// cores with Wg pre-split by the bank into fp16 hi + lo (x 2^sw), streamed through two
-// buffers in four K chunks; parallel-order fp32 sums, so north_star's near-tie exemption
-// applies. Then top-k + gate (model.cpp:214-227, :339-346), the plan, and the activation
-// rows scaled in place by 2^-s(k) with their correction Z (see unpack_chunk_raw).
-template <int BITS, int MT>
-__device__ __forceinline__ void dec_fused_route(const DecArgs& a, DecPlanSmem& P, unsigned char* hs, int hpitch,
-                                             unsigned char* rbase, int nbuf, float* part, uint64_t* rbar,
-                                             int warp, int lane, bool dry) {
-    const int T = a.T, E = a.E, K = a.topk, R = T * K, d = a.d, Kp1 = a.Kp1;
-    const int Ep = (E + 7) & ~7, ntiles = Ep / 8;
-    const int ks = ntiles >= 16 ? 1 : 16 / ntiles;
+// Fused routing (every CTA, redundantly and bit-identically): logits = Wg^T . h on the tensor
+// cores, Wg (pre-split by the bank into fp16 hi + lo, x 2^sw, four K chunks) as the 16-expert A
+// tiles and the activation rows as 8-token B tiles; parallel-order fp32 sums, so north_star's
+// near-tie exemption applies. In a cluster of cl CTAs (2 or 4), rank r owns chunks
+// [r*4/cl, (r+1)*4/cl) (staged before the PDL wait). A work item is one (expert tile, token
+// tile); two warps split its K range and meet over a named barrier, then the item's 16 x 8 table
+// goes into every CTA of the cluster (its own included) with st.async (mbarrier complete_tx: no
+// cluster barrier, no fence). Each CTA adds the cl tables in rank order, so every CTA of every
+// cluster holds the same logits. Without a cluster the four chunks stream through nbuf buffers.
+// Layout behind the chunk buffers: lg [32][Ep + 4], the per-rank tables [cl][Ep16][32 tokens],
+// the K-half scratch [8 items][32 lanes][4].
+struct DecRouteGeom {
+    int Ep, Ep16, lgp, cl;
+    __host__ __device__ DecRouteGeom(int E, int cl_) {
+        Ep = (E + 7) & ~7;
+        Ep16 = (E + 15) & ~15;
+        lgp = Ep + 4;  // 16 B row skew: conflict-free per-token scans
+        cl = cl_;
+    }
+    __host__ __device__ size_t recv_off() const { return size_t(32) * lgp; }
+    __host__ __device__ size_t pair_off() const { return recv_off() + size_t(cl) * 32 * Ep16; }
+    __host__ __device__ size_t floats() const { return pair_off() + 8 * 32 * 4; }
+};
+
+__device__ __forceinline__ float redux_max_f32(float v) {  // warp-wide (sm_100a)
+    float m;
+    asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(m) : "f"(v));
+    return m;
+}
+__device__ __forceinline__ unsigned redux_min_u32(unsigned v) {
+    unsigned m;
+    asm volatile("redux.sync.min.u32 %0, %1, 0xffffffff;" : "=r"(m) : "r"(v));
+    return m;
+}
+
+__device__ __forceinline__ void st_async_v2(uint32_t addr, float x, float y, uint32_t bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(addr), "f"(x),
+                 "f"(y), "r"(bar)
+                 : "memory");
+}
+
+template <int BITS>
+__device__ __forceinline__ void dec_fused_route(const DecArgs& a, unsigned char* hs, int hpitch, unsigned char* rbase,
+                                                int nbuf, float* lg, uint64_t* rbar, int warp, int lane) {
+    const int T = a.T, E = a.E, Kp1 = a.Kp1;
+    const int cl = int(cluster_nctas()), crank = int(cta_rank());
+    const DecRouteGeom G(E, cl);
+    const int Ep = G.Ep, Ep16 = G.Ep16;
     const int Kc = Kp1 / 4, cpitch = (Kc + 8) * 2, nsteps = Kc / 16;
     const uint32_t cbytes = uint32_t(2 * Ep) * cpitch;
     const int tid = threadIdx.x, g = lane >> 2, t = lane & 3;
-    constexpr int NW = kF1Warps + kF2Warps;  // compute warps
-    float acc[2][MT][2][4];  // [work item (<= 2 per warp)][m-tile][hi, lo][4]
+    constexpr int NW = kF1Warps + kF2Warps;  // compute warps (16)
+    const int mtiles = Ep16 / 16, ttiles = (T + 7) >> 3, items = mtiles * ttiles;
+    const int ks = 2 * items <= NW ? 2 : 1;  // K halves per item (warp pairs)
+    float* recv = lg + G.recv_off();          // [cl][Ep16 experts][32 tokens]
+    const int tab = 32 * Ep16;
+    if (tid == 0) mbar_arrive_expect_tx(rbar + 5, uint32_t(cl) * items * 128 * 4);
+    int rtr = 0;
+    const int rk = blockIdx.x < 8 ? int(blockIdx.x) : 7;
+    if (blockIdx.x < 8) route_trace(a, rk, rtr, 30);
+    const int cpr = 4 / cl;  // K chunks of this CTA
+    const int c_begin = crank * cpr, c_end = c_begin + cpr;
+    // up to two items per warp (E > 128 with T > 16)
+    float acc[2][2][4];  // [item][hi, lo][4]
 #pragma unroll
     for (int x = 0; x < 2; ++x)
 #pragma unroll
-        for (int m = 0; m < MT; ++m)
+        for (int h2 = 0; h2 < 2; ++h2)
 #pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2)
-#pragma unroll
-                for (int i = 0; i < 4; ++i) acc[x][m][h2][i] = 0.f;
-    int rtr = 0;
-    const int rk = blockIdx.x < 8 ? int(blockIdx.x) : 7;
-    if (blockIdx.x < 8 && !dry) route_trace(a, rk, rtr, 30);
-    // cluster of 4: CTA rank r takes K chunk r only (its Wg quarter was staged before the PDL
-    // wait), the four partial logit tables meet over DSMEM below
-    const int cl = int(cluster_nctas()), crank = int(cta_rank());
-    const int c_begin = cl == 4 ? crank : 0, c_end = cl == 4 ? crank + 1 : 4;
+            for (int i = 0; i < 4; ++i) acc[x][h2][i] = 0.f;
     for (int c = c_begin; c < c_end; ++c) {
-        const int bi = cl == 4 ? 0 : c % nbuf;
-        unsigned char* buf = rbase + size_t(bi) * cbytes;
-        if (!dry) mbar_wait(rbar + bi, cl == 4 ? 0 : (c / nbuf) & 1);
-        if (blockIdx.x < 8 && !dry) route_trace(a, rk, rtr, 31);
-        if (warp < NW) {
-#pragma unroll
-            for (int x = 0; x < 2; ++x) {
-                const int wi = warp + x * NW;
-                if (wi >= ntiles * ks) break;
-                const int nt = wi % ntiles, kq = wi / ntiles;
-                for (int st = kq; st < nsteps; st += ks) {
-                    const int kk = st * 16, k0 = c * Kc + kk;
-                    uint32_t b[2][2];
-#pragma unroll
-                    for (int h2 = 0; h2 < 2; ++h2) {
-                        const unsigned char* br = buf + size_t(h2 * Ep + nt * 8 + g) * cpitch + (kk + 2 * t) * 2;
-                        b[h2][0] = *reinterpret_cast<const uint32_t*>(br);
-                        b[h2][1] = *reinterpret_cast<const uint32_t*>(br + 16);
-                    }
-#pragma unroll
-                    for (int m = 0; m < MT; ++m) {
-                        {
-                            // rows past the last token reuse row T-1 (their logits are discarded)
-                            const unsigned char* r0 = hs + size_t(min(m * 16 + g, T - 1)) * hpitch + (k0 + 2 * t) * 2;
-                            const unsigned char* r1 = hs + size_t(min(m * 16 + g + 8, T - 1)) * hpitch + (k0 + 2 * t) * 2;
-                            const uint32_t a0 = *reinterpret_cast<const uint32_t*>(r0);
-                            const uint32_t a1 = *reinterpret_cast<const uint32_t*>(r1);
-                            const uint32_t a2 = *reinterpret_cast<const uint32_t*>(r0 + 16);
-                            const uint32_t a3 = *reinterpret_cast<const uint32_t*>(r1 + 16);
-                            mma_16816(acc[x][m][0], a0, a1, a2, a3, b[0][0], b[0][1]);
-                            mma_16816(acc[x][m][1], a0, a1, a2, a3, b[1][0], b[1][1]);
-                        }
-                    }
-                }
-            }
-        }
-        if (cl != 4 && c + nbuf < 4) {
-            __syncthreads();  // buffer bi is free again
-            if (tid == 0 && !dry) {
-                mbar_arrive_expect_tx(rbar + bi, cbytes);
-                bulk_g2s(buf, reinterpret_cast<const unsigned char*>(a.wgt) + size_t(c + nbuf) * cbytes, cbytes, rbar + bi);
-            }
-        }
-    }
-    // partial logits [kq][token][expert] (hi + lo), then the fixed-order sum over kq
-    if (warp < NW) {
+        const int bi = cl > 1 ? c - c_begin : c % nbuf;
+        const unsigned char* buf = rbase + size_t(bi) * cbytes;
+        mbar_wait(rbar + bi, cl > 1 ? 0 : (c / nbuf) & 1);
 #pragma unroll
         for (int x = 0; x < 2; ++x) {
-            const int wi = warp + x * NW;
-            if (wi >= ntiles * ks) break;
-            const int nt = wi % ntiles, kq = wi / ntiles;
+            const int wi = warp + x * NW;  // (item, K half)
+            if (warp < NW && wi < items * ks) {
+                const int it = wi % items, kq = wi / items;
+                const int mt = it % mtiles, nt = it / mtiles;
+                const unsigned char* ar = buf + size_t(mt * 16 + g) * cpitch + 4 * t;
+                const unsigned char* br = hs + size_t(min(nt * 8 + g, T - 1)) * hpitch + (c * Kc + 2 * t) * 2;
+                for (int st = kq; st < nsteps; st += ks) {
+                    const int kk = st * 16;
 #pragma unroll
-            for (int m = 0; m < MT; ++m) {
-                {
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const int tok = m * 16 + g + 8 * (i >> 1), e = nt * 8 + 2 * t + (i & 1);
-                        part[(kq * 32 + tok) * Ep + e] = acc[x][m][0][i] + acc[x][m][1][i];
+                    for (int h2 = 0; h2 < 2; ++h2) {
+                        const unsigned char* aa = ar + size_t(h2 * Ep) * cpitch + kk * 2;
+                        const uint32_t a0 = *reinterpret_cast<const uint32_t*>(aa);
+                        const uint32_t a1 = *reinterpret_cast<const uint32_t*>(aa + 8 * cpitch);
+                        const uint32_t a2 = *reinterpret_cast<const uint32_t*>(aa + 16);
+                        const uint32_t a3 = *reinterpret_cast<const uint32_t*>(aa + 8 * cpitch + 16);
+                        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(br + kk * 2);
+                        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(br + kk * 2 + 16);
+                        mma_16816(acc[x][h2], a0, a1, a2, a3, b0, b1);
                     }
                 }
             }
         }
-    }
-    __syncthreads();
-    float* lg = part + ks * 32 * Ep;  // [MT*16][Ep] summed logits
-    if (cl == 4) {
-        for (int o = tid; o < MT * 16 * Ep; o += blockDim.x) {
-            float v = part[o];
-            for (int kq = 1; kq < ks; ++kq) v += part[kq * 32 * Ep + o];
-            part[o] = v;  // this CTA's K quarter
+        if (cl == 1 && c + nbuf < 4) {
+            __syncthreads();  // buffer bi is free again
+            if (tid == 0) {
+                mbar_arrive_expect_tx(rbar + bi, cbytes);
+                bulk_g2s(const_cast<unsigned char*>(buf), reinterpret_cast<const unsigned char*>(a.wgt) + size_t(c + nbuf) * cbytes,
+                         cbytes, rbar + bi);
+            }
         }
-        cluster_sync();
-        for (int o = tid; o < MT * 16 * Ep; o += blockDim.x) {  // quarters summed in rank order
-            float v = ld_cluster_f32(map_rank(part + o, 0u));
+    }
+#ifdef DEC_PLAN_TRACE
+    if (blockIdx.x < 8) route_trace(a, rk, rtr, 40);
+#endif
+    // K halves meet (warp pairs, named barriers 1..), then the item's table goes to every CTA
+    if (cl > 1) cluster_wait_acquire();  // the peers' barriers are initialised (arrived at kernel start)
+    float* pair = lg + G.pair_off();  // the second K half of each item: [items <= 8][32 lanes][4]
 #pragma unroll
-            for (int r = 1; r < 4; ++r) v += ld_cluster_f32(map_rank(part + o, uint32_t(r)));
-            lg[o] = v * __int_as_float((127 - a.wg_shift) << 23);  // exact power-of-two unscale
-        }
-        cluster_sync();  // every peer has read this CTA's partials
-    } else {
-        for (int o = tid; o < MT * 16 * Ep; o += blockDim.x) {
-            float v = part[o];
-            for (int kq = 1; kq < ks; ++kq) v += part[kq * 32 * Ep + o];
-            lg[o] = v * __int_as_float((127 - a.wg_shift) << 23);  // exact power-of-two unscale
+    for (int x = 0; x < 2; ++x) {
+        const int wi = warp + x * NW;
+        if (warp < NW && wi < items * ks) {
+            const int it = wi % items, kq = wi / items;
+            float v[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[i] = acc[x][0][i] + acc[x][1][i];
+            if (ks == 2) {
+                float4* pp = reinterpret_cast<float4*>(pair) + it * 32 + lane;
+                if (kq == 1) *pp = make_float4(v[0], v[1], v[2], v[3]);
+                named_bar_sync(1 + it, 64);
+                if (kq == 1) continue;
+                const float4 o = *pp;
+                v[0] += o.x; v[1] += o.y; v[2] += o.z; v[3] += o.w;
+            }
+            const int mt = it % mtiles, nt = it / mtiles;
+            // c0, c1: expert mt*16+g, tokens nt*8+2t, +1; c2, c3: expert + 8. Table [expert][token].
+            const int e0 = mt * 16 + g, tk0 = nt * 8 + 2 * t;
+            float* tb = recv + size_t(crank) * tab;
+            for (int r = 0; r < cl; ++r) {
+                const uint32_t bar = map_rank(rbar + 5, uint32_t(r));
+                st_async_v2(map_rank(tb + e0 * 32 + tk0, uint32_t(r)), v[0], v[1], bar);
+                st_async_v2(map_rank(tb + (e0 + 8) * 32 + tk0, uint32_t(r)), v[2], v[3], bar);
+            }
         }
     }
+#ifdef DEC_PLAN_TRACE
+    if (blockIdx.x < 8) route_trace(a, rk, rtr, 42);
+#endif
+    mbar_wait(rbar + 5, 0);
+#ifdef DEC_PLAN_TRACE
+    if (blockIdx.x < 8) route_trace(a, rk, rtr, 43);
+#endif
+    const float unscale = __int_as_float((127 - a.wg_shift) << 23);  // exact power of two
+    for (int e = warp; e < E; e += kDecFfnWarps)
+        for (int tk = lane; tk < T; tk += 32) {
+            float v = recv[e * 32 + tk];
+            for (int r = 1; r < cl; ++r) v += recv[size_t(r) * tab + e * 32 + tk];  // rank order
+            lg[tk * G.lgp + e] = v * unscale;
+        }
     __syncthreads();
-    if (blockIdx.x < 8 && !dry) route_trace(a, rk, rtr, 32);
+    if (blockIdx.x < 8) route_trace(a, rk, rtr, 32);
 }
 
-// Top-k, gates, plan and the scaled activation rows from the summed logits lg [T][Ep]
-// (every CTA, identically). dry = true skips every global write (diagnostics / warm-up runs).
+// Top-k, gates and the plan from the logits lg [T][Ep + 4] (every CTA computes the same plan),
+// and the activation rows scaled in place by 2^-s(k) (the fc1 weight field shifts) with the
+// per-token correction Z (see unpack_chunk_raw).
+//
+// Top-k: one warp per token; each lane scans its experts ascending with strict '>', then
+// redux.sync max (value) and min (index among the lanes holding the max) give the reference's
+// argmax semantics (model.cpp:339-341: ties -> lowest index, NaN skipped unless it sits at the
+// scan's first index). Gates in fp32 (expf is within 2 ulp; the logits already differ from the
+// reference's in the last bits).
+// Plan (warp 0, while the other warps scale the rows): lane l owns rows l and l + 32 (row =
+// token * k + slot). Equal-expert masks come from ten ballots per half (expert bits + a unique
+// tag for empty rows), giving each row's stable rank and its expert's count; experts are
+// ordered by their first row, and one shuffle scan over those first rows yields row offsets and
+// unit bases (units of <= 16 rows).
 template <int BITS>
 __device__ __forceinline__ void dec_fused_decide(const DecArgs& a, DecPlanSmem& P, unsigned char* hs, int hpitch,
-                                                 const float* lg, int warp, int lane, bool dry) {
-    const int T = a.T, E = a.E, K = a.topk, R = T * K, d = a.d, Kp1 = a.Kp1;
-    const int Ep = (E + 7) & ~7;
-    const int tid = threadIdx.x;
+                                                 const float* lg, int warp, int lane) {
+    const int T = a.T, E = a.E, K = a.topk, R = T * K, Kp1 = a.Kp1;
+    const int lgp = DecRouteGeom(E, 1).lgp;
     int rtr = 8;
     const int rk = blockIdx.x < 8 ? int(blockIdx.x) : 7;
-    // top-k + gate: 8 lanes per token (4 tokens per warp, one round for T <= 32 * 17 / 8 ...).
-    // Gates in fp32 (expf is within 2 ulp; the logits already differ from the reference's in the
-    // last bits). Argmax keeps the reference's scan semantics (see warp_argmax).
     {
-        const int sub = lane & 7, grp = lane >> 3;
-        const unsigned gmask = 0xFFu << (grp * 8);
-        for (int tk = warp * 4 + grp; tk - grp < T; tk += kDecFfnWarps * 4) {
-            const bool live = tk < T;
-            const float* lt = lg + (live ? tk : 0) * Ep;
-            int best[2] = {-1, -1};
+        for (int tk = warp; tk < T; tk += kDecFfnWarps) {  // one warp per token (warp-uniform)
+            const float* lt = lg + tk * lgp;
+            int best[2] = {0, 0};
+            float mx0 = 0.f;
 #pragma unroll
             for (int slot = 0; slot < 2; ++slot) {
                 if (slot == 1 && K == 1) break;
@@ -730,43 +778,43 @@ __device__ __forceinline__ void dec_fused_decide(const DecArgs& a, DecPlanSmem& 
                 const int first = skip == 0 ? 1 : 0;
                 float bv = -__int_as_float(0x7f800000);
                 int bi = 1 << 30;
-                for (int e = sub; e < E; e += 8) {
+                for (int e = lane; e < E; e += 32) {  // ascending, strict '>': lowest index per lane
                     const float v = lt[e];
                     if (e == skip || v != v) continue;
                     if (bi == (1 << 30) || v > bv) { bv = v; bi = e; }
                 }
-#pragma unroll
-                for (int o = 4; o; o >>= 1) {
-                    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-                    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                    if (oi != (1 << 30) && (bi == (1 << 30) || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; }
-                }
-                best[slot] = (lt[first] != lt[first]) ? first : (bi == (1 << 30) ? first : bi);
+                const float m = redux_max_f32(bv);  // warp max over the non-NaN logits
+                const unsigned bmin = redux_min_u32(bi != (1 << 30) && bv == m ? unsigned(bi) : 0xffffffffu);
+                best[slot] = (lt[first] != lt[first]) ? first : (bmin == 0xffffffffu ? first : int(bmin));
+                if (slot == 0) mx0 = m;
             }
             float g1 = 1.f, g2 = 0.f;
+#ifdef DEC_PLAN_TRACE
+            if (blockIdx.x < 8) route_trace(a, rk, rtr, 44);
+#endif
             if (K == 1) {
-                float mx = -__int_as_float(0x7f800000);
-                for (int e = sub; e < E; e += 8) mx = fmaxf(mx, lt[e]);
-#pragma unroll
-                for (int o = 4; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                const float mx = mx0;  // = fmaxf over every logit (fmaxf drops NaNs)
                 float sm = 0.f;
-                for (int e = sub; e < E; e += 8) sm += expf(lt[e] - mx);
+                for (int e = lane; e < E; e += 32) sm += expf(lt[e] - mx);
 #pragma unroll
-                for (int o = 4; o; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+                for (int o = 16; o; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
                 g1 = expf(lt[best[0]] - mx) / sm;
             } else {
                 const float z = expf(lt[best[1]] - lt[best[0]]);
                 g1 = 1.f / (1.f + z);
                 g2 = z / (1.f + z);
             }
-            if (live && sub == 0) {
+#ifdef DEC_PLAN_TRACE
+            if (blockIdx.x < 8) route_trace(a, rk, rtr, 46);
+#endif
+            if (lane == 0) {
                 P.ch_e[tk * K] = best[0];
                 P.ch_g[tk * K] = g1;
                 if (K == 2) {
                     P.ch_e[tk * K + 1] = best[1];
                     P.ch_g[tk * K + 1] = g2;
                 }
-                if (blockIdx.x == 0 && !dry) {
+                if (blockIdx.x == 0) {
                     a.expert[tk * K] = best[0];
                     a.gate[tk * K] = g1;
                     if (K == 2) {
@@ -775,103 +823,109 @@ __device__ __forceinline__ void dec_fused_decide(const DecArgs& a, DecPlanSmem& 
                     }
                 }
             }
-            (void)gmask;
         }
     }
     __syncthreads();
-    if (blockIdx.x < 8 && !dry) route_trace(a, rk, rtr, 33);
-    // plan (warp 0): rows grouped by expert, ascending (token, slot) inside; units of <= 16 rows.
-    // Lane l holds rows l and l + 32; per-half counts from match masks into two expert tables,
-    // stable ranks from the masks, offsets / unit bases from one shuffle scan over the experts.
+    if (blockIdx.x < 8) route_trace(a, rk, rtr, 33);
+#ifdef DEC_PLAN_TRACE
+    if (blockIdx.x < 8) route_trace(a, rk, rtr, 47);
+#endif
     if (warp == 0) {
-        int* tabA = P.cnt;  // rows per expert in rows 0..31
-        int* tabB = P.off;  // rows per expert in rows 32..63
-        for (int e = lane; e < E; e += 32) { tabA[e] = 0; tabB[e] = 0; }
-        __syncwarp();
-        const int ea = lane < R ? P.ch_e[lane] : 0x40000000 + lane;
-        const int eb = lane + 32 < R ? P.ch_e[lane + 32] : 0x40000040 + lane;
-        const unsigned ma = __match_any_sync(0xffffffffu, ea), mb = __match_any_sync(0xffffffffu, eb);
-        const unsigned ltm = (1u << lane) - 1u;
-        const int ra = __popc(ma & ltm), rbl = __popc(mb & ltm);
-        if (lane < R && ra == 0) tabA[ea] = __popc(ma);
-        if (lane + 32 < R && rbl == 0) tabB[eb] = __popc(mb);
-        __syncwarp();
-        const int rank_a = ra, rank_b = (lane + 32 < R ? tabA[eb] : 0) + rbl;
-        // exclusive scans over experts of rows and units (lane owns a contiguous expert range)
-        const int per = (E + 31) / 32, e0 = lane * per, e1 = min(E, e0 + per);
-        int sr = 0, su = 0;
-        for (int e = e0; e < e1; ++e) {
-            const int c = tabA[e] + tabB[e];
-            sr += c;
-            su += (c + kDecUnitRows - 1) / kDecUnitRows;
+        int ee[2];
+        float gg[2];
+#pragma unroll
+        for (int hb = 0; hb < 2; ++hb) {
+            const int row = lane + 32 * hb;
+            const bool ok = row < R;
+            ee[hb] = ok ? P.ch_e[row] : (0x200 | row);  // empty rows: unique tags >= 512
+            gg[hb] = ok ? P.ch_g[row] : 0.f;
         }
-        int ir = sr, iu = su;
+        // equal-expert masks: m[x][y] = lanes of half y whose row has the expert of my row in half x
+        unsigned m00 = 0xffffffffu, m01 = 0xffffffffu, m10 = 0xffffffffu, m11 = 0xffffffffu;
+#pragma unroll
+        for (int b = 0; b < 10; ++b) {
+            const unsigned ba = __ballot_sync(0xffffffffu, (ee[0] >> b) & 1);
+            const unsigned bb = __ballot_sync(0xffffffffu, (ee[1] >> b) & 1);
+            const bool xa = (ee[0] >> b) & 1, xb = (ee[1] >> b) & 1;
+            m00 &= xa ? ba : ~ba;
+            m01 &= xa ? bb : ~bb;
+            m10 &= xb ? ba : ~ba;
+            m11 &= xb ? bb : ~bb;
+        }
+        const unsigned ltm = (1u << lane) - 1u;
+        const int rank0 = __popc(m00 & ltm), rank1 = __popc(m10) + __popc(m11 & ltm);
+        const bool first0 = lane < R && (m00 & ltm) == 0;
+        const bool first1 = lane + 32 < R && m10 == 0 && (m11 & ltm) == 0;
+        const int cnt0 = __popc(m00) + __popc(m01), cnt1 = __popc(m11);  // first rows only
+        // (rows, units) of each expert at its first row, packed: rows | units << 16
+        const int v0 = first0 ? (cnt0 | (((cnt0 + kDecUnitRows - 1) / kDecUnitRows) << 16)) : 0;
+        const int v1 = first1 ? (cnt1 | (((cnt1 + kDecUnitRows - 1) / kDecUnitRows) << 16)) : 0;
+        int i0 = v0, i1 = v1;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const int vr = __shfl_up_sync(0xffffffffu, ir, o), vu = __shfl_up_sync(0xffffffffu, iu, o);
-            if (lane >= o) { ir += vr; iu += vu; }
+            const int u0 = __shfl_up_sync(0xffffffffu, i0, o), u1 = __shfl_up_sync(0xffffffffu, i1, o);
+            if (lane >= o) { i0 += u0; i1 += u1; }
         }
-        const int nu_tot = __shfl_sync(0xffffffffu, iu, 31);
-        int pr = ir - sr, pu = iu - su;
-        // per expert: offset, unit base, count -> ubase[] (offset in the low 16 bits, unit base above)
-        for (int e = e0; e < e1; ++e) {
-            const int c = tabA[e] + tabB[e];
-            P.ubase[e] = pr | (pu << 16);
-            for (int q = 0; q * kDecUnitRows < c; ++q)
-                P.units[pu + q] = make_int4(e, pr + q * kDecUnitRows, min(kDecUnitRows, c - q * kDecUnitRows), 0);
-            pr += c;
-            pu += (c + kDecUnitRows - 1) / kDecUnitRows;
+        const int tot0 = __shfl_sync(0xffffffffu, i0, 31);
+        const int x0 = i0 - v0, x1 = i1 - v1 + tot0;  // exclusive (rows | units << 16)
+#pragma unroll
+        for (int hb = 0; hb < 2; ++hb) {
+            const bool fr = hb == 0 ? first0 : first1;
+            if (fr) {
+                const int x = hb == 0 ? x0 : x1, c = hb == 0 ? cnt0 : cnt1, e = ee[hb];
+                for (int q = 0; q * kDecUnitRows < c; ++q)
+                    P.units[(x >> 16) + q] =
+                        make_int4(e, (x & 0xFFFF) + q * kDecUnitRows, min(kDecUnitRows, c - q * kDecUnitRows), 0);
+            }
         }
-        __syncwarp();
+        // row positions: offset of the expert's first row + rank
+        const int f0 = __ffs(m00) - 1;
+        const int f1 = m10 ? __ffs(m10) - 1 : __ffs(m11) - 1;
+        const int o00 = __shfl_sync(0xffffffffu, x0, f0 & 31);
+        const int o10 = __shfl_sync(0xffffffffu, x0, f1 & 31), o11 = __shfl_sync(0xffffffffu, x1, f1 & 31);
         if (lane < R) {
-            const int ps = (P.ubase[ea] & 0xFFFF) + rank_a;
-            P.perm_token[ps] = lane / K;
-            P.perm_gate[ps] = P.ch_g[lane];
+            const int ps = (o00 & 0xFFFF) + rank0;
+            P.perm_token[ps] = K == 2 ? lane >> 1 : lane;
+            P.perm_gate[ps] = gg[0];
             P.row_of[lane] = ps;
         }
         if (lane + 32 < R) {
-            const int ps = (P.ubase[eb] & 0xFFFF) + rank_b;
-            P.perm_token[ps] = (lane + 32) / K;
-            P.perm_gate[ps] = P.ch_g[lane + 32];
+            const int ps = ((m10 ? o10 : o11) & 0xFFFF) + rank1;
+            P.perm_token[ps] = K == 2 ? (lane + 32) >> 1 : lane + 32;
+            P.perm_gate[ps] = gg[1];
             P.row_of[lane + 32] = ps;
         }
-        if (lane == 0) P.n_units = nu_tot;
-    }
-    if (blockIdx.x < 8 && !dry) route_trace(a, rk, rtr, 34);
-    // activation rows scaled in place by 2^-s(k) (the fc1 weight field shifts) + Z per token
-    constexpr int bias = 1 << (BITS - 1);
-    for (int tk = warp; tk < T; tk += kDecFfnWarps) {
-        unsigned char* row = hs + size_t(tk) * hpitch;
-        float zf = 0.f;
-        for (int k0 = lane * 8; k0 < Kp1; k0 += 256) {
-            uint4 q = *reinterpret_cast<const uint4*>(row + k0 * 2);
-            __half2* hp = reinterpret_cast<__half2*>(&q);
+        if (lane == 31) P.n_units = (i1 + tot0) >> 16;
+        if (blockIdx.x < 8) route_trace(a, rk, rtr, 34);
+    } else {
+        // activation rows scaled in place by 2^-s(k) (HMUL2 by a power of two: the same
+        // rounding as scaling in fp32 and converting) + Z per token (warps 1..)
+        constexpr int bias = 1 << (BITS - 1);
+        for (int tk = warp - 1; tk < T; tk += kDecFfnWarps - 1) {
+            unsigned char* row = hs + size_t(tk) * hpitch;
+            float zf = 0.f;
+            for (int k0 = lane * 8; k0 < Kp1; k0 += 256) {
+                uint4 q = *reinterpret_cast<const uint4*>(row + k0 * 2);
+                __half2* hp = reinterpret_cast<__half2*>(&q);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int sh = field_shift_c<BITS>((k0 + 2 * e) & 15);
-                const float2 f = __half22float2(hp[e]);
-                const float sc = __int_as_float((127 - sh) << 23);  // 2^-sh, exact
-                hp[e] = __floats2half2_rn(f.x * sc, f.y * sc);
-                const float m = 1024.f + float(bias << sh);  // exact; products of 11-bit factors
-                zf = fmaf(m, __low2float(hp[e]), zf);
-                zf = fmaf(m, __high2float(hp[e]), zf);
+                for (int e = 0; e < 4; ++e) {
+                    const int sh = field_shift_c<BITS>((k0 + 2 * e) & 15);
+                    hp[e] = __hmul2(hp[e], __half2half2(__ushort_as_half(uint16_t((15 - sh) << 10))));
+                    const float2 f = __half22float2(hp[e]);
+                    const float m = 1024.f + float(bias << sh);  // exact; products of 11-bit factors
+                    zf = fmaf(m, f.x, zf);
+                    zf = fmaf(m, f.y, zf);
+                }
+                *reinterpret_cast<uint4*>(row + k0 * 2) = q;
             }
-            *reinterpret_cast<uint4*>(row + k0 * 2) = q;
-        }
-        double z = zf;
+            double z = zf;
 #pragma unroll
-        for (int o = 16; o; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
-        if (lane == 0) P.z[tk] = float(z);
+            for (int o = 16; o; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+            if (lane == 0) P.z[tk] = float(z);
+        }
     }
-    (void)d;
     __syncthreads();
-    if (blockIdx.x < 8 && !dry) route_trace(a, rk, rtr, 35);
-}
-
-// the summed-logit table of the fused routing (behind the partial tables in the rings)
-__device__ __forceinline__ const float* dec_logits(const float* part, int E) {
-    const int Ep = (E + 7) & ~7, ntiles = Ep / 8, ks = ntiles >= 16 ? 1 : 16 / ntiles;
-    return part + ks * 32 * Ep;
+    if (blockIdx.x < 8) route_trace(a, rk, rtr, 35);
 }
 
 // Warp-specialised stream-K decode FFN. Warps 0-7 (fc1) and 8-15 (fc2) work on different
@@ -932,15 +986,22 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
         fence_barrier_init();
     }
     __syncthreads();
+    // the cluster's barrier inits are published before any peer pushes logits (the matching
+    // wait sits in dec_fused_route, long after this arrive)
+    if (FU && cluster_nctas() > 1) cluster_arrive_relaxed();
     // fused routing: gate-weight chunks that fit in the rings (bank constants: before the PDL wait)
     const int Ep_ = (a.E + 7) & ~7;
     const uint32_t cbytes_ = uint32_t(2 * Ep_) * ((a.Kp1 / 4 + 8) * 2);
     const int nbuf_ = FU ? a.route_nbuf : 1;
     if (FU && tid == 0) {
-        if (cluster_nctas() == 4) {  // this CTA's K quarter only
-            const uint32_t r = cta_rank();
-            mbar_arrive_expect_tx(rbar, cbytes_);
-            bulk_g2s(ring1, reinterpret_cast<const unsigned char*>(a.wgt) + size_t(r) * cbytes_, cbytes_, rbar);
+        const int cl = int(cluster_nctas());
+        if (cl > 1) {  // this CTA's K chunks only
+            const int cpr = 4 / cl, c0 = int(cta_rank()) * cpr;
+            for (int i = 0; i < cpr; ++i) {
+                mbar_arrive_expect_tx(rbar + i, cbytes_);
+                bulk_g2s(ring1 + size_t(i) * cbytes_, reinterpret_cast<const unsigned char*>(a.wgt) + size_t(c0 + i) * cbytes_,
+                         cbytes_, rbar + i);
+            }
         } else {
             for (int c = 0; c < nbuf_; ++c) {
                 mbar_arrive_expect_tx(rbar + c, cbytes_);
@@ -952,15 +1013,21 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
     pdl_trigger();
     pdl_wait();
     if (tid == 0) span_begin(a.span_ffn);
+    if (a.trace && tid == 0) {  // slot 63: this CTA's start after the PDL wait
+        unsigned long long* p = a.trace + (size_t(blockIdx.x) * kDecTrace + 63) * 2;
+        p[0] = 20u;
+        p[1] = gtime_ns();
+    }
     int rtr0 = 0;
     if (FU && blockIdx.x < 8) route_trace(a, blockIdx.x, rtr0, 28);
     if constexpr (FU) {
         // activation rows -> hs (one bulk copy per row), zero padding columns / rows
         const int T = a.T;
         const bool bulk = a.h_f16 && (d % 8 == 0) && ((reinterpret_cast<uintptr_t>(a.h) & 15) == 0);
-        if (bulk && tid == 0) {
-            mbar_arrive_expect_tx(rbar + 4, uint32_t(T) * d * 2);
-            for (int r = 0; r < T; ++r)
+        if (bulk && warp == 0) {  // one row per lane
+            if (lane == 0) mbar_arrive_expect_tx(rbar + 4, uint32_t(T) * d * 2);
+            __syncwarp();
+            for (int r = lane; r < T; r += 32)
                 bulk_g2s(xsb + size_t(r) * a.xpitch, static_cast<const __half*>(a.h) + size_t(r) * d, d * 2, rbar + 4);
         }
         if (!bulk) {
@@ -977,10 +1044,10 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
         if (bulk) mbar_wait(rbar + 4, 0);
         __syncthreads();
         if (blockIdx.x < 8) route_trace(a, blockIdx.x, rtr0, 29);
-        float* part = reinterpret_cast<float*>(ring1 + size_t(nbuf_) * cbytes_);
+        float* lg = reinterpret_cast<float*>(ring1 + size_t(nbuf_) * cbytes_);
         // one instantiation (two token m-tiles) keeps the kernel's instruction footprint small
-        dec_fused_route<BITS, 2>(a, *PS, xsb, a.xpitch, ring1, nbuf_, part, rbar, warp, lane, false);
-        dec_fused_decide<BITS>(a, *PS, xsb, a.xpitch, dec_logits(part, a.E), warp, lane, false);
+        dec_fused_route<BITS>(a, xsb, a.xpitch, ring1, nbuf_, lg, rbar, warp, lane);
+        dec_fused_decide<BITS>(a, *PS, xsb, a.xpitch, lg, warp, lane);
     }
     const int4* units = FU ? PS->units : a.units;
     const int* perm_token = FU ? PS->perm_token : a.perm_token;
@@ -1044,9 +1111,18 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
         return;
     }
 
-    if (warp < kF1Warps) {
+    // roles by SM sub-partition (warp % 4): fc1 on SMSPs 0-1, fc2 on SMSPs 2-3, so each
+    // sub-partition's L0 instruction cache (~6 KB) holds one role's unrolled loop
+#if DEC_ROLE_SPLIT
+    const bool is_f1 = (warp & 2) == 0;
+    const int rix = (warp >> 2) * 2 + (warp & 1);  // index within the role, 0..7
+#else
+    const bool is_f1 = warp < kF1Warps;
+    const int rix = is_f1 ? warp : warp - kF1Warps;
+#endif
+    if (is_f1) {
         // ------------------------------ fc1 warps ------------------------------
-        const int gw = warp & 3, kh = warp >> 2;
+        const int gw = rix & 3, kh = rix >> 2;
         int s1 = 0, nu = 0, n = 0, ntr = 0;
         uint32_t p1 = 0;
         int u = u0, j = j0;
@@ -1092,7 +1168,7 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
             for (int p = 0; p < NP; ++p) {
                 sl1 = s1;
                 mbar_wait(full1 + s1, p1);
-                if (lane == 0 && warp == 0) dec_trace(a, 0, ntr, 1);
+                if (lane == 0 && rix == 0) dec_trace(a, 0, ntr, 1);
                 const unsigned char* piece = ring1 + size_t(s1) * sb1 + size_t(kh * KH) * 64 * RB;
                 if (NBr == 1) dec_fc1_piece<BITS, KH, 1>(piece, p * KP + kh * KH, gw, g, t, xrow, ca, cb);
                 else dec_fc1_piece<BITS, KH, 2>(piece, p * KP + kh * KH, gw, g, t, xrow, ca, cb);
@@ -1168,7 +1244,7 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
 
     // ------------------------------ fc2 warps ------------------------------
     constexpr int NT2 = kF2Warps * 32;
-    const int v = warp - kF1Warps, tid2 = tid - kF1Warps * 32;
+    const int v = rix, tid2 = rix * 32 + lane;
     const int vp = v / WPP, q0 = (v % WPP) * QW;  // W2 piece of this warp, first group in it
     int s2 = 0, n = 0, ntr = 0;
     uint32_t p2 = 0;
@@ -1263,15 +1339,15 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
         j += len;
         if (j == S) { j = 0; ++u; }
         {
-            __threadfence();
+            // the fc2 warps' reds are ordered before one acq_rel counter update (bar.sync + the
+            // cumulative release of thread 0); the finisher's acquire covers its reads of acc
             named_bar_sync(2, NT2);
             if (tid2 == 0) {
                 const unsigned mine = unsigned(ju + 1 - ulo);
-                const unsigned old = atomicAdd(a.unit_done + uu, mine);
+                const unsigned old = atom_add_acq_rel(a.unit_done + uu, mine);
                 const int fin = old + mine == unsigned(S);
                 if (fin) a.unit_done[uu] = 0;
                 flag[0] = fin;
-                __threadfence();
             }
             named_bar_sync(2, NT2);
             if (tid2 == 0) dec_trace(a, 21, ntr, 5);
@@ -1297,14 +1373,12 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
                     }
                 }
                 if (a.topk == 2) {
-                    __threadfence();
-                    named_bar_sync(2, NT2);
-                    if (tid2 < un.z) {
+                    named_bar_sync(2, NT2);  // ybuf rows written; each token's acq_rel count below
+                    if (tid2 < un.z) {      // releases them (cumulative) and acquires the other slot's
                         const int tok = perm_token[un.y + tid2];
-                        const unsigned old = atomicAdd(a.tok_cnt + tok, 1u);
+                        const unsigned old = atom_add_acq_rel(a.tok_cnt + tok, 1u);
                         comb[tid2] = old == 1 ? tok : -1;
                         if (old == 1) a.tok_cnt[tok] = 0;
-                        __threadfence();
                     }
                     named_bar_sync(2, NT2);
                     for (int idx = tid2; idx < un.z * d; idx += NT2) {
@@ -1400,7 +1474,7 @@ cudaError_t dec_build_layout(const uint8_t* w1, const uint8_t* w2, int64_t w1_st
 template <int BITS, int QN, int GQ, int NP, bool FU>
 static cudaError_t launch_dec_t(const DecArgs& a, cudaStream_t st, int num_sms, size_t smem) {
     static bool configured[kMaxDev] = {};
-    static int clusters4[kMaxDev] = {};  // co-resident 4-CTA clusters (fused routing)
+    static int clusters[kMaxDev][3] = {};  // co-resident clusters of 2 / 4 CTAs (fused routing)
     int dev = 0;
     cudaGetDevice(&dev);
     const int di = dev < kMaxDev ? dev : 0;
@@ -1418,22 +1492,24 @@ static cudaError_t launch_dec_t(const DecArgs& a, cudaStream_t st, int num_sms, 
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     attr[1].id = cudaLaunchAttributeClusterDimension;
-    attr[1].val.clusterDim.x = 4;
+    const int cl = (FU && (a.route_cluster == 2 || a.route_cluster == 4)) ? a.route_cluster : 1;
+    attr[1].val.clusterDim.x = unsigned(cl);
     attr[1].val.clusterDim.y = 1;
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
     int grid = num_sms;
-    if (FU && a.route_cluster == 4) {
-        if (clusters4[di] == 0) {
+    if (cl > 1) {
+        int& nc = clusters[di][cl / 2];
+        if (nc == 0) {
             cudaLaunchConfig_t q = cfg;
-            q.gridDim = dim3(unsigned(num_sms / 4 * 4));
+            q.gridDim = dim3(unsigned(num_sms / cl * cl));
             q.attrs = attr + 1;
             q.numAttrs = 1;
             int n = 0;
-            if (cudaOccupancyMaxActiveClusters(&n, kern, &q) != cudaSuccess || n <= 0) n = num_sms / 4;
-            clusters4[di] = std::min(n, num_sms / 4);
+            if (cudaOccupancyMaxActiveClusters(&n, kern, &q) != cudaSuccess || n <= 0) n = num_sms / cl;
+            nc = std::min(n, num_sms / cl);
         }
-        grid = clusters4[di] * 4;
+        grid = nc * cl;
         cfg.numAttrs = 2;
     } else {
         cfg.numAttrs = 1;
@@ -1452,9 +1528,11 @@ static cudaError_t launch_dec_f(const DecArgs& a, cudaStream_t st, int num_sms, 
 template <int BITS, int QN>
 static cudaError_t launch_dec_q(const DecArgs& a, cudaStream_t st, int num_sms, size_t smem) {
     switch (a.Np2 / 256) {
+#ifndef DEC_AB_ONLY  // experiment builds (tools/ab_build.sh): d_model = 1024 only
         case 1: return launch_dec_f<BITS, QN, 1>(a, st, num_sms, smem);
         case 2: return launch_dec_f<BITS, QN, 2>(a, st, num_sms, smem);
         case 3: return launch_dec_f<BITS, QN, 3>(a, st, num_sms, smem);
+#endif
         case 4: return launch_dec_f<BITS, QN, 4>(a, st, num_sms, smem);
     }
     return cudaErrorInvalidValue;
@@ -1463,9 +1541,11 @@ static cudaError_t launch_dec_q(const DecArgs& a, cudaStream_t st, int num_sms, 
 template <int BITS>
 static cudaError_t launch_dec_b(const DecArgs& a, cudaStream_t st, int num_sms, size_t smem) {
     switch (a.Kp1 / 256) {
+#ifndef DEC_AB_ONLY
         case 1: return launch_dec_q<BITS, 1>(a, st, num_sms, smem);
         case 2: return launch_dec_q<BITS, 2>(a, st, num_sms, smem);
         case 3: return launch_dec_q<BITS, 3>(a, st, num_sms, smem);
+#endif
         case 4: return launch_dec_q<BITS, 4>(a, st, num_sms, smem);
     }
     return cudaErrorInvalidValue;
@@ -1511,8 +1591,8 @@ static bool dec_config(int bits, DecArgs& a, size_t* smem_out) {
     const int pairs = int(std::min<size_t>(8, budget / (a.stage_bytes + a.stage2_bytes + 32)));
     if (pairs < 2) return false;
     if (a.fused) {  // the routing phase borrows the rings: 2..4 Wg chunks + the partial logits
-        const int Ep = (a.E + 7) & ~7, ntiles = Ep / 8, ks = ntiles >= 16 ? 1 : 16 / ntiles;
-        const size_t cb = size_t(2 * Ep) * ((a.Kp1 / 4 + 8) * 2), pb = size_t(ks + 2) * 32 * Ep * 4;
+        const DecRouteGeom G(a.E, a.route_cluster);
+        const size_t cb = size_t(2 * G.Ep) * ((a.Kp1 / 4 + 8) * 2), pb = G.floats() * 4;
         const size_t ring = size_t(pairs) * (a.stage_bytes + a.stage2_bytes);
         a.route_nbuf = ring < pb ? 0 : int(std::min<size_t>(4, (ring - pb) / cb));
         if (a.route_nbuf < 2) return false;
@@ -1561,8 +1641,10 @@ cudaError_t launch_dec(int bits, const DecArgs& a0, cudaStream_t st, int num_sms
     switch (bits) {
         case 2: return launch_dec_b<2>(a, st, num_sms, smem);
         case 3: return launch_dec_b<3>(a, st, num_sms, smem);
+#ifndef DEC_AB_ONLY
         case 4: return launch_dec_b<4>(a, st, num_sms, smem);
         case 8: return launch_dec_b<8>(a, st, num_sms, smem);
+#endif
     }
 
     return cudaErrorInvalidValue;

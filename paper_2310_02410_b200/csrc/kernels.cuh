@@ -188,7 +188,7 @@ struct DecArgs {
     int wg_shift;
     int fused;             // routing inside k_dec (T <= 32, bank router, finite Wg)
     int route_nbuf;        // set by launch_dec: Wg chunk buffers of the fused routing
-    int route_cluster;     // fused routing: 4 = K quarters shared by a 4-CTA cluster, 1 = every CTA alone
+    int route_cluster;     // fused routing: CTAs per cluster sharing the K chunks (2 or 4), 1 = every CTA alone
     uint32_t stage_bytes, stage2_bytes;  // set by launch_dec: W1 / W2 ring stage sizes
     int n_stages, n_stages2;
 };

@@ -24,6 +24,7 @@ ap.add_argument("--f", type=int, default=4096)
 ap.add_argument("--layers", type=int, default=8)
 ap.add_argument("--topk", type=int, default=1)
 ap.add_argument("--reps", type=int, default=50)
+ap.add_argument("--isolated", action="store_true", help="also report the span of isolated (synchronised) forwards")
 a = ap.parse_args()
 lib = m.load_library()
 
@@ -89,6 +90,21 @@ for bits in a.bits:
         sums += np.array(tot[:])
         ns += np.array(cnt[:])
     span = sums / np.maximum(ns, 1)
+    if a.isolated:
+        for b in banks:
+            lib.moqe_gpu_bank_span(b._h, 1)
+            lib.moqe_gpu_bank_span_read(b._h, tot, cnt)
+        isums, ins = np.zeros(2), np.zeros(2)
+        for _ in range(10):
+            for i in range(a.layers):
+                m.moe_ffn_forward(hs[i], banks[i], top_k=a.topk, out=outs[i])
+                torch.cuda.synchronize()
+        for b in banks:
+            lib.moqe_gpu_bank_span_read(b._h, tot, cnt)
+            isums += np.array(tot[:])
+            ins += np.array(cnt[:])
+            lib.moqe_gpu_bank_span(b._h, 0)
+        print(f"  isolated forwards: span ffn {isums[1] / max(ins[1], 1):.2f} us")
     wbytes = np.mean(touched) * (2 * packed(bits, a.d * a.f) + 2 * (a.d + a.f))
     print(f"int{bits} T={a.tokens} k={a.topk} E={a.experts}: {us:.2f} us/forward ({a.tokens / us * 1e6:,.0f} tok/s), "
           f"touched {np.mean(touched):.1f}, weights {wbytes / 1e6:.1f} MB -> {wbytes / us / 1e3:.0f} GB/s per step; "

@@ -16,11 +16,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--bits", type=int, default=3)
 ap.add_argument("--tokens", type=int, default=24)
 ap.add_argument("--experts", type=int, default=32)
+ap.add_argument("--banks", type=int, default=8, help="layers rotated (8: the traced layer's weights are out of L2)")
 a = ap.parse_args()
 g = torch.Generator(device="cuda").manual_seed(1)
 d, f, E = 1024, 4096, a.experts
 banks = []
-for i in range(3):
+for i in range(a.banks):
     w1 = torch.randn(E, d, f, device="cuda", generator=g) * 0.02
     w2 = torch.randn(E, f, d, device="cuda", generator=g) * 0.02
     wg = torch.randn(d, E, device="cuda", generator=g) * 0.02
@@ -29,7 +30,7 @@ h = torch.randn(a.tokens, d, device="cuda", generator=g).half()
 for b in banks:
     m.moe_ffn_forward(h, b)
 torch.cuda.synchronize()
-b = banks[2]
+b = banks[-1]
 b.trace(True)
 for bb in banks:
     m.moe_ffn_forward(h, bb)
@@ -48,10 +49,15 @@ for c in range(ev.shape[0]):
     if c < 6 or c % 37 == 0:
         print(c, " ".join(f"{names.get(e, e)}@{t:.2f}" for e, t in row))
 print("exit us: min %.2f median %.2f max %.2f" % (min(ends), float(np.median(ends)), max(ends)))
+st = ev[:, 63, 1].astype(np.int64)
+st = (st[st > 0] - int(t0)) / 1e3
+print("start (after PDL wait) us: n %d min %.2f median %.2f max %.2f" % (len(st), st.min(), np.median(st), st.max()))
 # router events (k_dec_route, rank r at slots (160 + r) * 64): 20 after PDL wait, 21 h staged,
 # 22 Wg landed, 23/24 around each cluster barrier, 25 plan built, 26 rows written
 rt = tr.reshape(-1, 2)[160 * 64: 168 * 64].reshape(8, 64, 2)
 for r in range(8):
     row = [(int(e) & 255, (int(t) - int(t0)) / 1e3, int(e) >> 8) for e, t in rt[r] if t > 0]
+    row.sort(key=lambda x: x[2])
     ghz = (row[-1][2] - row[0][2]) / max(1e-9, (row[-1][1] - row[0][1]) * 1e3) if len(row) > 1 else 0
     print("router", r, " ".join(f"{e}@{t:.2f}" for e, t, c in row), f"  SM clock {ghz:.2f} GHz")
+    print("   cycles", " ".join(f"{e}:{c - row[0][2]}" for e, t, c in row))
