@@ -455,7 +455,7 @@ moqe_status moqe_gpu_bank_set_router(moqe_bank_t b, const float* wg, int on_devi
     if (!b->wg_blk) MOQE_CUDA(cudaMalloc(&b->wg_blk, sizeof(float) * route_wg_block_floats(int(b->d), b->E) + 16));
     int* flag = reinterpret_cast<int*>(b->wg_blk + route_wg_block_floats(int(b->d), b->E));
     MOQE_CUDA(route_block_wg(b->wg, int(b->d), b->E, b->wg_blk, flag, &b->wg_finite));
-    if (b->wdec) {  // decode banks: the split copy the fused routing streams (finite Wg only)
+    if (b->wg_finite && b->Kp1 % 64 == 0) {  // the split copy the fused decode and prefill routers stream
         std::vector<float> hw(size_t(b->d) * b->E);
         MOQE_CUDA(cudaMemcpy(hw.data(), b->wg, hw.size() * sizeof(float), cudaMemcpyDeviceToHost));
         float mx = 0.f;
@@ -598,6 +598,7 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
         self_plan = !pre && !need_gemm && R <= kSelfPlanRows && t <= 32 && b->E <= 256;
         ra.no_plan = self_plan ? 1 : 0;
         if (wg == b->wg && b->wg_blk) { ra.wg_blk = b->wg_blk; ra.wg_finite = b->wg_finite; }
+        if (wg == b->wg && b->wgt) { ra.wgt = b->wgt; ra.wg_shift = b->wg_shift; ra.Kp1 = int(b->Kp1); }
         ra.dbg = route_dbg();
         if (need_gemv && !pre && route_chain_used(ra) && xrows_in_router()) {
             // decode: the router leads the chain (waits for the previous grid itself) and its

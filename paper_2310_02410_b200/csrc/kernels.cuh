@@ -53,6 +53,11 @@ struct RouteArgs {
     uint8_t* xr;                // fc1 row blocks [T][nch1][xr bytes] or null
     int nch1, xr_bits;
     unsigned* ready;            // [kSelfPlanRows] or null
+    // tensor-core prefill logits (k_route_mma): the bank's split gate weights
+    // [4 K chunks][hi, lo][Ep][Kp1/4 + 8] fp16 = Wg * 2^wg_shift (finite Wg only), or null
+    const __half* wgt;
+    int wg_shift;
+    int Kp1;
 };
 bool route_chain_used(const RouteArgs& a);  // launch_route will run k_route_chain
 constexpr int kTraceRouteCtas = 64;

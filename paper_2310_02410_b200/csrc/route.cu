@@ -18,6 +18,9 @@
 // lists and resets the downstream schedulers — no extra launch, no host sync.
 #include <cuda_fp16.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "kernels.cuh"
 #include "ptx.cuh"
 #include "xrow.cuh"
@@ -124,33 +127,68 @@ __device__ void plan_lists(const RouteArgs& a, Plan& P, const int* cnt, int* s_o
 __device__ void plan_tail(const RouteArgs& a, Plan P, int n_ctas, int tt, int* scr, int scr_ints) {
     const int E = a.E, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nw = blockDim.x >> 5;
-    const bool staged = scr != nullptr && int64_t(n_ctas) * E + E <= scr_ints;
+    const int RB = blockDim.x >= E ? int(blockDim.x) / E : 1;  // row blocks of the two-level scan
+    const bool staged = scr != nullptr && int64_t(n_ctas) * E + E + int64_t(RB) * E <= scr_ints;
     int* s_cnt = staged ? scr + n_ctas * E : nullptr;
     if (staged) {
-        for (int i = threadIdx.x; i < n_ctas * E; i += blockDim.x) scr[i] = __ldcg(P.cta_counts + i);
-        __syncthreads();
-        // 1. exclusive scan over CTAs per expert: warp per expert, shuffle scans
-        for (int e = warp; e < E; e += nw) {
-            int running = 0;
-            for (int c0 = 0; c0 < n_ctas; c0 += 32) {
-                const int c = c0 + lane;
-                const int v = c < n_ctas ? scr[c * E + e] : 0;
-                int incl = v;
+        // the histograms: 16-byte loads, 8 in flight per thread (E % 4 == 0: rows stay aligned)
+        const int n = n_ctas * E;
+        if ((E & 3) == 0) {
+            const int n4 = n >> 2;
+            const int4* src = reinterpret_cast<const int4*>(P.cta_counts);
+            int4* dst = reinterpret_cast<int4*>(scr);
+            for (int i0 = threadIdx.x; i0 < n4; i0 += 8 * blockDim.x) {
+                int4 v[8];
 #pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const int y = __shfl_up_sync(0xffffffffu, incl, off);
-                    if (lane >= off) incl += y;
+                for (int u = 0; u < 8; ++u) {
+                    const int i = i0 + u * blockDim.x;
+                    v[u] = i < n4 ? __ldcg(src + i) : make_int4(0, 0, 0, 0);
                 }
-                if (c < n_ctas) scr[c * E + e] = running + incl - v;
-                running += __shfl_sync(0xffffffffu, incl, 31);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int i = i0 + u * blockDim.x;
+                    if (i < n4) dst[i] = v[u];
+                }
             }
-            if (lane == 0) {
-                s_cnt[e] = running;
-                P.counts[e] = running;
+        } else {
+            for (int i = threadIdx.x; i < n; i += blockDim.x) scr[i] = __ldcg(P.cta_counts + i);
+        }
+        __syncthreads();
+        if (a.trace && threadIdx.x == 0) a.trace[(kTraceRouteCtas - 1) * 16 + 9] = gtime_ns();
+        // 1. exclusive scan over CTAs per expert, two levels: thread (row block rb, expert e) sums
+        //    its block of CTAs, then rescans it from the sum of the blocks above
+        int* seg = s_cnt + E;  // [RB][E]
+        const int e = threadIdx.x % E, rb = threadIdx.x / E;
+        const int per = (n_ctas + RB - 1) / RB, r0 = rb * per, r1 = min(n_ctas, r0 + per);
+        if (rb < RB) {
+            int sum = 0;
+#pragma unroll 8
+            for (int r = r0; r < r1; ++r) sum += scr[r * E + e];
+            seg[rb * E + e] = sum;
+        }
+        __syncthreads();
+        if (rb < RB) {
+            int run = 0;
+            for (int q = 0; q < rb; ++q) run += seg[q * E + e];
+#pragma unroll 8
+            for (int r = r0; r < r1; ++r) {
+                const int v = scr[r * E + e];
+                scr[r * E + e] = run;
+                run += v;
+            }
+            if (rb == RB - 1) {
+                s_cnt[e] = run;
+                P.counts[e] = run;
             }
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < n_ctas * E; i += blockDim.x) P.cta_counts[i] = scr[i];
+        if (a.trace && threadIdx.x == 0) a.trace[(kTraceRouteCtas - 1) * 16 + 10] = gtime_ns();
+        if ((E & 3) == 0) {
+            for (int i = threadIdx.x; i < (n >> 2); i += blockDim.x)
+                reinterpret_cast<int4*>(P.cta_counts)[i] = reinterpret_cast<const int4*>(scr)[i];
+        } else {
+            for (int i = threadIdx.x; i < n; i += blockDim.x) P.cta_counts[i] = scr[i];
+        }
     } else {
     // 1. exclusive scan of per-CTA counts over CTAs, per expert (warp per expert)
     for (int e = warp; e < E; e += nw) {
@@ -179,6 +217,7 @@ __device__ void plan_tail(const RouteArgs& a, Plan P, int n_ctas, int tt, int* s
     }
     }
     __syncthreads();
+        if (a.trace && threadIdx.x == 0) a.trace[(kTraceRouteCtas - 1) * 16 + 15] = gtime_ns();
     // 2. offsets + expert lists (warp 0, expert order)
     plan_lists(a, P, staged ? s_cnt : P.counts, nullptr);
     for (int e = threadIdx.x; e < E; e += blockDim.x) P.done[e] = 0;
@@ -269,9 +308,11 @@ __device__ __forceinline__ void ranks_hist_plan(const RouteArgs& a, Plan& P, int
     __syncthreads();
     if (tr && threadIdx.x == 0) tr[11] = gtime_ns();
     if (!s_last) return;
+    if (a.trace && threadIdx.x == 0) a.trace[(kTraceRouteCtas - 1) * 16 + 13] = gtime_ns();  // plan start
     plan_tail(a, P, gridDim.x, tt, scr, scr_ints);
     __syncthreads();
     if (tr && threadIdx.x == 0) tr[12] = gtime_ns();
+    if (a.trace && threadIdx.x == 0) a.trace[(kTraceRouteCtas - 1) * 16 + 14] = gtime_ns();  // plan end
 }
 
 constexpr int kRouteSmallWarps = 4;   // token warps per CTA (one token each, one per SM sub-partition)
@@ -1131,6 +1172,430 @@ __global__ void __launch_bounds__((kRL2Warps + 1) * 32, 1) k_route_logits2(Route
     ranks_hist_plan(a, P, s_exp, s_hist, 32, reinterpret_cast<int*>(ring), NS * kRL2Rows * E);
 }
 
+// ---- large T, tensor-core logits (E in {32, 64}, finite Wg, fp16 rows) -----------------
+// The exact-order chains above cost one FMUL + one FADD per MAC (~130 us at T = 16384).
+// north_star lets tokens whose top-2 logit gap is < 1e-4 route differently, so the prefill
+// logits run on the tensor cores instead: the bank's split copy Wg * 2^s = hi + lo (fp16,
+// ~22 significant bits; see dec_split_wg) is the B operand, the fp16 token rows the A operand,
+// fp32 accumulation in a fixed per-CTA order (deterministic, |error| ~1e-7 relative). CTA =
+// 32 tokens (two 16-row A tiles) x all E experts, 8 MMA warps: warp w owns A tile w & 1 and the
+// 8-expert B tiles w >> 1 (+4 for E = 64), over the whole K. A producer warp stages the token
+// rows (zero-padded to Kp1) and streams the four Wg chunks through one slot (~100 KB of smem:
+// two CTAs per SM, so one CTA's loads overlap the other's MMAs). Selection,
+// ranks and the last-CTA plan are the shared tail (finish_token, ranks_hist_plan).
+constexpr int kRMWarps = 8, kRMSlots = 1;  // one Wg slot: two CTAs per SM overlap each other's loads
+__host__ __device__ inline int rm_hpitch(int Kp1) { return Kp1 * 2 + 16; }  // 16 mod 128: conflict-free
+__host__ __device__ inline uint32_t rm_chunk_bytes(int E, int Kp1) {
+    return uint32_t(2 * ((E + 7) & ~7)) * uint32_t((Kp1 / 4 + 8) * 2);
+}
+size_t rm_smem(int E, int Kp1) {
+    return size_t((32 * rm_hpitch(Kp1) + 127) / 128 * 128) + size_t(kRMSlots) * rm_chunk_bytes(E, Kp1) + 128 +
+           size_t(32) * (E + 1) * 4;
+}
+
+template <int EPL>
+__global__ void __launch_bounds__((kRMWarps + 1) * 32, 2) k_route_mma(RouteArgs a, Plan P) {
+    constexpr int E = 32 * EPL, NT = E / 8, IPW = 2 * NT / kRMWarps;  // B tiles; items per warp
+    extern __shared__ __align__(128) uint8_t sm[];
+    const int d = a.d, Kp1 = a.Kp1, hp = rm_hpitch(Kp1);
+    const int Kc = Kp1 / 4, cpitch = (Kc + 8) * 2, nsteps = Kc / 16;
+    const uint32_t cb = rm_chunk_bytes(E, Kp1);
+    uint8_t* ring = sm + (32 * hp + 127) / 128 * 128;
+    uint64_t* hbar = reinterpret_cast<uint64_t*>(ring + kRMSlots * cb);
+    uint64_t* full = hbar + 1;
+    uint64_t* empty = full + kRMSlots;
+    float* s_l = reinterpret_cast<float*>(sm + (32 * hp + 127) / 128 * 128 + kRMSlots * cb + 128);  // [32][E + 1]
+    __shared__ int s_exp[64];
+    __shared__ int s_hist[256];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int64_t t0 = int64_t(blockIdx.x) * 32;
+    // diagnostics: globaltimer stamps of CTAs < kTraceRouteCtas (0 start, 1 rows, 2-5 chunks,
+    // 6 MMAs done, 7 logits in smem, 8 selection done, 11 ticket, 12 plan)
+    const int trs = (gridDim.x + kTraceRouteCtas - 1) / kTraceRouteCtas;  // every trs-th CTA
+    unsigned long long* tr = a.trace && blockIdx.x % trs == 0 ? a.trace + (blockIdx.x / trs) * 16 : nullptr;
+    if (tr && threadIdx.x == 0) tr[0] = gtime_ns();
+    for (int e = threadIdx.x; e < E; e += blockDim.x) s_hist[e] = 0;
+    const int ntok = a.T - t0 < 32 ? int(a.T - t0) : 32;
+    if (threadIdx.x == 0) {
+        mbar_init(hbar, 1);
+        for (int s = 0; s < kRMSlots; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kRMWarps); }
+        fence_barrier_init();
+    }
+    for (int i = threadIdx.x; i < 32 * (Kp1 - d); i += blockDim.x) {  // K padding of the rows: zeros
+        const int r = i / (Kp1 - d), k = d + i % (Kp1 - d);
+        reinterpret_cast<__half*>(sm + r * hp)[k] = __float2half_rn(0.f);
+    }
+    __syncthreads();
+    if (warp == kRMWarps) {
+        if (lane == 0) {
+            const __half* h = static_cast<const __half*>(a.h);
+            mbar_arrive_expect_tx(hbar, uint32_t(ntok * d * 2));
+            for (int r = 0; r < ntok; ++r) bulk_g2s(sm + r * hp, h + (t0 + r) * d, uint32_t(d * 2), hbar);
+            for (int c = 0; c < 4; ++c) {
+                const int s = c % kRMSlots;
+                if (c >= kRMSlots) mbar_wait(&empty[s], ((c / kRMSlots) - 1) & 1);
+                mbar_arrive_expect_tx(&full[s], cb);
+                bulk_g2s(ring + s * cb, reinterpret_cast<const uint8_t*>(a.wgt) + size_t(c) * cb, cb, &full[s]);
+            }
+        }
+        __syncwarp();
+    } else {
+        float acc[IPW][2][2][4];  // [item][hi, lo][even, odd k-step][4]
+#pragma unroll
+        for (int x = 0; x < IPW; ++x)
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2)
+#pragma unroll
+                for (int q = 0; q < 2; ++q)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) acc[x][h2][q][i] = 0.f;
+        const int mt = warp & 1;
+        // ldmatrix row addresses. A (token rows): matrices (rows 0-7 | 8-15) x (k 0-7 | 8-15) ->
+        // a0..a3; B (expert rows of the hi | lo halves) x (k 0-7 | 8-15) -> b0, b1 of hi and lo.
+        const int lr = lane & 7, lm = lane >> 3;
+        const uint32_t a_row = smem_u32(sm) + min(mt * 16 + lr + (lm & 1) * 8, ntok - 1) * hp + (lm >> 1) * 16;
+        mbar_wait(hbar, 0);
+        if (tr && threadIdx.x == 0) tr[1] = gtime_ns();
+        for (int c = 0; c < 4; ++c) {
+            const int s = c % kRMSlots;
+            mbar_wait(&full[s], (c / kRMSlots) & 1);
+            if (tr && threadIdx.x == 0) tr[2 + c] = gtime_ns();
+            const uint32_t buf = smem_u32(ring + s * cb);
+#pragma unroll
+            for (int x = 0; x < IPW; ++x) {
+                const int nt = (warp >> 1) + x * (kRMWarps / 2);
+                const uint32_t b_row = buf + ((lm >> 1) * E + nt * 8 + lr) * cpitch + (lm & 1) * 16;
+                const uint32_t a_c = a_row + c * Kc * 2;
+#pragma unroll 2
+                for (int s2 = 0; s2 < nsteps; s2 += 2) {  // nsteps is even (Kp1 % 128 == 0)
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {  // even / odd k-step: two accumulator sets
+                        const int st = s2 + q;
+                        uint32_t a0, a1, a2, a3, bh0, bh1, bl0, bl1;
+                        ldsm_x4(a_c + st * 32, a0, a1, a2, a3);
+                        ldsm_x4(b_row + st * 32, bh0, bh1, bl0, bl1);
+                        mma_16816(acc[x][0][q], a0, a1, a2, a3, bh0, bh1);
+                        mma_16816(acc[x][1][q], a0, a1, a2, a3, bl0, bl1);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        if (tr && threadIdx.x == 0) tr[6] = gtime_ns();
+        // c0, c1: token mt*16+g, experts nt*8+2t, +1; c2, c3: token + 8 (fixed summation order)
+        const float us = __int_as_float((127 - a.wg_shift) << 23);  // exact power of two
+#pragma unroll
+        for (int x = 0; x < IPW; ++x) {
+            const int nt = (warp >> 1) + x * (kRMWarps / 2);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float v = ((acc[x][0][0][i] + acc[x][0][1][i]) + (acc[x][1][0][i] + acc[x][1][1][i])) * us;
+                const int tok = mt * 16 + g + 8 * (i >> 1), e = nt * 8 + 2 * t + (i & 1);
+                s_l[tok * (E + 1) + e] = v;
+            }
+        }
+        named_bar_sync(1, kRMWarps * 32);  // all 32 x E logits of the CTA in smem
+        if (tr && threadIdx.x == 0) tr[7] = gtime_ns();
+        // selection: 8 lanes per token, all 32 tokens at once (lane j of a group holds experts
+        // j, j+8, ...); argmax with the reference's scan semantics (NaN skipped unless at the
+        // first index, ties -> lowest index), softmax gate in double (model.cpp:214-227)
+        {
+            constexpr int PER = E / 8;
+            const int lt = warp * 4 + (lane >> 3), sub = lane & 7;
+            const int ltc = lt < ntok ? lt : ntok - 1;
+            const float* lrow = s_l + ltc * (E + 1);
+            float l[PER];
+#pragma unroll
+            for (int j = 0; j < PER; ++j) l[j] = lrow[sub + 8 * j];
+            int best[2] = {0, 0};
+            float bvs[2] = {0.f, 0.f};
+#pragma unroll
+            for (int slot = 0; slot < 2; ++slot) {
+                if (slot == 1 && a.topk == 1) break;
+                const int skip = slot == 0 ? -1 : best[0];
+                const int first = skip == 0 ? 1 : 0;
+                float bv = -INFINITY;
+                int bi = 1 << 30;
+#pragma unroll
+                for (int j = 0; j < PER; ++j) {
+                    const int e = sub + 8 * j;
+                    if (e == skip || l[j] != l[j]) continue;
+                    if (bi == (1 << 30) || l[j] > bv) { bv = l[j]; bi = e; }
+                }
+#pragma unroll
+                for (int o = 4; o; o >>= 1) {
+                    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                    if (oi != (1 << 30) && (bi == (1 << 30) || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; }
+                }
+                const float lf = lrow[first];
+                if (lf != lf) { bi = first; bv = lf; }
+                else if (bi == (1 << 30)) { bi = first; bv = lf; }
+                best[slot] = bi;
+                bvs[slot] = bv;
+            }
+            float g1, g2 = 0.f;
+            if (a.topk == 1) {
+                const double mx = double(bvs[0]);
+                double sum = 0.0;
+#pragma unroll
+                for (int j = 0; j < PER; ++j) sum += exp(double(l[j]) - mx);
+#pragma unroll
+                for (int o = 4; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+                g1 = float(double(float(exp(double(bvs[0]) - mx))) / sum);
+            } else {
+                const double z = exp(double(bvs[1]) - double(bvs[0]));
+                g1 = float(1.0 / (1.0 + z));
+                g2 = float(z / (1.0 + z));
+            }
+            if (sub == 0) {
+                const int k = a.topk;
+                if (lt < ntok) {
+                    const int64_t t = t0 + lt;
+                    P.expert[t * k] = best[0];
+                    P.gate[t * k] = g1;
+                    s_exp[lt * k] = best[0];
+                    if (k == 2) {
+                        P.expert[t * k + 1] = best[1];
+                        P.gate[t * k + 1] = g2;
+                        s_exp[lt * k + 1] = best[1];
+                    }
+                } else {
+                    s_exp[lt * k] = -1;
+                    if (k == 2) s_exp[lt * k + 1] = -1;
+                }
+            }
+        }
+        if (tr && threadIdx.x == 0) tr[8] = gtime_ns();
+    }
+    // the drained token rows + Wg slot stage the per-CTA histograms of the last-CTA plan
+    ranks_hist_plan(a, P, s_exp, s_hist, 32, reinterpret_cast<int*>(sm), int((ring - sm + kRMSlots * cb) / 4), tr);
+}
+
+// ---- persistent tensor-core router (E = 32, Kp1 <= 1024): Wg resident, token rows streamed ----
+// k_route_mma reloads all of Wg (135 KB at d = 1024) for every 32-token CTA and pays the
+// two-wave tail; here one CTA per SM keeps the split Wg in shared memory for the whole launch
+// and walks the 32-token tiles tile = blockIdx.x, + gridDim.x, ... (the same tiles, histograms
+// and lrank layout as the per-CTA kernels, so scatter and plan_tail are unchanged). Each tile
+// is two 16-token halves streamed by a producer warp through two row buffers; warp w computes
+// expert tile w & 3 over K half w >> 2 (hi + lo, even / odd k-step accumulators) and the two K
+// halves meet in a fixed order at selection. Each CTA adds its tile count to the ticket once;
+// the CTA that completes the count runs the plan, with all of its shared memory as staging.
+constexpr int kRPWarps = 8;
+__host__ __device__ inline size_t rp_smem(int Kp1) {
+    return size_t(4) * rm_chunk_bytes(32, Kp1) + 2 * size_t(16) * rm_hpitch(Kp1) + 2 * 32 * 33 * 4 + 128;
+}
+
+__global__ void __launch_bounds__((kRPWarps + 1) * 32, 1) k_route_mma_p(RouteArgs a, Plan P) {
+    constexpr int E = 32, NTHR = kRPWarps * 32;
+    extern __shared__ __align__(128) uint8_t sm[];
+    const int d = a.d, Kp1 = a.Kp1, hp = rm_hpitch(Kp1);
+    const int Kc = Kp1 / 4, cpitch = (Kc + 8) * 2, nsteps = Kc / 16;
+    const uint32_t cb = rm_chunk_bytes(E, Kp1);
+    uint8_t* wgs = sm;                                  // [4 chunks][hi, lo][32][Kc + 8]
+    uint8_t* hb = wgs + 4 * cb;                         // [2 buffers][16 rows][hp]
+    float* part = reinterpret_cast<float*>(hb + 2 * 16 * hp);  // [K half][32 tokens][33]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(part + 2 * 32 * 33);
+    uint64_t* wbar = bars;          // Wg landed
+    uint64_t* hfull = bars + 1;     // [2]
+    uint64_t* hempty = bars + 3;    // [2]
+    __shared__ int s_exp[64];
+    __shared__ int s_hist[E];
+    __shared__ int s_last;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ntiles = int((a.T + 31) / 32);
+    // diagnostics (CTAs < kTraceRouteCtas): 0 start, 1 Wg landed, per tile i < 3: 2+3i rows,
+    // 3+3i MMAs, 4+3i tile done; 11 ticket
+    unsigned long long* tr = a.trace && blockIdx.x < kTraceRouteCtas ? a.trace + blockIdx.x * 16 : nullptr;
+    if (tr && threadIdx.x == 0) tr[0] = gtime_ns();
+    if (threadIdx.x == 0) {
+        mbar_init(wbar, 1);
+        for (int b = 0; b < 2; ++b) { mbar_init(hfull + b, 1); mbar_init(hempty + b, kRPWarps); }
+        fence_barrier_init();
+        s_last = 0;
+    }
+    // K padding columns of both row buffers: zeros (the copies never touch them)
+    for (int i = threadIdx.x; i < 2 * 16 * (Kp1 - d); i += blockDim.x) {
+        const int r = i / (Kp1 - d), k = d + i % (Kp1 - d);
+        reinterpret_cast<__half*>(hb + r * hp)[k] = __float2half_rn(0.f);
+    }
+    __syncthreads();
+    if (warp == kRPWarps) {
+        // ------------------------------ producer ------------------------------
+        if (lane == 0) {
+            mbar_arrive_expect_tx(wbar, 4 * cb);
+            bulk_g2s(wgs, a.wgt, 4 * cb, wbar);
+            const __half* h = static_cast<const __half*>(a.h);
+            int n = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+                for (int half = 0; half < 2; ++half, ++n) {
+                    const int b = n & 1;
+                    if (n >= 2) mbar_wait(hempty + b, ((n >> 1) - 1) & 1);
+                    const int64_t r0 = int64_t(tile) * 32 + half * 16;
+                    const int rows = int(a.T - r0 < 16 ? a.T - r0 : 16);
+                    mbar_arrive_expect_tx(hfull + b, rows > 0 ? uint32_t(rows * d * 2) : 0u);
+                    for (int r = 0; r < rows; ++r)
+                        bulk_g2s(hb + (b * 16 + r) * hp, h + (r0 + r) * d, uint32_t(d * 2), hfull + b);
+                }
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------ MMA + selection warps ------------------------------
+        const int nt = warp & 3, kq = warp >> 2;  // expert tile, K half (chunks 2kq, 2kq + 1)
+        const int lr = lane & 7, lm = lane >> 3, g = lane >> 2, t = lane & 3;
+        const float us = __int_as_float((127 - a.wg_shift) << 23);
+        mbar_wait(wbar, 0);
+        if (tr && threadIdx.x == 0) tr[1] = gtime_ns();
+        int n = 0, it = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            const int64_t t0 = int64_t(tile) * 32;
+            const int ntok = int(a.T - t0 < 32 ? a.T - t0 : 32);
+            for (int e = threadIdx.x; e < E; e += NTHR) s_hist[e] = 0;
+            for (int half = 0; half < 2; ++half, ++n) {
+                const int b = n & 1;
+                mbar_wait(hfull + b, (n >> 1) & 1);
+                if (tr && threadIdx.x == 0 && half == 0 && it < 3) tr[2 + 3 * it] = gtime_ns();
+                const int hrows = max(1, min(16, ntok - half * 16));
+                const uint32_t a_row = smem_u32(hb) + (b * 16 + min(lr + (lm & 1) * 8, hrows - 1)) * hp + (lm >> 1) * 16;
+                float acc[2][2][4];  // [hi, lo][even, odd][4]
+#pragma unroll
+                for (int h2 = 0; h2 < 2; ++h2)
+#pragma unroll
+                    for (int q = 0; q < 2; ++q)
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) acc[h2][q][i] = 0.f;
+                for (int c = 2 * kq; c < 2 * kq + 2; ++c) {
+                    const uint32_t b_row = smem_u32(wgs + c * cb) + ((lm >> 1) * E + nt * 8 + lr) * cpitch + (lm & 1) * 16;
+                    const uint32_t a_c = a_row + c * Kc * 2;
+#pragma unroll 2
+                    for (int s2 = 0; s2 < nsteps; s2 += 2) {
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) {
+                            const int st = s2 + q;
+                            uint32_t a0, a1, a2, a3, bh0, bh1, bl0, bl1;
+                            ldsm_x4(a_c + st * 32, a0, a1, a2, a3);
+                            ldsm_x4(b_row + st * 32, bh0, bh1, bl0, bl1);
+                            mma_16816(acc[0][q], a0, a1, a2, a3, bh0, bh1);
+                            mma_16816(acc[1][q], a0, a1, a2, a3, bl0, bl1);
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(hempty + b);  // this warp is done with the rows
+                // c0, c1: token g, experts nt*8+2t, +1; c2, c3: token g + 8
+                float* pk = part + kq * 32 * 33;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int tok = half * 16 + g + 8 * (i >> 1), e = nt * 8 + 2 * t + (i & 1);
+                    pk[tok * 33 + e] = (acc[0][0][i] + acc[0][1][i]) + (acc[1][0][i] + acc[1][1][i]);
+                }
+            }
+            named_bar_sync(1, NTHR);  // the tile's partial logits are in smem
+            if (tr && threadIdx.x == 0 && it < 3) tr[3 + 3 * it] = gtime_ns();
+            // selection: 8 lanes per token, all 32 tokens (see k_route_mma)
+            {
+                constexpr int PER = E / 8;
+                const int lt = warp * 4 + (lane >> 3), sub = lane & 7;
+                const int ltc = lt < ntok ? lt : ntok - 1;
+                float l[PER];
+#pragma unroll
+                for (int j = 0; j < PER; ++j)
+                    l[j] = (part[ltc * 33 + sub + 8 * j] + part[32 * 33 + ltc * 33 + sub + 8 * j]) * us;
+                int best[2] = {0, 0};
+                float bvs[2] = {0.f, 0.f};
+#pragma unroll
+                for (int slot = 0; slot < 2; ++slot) {
+                    if (slot == 1 && a.topk == 1) break;
+                    const int skip = slot == 0 ? -1 : best[0];
+                    const int first = skip == 0 ? 1 : 0;
+                    float bv = -INFINITY;
+                    int bi = 1 << 30;
+                    float lf = 0.f;
+#pragma unroll
+                    for (int j = 0; j < PER; ++j) {
+                        const int e = sub + 8 * j;
+                        if (e == first) lf = l[j];
+                        if (e == skip || l[j] != l[j]) continue;
+                        if (bi == (1 << 30) || l[j] > bv) { bv = l[j]; bi = e; }
+                    }
+#pragma unroll
+                    for (int o = 4; o; o >>= 1) {
+                        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                        if (oi != (1 << 30) && (bi == (1 << 30) || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; }
+                    }
+                    lf = __shfl_sync(0xffffffffu, lf, (lane & ~7) | first);  // the scan's first logit
+                    if (lf != lf || bi == (1 << 30)) { bi = first; bv = lf; }
+                    best[slot] = bi;
+                    bvs[slot] = bv;
+                }
+                float g1, g2 = 0.f;
+                if (a.topk == 1) {
+                    const double mx = double(bvs[0]);
+                    double sum = 0.0;
+#pragma unroll
+                    for (int j = 0; j < PER; ++j) sum += exp(double(l[j]) - mx);
+#pragma unroll
+                    for (int o = 4; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+                    g1 = float(double(float(exp(double(bvs[0]) - mx))) / sum);
+                } else {
+                    const double z = exp(double(bvs[1]) - double(bvs[0]));
+                    g1 = float(1.0 / (1.0 + z));
+                    g2 = float(z / (1.0 + z));
+                }
+                if (sub == 0) {
+                    const int k = a.topk;
+                    if (lt < ntok) {
+                        const int64_t tk = t0 + lt;
+                        P.expert[tk * k] = best[0];
+                        P.gate[tk * k] = g1;
+                        s_exp[lt * k] = best[0];
+                        if (k == 2) {
+                            P.expert[tk * k + 1] = best[1];
+                            P.gate[tk * k + 1] = g2;
+                            s_exp[lt * k + 1] = best[1];
+                        }
+                    } else {
+                        s_exp[lt * k] = -1;
+                        if (k == 2) s_exp[lt * k + 1] = -1;
+                    }
+                }
+            }
+            named_bar_sync(1, NTHR);
+            // stable ranks inside the tile + tile histogram (as ranks_hist_plan)
+            for (int i = threadIdx.x; i < 32 * a.topk; i += NTHR) {
+                const int e = s_exp[i];
+                if (e < 0) continue;
+                int r = 0;
+                for (int j = 0; j < i; ++j) r += s_exp[j] == e;
+                P.lrank[int64_t(tile) * 32 * a.topk + i] = r;
+                atomicAdd(&s_hist[e], 1);
+            }
+            named_bar_sync(1, NTHR);
+            for (int e = threadIdx.x; e < E; e += NTHR) P.cta_counts[int64_t(tile) * E + e] = s_hist[e];
+            named_bar_sync(1, NTHR);
+            if (tr && threadIdx.x == 0 && it < 3) tr[4 + 3 * it] = gtime_ns();
+        }
+    }
+    __syncthreads();  // producer and consumers: the loop is over, all of smem is free
+    if (threadIdx.x == 0) {  // one ticket per CTA: its tile count
+        const unsigned mine = unsigned((ntiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1);
+        __threadfence();  // release this CTA's tiles (ordered by the barrier)
+        if (atomicAdd(&P.tickets[0], mine) + mine == unsigned(ntiles)) {
+            __threadfence();  // acquire every other CTA's
+            s_last = 1;
+        }
+        if (tr) tr[11] = gtime_ns();
+    }
+    __syncthreads();
+    if (!s_last) return;
+    if (a.trace && threadIdx.x == 0) a.trace[(kTraceRouteCtas - 1) * 16 + 13] = gtime_ns();  // plan start
+    plan_tail(a, P, ntiles, 32, reinterpret_cast<int*>(sm), int(rp_smem(Kp1) / 4) - 64);
+    __syncthreads();
+    if (a.trace && threadIdx.x == 0) a.trace[(kTraceRouteCtas - 1) * 16 + 14] = gtime_ns();  // plan end
+}
+
 // ---- large T (prefill) ----------------------------------------------------------------
 // k_route_logits: one warp = 32 tokens (lane = token) x 8 experts; a CTA = 4
 // warps = 32 tokens x 32 experts, grid (T/32, E/32). Each Wg row is a smem
@@ -1396,6 +1861,12 @@ cudaError_t launch_route_decode(const RouteArgs& a, const Plan& P, size_t smem, 
     }
 }
 
+// MOQE_ROUTE_EXACT=1: prefill routing keeps the reference's exact-order fp32 chains
+bool route_mma_enabled() {
+    static const bool v = [] { const char* s = getenv("MOQE_ROUTE_EXACT"); return !(s && atoi(s) == 1); }();
+    return v;
+}
+
 // Route tile: tokens per routing CTA for a given T (must match scatter's tt).
 constexpr int64_t kRouteBigThreshold = 512;
 int route_tokens_per_cta(int64_t T) { return T <= kRouteBigThreshold ? kRouteSmallWarps : kRouteSelWarps; }
@@ -1408,8 +1879,40 @@ cudaError_t launch_route(const RouteArgs& a, const Plan& P, cudaStream_t st) {
         dim3 lg(unsigned((a.T + kRLTok - 1) / kRLTok), unsigned((a.E + kRLExp - 1) / kRLExp));
         const bool vec = a.h_f16 && (a.d % 8) == 0 && (a.E % 32) == 0 && (reinterpret_cast<uintptr_t>(a.h) & 15) == 0;
         const size_t sm2 = rl2_smem(a.d, a.E);
+        int dev_ = 0;
+        cudaGetDevice(&dev_);
+        const int di = dev_ < kMaxDevices ? dev_ : 0;
+        const size_t smm = rm_smem(a.E, a.Kp1);
+        if (vec && a.wgt && a.wg_finite && a.E == 32 && a.Kp1 % 128 == 0 && a.Kp1 >= a.d &&
+            rp_smem(a.Kp1) <= 220 * 1024 && route_mma_enabled()) {
+            static bool cfgp[kMaxDevices] = {};
+            static int nsm[kMaxDevices] = {};
+            if (!cfgp[di]) {
+                cudaFuncSetAttribute(k_route_mma_p, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+                cudaDeviceGetAttribute(&nsm[di], cudaDevAttrMultiProcessorCount, dev_);
+                cfgp[di] = true;
+            }
+            const unsigned gp = unsigned(std::min<int64_t>((a.T + 31) / 32, nsm[di]));
+            k_route_mma_p<<<gp, (kRPWarps + 1) * 32, rp_smem(a.Kp1), st>>>(a, P);
+            return cudaGetLastError();
+        }
+        if (vec && a.wgt && a.wg_finite && (a.E == 32 || a.E == 64) && a.Kp1 % 128 == 0 && a.Kp1 >= a.d &&
+            smm <= 220 * 1024 && route_mma_enabled()) {
+            static bool cfgm[kMaxDevices][2] = {};
+            const unsigned gm = unsigned((a.T + 31) / 32);
+            if (a.E == 32) {
+                if (!cfgm[di][0]) { cudaFuncSetAttribute(k_route_mma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); cfgm[di][0] = true; }
+                k_route_mma<1><<<gm, (kRMWarps + 1) * 32, smm, st>>>(a, P);
+            } else {
+                if (!cfgm[di][1]) { cudaFuncSetAttribute(k_route_mma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); cfgm[di][1] = true; }
+                k_route_mma<2><<<gm, (kRMWarps + 1) * 32, smm, st>>>(a, P);
+            }
+            return cudaGetLastError();
+        }
         if (vec && (a.E == 32 || a.E == 64) && sm2 <= 220 * 1024 && (reinterpret_cast<uintptr_t>(a.wg) & 15) == 0) {
-            static bool cfg32 = false, cfg64 = false;
+            static bool cfg2[kMaxDevices][2] = {};
+            bool& cfg32 = cfg2[di][0];
+            bool& cfg64 = cfg2[di][1];
             const unsigned g2 = unsigned((a.T + 31) / 32);
             if (a.E == 32) {
                 if (!cfg32) { cudaFuncSetAttribute(k_route_logits2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); cfg32 = true; }
