@@ -47,6 +47,12 @@ constexpr int kMaxRouteSmem = 200 * 1024;
 #define DEC_F1_UNROLL 8
 #endif
 constexpr int kF1Unroll = DEC_F1_UNROLL;
+#ifndef DEC_PLAN_ROWS
+#define DEC_PLAN_ROWS 16
+#endif
+// rows per planned unit (<= kDecUnitRows, the buffer capacity); an expert with more rows gets
+// several units. Units of <= 8 rows keep their fc2 partials in registers for the whole run.
+constexpr int kDecPlanRows = DEC_PLAN_ROWS;
 
 __device__ __forceinline__ void red_add_s64(long long* p, long long v) {
     asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -336,7 +342,7 @@ __global__ void __launch_bounds__(kDecThreads) k_dec_route(const DecArgs a) {
     if (warp == 0) {  // exclusive scans of rows and of units (<= 16 rows each), E <= 256
         const int per = (E + 31) / 32, e0 = lane * per;
         int sr = 0, su = 0;
-        for (int e = e0; e < min(E, e0 + per); ++e) { sr += cnt[e]; su += (cnt[e] + kDecUnitRows - 1) / kDecUnitRows; }
+        for (int e = e0; e < min(E, e0 + per); ++e) { sr += cnt[e]; su += (cnt[e] + kDecPlanRows - 1) / kDecPlanRows; }
         int ir = sr, iu = su;
         for (int o = 1; o < 32; o <<= 1) {
             const int vr = __shfl_up_sync(0xffffffffu, ir, o), vu = __shfl_up_sync(0xffffffffu, iu, o);
@@ -347,7 +353,7 @@ __global__ void __launch_bounds__(kDecThreads) k_dec_route(const DecArgs a) {
             off[e] = pr;
             ubase[e] = pu;
             pr += cnt[e];
-            pu += (cnt[e] + kDecUnitRows - 1) / kDecUnitRows;
+            pu += (cnt[e] + kDecPlanRows - 1) / kDecPlanRows;
         }
         if (lane == 31) { off[E] = ir; ubase[E] = iu; }
     }
@@ -367,8 +373,8 @@ __global__ void __launch_bounds__(kDecThreads) k_dec_route(const DecArgs a) {
         }
         for (int e = tid; e < E; e += kDecThreads) {
             const int n = cnt[e];
-            for (int p = 0; p * kDecUnitRows < n; ++p)
-                a.units[ubase[e] + p] = make_int4(e, off[e] + p * kDecUnitRows, min(kDecUnitRows, n - p * kDecUnitRows), 0);
+            for (int p = 0; p * kDecPlanRows < n; ++p)
+                a.units[ubase[e] + p] = make_int4(e, off[e] + p * kDecPlanRows, min(kDecPlanRows, n - p * kDecPlanRows), 0);
         }
         if (tid == 0) *a.n_units = ubase[E];
     }
@@ -858,8 +864,8 @@ __device__ __forceinline__ void dec_fused_decide(const DecArgs& a, DecPlanSmem& 
         const bool first1 = lane + 32 < R && m10 == 0 && (m11 & ltm) == 0;
         const int cnt0 = __popc(m00) + __popc(m01), cnt1 = __popc(m11);  // first rows only
         // (rows, units) of each expert at its first row, packed: rows | units << 16
-        const int v0 = first0 ? (cnt0 | (((cnt0 + kDecUnitRows - 1) / kDecUnitRows) << 16)) : 0;
-        const int v1 = first1 ? (cnt1 | (((cnt1 + kDecUnitRows - 1) / kDecUnitRows) << 16)) : 0;
+        const int v0 = first0 ? (cnt0 | (((cnt0 + kDecPlanRows - 1) / kDecPlanRows) << 16)) : 0;
+        const int v1 = first1 ? (cnt1 | (((cnt1 + kDecPlanRows - 1) / kDecPlanRows) << 16)) : 0;
         int i0 = v0, i1 = v1;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -873,9 +879,9 @@ __device__ __forceinline__ void dec_fused_decide(const DecArgs& a, DecPlanSmem& 
             const bool fr = hb == 0 ? first0 : first1;
             if (fr) {
                 const int x = hb == 0 ? x0 : x1, c = hb == 0 ? cnt0 : cnt1, e = ee[hb];
-                for (int q = 0; q * kDecUnitRows < c; ++q)
+                for (int q = 0; q * kDecPlanRows < c; ++q)
                     P.units[(x >> 16) + q] =
-                        make_int4(e, (x & 0xFFFF) + q * kDecUnitRows, min(kDecUnitRows, c - q * kDecUnitRows), 0);
+                        make_int4(e, (x & 0xFFFF) + q * kDecPlanRows, min(kDecPlanRows, c - q * kDecPlanRows), 0);
             }
         }
         // row positions: offset of the expert's first row + rank

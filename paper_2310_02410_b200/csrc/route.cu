@@ -128,67 +128,74 @@ __device__ void plan_tail(const RouteArgs& a, Plan P, int n_ctas, int tt, int* s
     const int E = a.E, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nw = blockDim.x >> 5;
     const int RB = blockDim.x >= E ? int(blockDim.x) / E : 1;  // row blocks of the two-level scan
-    const bool staged = scr != nullptr && int64_t(n_ctas) * E + E + int64_t(RB) * E <= scr_ints;
-    int* s_cnt = staged ? scr + n_ctas * E : nullptr;
+    // staging: [rows][E] histogram rows (as many as fit), s_cnt [E] carries, seg [RB][E]
+    const int rows_fit = scr ? int((int64_t(scr_ints) - E - int64_t(RB) * E) / E) & ~3 : 0;
+    const bool staged = rows_fit >= 32;
+    int* s_cnt = staged ? scr + rows_fit * E : nullptr;
     if (staged) {
-        // the histograms: 16-byte loads, 8 in flight per thread (E % 4 == 0: rows stay aligned)
-        const int n = n_ctas * E;
-        if ((E & 3) == 0) {
-            const int n4 = n >> 2;
-            const int4* src = reinterpret_cast<const int4*>(P.cta_counts);
-            int4* dst = reinterpret_cast<int4*>(scr);
-            for (int i0 = threadIdx.x; i0 < n4; i0 += 8 * blockDim.x) {
-                int4 v[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int i = i0 + u * blockDim.x;
-                    v[u] = i < n4 ? __ldcg(src + i) : make_int4(0, 0, 0, 0);
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int i = i0 + u * blockDim.x;
-                    if (i < n4) dst[i] = v[u];
-                }
-            }
-        } else {
-            for (int i = threadIdx.x; i < n; i += blockDim.x) scr[i] = __ldcg(P.cta_counts + i);
-        }
-        __syncthreads();
-        if (a.trace && threadIdx.x == 0) a.trace[(kTraceRouteCtas - 1) * 16 + 9] = gtime_ns();
-        // 1. exclusive scan over CTAs per expert, two levels: thread (row block rb, expert e) sums
-        //    its block of CTAs, then rescans it from the sum of the blocks above
         int* seg = s_cnt + E;  // [RB][E]
         const int e = threadIdx.x % E, rb = threadIdx.x / E;
-        const int per = (n_ctas + RB - 1) / RB, r0 = rb * per, r1 = min(n_ctas, r0 + per);
-        if (rb < RB) {
-            int sum = 0;
-#pragma unroll 8
-            for (int r = r0; r < r1; ++r) sum += scr[r * E + e];
-            seg[rb * E + e] = sum;
-        }
-        __syncthreads();
-        if (rb < RB) {
-            int run = 0;
-            for (int q = 0; q < rb; ++q) run += seg[q * E + e];
-#pragma unroll 8
-            for (int r = r0; r < r1; ++r) {
-                const int v = scr[r * E + e];
-                scr[r * E + e] = run;
-                run += v;
+        for (int i = threadIdx.x; i < E; i += blockDim.x) s_cnt[i] = 0;
+        // blocks of rows_fit histogram rows; each: load (16-byte loads, 8 in flight per thread),
+        // two-level exclusive scan per expert carried across blocks, write back
+        for (int blk0 = 0; blk0 < n_ctas; blk0 += rows_fit) {
+            const int nb = min(rows_fit, n_ctas - blk0);
+            const int n = nb * E;
+            int32_t* gsrc = P.cta_counts + int64_t(blk0) * E;
+            if ((E & 3) == 0) {
+                const int n4 = n >> 2;
+                const int4* src = reinterpret_cast<const int4*>(gsrc);
+                int4* dst = reinterpret_cast<int4*>(scr);
+                for (int i0 = threadIdx.x; i0 < n4; i0 += 8 * blockDim.x) {
+                    int4 v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int i = i0 + u * blockDim.x;
+                        v[u] = i < n4 ? __ldcg(src + i) : make_int4(0, 0, 0, 0);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int i = i0 + u * blockDim.x;
+                        if (i < n4) dst[i] = v[u];
+                    }
+                }
+            } else {
+                for (int i = threadIdx.x; i < n; i += blockDim.x) scr[i] = __ldcg(gsrc + i);
             }
-            if (rb == RB - 1) {
-                s_cnt[e] = run;
-                P.counts[e] = run;
+            __syncthreads();
+            const int per = (nb + RB - 1) / RB, r0 = rb * per, r1 = min(nb, r0 + per);
+            if (rb < RB) {
+                int sum = 0;
+#pragma unroll 8
+                for (int r = r0; r < r1; ++r) sum += scr[r * E + e];
+                seg[rb * E + e] = sum;
             }
+            __syncthreads();
+            if (rb < RB) {
+                int run = s_cnt[e];
+                for (int q = 0; q < rb; ++q) run += seg[q * E + e];
+#pragma unroll 8
+                for (int r = r0; r < r1; ++r) {
+                    const int v = scr[r * E + e];
+                    scr[r * E + e] = run;
+                    run += v;
+                }
+            }
+            __syncthreads();
+            if (rb == 0) {  // carry into the next block: + this block's column total
+                int tot = 0;
+                for (int q = 0; q < RB; ++q) tot += seg[q * E + e];
+                s_cnt[e] += tot;
+            }
+            if ((E & 3) == 0) {
+                for (int i = threadIdx.x; i < (n >> 2); i += blockDim.x)
+                    reinterpret_cast<int4*>(gsrc)[i] = reinterpret_cast<const int4*>(scr)[i];
+            } else {
+                for (int i = threadIdx.x; i < n; i += blockDim.x) gsrc[i] = scr[i];
+            }
+            __syncthreads();
         }
-        __syncthreads();
-        if (a.trace && threadIdx.x == 0) a.trace[(kTraceRouteCtas - 1) * 16 + 10] = gtime_ns();
-        if ((E & 3) == 0) {
-            for (int i = threadIdx.x; i < (n >> 2); i += blockDim.x)
-                reinterpret_cast<int4*>(P.cta_counts)[i] = reinterpret_cast<const int4*>(scr)[i];
-        } else {
-            for (int i = threadIdx.x; i < n; i += blockDim.x) P.cta_counts[i] = scr[i];
-        }
+        for (int i = threadIdx.x; i < E; i += blockDim.x) P.counts[i] = s_cnt[i];
     } else {
     // 1. exclusive scan of per-CTA counts over CTAs, per expert (warp per expert)
     for (int e = warp; e < E; e += nw) {
@@ -228,7 +235,7 @@ __device__ void plan_tail(const RouteArgs& a, Plan P, int n_ctas, int tt, int* s
         for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
             const int64_t t = i / a.topk;
             const int e = __ldcg(P.expert + i);
-            const int base = staged ? scr[(t / tt) * E + e] : P.cta_counts[(t / tt) * E + e];
+            const int base = staged && n_ctas <= rows_fit ? scr[(t / tt) * E + e] : __ldcg(P.cta_counts + (t / tt) * E + e);
             const int pos = P.offsets[e] + base + __ldcg(P.lrank + i);
             P.perm_token[pos] = int32_t(t);
             P.perm_gate[pos] = __ldcg(P.gate + i);
