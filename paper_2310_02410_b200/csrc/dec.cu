@@ -1601,7 +1601,9 @@ static bool dec_config(int bits, DecArgs& a, size_t* smem_out) {
         const size_t cb = size_t(2 * G.Ep) * ((a.Kp1 / 4 + 8) * 2), pb = G.floats() * 4;
         const size_t ring = size_t(pairs) * (a.stage_bytes + a.stage2_bytes);
         a.route_nbuf = ring < pb ? 0 : int(std::min<size_t>(4, (ring - pb) / cb));
-        if (a.route_nbuf < 2) return false;
+        // a cluster CTA holds its 4/cl chunks at once; alone it streams them through >= 2 buffers
+        const int cl = a.route_cluster == 2 || a.route_cluster == 4 ? a.route_cluster : 1;
+        if (a.route_nbuf < (cl > 1 ? 4 / cl : 2)) return false;
     }
     a.n_stages = a.n_stages2 = pairs;
     *smem_out = size_t(pairs) * (a.stage_bytes + a.stage2_bytes) + fixed + size_t(pairs) * 32;
@@ -1611,7 +1613,11 @@ static bool dec_config(int bits, DecArgs& a, size_t* smem_out) {
 cudaError_t launch_dec(int bits, const DecArgs& a0, cudaStream_t st, int num_sms) {
     DecArgs a = a0;
     size_t smem = 0;
-    if (a.fused && !dec_config(bits, a, &smem)) a.fused = 0;  // fall back to the router launch
+    if (a.fused && !dec_config(bits, a, &smem)) {
+        // a larger cluster needs fewer gate-weight chunks per CTA (e.g. E = 64 at d = 1024)
+        if (a.route_cluster == 2) a.route_cluster = 4;
+        if (a.route_cluster != 4 || !dec_config(bits, a, &smem)) a.fused = 0;  // separate router launch
+    }
     if (!a.fused && !dec_config(bits, a, &smem)) return cudaErrorInvalidConfiguration;
     if (!a.fused) {  // ---- router (one cluster) ----
         const int C = route_cluster(a.d, a.E);
