@@ -479,6 +479,13 @@ namespace {
 // Shared forward body. With pre_expert/pre_gate (expert-parallel owner side),
 // rows arrive already routed: the plan is built from the given ids (top-1 per
 // row) and the router is skipped.
+// The decode kernel (k_dec) takes the forward: its output is written with plain stores only
+// (no atomics), so it may target mapped pinned host memory directly.
+bool dec_path_taken(moqe_bank_t b, int64_t t, int top_k, moqe_path path) {
+    return !b->log && b->wdec && dec_enabled() && (path == MOQE_PATH_AUTO || path == MOQE_PATH_GEMV) &&
+           dec_supported(t, top_k, int(b->d), b->E, b->Kp1, b->Np1, b->Np2);
+}
+
 moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64_t t, const float* wg, int top_k,
                          void* out, moqe_dtype out_dtype, int32_t* expert_out, float* gate_out, moqe_path path,
                          void* stream, const int32_t* pre_expert, const float* pre_gate) {
@@ -501,8 +508,7 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
         if (path == MOQE_PATH_GEMV) return fail(MOQE_NOT_SUPPORTED, "moe_forward: log-scale banks take the GEMM path");
         path = MOQE_PATH_GEMM;
     }
-    if (!pre && !b->log && b->wdec && dec_enabled() && (path == MOQE_PATH_AUTO || path == MOQE_PATH_GEMV) &&
-        dec_supported(t, top_k, int(b->d), b->E, b->Kp1, b->Np1, b->Np2)) {
+    if (!pre && dec_path_taken(b, t, top_k, path)) {
         moqe_status s = ensure_dec_workspace(b);
         if (s != MOQE_OK) return s;
         s = ensure_workspace(b, t, top_k);  // routing outputs when the caller passes none
@@ -763,11 +769,21 @@ moqe_status moqe_gpu_moe_forward_host(moqe_bank_t b, const void* h_host, moqe_dt
         MOQE_CUDA(cudaMalloc(&b->o_dev, need));
         b->host_cap = need;
     }
+    // Pinned (page-locked, mapped) output buffer on the decode path: the kernel's finishers store
+    // the rows straight into host memory (posted writes over the host link, overlapped with the
+    // kernel's tail), which removes the D2H copy and its launch from the call.
+    void* out_dev = nullptr;
+    if (b->wg && dec_path_taken(b, t, top_k, MOQE_PATH_AUTO)) {
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, out_host) == cudaSuccess && pa.type == cudaMemoryTypeHost)
+            out_dev = pa.devicePointer;
+        (void)cudaGetLastError();  // pageable memory: not an error, just no direct path
+    }
     MOQE_CUDA(cudaMemcpyAsync(b->h_dev, h_host, hb, cudaMemcpyHostToDevice, st));
-    moqe_status s = moqe_gpu_moe_forward(b, b->h_dev, h_dtype, t, nullptr, top_k, b->o_dev, out_dtype,
-                                         nullptr, nullptr, MOQE_PATH_AUTO, st);
+    moqe_status s = moqe_gpu_moe_forward(b, b->h_dev, h_dtype, t, nullptr, top_k, out_dev ? out_dev : b->o_dev,
+                                         out_dtype, nullptr, nullptr, MOQE_PATH_AUTO, st);
     if (s != MOQE_OK) return s;
-    MOQE_CUDA(cudaMemcpyAsync(out_host, b->o_dev, ob, cudaMemcpyDeviceToHost, st));
+    if (!out_dev) MOQE_CUDA(cudaMemcpyAsync(out_host, b->o_dev, ob, cudaMemcpyDeviceToHost, st));
     MOQE_CUDA(cudaStreamSynchronize(st));
     return MOQE_OK;
 }

@@ -546,10 +546,11 @@ __device__ __forceinline__ void dec_fc1_piece(const unsigned char* piece, int kt
 }
 
 // fc2 partial of one slice for one warp: QW channel groups starting at group q0 of a piece.
-// fc2 converts exactly (codec.cuh unpack_chunk: LOP3 + HFMA2 per code pair). A magic-offset
-// variant (signed magics over a complemented layout, per-slice correction) was built and
-// measured: parity-green, no faster (the decode slice is bound by the fc1 warps' latency, see
-// DESIGN.md), slower for int8; the exact path stays.
+// fc2 converts exactly (codec.cuh unpack_chunk: LOP3 + HFMA2 per code pair). A raw variant (the
+// fc1 unpack against mid rows pre-scaled by 2^-s(k), per-slice correction Z) was built twice
+// and measured parity-green but no faster: removing the fc2 math entirely (DEC_SKIP_FC2) saves
+// only ~4 us of the ~32 us step, the slice pipeline being bound by data arrival and the
+// tail, not by the converter ALU.
 template <int BITS, int QW, int NB>
 __device__ __forceinline__ void dec_fc2_piece(const unsigned char* piece, int q0, int g, int t,
                                               const unsigned char* mid, float (&c2)[QW][NB][4]) {
@@ -597,40 +598,32 @@ struct DecPlanSmem {
 // cores, Wg (pre-split by the bank into fp16 hi + lo, x 2^sw, four K chunks) as the 16-expert A
 // tiles and the activation rows as 8-token B tiles; parallel-order fp32 sums, so north_star's
 // near-tie exemption applies. In a cluster of cl CTAs (2 or 4), rank r owns chunks
-// [r*4/cl, (r+1)*4/cl) (staged before the PDL wait). A work item is one (expert tile, token
-// tile); two warps split its K range and meet over a named barrier, then the item's 16 x 8 table
-// goes into every CTA of the cluster (its own included) with st.async (mbarrier complete_tx: no
-// cluster barrier, no fence). Each CTA adds the cl tables in rank order, so every CTA of every
-// cluster holds the same logits. Without a cluster the four chunks stream through nbuf buffers.
-// Layout behind the chunk buffers: lg [32][Ep + 4], the per-rank tables [cl][Ep16][32 tokens],
-// the K-half scratch [8 items][32 lanes][4].
+// [r*4/cl, (r+1)*4/cl) (staged before the PDL wait). Warp w owns expert tile w % mtiles and the
+// K steps s = w / mtiles (mod KP) of the CTA's range, for EVERY token tile: each Wg byte is read
+// from shared memory once per CTA (the routing phase is bound by shared-memory wavefronts, not
+// by the HMMAs). The KP partial tables of an expert tile meet in shared memory (fixed kp order),
+// and each (expert tile, token tile) table goes into every CTA of the cluster (its own included)
+// with st.async (mbarrier complete_tx: no cluster barrier, no fence), transposed to
+// [token][expert]. The top-k adds the cl tables in rank order, so every CTA of every cluster
+// holds the same logits. Without a cluster the four chunks stream through nbuf buffers.
+// Layout behind the chunk buffers: the per-rank tables [cl][32 tokens][Ep16 + 4], the K-part
+// scratch [16 warps][4 token tiles][32 lanes][4].
 struct DecRouteGeom {
-    int Ep, Ep16, lgp, cl;
+    int Ep, Ep16, tp, cl;
     __host__ __device__ DecRouteGeom(int E, int cl_) {
         Ep = (E + 7) & ~7;
         Ep16 = (E + 15) & ~15;
-        lgp = Ep + 4;  // 16 B row skew: conflict-free per-token scans
+        tp = Ep16 + 4;  // 16 B row skew
         cl = cl_;
     }
-    __host__ __device__ size_t recv_off() const { return size_t(32) * lgp; }
-    __host__ __device__ size_t pair_off() const { return recv_off() + size_t(cl) * 32 * Ep16; }
-    __host__ __device__ size_t floats() const { return pair_off() + 8 * 32 * 4; }
+    __host__ __device__ size_t tab() const { return size_t(32) * tp; }
+    __host__ __device__ size_t pair_off() const { return size_t(cl) * tab(); }
+    __host__ __device__ size_t floats() const { return pair_off() + 16 * 4 * 32 * 4; }
 };
 
-__device__ __forceinline__ float redux_max_f32(float v) {  // warp-wide (sm_100a)
-    float m;
-    asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(m) : "f"(v));
-    return m;
-}
-__device__ __forceinline__ unsigned redux_min_u32(unsigned v) {
-    unsigned m;
-    asm volatile("redux.sync.min.u32 %0, %1, 0xffffffff;" : "=r"(m) : "r"(v));
-    return m;
-}
-
-__device__ __forceinline__ void st_async_v2(uint32_t addr, float x, float y, uint32_t bar) {
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(addr), "f"(x),
-                 "f"(y), "r"(bar)
+__device__ __forceinline__ void st_async_f32(uint32_t addr, float x, uint32_t bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(addr),
+                 "r"(__float_as_uint(x)), "r"(bar)
                  : "memory");
 }
 
@@ -646,47 +639,52 @@ __device__ __forceinline__ void dec_fused_route(const DecArgs& a, unsigned char*
     const int tid = threadIdx.x, g = lane >> 2, t = lane & 3;
     constexpr int NW = kF1Warps + kF2Warps;  // compute warps (16)
     const int mtiles = Ep16 / 16, ttiles = (T + 7) >> 3, items = mtiles * ttiles;
-    const int ks = 2 * items <= NW ? 2 : 1;  // K halves per item (warp pairs)
-    float* recv = lg + G.recv_off();          // [cl][Ep16 experts][32 tokens]
-    const int tab = 32 * Ep16;
+    const int KP = NW / mtiles;  // K parts per expert tile (E <= 256: mtiles <= 16)
+    const int mt = warp % mtiles, kp = warp / mtiles;
+    const bool mma_warp = warp < mtiles * KP;
     if (tid == 0) mbar_arrive_expect_tx(rbar + 5, uint32_t(cl) * items * 128 * 4);
     int rtr = 0;
     const int rk = blockIdx.x < 8 ? int(blockIdx.x) : 7;
     if (blockIdx.x < 8) route_trace(a, rk, rtr, 30);
     const int cpr = 4 / cl;  // K chunks of this CTA
     const int c_begin = crank * cpr, c_end = c_begin + cpr;
-    // up to two items per warp (E > 128 with T > 16)
-    float acc[2][2][4];  // [item][hi, lo][4]
+    float acc[4][2][4];  // [token tile][hi, lo][4]
 #pragma unroll
-    for (int x = 0; x < 2; ++x)
+    for (int x = 0; x < 4; ++x)
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2)
 #pragma unroll
             for (int i = 0; i < 4; ++i) acc[x][h2][i] = 0.f;
+    const unsigned char* br[4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x) br[x] = hs + size_t(min(x * 8 + g, T - 1)) * hpitch + 4 * t;
     for (int c = c_begin; c < c_end; ++c) {
         const int bi = cl > 1 ? c - c_begin : c % nbuf;
         const unsigned char* buf = rbase + size_t(bi) * cbytes;
         mbar_wait(rbar + bi, cl > 1 ? 0 : (c / nbuf) & 1);
+        if (mma_warp) {
+            const unsigned char* ar = buf + size_t(mt * 16 + g) * cpitch + 4 * t;
+            const int gs0 = (c - c_begin) * nsteps;  // K steps are dealt round-robin over the kp warps
+            for (int st = ((kp - gs0) % KP + KP) % KP; st < nsteps; st += KP) {
+                const int kk = st * 16;
+                uint32_t af[2][4];
 #pragma unroll
-        for (int x = 0; x < 2; ++x) {
-            const int wi = warp + x * NW;  // (item, K half)
-            if (warp < NW && wi < items * ks) {
-                const int it = wi % items, kq = wi / items;
-                const int mt = it % mtiles, nt = it / mtiles;
-                const unsigned char* ar = buf + size_t(mt * 16 + g) * cpitch + 4 * t;
-                const unsigned char* br = hs + size_t(min(nt * 8 + g, T - 1)) * hpitch + (c * Kc + 2 * t) * 2;
-                for (int st = kq; st < nsteps; st += ks) {
-                    const int kk = st * 16;
+                for (int h2 = 0; h2 < 2; ++h2) {
+                    const unsigned char* aa = ar + size_t(h2 * Ep) * cpitch + kk * 2;
+                    af[h2][0] = *reinterpret_cast<const uint32_t*>(aa);
+                    af[h2][1] = *reinterpret_cast<const uint32_t*>(aa + 8 * cpitch);
+                    af[h2][2] = *reinterpret_cast<const uint32_t*>(aa + 16);
+                    af[h2][3] = *reinterpret_cast<const uint32_t*>(aa + 8 * cpitch + 16);
+                }
+                const int ko = (c * Kc + kk) * 2;
 #pragma unroll
-                    for (int h2 = 0; h2 < 2; ++h2) {
-                        const unsigned char* aa = ar + size_t(h2 * Ep) * cpitch + kk * 2;
-                        const uint32_t a0 = *reinterpret_cast<const uint32_t*>(aa);
-                        const uint32_t a1 = *reinterpret_cast<const uint32_t*>(aa + 8 * cpitch);
-                        const uint32_t a2 = *reinterpret_cast<const uint32_t*>(aa + 16);
-                        const uint32_t a3 = *reinterpret_cast<const uint32_t*>(aa + 8 * cpitch + 16);
-                        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(br + kk * 2);
-                        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(br + kk * 2 + 16);
-                        mma_16816(acc[x][h2], a0, a1, a2, a3, b0, b1);
+                for (int x = 0; x < 4; ++x) {
+                    if (x < ttiles) {
+                        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(br[x] + ko);
+                        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(br[x] + ko + 16);
+#pragma unroll
+                        for (int h2 = 0; h2 < 2; ++h2)
+                            mma_16816(acc[x][h2], af[h2][0], af[h2][1], af[h2][2], af[h2][3], b0, b1);
                     }
                 }
             }
@@ -703,61 +701,52 @@ __device__ __forceinline__ void dec_fused_route(const DecArgs& a, unsigned char*
 #ifdef DEC_PLAN_TRACE
     if (blockIdx.x < 8) route_trace(a, rk, rtr, 40);
 #endif
-    // K halves meet (warp pairs, named barriers 1..), then the item's table goes to every CTA
+    // the K parts of each expert tile meet in shared memory (kp order), then each table goes to
+    // every CTA of the cluster
+    float* pair = lg + G.pair_off();  // [NW][4 token tiles][32 lanes][4]
+    if (mma_warp) {
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+            if (x < ttiles)
+                reinterpret_cast<float4*>(pair)[(warp * 4 + x) * 32 + lane] =
+                    make_float4(acc[x][0][0] + acc[x][1][0], acc[x][0][1] + acc[x][1][1], acc[x][0][2] + acc[x][1][2],
+                                acc[x][0][3] + acc[x][1][3]);
+    }
     if (cl > 1) cluster_wait_acquire();  // the peers' barriers are initialised (arrived at kernel start)
-    float* pair = lg + G.pair_off();  // the second K half of each item: [items <= 8][32 lanes][4]
-#pragma unroll
-    for (int x = 0; x < 2; ++x) {
-        const int wi = warp + x * NW;
-        if (warp < NW && wi < items * ks) {
-            const int it = wi % items, kq = wi / items;
-            float v[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) v[i] = acc[x][0][i] + acc[x][1][i];
-            if (ks == 2) {
-                float4* pp = reinterpret_cast<float4*>(pair) + it * 32 + lane;
-                if (kq == 1) *pp = make_float4(v[0], v[1], v[2], v[3]);
-                named_bar_sync(1 + it, 64);
-                if (kq == 1) continue;
-                const float4 o = *pp;
-                v[0] += o.x; v[1] += o.y; v[2] += o.z; v[3] += o.w;
-            }
-            const int mt = it % mtiles, nt = it / mtiles;
-            // c0, c1: expert mt*16+g, tokens nt*8+2t, +1; c2, c3: expert + 8. Table [expert][token].
-            const int e0 = mt * 16 + g, tk0 = nt * 8 + 2 * t;
-            float* tb = recv + size_t(crank) * tab;
-            for (int r = 0; r < cl; ++r) {
-                const uint32_t bar = map_rank(rbar + 5, uint32_t(r));
-                st_async_v2(map_rank(tb + e0 * 32 + tk0, uint32_t(r)), v[0], v[1], bar);
-                st_async_v2(map_rank(tb + (e0 + 8) * 32 + tk0, uint32_t(r)), v[2], v[3], bar);
-            }
+    __syncthreads();
+    float* recv = lg;  // [cl][32 tokens][tp]
+    for (int it = warp; it < items; it += kDecFfnWarps) {
+        const int imt = it % mtiles, x = it / mtiles;
+        float4 v = reinterpret_cast<const float4*>(pair)[(imt * 4 + x) * 32 + lane];
+        for (int q = 1; q < KP; ++q) {
+            const float4 o = reinterpret_cast<const float4*>(pair)[((q * mtiles + imt) * 4 + x) * 32 + lane];
+            v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+        }
+        // c0, c1: expert imt*16+g, tokens x*8+2t, +1; c2, c3: expert + 8
+        const int e0 = imt * 16 + g, tk0 = x * 8 + 2 * t;
+        float* tb = recv + size_t(crank) * G.tab();
+        for (int r = 0; r < cl; ++r) {
+            const uint32_t bar = map_rank(rbar + 5, uint32_t(r));
+            st_async_f32(map_rank(tb + tk0 * G.tp + e0, uint32_t(r)), v.x, bar);
+            st_async_f32(map_rank(tb + (tk0 + 1) * G.tp + e0, uint32_t(r)), v.y, bar);
+            st_async_f32(map_rank(tb + tk0 * G.tp + e0 + 8, uint32_t(r)), v.z, bar);
+            st_async_f32(map_rank(tb + (tk0 + 1) * G.tp + e0 + 8, uint32_t(r)), v.w, bar);
         }
     }
 #ifdef DEC_PLAN_TRACE
     if (blockIdx.x < 8) route_trace(a, rk, rtr, 42);
 #endif
     mbar_wait(rbar + 5, 0);
-#ifdef DEC_PLAN_TRACE
-    if (blockIdx.x < 8) route_trace(a, rk, rtr, 43);
-#endif
-    const float unscale = __int_as_float((127 - a.wg_shift) << 23);  // exact power of two
-    for (int e = warp; e < E; e += kDecFfnWarps)
-        for (int tk = lane; tk < T; tk += 32) {
-            float v = recv[e * 32 + tk];
-            for (int r = 1; r < cl; ++r) v += recv[size_t(r) * tab + e * 32 + tk];  // rank order
-            lg[tk * G.lgp + e] = v * unscale;
-        }
-    __syncthreads();
     if (blockIdx.x < 8) route_trace(a, rk, rtr, 32);
 }
 
-// Top-k, gates and the plan from the logits lg [T][Ep + 4] (every CTA computes the same plan),
+// Top-k, gates and the plan from the logit tables (every CTA computes the same plan),
 // and the activation rows scaled in place by 2^-s(k) (the fc1 weight field shifts) with the
 // per-token correction Z (see unpack_chunk_raw).
 //
-// Top-k: one warp per token; each lane scans its experts ascending with strict '>', then
-// redux.sync max (value) and min (index among the lanes holding the max) give the reference's
-// argmax semantics (model.cpp:339-341: ties -> lowest index, NaN skipped unless it sits at the
+// Top-k: 8 lanes per token, reading the cl partial tables (rank order) directly; each lane
+// scans its experts ascending with strict '>', then shuffle max (value) and min (index among
+// the lanes holding the max) give the reference's argmax semantics (model.cpp:339-341: ties -> lowest index, NaN skipped unless it sits at the
 // scan's first index). Gates in fp32 (expf is within 2 ulp; the logits already differ from the
 // reference's in the last bits).
 // Plan (warp 0, while the other warps scale the rows): lane l owns rows l and l + 32 (row =
@@ -769,12 +758,22 @@ template <int BITS>
 __device__ __forceinline__ void dec_fused_decide(const DecArgs& a, DecPlanSmem& P, unsigned char* hs, int hpitch,
                                                  const float* lg, int warp, int lane) {
     const int T = a.T, E = a.E, K = a.topk, R = T * K, Kp1 = a.Kp1;
-    const int lgp = DecRouteGeom(E, 1).lgp;
+    const int cl = int(cluster_nctas());
+    const DecRouteGeom G(E, cl);
+    const float unscale = __int_as_float((127 - a.wg_shift) << 23);  // exact power of two
     int rtr = 8;
     const int rk = blockIdx.x < 8 ? int(blockIdx.x) : 7;
     {
-        for (int tk = warp; tk < T; tk += kDecFfnWarps) {  // one warp per token (warp-uniform)
-            const float* lt = lg + tk * lgp;
+        // 8 lanes per token; lane sub scans experts [sub * EPL, (sub + 1) * EPL) ascending
+        const int sub = lane & 7, EPL = G.Ep16 / 8, e_lo = sub * EPL, e_hi = min(E, e_lo + EPL);
+        auto logit = [&](int tk, int e) {  // the cl partial tables in rank order, then the 2^-sw scale
+            float v = lg[size_t(tk) * G.tp + e];
+            for (int r = 1; r < cl; ++r) v += lg[size_t(r) * G.tab() + size_t(tk) * G.tp + e];
+            return v * unscale;
+        };
+        for (int tb = warp * 4; tb < T; tb += kDecFfnWarps * 4) {  // warp-uniform trip count
+            const bool live = tb + (lane >> 3) < T;
+            const int tk = live ? tb + (lane >> 3) : T - 1;  // idle groups redo the last token
             int best[2] = {0, 0};
             float mx0 = 0.f;
 #pragma unroll
@@ -784,14 +783,19 @@ __device__ __forceinline__ void dec_fused_decide(const DecArgs& a, DecPlanSmem& 
                 const int first = skip == 0 ? 1 : 0;
                 float bv = -__int_as_float(0x7f800000);
                 int bi = 1 << 30;
-                for (int e = lane; e < E; e += 32) {  // ascending, strict '>': lowest index per lane
-                    const float v = lt[e];
+                for (int e = e_lo; e < e_hi; ++e) {  // ascending, strict '>': lowest index per lane
+                    const float v = logit(tk, e);
                     if (e == skip || v != v) continue;
                     if (bi == (1 << 30) || v > bv) { bv = v; bi = e; }
                 }
-                const float m = redux_max_f32(bv);  // warp max over the non-NaN logits
-                const unsigned bmin = redux_min_u32(bi != (1 << 30) && bv == m ? unsigned(bi) : 0xffffffffu);
-                best[slot] = (lt[first] != lt[first]) ? first : (bmin == 0xffffffffu ? first : int(bmin));
+                float m = bv;
+#pragma unroll
+                for (int o = 4; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+                unsigned bmin = bi != (1 << 30) && bv == m ? unsigned(bi) : 0xffffffffu;
+#pragma unroll
+                for (int o = 4; o; o >>= 1) bmin = min(bmin, __shfl_xor_sync(0xffffffffu, bmin, o));
+                const float lf = logit(tk, first);
+                best[slot] = (lf != lf) ? first : (bmin == 0xffffffffu ? first : int(bmin));
                 if (slot == 0) mx0 = m;
             }
             float g1 = 1.f, g2 = 0.f;
@@ -801,19 +805,19 @@ __device__ __forceinline__ void dec_fused_decide(const DecArgs& a, DecPlanSmem& 
             if (K == 1) {
                 const float mx = mx0;  // = fmaxf over every logit (fmaxf drops NaNs)
                 float sm = 0.f;
-                for (int e = lane; e < E; e += 32) sm += expf(lt[e] - mx);
+                for (int e = e_lo; e < e_hi; ++e) sm += expf(logit(tk, e) - mx);
 #pragma unroll
-                for (int o = 16; o; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
-                g1 = expf(lt[best[0]] - mx) / sm;
+                for (int o = 4; o; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+                g1 = expf(logit(tk, best[0]) - mx) / sm;
             } else {
-                const float z = expf(lt[best[1]] - lt[best[0]]);
+                const float z = expf(logit(tk, best[1]) - logit(tk, best[0]));
                 g1 = 1.f / (1.f + z);
                 g2 = z / (1.f + z);
             }
 #ifdef DEC_PLAN_TRACE
             if (blockIdx.x < 8) route_trace(a, rk, rtr, 46);
 #endif
-            if (lane == 0) {
+            if (sub == 0 && live) {
                 P.ch_e[tk * K] = best[0];
                 P.ch_g[tk * K] = g1;
                 if (K == 2) {
@@ -1176,8 +1180,10 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
                 mbar_wait(full1 + s1, p1);
                 if (lane == 0 && rix == 0) dec_trace(a, 0, ntr, 1);
                 const unsigned char* piece = ring1 + size_t(s1) * sb1 + size_t(kh * KH) * 64 * RB;
+#ifndef DEC_SKIP_FC1  // timing experiments only (tools/ab_build.sh): results are wrong
                 if (NBr == 1) dec_fc1_piece<BITS, KH, 1>(piece, p * KP + kh * KH, gw, g, t, xrow, ca, cb);
                 else dec_fc1_piece<BITS, KH, 2>(piece, p * KP + kh * KH, gw, g, t, xrow, ca, cb);
+#endif
                 if (p < NP - 1 || kh == 1) {
                     __syncwarp();
                     if (lane == 0) mbar_arrive(empty1 + s1);
@@ -1292,8 +1298,10 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
             for (int r = 0; r < len; ++r, ++n) {
                 int myst;
                 wait_slice(myst);
+#ifndef DEC_SKIP_FC2
                 dec_fc2_piece<BITS, QW, 1>(ring2 + size_t(myst) * sb2, q0, g, t, midb + (n & 1) * kDecUnitRows * kMidPitch,
                                            c2);
+#endif
                 release_slice(myst);
             }
 #pragma unroll
@@ -1344,6 +1352,11 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
         w += len;
         j += len;
         if (j == S) { j = 0; ++u; }
+        if (a.trace && tid2 == 0) {  // slot 60: the run's reds are issued (diagnostics)
+            unsigned long long* p = a.trace + (size_t(blockIdx.x) * kDecTrace + 60) * 2;
+            p[0] = 7u;
+            p[1] = gtime_ns();
+        }
         {
             // the fc2 warps' reds are ordered before one acq_rel counter update (bar.sync + the
             // cumulative release of thread 0); the finisher's acquire covers its reads of acc
@@ -1401,10 +1414,20 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
                     }
                 }
                 named_bar_sync(2, NT2);
+                if (a.trace && tid2 == 0) {  // slot 61: the unit's final epilogue is done
+                    unsigned long long* p = a.trace + (size_t(blockIdx.x) * kDecTrace + 61) * 2;
+                    p[0] = 8u;
+                    p[1] = gtime_ns();
+                }
             }
         }
     }
     named_bar_sync(2, NT2);
+    if (a.trace && tid2 == 0) {  // slot 62: this CTA's exit
+        unsigned long long* p = a.trace + (size_t(blockIdx.x) * kDecTrace + 62) * 2;
+        p[0] = 6u;
+        p[1] = gtime_ns();
+    }
     if (tid2 == 0) span_end(a.span_ffn, gridDim.x);
 }
 

@@ -38,7 +38,7 @@ torch.cuda.synchronize()
 tr, _ = b.trace_read()
 ev = tr[:, :64, :]  # [cta][64][(event, ns)]
 t0 = ev[:, :, 1][ev[:, :, 1] > 0].min()
-names = {1: "F1:w1", 2: "F1:mid", 3: "F2:w2", 4: "F2:mid", 5: "F2:flush", 10: "P:w1", 11: "P:w2"}
+names = {7: "F2:reds", 8: "FIN", 6: "EXIT", 20: "START", 1: "F1:w1", 2: "F1:mid", 3: "F2:w2", 4: "F2:mid", 5: "F2:flush", 10: "P:w1", 11: "P:w2"}
 ends = []
 for c in range(ev.shape[0]):
     row = [(int(e), (int(t) - int(t0)) / 1e3) for e, t in ev[c] if t > 0]
@@ -49,6 +49,12 @@ for c in range(ev.shape[0]):
     if c < 6 or c % 37 == 0:
         print(c, " ".join(f"{names.get(e, e)}@{t:.2f}" for e, t in row))
 print("exit us: min %.2f median %.2f max %.2f" % (min(ends), float(np.median(ends)), max(ends)))
+q = np.quantile(ends, [0.1, 0.25, 0.5, 0.75, 0.9, 1.0])
+print("last event quantiles (10/25/50/75/90/100 %):", " ".join("%.2f" % x for x in q), " n", len(ends))
+slow = sorted(range(len(ends)), key=lambda i: -ends[i])[:4]
+for c in slow:
+    row = sorted([(int(e), (int(t) - int(t0)) / 1e3) for e, t in ev[c] if t > 0], key=lambda x: x[1])
+    print("late", c, " ".join(f"{names.get(e, e)}@{t:.2f}" for e, t in row))
 st = ev[:, 63, 1].astype(np.int64)
 st = (st[st > 0] - int(t0)) / 1e3
 print("start (after PDL wait) us: n %d min %.2f median %.2f max %.2f" % (len(st), st.min(), np.median(st), st.max()))
