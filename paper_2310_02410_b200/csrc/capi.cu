@@ -128,6 +128,18 @@ int route_cluster_env() {  // MOQE_DEC_CLUSTER=1|2|4: CTAs per routing cluster o
     }();
     return v;
 }
+bool dec_mid_enabled() {  // MOQE_DEC_MID=0: mid-size batches keep the round-1 GEMV for their small experts
+    static const bool v = [] { const char* s = getenv("MOQE_DEC_MID"); return !(s && atoi(s) == 0); }();
+    return v;
+}
+int dec_mid_rows() {  // MOQE_DEC_MID_ROWS: experts with at most this many rows run on k_dec (default 32)
+    static const int v = [] {
+        const char* s = getenv("MOQE_DEC_MID_ROWS");
+        const int r = s ? atoi(s) : 32;
+        return r < 1 ? 1 : r;
+    }();
+    return v;
+}
 bool xrows_in_router() {  // MOQE_XROWS_IN_ROUTER=0: decode keeps the separate k_xrows launch
     static const bool v = [] { const char* s = getenv("MOQE_XROWS_IN_ROUTER"); return !(s && atoi(s) == 0); }();
     return v;
@@ -231,8 +243,10 @@ moqe_status ensure_dec_workspace(moqe_bank* b) {
     const int64_t R = kDecMaxRows, xpitch = int64_t(b->Kp1) * 2 + 16;
     int64_t bytes = 0;
     auto add = [&](int64_t n) { int64_t o = bytes; bytes += round_up(std::max<int64_t>(n, 1), 256); return o; };
-    const int64_t o_units = add(16 * R), o_nu = add(16), o_pt = add(4 * R), o_pg = add(4 * R), o_ro = add(4 * R),
-                  o_x = add(xpitch * R), o_acc = add(8 * R * b->Np2), o_ud = add(4 * R), o_yb = add(4 * R * b->d),
+    // units, permuted rows, fc2 accumulators and unit counters also serve the mid-size path
+    const int64_t RM = kDecMidMaxRows, UM = kDecMidMaxUnits;
+    const int64_t o_units = add(16 * UM), o_nu = add(16), o_pt = add(4 * R), o_pg = add(4 * R), o_ro = add(4 * R),
+                  o_x = add(xpitch * RM), o_acc = add(8 * RM * b->Np2), o_ud = add(4 * UM), o_yb = add(4 * R * b->d),
                   o_tc = add(4 * R);
     MOQE_CUDA(cudaMalloc(&w.dblock, bytes));
     MOQE_CUDA(cudaMemset(w.dblock, 0, bytes));
@@ -589,24 +603,33 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
     const bool need_gemm = eff_path == MOQE_PATH_GEMM || (eff_path == MOQE_PATH_AUTO && R > kGemvMaxRows);
     const bool need_gemv = eff_path != MOQE_PATH_GEMM;
     const bool inline_scatter = !need_gemm && R <= 256;
+    // mid-size top-1 batches on a decode-capable bank: the small experts (<= dec_mid_rows() rows)
+    // run on k_dec from the router's plan instead of the round-1 GEMV. Not for pre-routed rows:
+    // the expert-parallel owner keeps the kernels of the top-k forward it stands in for (an fp32
+    // return then equals the single-GPU forward bit for bit, ep.py)
+    const bool dec_mid = !pre && need_gemv && top_k == 1 && !b->log && b->wdec && dec_enabled() && dec_mid_enabled() &&
+                         R <= kDecMidMaxRows && R <= 16 * int64_t(b->E) &&  // ~1-2 units per expert on average
+                         dec_mid_supported(int(b->d), b->E, b->Kp1, b->Np1, b->Np2);
+    const int gemv_max = dec_mid ? dec_mid_rows() : kGemvMaxRows;
     float* acc = nullptr;
     if (top_k == 2) acc = out_dtype == MOQE_F32 ? static_cast<float*>(out) : w.out_acc;
 
     RouteArgs ra{h, h_dtype == MOQE_F16, t, int(b->d), wg, b->E, top_k, eff_path, inline_scatter ? 1 : 0,
                  gemm_block_n(), inline_scatter ? acc : nullptr,
                  b->trace ? b->trace + int64_t(b->num_sms) * kTraceCap * 2 : nullptr};
+    ra.gemv_max = gemv_max;
     cudaError_t ce;
     bool self_plan = false;
     {
         KernelTimer kt(b, 0, st);
         // decode, every expert on the GEMV path: the router writes only the choices and the
         // GEMV kernels build the plan themselves (no serial plan step between them)
-        self_plan = !pre && !need_gemm && R <= kSelfPlanRows && t <= 32 && b->E <= 256;
+        self_plan = !dec_mid && !pre && !need_gemm && R <= kSelfPlanRows && t <= 32 && b->E <= 256;
         ra.no_plan = self_plan ? 1 : 0;
         if (wg == b->wg && b->wg_blk) { ra.wg_blk = b->wg_blk; ra.wg_finite = b->wg_finite; }
         if (wg == b->wg && b->wgt) { ra.wgt = b->wgt; ra.wg_shift = b->wg_shift; ra.Kp1 = int(b->Kp1); }
         ra.dbg = route_dbg();
-        if (need_gemv && !pre && route_chain_used(ra) && xrows_in_router()) {
+        if (need_gemv && !dec_mid && !pre && route_chain_used(ra) && xrows_in_router()) {
             // decode: the router leads the chain (waits for the previous grid itself) and its
             // copy warp writes the fc1 row blocks — two launches per forward
             ra.first = 1;
@@ -615,7 +638,7 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
             ra.nch1 = gemv_chunks(b->Kp1);
             ra.xr_bits = b->bits;
             ra.ready = self_plan && gemv_fused() ? w.ready : nullptr;
-        } else if (need_gemv) {  // token rows -> fc1 row blocks; the decode router overlaps it (PDL)
+        } else if (need_gemv && !dec_mid) {  // token rows -> fc1 row blocks; the decode router overlaps it (PDL)
             XrowArgs xa{h, h_dtype == MOQE_F16, t, int(b->d), gemv_chunks(b->Kp1), w.xr,
                         self_plan && gemv_fused() ? w.ready : nullptr};
             ce = launch_xrows(b->bits, xa, st);
@@ -628,11 +651,56 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
     if (!inline_scatter) {
         KernelTimer kt(b, 1, st);
         const int tt = pre ? kPlanIdsTile : route_tokens_per_cta(t);
-        ce = launch_scatter(h, h_dtype == MOQE_F16, t, int(b->d), top_k, b->E, eff_path, tt, P,
+        ce = launch_scatter(h, h_dtype == MOQE_F16, t, int(b->d), top_k, b->E, eff_path, gemv_max, tt, P,
                             need_gemm ? w.x_perm : nullptr, b->Kp1, acc, st);
         if (ce != cudaSuccess) return cuda_fail(ce, "k_scatter");
     }
-    if (need_gemv) {
+    if (dec_mid) {
+        moqe_status s2 = ensure_dec_workspace(b);
+        if (s2 != MOQE_OK) return s2;
+        KernelTimer kt(b, 2, st);
+        ce = launch_dec_prep(b->bits, h, h_dtype == MOQE_F16, t, int(b->d), b->E, b->Kp1, eff_path, gemv_max, P,
+                             w.d_units, w.d_nunits, w.d_xperm, b->Kp1 * 2 + 16, st);
+        if (ce != cudaSuccess) return cuda_fail(ce, "k_dec_prep");
+        DecArgs a{};
+        a.h = h;
+        a.h_f16 = h_dtype == MOQE_F16;
+        a.T = int(t);
+        a.d = int(b->d);
+        a.E = b->E;
+        a.topk = 1;
+        a.bits = b->bits;
+        a.units = w.d_units;
+        a.n_units = w.d_nunits;
+        a.perm_token = P.perm_token;
+        a.perm_gate = P.perm_gate;
+        a.row_of = P.inv_pos;
+        a.xperm = w.d_xperm;
+        a.xpitch = b->Kp1 * 2 + 16;
+        a.Kp1 = b->Kp1;
+        a.Np1 = b->Np1;
+        a.Np2 = b->Np2;
+        a.S = b->Np1 / 64;
+        a.wdec = b->wdec;
+        a.wdec_stride = b->wdec_stride;
+        a.slice_bytes = b->dec_slice;
+        a.s1 = b->s1;
+        a.b1 = b->b1;
+        a.s2 = b->s2;
+        a.b2 = b->b2;
+        a.acc = w.d_acc;
+        a.unit_done = w.d_unit_done;
+        a.ybuf = w.d_ybuf;
+        a.tok_cnt = w.d_tok_cnt;
+        a.out = out;
+        a.out_f16 = out_dtype == MOQE_F16;
+        a.trace = b->trace;
+        a.fused = 0;
+        a.plan_ready = 1;
+        a.route_cluster = 1;
+        ce = launch_dec(b->bits, a, st, b->num_sms);
+        if (ce != cudaSuccess) return cuda_fail(ce, "k_dec (mid)");
+    } else if (need_gemv) {
         GemvArgs g{h, h_dtype == MOQE_F16, t, int(b->d), int(b->f), top_k, b->E, b->w1, b->w2,
                    b->w1_stride, b->w2_stride, b->s1, b->s2, b->b1, b->b2, b->Kp1, b->Np1, b->Kp2, b->Np2,
                    out, out_dtype == MOQE_F16, acc, w.xr, gemv_chunks(b->Kp1), w.xb, b->smax1, b->bmax1, b->trace, gemv_dbg(), self_plan ? 1 : 0,

@@ -1431,6 +1431,85 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
     if (tid2 == 0) span_end(a.span_ffn, gridDim.x);
 }
 
+// Mid-size batches: the plan of the batched router + k_scatter (counts, offsets, perm_token)
+// becomes k_dec's work list. The last block's warp 0 turns every expert with 0 < rows <=
+// gemv_max (path 1: every expert) into units of <= kDecMidUnitRows permuted rows (expert order);
+// the other warps write those rows, scaled by 2^-s(k) with the per-row correction Z in the
+// 16 bytes after Kp1 (the layout k_dec's non-fused path reads; same arithmetic as
+// dec_fused_decide). Top-1 only (one row per token).
+template <int BITS>
+__global__ void __launch_bounds__(256) k_dec_prep(const void* h, int h_f16, int T, int d, int E, int Kp1, int path,
+                                                  int gemv_max, Plan P, int4* units, int* n_units, __half* xperm,
+                                                  int xpitch) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (blockIdx.x == gridDim.x - 1) {
+        if (warp != 0) return;
+        int base = 0;
+        for (int e0 = 0; e0 < E; e0 += 32) {
+            const int e = e0 + lane;
+            const int n = e < E ? P.counts[e] : 0;
+            const bool sel = n > 0 && (path == 1 || n <= gemv_max);
+            const int nu = sel ? (n + kDecMidUnitRows - 1) / kDecMidUnitRows : 0;
+            int incl = nu;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (sel) {
+                const int off = P.offsets[e];
+                for (int q = 0; q < nu; ++q)
+                    units[base + incl - nu + q] =
+                        make_int4(e, off + q * kDecMidUnitRows, min(kDecMidUnitRows, n - q * kDecMidUnitRows), 0);
+            }
+            base += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) *n_units = base;
+        return;
+    }
+    const int r = blockIdx.x * 8 + warp;  // permuted row
+    if (r >= T) return;
+    const int t = P.perm_token[r];
+    const int n = P.counts[P.expert[t]];
+    if (!(n > 0 && (path == 1 || n <= gemv_max))) return;
+    unsigned char* row = reinterpret_cast<unsigned char*>(xperm) + size_t(r) * xpitch;
+    constexpr int bias = 1 << (BITS - 1);
+    const bool vec = h_f16 && (d % 8) == 0 && ((reinterpret_cast<uintptr_t>(h) & 15) == 0);
+    float zf = 0.f;
+    for (int k0 = lane * 8; k0 < Kp1; k0 += 256) {
+        uint4 q;
+        if (vec && k0 < d) {
+            q = __ldg(reinterpret_cast<const uint4*>(static_cast<const __half*>(h) + size_t(t) * d + k0));
+        } else {
+            __half v8[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int k = k0 + i;
+                const float v = k < d ? (h_f16 ? __half2float(static_cast<const __half*>(h)[size_t(t) * d + k])
+                                                : static_cast<const float*>(h)[size_t(t) * d + k])
+                                      : 0.f;
+                v8[i] = __float2half_rn(v);
+            }
+            q = *reinterpret_cast<const uint4*>(v8);
+        }
+        __half2* hp = reinterpret_cast<__half2*>(&q);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int sh = field_shift_c<BITS>((k0 + 2 * e) & 15);
+            hp[e] = __hmul2(hp[e], __half2half2(__ushort_as_half(uint16_t((15 - sh) << 10))));
+            const float2 f = __half22float2(hp[e]);
+            const float m = 1024.f + float(bias << sh);  // exact; products of 11-bit factors
+            zf = fmaf(m, f.x, zf);
+            zf = fmaf(m, f.y, zf);
+        }
+        *reinterpret_cast<uint4*>(row + k0 * 2) = q;
+    }
+    double z = zf;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+    if (lane == 0) *reinterpret_cast<float*>(row + size_t(Kp1) * 2) = float(z);
+}
+
 // Bank layout for the decode kernel: per expert, per 64-channel f-slice j, contiguous
 // [W1 part: Kp1/64 k-tiles x 64 channel rows][W2 part: Np2/128 x 128 channel rows] of
 // tile rows (64 codes each, the codec of codec.cuh), copied from the tiled bank.
@@ -1482,6 +1561,24 @@ size_t route_smem(int T, int d, int E, int C) {
 }  // namespace
 
 int64_t dec_slice_bytes(int bits, int Kp1, int Np2) { return int64_t(Kp1 + Np2) * 8 * bits; }
+
+bool dec_mid_supported(int d, int E, int Kp1, int Np1, int Np2) {
+    return d <= Kp1 && Kp1 <= 1024 && Kp1 % 256 == 0 && Np2 <= 1024 && Np2 % 256 == 0 && Np1 % 64 == 0 && E <= 256;
+}
+
+cudaError_t launch_dec_prep(int bits, const void* h, int h_f16, int64_t T, int d, int E, int Kp1, int path,
+                            int gemv_max, const Plan& P, int4* units, int* n_units, __half* xperm, int xpitch,
+                            cudaStream_t st) {
+    const unsigned grid = unsigned((T + 7) / 8 + 1);
+    switch (bits) {
+        case 2: k_dec_prep<2><<<grid, 256, 0, st>>>(h, h_f16, int(T), d, E, Kp1, path, gemv_max, P, units, n_units, xperm, xpitch); break;
+        case 3: k_dec_prep<3><<<grid, 256, 0, st>>>(h, h_f16, int(T), d, E, Kp1, path, gemv_max, P, units, n_units, xperm, xpitch); break;
+        case 4: k_dec_prep<4><<<grid, 256, 0, st>>>(h, h_f16, int(T), d, E, Kp1, path, gemv_max, P, units, n_units, xperm, xpitch); break;
+        case 8: k_dec_prep<8><<<grid, 256, 0, st>>>(h, h_f16, int(T), d, E, Kp1, path, gemv_max, P, units, n_units, xperm, xpitch); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
 
 bool dec_supported(int64_t T, int topk, int d, int E, int Kp1, int Np1, int Np2) {
     if (T * topk > kDecMaxRows || T < 1) return false;
@@ -1642,7 +1739,7 @@ cudaError_t launch_dec(int bits, const DecArgs& a0, cudaStream_t st, int num_sms
         if (a.route_cluster != 4 || !dec_config(bits, a, &smem)) a.fused = 0;  // separate router launch
     }
     if (!a.fused && !dec_config(bits, a, &smem)) return cudaErrorInvalidConfiguration;
-    if (!a.fused) {  // ---- router (one cluster) ----
+    if (!a.fused && !a.plan_ready) {  // ---- router (one cluster) ----
         const int C = route_cluster(a.d, a.E);
         const size_t rs = route_smem(int(a.T), a.d, a.E, C);
         static bool configured[kMaxDev] = {};

@@ -58,6 +58,7 @@ struct RouteArgs {
     const __half* wgt;
     int wg_shift;
     int Kp1;
+    int gemv_max;               // experts with <= this many rows are planned for the GEMV-class path (0: kGemvMaxRows)
 };
 bool route_chain_used(const RouteArgs& a);  // launch_route will run k_route_chain
 constexpr int kTraceRouteCtas = 64;
@@ -69,7 +70,7 @@ int route_tokens_per_cta(int64_t T);
 // rows already routed: plan with kRouteSelWarps rows per CTA (scatter must use that tile)
 cudaError_t launch_plan_from_ids(const RouteArgs& a, const Plan& P, cudaStream_t st);
 constexpr int kPlanIdsTile = 32;
-cudaError_t launch_scatter(const void* h, int h_f16, int64_t T, int d, int topk, int E, int path, int tt,
+cudaError_t launch_scatter(const void* h, int h_f16, int64_t T, int d, int topk, int E, int path, int gemv_max, int tt,
                            const Plan& P, __half* x_perm, int ldx, float* zero_out, cudaStream_t st);
 
 moqe_status retile(const uint8_t* src, int64_t K, int64_t N, int bits, int n_mats, uint8_t* dst,
@@ -151,6 +152,12 @@ cudaError_t launch_gemm(int bits, int phase, const GemmArgs& g, const Plan& P, c
 // Decode path (dec.cu): k_dec_route (one cluster: parallel-order logits, top-k, plan,
 // permuted fp16 rows) -> PDL -> k_dec<BITS> (stream-K over (unit, 64-channel f-slice)).
 constexpr int kDecMaxRows = 64;   // T * top_k handled by the decode path
+// Mid-size batches (T * k <= kDecMidMaxRows, top-1): after the batched router + scatter, the
+// experts with few rows (<= the plan's GEMV-class limit) run on k_dec from a prepared plan
+// (k_dec_prep: units of <= kDecMidUnitRows rows, scaled rows + Z); the rest on tcgen05.
+constexpr int kDecMidMaxRows = 1024;
+constexpr int kDecMidUnitRows = 8;
+constexpr int kDecMidMaxUnits = kDecMidMaxRows / kDecMidUnitRows + 256;
 constexpr int kDecTrace = 64;
 constexpr int kDecUnitRows = 16;  // rows per unit (an expert with more rows has several units)
 struct DecSpan {                  // in-kernel launch span: first CTA start (after PDL wait) -> last CTA exit
@@ -194,6 +201,7 @@ struct DecArgs {
     int fused;             // routing inside k_dec (T <= 32, bank router, finite Wg)
     int route_nbuf;        // set by launch_dec: Wg chunk buffers of the fused routing
     int route_cluster;     // fused routing: CTAs per cluster sharing the K chunks (2 or 4), 1 = every CTA alone
+    int plan_ready;        // units / permuted rows prepared by k_dec_prep (no k_dec_route launch)
     uint32_t stage_bytes, stage2_bytes;  // set by launch_dec: W1 / W2 ring stage sizes
     int n_stages, n_stages2;
 };
@@ -202,6 +210,12 @@ int64_t dec_slice_bytes(int bits, int Kp1, int Np2);
 cudaError_t dec_build_layout(const uint8_t* w1, const uint8_t* w2, int64_t w1_stride, int64_t w2_stride, int E,
                              int Kp1, int Np1, int Np2, int bits, uint8_t* out, cudaStream_t st);
 cudaError_t launch_dec(int bits, const DecArgs& a, cudaStream_t st, int num_sms);
+bool dec_mid_supported(int d, int E, int Kp1, int Np1, int Np2);
+// k_dec_prep: units of the experts with 0 < rows <= gemv_max (path 1: every expert) from the
+// plan's counts / offsets, and their permuted rows scaled by 2^-s(k) with Z, into xperm.
+cudaError_t launch_dec_prep(int bits, const void* h, int h_f16, int64_t T, int d, int E, int Kp1, int path,
+                            int gemv_max, const Plan& P, int4* units, int* n_units, __half* xperm, int xpitch,
+                            cudaStream_t st);
 int64_t dec_wgt_halves(int E, int Kp1);
 cudaError_t dec_split_wg(const float* wg, int d, int E, int Kp1, int shift, __half* out, cudaStream_t st);
 

@@ -79,7 +79,8 @@ __device__ void plan_lists(const RouteArgs& a, Plan& P, const int* cnt, int* s_o
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
             mx = max(mx, m);
-            const bool gemv = n > 0 && (a.path == 1 || (a.path == 0 && n <= kGemvMaxRows));
+            const int gmax = a.gemv_max > 0 ? a.gemv_max : kGemvMaxRows;
+            const bool gemv = n > 0 && (a.path == 1 || (a.path == 0 && n <= gmax));
             const bool gemm = n > 0 && !gemv;
             const unsigned bg = __ballot_sync(0xffffffffu, gemv), bm = __ballot_sync(0xffffffffu, gemm);
             const unsigned lt = (1u << lane) - 1u;
@@ -1763,7 +1764,7 @@ cudaError_t launch_plan_from_ids(const RouteArgs& a, const Plan& P, cudaStream_t
 // fp16 activation matrix x_perm [T*k x ldx] (tcgen05 B operand; zero-padded
 // to ldx columns). One warp per (token, slot).
 __global__ void __launch_bounds__(256) k_scatter(const void* h, int h_f16, int64_t T, int d, int topk,
-                                                 int E, int tt, int path, Plan P, __half* x_perm,
+                                                 int E, int tt, int path, int gemv_max, Plan P, __half* x_perm,
                                                  int ldx, float* zero_out) {
     const int64_t i = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -1779,7 +1780,7 @@ __global__ void __launch_bounds__(256) k_scatter(const void* h, int h_f16, int64
     }
     if (zero_out && (i % topk) == 0)
         for (int j = lane; j < d; j += 32) zero_out[t * d + j] = 0.f;
-    const bool gemm = n_e > 0 && (path == 2 || (path == 0 && n_e > kGemvMaxRows));
+    const bool gemm = n_e > 0 && (path == 2 || (path == 0 && n_e > gemv_max));
     if (!gemm || x_perm == nullptr) return;
     __half* dst = x_perm + int64_t(pos) * ldx;
     if (h_f16 && (d % 8) == 0) {
@@ -1874,14 +1875,22 @@ bool route_mma_enabled() {
     return v;
 }
 
-// Route tile: tokens per routing CTA for a given T (must match scatter's tt).
-constexpr int64_t kRouteBigThreshold = 512;
-int route_tokens_per_cta(int64_t T) { return T <= kRouteBigThreshold ? kRouteSmallWarps : kRouteSelWarps; }
+// Route tile: tokens per routing CTA for a given T (must match scatter's tt). Above the
+// threshold the batched routers run (tensor-core logits for E = 32 / 64 with the bank's split
+// gate weights); at or below it the per-token exact-order kernels. MOQE_ROUTE_BIG_T overrides.
+int64_t route_big_threshold() {
+    static const int64_t v = [] {
+        const char* s = getenv("MOQE_ROUTE_BIG_T");
+        return s ? std::max<int64_t>(32, atoll(s)) : int64_t(64);
+    }();
+    return v;
+}
+int route_tokens_per_cta(int64_t T) { return T <= route_big_threshold() ? kRouteSmallWarps : kRouteSelWarps; }
 
 cudaError_t launch_route(const RouteArgs& a, const Plan& P, cudaStream_t st) {
     const int tt = route_tokens_per_cta(a.T);
     const unsigned grid = unsigned((a.T + tt - 1) / tt);
-    if (a.T > kRouteBigThreshold) {
+    if (a.T > route_big_threshold()) {
         if (P.logits == nullptr) return cudaErrorInvalidValue;
         dim3 lg(unsigned((a.T + kRLTok - 1) / kRLTok), unsigned((a.E + kRLExp - 1) / kRLExp));
         const bool vec = a.h_f16 && (a.d % 8) == 0 && (a.E % 32) == 0 && (reinterpret_cast<uintptr_t>(a.h) & 15) == 0;
@@ -1961,11 +1970,12 @@ cudaError_t launch_route(const RouteArgs& a, const Plan& P, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_scatter(const void* h, int h_f16, int64_t T, int d, int topk, int E, int path, int tt,
+cudaError_t launch_scatter(const void* h, int h_f16, int64_t T, int d, int topk, int E, int path, int gemv_max, int tt,
                            const Plan& P, __half* x_perm, int ldx, float* zero_out, cudaStream_t st) {
     const int64_t n = T * topk;
     if (n == 0) return cudaSuccess;
-    k_scatter<<<unsigned((n + 7) / 8), 256, 0, st>>>(h, h_f16, T, d, topk, E, tt, path, P, x_perm, ldx, zero_out);
+    k_scatter<<<unsigned((n + 7) / 8), 256, 0, st>>>(h, h_f16, T, d, topk, E, tt, path,
+                                                     gemv_max > 0 ? gemv_max : kGemvMaxRows, P, x_perm, ldx, zero_out);
     return cudaGetLastError();
 }
 
