@@ -496,6 +496,10 @@ namespace {
 // The decode kernel (k_dec) takes the forward: its output is written with plain stores only
 // (no atomics), so it may target mapped pinned host memory directly.
 bool dec_path_taken(moqe_bank_t b, int64_t t, int top_k, moqe_path path) {
+    // 32 < T <= 64 top-1: the batched router + the mid-size k_dec path, unless MOQE_DEC_ROUTER=1
+    // keeps the one-cluster decode router (k_dec_route)
+    static const bool dec_router = [] { const char* s = getenv("MOQE_DEC_ROUTER"); return s && atoi(s) == 1; }();
+    if (t > 32 && top_k == 1 && !dec_router && dec_mid_enabled() && t <= 16 * int64_t(b->E)) return false;
     return !b->log && b->wdec && dec_enabled() && (path == MOQE_PATH_AUTO || path == MOQE_PATH_GEMV) &&
            dec_supported(t, top_k, int(b->d), b->E, b->Kp1, b->Np1, b->Np2);
 }

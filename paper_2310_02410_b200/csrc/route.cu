@@ -1881,7 +1881,7 @@ bool route_mma_enabled() {
 int64_t route_big_threshold() {
     static const int64_t v = [] {
         const char* s = getenv("MOQE_ROUTE_BIG_T");
-        return s ? std::max<int64_t>(32, atoll(s)) : int64_t(64);
+        return s ? std::max<int64_t>(32, atoll(s)) : int64_t(32);
     }();
     return v;
 }

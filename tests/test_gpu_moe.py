@@ -59,6 +59,9 @@ CASES = [
     (32, 512, 1024, 4, 33, 1, False),    # T = 33: routed plan + packed GEMV table path
     (8, 2048, 1024, 3, 8, 1, True),      # d = 2048: fc1 split-K over a 2-CTA cluster
     (4, 256, 8192, 2, 6, 2, False),      # f = 8192: fc2 split-K over an 8-CTA cluster
+    # mid-size top-1 batches: batched router + k_dec on the experts with <= 32 rows (k_dec_prep units)
+    (24, 256, 512, 3, 150, 1, True),
+    (40, 72, 200, 4, 320, 1, False),     # ragged dims on the mid path
 ]
 
 
