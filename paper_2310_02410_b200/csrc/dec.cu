@@ -513,7 +513,18 @@ __device__ __forceinline__ void make_magics(uint32_t (&mg)[8]) {
 // ---- warp roles of k_dec -------------------------------------------------------------
 constexpr int kF1Warps = 8;   // fc1: (16-channel group of the slice's 64, half of Kp1) each
 constexpr int kF2Warps = 8;   // fc2: Np2 / 8 channels each, the slice's 64 k
-constexpr int kDecFfnWarps = kF1Warps + kF2Warps + 1;  // + the TMA producer
+// + one warpgroup for the TMA producer (warp 16; warps 17-19 only help the routing phase).
+// 17 warps would cap every thread at 96 registers (5 warps on one SM sub-partition); with 20,
+// the producer warpgroup drops to kDecProdRegs after the routing phase and the fc1 / fc2
+// warpgroups grow to kDecMathRegs (setmaxnreg). The increases draw only on what the CTA got at
+// launch (640 x 96): 512 x 112 + 128 x 24 fits, 512 x 120 + 128 x 32 never completes.
+// Measured: parity-green, no faster (int3 32.6 vs 32.4 us, int2 30.5 vs 29.8), so off by
+// default; the slice loops are not register-bound.
+#ifndef DEC_SETMAXNREG
+#define DEC_SETMAXNREG 0
+#endif
+constexpr int kDecFfnWarps = DEC_SETMAXNREG ? kF1Warps + kF2Warps + 4 : kF1Warps + kF2Warps + 1;
+constexpr int kDecProdRegs = 24, kDecMathRegs = 112;
 
 // fc1 of one slice for one warp: channels gw*16 .. +15, KP k-tiles from global k-tile kt0.
 // xrow[nb] = this lane's activation row (row g of n-block nb) scaled by 2^-s(k).
@@ -1067,6 +1078,14 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
     const int W = U * S;
     const int w0 = int((long long)W * blockIdx.x / gridDim.x), w1 = int((long long)W * (blockIdx.x + 1) / gridDim.x);
     const int u0 = w0 / S, j0 = w0 - u0 * S;
+#if DEC_SETMAXNREG
+    if (warp >= kF1Warps + kF2Warps) {  // warpgroup 4: hand registers to the math warpgroups
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kDecProdRegs));
+        if (warp != kF1Warps + kF2Warps) return;
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kDecMathRegs));
+    }
+#endif
 
     if (warp == kF1Warps + kF2Warps) {
         // ------------------------------ producer ------------------------------
