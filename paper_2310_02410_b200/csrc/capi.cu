@@ -140,6 +140,14 @@ int dec_mid_rows() {  // MOQE_DEC_MID_ROWS: experts with at most this many rows 
     }();
     return v;
 }
+int64_t dec_mid_avg() {  // MOQE_DEC_MID_AVG: mid-size path while T*k <= this many rows per expert on average (16)
+    static const int64_t v = [] {
+        const char* s = getenv("MOQE_DEC_MID_AVG");
+        const int r = s ? atoi(s) : 16;
+        return int64_t(r < 1 ? 1 : r);
+    }();
+    return v;
+}
 bool xrows_in_router() {  // MOQE_XROWS_IN_ROUTER=0: decode keeps the separate k_xrows launch
     static const bool v = [] { const char* s = getenv("MOQE_XROWS_IN_ROUTER"); return !(s && atoi(s) == 0); }();
     return v;
@@ -612,7 +620,7 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
     // the expert-parallel owner keeps the kernels of the top-k forward it stands in for (an fp32
     // return then equals the single-GPU forward bit for bit, ep.py)
     const bool dec_mid = !pre && need_gemv && top_k == 1 && !b->log && b->wdec && dec_enabled() && dec_mid_enabled() &&
-                         R <= kDecMidMaxRows && R <= 16 * int64_t(b->E) &&  // ~1-2 units per expert on average
+                         R <= kDecMidMaxRows && R <= dec_mid_avg() * int64_t(b->E) &&  // ~1-2 units per expert on average
                          dec_mid_supported(int(b->d), b->E, b->Kp1, b->Np1, b->Np2);
     const int gemv_max = dec_mid ? dec_mid_rows() : kGemvMaxRows;
     float* acc = nullptr;

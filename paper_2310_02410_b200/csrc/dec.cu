@@ -524,7 +524,9 @@ constexpr int kF2Warps = 8;   // fc2: Np2 / 8 channels each, the slice's 64 k
 #define DEC_SETMAXNREG 0
 #endif
 constexpr int kDecFfnWarps = DEC_SETMAXNREG ? kF1Warps + kF2Warps + 4 : kF1Warps + kF2Warps + 1;
+#if DEC_SETMAXNREG
 constexpr int kDecProdRegs = 24, kDecMathRegs = 112;
+#endif
 
 // fc1 of one slice for one warp: channels gw*16 .. +15, KP k-tiles from global k-tile kt0.
 // xrow[nb] = this lane's activation row (row g of n-block nb) scaled by 2^-s(k).
@@ -617,19 +619,21 @@ struct DecPlanSmem {
 // with st.async (mbarrier complete_tx: no cluster barrier, no fence), transposed to
 // [token][expert]. The top-k adds the cl tables in rank order, so every CTA of every cluster
 // holds the same logits. Without a cluster the four chunks stream through nbuf buffers.
-// Layout behind the chunk buffers: the per-rank tables [cl][32 tokens][Ep16 + 4], the K-part
-// scratch [16 warps][4 token tiles][32 lanes][4].
+// Layout behind the chunk buffers: the per-rank tables [cl][8 ceil(T / 8) tokens][Ep16 + 4], the K-part
+// scratch [16 warps][ceil(T / 8) token tiles][32 lanes][4].
 struct DecRouteGeom {
-    int Ep, Ep16, tp, cl;
-    __host__ __device__ DecRouteGeom(int E, int cl_) {
+    int Ep, Ep16, tp, cl, tt;
+    __host__ __device__ DecRouteGeom(int E, int cl_, int T) {
         Ep = (E + 7) & ~7;
         Ep16 = (E + 15) & ~15;
         tp = Ep16 + 4;  // 16 B row skew
         cl = cl_;
+        tt = (T + 7) >> 3;  // token tiles
     }
-    __host__ __device__ size_t tab() const { return size_t(32) * tp; }
+    __host__ __device__ size_t tab() const { return size_t(tt) * 8 * tp; }
     __host__ __device__ size_t pair_off() const { return size_t(cl) * tab(); }
-    __host__ __device__ size_t floats() const { return pair_off() + 16 * 4 * 32 * 4; }
+    __host__ __device__ size_t lg_off() const { return pair_off() + size_t(16) * tt * 32 * 4; }
+    __host__ __device__ size_t floats() const { return lg_off() + size_t(tt) * 8 * tp; }
 };
 
 __device__ __forceinline__ void st_async_f32(uint32_t addr, float x, uint32_t bar) {
@@ -643,7 +647,7 @@ __device__ __forceinline__ void dec_fused_route(const DecArgs& a, unsigned char*
                                                 int nbuf, float* lg, uint64_t* rbar, int warp, int lane) {
     const int T = a.T, E = a.E, Kp1 = a.Kp1;
     const int cl = int(cluster_nctas()), crank = int(cta_rank());
-    const DecRouteGeom G(E, cl);
+    const DecRouteGeom G(E, cl, T);
     const int Ep = G.Ep, Ep16 = G.Ep16;
     const int Kc = Kp1 / 4, cpitch = (Kc + 8) * 2, nsteps = Kc / 16;
     const uint32_t cbytes = uint32_t(2 * Ep) * cpitch;
@@ -673,6 +677,9 @@ __device__ __forceinline__ void dec_fused_route(const DecArgs& a, unsigned char*
         const int bi = cl > 1 ? c - c_begin : c % nbuf;
         const unsigned char* buf = rbase + size_t(bi) * cbytes;
         mbar_wait(rbar + bi, cl > 1 ? 0 : (c / nbuf) & 1);
+#ifdef DEC_PLAN_TRACE
+        if (blockIdx.x < 8 && c == c_begin) route_trace(a, rk, rtr, 41);
+#endif
         if (mma_warp) {
             const unsigned char* ar = buf + size_t(mt * 16 + g) * cpitch + 4 * t;
             const int gs0 = (c - c_begin) * nsteps;  // K steps are dealt round-robin over the kp warps
@@ -714,23 +721,23 @@ __device__ __forceinline__ void dec_fused_route(const DecArgs& a, unsigned char*
 #endif
     // the K parts of each expert tile meet in shared memory (kp order), then each table goes to
     // every CTA of the cluster
-    float* pair = lg + G.pair_off();  // [NW][4 token tiles][32 lanes][4]
+    float* pair = lg + G.pair_off();  // [NW][token tiles][32 lanes][4]
     if (mma_warp) {
 #pragma unroll
         for (int x = 0; x < 4; ++x)
             if (x < ttiles)
-                reinterpret_cast<float4*>(pair)[(warp * 4 + x) * 32 + lane] =
+                reinterpret_cast<float4*>(pair)[(warp * ttiles + x) * 32 + lane] =
                     make_float4(acc[x][0][0] + acc[x][1][0], acc[x][0][1] + acc[x][1][1], acc[x][0][2] + acc[x][1][2],
                                 acc[x][0][3] + acc[x][1][3]);
     }
     if (cl > 1) cluster_wait_acquire();  // the peers' barriers are initialised (arrived at kernel start)
     __syncthreads();
-    float* recv = lg;  // [cl][32 tokens][tp]
+    float* recv = lg;  // [cl][8 ceil(T / 8) tokens][tp]
     for (int it = warp; it < items; it += kDecFfnWarps) {
         const int imt = it % mtiles, x = it / mtiles;
-        float4 v = reinterpret_cast<const float4*>(pair)[(imt * 4 + x) * 32 + lane];
+        float4 v = reinterpret_cast<const float4*>(pair)[(imt * ttiles + x) * 32 + lane];
         for (int q = 1; q < KP; ++q) {
-            const float4 o = reinterpret_cast<const float4*>(pair)[((q * mtiles + imt) * 4 + x) * 32 + lane];
+            const float4 o = reinterpret_cast<const float4*>(pair)[((q * mtiles + imt) * ttiles + x) * 32 + lane];
             v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
         }
         // c0, c1: expert imt*16+g, tokens x*8+2t, +1; c2, c3: expert + 8
@@ -748,6 +755,18 @@ __device__ __forceinline__ void dec_fused_route(const DecArgs& a, unsigned char*
     if (blockIdx.x < 8) route_trace(a, rk, rtr, 42);
 #endif
     mbar_wait(rbar + 5, 0);
+    // the logits, once: the cl tables in rank order, then the exact 2^-sw scale
+    {
+        const float unscale = __int_as_float((127 - a.wg_shift) << 23);
+        float* lgt = lg + G.lg_off();  // [8 ceil(T / 8) tokens][tp]
+        for (int i = threadIdx.x; i < T * E; i += blockDim.x) {
+            const int tk = i / E, e = i - tk * E;
+            float v = recv[size_t(tk) * G.tp + e];
+            for (int r = 1; r < cl; ++r) v += recv[size_t(r) * G.tab() + size_t(tk) * G.tp + e];
+            lgt[size_t(tk) * G.tp + e] = v * unscale;
+        }
+    }
+    __syncthreads();
     if (blockIdx.x < 8) route_trace(a, rk, rtr, 32);
 }
 
@@ -755,7 +774,7 @@ __device__ __forceinline__ void dec_fused_route(const DecArgs& a, unsigned char*
 // and the activation rows scaled in place by 2^-s(k) (the fc1 weight field shifts) with the
 // per-token correction Z (see unpack_chunk_raw).
 //
-// Top-k: 8 lanes per token, reading the cl partial tables (rank order) directly; each lane
+// Top-k: 8 lanes per token on the assembled logits (one load per logit); each lane
 // scans its experts ascending with strict '>', then shuffle max (value) and min (index among
 // the lanes holding the max) give the reference's argmax semantics (model.cpp:339-341: ties -> lowest index, NaN skipped unless it sits at the
 // scan's first index). Gates in fp32 (expf is within 2 ulp; the logits already differ from the
@@ -770,18 +789,14 @@ __device__ __forceinline__ void dec_fused_decide(const DecArgs& a, DecPlanSmem& 
                                                  const float* lg, int warp, int lane) {
     const int T = a.T, E = a.E, K = a.topk, R = T * K, Kp1 = a.Kp1;
     const int cl = int(cluster_nctas());
-    const DecRouteGeom G(E, cl);
-    const float unscale = __int_as_float((127 - a.wg_shift) << 23);  // exact power of two
+    const DecRouteGeom G(E, cl, T);
     int rtr = 8;
     const int rk = blockIdx.x < 8 ? int(blockIdx.x) : 7;
     {
         // 8 lanes per token; lane sub scans experts [sub * EPL, (sub + 1) * EPL) ascending
         const int sub = lane & 7, EPL = G.Ep16 / 8, e_lo = sub * EPL, e_hi = min(E, e_lo + EPL);
-        auto logit = [&](int tk, int e) {  // the cl partial tables in rank order, then the 2^-sw scale
-            float v = lg[size_t(tk) * G.tp + e];
-            for (int r = 1; r < cl; ++r) v += lg[size_t(r) * G.tab() + size_t(tk) * G.tp + e];
-            return v * unscale;
-        };
+        const float* lgt = lg + G.lg_off();
+        auto logit = [&](int tk, int e) { return lgt[size_t(tk) * G.tp + e]; };
         for (int tb = warp * 4; tb < T; tb += kDecFfnWarps * 4) {  // warp-uniform trip count
             const bool live = tb + (lane >> 3) < T;
             const int tk = live ? tb + (lane >> 3) : T - 1;  // idle groups redo the last token
@@ -1736,7 +1751,7 @@ static bool dec_config(int bits, DecArgs& a, size_t* smem_out) {
     const int pairs = int(std::min<size_t>(8, budget / (a.stage_bytes + a.stage2_bytes + 32)));
     if (pairs < 2) return false;
     if (a.fused) {  // the routing phase borrows the rings: 2..4 Wg chunks + the partial logits
-        const DecRouteGeom G(a.E, a.route_cluster);
+        const DecRouteGeom G(a.E, a.route_cluster, a.T);
         const size_t cb = size_t(2 * G.Ep) * ((a.Kp1 / 4 + 8) * 2), pb = G.floats() * 4;
         const size_t ring = size_t(pairs) * (a.stage_bytes + a.stage2_bytes);
         a.route_nbuf = ring < pb ? 0 : int(std::min<size_t>(4, (ring - pb) / cb));

@@ -18,3 +18,7 @@ for r in k_dec k_dec_mid512; do
   ncu -i $O/$r.ncu-rep --page raw --csv --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,sm__throughput.avg.pct_of_peak_sustained_elapsed,sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active > $O/${r}_raw.csv 2>/dev/null
 done
 ls -la $O
+ncu -i $O/k_dec.ncu-rep --page source --csv --print-source sass > $O/k_dec_sass.csv 2>/dev/null
+python tools/ncu_sass_regions.py $O/k_dec_sass.csv 64 > $O/k_dec_regions.txt 2>&1
+rm -f $O/*.ncu-rep $O/k_dec_sass.csv
+for a in 16 24; do echo -n "mid_avg=$a T=768 "; MOQE_DEC_MID_AVG=$a timeout 300 python bench.py --tokens 768 --bits 3 --no-sweep --no-cpu --steps 100 --warmup 5 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'])"; done
