@@ -786,7 +786,7 @@ __device__ __forceinline__ void dec_fused_route(const DecArgs& a, unsigned char*
 // unit bases (units of <= 16 rows).
 template <int BITS>
 __device__ __forceinline__ void dec_fused_decide(const DecArgs& a, DecPlanSmem& P, unsigned char* hs, int hpitch,
-                                                 const float* lg, int warp, int lane) {
+                                                 const float* lg, uint64_t* rbar6, int warp, int lane) {
     const int T = a.T, E = a.E, K = a.topk, R = T * K, Kp1 = a.Kp1;
     const int cl = int(cluster_nctas());
     const DecRouteGeom G(E, cl, T);
@@ -935,7 +935,9 @@ __device__ __forceinline__ void dec_fused_decide(const DecArgs& a, DecPlanSmem& 
         if (blockIdx.x < 8) route_trace(a, rk, rtr, 34);
     } else {
         // activation rows scaled in place by 2^-s(k) (HMUL2 by a power of two: the same
-        // rounding as scaling in fp32 and converting) + Z per token (warps 1..)
+        // rounding as scaling in fp32 and converting) + Z per token (warps 1..), once the rest of
+        // each row (outside this CTA's routing K range) has landed
+        if (a.h_f16 && (a.d % 8 == 0) && ((reinterpret_cast<uintptr_t>(a.h) & 15) == 0)) mbar_wait(rbar6, 0);
         constexpr int bias = 1 << (BITS - 1);
         for (int tk = warp - 1; tk < T; tk += kDecFfnWarps - 1) {
             unsigned char* row = hs + size_t(tk) * hpitch;
@@ -1061,10 +1063,29 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
         const int T = a.T;
         const bool bulk = a.h_f16 && (d % 8 == 0) && ((reinterpret_cast<uintptr_t>(a.h) & 15) == 0);
         if (bulk && warp == 0) {  // one row per lane
-            if (lane == 0) mbar_arrive_expect_tx(rbar + 4, uint32_t(T) * d * 2);
+            // this CTA's K range of the routing logits first (rbar 4, waited for below), the rest of
+            // each row behind it (rbar 6, waited for by the row scaling in dec_fused_decide)
+            const int cl = int(cluster_nctas());
+            int k_lo = 0, k_hi = d;
+            if (cl > 1) {
+                const int span = (4 / cl) * (a.Kp1 / 4);
+                k_lo = min(d, int(cta_rank()) * span);
+                k_hi = min(d, k_lo + span);
+            }
+            if (lane == 0) {
+                mbar_arrive_expect_tx(rbar + 4, uint32_t(T) * (k_hi - k_lo) * 2);
+                mbar_arrive_expect_tx(rbar + 6, uint32_t(T) * (d - (k_hi - k_lo)) * 2);
+            }
             __syncwarp();
+            const __half* hh = static_cast<const __half*>(a.h);
             for (int r = lane; r < T; r += 32)
-                bulk_g2s(xsb + size_t(r) * a.xpitch, static_cast<const __half*>(a.h) + size_t(r) * d, d * 2, rbar + 4);
+                if (k_hi > k_lo)
+                    bulk_g2s(xsb + size_t(r) * a.xpitch + k_lo * 2, hh + size_t(r) * d + k_lo, (k_hi - k_lo) * 2, rbar + 4);
+            for (int r = lane; r < T; r += 32) {
+                if (k_lo > 0) bulk_g2s(xsb + size_t(r) * a.xpitch, hh + size_t(r) * d, k_lo * 2, rbar + 6);
+                if (k_hi < d)
+                    bulk_g2s(xsb + size_t(r) * a.xpitch + k_hi * 2, hh + size_t(r) * d + k_hi, (d - k_hi) * 2, rbar + 6);
+            }
         }
         if (!bulk) {
             for (int i = tid; i < T * d; i += blockDim.x) {
@@ -1083,7 +1104,7 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
         float* lg = reinterpret_cast<float*>(ring1 + size_t(nbuf_) * cbytes_);
         // one instantiation (two token m-tiles) keeps the kernel's instruction footprint small
         dec_fused_route<BITS>(a, xsb, a.xpitch, ring1, nbuf_, lg, rbar, warp, lane);
-        dec_fused_decide<BITS>(a, *PS, xsb, a.xpitch, lg, warp, lane);
+        dec_fused_decide<BITS>(a, *PS, xsb, a.xpitch, lg, rbar + 6, warp, lane);
     }
     const int4* units = FU ? PS->units : a.units;
     const int* perm_token = FU ? PS->perm_token : a.perm_token;
