@@ -641,7 +641,10 @@ moqe_status forward_impl(moqe_bank_t b, const void* h, moqe_dtype h_dtype, int64
         if (wg == b->wg && b->wg_blk) { ra.wg_blk = b->wg_blk; ra.wg_finite = b->wg_finite; }
         if (wg == b->wg && b->wgt) { ra.wgt = b->wgt; ra.wg_shift = b->wg_shift; ra.Kp1 = int(b->Kp1); }
         ra.dbg = route_dbg();
-        if (need_gemv && !dec_mid && !pre && route_chain_used(ra) && xrows_in_router()) {
+        // the router's copy warp writes the fc1 row blocks only with the one-chunk Wg layout: with
+        // two chunks it would run after the chain's last chunk, k_xrows overlaps better
+        if (need_gemv && !dec_mid && !pre && route_chain_used(ra) && xrows_in_router() &&
+            route_chain_one_chunk(int(b->d), b->E)) {
             // decode: the router leads the chain (waits for the previous grid itself) and its
             // copy warp writes the fc1 row blocks — two launches per forward
             ra.first = 1;

@@ -66,6 +66,7 @@ constexpr int kTraceRouteCtas = 64;
 int64_t route_wg_block_floats(int d, int E);
 cudaError_t route_block_wg(const float* wg, int d, int E, float* out, int* d_flag, int* finite);
 cudaError_t launch_route(const RouteArgs& a, const Plan& P, cudaStream_t st);
+bool route_chain_one_chunk(int d, int E);  // the decode chain router holds all of Wg in one chunk
 int route_tokens_per_cta(int64_t T);
 // rows already routed: plan with kRouteSelWarps rows per CTA (scatter must use that tile)
 cudaError_t launch_plan_from_ids(const RouteArgs& a, const Plan& P, cudaStream_t st);

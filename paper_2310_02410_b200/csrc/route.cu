@@ -784,12 +784,13 @@ size_t route_chain_smem(int d, int E) {
 
 // fc1 row blocks of a router CTA's tokens from their rows in smem (the decode router's
 // copy warp; out of line so the chain warp's code and registers are unaffected).
-__device__ __noinline__ void route_xrows(const RouteArgs& a, const float* hrow, int hs, int ntok, int64_t t0,
-                                         int lane) {
-    const int d = a.d;
+// The fields it needs come by value: taking the kernel parameter's address would force a
+// local-memory copy of RouteArgs into every thread.
+__device__ __noinline__ void route_xrows(int d, int h_f16, int nch1, int xr_bits, uint8_t* xr, const float* hrow, int hs,
+                                         int ntok, int64_t t0, int lane) {
     for (int r = 0; r < ntok; ++r) {
         const float* hr = hrow + r * hs;
-        auto q16 = [&](float x) { return a.h_f16 ? x : __half2float(__float2half_rn(x)); };
+        auto q16 = [&](float x) { return h_f16 ? x : __half2float(__float2half_rn(x)); };
         float m = 0.f, l1 = 0.f;
         for (int kk = lane; kk < d; kk += 32) {
             const float x = fabsf(q16(hr[kk]));
@@ -802,7 +803,7 @@ __device__ __noinline__ void route_xrows(const RouteArgs& a, const float* hrow, 
             l1 += __shfl_xor_sync(0xffffffffu, l1, off);
         }
         const int st = lane >> 2, tq = lane & 3;
-        for (int c = 0; c < a.nch1; ++c) {
+        for (int c = 0; c < nch1; ++c) {
             float v[32];
             const int k0 = c * kChunkK + st * kStageK + 16 * tq;
 #pragma unroll
@@ -810,17 +811,19 @@ __device__ __noinline__ void route_xrows(const RouteArgs& a, const float* hrow, 
                 v[i] = k0 + i < d ? q16(hr[k0 + i]) : 0.f;
                 v[16 + i] = k0 + 64 + i < d ? q16(hr[k0 + 64 + i]) : 0.f;
             }
-            const int64_t row = (t0 + r) * a.nch1 + c;
-            switch (a.xr_bits) {
-                case 2: xrow_encode<2>(v, m, l1, a.xr + row * RB<2>::XR1, lane); break;
-                case 3: xrow_encode<3>(v, m, l1, a.xr + row * RB<3>::XR1, lane); break;
-                case 4: xrow_encode<4>(v, m, l1, a.xr + row * RB<4>::XR1, lane); break;
-                default: xrow_encode<8>(v, m, l1, a.xr + row * RB<8>::XR1, lane); break;
+            const int64_t row = (t0 + r) * nch1 + c;
+            switch (xr_bits) {
+                case 2: xrow_encode<2>(v, m, l1, xr + row * RB<2>::XR1, lane); break;
+                case 3: xrow_encode<3>(v, m, l1, xr + row * RB<3>::XR1, lane); break;
+                case 4: xrow_encode<4>(v, m, l1, xr + row * RB<4>::XR1, lane); break;
+                default: xrow_encode<8>(v, m, l1, xr + row * RB<8>::XR1, lane); break;
             }
         }
     }
 }
 
+// thread 0..kSelfPlanRows-1 zero the GEMV readiness counters below
+static_assert((kRCTok + 1) * 32 >= kSelfPlanRows, "k_route_chain blocks must cover the readiness counters");
 template <int EPL, int EFIX, bool SEL>
 __global__ void __launch_bounds__((kRCTok + 1) * 32, 1) k_route_chain(RouteArgs a, Plan P) {
     extern __shared__ __align__(128) float s_dyn[];
@@ -901,7 +904,7 @@ __global__ void __launch_bounds__((kRCTok + 1) * 32, 1) k_route_chain(RouteArgs 
         __syncwarp();
         // this warp is otherwise idle during the chain: the tokens' fc1 row blocks from the
         // rows in smem (fp16-valued, as k_xrows reads them; same exponent, digits and planes)
-        if (a.xr) route_xrows(a, hrow, hs, ntok, t0, lane);
+        if (a.xr) route_xrows(a.d, a.h_f16, a.nch1, a.xr_bits, a.xr, hrow, hs, ntok, t0, lane);
     } else {
         // ===== chain warp: token t0 + warp
         const int64_t t = t0 + warp;
@@ -1849,12 +1852,16 @@ cudaError_t launch_dec(const RouteArgs& a, const Plan& P, size_t smem, cudaStrea
         const size_t cs = route_chain_smem(a.d, EFIX ? EFIX : a.E);
         if (a.wg_blk && cs <= 220 * 1024 && a.dbg != 7)  // dbg 7: the strided-Wg chain (comparison)
             return a.wg_finite ? launch_chain<EPL, EFIX, false>(a, P, cs, st) : launch_chain<EPL, EFIX, true>(a, P, cs, st);
+        // only the chain kernel writes the fc1 row blocks: a caller that skipped k_xrows because
+        // route_chain_used() said so must not silently get k_route_decode
+        if (a.xr) return cudaErrorInvalidValue;
         return launch_dec_tt<EPL, EFIX, 1>(a, P, smem, st);
     }
     return launch_dec_tt<EPL, EFIX, kRouteSmallWarps>(a, P, smem, st);
 }
 }  // namespace
 
+bool route_chain_one_chunk(int d, int E) { return rc_slots(d, E) == 1; }
 bool route_chain_used(const RouteArgs& a) {
     return a.no_plan && a.wg_blk && a.T <= kRouteDecMaxT && a.E <= kRouteDecMaxE && a.dbg != 7 &&
            route_chain_smem(a.d, a.E) <= 220 * 1024 && route_small_smem(a.d, a.E) <= 220 * 1024;
