@@ -1429,7 +1429,42 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
                 // final epilogue of the unit: y = s2 * acc * 2^-24 + b2, gated (model.cpp:385-390)
                 const float* s2p = a.s2 + size_t(un.x) * Np2;
                 const float* b2p = a.b2 ? a.b2 + size_t(un.x) * Np2 : nullptr;
-                for (int idx = tid2; idx < un.z * d; idx += NT2) {
+                // four channels per thread and step (two 16-byte acc loads in flight): the unit's
+                // tail is a chain of L2 round trips under full HBM load, so fewer, wider steps
+                const int dq = d >> 2;
+                for (int idx = tid2; idx < ((d & 3) ? 0 : un.z * dq); idx += NT2) {
+                    const int r = idx / dq, ch = 4 * (idx - r * dq);
+                    longlong2* ap = reinterpret_cast<longlong2*>(acc + size_t(r) * Np2 + ch);
+                    const longlong2 v0 = __ldcg(ap), v1 = __ldcg(ap + 1);
+                    ap[0] = make_longlong2(0, 0);  // self-cleaning for the next forward
+                    ap[1] = make_longlong2(0, 0);
+                    const float4 sc = *reinterpret_cast<const float4*>(s2p + ch);
+                    float y[4] = {float(v0.x) * (1.0f / kFix) * sc.x, float(v0.y) * (1.0f / kFix) * sc.y,
+                                  float(v1.x) * (1.0f / kFix) * sc.z, float(v1.y) * (1.0f / kFix) * sc.w};
+                    if (b2p) {
+                        const float4 bb = *reinterpret_cast<const float4*>(b2p + ch);
+                        y[0] = y[0] + bb.x;
+                        y[1] = y[1] + bb.y;
+                        y[2] = y[2] + bb.z;
+                        y[3] = y[3] + bb.w;
+                    }
+                    const int row = un.y + r;
+                    const float gt = perm_gate[row];
+                    const float4 g4 = make_float4(gt * y[0], gt * y[1], gt * y[2], gt * y[3]);
+                    if (a.topk == 1) {
+                        const size_t o = size_t(perm_token[row]) * d + ch;
+                        if (a.out_f16) {
+                            __half2* op = reinterpret_cast<__half2*>(static_cast<__half*>(a.out) + o);
+                            op[0] = __floats2half2_rn(g4.x, g4.y);
+                            op[1] = __floats2half2_rn(g4.z, g4.w);
+                        } else {
+                            *reinterpret_cast<float4*>(static_cast<float*>(a.out) + o) = g4;
+                        }
+                    } else {
+                        *reinterpret_cast<float4*>(a.ybuf + size_t(row) * d + ch) = g4;
+                    }
+                }
+                for (int idx = tid2; idx < ((d & 3) ? un.z * d : 0); idx += NT2) {  // d_model % 4 != 0
                     const int r = idx / d, ch = idx - r * d;
                     long long* ap = acc + size_t(r) * Np2 + ch;
                     const long long vv = __ldcg(ap);

@@ -140,8 +140,14 @@ def test_bank_from_float_and_host_api(gpu, orc):
     out = gpu.moe_ffn_forward(_t(L["h"]), bank)  # bank's router
     assert allclose_report(out.cpu().numpy(), want, ATOL, RTOL)[0] == 0
     h_host = torch.from_numpy(L["h"]).pin_memory()
-    out_h = gpu.moe_ffn_forward_host(h_host, bank)
+    out_h = gpu.moe_ffn_forward_host(h_host, bank)  # page-locked output: the kernel stores into it
     assert torch.equal(out_h, out.cpu())
+    out_p = torch.full((L["h"].shape[0], 128), float("nan"))  # pageable output: the D2H copy path
+    gpu.moe_ffn_forward_host(torch.from_numpy(L["h"]), bank, out=out_p)
+    assert torch.equal(out_p, out.cpu())
+    out_16 = torch.empty((L["h"].shape[0], 128), dtype=torch.float16).pin_memory()
+    gpu.moe_ffn_forward_host(h_host.half(), bank, out=out_16)
+    assert torch.equal(out_16, gpu.moe_ffn_forward(_t(L["h"]).half(), bank, out_dtype=torch.float16).cpu())
 
 
 def test_zero_input_gives_gated_bias(gpu):
