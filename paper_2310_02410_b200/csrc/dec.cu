@@ -1490,7 +1490,26 @@ __global__ void __launch_bounds__(kDecFfnWarps * 32, 1) k_dec(const DecArgs a) {
                         if (old == 1) a.tok_cnt[tok] = 0;
                     }
                     named_bar_sync(2, NT2);
-                    for (int idx = tid2; idx < un.z * d; idx += NT2) {
+                    // four channels per step (16-byte ybuf loads), as the unit epilogue above
+                    const int dq = d >> 2;
+                    for (int idx = tid2; idx < ((d & 3) ? 0 : un.z * dq); idx += NT2) {
+                        const int r = idx / dq, ch = 4 * (idx - r * dq);
+                        const int tok = comb[r];
+                        if (tok < 0) continue;
+                        // o = g0*y0; o = o + g1*y1 (slot order, like the oracle's combine)
+                        const float4 y0 = __ldcg(reinterpret_cast<const float4*>(a.ybuf + size_t(row_of[2 * tok]) * d + ch));
+                        const float4 y1 = __ldcg(reinterpret_cast<const float4*>(a.ybuf + size_t(row_of[2 * tok + 1]) * d + ch));
+                        const float4 o = make_float4(y0.x + y1.x, y0.y + y1.y, y0.z + y1.z, y0.w + y1.w);
+                        const size_t oi = size_t(tok) * d + ch;
+                        if (a.out_f16) {
+                            __half2* op = reinterpret_cast<__half2*>(static_cast<__half*>(a.out) + oi);
+                            op[0] = __floats2half2_rn(o.x, o.y);
+                            op[1] = __floats2half2_rn(o.z, o.w);
+                        } else {
+                            *reinterpret_cast<float4*>(static_cast<float*>(a.out) + oi) = o;
+                        }
+                    }
+                    for (int idx = tid2; idx < ((d & 3) ? un.z * d : 0); idx += NT2) {  // d_model % 4 != 0
                         const int r = idx / d, ch = idx - r * d;
                         const int tok = comb[r];
                         if (tok < 0) continue;
