@@ -76,3 +76,22 @@ print("sync only               %.1f us" % bench(lambda i: s.synchronize()))
 ok = torch.equal(outs[0], od[0].cpu()) if False else None
 fwd_dev_out(0, od[0].data_ptr()); fwd_dev_out(0, outs[0].data_ptr()); s.synchronize()
 print("pinned-out result identical:", torch.equal(outs[0], od[0].cpu()))
+
+# the same call replayed from a CUDA graph (H2D copy node + forward kernel, output stored into the
+# pinned host buffer by the kernel): what a per-signature graph cache in the C-ABI would buy
+graphs = []
+gs = torch.cuda.Stream()
+for i in range(8):
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(gs):
+        fwd_dev_out(i, outs[i].data_ptr())  # warm (workspace, lazy init) outside capture
+        gs.synchronize()
+        with torch.cuda.graph(gr, stream=gs):
+            hd[i].copy_(hs[i], non_blocking=True)
+            r = lib.moqe_gpu_moe_forward(banks[i]._h, C.c_void_p(hd[i].data_ptr()), _lib.F16, T, None, 1,
+                                         C.c_void_p(outs[i].data_ptr()), _lib.F32, None, None, 0,
+                                         C.c_void_p(gs.cuda_stream))
+            assert r == 0
+    graphs.append(gr)
+torch.cuda.synchronize()
+print("graph(H2D + fwd->pinned) + sync %.1f us" % bench(lambda i: (graphs[i].replay(), torch.cuda.current_stream().synchronize(), gs.synchronize())))
