@@ -779,7 +779,8 @@ __device__ __forceinline__ void dec_fused_route(const DecArgs& a, unsigned char*
 // the lanes holding the max) give the reference's argmax semantics (model.cpp:339-341: ties -> lowest index, NaN skipped unless it sits at the
 // scan's first index). Gates in fp32 (expf is within 2 ulp; the logits already differ from the
 // reference's in the last bits).
-// Plan (warp 0, while the other warps scale the rows): lane l owns rows l and l + 32 (row =
+// Plan (the producer warp, while the other warps scale the rows; it then streams its first
+// slices without waiting for the rows): lane l owns rows l and l + 32 (row =
 // token * k + slot). Equal-expert masks come from ten ballots per half (expert bits + a unique
 // tag for empty rows), giving each row's stable rank and its expert's count; experts are
 // ordered by their first row, and one shuffle scan over those first rows yields row offsets and
@@ -866,7 +867,7 @@ __device__ __forceinline__ void dec_fused_decide(const DecArgs& a, DecPlanSmem& 
 #ifdef DEC_PLAN_TRACE
     if (blockIdx.x < 8) route_trace(a, rk, rtr, 47);
 #endif
-    if (warp == 0) {
+    if (warp == kF1Warps + kF2Warps) {  // the producer warp: it needs the plan first
         int ee[2];
         float gg[2];
 #pragma unroll
@@ -939,7 +940,7 @@ __device__ __forceinline__ void dec_fused_decide(const DecArgs& a, DecPlanSmem& 
         // each row (outside this CTA's routing K range) has landed
         if (a.h_f16 && (a.d % 8 == 0) && ((reinterpret_cast<uintptr_t>(a.h) & 15) == 0)) mbar_wait(rbar6, 0);
         constexpr int bias = 1 << (BITS - 1);
-        for (int tk = warp - 1; tk < T; tk += kDecFfnWarps - 1) {
+        for (int tk = warp; tk < T; tk += kDecFfnWarps - 1) {  // warps 0-15 (and 17-19)
             unsigned char* row = hs + size_t(tk) * hpitch;
             float zf = 0.f;
             for (int k0 = lane * 8; k0 < Kp1; k0 += 256) {
@@ -962,7 +963,14 @@ __device__ __forceinline__ void dec_fused_decide(const DecArgs& a, DecPlanSmem& 
             if (lane == 0) P.z[tk] = float(z);
         }
     }
-    __syncthreads();
+    // the plan (producer warp) and the scaled rows (the others) meet at barrier 7; the producer
+    // only arrives, so it starts streaming its first slices while the rows are still scaled
+    if (warp == kF1Warps + kF2Warps) {
+        __syncwarp();
+        asm volatile("bar.arrive 7, %0;" ::"r"(kDecFfnWarps * 32) : "memory");
+    } else {
+        named_bar_sync(7, kDecFfnWarps * 32);
+    }
     if (blockIdx.x < 8) route_trace(a, rk, rtr, 35);
 }
 
