@@ -210,6 +210,23 @@ moqe_status moqe_gpu_add_layer_norm(float* x, const float* delta, int64_t rows, 
                                     const float* gain, const float* bias, void* out,
                                     moqe_dtype out_dtype, void* stream);
 
+/* Expert-parallel dispatch / combine (BASELINE config 4). The reference is
+ * single-process; these are the sharded form of its gather (model.cpp:360-364)
+ * and scatter (model.cpp:387-390), replacing the sort / bincount / index_select / index_add_
+ * of an eager exchange. Rank g owns experts [g*E/G, (g+1)*E/G).
+ * ep_dispatch: h [t][d] f16 (d even), expert/gate [t][top_k] (global ids, f32 gates) ->
+ *   records [t*top_k][d+4] f16 = [row | owner-local expert id (i32) | gate (f32)] ordered by
+ *   owner rank, stable in flat order t*top_k+s; pos [t*top_k] = record row of each assignment;
+ *   send_counts [world] i64; *err (device i32) = 1 if an id is out of range (not packed).
+ * ep_combine: out [t][d] f32 = 0 + back[pos[t*k]] (+ back[pos[t*k+1]]) (f16 or f32 rows in
+ *   record order, i.e. as returned by the all_to_all). Stream-ordered, no host sync. */
+moqe_status moqe_gpu_ep_dispatch(const void* h, int64_t t, int64_t d, const int32_t* expert,
+                                 const float* gate, int top_k, int n_experts, int world,
+                                 void* records, int32_t* pos, int64_t* send_counts,
+                                 int32_t* err, void* stream);
+moqe_status moqe_gpu_ep_combine(const void* back, moqe_dtype back_dtype, const int32_t* pos, int64_t t,
+                                int top_k, int64_t d, float* out, void* stream);
+
 /* In-kernel launch spans of the decode path (measurement support, off by default):
  * with span(bank, 1) each decode forward's router and expert-FFN kernels record,
  * on the device, the time from the first CTA's start (after the programmatic-

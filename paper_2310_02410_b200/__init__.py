@@ -5,14 +5,15 @@ Drop-in for the reference's quantize-experts -> moe_ffn_forward path
 """
 from ._lib import (CheckpointError, CudaError, InvalidArgument, MoqeError, NotSupported, OutOfRange,
                    RangeError, load as load_library)
-from .api import (EXPERT_FFN, PER_CHANNEL, PER_TENSOR, ExpertBank, Mqe1, QuantizedTensor, expert_ffn,
+from .api import (EXPERT_FFN, PER_CHANNEL, PER_TENSOR, ExpertBank, Mqe1, QuantizedTensor, ep_combine, ep_dispatch,
+                  expert_ffn,
                   linear_scales, moe_ffn_forward, moe_ffn_forward_host, pack, packed_size,
                   quantize_linear, quantize_model, quantize_pack, route, top1_route, unpack,
                   valid_bits)
 
 __all__ = [
     "CheckpointError", "Mqe1", "CudaError", "InvalidArgument", "MoqeError", "NotSupported", "OutOfRange", "RangeError",
-    "load_library", "expert_ffn", "EXPERT_FFN", "PER_CHANNEL", "PER_TENSOR", "ExpertBank", "QuantizedTensor",
+    "load_library", "ep_combine", "ep_dispatch", "expert_ffn", "EXPERT_FFN", "PER_CHANNEL", "PER_TENSOR", "ExpertBank", "QuantizedTensor",
     "linear_scales", "moe_ffn_forward", "moe_ffn_forward_host", "pack", "packed_size",
     "quantize_linear", "quantize_model", "quantize_pack", "route", "top1_route", "unpack",
     "valid_bits",

@@ -58,6 +58,8 @@ SIGNATURES = {
     "moqe_gpu_bank_trace": (_i32, [_vp, _i32]),
     "moqe_gpu_bank_trace_read": (_i64, [_vp, _vp, _i64]),
     "moqe_gpu_moe_forward_host": (_i32, [_vp, _vp, _i32, _i64, _i32, _vp, _i32, _vp]),
+    "moqe_gpu_ep_dispatch": (_i32, [_vp, _i64, _i64, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
+    "moqe_gpu_ep_combine": (_i32, [_vp, _i32, _vp, _i64, _i32, _i64, _vp, _vp]),
 }
 
 

@@ -161,6 +161,38 @@ def route(h: torch.Tensor, gate_weights: torch.Tensor, top_k: int = 1):
     return ex[: T * top_k].reshape(shape), gt[: T * top_k].reshape(shape)
 
 
+def ep_dispatch(h: torch.Tensor, expert: torch.Tensor, gate: torch.Tensor, n_experts: int, world: int):
+    """Expert-parallel dispatch on the device (moqe_gpu_ep_dispatch; the sharded gather of
+    model.cpp:360-364). Returns (records [T*k, d+4] f16, pos [T*k] i32, send_counts [world]
+    i64, err [1] i32): records ordered by owner rank (stable), pos = record row per
+    (token, slot). No host sync."""
+    T, d = h.shape
+    k = 1 if expert.dim() == 1 else expert.shape[1]
+    h = _dev(h, torch.float16, "ep_dispatch")
+    ex = _dev(expert.reshape(-1), torch.int32, "ep_dispatch")
+    gt = _dev(gate.reshape(-1), torch.float32, "ep_dispatch")
+    rec = torch.empty((T * k, d + 4), dtype=torch.float16, device=h.device)
+    pos = torch.empty((T * k,), dtype=torch.int32, device=h.device)
+    counts = torch.empty((world,), dtype=torch.int64, device=h.device)
+    err = torch.empty((1,), dtype=torch.int32, device=h.device)
+    check(_lib.load().moqe_gpu_ep_dispatch(_ptr(h), T, d, _ptr(ex), _ptr(gt), k, n_experts, world,
+                                           _ptr(rec), _ptr(pos), _ptr(counts), _ptr(err), _stream()))
+    return rec, pos, counts, err
+
+
+def ep_combine(back: torch.Tensor, pos: torch.Tensor, T: int, top_k: int) -> torch.Tensor:
+    """out[t] = 0 + back[pos[t,0]] (+ back[pos[t,1]]) in fp32 (moqe_gpu_ep_combine; the
+    scatter of model.cpp:387-390 over the returned rows)."""
+    if back.dtype not in (torch.float16, torch.float32):
+        raise _lib.InvalidArgument("ep_combine: rows must be f16 or f32")
+    back = _dev(back, back.dtype, "ep_combine")
+    d = back.shape[1]
+    out = torch.empty((T, d), dtype=torch.float32, device=back.device)
+    check(_lib.load().moqe_gpu_ep_combine(_ptr(back), _lib.F16 if back.dtype == torch.float16 else _lib.F32,
+                                          _ptr(pos), T, top_k, d, _ptr(out), _stream()))
+    return out
+
+
 def top1_route(h: torch.Tensor, gate_weights: torch.Tensor):
     """moqe::top1_route (model.hpp:65)."""
     return route(h, gate_weights, 1)

@@ -9,7 +9,8 @@ weights are replicated.
 
 One forward:
   1. route local tokens (exact fp32 router kernel; global expert ids + gates)
-  2. group (token, slot) rows by owner rank, ascending token order (stable)
+  2. group (token, slot) rows by owner rank, ascending token order (stable); on the GPU
+     one kernel pair does it (k_ep_plan + k_ep_pack, csrc/ep.cu: moqe_gpu_ep_dispatch)
   3. exchange per-rank counts (one small all_to_all + one read of G counts), then ONE
      all_to_all of packed records: the fp16 row with the owner-local expert id and the
      gate bit-cast into 4 trailing fp16 slots (NCCL over NVLink on GPU, gloo on CPU)
@@ -18,7 +19,9 @@ One forward:
   5. all_to_all the gate-weighted rows back, fp16 by default (half the return bytes;
      return_dtype=torch.float32 keeps the bit-exact fp32 return)
   6. combine: out[t] = sum over t's slots, added onto zero (two addends,
-     commutative -> deterministic).
+     commutative -> deterministic); on the GPU k_ep_combine (moqe_gpu_ep_combine).
+The CPU form of steps 2 and 6 (torch.sort / bincount / index_add_) only serves the gloo
+tests of the exchange logic; CUDA tensors always take the kernels.
 With an fp32 return the output equals the single-GPU moe_forward of the whole layer bit for
 bit (combine order identical for top-1/top-2); the fp16 return rounds each gated row once.
 """
@@ -83,6 +86,30 @@ class ExpertParallelMoE:
                                                                          out_dtype=self.return_dtype,
                                                                          validate=False))
 
+    def _forward_device(self, h: torch.Tensor, ex: torch.Tensor, gate: torch.Tensor) -> torch.Tensor:
+        """The GPU step: dispatch and combine in this package's kernels (ep.cu), one host
+        read (the G send / receive counts + the id-range flag, one copy)."""
+        from . import api
+        T, d = h.shape
+        k = ex.shape[1]
+        rec, pos, send_counts, err = api.ep_dispatch(h, ex, gate, self.E, self.world)
+        recv_counts = torch.empty_like(send_counts)
+        self._a2a(recv_counts, send_counts, None, None)
+        host = torch.cat([send_counts, recv_counts, err.to(torch.int64)]).tolist()
+        G = self.world
+        s_split, r_split = host[:G], host[G:2 * G]
+        if host[2 * G]:
+            raise IndexError("ep: expert id out of range")
+        R = int(sum(r_split))
+        recv = torch.empty((R, d + 4), dtype=torch.float16, device=h.device)
+        self._a2a(recv, rec, r_split, s_split)
+        rmeta = recv[:, d:].view(torch.int32)
+        y = self.expert_fn(recv[:, :d], rmeta[:, 0].contiguous(),
+                           rmeta[:, 1].contiguous().view(torch.float32)).to(self.return_dtype).contiguous()
+        back = torch.empty((T * k, d), dtype=self.return_dtype, device=h.device)
+        self._a2a(back, y, s_split, r_split)
+        return api.ep_combine(back, pos, T, k)
+
     def _a2a(self, out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits) -> None:
         dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
 
@@ -91,6 +118,8 @@ class ExpertParallelMoE:
         ex, gate = self.route_fn(h)
         ex = ex.reshape(T, -1)
         gate = gate.reshape(T, -1)
+        if h.is_cuda:
+            return self._forward_device(h, ex, gate)
         order, tok, dest_sorted, send_counts = dispatch_plan(ex, self.E, self.world)
         src_tok = tok[order]
         R_send = src_tok.shape[0]

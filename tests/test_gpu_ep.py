@@ -57,3 +57,47 @@ def test_ep_world1_nccl(gpu, orc):
                 assert torch.allclose(out, ref, rtol=0, atol=1e-6)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("T,k,E,G,d", [(0, 2, 8, 2, 64), (1, 1, 8, 4, 64), (24, 1, 32, 8, 1024), (1000, 2, 128, 8, 2048),
+                                       (3000, 2, 64, 4, 256), (2500, 1, 96, 3, 100)])
+def test_ep_dispatch_combine_kernels(gpu, T, k, E, G, d):
+    """moqe_gpu_ep_dispatch / ep_combine (csrc/ep.cu) against the torch form of the same
+    plan (ep.dispatch_plan: stable sort by owner rank) — bit-exact records, counts, combine;
+    includes empty input, a >1024-assignment (multi-chunk) plan and a d % 4 != 0 row."""
+    import torch
+    from paper_2310_02410_b200.ep import dispatch_plan
+    g = torch.Generator().manual_seed(T * 7 + G)
+    h = torch.randn((T, d), generator=g).half().cuda()
+    ex = torch.randint(0, E, (T, k), generator=g, dtype=torch.int32).cuda()
+    gt = torch.rand((T, k), generator=g).cuda()
+    rec, pos, counts, err = gpu.ep_dispatch(h, ex, gt, E, G)
+    order, tok, dest_sorted, want_counts = dispatch_plan(ex, E, G)
+    assert int(err.item()) == 0
+    assert torch.equal(counts.cpu(), want_counts.cpu())
+    src = tok[order]
+    assert torch.equal(rec[:, :d], h.index_select(0, src))
+    meta = rec[:, d:].view(torch.int32)
+    assert torch.equal(meta[:, 0], (ex.reshape(-1)[order] - dest_sorted * (E // G)).int())
+    assert torch.equal(meta[:, 1].view(torch.float32), gt.reshape(-1)[order])
+    want_pos = torch.empty_like(order)
+    want_pos[order] = torch.arange(order.numel(), device=order.device)
+    assert torch.equal(pos.long(), want_pos)
+    for dt in (torch.float16, torch.float32):
+        back = torch.randn((T * k, d), generator=g).to(dt).cuda()
+        out = gpu.ep_combine(back, pos, T, k)
+        exp = back.float().index_select(0, pos.long()).reshape(T, k, d)
+        ref = torch.zeros((T, d), dtype=torch.float32, device="cuda")
+        for s in range(k):
+            ref = ref + exp[:, s]
+        assert torch.equal(out, ref)
+
+
+def test_ep_dispatch_rejects_bad_ids(gpu):
+    import torch
+    h = torch.zeros((4, 64), dtype=torch.float16, device="cuda")
+    ex = torch.tensor([[0], [9], [3], [-1]], dtype=torch.int32, device="cuda")
+    _, _, _, err = gpu.ep_dispatch(h, ex, torch.ones((4, 1), device="cuda"), 8, 2)
+    assert int(err.item()) == 1
+    with pytest.raises(ValueError):
+        gpu.ep_dispatch(h, ex, torch.ones((4, 1), device="cuda"), 9, 2)
