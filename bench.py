@@ -452,7 +452,18 @@ def run_point_ep(m, torch, dist, E, d, f, bits, T, top_k, steps, warmup, dev, ra
     torch.cuda.synchronize()
     fwd = lambda L: L[0].forward(L[1])
     ms = time_steps(torch, fwd, layers, steps, warmup, dist, graphs=False)
-    return {"ms_per_step": ms, "tokens_per_s_per_rank": T / (ms * 1e-3), "experts_per_rank": hi - lo}
+    # e2e: the same step from pinned HOST token rows to a pinned HOST output (H2D + D2H timed)
+    hosts = {id(L): (L[1].cpu().pin_memory(), torch.empty((T, d), dtype=torch.float32).pin_memory())
+             for L in layers}
+
+    def fwd_host(L):
+        hh, oh = hosts[id(L)]
+        oh.copy_(L[0].forward(hh.to(dev, non_blocking=True)), non_blocking=True)
+
+    ms_e2e = time_steps(torch, fwd_host, layers, max(steps // 2, 5), warmup, dist, graphs=False)
+    e2e = {"value": round(T * world / (ms_e2e * 1e-3), 1), "unit": "tokens/s", "h2d_bytes_per_step": int(T * d * 2),
+           "d2h_bytes_per_step": int(T * d * 4), "ms_per_step": round(ms_e2e, 5)}
+    return {"ms_per_step": ms, "tokens_per_s_per_rank": T / (ms * 1e-3), "experts_per_rank": hi - lo, "e2e": e2e}
 
 
 def ep_cpu_baseline(E, d, f, bits, top_k, sample_tokens=16, threads=None):
@@ -632,10 +643,10 @@ def main():
                     "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                     "ms_per_step": round(ep["ms_per_step"], 5), "higher_is_better": True, "scaling": "weak",
                     "vs_baseline": None, "dtype": "f16", "data": "synthetic", "config": config,
-                    "roofline": roof, "cpu_baseline": cpu, "e2e": None, "gpu_launches": None, "clocks": clocks,
-                    "detail": {"note": "eager EP steps: router kernel, packed fp16 dispatch records (one NCCL "
-                                       "all_to_all + a G-int count exchange), owner expert FFN kernels, fp16 "
-                                       "return all_to_all, combine; max over ranks"}}
+                    "roofline": roof, "cpu_baseline": cpu, "e2e": ep["e2e"], "gpu_launches": None, "clocks": clocks,
+                    "detail": {"note": "eager EP steps: router kernel, device dispatch (k_ep_plan + k_ep_pack: "
+                                       "packed fp16 records, one NCCL all_to_all + a G-int count exchange), owner "
+                                       "expert FFN kernels, fp16 return all_to_all, k_ep_combine; max over ranks"}}
             print(json.dumps(line), flush=True)
         dist.barrier()
         dist.destroy_process_group()

@@ -171,3 +171,32 @@ def test_multi_tile_full_oracle(gpu, orc, E, d, f, bits, T, topk):
     """Small layers with > 256 rows per expert, checked on EVERY token."""
     L = GpuLayer(gpu, orc, E * 7 + T, E, d, f, bits, T)
     check_layer(gpu, L, topk, T, ["auto", "gemm"], 9, min_rows=512)
+
+
+def test_config4_ep_world1(gpu, orc):
+    """BASELINE config 4 through the expert-parallel layer (ep.ExpertParallelMoE: device
+    dispatch / combine kernels + NCCL all_to_all at world size 1, fp16 and fp32 returns) at
+    its full shape (E=128, d=2048, f=8192, top-2, int2), T=4096: equal to the 1-GPU
+    moe_ffn_forward within the north_star tolerance (fp32 return: 1e-6 + 1e-5 rel)."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+    from paper_2310_02410_b200.ep import ExpertParallelMoE
+    L = GpuLayer(gpu, orc, 401, 128, 2048, 8192, 2, 4096)
+    h = torch.from_numpy(L.h).cuda().half()
+    wg = torch.from_numpy(L.wg).cuda()
+    ref = gpu.moe_ffn_forward(h, L.bank, wg, top_k=2)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", world_size=1, rank=0)
+    try:
+        for rdt in (torch.float16, torch.float32):
+            out = ExpertParallelMoE(L.bank, wg, 128, top_k=2, return_dtype=rdt).forward(h)
+            err = (out - ref).abs()
+            lim = (ATOL + RTOL * ref.abs()) if rdt == torch.float16 else 1e-6 + 1e-5 * ref.abs()
+            assert bool((err <= lim).all()), (rdt, float(err.max()))
+    finally:
+        dist.destroy_process_group()
