@@ -68,9 +68,9 @@ cudaError_t route_block_wg(const float* wg, int d, int E, float* out, int* d_fla
 cudaError_t launch_route(const RouteArgs& a, const Plan& P, cudaStream_t st);
 bool route_chain_one_chunk(int d, int E);  // the decode chain router holds all of Wg in one chunk
 int route_tokens_per_cta(int64_t T);
-// rows already routed: plan with kRouteSelWarps rows per CTA (scatter must use that tile)
+// rows already routed (top-1): plan with kPlanIdsTile rows per CTA (scatter must use that tile)
 cudaError_t launch_plan_from_ids(const RouteArgs& a, const Plan& P, cudaStream_t st);
-constexpr int kPlanIdsTile = 32;
+constexpr int kPlanIdsTile = 256;
 cudaError_t launch_scatter(const void* h, int h_f16, int64_t T, int d, int topk, int E, int path, int gemv_max, int tt,
                            const Plan& P, __half* x_perm, int ldx, float* zero_out, cudaStream_t st);
 

@@ -1739,14 +1739,16 @@ __global__ void __launch_bounds__(kRouteSelWarps * 32) k_route_select(RouteArgs 
     ranks_hist_plan(a, P, s_exp, s_hist, kRouteSelWarps);
 }
 
-// Pre-routed rows (expert-parallel owner side): expert ids / gates are inputs;
-// build stable ranks, per-CTA histograms and the plan exactly as routing does.
-__global__ void __launch_bounds__(kRouteSelWarps * 32) k_plan_from_ids(RouteArgs a, Plan P) {
-    __shared__ int s_exp[kRouteSelWarps * 2];
+// Pre-routed rows (expert-parallel owner side): expert ids / gates are inputs (one expert per
+// row); build stable ranks, per-CTA histograms and the plan exactly as routing does. Tiles of
+// kPlanIdsTile rows keep the last CTA's plan scan short (config 4 owner: 32 K rows -> 128
+// tiles x E counts instead of 1024).
+__global__ void __launch_bounds__(kPlanIdsTile) k_plan_from_ids(RouteArgs a, Plan P) {
+    __shared__ int s_exp[kPlanIdsTile];
     __shared__ int s_hist[256];
     for (int e = threadIdx.x; e < a.E; e += blockDim.x) s_hist[e] = 0;
-    if (threadIdx.x < kRouteSelWarps) {
-        const int64_t t = int64_t(blockIdx.x) * kRouteSelWarps + threadIdx.x;
+    {
+        const int64_t t = int64_t(blockIdx.x) * kPlanIdsTile + threadIdx.x;
         int e = -1;
         if (t < a.T) {
             e = P.expert[t];
@@ -1754,12 +1756,13 @@ __global__ void __launch_bounds__(kRouteSelWarps * 32) k_plan_from_ids(RouteArgs
         }
         s_exp[threadIdx.x] = e;
     }
-    ranks_hist_plan(a, P, s_exp, s_hist, kRouteSelWarps);
+    ranks_hist_plan(a, P, s_exp, s_hist, kPlanIdsTile);
 }
 
 cudaError_t launch_plan_from_ids(const RouteArgs& a, const Plan& P, cudaStream_t st) {
-    const unsigned grid = unsigned((a.T + kRouteSelWarps - 1) / kRouteSelWarps);
-    k_plan_from_ids<<<grid, kRouteSelWarps * 32, 0, st>>>(a, P);
+    if (a.topk != 1) return cudaErrorInvalidValue;
+    const unsigned grid = unsigned((a.T + kPlanIdsTile - 1) / kPlanIdsTile);
+    k_plan_from_ids<<<grid, kPlanIdsTile, 0, st>>>(a, P);
     return cudaGetLastError();
 }
 

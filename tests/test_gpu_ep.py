@@ -60,11 +60,11 @@ def test_ep_world1_nccl(gpu, orc):
 
 
 @pytest.mark.parametrize("T,k,E,G,d", [(0, 2, 8, 2, 64), (1, 1, 8, 4, 64), (24, 1, 32, 8, 1024), (1000, 2, 128, 8, 2048),
-                                       (3000, 2, 64, 4, 256), (2500, 1, 96, 3, 100)])
+                                       (3000, 2, 64, 4, 256), (2500, 1, 96, 3, 100), (50, 2, 8, 2, 98)])
 def test_ep_dispatch_combine_kernels(gpu, T, k, E, G, d):
     """moqe_gpu_ep_dispatch / ep_combine (csrc/ep.cu) against the torch form of the same
     plan (ep.dispatch_plan: stable sort by owner rank) — bit-exact records, counts, combine;
-    includes empty input, a >1024-assignment (multi-chunk) plan and a d % 4 != 0 row."""
+    includes empty input, a >1024-assignment (multi-chunk) plan and d % 4 != 0 rows (scalar paths)."""
     import torch
     from paper_2310_02410_b200.ep import dispatch_plan
     g = torch.Generator().manual_seed(T * 7 + G)
