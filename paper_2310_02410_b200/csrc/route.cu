@@ -1713,6 +1713,99 @@ __global__ void __launch_bounds__(128) k_route_logits(RouteArgs a, float* __rest
     }
 }
 
+// k_route_logits2t: the VEC case with two tokens per lane (lane, lane + 32): a CTA = 64 tokens x
+// 32 experts, so each Wg smem broadcast feeds 16 products instead of 8. Same exact chain per
+// (token, expert) as k_route_logits (FMUL then FADD in ascending k, zero activations skipped).
+constexpr int kRL2Tok = 64;
+__global__ void __launch_bounds__(128) k_route_logits2t(RouteArgs a, float* __restrict__ logits) {
+    __shared__ __align__(16) float s_h[2][kRLRows][kRL2Tok + 1];
+    __shared__ __align__(16) float s_w[2][kRLRows][kRLExp];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int E = a.E, d = a.d;
+    const int64_t t0 = int64_t(blockIdx.x) * kRL2Tok;
+    const int e0 = blockIdx.y * kRLExp;
+    const int nchunks = (d + kRLRows - 1) / kRLRows;
+    float ph[16], pw[8];
+    auto load = [&](int c) {
+        const int p0 = c * kRLRows;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int r = (tid >> 2) + 32 * u, c8 = tid & 3;  // token row, 8-wide p segment
+            const int64_t t = t0 + r;
+            uint4 hv = make_uint4(0, 0, 0, 0);
+            if (t < a.T && p0 + 8 * c8 < d)
+                hv = __ldg(reinterpret_cast<const uint4*>(static_cast<const __half*>(a.h) + t * d + p0 + 8 * c8));
+            const __half2* h2 = reinterpret_cast<const __half2*>(&hv);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float2 f = __half22float2(h2[i]);
+                ph[8 * u + 2 * i] = f.x;
+                ph[8 * u + 2 * i + 1] = f.y;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int idx = i * 128 + tid, q = idx >> 3, c4 = idx & 7;
+            float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (p0 + q < d) w = __ldg(reinterpret_cast<const float4*>(a.wg + int64_t(p0 + q) * E + e0 + 4 * c4));
+            pw[4 * i] = w.x; pw[4 * i + 1] = w.y; pw[4 * i + 2] = w.z; pw[4 * i + 3] = w.w;
+        }
+    };
+    auto store = [&](int b) {
+        const int c8 = tid & 3;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int r = (tid >> 2) + 32 * u;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) s_h[b][8 * c8 + i][r] = ph[8 * u + i];
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int idx = i * 128 + tid, q = idx >> 3, c4 = idx & 7;
+            *reinterpret_cast<float4*>(&s_w[b][q][4 * c4]) = make_float4(pw[4 * i], pw[4 * i + 1], pw[4 * i + 2], pw[4 * i + 3]);
+        }
+    };
+    float acc0[8], acc1[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc0[e] = acc1[e] = 0.0f;
+    load(0);
+    for (int c = 0; c < nchunks; ++c) {
+        const int b = c & 1;
+        store(b);
+        __syncthreads();
+        if (c + 1 < nchunks) load(c + 1);
+        const int pn = min(kRLRows, d - c * kRLRows);
+#pragma unroll 8
+        for (int q = 0; q < kRLRows; ++q) {
+            if (q >= pn) break;
+            const float av0 = s_h[b][q][lane], av1 = s_h[b][q][lane + 32];
+            const float4 w0 = *reinterpret_cast<const float4*>(&s_w[b][q][8 * warp]);
+            const float4 w1 = *reinterpret_cast<const float4*>(&s_w[b][q][8 * warp + 4]);
+            const float w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+            // reference: `if (av == 0.0f) continue; orow[j] += av * brow[j];`
+            if (av0 != 0.0f) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc0[e] = __fadd_rn(acc0[e], __fmul_rn(av0, w[e]));
+            }
+            if (av1 != 0.0f) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc1[e] = __fadd_rn(acc1[e], __fmul_rn(av1, w[e]));
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const int64_t t = t0 + lane + 32 * u;
+        if (t < a.T) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int j = e0 + 8 * warp + e;
+                if (j < E) logits[t * E + j] = u ? acc1[e] : acc0[e];
+            }
+        }
+    }
+}
+
 constexpr int kRouteSelWarps = 32;  // tokens per selection CTA
 // k_route_select: one warp per token reads its E logits, applies the
 // reference argmax / softmax gate (or top-2), then stable ranks, CTA
@@ -1897,6 +1990,14 @@ int64_t route_big_threshold() {
 }
 int route_tokens_per_cta(int64_t T) { return T <= route_big_threshold() ? kRouteSmallWarps : kRouteSelWarps; }
 
+static bool route_logits2t_enabled() {  // MOQE_ROUTE_LOGITS_2T=0: one token per lane (A/B)
+    static const bool v = [] {
+        const char* s = getenv("MOQE_ROUTE_LOGITS_2T");
+        return !(s && s[0] == '0');
+    }();
+    return v;
+}
+
 cudaError_t launch_route(const RouteArgs& a, const Plan& P, cudaStream_t st) {
     const int tt = route_tokens_per_cta(a.T);
     const unsigned grid = unsigned((a.T + tt - 1) / tt);
@@ -1948,6 +2049,9 @@ cudaError_t launch_route(const RouteArgs& a, const Plan& P, cudaStream_t st) {
                 k_route_logits2<8><<<g2, (kRL2Warps + 1) * 32, sm2, st>>>(a, P);
             }
             return cudaGetLastError();  // selection and plan are fused into the logits kernel
+        } else if (vec && route_logits2t_enabled()) {
+            dim3 lg2(unsigned((a.T + kRL2Tok - 1) / kRL2Tok), unsigned((a.E + kRLExp - 1) / kRLExp));
+            k_route_logits2t<<<lg2, 128, 0, st>>>(a, P.logits);
         } else if (vec) k_route_logits<true><<<lg, 128, 0, st>>>(a, P.logits);
         else k_route_logits<false><<<lg, 128, 0, st>>>(a, P.logits);
         k_route_select<<<grid, kRouteSelWarps * 32, 0, st>>>(a, P);
