@@ -461,9 +461,24 @@ def run_point_ep(m, torch, dist, E, d, f, bits, T, top_k, steps, warmup, dev, ra
         oh.copy_(L[0].forward(hh.to(dev, non_blocking=True)), non_blocking=True)
 
     ms_e2e = time_steps(torch, fwd_host, layers, max(steps // 2, 5), warmup, dist, graphs=False)
+    # this library's kernels per step (CUPTI kernel records of one step per layer; NCCL excluded)
+    launches = None
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            for L in layers:
+                fwd(L)
+            torch.cuda.synchronize()
+        names = [e.name for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+        ours = [n for n in names if "moqe_gpu::" in n or n.startswith("k_")]
+        launches = len(ours) // len(layers) * steps if ours else None
+    except Exception:  # profiler unavailable: no claim
+        launches = None
+
     e2e = {"value": round(T * world / (ms_e2e * 1e-3), 1), "unit": "tokens/s", "h2d_bytes_per_step": int(T * d * 2),
            "d2h_bytes_per_step": int(T * d * 4), "ms_per_step": round(ms_e2e, 5)}
-    return {"ms_per_step": ms, "tokens_per_s_per_rank": T / (ms * 1e-3), "experts_per_rank": hi - lo, "e2e": e2e}
+    return {"ms_per_step": ms, "tokens_per_s_per_rank": T / (ms * 1e-3), "experts_per_rank": hi - lo, "e2e": e2e,
+            "gpu_launches": launches}
 
 
 def ep_cpu_baseline(E, d, f, bits, top_k, sample_tokens=16, threads=None):
@@ -643,7 +658,7 @@ def main():
                     "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                     "ms_per_step": round(ep["ms_per_step"], 5), "higher_is_better": True, "scaling": "weak",
                     "vs_baseline": None, "dtype": "f16", "data": "synthetic", "config": config,
-                    "roofline": roof, "cpu_baseline": cpu, "e2e": ep["e2e"], "gpu_launches": None, "clocks": clocks,
+                    "roofline": roof, "cpu_baseline": cpu, "e2e": ep["e2e"], "gpu_launches": ep["gpu_launches"], "clocks": clocks,
                     "detail": {"note": "eager EP steps: router kernel, device dispatch (k_ep_plan + k_ep_pack: "
                                        "packed fp16 records, one NCCL all_to_all + a G-int count exchange), owner "
                                        "expert FFN kernels, fp16 return all_to_all, k_ep_combine; max over ranks"}}
